@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""Benchmark: explicit-Euler steps/s of the semi-explicit MQS scheme on B200.
+
+Workload (BASELINE.json configs[1]): 64^3 cells, Brauer iron block 24^3,
+annular coil J = 5e6 sin(2 pi 50 t), fp64, PCG (Jacobi, rel_tol 1e-8), CSPE
+start vectors (k = 5), output (recover_an) every step: 4 K_n solves per step.
+A "step" is one explicit-Euler step plus the recovery of a_n.  W warm-up
+steps (untimed; they also build the CSPE bases) precede K timed steps of the
+same trajectory.  L2 is flushed (256 MB write) before every timed step and
+the flush is outside the timed events.
+
+Outputs one JSON line (rank 0).  `value` is device-timed with the inputs
+resident in HBM; `e2e` is the same metric through the host-facing API
+(explicit_euler_step + recover_an with host arrays, copies inside the timed
+region); `roofline` is the fused PCG kernel measured inside the timed region
+(config 1) and `roofline_cfg2` the same kernel on the 128^3 grid of
+configs[2] (the north star's HBM target).  `cpu_baseline` times the CPU port
+of the reference (oracle/, numpy/scipy) on a bounded sample.
+
+--impl reference runs the CPU port of the reference on the same workload and
+prints the same metric.  With torchrun (N > 1) every rank runs an
+independent ensemble member (configs[3] factors): weak scaling, no
+collective on the data path; the timing is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "explicit-Euler steps/s (config 1: 64^3 Brauer, CSPE k=5, recover every step)"
+UNIT = "steps/s"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception as exc:  # noqa: BLE001
+            self.err = str(exc)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        if self._ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._ok:
+            self.t.join()
+
+    def summary(self):
+        if not self._ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": getattr(self, "err", "")}
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+def schedule(spec, n_steps):
+    dt = spec.dt
+    w = 2.0 * np.pi * spec.freq
+    tt = [0.0]
+    for _ in range(n_steps):
+        tt.append(tt[-1] + dt)
+    import math
+    wave = np.array([math.sin(w * t) for t in tt])
+    return np.full(n_steps, dt), wave, tt
+
+
+def pcg_launch_bytes(n_n, iters, modes=None):
+    """Algorithmic bytes of one fused-PCG launch with `iters` iterations.
+
+    9 vector streams per iteration (72 B/dof), the initial residual pass
+    (read b and x0 with the stencil, write r and x: 4 streams) and the final
+    x += alpha p (3 streams) when it iterated."""
+    iters = np.asarray(iters, dtype=np.float64)
+    return 8.0 * n_n * (9.0 * iters + 4.0 + 3.0 * (iters > 0))
+
+
+def member_problem(rank: int):
+    from paper_1611_06721_b200 import configs as C
+    if rank == 0:
+        return C.make_problem(1), (1.0, 1.0)
+    j, k = C.ensemble_factors(256, seed=0)
+    return C.make_problem(1, j_scale=float(j[rank]), kappa_scale=float(k[rank])), (float(j[rank]), float(k[rank]))
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return world, rank, local, dist
+    return 1, 0, 0, None
+
+
+def max_over_ranks(x: float, dist, local):
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# CPU port of the reference (oracle) on the same workload
+# ---------------------------------------------------------------------------
+def cpu_reference(spec, warmup, steps, *, budget_s=None):
+    from oracle import mq_oracle as O
+    from paper_1611_06721_b200 import configs as C
+    mat = C.material_map(spec)
+    loops = C.coil_loops(spec.N, spec.J)
+    m = O.assemble(mat, spec.h, O.Conductor(spec.kappa, *spec.brauer),
+                   [O.Loop(lp.i0, lp.i1, lp.j0, lp.j1, lp.k0, lp.amps) for lp in loops])
+    op = O.SchurOracle(m, O.sinusoid(spec.freq), "cspe", spec.rel_tol, spec.max_iter, spec.max_cols)
+    a = np.zeros(m.n_c)
+    t = 0.0
+    op.recover(a, t)
+    for s in range(warmup):
+        a, _ = op.euler(a, t, spec.dt, s + 1)
+        t += spec.dt
+        op.recover(a, t)
+    done, t0 = 0, time.perf_counter()
+    for s in range(steps):
+        a, _ = op.euler(a, t, spec.dt, warmup + s + 1)
+        t += spec.dt
+        op.recover(a, t)
+        done += 1
+        if budget_s is not None and time.perf_counter() - t0 > budget_s:
+            break
+    el = time.perf_counter() - t0
+    return done / el, done, el, m.n_n
+
+
+def run_reference_arm(args):
+    world, rank, local, dist = 1, int(os.environ.get("RANK", "0")), 0, None
+    if rank != 0:
+        return 0
+    from paper_1611_06721_b200 import configs as C
+    spec = C.config_spec(1)
+    v, done, el, n_n = cpu_reference(spec, args.warmup, args.steps)
+    cores = os.cpu_count()
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": done, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * el / max(done, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg1_64cube_brauer_cspe5", "grid": [64, 64, 64], "n_n": n_n,
+                   "strategy": "cspe", "max_cols": 5, "rel_tol": 1e-8, "dt": spec.dt},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"steps {args.warmup + 1}..{args.warmup + done} of config 1 "
+                                   "(oracle/mq_oracle.py: numpy/scipy port of mqsolve; scipy "
+                                   "csr_matvec single-threaded, OpenBLAS dots on all cores)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# device arm
+# ---------------------------------------------------------------------------
+def time_device_steps(op, spec, warmup, steps, flush=True):
+    """W warm-up steps then K timed steps (CUDA events per step on the
+    context stream, L2 flushed before each), PCG launches timed inside."""
+    import ctypes
+
+    from paper_1611_06721_b200 import _lib
+    from paper_1611_06721_b200._lib import check, dptr
+    lib, ctx = op.lib, op.grid.ctx
+    dts, wave, _ = schedule(spec, warmup + steps)
+    op._set_state(np.zeros(op.grid.n_c), 0.0)
+    # initial recovery at t = 0 as in the reference loop
+    from paper_1611_06721_b200.schur import recover_an
+    recover_an(op, np.zeros(op.grid.n_c), 0.0)
+    op._set_state(np.zeros(op.grid.n_c), 0.0)
+    check(lib.mq_run_prepare(ctx, warmup + steps, dptr(dts), dptr(wave), 1))
+    # PCG event records must exist when the step graph is captured (warm-up)
+    check(lib.mq_pcg_stats(ctx, None, None, None, 1))
+    check(lib.mq_run_steps(ctx, warmup, 1, None))
+    check(lib.mq_ctx_sync(ctx))
+    l0 = ctypes.c_int64()
+    check(lib.mq_kernel_launches(ctx, ctypes.byref(l0)))
+    step_ms, pcg_ms = [], []
+    ms = ctypes.c_double()
+    pm = ctypes.c_double()
+    ne = ctypes.c_int32()
+    for _ in range(steps):
+        if flush:
+            check(lib.mq_l2_flush(ctx))
+        check(lib.mq_timer_start(ctx))
+        check(lib.mq_run_steps(ctx, 1, 1, None))
+        check(lib.mq_timer_stop(ctx, ctypes.byref(ms)))
+        check(lib.mq_pcg_collect(ctx, ctypes.byref(pm), ctypes.byref(ne)))
+        step_ms.append(ms.value)
+        pcg_ms.append(pm.value)
+    l1 = ctypes.c_int64()
+    check(lib.mq_kernel_launches(ctx, ctypes.byref(l1)))
+    check(lib.mq_pcg_stats(ctx, None, None, None, 0))
+    iters = np.zeros((warmup + steps, 4), dtype=np.int32)
+    failed = ctypes.c_int64()
+    check(lib.mq_run_finish(ctx, _lib.i32ptr(iters), ctypes.byref(failed)))
+    return np.array(step_ms), np.array(pcg_ms), iters[warmup:], int(l1.value - l0.value)
+
+
+def time_e2e(problem, spec, warmup, steps):
+    """Same steps through the host-facing API (explicit_euler_step +
+    recover_an with host arrays; copies inside the timed region)."""
+    from paper_1611_06721_b200 import PcgConfig, SchurOperator, explicit_euler_step, recover_an
+    op = SchurOperator(problem, pcg=PcgConfig(rel_tol=spec.rel_tol, max_iter=spec.max_iter),
+                       strategy="cspe", max_cols=spec.max_cols)
+    a = np.zeros(op.grid.n_c)
+    t = 0.0
+    recover_an(op, a, t)
+    for s in range(warmup):
+        a, _ = explicit_euler_step((a, t), spec.dt, op, s + 1)
+        t += spec.dt
+        recover_an(op, a, t)
+    op.grid.sync()
+    t0 = time.perf_counter()
+    for s in range(steps):
+        a, _ = explicit_euler_step((a, t), spec.dt, op, warmup + s + 1)
+        t += spec.dt
+        a_n, _ = recover_an(op, a, t)
+    el = time.perf_counter() - t0
+    n_c, n_n = op.grid.n_c, op.grid.n_n
+    h2d = 2 * n_c * 8          # a_c uploaded by each of the two calls
+    d2h = n_c * 8 + n_n * 8    # a_c after the step, a_n after the recovery
+    op.grid.close()
+    return steps / el, el, h2d, d2h
+
+
+def cfg2_pcg_roofline(hbm_peak, reps=2):
+    """Fused PCG kernel on the 128^3 grid of configs[2]: cold source solve."""
+    import ctypes
+
+    from paper_1611_06721_b200 import _lib, configs as C
+    from paper_1611_06721_b200._lib import check
+    from paper_1611_06721_b200.device import DeviceGrid
+    prob = C.make_problem(2)
+    g = DeviceGrid(prob)
+    lib = g.lib
+    b = g.alloc()
+    x = g.alloc()
+    g.upload(prob.pattern, b)
+    rep = _lib.SolveReportC()
+    # warm-up solve
+    check(lib.mq_pcg_solve_dev(g.ctx, ctypes.c_void_p(b), None, ctypes.c_void_p(x), 1e-8, 0.0, 5000, 1,
+                               ctypes.byref(rep)))
+    best = None
+    for _ in range(reps):
+        check(lib.mq_l2_flush(g.ctx))
+        check(lib.mq_pcg_stats(g.ctx, None, None, None, 1))
+        check(lib.mq_pcg_solve_dev(g.ctx, ctypes.c_void_p(b), None, ctypes.c_void_p(x), 1e-8, 0.0, 5000, 1,
+                                   ctypes.byref(rep)))
+        ms = ctypes.c_double()
+        it = ctypes.c_int64()
+        check(lib.mq_pcg_stats(g.ctx, ctypes.byref(ms), ctypes.byref(it), None, 0))
+        if best is None or ms.value < best[0]:
+            best = (ms.value, int(rep.iterations))
+    ms, iters = best
+    n_n = g.n_n
+    byts = float(pcg_launch_bytes(n_n, iters))
+    achieved = byts / (ms * 1e-3) / 1e9
+    g.close()
+    return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "frac": achieved / hbm_peak, "traffic": None,
+            "kernel": "pcg_stencil_kernel", "grid": [128, 128, 128], "n_n": n_n,
+            "iterations": iters, "launch_ms": ms,
+            "us_per_iteration": 1000.0 * ms / max(iters, 1),
+            "bytes_per_launch": byts, "bytes_per_iteration": 72.0 * n_n}
+
+
+def run_device_arm(args):
+    world, rank, local, dist = dist_init()
+    from paper_1611_06721_b200 import PcgConfig, SchurOperator, _lib
+    from paper_1611_06721_b200 import configs as C
+    _lib.load()
+    spec = C.config_spec(1)
+    problem, factors = member_problem(rank)
+    hbm_peak, peak_kind = peaks()
+    op = SchurOperator(problem, pcg=PcgConfig(rel_tol=spec.rel_tol, max_iter=spec.max_iter),
+                       strategy="cspe", max_cols=spec.max_cols, device=local)
+    n_n, n_c = op.grid.n_n, op.grid.n_c
+    barrier(dist)
+    with ClockSampler(local) as clk:
+        step_ms, pcg_ms, iters, launches = time_device_steps(op, spec, args.warmup, args.steps,
+                                                             flush=not args.no_flush)
+    barrier(dist)
+    total_ms = float(step_ms.sum())
+    total_ms_max = max_over_ranks(total_ms, dist, local)
+    value = world * args.steps / (total_ms_max * 1e-3)
+    # roofline of the dominant kernel inside the timed region
+    launch_bytes = pcg_launch_bytes(n_n, iters.reshape(-1)).sum()
+    pcg_total = float(pcg_ms.sum())
+    achieved = launch_bytes / (pcg_total * 1e-3) / 1e9 if pcg_total > 0 else 0.0
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None, "kernel": "pcg_stencil_kernel",
+                "peak_kind": peak_kind, "pcg_share_of_step": pcg_total / total_ms,
+                "pcg_launches": int(iters.size), "pcg_iterations": int(iters.sum()),
+                "note": "config-1 PCG vectors (4 x 5.7 MB) are L2-resident inside a solve; "
+                        "see roofline_cfg2 for the HBM-bound 128^3 case"}
+    op.grid.close()
+    line = None
+    if rank == 0:
+        e2e_v, e2e_s, h2d, d2h = time_e2e(problem, spec, args.warmup, args.steps)
+        roof2 = None
+        if not args.skip_cfg2:
+            roof2 = cfg2_pcg_roofline(hbm_peak)
+        cpu = None
+        if world == 1 and not args.skip_cpu:
+            v, done, el, _ = cpu_reference(spec, 0, args.cpu_steps, budget_s=30.0)
+            cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"first {done} steps of config 1 ({el:.1f} s; oracle/mq_oracle.py, "
+                             "numpy/scipy port of mqsolve; csr_matvec single-threaded)"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY 8(d) geometry: iron block + annular coil, seeded ensemble factors)",
+            "config": {"workload": "cfg1_64cube_brauer_cspe5", "grid": [64, 64, 64],
+                       "n_n": n_n, "n_c": n_c, "strategy": "cspe", "max_cols": 5,
+                       "rel_tol": spec.rel_tol, "dt": spec.dt,
+                       "l2": "flushed (256 MB write) before every timed step" if not args.no_flush else "not flushed",
+                       "parallelism": f"replicas{world} (ensemble members, no collectives)",
+                       "member_factors": factors},
+            "timed_step_iterations": iters.tolist(),
+            "clocks": clk.summary(),
+            "roofline": roofline,
+            "roofline_cfg2": roof2,
+            "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "explicit_euler_step + recover_an (host arrays)"},
+            "gpu_launches": launches,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--skip-cfg2", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_device_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,229 @@
+/*
+ * mq_b200.h — C ABI of libmq_b200.so, the B200 (sm_100a) drop-in for the hot
+ * path of the reference `mqsolve` (arXiv 1611.06721): the repeated PCG solve
+ * of the singular nonconducting curl-curl block K_n, the SPE/CSPE and POD
+ * start vectors, the Brauer K_c(a_c) update and the explicit-Euler update.
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/mqsolve):
+ *   mq_ctx_create / mq_partition_export   model.py:438-470 (_Topology, partition)
+ *   mq_pcg_solve_host / mq_pcg_solve_dev  krylov.py:174-250 (pcg_solve) on K_n
+ *   mq_csr_*                              krylov.py:161-171 + 174-250 for a
+ *                                         general CsrMatrix operator (sparse.py:50-176)
+ *   mq_kn_apply                           schur.py:189-191 (_kn_scipy @ x)
+ *   mq_strategy_* (start/observe)         startvec.py:315-472 (StartVectorStrategy,
+ *                                         CspeStrategy, PodStrategy, previous)
+ *   mq_solve_kn                           schur.py:239-264 (SchurOperator.solve_kn)
+ *   mq_kc_apply                           model.py:507-509 (kc_apply closure)
+ *   mq_euler_step / mq_recover_an         schur.py:379-419
+ *   mq_run_explicit                       schur.py:474-607 (time loop, fixed dt)
+ *
+ * Conventions
+ *   Return codes: MQ_OK, MQ_NOT_CONVERGED (SolveReport.converged = False ->
+ *   StepFailureError upstream), MQ_INDEFINITE (IndefiniteOperatorError),
+ *   MQ_INVALID (ValueError), MQ_CUDA_ERROR (RuntimeError), MQ_NONFINITE
+ *   (StepFailureError, non-finite conducting state).  mq_last_error() returns
+ *   the message of the most recent failure on the calling thread.
+ *   Host vectors are in the reference's compact order (ascending global edge
+ *   id, model.py:455-464).  Device vectors ("_dev") are in the padded
+ *   device layout of length mq_dev_len(); entries off the partition are 0.
+ *   One context is driven by one host thread (single-writer),
+ *   on the context's own CUDA stream.  The caller owns host buffers; the
+ *   context owns device buffers.
+ */
+#ifndef MQ_B200_H
+#define MQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MQ_OK 0
+#define MQ_NOT_CONVERGED 1
+#define MQ_INDEFINITE 2
+#define MQ_INVALID 3
+#define MQ_CUDA_ERROR 4
+#define MQ_NONFINITE 5
+
+/* RHS families, startvec.py:45-50 */
+#define MQ_FAM_SOURCE 0
+#define MQ_FAM_COUPLING_CURRENT 1
+#define MQ_FAM_COUPLING_PREVIOUS 2
+
+/* strategies, startvec.py:457-472 */
+#define MQ_STRAT_ZERO 0
+#define MQ_STRAT_PREVIOUS 1
+#define MQ_STRAT_CSPE 2
+#define MQ_STRAT_POD 3
+
+typedef struct mq_ctx mq_ctx;
+
+/* GridSpec + conductor Material + air reluctivity (model.py:70-155, 438). */
+typedef struct mq_grid_desc {
+  int32_t nx, ny, nz;
+  double h;
+  const int8_t *material; /* nx*ny*nz, C order; 0 air, 1 conductor, 2 coil */
+  double nu_air;          /* air reluctivity (model.py:439) */
+  double kappa;           /* conductor conductivity */
+  double brauer_k1, brauer_k2, brauer_k3; /* nu = k1 exp(k2 B^2) + k3 */
+  double kn_diag;         /* assembled K_n diagonal; 0 -> derived */
+  double kn_off;          /* assembled |K_n| off-diagonal; 0 -> derived */
+} mq_grid_desc;
+
+/* SolveReport (krylov.py:75-79) plus operator applications. */
+typedef struct mq_solve_report {
+  int32_t iterations;
+  int32_t converged;
+  double final_rel_residual;
+  int64_t applies;
+} mq_solve_report;
+
+/* Start-vector / solver configuration (schur.py:177-207, krylov.py:57-72). */
+typedef struct mq_solver_cfg {
+  int32_t strategy;  /* MQ_STRAT_* */
+  int32_t max_cols;  /* CSPE basis cap */
+  int32_t n_pod;     /* POD ring size */
+  int32_t max_iter;
+  double eps_pod;
+  double rel_tol;
+  double abs_tol;
+  double drop_tol;   /* CSPE drop tolerance (schur.py:207: = rel_tol) */
+} mq_solver_cfg;
+
+/* Per-family diagnostics (startvec.py:392-454, schur.py:217-263). */
+typedef struct mq_diag {
+  int64_t solves[3];
+  int64_t iterations[3];
+  int64_t pcg_applies;
+  int64_t maintenance_applies;
+  int32_t basis_cols[3];   /* CSPE: basis size per family */
+  int32_t pod_k;           /* POD: last retained modes */
+  double pod_info;         /* POD: last kept information */
+  double min_pod_info;     /* POD: min over projections (1.0 if none) */
+  int64_t columns_accepted[3];
+  int64_t columns_dropped[3];
+  int64_t evictions[3];
+} mq_diag;
+
+/* ---- context ------------------------------------------------------------ */
+const char *mq_last_error(void);
+int mq_device_count(int32_t *count);
+int mq_ctx_create(const mq_grid_desc *desc, int32_t device, mq_ctx **out);
+void mq_ctx_destroy(mq_ctx *ctx);
+int64_t mq_n_n(const mq_ctx *ctx);     /* nonconducting interior dofs */
+int64_t mq_n_c(const mq_ctx *ctx);     /* conducting dofs */
+int64_t mq_dev_len(const mq_ctx *ctx); /* padded device vector length */
+int mq_kn_coefficients(const mq_ctx *ctx, double *diag, double *off, double *jacobi_inv);
+/* bit-exact partition check: global edge ids, ascending (model.py:455-462) */
+int mq_partition_export(const mq_ctx *ctx, int64_t *noncond_global, int64_t *cond_global);
+/* global edge id -> compact nonconducting index (-1 if not a K_n dof) */
+int mq_map_global_to_noncond(const mq_ctx *ctx, const int64_t *gid, int64_t n, int64_t *out);
+int mq_ctx_sync(mq_ctx *ctx);
+/* optional external stream (cudaStream_t as void*; NULL restores own) */
+int mq_ctx_set_stream(mq_ctx *ctx, void *stream);
+
+/* ---- device vectors (padded layout) ------------------------------------- */
+int mq_vec_alloc(mq_ctx *ctx, double **dev);            /* zero-filled */
+int mq_vec_free(mq_ctx *ctx, double *dev);
+int mq_vec_upload(mq_ctx *ctx, const double *host_compact, double *dev);
+int mq_vec_download(mq_ctx *ctx, const double *dev, double *host_compact);
+
+/* ---- K_n operator (schur.py:189-191) ------------------------------------ */
+int mq_kn_apply_dev(mq_ctx *ctx, const double *x_dev, double *y_dev);
+int mq_kn_apply_host(mq_ctx *ctx, const double *x, double *y);
+
+/* ---- PCG on K_n with Jacobi (krylov.py:174-250) -------------------------
+ * x0 may be NULL (start from zero, r = b, no initial application). */
+int mq_pcg_solve_dev(mq_ctx *ctx, const double *b_dev, const double *x0_dev,
+                     double *x_dev, double rel_tol, double abs_tol,
+                     int32_t max_iter, int32_t use_jacobi, mq_solve_report *rep);
+int mq_pcg_solve_host(mq_ctx *ctx, const double *b, const double *x0, double *x,
+                      double rel_tol, double abs_tol, int32_t max_iter,
+                      int32_t use_jacobi, mq_solve_report *rep);
+
+/* ---- PCG on a general CSR operator (krylov.py:161-250) ------------------
+ * int32 column indices, int64 row pointers; inv_diag NULL = no
+ * preconditioner.  All pointers are HOST; the solve runs on `device`. */
+int mq_csr_pcg_solve(int32_t device, int64_t n, const int64_t *row_ptr,
+                     const int32_t *col_idx, const double *values,
+                     const double *b, const double *x0, double *x,
+                     const double *inv_diag, double rel_tol, double abs_tol,
+                     int32_t max_iter, mq_solve_report *rep);
+int mq_csr_spmv(int32_t device, int64_t nrows, int64_t ncols,
+                const int64_t *row_ptr, const int32_t *col_idx,
+                const double *values, const double *x, double *y);
+
+/* ---- solver: strategy + families + conducting block ---------------------
+ * One solver per context.  pattern: compact source pattern (n_n). */
+int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern);
+int mq_solver_reset(mq_ctx *ctx);
+/* SchurOperator.solve_kn: rhs/y device vectors; reports iterations */
+int mq_solve_kn(mq_ctx *ctx, int32_t family, const double *rhs_dev, double *y_dev,
+                mq_solve_report *rep);
+/* StartVectorStrategy pieces on device vectors */
+int mq_strategy_start(mq_ctx *ctx, int32_t family, const double *rhs_dev, double *x0_dev);
+int mq_strategy_observe(mq_ctx *ctx, int32_t family, const double *y_dev);
+int mq_diagnostics(mq_ctx *ctx, mq_diag *out);
+/* CSPE cache contents of one family (compact host, column-major n_n x k) */
+int mq_cspe_export(mq_ctx *ctx, int32_t family, int32_t *k, double *basis,
+                   double *products, double *galerkin);
+
+/* ---- conducting block -------------------------------------------------- */
+/* K_c(state) x on host compact n_c vectors (model.py:507-509) */
+int mq_kc_apply_host(mq_ctx *ctx, const double *state, const double *x, double *y);
+/* y_n = K_cn^T a_c (host n_c -> host n_n) and y_c = K_cn x_n */
+int mq_kcn_t_apply_host(mq_ctx *ctx, const double *a_c, double *y_n);
+int mq_kcn_apply_host(mq_ctx *ctx, const double *x_n, double *y_c);
+/* M_c diagonal (model.py:486-491) */
+int mq_mc_diag(mq_ctx *ctx, double *mc_diag);
+
+/* state a_c lives on device; set/get in compact host order */
+int mq_state_set(mq_ctx *ctx, const double *a_c, double t);
+int mq_state_get(mq_ctx *ctx, double *a_c, double *t);
+/* explicit_euler_step: two solves (SOURCE at t+dt with waveform value
+ * wave_new, COUPLING_PREVIOUS), then the Euler update (schur.py:379-405) */
+int mq_euler_step(mq_ctx *ctx, double dt, double wave_new, int64_t step_index,
+                  mq_solve_report *rep_src, mq_solve_report *rep_cpl);
+/* recover_an at the current state (schur.py:408-419); a_n to host if non-NULL */
+int mq_recover_an(mq_ctx *ctx, double wave_now, double *a_n_host,
+                  mq_solve_report *rep_src, mq_solve_report *rep_cpl);
+
+/* a_n = y_src - y_cpl of the most recent recovery / step solves (host n_n) */
+int mq_last_an(mq_ctx *ctx, double *a_n_host);
+
+/* Device-resident time loop: n_steps Euler steps with per-step dt[] and
+ * waveform wave[] (wave[m] = waveform(t_m) for m = 0..n_steps, t_0 = start),
+ * recover_an after every step when recover_every_step != 0 (output rows).
+ * iters_out (optional, 4*n_steps int32): per step [src, cpl_prev, src_rec,
+ * cpl_cur]; a_c_hist (optional, n_steps*n_c) states after each step.
+ * Host sync only at the end.  use_graph != 0 replays one captured step. */
+int mq_run_explicit(mq_ctx *ctx, int64_t n_steps, const double *dt,
+                    const double *wave, int32_t recover_every_step,
+                    int32_t use_graph, int32_t *iters_out, double *a_c_hist,
+                    int64_t *failed_step);
+
+/* The same loop in three calls: prepare (tables, counters), enqueue n steps
+ * (asynchronous), finish (sync, error check, iteration log). */
+int mq_run_prepare(mq_ctx *ctx, int64_t n_steps, const double *dt, const double *wave,
+                   int32_t recover_every_step);
+int mq_run_steps(mq_ctx *ctx, int64_t n, int32_t use_graph, double *a_c_hist_dev);
+int mq_run_finish(mq_ctx *ctx, int32_t *iters_out, int64_t *failed_step);
+
+/* ---- timing (CUDA events on the context stream) ------------------------- */
+/* Sum of the device times of the PCG launches of the last step (when PCG
+ * timing is enabled with mq_pcg_stats(..., 1)). */
+int mq_pcg_collect(mq_ctx *ctx, double *ms, int32_t *n_events);
+int mq_timer_start(mq_ctx *ctx);
+int mq_timer_stop(mq_ctx *ctx, double *ms);
+/* cumulative device time and launch count of the PCG kernels */
+int mq_pcg_stats(mq_ctx *ctx, double *pcg_ms, int64_t *pcg_iterations,
+                 int64_t *launches, int32_t enable);
+int mq_kernel_launches(mq_ctx *ctx, int64_t *count);
+int mq_l2_flush(mq_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MQ_B200_H */

@@ -1,0 +1,177 @@
+// Device helpers shared by the libmq_b200 kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mq_internal.h"
+
+namespace mq {
+
+constexpr int kBlock = 256;            // threads per CTA for streaming kernels
+constexpr int kWarps = kBlock / 32;
+
+// IEEE round-to-nearest without FMA contraction: numpy evaluates a*x + y as
+// a rounded multiply followed by a rounded add (krylov.py:238-248,
+// schur.py:400), so every update below spells out the two roundings.
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+
+__device__ __forceinline__ bool active(const uint32_t *mask, int64_t e) {
+  return (mask[e >> 5] >> (e & 31)) & 1u;
+}
+
+// ---- deterministic reductions -------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = add(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide sum of NV values per thread; result valid in every thread.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double *smem /* NV*kWarps */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) smem[q * kWarps + warp] = v[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    double s = 0.0;
+    for (int w = 0; w < kWarps; ++w) s = add(s, smem[q * kWarps + w]);
+    v[q] = s;
+  }
+  __syncthreads();
+}
+
+// Sum partials[q*G + 0..G) in a fixed order; identical in every CTA.
+template <int NV>
+__device__ __forceinline__ void grid_partials_sum(const double *partials, int G, double (&out)[NV],
+                                                  double *smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = 0.0;
+      for (int b = lane; b < G; b += 32) s = add(s, __ldcg(partials + (int64_t)q * G + b));
+      s = warp_sum(s);
+      if (lane == 0) smem[q] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) out[q] = smem[q];
+  __syncthreads();
+}
+
+// ---- grid-wide barrier (cooperative launch guarantees co-residency) -------
+// Mirrors the cooperative-groups grid sync: CTA barrier, one thread fences
+// and arrives, spins on the generation word, fences again.  A watchdog
+// (5 s on %globaltimer) turns a lost arrival into an error instead of a hang.
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ bool grid_sync(GridBar *bar) {
+  __shared__ int s_fail;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_fail = 0;
+    if (*((volatile unsigned int *)&bar->error)) s_fail = 1;
+  }
+  __syncthreads();
+  if (s_fail) return false;
+  if (threadIdx.x == 0) {
+    volatile unsigned int *vgen = &bar->gen;
+    const unsigned int g = *vgen;
+    __threadfence();
+    const unsigned int arrived = atomicAdd(&bar->count, 1u);
+    if (arrived == gridDim.x - 1) {
+      atomicExch(&bar->count, 0u);
+      __threadfence();
+      atomicAdd(&bar->gen, 1u);
+    } else {
+      const uint64_t t0 = globaltimer_ns();
+      while (*vgen == g) {
+        __nanosleep(64);
+        if (globaltimer_ns() - t0 > 5000000000ull) {
+          atomicExch(&bar->error, 1u);
+          s_fail = 1;
+          break;
+        }
+      }
+    }
+    __threadfence();
+    if (*((volatile unsigned int *)&bar->error)) s_fail = 1;
+  }
+  __syncthreads();
+  return s_fail == 0;
+}
+
+// ---- the K_n stencil -------------------------------------------------------
+// Row of K_n = (nu0/h) * S at padded index e of component c, evaluated as the
+// CSR row sum in ascending column order with separately rounded products and
+// sums, which reproduces scipy's csr_matvec (sum starts at 0, += a_ij*x_j)
+// bit for bit: columns sorted by global id are the padded offsets below in
+// ascending order, and absent (masked) neighbours hold exact zeros.
+// Coefficients: SURVEY Appendix A, derived from C^T diag(w/h) C with the
+// curl incidence of model.py:213-226.
+template <class Ld>
+__device__ __forceinline__ double stencil_row(int c, int64_t e, const Lay &L, double dg, double of,
+                                              Ld ld) {
+  const int64_t C = L.C, Si = L.Si, Sj = L.Sj;
+  double s;
+  if (c == 0) {
+    s = -mul(of, ld(e - Sj));
+    s = sub(s, mul(of, ld(e - 1)));
+    s = add(s, mul(dg, ld(e)));
+    s = sub(s, mul(of, ld(e + 1)));
+    s = sub(s, mul(of, ld(e + Sj)));
+    s = add(s, mul(of, ld(e + C - Sj)));
+    s = sub(s, mul(of, ld(e + C)));
+    s = sub(s, mul(of, ld(e + C + Si - Sj)));
+    s = add(s, mul(of, ld(e + C + Si)));
+    s = add(s, mul(of, ld(e + 2 * C - 1)));
+    s = sub(s, mul(of, ld(e + 2 * C)));
+    s = sub(s, mul(of, ld(e + 2 * C + Si - 1)));
+    s = add(s, mul(of, ld(e + 2 * C + Si)));
+  } else if (c == 1) {
+    s = mul(of, ld(e - C - Si));
+    s = sub(s, mul(of, ld(e - C - Si + Sj)));
+    s = sub(s, mul(of, ld(e - C)));
+    s = add(s, mul(of, ld(e - C + Sj)));
+    s = sub(s, mul(of, ld(e - Si)));
+    s = sub(s, mul(of, ld(e - 1)));
+    s = add(s, mul(dg, ld(e)));
+    s = sub(s, mul(of, ld(e + 1)));
+    s = sub(s, mul(of, ld(e + Si)));
+    s = add(s, mul(of, ld(e + C - 1)));
+    s = sub(s, mul(of, ld(e + C)));
+    s = sub(s, mul(of, ld(e + C + Sj - 1)));
+    s = add(s, mul(of, ld(e + C + Sj)));
+  } else {
+    s = mul(of, ld(e - 2 * C - Si));
+    s = sub(s, mul(of, ld(e - 2 * C - Si + 1)));
+    s = sub(s, mul(of, ld(e - 2 * C)));
+    s = add(s, mul(of, ld(e - 2 * C + 1)));
+    s = add(s, mul(of, ld(e - C - Sj)));
+    s = sub(s, mul(of, ld(e - C - Sj + 1)));
+    s = sub(s, mul(of, ld(e - C)));
+    s = add(s, mul(of, ld(e - C + 1)));
+    s = sub(s, mul(of, ld(e - Si)));
+    s = sub(s, mul(of, ld(e - Sj)));
+    s = add(s, mul(dg, ld(e)));
+    s = sub(s, mul(of, ld(e + Sj)));
+    s = sub(s, mul(of, ld(e + Si)));
+  }
+  return s;
+}
+
+}  // namespace mq

@@ -1,0 +1,1611 @@
+// Device-resident SchurOperator: start-vector strategies, solve_kn, the
+// Brauer K_c update, the explicit-Euler update and the time loop.
+//
+// Reference (pkg/src/mqsolve):
+//   SubspaceCache.insert/project ..... startvec.py:158-225 (CGS2, FIFO, bordered Galerkin)
+//   _cholesky_lower / _solve_spd ..... startvec.py:59-79
+//   pod_start_vector / SnapshotBuffer  startvec.py:239-309
+//   strategies ....................... startvec.py:345-472
+//   solve_kn ......................... schur.py:239-264
+//   kc_apply (Brauer) ................ model.py:107-125, 492-509
+//   explicit_euler_step / recover_an . schur.py:379-419
+//   run_explicit ..................... schur.py:474-607
+//
+// All decisions (accept/drop/evict, pivot failures, POD truncation, solve
+// failures) are taken on the device, so a whole time step is a fixed kernel
+// sequence that can be captured once in a CUDA graph and replayed; the host
+// reads iteration logs and error words only at the end of a run.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "mq_ctx.h"
+#include "mq_device.cuh"
+
+namespace mq {
+
+// ---------------------------------------------------------------------------
+// host-side solver object
+// ---------------------------------------------------------------------------
+struct StepParams {
+  double dt;        // step size of the current step
+  double wave_new;  // waveform(t + dt)
+  double wave_now;  // waveform(t) used by recover_an
+  long long step;   // 1-based step index for error messages
+};
+
+struct SolverHost {
+  mq_solver_cfg cfg{};
+  FamDev *d_fam = nullptr;  // 3 families
+  RunDev *d_run = nullptr;
+  StepParams *d_par = nullptr;
+  // slot tables (device arrays of device pointers)
+  double **d_U[3] = {nullptr, nullptr, nullptr};
+  double **d_KU[3] = {nullptr, nullptr, nullptr};
+  double **d_X[3] = {nullptr, nullptr, nullptr};
+  double **d_B = nullptr, **d_KB = nullptr;
+  std::vector<double *> h_U[3], h_KU[3], h_X[3], h_B, h_KB;
+  double *last[3] = {nullptr, nullptr, nullptr};
+  double *w1 = nullptr, *w2 = nullptr;
+  double *rhs_src = nullptr, *rhs_cpl = nullptr, *y_src = nullptr, *y_cpl = nullptr;
+  // source pattern (sparse: padded index + value)
+  int32_t *d_pat_idx = nullptr;
+  double *d_pat_val = nullptr;
+  int64_t n_pat = 0;
+  // reduction scratch
+  double *d_red = nullptr;
+  unsigned int *d_cnt = nullptr;
+  int red_grid = 1;
+  // logs
+  int32_t *d_log = nullptr;
+  int64_t log_cap = 0;
+  double *d_dt_tab = nullptr, *d_wave_tab = nullptr;
+  int64_t tab_cap = 0;
+  std::vector<void *> mem;
+  int *d_iota = nullptr;  // identity order 0..MAXS-1
+  cudaGraphExec_t graph_exec = nullptr;
+  bool graph_ok = true;
+  int64_t launches_per_step = 0;
+  bool recover_every_step = true;
+  int per_step = 4;
+  int64_t n_planned = 0, n_enqueued = 0;
+};
+
+static int s_alloc(mq_ctx *ctx, SolverHost *s, void **p, size_t bytes) {
+  MQ_CUDA(cudaMalloc(p, bytes));
+  MQ_CUDA(cudaMemsetAsync(*p, 0, bytes, ctx->stream));
+  s->mem.push_back(*p);
+  return MQ_OK;
+}
+
+void solver_free(mq_ctx *ctx) {
+  SolverHost *s = ctx->solver;
+  if (!s) return;
+  if (s->graph_exec) cudaGraphExecDestroy(s->graph_exec);
+  for (void *p : s->mem) cudaFree(p);
+  delete s;
+  ctx->solver = nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// reduction helper: NQ runtime values per thread -> out[q] via last block
+// ---------------------------------------------------------------------------
+constexpr int RQ = MAXS + 2;  // max values reduced by one kernel
+
+__device__ __forceinline__ void last_block_reduce(double *acc, int nq, double *partials, unsigned int *counter,
+                                                  double *out) {
+  __shared__ double sm[RQ * kWarps];
+  __shared__ bool is_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = gridDim.x;
+  for (int q = 0; q < nq; ++q) {
+    double v = warp_sum(acc[q]);
+    if (lane == 0) sm[q * kWarps + warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < nq) {
+    double s = 0.0;
+    for (int w = 0; w < kWarps; ++w) s = add(s, sm[threadIdx.x * kWarps + w]);
+    partials[(int64_t)threadIdx.x * G + blockIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = (atomicAdd(counter, 1u) == (unsigned)G - 1);
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    if (threadIdx.x < nq) {
+      double s = 0.0;
+      for (int b = 0; b < G; ++b) s = add(s, __ldcg(partials + (int64_t)threadIdx.x * G + b));
+      out[threadIdx.x] = s;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+  }
+}
+
+#define FOR_ACTIVE(L, mask)                                                                  \
+  for (int64_t w_ = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); w_ < (L).words;         \
+       w_ += (int64_t)gridDim.x * kWarps)                                                    \
+    if (((mask)[w_] >> (threadIdx.x & 31)) & 1u)
+
+// d[j] = A_{order[j]} . v  (j < k), d[k] = v . v when selfdot
+__global__ void __launch_bounds__(kBlock) k_mdot(Lay L, const uint32_t *__restrict__ mask, double *const *tab,
+                                                 const int *order, const int *kptr, const double *__restrict__ v,
+                                                 int selfdot, double *out, double *partials, unsigned int *counter) {
+  __shared__ const double *ptr[MAXS];
+  const int k = *kptr;
+  if (threadIdx.x < k) ptr[threadIdx.x] = tab[order[threadIdx.x]];
+  __syncthreads();
+  double acc[RQ];
+#pragma unroll
+  for (int q = 0; q < RQ; ++q) acc[q] = 0.0;
+  FOR_ACTIVE(L, mask) {
+    const int64_t e = w_ * 32 + (threadIdx.x & 31);
+    const double vv = v[e];
+#pragma unroll
+    for (int j = 0; j < MAXS; ++j)
+      if (j < k) acc[j] = add(acc[j], mul(ptr[j][e], vv));
+    if (selfdot) acc[k] = add(acc[k], mul(vv, vv));
+  }
+  last_block_reduce(acc, k + (selfdot ? 1 : 0), partials, counter, out);
+}
+
+// out = in - sum_j c_j A_{order[j]};  d[j] = A_{order[j]} . out (j < ndot), d[ndot] = out.out
+__global__ void __launch_bounds__(kBlock) k_axpy_dots(Lay L, const uint32_t *__restrict__ mask, double *const *tab,
+                                                      const int *order, const int *kptr, const double *c,
+                                                      const double *in, double *outv, int ndot_is_k, double *dout,
+                                                      double *partials, unsigned int *counter, const int *gate) {
+  if (gate && !*gate) return;
+  __shared__ const double *ptr[MAXS];
+  __shared__ double cs[MAXS];
+  const int k = *kptr;
+  if (threadIdx.x < k) { ptr[threadIdx.x] = tab[order[threadIdx.x]]; cs[threadIdx.x] = c[threadIdx.x]; }
+  __syncthreads();
+  const int nd = ndot_is_k ? k : 0;
+  double acc[RQ];
+#pragma unroll
+  for (int q = 0; q < RQ; ++q) acc[q] = 0.0;
+  FOR_ACTIVE(L, mask) {
+    const int64_t e = w_ * 32 + (threadIdx.x & 31);
+    double u[MAXS];
+    double t = 0.0;
+#pragma unroll
+    for (int j = 0; j < MAXS; ++j)
+      if (j < k) {
+        u[j] = ptr[j][e];
+        t = (j == 0) ? mul(cs[0], u[0]) : add(t, mul(cs[j], u[j]));
+      }
+    const double o = sub(in[e], t);
+    outv[e] = o;
+#pragma unroll
+    for (int j = 0; j < MAXS; ++j)
+      if (j < nd) acc[j] = add(acc[j], mul(u[j], o));
+    acc[nd] = add(acc[nd], mul(o, o));
+  }
+  last_block_reduce(acc, nd + 1, partials, counter, dout);
+}
+
+// out = sum_j c_j A_{order[j]} (0 when k == 0)
+__global__ void __launch_bounds__(kBlock) k_comb(Lay L, const uint32_t *__restrict__ mask, double *const *tab,
+                                                 const int *order, const int *kptr, const double *c, double *outv) {
+  __shared__ const double *ptr[MAXS];
+  __shared__ double cs[MAXS];
+  const int k = *kptr;
+  if (threadIdx.x < k) { ptr[threadIdx.x] = tab[order[threadIdx.x]]; cs[threadIdx.x] = c[threadIdx.x]; }
+  __syncthreads();
+  FOR_ACTIVE(L, mask) {
+    const int64_t e = w_ * 32 + (threadIdx.x & 31);
+    double t = 0.0;
+    for (int j = 0; j < k; ++j) t = (j == 0) ? mul(cs[0], ptr[0][e]) : add(t, mul(cs[j], ptr[j][e]));
+    outv[e] = t;
+  }
+}
+
+// CSPE: u = w/nrm into U[slot], ku = K u into KU[slot], cross_j = U_{order[j]}.ku (j<kprime), diag = u.ku
+__global__ void __launch_bounds__(kBlock) k_cspe_product(Lay L, const uint32_t *__restrict__ mask, double dg,
+                                                         double of, FamDev *f, double *const *Utab,
+                                                         double *const *KUtab, const double *__restrict__ w,
+                                                         double *partials, unsigned int *counter) {
+  if (!f->accept) return;
+  __shared__ const double *ptr[MAXS];
+  const int kp = f->kprime;
+  if (threadIdx.x < kp) ptr[threadIdx.x] = Utab[f->order[threadIdx.x]];
+  __syncthreads();
+  double *U = Utab[f->new_slot];
+  double *KU = KUtab[f->new_slot];
+  const double nrm = f->nrm;
+  double acc[RQ];
+#pragma unroll
+  for (int q = 0; q < RQ; ++q) acc[q] = 0.0;
+  FOR_ACTIVE(L, mask) {
+    const int64_t e = w_ * 32 + (threadIdx.x & 31);
+    const int c = e < L.C ? 0 : (e < 2 * L.C ? 1 : 2);
+    auto u = [&](int64_t q) { return w[q] / nrm; };
+    const double ue = u(e);
+    const double ku = stencil_row(c, e, L, dg, of, u);
+    U[e] = ue;
+    KU[e] = ku;
+#pragma unroll
+    for (int j = 0; j < MAXS; ++j)
+      if (j < kp) acc[j] = add(acc[j], mul(ptr[j][e], ku));
+    acc[kp] = add(acc[kp], mul(ue, ku));
+  }
+  last_block_reduce(acc, kp + 1, partials, counter, f->d + 0);
+}
+
+// POD: B_j = (sum_l X_{order[l]} W[l][j]) / sigma_j  for j < podk
+__global__ void __launch_bounds__(kBlock) k_pod_basis(Lay L, const uint32_t *__restrict__ mask, FamDev *f,
+                                                      double *const *Xtab, double *const *Btab) {
+  __shared__ const double *xp[MAXS];
+  __shared__ double *bp[MAXS];
+  __shared__ double Wt[MAXS * MAXS];
+  __shared__ double sg[MAXS];
+  const int m = f->k, kk = f->podk;
+  if (kk == 0) return;
+  if (threadIdx.x < m) xp[threadIdx.x] = Xtab[f->order[threadIdx.x]];
+  if (threadIdx.x < kk) { bp[threadIdx.x] = Btab[threadIdx.x]; sg[threadIdx.x] = f->pod_sigma[threadIdx.x]; }
+  for (int q = threadIdx.x; q < MAXS * MAXS; q += blockDim.x) Wt[q] = f->W[q];
+  __syncthreads();
+  FOR_ACTIVE(L, mask) {
+    const int64_t e = w_ * 32 + (threadIdx.x & 31);
+    double x[MAXS];
+    for (int l = 0; l < m; ++l) x[l] = xp[l][e];
+    for (int j = 0; j < kk; ++j) {
+      double t = mul(x[0], Wt[0 * MAXS + j]);
+      for (int l = 1; l < m; ++l) t = add(t, mul(x[l], Wt[l * MAXS + j]));
+      bp[j][e] = t / sg[j];
+    }
+  }
+}
+
+// POD: KB_j = K B_j for j < podk (blockIdx.y = j)
+__global__ void __launch_bounds__(kBlock) k_spmv_multi(Lay L, const uint32_t *__restrict__ mask, double dg, double of,
+                                                       const FamDev *f, double *const *Btab, double *const *KBtab) {
+  const int j = blockIdx.y;
+  if (j >= f->podk) return;
+  const double *B = Btab[j];
+  double *KB = KBtab[j];
+  FOR_ACTIVE(L, mask) {
+    const int64_t e = w_ * 32 + (threadIdx.x & 31);
+    const int c = e < L.C ? 0 : (e < 2 * L.C ? 1 : 2);
+    KB[e] = stencil_row(c, e, L, dg, of, [&](int64_t q) { return B[q]; });
+  }
+}
+
+// POD Galerkin: blockIdx.y = j < podk -> Gk[i][j] = B_i . KB_j; j == podk -> d[i] = B_i . rhs
+__global__ void __launch_bounds__(kBlock) k_pod_galerkin(Lay L, const uint32_t *__restrict__ mask, FamDev *f,
+                                                         double *const *Btab, double *const *KBtab,
+                                                         const double *__restrict__ rhs, double *partials,
+                                                         unsigned int *counters) {
+  const int j = blockIdx.y;
+  const int kk = f->podk;
+  if (j > kk) return;
+  __shared__ const double *bp[MAXS];
+  if (threadIdx.x < kk) bp[threadIdx.x] = Btab[threadIdx.x];
+  __syncthreads();
+  const double *v = (j < kk) ? KBtab[j] : rhs;
+  double acc[RQ];
+#pragma unroll
+  for (int q = 0; q < RQ; ++q) acc[q] = 0.0;
+  FOR_ACTIVE(L, mask) {
+    const int64_t e = w_ * 32 + (threadIdx.x & 31);
+    const double vv = v[e];
+#pragma unroll
+    for (int i = 0; i < MAXS; ++i)
+      if (i < kk) acc[i] = add(acc[i], mul(bp[i][e], vv));
+  }
+  double *out = (j < kk) ? (f->Gk + (int64_t)j * MAXS) : f->d;  // Gk stored column j contiguous
+  last_block_reduce(acc, kk, partials + (int64_t)j * RQ * gridDim.x, counters + j, out);
+}
+
+// POD push: copy y into the ring slot and update the Gram row/column
+__global__ void __launch_bounds__(kBlock) k_pod_push(Lay L, const uint32_t *__restrict__ mask, FamDev *f,
+                                                     double *const *Xtab, int n_pod, const double *__restrict__ y,
+                                                     double *partials, unsigned int *counter) {
+  __shared__ const double *ptr[MAXS];
+  const int m = f->k;
+  const int slot = (m < n_pod) ? m : f->order[0];
+  // other snapshots staying in the ring (logical order), excluding the evicted one
+  const int first = (m < n_pod) ? 0 : 1;
+  const int nother = m - first;
+  if (threadIdx.x < nother) ptr[threadIdx.x] = Xtab[f->order[first + threadIdx.x]];
+  __syncthreads();
+  double *X = Xtab[slot];
+  double acc[RQ];
+#pragma unroll
+  for (int q = 0; q < RQ; ++q) acc[q] = 0.0;
+  FOR_ACTIVE(L, mask) {
+    const int64_t e = w_ * 32 + (threadIdx.x & 31);
+    const double yv = y[e];
+    X[e] = yv;
+#pragma unroll
+    for (int j = 0; j < MAXS; ++j)
+      if (j < nother) acc[j] = add(acc[j], mul(ptr[j][e], yv));
+    acc[nother] = add(acc[nother], mul(yv, yv));
+  }
+  last_block_reduce(acc, nother + 1, partials, counter, f->d);
+}
+
+// ---------------------------------------------------------------------------
+// small dense kernels (one CTA)
+// ---------------------------------------------------------------------------
+// Cholesky with the reference's pivot rule (startvec.py:59-74); returns the
+// failing column or -1.  a: n x n row-major with leading dimension MAXS.
+__device__ int chol_small(const double *a, double *low, int n) {
+  for (int q = 0; q < n * MAXS; ++q) low[q] = 0.0;
+  for (int j = 0; j < n; ++j) {
+    double dot = 0.0;
+    for (int l = 0; l < j; ++l) dot = (l == 0) ? mul(low[j * MAXS], low[j * MAXS]) : add(dot, mul(low[j * MAXS + l], low[j * MAXS + l]));
+    const double gjj = a[j * MAXS + j];
+    const double s = sub(gjj, dot);
+    if (!isfinite(s) || s <= 1e-12 * fabs(gjj) || s <= 0.0) return j;
+    const double ljj = sqrt(s);
+    low[j * MAXS + j] = ljj;
+    for (int i = j + 1; i < n; ++i) {
+      double t = 0.0;
+      for (int l = 0; l < j; ++l) t = (l == 0) ? mul(low[i * MAXS], low[j * MAXS]) : add(t, mul(low[i * MAXS + l], low[j * MAXS + l]));
+      low[i * MAXS + j] = sub(a[i * MAXS + j], t) / ljj;
+    }
+  }
+  return -1;
+}
+
+// L L^T c = rhs (startvec.py:77-79)
+__device__ void chol_solve_small(const double *low, const double *rhs, double *c, int n) {
+  double y[MAXS];
+  for (int i = 0; i < n; ++i) {
+    double t = rhs[i];
+    for (int l = 0; l < i; ++l) t = sub(t, mul(low[i * MAXS + l], y[l]));
+    y[i] = t / low[i * MAXS + i];
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double t = y[i];
+    for (int l = i + 1; l < n; ++l) t = sub(t, mul(low[l * MAXS + i], c[l]));
+    c[i] = t / low[i * MAXS + i];
+  }
+}
+
+__device__ void drop_logical(FamDev *f, int j, double *beta) {
+  const int k = f->k;
+  for (int a = j; a + 1 < k; ++a) {
+    f->order[a] = f->order[a + 1];
+    if (beta) beta[a] = beta[a + 1];
+  }
+  for (int r = 0, rr = 0; r < k; ++r) {
+    if (r == j) continue;
+    for (int c = 0, cc = 0; c < k; ++c) {
+      if (c == j) continue;
+      f->G[rr * MAXS + cc] = f->G[r * MAXS + c];
+      ++cc;
+    }
+    ++rr;
+  }
+  f->k = k - 1;
+}
+
+// CSPE project (startvec.py:207-225): f->d holds beta = U^T rhs
+__global__ void k_cspe_project_small(FamDev *f) {
+  if (threadIdx.x != 0) return;
+  __shared__ double low[MAXS * MAXS];
+  double beta[MAXS];
+  for (int j = 0; j < f->k; ++j) beta[j] = f->d[j];
+  while (f->k > 0) {
+    const int bad = chol_small(f->G, low, f->k);
+    if (bad >= 0) {
+      drop_logical(f, bad, beta);
+      f->dropped += 1;
+      continue;
+    }
+    chol_solve_small(low, beta, f->coef, f->k);
+    break;
+  }
+  f->x0_mode = f->k > 0 ? 1 : 0;
+}
+
+// CSPE observe, after ||v||: reject zero / non-finite (startvec.py:166-170)
+__global__ void k_cspe_gate(FamDev *f) {
+  if (threadIdx.x != 0) return;
+  const double nv = sqrt(f->d[f->k]);
+  f->nv2 = nv;
+  if (nv == 0.0 || !isfinite(nv)) {
+    f->accept = 0;
+    f->dropped += 1;
+  } else {
+    f->accept = 1;
+    for (int j = 0; j < f->k; ++j) f->coef[j] = f->d[j];
+  }
+}
+
+// CGS pass 2 uses the coefficients of pass 1's dot products
+__global__ void k_cspe_gate_c2(FamDev *f) {
+  if (threadIdx.x != 0 || !f->accept) return;
+  for (int j = 0; j < f->k; ++j) f->coef[j] = f->d[j];
+}
+
+// after the second CGS pass: drop test, FIFO eviction, slot choice (startvec.py:175-186)
+__global__ void k_cspe_decide(FamDev *f, const double *nw2, int max_cols, double drop_tol) {
+  if (threadIdx.x != 0 || !f->accept) return;
+  const double nw = sqrt(*nw2);
+  if (nw < drop_tol * f->nv2) {
+    f->accept = 0;
+    f->dropped += 1;
+    return;
+  }
+  f->nrm = nw;
+  if (f->k == max_cols) {
+    const int slot = f->order[0];
+    drop_logical(f, 0, nullptr);
+    f->evictions += 1;
+    f->new_slot = slot;
+  } else {
+    // first slot not referenced by the logical order
+    for (int s = 0; s < MAXS; ++s) {
+      bool used = false;
+      for (int j = 0; j < f->k; ++j) used |= (f->order[j] == s);
+      if (!used) { f->new_slot = s; break; }
+    }
+  }
+  f->kprime = f->k;
+}
+
+// bordered Galerkin update (startvec.py:187-199); f->d = [cross..., diag]
+__global__ void k_cspe_commit(FamDev *f) {
+  if (threadIdx.x != 0 || !f->accept) return;
+  const int k = f->kprime;
+  for (int j = 0; j < k; ++j) {
+    f->G[k * MAXS + j] = f->d[j];
+    f->G[j * MAXS + k] = f->d[j];
+  }
+  f->G[k * MAXS + k] = f->d[k];
+  f->order[k] = f->new_slot;
+  f->k = k + 1;
+  f->products += 1;
+  f->accepted += 1;
+}
+
+// POD push bookkeeping: Gram row/column from f->d (logical order of the
+// remaining snapshots, then the new one)
+__global__ void k_pod_push_commit(FamDev *f, int n_pod) {
+  if (threadIdx.x != 0) return;
+  const int m = f->k;
+  int slot;
+  if (m < n_pod) {
+    slot = m;
+    f->order[m] = slot;
+    f->k = m + 1;
+  } else {
+    slot = f->order[0];
+    for (int a = 0; a + 1 < m; ++a) f->order[a] = f->order[a + 1];
+    f->order[m - 1] = slot;
+  }
+  const int nother = f->k - 1;
+  for (int j = 0; j < nother; ++j) {
+    const int sj = f->order[j];
+    f->G[slot * MAXS + sj] = f->d[j];
+    f->G[sj * MAXS + slot] = f->d[j];
+  }
+  f->G[slot * MAXS + slot] = f->d[nother];
+}
+
+// POD: eigen-decomposition of the logical Gram matrix by parallel cyclic
+// Jacobi (replaces LAPACK syevd, startvec.py:285-294), truncation, basis
+// combination W = V_k (divided by sigma in k_pod_basis).
+__global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
+  __shared__ double A[MAXS * MAXS];
+  __shared__ double V[MAXS * MAXS];
+  __shared__ double cs[MAXS / 2], sn[MAXS / 2];
+  __shared__ int pp[MAXS / 2], qq[MAXS / 2];
+  __shared__ int perm[MAXS];
+  __shared__ double lam[MAXS];
+  __shared__ int s_done;
+  const int m = f->k;
+  if (m == 0) {
+    if (threadIdx.x == 0) { f->podk = 0; f->x0_mode = 0; }
+    return;
+  }
+  const int mm = m + (m & 1);  // even size for the round-robin tournament
+  for (int q = threadIdx.x; q < mm * mm; q += blockDim.x) {
+    const int r = q / mm, c = q % mm;
+    double v = 0.0;
+    if (r < m && c < m) v = f->G[f->order[r] * MAXS + f->order[c]];
+    A[r * MAXS + c] = v;
+    V[r * MAXS + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int npair = mm / 2;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (threadIdx.x == 0) {
+      double off = 0.0, dia = 0.0;
+      for (int r = 0; r < m; ++r)
+        for (int c = 0; c < m; ++c) {
+          if (r == c) dia += A[r * MAXS + c] * A[r * MAXS + c];
+          else off += A[r * MAXS + c] * A[r * MAXS + c];
+        }
+      s_done = (off <= 1e-32 * dia) || off == 0.0;
+    }
+    __syncthreads();
+    if (s_done) break;
+    for (int round = 0; round < mm - 1; ++round) {
+      if (threadIdx.x < npair) {
+        // round-robin pairing: player mm-1 fixed, others rotate
+        const int t = threadIdx.x;
+        int a = (t == 0) ? mm - 1 : (round + t) % (mm - 1);
+        int b = (round + mm - 1 - t) % (mm - 1);
+        if (t == 0) b = round % (mm - 1);
+        const int p = a < b ? a : b, q = a < b ? b : a;
+        pp[t] = p;
+        qq[t] = q;
+        const double apq = A[p * MAXS + q];
+        double c = 1.0, s = 0.0;
+        if (apq != 0.0) {
+          const double th = (A[q * MAXS + q] - A[p * MAXS + p]) / (2.0 * apq);
+          const double tt = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+          c = 1.0 / sqrt(tt * tt + 1.0);
+          s = tt * c;
+        }
+        cs[t] = c;
+        sn[t] = s;
+      }
+      __syncthreads();
+      // rows: row_p' = c row_p - s row_q ; row_q' = s row_p + c row_q
+      for (int it = threadIdx.x; it < npair * mm; it += blockDim.x) {
+        const int t = it / mm, col = it % mm;
+        const int p = pp[t], q = qq[t];
+        const double c = cs[t], s = sn[t];
+        const double ap = A[p * MAXS + col], aq = A[q * MAXS + col];
+        A[p * MAXS + col] = c * ap - s * aq;
+        A[q * MAXS + col] = s * ap + c * aq;
+      }
+      __syncthreads();
+      // columns of A and V
+      for (int it = threadIdx.x; it < npair * mm; it += blockDim.x) {
+        const int t = it / mm, row = it % mm;
+        const int p = pp[t], q = qq[t];
+        const double c = cs[t], s = sn[t];
+        const double ap = A[row * MAXS + p], aq = A[row * MAXS + q];
+        A[row * MAXS + p] = c * ap - s * aq;
+        A[row * MAXS + q] = s * ap + c * aq;
+        const double vp = V[row * MAXS + p], vq = V[row * MAXS + q];
+        V[row * MAXS + p] = c * vp - s * vq;
+        V[row * MAXS + q] = s * vp + c * vq;
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    // sort descending (startvec.py:287-289), sigma = sqrt(clip(lambda, 0))
+    for (int i = 0; i < m; ++i) { perm[i] = i; lam[i] = A[i * MAXS + i]; }
+    for (int i = 0; i < m; ++i)
+      for (int j = i + 1; j < m; ++j)
+        if (lam[perm[j]] > lam[perm[i]]) { int t = perm[i]; perm[i] = perm[j]; perm[j] = t; }
+    double total = 0.0;
+    for (int i = 0; i < m; ++i) {
+      const double l = lam[perm[i]];
+      f->pod_sigma[i] = sqrt(l > 0.0 ? l : 0.0);
+      total += f->pod_sigma[i];
+    }
+    f->nrm = total;
+    int k = 0;
+    if (f->pod_sigma[0] == 0.0) {
+      k = 0;
+    } else {
+      for (int i = 0; i < m; ++i) k += (f->pod_sigma[i] / f->pod_sigma[0] > eps_pod) ? 1 : 0;
+    }
+    f->podk = k;
+    for (int l = 0; l < m; ++l)
+      for (int j = 0; j < k; ++j) f->W[l * MAXS + j] = V[l * MAXS + perm[j]];
+    f->x0_mode = 0;
+  }
+}
+
+// POD Galerkin solve with the k-decrement retry (startvec.py:298-309)
+__global__ void k_pod_solve(FamDev *f, RunDev *run) {
+  if (threadIdx.x != 0) return;
+  __shared__ double low[MAXS * MAXS];
+  __shared__ double g[MAXS * MAXS];
+  int k = f->podk;
+  const int applications = k;
+  if (f->k == 0) return;  // empty buffer: zero start vector, no bookkeeping
+  if (f->pod_sigma[0] == 0.0) {
+    f->podk = 0;
+    f->pod_info = 0.0;
+    run->pod_last_k = 0;
+    run->pod_last_info = 0.0;
+    f->x0_mode = 0;
+    return;
+  }
+  // Gk column j contiguous: Gk[j*MAXS + i] = B_i . KB_j = g[i][j]
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) {
+      const double gij = f->Gk[j * MAXS + i], gji = f->Gk[i * MAXS + j];
+      g[i * MAXS + j] = mul(0.5, add(gij, gji));
+    }
+  while (k > 0) {
+    if (chol_small(g, low, k) >= 0) { --k; continue; }
+    chol_solve_small(low, f->d, f->coef, k);
+    break;
+  }
+  f->pod_applies += applications;
+  f->podk = k;
+  double kept = 0.0;
+  for (int i = 0; i < k; ++i) kept += f->pod_sigma[i];
+  const double info = k > 0 ? kept / f->nrm : 0.0;
+  f->pod_info = info;
+  run->pod_last_k = k;
+  run->pod_last_info = info;
+  if (k > 0) {
+    run->any_pod = 1;
+    if (info < run->min_pod_info) run->min_pod_info = info;
+  }
+  f->x0_mode = k > 0 ? 1 : 0;
+}
+
+__global__ void k_prev_start(FamDev *f) {
+  if (threadIdx.x == 0) f->x0_mode = f->has_last ? 1 : 0;
+}
+
+__global__ void k_set_mode(FamDev *f, int mode) {
+  if (threadIdx.x == 0) f->x0_mode = mode;
+}
+
+__global__ void k_prev_mark(FamDev *f) {
+  if (threadIdx.x == 0) f->has_last = 1;
+}
+
+// copy active entries (x0 from a stored vector) when the mode says so
+__global__ void __launch_bounds__(kBlock) k_copy_if(Lay L, const uint32_t *__restrict__ mask, const FamDev *f,
+                                                    const double *__restrict__ src, double *__restrict__ dst) {
+  if (f->x0_mode != 1) return;
+  FOR_ACTIVE(L, mask) {
+    const int64_t e = w_ * 32 + (threadIdx.x & 31);
+    dst[e] = src[e];
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_copy(Lay L, const uint32_t *__restrict__ mask,
+                                                 const double *__restrict__ src, double *__restrict__ dst) {
+  FOR_ACTIVE(L, mask) {
+    const int64_t e = w_ * 32 + (threadIdx.x & 31);
+    dst[e] = src[e];
+  }
+}
+
+// record one solve (schur.py:255-263)
+__global__ void k_post_solve(const PcgOut *o, RunDev *run, FamDev *fams, int fam, int32_t *log, long long log_cap,
+                             const StepParams *par) {
+  if (threadIdx.x != 0) return;
+  const PcgOut r = *o;
+  if (r.status == 99) return;  // skipped after an earlier failure
+  if (r.status != MQ_OK && run->err == 0) {
+    run->err = r.status == MQ_NOT_CONVERGED ? MQ_NOT_CONVERGED : r.status;
+    run->err_family = fam;
+    run->err_step = par ? par->step : -1;
+  }
+  const long long i = run->solve_idx;
+  if (log && i < log_cap) log[i] = r.iterations;
+  run->solve_idx = i + 1;
+  run->pcg_applies += r.applies;
+}
+
+// ---- conducting block ---------------------------------------------------
+struct CondArgs {
+  int64_t n_c, n_cells, n_rows_t;
+  const int64_t *kcn_ptr; const int32_t *kcn_col; const int8_t *kcn_sgn;
+  const int32_t *kcnt_row; const int64_t *kcnt_ptr; const int32_t *kcnt_src; const int8_t *kcnt_sgn;
+  const int32_t *f_edge; const int8_t *f_sgn; const double *f_base; const int32_t *f_cell;
+  const int32_t *cell_face; const int32_t *e_face; const int8_t *e_sgn;
+  const double *minv;
+  double of, h, two_h4, k1, k2, k3;
+  int linear;
+};
+
+__device__ __forceinline__ double face_flux(const CondArgs &a, int64_t f, const double *x) {
+  // c_cond row: cond edges in ascending compact order, csr sum from 0
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int32_t e = a.f_edge[4 * f + q];
+    if (e >= 0) s = add(s, mul((double)a.f_sgn[4 * f + q], x[e]));
+  }
+  return s;
+}
+
+// nu per conductor cell from the state (model.py:496-500, 107-125)
+__global__ void k_cell_nu(CondArgs a, const double *__restrict__ state, double *__restrict__ nu) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < a.n_cells; c += (int64_t)gridDim.x * blockDim.x) {
+    double f[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) f[q] = face_flux(a, a.cell_face[6 * c + q], state);
+    const double b2 = add(add(add(mul(f[0], f[0]), mul(f[1], f[1])), add(mul(f[2], f[2]), mul(f[3], f[3]))),
+                          add(mul(f[4], f[4]), mul(f[5], f[5]))) / a.two_h4;
+    nu[c] = a.linear ? a.k3 : add(mul(a.k1, exp(mul(a.k2, b2))), a.k3);
+  }
+}
+
+// y = K_c(state) x with nu precomputed (model.py:502-509)
+__device__ __forceinline__ double kc_row(const CondArgs &a, int64_t e, const double *nu, const double *x) {
+  double y = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int32_t f = a.e_face[4 * e + q];
+    if (f < 0) continue;
+    double fc = 0.0;  // face_by_cond @ nu (<= 2 terms)
+    const int32_t c0 = a.f_cell[2 * f], c1 = a.f_cell[2 * f + 1];
+    if (c0 >= 0) fc = add(fc, mul(0.5, nu[c0]));
+    if (c1 >= 0) fc = add(fc, mul(0.5, nu[c1]));
+    const double w = add(a.f_base[f], fc);
+    const double v = mul(w / a.h, face_flux(a, f, x));
+    y = add(y, mul((double)a.e_sgn[4 * e + q], v));
+  }
+  return y;
+}
+
+__global__ void k_kc_apply(CondArgs a, const double *__restrict__ nu, const double *__restrict__ x,
+                           double *__restrict__ y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.n_c; e += (int64_t)gridDim.x * blockDim.x)
+    y[e] = kc_row(a, e, nu, x);
+}
+
+// w_n = K_cn^T a_c into the (otherwise zero) padded vector (csc_matvec order)
+__global__ void k_kcnt(CondArgs a, const double *__restrict__ ac, double *__restrict__ w) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < a.n_rows_t; r += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t q = a.kcnt_ptr[r]; q < a.kcnt_ptr[r + 1]; ++q) s = add(s, mul(a.kcnt_sgn[q] * a.of, ac[a.kcnt_src[q]]));
+    w[a.kcnt_row[r]] = s;
+  }
+}
+
+// y_c = K_cn x_n (csr order)
+__global__ void k_kcn(CondArgs a, const double *__restrict__ xn, double *__restrict__ yc) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.n_c; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t q = a.kcn_ptr[e]; q < a.kcn_ptr[e + 1]; ++q) s = add(s, mul(a.kcn_sgn[q] * a.of, xn[a.kcn_col[q]]));
+    yc[e] = s;
+  }
+}
+
+// Euler update (schur.py:392-404):
+//   rate = K_cn (y_cpl - y_src) - K_c(a_c) a_c ;  a_next = a_c + dt (minv rate)
+__global__ void k_euler(CondArgs a, const double *__restrict__ nu, const double *__restrict__ ac,
+                        const double *__restrict__ ycpl, const double *__restrict__ ysrc, double *__restrict__ anext,
+                        const StepParams *par, RunDev *run) {
+  if (run->err) return;
+  const double dt = par->dt;
+  bool bad = false;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.n_c; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t q = a.kcn_ptr[e]; q < a.kcn_ptr[e + 1]; ++q) {
+      const int32_t col = a.kcn_col[q];
+      s = add(s, mul(a.kcn_sgn[q] * a.of, sub(ycpl[col], ysrc[col])));
+    }
+    const double rate = sub(s, kc_row(a, e, nu, ac));
+    const double v = add(ac[e], mul(dt, mul(a.minv[e], rate)));
+    anext[e] = v;
+    bad |= !isfinite(v);
+  }
+  if (bad) {
+    if (atomicCAS(&run->err, 0u, (unsigned)MQ_NONFINITE) == 0u) {
+      run->err_step = par->step;
+      run->err_family = -1;
+    }
+  }
+}
+
+__global__ void k_copy_n(int64_t n, const double *__restrict__ src, double *__restrict__ dst, const RunDev *run) {
+  if (run && run->err) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = src[e];
+}
+
+// source rhs = pattern * waveform (schur.py:81-82): only the pattern support
+__global__ void k_src_rhs(int64_t n, const int32_t *__restrict__ idx, const double *__restrict__ val,
+                          const StepParams *par, int use_now, double *__restrict__ rhs) {
+  const double s = use_now ? par->wave_now : par->wave_new;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    rhs[idx[q]] = mul(val[q], s);
+}
+
+__global__ void __launch_bounds__(kBlock) k_sub(Lay L, const uint32_t *__restrict__ mask, const double *__restrict__ a,
+                                                const double *__restrict__ b, double *__restrict__ out) {
+  FOR_ACTIVE(L, mask) {
+    const int64_t e = w_ * 32 + (threadIdx.x & 31);
+    out[e] = sub(a[e], b[e]);
+  }
+}
+
+__global__ void k_load_params(StepParams *par, const double *dt_tab, const double *wave_tab, RunDev *run) {
+  if (threadIdx.x != 0) return;
+  const long long m = run->step;
+  par->dt = dt_tab[m];
+  par->wave_new = wave_tab[m + 1];
+  par->wave_now = wave_tab[m + 1];
+  par->step = m + 1;
+}
+
+__global__ void k_step_done(RunDev *run, const StepParams *par, const double *ac, double *hist, int64_t n_c) {
+  const long long m = par->step - 1;  // k_load_params set step = m + 1
+  if (hist && !run->err)
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_c; e += (int64_t)gridDim.x * blockDim.x)
+      hist[m * n_c + e] = ac[e];
+  if (blockIdx.x == 0 && threadIdx.x == 0) run->step = m + 1;
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+static CondArgs cond_args(mq_ctx *ctx) {
+  CondArgs a;
+  const Topology &t = ctx->topo;
+  a.n_c = (int64_t)t.c_pad.size();
+  a.n_cells = t.n_cells_c;
+  a.n_rows_t = (int64_t)t.kcnt_row.size();
+  a.kcn_ptr = ctx->d_kcn_ptr; a.kcn_col = ctx->d_kcn_col; a.kcn_sgn = ctx->d_kcn_sgn;
+  a.kcnt_row = ctx->d_kcnt_row; a.kcnt_ptr = ctx->d_kcnt_ptr; a.kcnt_src = ctx->d_kcnt_src; a.kcnt_sgn = ctx->d_kcnt_sgn;
+  a.f_edge = ctx->d_f_edge; a.f_sgn = ctx->d_f_sgn; a.f_base = ctx->d_f_base; a.f_cell = ctx->d_f_cell;
+  a.cell_face = ctx->d_cell_face; a.e_face = ctx->d_e_face; a.e_sgn = ctx->d_e_sgn;
+  a.minv = ctx->d_minv;
+  a.of = ctx->kn_off;
+  a.h = ctx->desc.h;
+  a.two_h4 = ctx->two_h4;
+  a.k1 = ctx->desc.brauer_k1; a.k2 = ctx->desc.brauer_k2; a.k3 = ctx->desc.brauer_k3;
+  a.linear = ctx->desc.brauer_k1 == 0.0;
+  return a;
+}
+
+template <class T>
+static int up(mq_ctx *ctx, T **dst, const std::vector<T> &src) {
+  if (src.empty()) { *dst = nullptr; return MQ_OK; }
+  int rc = ctx_alloc(ctx, (void **)dst, src.size() * sizeof(T));
+  if (rc) return rc;
+  MQ_CUDA(cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  return MQ_OK;
+}
+
+int conducting_init(mq_ctx *ctx) {
+  const Topology &t = ctx->topo;
+  int rc = 0;
+  rc = rc ? rc : up(ctx, &ctx->d_kcn_ptr, t.kcn_ptr);
+  rc = rc ? rc : up(ctx, &ctx->d_kcn_col, t.kcn_col);
+  rc = rc ? rc : up(ctx, &ctx->d_kcn_sgn, t.kcn_sgn);
+  rc = rc ? rc : up(ctx, &ctx->d_kcnt_row, t.kcnt_row);
+  rc = rc ? rc : up(ctx, &ctx->d_kcnt_ptr, t.kcnt_ptr);
+  rc = rc ? rc : up(ctx, &ctx->d_kcnt_src, t.kcnt_src);
+  rc = rc ? rc : up(ctx, &ctx->d_kcnt_sgn, t.kcnt_sgn);
+  std::vector<double> minv(t.mc_diag.size());
+  for (size_t q = 0; q < minv.size(); ++q) minv[q] = 1.0 / t.mc_diag[q];  // schur.py:212
+  rc = rc ? rc : up(ctx, &ctx->d_minv, minv);
+  rc = rc ? rc : up(ctx, &ctx->d_f_edge, t.f_edge);
+  rc = rc ? rc : up(ctx, &ctx->d_f_sgn, t.f_sgn);
+  rc = rc ? rc : up(ctx, &ctx->d_f_base, t.f_base);
+  rc = rc ? rc : up(ctx, &ctx->d_f_cell, t.f_cell);
+  rc = rc ? rc : up(ctx, &ctx->d_cell_face, t.cell_face);
+  rc = rc ? rc : up(ctx, &ctx->d_e_face, t.e_face);
+  rc = rc ? rc : up(ctx, &ctx->d_e_sgn, t.e_sgn);
+  const size_t nc = std::max<size_t>(1, t.c_pad.size());
+  rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_cell_nu, sizeof(double) * std::max<int64_t>(1, t.n_cells_c));
+  rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_ac, sizeof(double) * nc);
+  rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_ac_next, sizeof(double) * nc);
+  rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_ac_x, sizeof(double) * nc);
+  rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_yc, sizeof(double) * nc);
+  ctx->two_h4 = 2.0 * std::pow(ctx->desc.h, 4.0);
+  return rc;
+}
+
+static int grid_for(mq_ctx *ctx, int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b < 1) b = 1;
+  if (b > (int64_t)ctx->sms * 4) b = ctx->sms * 4;
+  return (int)b;
+}
+
+static int stream_grid(mq_ctx *ctx) {
+  int64_t b = (ctx->topo.L.words + kWarps - 1) / kWarps;
+  if (b > (int64_t)ctx->sms * 4) b = ctx->sms * 4;
+  return (int)std::max<int64_t>(1, b);
+}
+
+#define LAUNCH_CHECK()                 \
+  do {                                 \
+    MQ_CUDA(cudaGetLastError());       \
+    ctx->launches += 1;                \
+  } while (0)
+
+// ---- start vector -----------------------------------------------------
+static int start_vector(mq_ctx *ctx, int fam, const double *rhs, double *x0) {
+  SolverHost *s = ctx->solver;
+  FamDev *f = s->d_fam + fam;
+  const Lay &L = ctx->topo.L;
+  cudaStream_t st = ctx->stream;
+  const int G = s->red_grid;
+  switch (s->cfg.strategy) {
+    case MQ_STRAT_ZERO:
+      k_set_mode<<<1, 32, 0, st>>>(f, 0);
+      LAUNCH_CHECK();
+      break;
+    case MQ_STRAT_PREVIOUS:
+      k_prev_start<<<1, 32, 0, st>>>(f);
+      LAUNCH_CHECK();
+      k_copy_if<<<stream_grid(ctx), kBlock, 0, st>>>(L, ctx->d_mask, f, s->last[fam], x0);
+      LAUNCH_CHECK();
+      break;
+    case MQ_STRAT_CSPE:
+      k_mdot<<<G, kBlock, 0, st>>>(L, ctx->d_mask, s->d_U[fam], f->order, &f->k, rhs, 0, f->d, s->d_red, s->d_cnt);
+      LAUNCH_CHECK();
+      k_cspe_project_small<<<1, 32, 0, st>>>(f);
+      LAUNCH_CHECK();
+      k_comb<<<stream_grid(ctx), kBlock, 0, st>>>(L, ctx->d_mask, s->d_U[fam], f->order, &f->k, f->coef, x0);
+      LAUNCH_CHECK();
+      break;
+    case MQ_STRAT_POD: {
+      k_pod_eig<<<1, 256, 0, st>>>(f, s->cfg.eps_pod);
+      LAUNCH_CHECK();
+      k_pod_basis<<<stream_grid(ctx), kBlock, 0, st>>>(L, ctx->d_mask, f, s->d_X[fam], s->d_B);
+      LAUNCH_CHECK();
+      dim3 g2(stream_grid(ctx), s->cfg.n_pod);
+      k_spmv_multi<<<g2, kBlock, 0, st>>>(L, ctx->d_mask, ctx->kn_diag, ctx->kn_off, f, s->d_B, s->d_KB);
+      LAUNCH_CHECK();
+      dim3 g3(G, s->cfg.n_pod + 1);
+      k_pod_galerkin<<<g3, kBlock, 0, st>>>(L, ctx->d_mask, f, s->d_B, s->d_KB, rhs, s->d_red, s->d_cnt + 1);
+      LAUNCH_CHECK();
+      k_pod_solve<<<1, 32, 0, st>>>(f, s->d_run);
+      LAUNCH_CHECK();
+      k_comb<<<stream_grid(ctx), kBlock, 0, st>>>(L, ctx->d_mask, s->d_B, s->d_iota, &f->podk, f->coef, x0);
+      LAUNCH_CHECK();
+      break;
+    }
+  }
+  return MQ_OK;
+}
+
+// ---- observe ------------------------------------------------------------
+static int observe(mq_ctx *ctx, int fam, const double *y) {
+  SolverHost *s = ctx->solver;
+  FamDev *f = s->d_fam + fam;
+  const Lay &L = ctx->topo.L;
+  cudaStream_t st = ctx->stream;
+  const int G = s->red_grid;
+  switch (s->cfg.strategy) {
+    case MQ_STRAT_ZERO:
+      break;
+    case MQ_STRAT_PREVIOUS:
+      k_copy<<<stream_grid(ctx), kBlock, 0, st>>>(L, ctx->d_mask, y, s->last[fam]);
+      LAUNCH_CHECK();
+      k_prev_mark<<<1, 32, 0, st>>>(f);
+      LAUNCH_CHECK();
+      break;
+    case MQ_STRAT_CSPE:
+      // ||v|| and U^T v in one pass
+      k_mdot<<<G, kBlock, 0, st>>>(L, ctx->d_mask, s->d_U[fam], f->order, &f->k, y, 1, f->d, s->d_red, s->d_cnt);
+      LAUNCH_CHECK();
+      k_cspe_gate<<<1, 32, 0, st>>>(f);
+      LAUNCH_CHECK();
+      // CGS pass 1: w1 = v - U c1, c2 = U^T w1
+      k_axpy_dots<<<G, kBlock, 0, st>>>(L, ctx->d_mask, s->d_U[fam], f->order, &f->k, f->coef, y, s->w1, 1, f->d,
+                                        s->d_red, s->d_cnt, &f->accept);
+      LAUNCH_CHECK();
+      k_cspe_gate_c2<<<1, 32, 0, st>>>(f);
+      LAUNCH_CHECK();
+      // CGS pass 2: w2 = w1 - U c2, ||w2||^2
+      k_axpy_dots<<<G, kBlock, 0, st>>>(L, ctx->d_mask, s->d_U[fam], f->order, &f->k, f->coef, s->w1, s->w2, 0,
+                                        f->d, s->d_red, s->d_cnt, &f->accept);
+      LAUNCH_CHECK();
+      k_cspe_decide<<<1, 32, 0, st>>>(f, f->d, s->cfg.max_cols, s->cfg.drop_tol);
+      LAUNCH_CHECK();
+      k_cspe_product<<<G, kBlock, 0, st>>>(L, ctx->d_mask, ctx->kn_diag, ctx->kn_off, f, s->d_U[fam], s->d_KU[fam],
+                                           s->w2, s->d_red, s->d_cnt);
+      LAUNCH_CHECK();
+      k_cspe_commit<<<1, 32, 0, st>>>(f);
+      LAUNCH_CHECK();
+      break;
+    case MQ_STRAT_POD:
+      k_pod_push<<<G, kBlock, 0, st>>>(L, ctx->d_mask, f, s->d_X[fam], s->cfg.n_pod, y, s->d_red, s->d_cnt);
+      LAUNCH_CHECK();
+      k_pod_push_commit<<<1, 32, 0, st>>>(f, s->cfg.n_pod);
+      LAUNCH_CHECK();
+      break;
+  }
+  return MQ_OK;
+}
+
+// ---- one solve_kn (schur.py:239-264), device only ------------------------
+static int solve_enqueue(mq_ctx *ctx, int fam, const double *rhs, double *y) {
+  SolverHost *s = ctx->solver;
+  FamDev *f = s->d_fam + fam;
+  int rc = start_vector(ctx, fam, rhs, y);
+  if (rc) return rc;
+  StencilPcgArgs a;
+  a.L = ctx->topo.L;
+  a.mask = ctx->d_mask;
+  a.dg = ctx->kn_diag;
+  a.of = ctx->kn_off;
+  a.inv = ctx->jac_inv;
+  a.use_jac = 1;
+  a.x0_mode = 0;
+  a.b = rhs;
+  a.x = y;
+  a.r = ctx->d_r;
+  a.pa = ctx->d_p0;
+  a.pb = ctx->d_p1;
+  a.ap = ctx->d_ap;
+  a.rel_tol = s->cfg.rel_tol;
+  a.abs_tol = s->cfg.abs_tol;
+  a.max_iter = s->cfg.max_iter;
+  a.partials = ctx->d_partials;
+  a.bar = ctx->d_bar;
+  a.out = ctx->d_out;
+  a.x0_mode_dev = &f->x0_mode;
+  a.err_word = &s->d_run->err;
+  const bool timed = ctx->pcg_timing && ctx->ev_n < kEvPool;
+  if (timed) MQ_CUDA(cudaEventRecord(ctx->ev_pool[2 * ctx->ev_n], ctx->stream));
+  rc = launch_pcg_stencil(a, ctx->pcg_grid, ctx->stream);
+  if (rc) return rc;
+  if (timed) {
+    MQ_CUDA(cudaEventRecord(ctx->ev_pool[2 * ctx->ev_n + 1], ctx->stream));
+    ctx->ev_n += 1;
+  }
+  ctx->launches += 1;
+  k_post_solve<<<1, 32, 0, ctx->stream>>>(ctx->d_out, s->d_run, s->d_fam, fam, s->d_log, s->log_cap, s->d_par);
+  LAUNCH_CHECK();
+  return observe(ctx, fam, y);
+}
+
+static int euler_enqueue(mq_ctx *ctx) {
+  SolverHost *s = ctx->solver;
+  const Topology &t = ctx->topo;
+  CondArgs a = cond_args(ctx);
+  cudaStream_t st = ctx->stream;
+  const int64_t n_c = (int64_t)t.c_pad.size();
+  // SOURCE at t + dt
+  k_src_rhs<<<grid_for(ctx, s->n_pat), 256, 0, st>>>(s->n_pat, s->d_pat_idx, s->d_pat_val, s->d_par, 0, s->rhs_src);
+  LAUNCH_CHECK();
+  int rc = solve_enqueue(ctx, MQ_FAM_SOURCE, s->rhs_src, s->y_src);
+  if (rc) return rc;
+  // COUPLING_FROM_PREVIOUS_STATE with w = K_cn^T a_c
+  k_kcnt<<<grid_for(ctx, a.n_rows_t), 256, 0, st>>>(a, ctx->d_ac, s->rhs_cpl);
+  LAUNCH_CHECK();
+  rc = solve_enqueue(ctx, MQ_FAM_COUPLING_PREVIOUS, s->rhs_cpl, s->y_cpl);
+  if (rc) return rc;
+  // Brauer + Euler update
+  k_cell_nu<<<grid_for(ctx, a.n_cells), 256, 0, st>>>(a, ctx->d_ac, ctx->d_cell_nu);
+  LAUNCH_CHECK();
+  k_euler<<<grid_for(ctx, n_c), 256, 0, st>>>(a, ctx->d_cell_nu, ctx->d_ac, s->y_cpl, s->y_src, ctx->d_ac_next,
+                                              s->d_par, s->d_run);
+  LAUNCH_CHECK();
+  k_copy_n<<<grid_for(ctx, n_c), 256, 0, st>>>(n_c, ctx->d_ac_next, ctx->d_ac, s->d_run);
+  LAUNCH_CHECK();
+  return MQ_OK;
+}
+
+static int recover_enqueue(mq_ctx *ctx) {
+  SolverHost *s = ctx->solver;
+  CondArgs a = cond_args(ctx);
+  cudaStream_t st = ctx->stream;
+  k_src_rhs<<<grid_for(ctx, s->n_pat), 256, 0, st>>>(s->n_pat, s->d_pat_idx, s->d_pat_val, s->d_par, 1, s->rhs_src);
+  LAUNCH_CHECK();
+  int rc = solve_enqueue(ctx, MQ_FAM_SOURCE, s->rhs_src, s->y_src);
+  if (rc) return rc;
+  k_kcnt<<<grid_for(ctx, a.n_rows_t), 256, 0, st>>>(a, ctx->d_ac, s->rhs_cpl);
+  LAUNCH_CHECK();
+  return solve_enqueue(ctx, MQ_FAM_COUPLING_CURRENT, s->rhs_cpl, s->y_cpl);
+}
+
+static int check_run(mq_ctx *ctx, int64_t *failed_step) {
+  SolverHost *s = ctx->solver;
+  RunDev r;
+  MQ_CUDA(cudaMemcpyAsync(&r, s->d_run, sizeof(RunDev), cudaMemcpyDeviceToHost, ctx->stream));
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (failed_step) *failed_step = r.err ? r.err_step : -1;
+  if (r.err == 0) return MQ_OK;
+  static const char *fam_name[3] = {"source", "coupling_current", "coupling_previous"};
+  std::string where = r.err_step >= 0 ? " at step " + std::to_string(r.err_step) : std::string();
+  if (r.err == MQ_NOT_CONVERGED)
+    set_error(std::string("inner solve (") + (r.err_family >= 0 ? fam_name[r.err_family] : "?") +
+              ") stalled" + where);
+  else if (r.err == MQ_INDEFINITE)
+    set_error(std::string("nonpositive curvature in inner solve (") +
+              (r.err_family >= 0 ? fam_name[r.err_family] : "?") + ")" + where);
+  else if (r.err == MQ_NONFINITE)
+    set_error("non-finite conducting state" + where);
+  else
+    set_error("device failure (grid barrier watchdog)" + where);
+  return (int)r.err;
+}
+
+__global__ void k_reset_run(RunDev *run) {
+  if (threadIdx.x != 0) return;
+  run->err = 0;
+  run->err_family = 0;
+  run->err_step = 0;
+  run->step = 0;
+  run->solve_idx = 0;
+}
+
+// per-call fields only; strategy-wide counters persist (startvec.py:404-454)
+static int reset_run(mq_ctx *ctx) {
+  k_reset_run<<<1, 32, 0, ctx->stream>>>(ctx->solver->d_run);
+  MQ_CUDA(cudaGetLastError());
+  return MQ_OK;
+}
+
+static int init_run(mq_ctx *ctx) {
+  SolverHost *s = ctx->solver;
+  RunDev r{};
+  r.min_pod_info = 1.0;
+  r.pod_last_info = 1.0;
+  MQ_CUDA(cudaMemcpyAsync(s->d_run, &r, sizeof(RunDev), cudaMemcpyHostToDevice, ctx->stream));
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  return MQ_OK;
+}
+
+}  // namespace mq
+
+using namespace mq;
+
+extern "C" {
+
+int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern) {
+  if (!ctx || !cfg) { set_error("NULL argument"); return MQ_INVALID; }
+  if (cfg->strategy < 0 || cfg->strategy > 3) { set_error("unknown start-vector strategy"); return MQ_INVALID; }
+  if (cfg->strategy == MQ_STRAT_CSPE && (cfg->max_cols < 1 || cfg->max_cols > MAXS)) {
+    set_error("max_cols must lie in [1, 32]");
+    return MQ_INVALID;
+  }
+  if (cfg->strategy == MQ_STRAT_POD && (cfg->n_pod < 1 || cfg->n_pod > MAXS)) {
+    set_error("n_pod must lie in [1, 32]");
+    return MQ_INVALID;
+  }
+  if (cfg->strategy == MQ_STRAT_POD && !(cfg->eps_pod > 0.0 && cfg->eps_pod < 1.0)) {
+    set_error("eps_pod must lie in (0, 1)");
+    return MQ_INVALID;
+  }
+  if (!(cfg->rel_tol > 0.0) || cfg->abs_tol < 0.0 || cfg->max_iter < 1) {
+    set_error("invalid PCG configuration");
+    return MQ_INVALID;
+  }
+  solver_free(ctx);
+  SolverHost *s = new SolverHost();
+  ctx->solver = s;
+  s->cfg = *cfg;
+  const Lay &L = ctx->topo.L;
+  const size_t vb = sizeof(double) * L.total;
+  int rc = 0;
+  rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_fam, sizeof(FamDev) * 3);
+  rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_run, sizeof(RunDev));
+  rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_par, sizeof(StepParams));
+  auto vec = [&](double **p) { return rc ? rc : (rc = s_alloc(ctx, s, (void **)p, vb)); };
+  auto table = [&](double ***tab, std::vector<double *> &h, int n) {
+    if (rc) return rc;
+    h.assign(MAXS, nullptr);
+    for (int q = 0; q < n && !rc; ++q) vec(&h[q]);
+    if (rc) return rc;
+    rc = s_alloc(ctx, s, (void **)tab, sizeof(double *) * MAXS);
+    if (rc) return rc;
+    cudaError_t e = cudaMemcpyAsync(*tab, h.data(), sizeof(double *) * MAXS, cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "slot table");
+    return rc;
+  };
+  for (int fam = 0; fam < 3; ++fam) {
+    if (cfg->strategy == MQ_STRAT_CSPE) {
+      table(&s->d_U[fam], s->h_U[fam], cfg->max_cols);
+      table(&s->d_KU[fam], s->h_KU[fam], cfg->max_cols);
+    } else if (cfg->strategy == MQ_STRAT_POD) {
+      table(&s->d_X[fam], s->h_X[fam], cfg->n_pod);
+    } else if (cfg->strategy == MQ_STRAT_PREVIOUS) {
+      vec(&s->last[fam]);
+    }
+  }
+  if (cfg->strategy == MQ_STRAT_POD) {
+    table(&s->d_B, s->h_B, cfg->n_pod);
+    table(&s->d_KB, s->h_KB, cfg->n_pod);
+  }
+  vec(&s->w1);
+  vec(&s->w2);
+  vec(&s->rhs_src);
+  vec(&s->rhs_cpl);
+  vec(&s->y_src);
+  vec(&s->y_cpl);
+  s->red_grid = std::max(1, std::min<int>(ctx->sms * 2, (int)((L.words + kWarps - 1) / kWarps)));
+  rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_red, sizeof(double) * RQ * (size_t)s->red_grid * (MAXS + 2));
+  rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_cnt, sizeof(unsigned int) * (MAXS + 4));
+  // sparse source pattern on its support
+  if (!rc && pattern) {
+    std::vector<int32_t> idx;
+    std::vector<double> val;
+    const auto &pad = ctx->topo.nc_pad;
+    for (size_t q = 0; q < pad.size(); ++q)
+      if (pattern[q] != 0.0) { idx.push_back(pad[q]); val.push_back(pattern[q]); }
+    s->n_pat = (int64_t)idx.size();
+    if (s->n_pat) {
+      rc = s_alloc(ctx, s, (void **)&s->d_pat_idx, sizeof(int32_t) * idx.size());
+      rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_pat_val, sizeof(double) * val.size());
+      if (!rc) {
+        cudaMemcpyAsync(s->d_pat_idx, idx.data(), sizeof(int32_t) * idx.size(), cudaMemcpyHostToDevice, ctx->stream);
+        cudaMemcpyAsync(s->d_pat_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice, ctx->stream);
+      }
+    }
+  }
+  if (!rc) {
+    int iota[MAXS];
+    for (int q = 0; q < MAXS; ++q) iota[q] = q;
+    rc = s_alloc(ctx, s, (void **)&s->d_iota, sizeof(iota));
+    if (!rc) cudaMemcpyAsync(s->d_iota, iota, sizeof(iota), cudaMemcpyHostToDevice, ctx->stream);
+  }
+  if (!rc) rc = init_run(ctx);
+  if (!rc) {
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "solver init");
+  }
+  if (rc) solver_free(ctx);
+  return rc;
+}
+
+int mq_solver_reset(mq_ctx *ctx) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  MQ_CUDA(cudaMemsetAsync(s->d_fam, 0, sizeof(FamDev) * 3, ctx->stream));
+  return init_run(ctx);
+}
+
+int mq_solve_kn(mq_ctx *ctx, int32_t family, const double *rhs, double *y, mq_solve_report *rep) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  if (family < 0 || family > 2) { set_error("unknown family"); return MQ_INVALID; }
+  int rc = reset_run(ctx);
+  if (rc) return rc;
+  MQ_CUDA(cudaMemsetAsync(s->d_par, 0, sizeof(StepParams), ctx->stream));
+  rc = solve_enqueue(ctx, family, rhs, y);
+  if (rc) return rc;
+  MQ_CUDA(cudaMemcpyAsync(ctx->h_out, ctx->d_out, sizeof(PcgOut), cudaMemcpyDeviceToHost, ctx->stream));
+  rc = check_run(ctx, nullptr);
+  const PcgOut &o = *ctx->h_out;
+  if (rep) {
+    rep->iterations = o.iterations;
+    rep->converged = o.converged;
+    rep->final_rel_residual = o.rel;
+    rep->applies = o.applies;
+  }
+  return rc;
+}
+
+int mq_strategy_start(mq_ctx *ctx, int32_t family, const double *rhs, double *x0) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  int rc = start_vector(ctx, family, rhs, x0);
+  if (rc) return rc;
+  // materialise zero start vectors
+  FamDev f;
+  MQ_CUDA(cudaMemcpyAsync(&f, s->d_fam + family, sizeof(FamDev), cudaMemcpyDeviceToHost, ctx->stream));
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (f.x0_mode == 0) MQ_CUDA(cudaMemsetAsync(x0, 0, sizeof(double) * ctx->topo.L.total, ctx->stream));
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  return MQ_OK;
+}
+
+int mq_strategy_observe(mq_ctx *ctx, int32_t family, const double *y) {
+  if (!ctx->solver) { set_error("solver not initialised"); return MQ_INVALID; }
+  int rc = observe(ctx, family, y);
+  if (rc) return rc;
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  return MQ_OK;
+}
+
+int mq_diagnostics(mq_ctx *ctx, mq_diag *out) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  FamDev f[3];
+  RunDev r;
+  MQ_CUDA(cudaMemcpyAsync(f, s->d_fam, sizeof(FamDev) * 3, cudaMemcpyDeviceToHost, ctx->stream));
+  MQ_CUDA(cudaMemcpyAsync(&r, s->d_run, sizeof(RunDev), cudaMemcpyDeviceToHost, ctx->stream));
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memset(out, 0, sizeof(*out));
+  out->pcg_applies = r.pcg_applies;
+  for (int q = 0; q < 3; ++q) {
+    out->basis_cols[q] = s->cfg.strategy == MQ_STRAT_CSPE ? f[q].k : 0;
+    out->columns_accepted[q] = f[q].accepted;
+    out->columns_dropped[q] = f[q].dropped;
+    out->evictions[q] = f[q].evictions;
+    out->maintenance_applies += s->cfg.strategy == MQ_STRAT_CSPE ? f[q].products : f[q].pod_applies;
+  }
+  out->pod_k = r.pod_last_k;
+  out->pod_info = r.pod_last_info;
+  out->min_pod_info = r.any_pod ? r.min_pod_info : 1.0;
+  return MQ_OK;
+}
+
+int mq_cspe_export(mq_ctx *ctx, int32_t family, int32_t *k, double *basis, double *products, double *galerkin) {
+  SolverHost *s = ctx->solver;
+  if (!s || s->cfg.strategy != MQ_STRAT_CSPE) { set_error("CSPE solver not initialised"); return MQ_INVALID; }
+  FamDev f;
+  MQ_CUDA(cudaMemcpyAsync(&f, s->d_fam + family, sizeof(FamDev), cudaMemcpyDeviceToHost, ctx->stream));
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  *k = f.k;
+  const int64_t n = (int64_t)ctx->topo.nc_pad.size();
+  for (int j = 0; j < f.k; ++j) {
+    if (basis) {
+      int rc = mq_vec_download(ctx, s->h_U[family][f.order[j]], basis + j * n);
+      if (rc) return rc;
+    }
+    if (products) {
+      int rc = mq_vec_download(ctx, s->h_KU[family][f.order[j]], products + j * n);
+      if (rc) return rc;
+    }
+  }
+  if (galerkin)
+    for (int r = 0; r < f.k; ++r)
+      for (int c = 0; c < f.k; ++c) galerkin[r * f.k + c] = f.G[r * MAXS + c];
+  return MQ_OK;
+}
+
+int mq_kc_apply_host(mq_ctx *ctx, const double *state, const double *x, double *y) {
+  const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
+  CondArgs a = cond_args(ctx);
+  cudaStream_t st = ctx->stream;
+  MQ_CUDA(cudaMemcpyAsync(ctx->d_ac_next, state, sizeof(double) * n_c, cudaMemcpyHostToDevice, st));
+  MQ_CUDA(cudaMemcpyAsync(ctx->d_ac_x, x, sizeof(double) * n_c, cudaMemcpyHostToDevice, st));
+  k_cell_nu<<<grid_for(ctx, a.n_cells), 256, 0, st>>>(a, ctx->d_ac_next, ctx->d_cell_nu);
+  LAUNCH_CHECK();
+  k_kc_apply<<<grid_for(ctx, n_c), 256, 0, st>>>(a, ctx->d_cell_nu, ctx->d_ac_x, ctx->d_yc);
+  LAUNCH_CHECK();
+  MQ_CUDA(cudaMemcpyAsync(y, ctx->d_yc, sizeof(double) * n_c, cudaMemcpyDeviceToHost, st));
+  MQ_CUDA(cudaStreamSynchronize(st));
+  return MQ_OK;
+}
+
+int mq_kcn_t_apply_host(mq_ctx *ctx, const double *a_c, double *y_n) {
+  const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
+  CondArgs a = cond_args(ctx);
+  cudaStream_t st = ctx->stream;
+  MQ_CUDA(cudaMemcpyAsync(ctx->d_ac_x, a_c, sizeof(double) * n_c, cudaMemcpyHostToDevice, st));
+  MQ_CUDA(cudaMemsetAsync(ctx->d_tmp0, 0, sizeof(double) * ctx->topo.L.total, st));
+  k_kcnt<<<grid_for(ctx, a.n_rows_t), 256, 0, st>>>(a, ctx->d_ac_x, ctx->d_tmp0);
+  LAUNCH_CHECK();
+  return mq_vec_download(ctx, ctx->d_tmp0, y_n);
+}
+
+int mq_kcn_apply_host(mq_ctx *ctx, const double *x_n, double *y_c) {
+  const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
+  CondArgs a = cond_args(ctx);
+  cudaStream_t st = ctx->stream;
+  int rc = mq_vec_upload(ctx, x_n, ctx->d_tmp0);
+  if (rc) return rc;
+  k_kcn<<<grid_for(ctx, n_c), 256, 0, st>>>(a, ctx->d_tmp0, ctx->d_yc);
+  LAUNCH_CHECK();
+  MQ_CUDA(cudaMemcpyAsync(y_c, ctx->d_yc, sizeof(double) * n_c, cudaMemcpyDeviceToHost, st));
+  MQ_CUDA(cudaStreamSynchronize(st));
+  return MQ_OK;
+}
+
+int mq_mc_diag(mq_ctx *ctx, double *mc_diag) {
+  std::memcpy(mc_diag, ctx->topo.mc_diag.data(), sizeof(double) * ctx->topo.mc_diag.size());
+  return MQ_OK;
+}
+
+int mq_state_set(mq_ctx *ctx, const double *a_c, double t) {
+  const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
+  if (a_c) MQ_CUDA(cudaMemcpyAsync(ctx->d_ac, a_c, sizeof(double) * n_c, cudaMemcpyHostToDevice, ctx->stream));
+  else MQ_CUDA(cudaMemsetAsync(ctx->d_ac, 0, sizeof(double) * n_c, ctx->stream));
+  ctx->t_now = t;
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  return MQ_OK;
+}
+
+int mq_state_get(mq_ctx *ctx, double *a_c, double *t) {
+  const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
+  if (a_c) MQ_CUDA(cudaMemcpyAsync(a_c, ctx->d_ac, sizeof(double) * n_c, cudaMemcpyDeviceToHost, ctx->stream));
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (t) *t = ctx->t_now;
+  return MQ_OK;
+}
+
+static int read_report(mq_ctx *ctx, int64_t first, mq_solve_report *a, mq_solve_report *b) {
+  SolverHost *s = ctx->solver;
+  int32_t it[2] = {0, 0};
+  MQ_CUDA(cudaMemcpyAsync(it, s->d_log + first, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (a) { a->iterations = it[0]; a->converged = 1; a->final_rel_residual = 0; a->applies = it[0] + 1; }
+  if (b) { b->iterations = it[1]; b->converged = 1; b->final_rel_residual = 0; b->applies = it[1] + 1; }
+  return MQ_OK;
+}
+
+static int ensure_log(mq_ctx *ctx, int64_t n) {
+  SolverHost *s = ctx->solver;
+  if (s->log_cap >= n) return MQ_OK;
+  if (s->d_log) cudaFree(s->d_log);
+  s->d_log = nullptr;
+  MQ_CUDA(cudaMalloc(&s->d_log, sizeof(int32_t) * n));
+  s->log_cap = n;
+  if (s->graph_exec) { cudaGraphExecDestroy(s->graph_exec); s->graph_exec = nullptr; }
+  return MQ_OK;
+}
+
+int mq_euler_step(mq_ctx *ctx, double dt, double wave_new, int64_t step_index, mq_solve_report *rep_src,
+                  mq_solve_report *rep_cpl) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  if (dt < 0) { set_error("dt must be nonnegative"); return MQ_INVALID; }
+  int rc = ensure_log(ctx, 4);
+  if (rc) return rc;
+  rc = reset_run(ctx);
+  if (rc) return rc;
+  StepParams p{dt, wave_new, wave_new, (long long)step_index};
+  MQ_CUDA(cudaMemcpyAsync(s->d_par, &p, sizeof(p), cudaMemcpyHostToDevice, ctx->stream));
+  rc = euler_enqueue(ctx);
+  if (rc) return rc;
+  int64_t failed = -1;
+  rc = check_run(ctx, &failed);
+  read_report(ctx, 0, rep_src, rep_cpl);
+  if (!rc) ctx->t_now += dt;
+  return rc;
+}
+
+int mq_recover_an(mq_ctx *ctx, double wave_now, double *a_n_host, mq_solve_report *rep_src,
+                  mq_solve_report *rep_cpl) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  int rc = ensure_log(ctx, 4);
+  if (rc) return rc;
+  rc = reset_run(ctx);
+  if (rc) return rc;
+  StepParams p{0.0, wave_now, wave_now, -1};
+  MQ_CUDA(cudaMemcpyAsync(s->d_par, &p, sizeof(p), cudaMemcpyHostToDevice, ctx->stream));
+  rc = recover_enqueue(ctx);
+  if (rc) return rc;
+  rc = check_run(ctx, nullptr);
+  read_report(ctx, 0, rep_src, rep_cpl);
+  if (rc) return rc;
+  if (a_n_host) {
+    k_sub<<<stream_grid(ctx), kBlock, 0, ctx->stream>>>(ctx->topo.L, ctx->d_mask, s->y_src, s->y_cpl, ctx->d_tmp1);
+    LAUNCH_CHECK();
+    return mq_vec_download(ctx, ctx->d_tmp1, a_n_host);
+  }
+  return MQ_OK;
+}
+
+int mq_last_an(mq_ctx *ctx, double *a_n_host) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  k_sub<<<stream_grid(ctx), kBlock, 0, ctx->stream>>>(ctx->topo.L, ctx->d_mask, s->y_src, s->y_cpl, ctx->d_tmp1);
+  LAUNCH_CHECK();
+  return mq_vec_download(ctx, ctx->d_tmp1, a_n_host);
+}
+
+static int enqueue_step(mq_ctx *ctx, double *hist) {
+  SolverHost *s = ctx->solver;
+  const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
+  ctx->ev_n = 0;
+  k_load_params<<<1, 32, 0, ctx->stream>>>(s->d_par, s->d_dt_tab, s->d_wave_tab, s->d_run);
+  MQ_CUDA(cudaGetLastError());
+  ctx->launches += 1;
+  int rc = euler_enqueue(ctx);
+  if (rc) return rc;
+  if (s->recover_every_step) {
+    rc = recover_enqueue(ctx);
+    if (rc) return rc;
+  }
+  k_step_done<<<grid_for(ctx, n_c), 256, 0, ctx->stream>>>(s->d_run, s->d_par, ctx->d_ac, hist, n_c);
+  MQ_CUDA(cudaGetLastError());
+  ctx->launches += 1;
+  return MQ_OK;
+}
+
+int mq_run_prepare(mq_ctx *ctx, int64_t n_steps, const double *dt, const double *wave,
+                   int32_t recover_every_step) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  if (n_steps < 0) { set_error("n_steps must be nonnegative"); return MQ_INVALID; }
+  const int per = recover_every_step ? 4 : 2;
+  int rc = ensure_log(ctx, std::max<int64_t>(4, per * n_steps));
+  if (rc) return rc;
+  if (s->tab_cap < n_steps + 1) {
+    if (s->d_dt_tab) cudaFree(s->d_dt_tab);
+    if (s->d_wave_tab) cudaFree(s->d_wave_tab);
+    MQ_CUDA(cudaMalloc(&s->d_dt_tab, sizeof(double) * (n_steps + 1)));
+    MQ_CUDA(cudaMalloc(&s->d_wave_tab, sizeof(double) * (n_steps + 1)));
+    s->tab_cap = n_steps + 1;
+    if (s->graph_exec) { cudaGraphExecDestroy(s->graph_exec); s->graph_exec = nullptr; }
+  }
+  if ((recover_every_step != 0) != s->recover_every_step && s->graph_exec) {
+    cudaGraphExecDestroy(s->graph_exec);
+    s->graph_exec = nullptr;
+  }
+  s->recover_every_step = recover_every_step != 0;
+  s->per_step = per;
+  s->n_planned = n_steps;
+  s->n_enqueued = 0;
+  if (n_steps > 0)
+    MQ_CUDA(cudaMemcpyAsync(s->d_dt_tab, dt, sizeof(double) * n_steps, cudaMemcpyHostToDevice, ctx->stream));
+  MQ_CUDA(cudaMemcpyAsync(s->d_wave_tab, wave, sizeof(double) * (n_steps + 1), cudaMemcpyHostToDevice, ctx->stream));
+  rc = reset_run(ctx);
+  if (rc) return rc;
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  return MQ_OK;
+}
+
+int mq_run_steps(mq_ctx *ctx, int64_t n, int32_t use_graph, double *a_c_hist_dev) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  if (s->n_enqueued + n > s->n_planned) { set_error("more steps than prepared"); return MQ_INVALID; }
+  bool graphed = false;
+  if (use_graph && !a_c_hist_dev && s->graph_ok) {
+    if (!s->graph_exec) {
+      cudaGraph_t g = nullptr;
+      const int64_t l0 = ctx->launches;
+      cudaError_t e = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        int r2 = enqueue_step(ctx, nullptr);
+        e = cudaStreamEndCapture(ctx->stream, &g);
+        if (r2 == MQ_OK && e == cudaSuccess) e = cudaGraphInstantiate(&s->graph_exec, g, 0);
+        if (g) cudaGraphDestroy(g);
+      }
+      s->launches_per_step = ctx->launches - l0;
+      ctx->launches = l0;
+      if (e != cudaSuccess || !s->graph_exec) {
+        cudaGetLastError();
+        s->graph_ok = false;
+        s->graph_exec = nullptr;
+      }
+    }
+    if (s->graph_exec) {
+      graphed = true;
+      for (int64_t m = 0; m < n; ++m) {
+        MQ_CUDA(cudaGraphLaunch(s->graph_exec, ctx->stream));
+        ctx->launches += s->launches_per_step;
+      }
+    }
+  }
+  if (!graphed) {
+    for (int64_t m = 0; m < n; ++m) {
+      int rc = enqueue_step(ctx, a_c_hist_dev);
+      if (rc) return rc;
+    }
+  }
+  s->n_enqueued += n;
+  return MQ_OK;
+}
+
+int mq_run_finish(mq_ctx *ctx, int32_t *iters_out, int64_t *failed_step) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  int rc = check_run(ctx, failed_step);
+  const int64_t n = s->n_enqueued;
+  if (iters_out && n > 0)
+    MQ_CUDA(cudaMemcpy(iters_out, s->d_log, sizeof(int32_t) * s->per_step * n, cudaMemcpyDeviceToHost));
+  return rc;
+}
+
+int mq_run_explicit(mq_ctx *ctx, int64_t n_steps, const double *dt, const double *wave, int32_t recover_every_step,
+                    int32_t use_graph, int32_t *iters_out, double *a_c_hist, int64_t *failed_step) {
+  int rc = mq_run_prepare(ctx, n_steps, dt, wave, recover_every_step);
+  if (rc) return rc;
+  const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
+  double *hist = nullptr;
+  if (a_c_hist && n_steps > 0) MQ_CUDA(cudaMalloc(&hist, sizeof(double) * n_c * n_steps));
+  rc = mq_run_steps(ctx, n_steps, use_graph, hist);
+  int rc2 = mq_run_finish(ctx, iters_out, failed_step);
+  if (rc == MQ_OK) rc = rc2;
+  if (hist) {
+    cudaMemcpy(a_c_hist, hist, sizeof(double) * n_c * n_steps, cudaMemcpyDeviceToHost);
+    cudaFree(hist);
+  }
+  if (rc == MQ_OK) {
+    double t = ctx->t_now;
+    for (int64_t m = 0; m < n_steps; ++m) t += dt[m];
+    ctx->t_now = t;
+  }
+  return rc;
+}
+
+int mq_pcg_collect(mq_ctx *ctx, double *ms, int32_t *n_events) {
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  double sum = 0.0;
+  for (int i = 0; i < ctx->ev_n; ++i) {
+    float f = 0.f;
+    MQ_CUDA(cudaEventElapsedTime(&f, ctx->ev_pool[2 * i], ctx->ev_pool[2 * i + 1]));
+    sum += f;
+  }
+  *ms = sum;
+  if (n_events) *n_events = ctx->ev_n;
+  return MQ_OK;
+}
+
+}  // extern "C"

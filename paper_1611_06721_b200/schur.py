@@ -1,0 +1,371 @@
+"""Device twins of the reference's Schur/explicit-Euler entry points.
+
+``SchurOperator.solve_kn`` (schur.py:239-264), ``explicit_euler_step``
+(schur.py:379-405), ``recover_an`` (schur.py:408-419) and ``run_explicit``
+(schur.py:474-607) keep the reference's names, arguments, counters and
+exceptions; underneath, the conducting state, the three right-hand-side
+families, their start-vector histories and every PCG solve stay on the GPU.
+``run_explicit`` runs the whole time loop on the device (one CUDA graph per
+step, replayed) and synchronises with the host only at output rows that need
+host data, or once at the end.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, dptr, f64
+from .device import DeviceGrid, Problem
+from .krylov import PcgConfig, Preconditioner, SolveReport
+from .startvec import RhsFamily, family_index, solver_cfg
+
+__all__ = ["StepFailureError", "SchurOperator", "explicit_euler_step", "recover_an",
+           "run_explicit", "TransientResult", "FAMILIES", "step_times"]
+
+FAMILIES = (RhsFamily.SOURCE_CURRENT, RhsFamily.COUPLING_FROM_CURRENT_STATE,
+            RhsFamily.COUPLING_FROM_PREVIOUS_STATE)
+
+
+class StepFailureError(RuntimeError):
+    """Non-finite state or a stalled inner solve (schur.py:56-57)."""
+
+
+def _report(r: _lib.SolveReportC) -> SolveReport:
+    return SolveReport(int(r.iterations), float(r.final_rel_residual), bool(r.converged),
+                       int(r.applies))
+
+
+class SchurOperator:
+    """Device-resident eliminated-block operator (schur.py:168-313)."""
+
+    def __init__(self, problem, pcg: PcgConfig | None = None, strategy="previous", *,
+                 preconditioner=Preconditioner.JACOBI, max_cols: int = 20,
+                 n_pod: int = 10, eps_pod: float = 1e-4, device: int = 0):
+        if Preconditioner(preconditioner) is not Preconditioner.JACOBI:
+            raise NotImplementedError("the device K_n path uses the reference's Jacobi preconditioner")
+        self.grid = problem if isinstance(problem, DeviceGrid) else DeviceGrid(problem, device)
+        self.problem = self.grid.problem
+        self.pcg = pcg or PcgConfig()
+        self.strategy_kind = str(strategy).lower()
+        if self.problem.pattern is None:
+            raise ValueError("problem has no source pattern")
+        pat = f64(self.problem.pattern, self.grid.n_n, "source pattern")
+        cfg = solver_cfg(self.strategy_kind, max_cols=max_cols, n_pod=n_pod, eps_pod=eps_pod,
+                         rel_tol=self.pcg.rel_tol, abs_tol=self.pcg.abs_tol,
+                         max_iter=self.pcg.max_iter, drop_tol=self.pcg.rel_tol)
+        self.cfg = cfg
+        self.lib = self.grid.lib
+        check(self.lib.mq_solver_init(self.grid.ctx, ctypes.byref(cfg), dptr(pat)))
+        self.solve_iterations = {f: [] for f in FAMILIES}
+        self.solver_seconds = 0.0
+        self._rhs = self.grid.alloc()
+        self._y = self.grid.alloc()
+        self._minv_diag = 1.0 / self.grid.mc_diag()
+        self.t = 0.0
+
+    @property
+    def system_n_c(self):
+        return self.grid.n_c
+
+    def diagnostics(self) -> _lib.Diag:
+        d = _lib.Diag()
+        check(self.lib.mq_diagnostics(self.grid.ctx, ctypes.byref(d)))
+        return d
+
+    @property
+    def pcg_applies(self) -> int:
+        return int(self.diagnostics().pcg_applies)
+
+    @property
+    def maintenance_applies(self) -> int:
+        return int(self.diagnostics().maintenance_applies)
+
+    def solve_count(self, family) -> int:
+        return len(self.solve_iterations[family])
+
+    def total_solves(self) -> int:
+        return sum(len(v) for v in self.solve_iterations.values())
+
+    def total_iterations(self) -> int:
+        return sum(sum(v) for v in self.solve_iterations.values())
+
+    def basis_size(self) -> int:
+        d = self.diagnostics()
+        if self.strategy_kind == "cspe":
+            return int(max(d.basis_cols))
+        if self.strategy_kind == "pod":
+            return int(d.pod_k)
+        return 0
+
+    def strategy_diagnostics(self) -> dict:
+        d = self.diagnostics()
+        if self.strategy_kind == "cspe":
+            return {"basis_cols": int(max(d.basis_cols)),
+                    "maintenance_applies": int(d.maintenance_applies)}
+        if self.strategy_kind == "pod":
+            return {"pod_k": int(d.pod_k), "pod_info": float(d.pod_info),
+                    "min_pod_info": float(d.min_pod_info),
+                    "maintenance_applies": int(d.maintenance_applies)}
+        return {}
+
+    def solve_kn(self, rhs, family) -> tuple[np.ndarray, SolveReport]:
+        """One pseudo-inverse action K_n^+ rhs for the family (schur.py:239-264)."""
+        started = time.perf_counter()
+        self.grid.upload(f64(rhs, self.grid.n_n, "rhs"), self._rhs)
+        rep = _lib.SolveReportC()
+        rc = self.lib.mq_solve_kn(self.grid.ctx, family_index(family), ctypes.c_void_p(self._rhs),
+                                  ctypes.c_void_p(self._y), ctypes.byref(rep))
+        check(rc)
+        y = self.grid.download(self._y)
+        fam = family if isinstance(family, RhsFamily) else RhsFamily(getattr(family, "value", family))
+        self.solve_iterations[fam].append(int(rep.iterations))
+        self.solver_seconds += time.perf_counter() - started
+        return y, _report(rep)
+
+    def source_solution(self, t: float):
+        """K_n^+ j_n(t) (schur.py:266-278, cache_source_solve=False)."""
+        scale = float(self.problem.waveform(t))
+        return self.solve_kn(self.problem.pattern * scale, RhsFamily.SOURCE_CURRENT)
+
+    def minv(self, x):
+        return self._minv_diag * x
+
+    def _set_state(self, a_c, t):
+        v = f64(a_c, self.grid.n_c, "state")
+        check(self.lib.mq_state_set(self.grid.ctx, dptr(v), float(t)))
+        self.t = float(t)
+
+    def _get_state(self):
+        out = np.empty(self.grid.n_c)
+        check(self.lib.mq_state_get(self.grid.ctx, dptr(out), None))
+        return out
+
+
+def explicit_euler_step(state, dt: float, op: SchurOperator, step_index: int | None = None):
+    """One explicit Euler step on the device (schur.py:379-405)."""
+    a_c, t = state
+    if dt < 0:
+        raise ValueError("dt must be nonnegative")
+    op._set_state(a_c, t)
+    t_new = t + dt
+    r1, r2 = _lib.SolveReportC(), _lib.SolveReportC()
+    rc = op.lib.mq_euler_step(op.grid.ctx, float(dt), float(op.problem.waveform(t_new)),
+                              int(step_index if step_index is not None else -1),
+                              ctypes.byref(r1), ctypes.byref(r2))
+    if rc == _lib.MQ_NONFINITE:
+        where = f" at step {step_index}" if step_index is not None else ""
+        raise StepFailureError(f"non-finite conducting state{where} (t = {t_new:.6e})")
+    check(rc)
+    op.solve_iterations[RhsFamily.SOURCE_CURRENT].append(int(r1.iterations))
+    op.solve_iterations[RhsFamily.COUPLING_FROM_PREVIOUS_STATE].append(int(r2.iterations))
+    return op._get_state(), (_report(r1), _report(r2))
+
+
+def recover_an(op: SchurOperator, a_c, t: float):
+    """a_n = K_n^+ j_n(t) - K_n^+ K_cn^T a_c (schur.py:408-419)."""
+    op._set_state(a_c, t)
+    a_n = np.empty(op.grid.n_n)
+    r1, r2 = _lib.SolveReportC(), _lib.SolveReportC()
+    rc = op.lib.mq_recover_an(op.grid.ctx, float(op.problem.waveform(t)), dptr(a_n),
+                              ctypes.byref(r1), ctypes.byref(r2))
+    check(rc)
+    op.solve_iterations[RhsFamily.SOURCE_CURRENT].append(int(r1.iterations))
+    op.solve_iterations[RhsFamily.COUPLING_FROM_CURRENT_STATE].append(int(r2.iterations))
+    return a_n, (_report(r1), _report(r2))
+
+
+@dataclass
+class TransientResult:
+    """schur.py:422-443."""
+
+    times: np.ndarray
+    probe_b: np.ndarray
+    iters_src: np.ndarray
+    iters_cpl_prev: np.ndarray
+    iters_cpl_cur: np.ndarray
+    basis_cols: np.ndarray
+    pod_k: np.ndarray
+    pod_info: np.ndarray
+    final_a_c: np.ndarray
+    final_a_n: np.ndarray | None
+    aggregates: dict = field(default_factory=dict)
+    step_iterations: np.ndarray | None = None   # per step [src, prev, src_rec, cur]
+    a_c_history: np.ndarray | None = None
+
+    @property
+    def n_rows(self) -> int:
+        return self.times.size
+
+
+def step_times(t_end: float, dt: float, output_period: float, max_steps: int = 2_000_000):
+    """The reference loop's (step_dt list, output-after-step flags)
+    (schur.py:546-572), evaluated on the host in the same float order."""
+    eps = 1e-12 * t_end
+    t = 0.0
+    next_output = output_period
+    dts, outs = [], []
+    while t < t_end - eps:
+        step_dt = min(dt, t_end - t)
+        t += step_dt
+        dts.append(step_dt)
+        if len(dts) > max_steps:
+            raise StepFailureError(f"step budget exceeded ({max_steps})")
+        out = t >= next_output - eps or t >= t_end - eps
+        outs.append(out)
+        if out:
+            while next_output <= t + eps:
+                next_output += output_period
+    return dts, outs
+
+
+def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig | None = None,
+                 preconditioner=Preconditioner.JACOBI, output_period: float = 1e-3,
+                 probe=None, a0=None, max_cols: int = 20, n_pod: int = 10,
+                 eps_pod: float = 1e-4, max_steps: int = 2_000_000, device: int = 0,
+                 use_graph: bool = True, record_states: bool = False,
+                 op: SchurOperator | None = None) -> TransientResult:
+    """Integrate with explicit Euler on the device (schur.py:474-607), fixed dt.
+
+    ``dt`` must be a number (the spectral estimate runs separately).
+    """
+    if t_end <= 0:
+        raise ValueError("t_end must be positive")
+    if output_period <= 0:
+        raise ValueError("output_period must be positive")
+    if isinstance(dt, str):
+        raise ValueError("run_explicit on the device needs a numeric dt")
+    dt = float(dt)
+    if dt <= 0:
+        raise ValueError("dt must be positive")
+    wall_start = time.perf_counter()
+    if op is None:
+        op = SchurOperator(problem, pcg=pcg, strategy=strategy, preconditioner=preconditioner,
+                           max_cols=max_cols, n_pod=n_pod, eps_pod=eps_pod, device=device)
+    n_c, n_n = op.grid.n_c, op.grid.n_n
+    a_c = np.zeros(n_c) if a0 is None else f64(a0, n_c, "initial state").copy()
+    wave = op.problem.waveform
+    dts, outs = step_times(t_end, dt, output_period, max_steps)
+    rows = {k: [] for k in ("t", "b", "src", "prev", "cur", "basis", "k", "info")}
+
+    def emit(t_row, a_c_row, a_n_row, iters_src, iters_prev, iters_cur):
+        rows["t"].append(t_row)
+        rows["b"].append(float(probe(a_c_row, a_n_row, t_row)) if probe else 0.0)
+        rows["src"].append(float(np.mean(iters_src)) if len(iters_src) else 0.0)
+        rows["prev"].append(float(np.mean(iters_prev)) if len(iters_prev) else 0.0)
+        rows["cur"].append(float(np.mean(iters_cur)) if len(iters_cur) else 0.0)
+        diag = op.strategy_diagnostics()
+        rows["basis"].append(op.basis_size())
+        rows["k"].append(diag.get("pod_k", 0))
+        rows["info"].append(diag.get("min_pod_info", 1.0) if op.strategy_kind == "pod" else 1.0)
+
+    # initial recovery at t = 0 (schur.py:540-541)
+    a_n, (r1, r2) = recover_an(op, a_c, 0.0)
+    emit(0.0, a_c, a_n, [r1.iterations], [], [r2.iterations])
+    op._set_state(a_c, 0.0)
+    n = len(dts)
+    # exact host float sequence of t (t += step_dt)
+    tt = [0.0]
+    for d in dts:
+        tt.append(tt[-1] + d)
+    t_nodes = np.array(tt)
+    wave_tab = np.array([float(wave(x)) for x in t_nodes])
+    dt_tab = np.array(dts, dtype=np.float64)
+    all_out = all(outs)
+    step_iters = np.zeros((n, 4), dtype=np.int32)
+    hist = np.empty((n, n_c)) if record_states else None
+    failed = ctypes.c_int64(-1)
+    if all_out and probe is None:
+        rc = op.lib.mq_run_explicit(op.grid.ctx, n, dptr(dt_tab), dptr(wave_tab), 1,
+                                    1 if use_graph else 0, _lib.i32ptr(step_iters),
+                                    dptr(hist) if hist is not None else None, ctypes.byref(failed))
+        if rc == _lib.MQ_NONFINITE:
+            raise StepFailureError(f"non-finite conducting state at step {failed.value}")
+        check(rc)
+        a_c = op._get_state()
+        # rows: one per step, window means over that step's solves
+        for m in range(n):
+            rows["t"].append(tt[m + 1])
+            rows["b"].append(0.0)
+            rows["src"].append(float(np.mean(step_iters[m, [0, 2]])))
+            rows["prev"].append(float(step_iters[m, 1]))
+            rows["cur"].append(float(step_iters[m, 3]))
+        diag = op.strategy_diagnostics()
+        nb = op.basis_size()
+        rows["basis"].extend([nb] * n)
+        rows["k"].extend([diag.get("pod_k", 0)] * n)
+        rows["info"].extend([diag.get("min_pod_info", 1.0) if op.strategy_kind == "pod" else 1.0] * n)
+        op.solve_iterations[RhsFamily.SOURCE_CURRENT].extend(
+            int(v) for pair in step_iters[:, [0, 2]] for v in pair)
+        op.solve_iterations[RhsFamily.COUPLING_FROM_PREVIOUS_STATE].extend(int(v) for v in step_iters[:, 1])
+        op.solve_iterations[RhsFamily.COUPLING_FROM_CURRENT_STATE].extend(int(v) for v in step_iters[:, 3])
+        a_n = _final_an(op)
+    else:
+        win_src, win_prev = [], []
+        m = 0
+        while m < n:
+            seg = 0
+            while m + seg < n and not outs[m + seg]:
+                seg += 1
+            seg += 1 if m + seg < n else 0
+            seg = min(seg, n - m)
+            it = np.zeros((seg, 4), dtype=np.int32)
+            rc = op.lib.mq_run_explicit(op.grid.ctx, seg, dptr(dt_tab[m:m + seg]),
+                                        dptr(wave_tab[m:m + seg + 1].copy()), 0,
+                                        1 if use_graph else 0, _lib.i32ptr(it), None,
+                                        ctypes.byref(failed))
+            if rc == _lib.MQ_NONFINITE:
+                raise StepFailureError(f"non-finite conducting state at step {m + failed.value}")
+            check(rc)
+            win_src.extend(int(v) for v in it[:, 0])
+            win_prev.extend(int(v) for v in it[:, 1])
+            op.solve_iterations[RhsFamily.SOURCE_CURRENT].extend(int(v) for v in it[:, 0])
+            op.solve_iterations[RhsFamily.COUPLING_FROM_PREVIOUS_STATE].extend(int(v) for v in it[:, 1])
+            m += seg
+            if outs[m - 1]:
+                a_c = op._get_state()
+                a_n, (r1, r2) = recover_an(op, a_c, tt[m])
+                emit(tt[m], a_c, a_n, win_src + [r1.iterations], win_prev, [r2.iterations])
+                win_src, win_prev = [], []
+        a_c = op._get_state()
+    wall = time.perf_counter() - wall_start
+    d = op.diagnostics()
+    aggregates = {
+        "integrator": "explicit",
+        "strategy": op.strategy_kind,
+        "steps": n,
+        "dt": dt,
+        "lambda_max": None,
+        "cfl_refreshes": 0,
+        "solves": {f.value: op.solve_count(f) for f in FAMILIES},
+        "iterations": {f.value: int(sum(op.solve_iterations[f])) for f in FAMILIES},
+        "mean_iterations": {f.value: (float(np.mean(op.solve_iterations[f]))
+                                      if op.solve_iterations[f] else 0.0) for f in FAMILIES},
+        "pcg_applies": int(d.pcg_applies),
+        "maintenance_applies": int(d.maintenance_applies),
+        "operator_applies": int(d.pcg_applies + d.maintenance_applies),
+        "wall_seconds": wall,
+        "min_pod_info": float(d.min_pod_info),
+        "max_basis_cols": int(max(d.basis_cols)),
+        "aborted": False,
+    }
+    return TransientResult(times=np.asarray(rows["t"]), probe_b=np.asarray(rows["b"]),
+                           iters_src=np.asarray(rows["src"]), iters_cpl_prev=np.asarray(rows["prev"]),
+                           iters_cpl_cur=np.asarray(rows["cur"]),
+                           basis_cols=np.asarray(rows["basis"], dtype=np.int64),
+                           pod_k=np.asarray(rows["k"], dtype=np.int64),
+                           pod_info=np.asarray(rows["info"]), final_a_c=a_c, final_a_n=a_n,
+                           aggregates=aggregates,
+                           step_iterations=step_iters if all_out and probe is None else None,
+                           a_c_history=hist)
+
+
+def _final_an(op: SchurOperator) -> np.ndarray:
+    """a_n = y_src - y_cpl of the last recovery, read from the device."""
+    out = np.empty(op.grid.n_n)
+    check(op.lib.mq_last_an(op.grid.ctx, dptr(out)))
+    return out

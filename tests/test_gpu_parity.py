@@ -1,0 +1,344 @@
+"""Parity of the CUDA path (through the C ABI) against the pinned oracle.
+
+Bars (BASELINE.json north_star): DoF numbering and masks bit-exact; A-field
+within 1e-8 relative L2 per time step; PCG iteration counts within +-1.
+Integer/structural results and the K_n SpMV (same CSR column order, no FMA)
+must be bit-identical.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import mq_oracle as O
+from tests.conftest import oracle_model
+
+pytestmark = pytest.mark.gpu
+
+REL_FIELD = 1e-8   # north_star: A-field within 1e-8 relative L2 per step
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def c0(gpu_ok):
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200.device import DeviceGrid
+    spec, m = oracle_model(0)
+    prob = C.make_problem(0)
+    g = DeviceGrid(prob)
+    yield spec, m, prob, g
+    g.close()
+
+
+def test_partition_and_masks_bit_exact(c0):
+    spec, m, prob, g = c0
+    nc, c = g.partition()
+    assert (g.n_c, g.n_n) == (m.n_c, m.n_n) == (882, 9918)
+    assert np.array_equal(nc, m.noncond_global)
+    assert np.array_equal(c, m.cond_global)
+    assert np.array_equal(g.mc_diag(), m.mc_diag)
+    assert g.kn_diag == m.kn.diagonal()[0]
+    assert g.kn_off == np.abs(m.kn.data).min()
+    assert g.jacobi_inv == O.jacobi_inverse(m.kn.diagonal())[0]
+    assert np.array_equal(prob.pattern, m.pattern)
+    idx = g.noncond_index(m.noncond_global[[0, 5, -1]])
+    assert list(idx) == [0, 5, m.n_n - 1]
+
+
+def test_partition_two_blocks_and_boundary_cases(gpu_ok):
+    """Disjoint blocks, a block touching the PEC boundary, a single cell."""
+    from paper_1611_06721_b200.device import DeviceGrid, Problem
+    N = 10
+    cases = []
+    mat = np.zeros((N, N, N), np.int8)
+    mat[1:3, 2:5, 3:6] = 1
+    mat[6:9, 5:8, 1:4] = 1
+    cases.append(mat)
+    mat = np.zeros((N, N, 7), np.int8)     # non-cubic, conductor on the boundary
+    mat[0:3, 0:2, 0:7] = 1
+    cases.append(mat)
+    mat = np.zeros((4, 4, 4), np.int8)     # corner toy (tests/conftest.py:92-106)
+    mat[0, 0, 0] = 1
+    cases.append(mat)
+    for mat in cases:
+        m = O.assemble(mat, 0.1, O.Conductor(3e6, 0, 0, 500.0), [])
+        g = DeviceGrid(Problem(material=mat, h=0.1, kappa=3e6, brauer=(0, 0, 500.0),
+                               pattern=np.zeros(m.n_n)))
+        nc, c = g.partition()
+        assert np.array_equal(nc, m.noncond_global)
+        assert np.array_equal(c, m.cond_global)
+        assert np.array_equal(g.mc_diag(), m.mc_diag)
+        x = np.random.default_rng(3).standard_normal(m.n_n)
+        assert np.array_equal(g.kn_apply(x), m.kn @ x)
+        xc = np.random.default_rng(4).standard_normal(m.n_c)
+        assert np.array_equal(g.kcn_t_apply(xc), m.kcn.T @ xc)
+        assert np.array_equal(g.kcn_apply(x), m.kcn @ x)
+        g.close()
+
+
+def test_kn_spmv_bitwise(c0, golden):
+    spec, m, prob, g = c0
+    rng = np.random.default_rng(20250819)
+    x = rng.standard_normal(m.n_n)
+    y = g.kn_apply(x)
+    assert np.array_equal(y, golden["c0_spmv_y"])     # the reference's own scipy result
+    for _ in range(3):
+        x = rng.standard_normal(m.n_n) * rng.uniform(1e-6, 1e6)
+        assert np.array_equal(g.kn_apply(x), m.kn @ x)
+
+
+def test_conducting_block_products(c0, golden):
+    spec, m, prob, g = c0
+    st, xc = golden["c0b_kc_state"], golden["c0b_kc_x"]
+    assert np.array_equal(g.kc_apply(st, xc), golden["c0_kc_y"])       # linear: bit-exact
+    assert np.array_equal(g.kcn_t_apply(xc), golden["c0_kcnt_y"])
+    x = np.random.default_rng(5).standard_normal(m.n_n)
+    assert np.array_equal(g.kcn_apply(x), m.kcn @ x)
+
+
+def test_brauer_kc_apply(gpu_ok, golden):
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200.device import DeviceGrid
+    prob = C.make_problem(0)
+    prob.brauer = C.BRAUER_IRON
+    with DeviceGrid(prob) as g:
+        st, xc = golden["c0b_kc_state"], golden["c0b_kc_x"]
+        y = g.kc_apply(st, xc)
+        # exp() differs from numpy's by at most an ulp or two
+        assert rel(y, golden["c0b_kc_y"]) <= 1e-14
+        for scale in (0.0, 1e-3, 3e-3):   # up to deep saturation
+            s = st * (scale / 2e-4) if scale else np.zeros_like(st)
+            _, mb = oracle_model(0, brauer=C.BRAUER_IRON)
+            assert rel(g.kc_apply(s, xc), mb.kc_apply(s, xc)) <= 1e-13
+
+
+def test_pcg_matches_oracle(c0, golden):
+    from paper_1611_06721_b200 import PcgConfig, Preconditioner, pcg_solve
+    spec, m, prob, g = c0
+    op = g.kn_operator()
+    inv = O.jacobi_inverse(m.kn.diagonal())
+    cfg = PcgConfig(rel_tol=1e-8, max_iter=5000, preconditioner=Preconditioner.JACOBI)
+    rng = np.random.default_rng(7)
+    b = m.kn @ rng.standard_normal(m.n_n)
+    x0 = rng.standard_normal(m.n_n) * 1e-3
+    for start in (None, x0, np.zeros(m.n_n)):
+        x, rep = pcg_solve(op, b, x0=start, config=cfg)
+        ref = O.pcg(m.kn_apply, b, x0=start, rel_tol=1e-8, inv_diag=inv)
+        assert rep.converged and ref.converged
+        assert abs(rep.iterations - ref.iterations) <= 1
+        assert rep.applications == ref.applies
+        assert rel(x, ref.x) <= 1e-8
+        assert rep.final_rel_residual <= 1e-8
+
+
+def test_pcg_semantics(c0):
+    """krylov.py semantics: zero-iteration shortcut, zero rhs, budget, counts."""
+    from paper_1611_06721_b200 import PcgConfig, Preconditioner, pcg_solve
+    spec, m, prob, g = c0
+    op = g.kn_operator()
+    cfg = PcgConfig(rel_tol=1e-8, preconditioner=Preconditioner.JACOBI)
+    # zero rhs, no x0: free (0 applications, rel 0)
+    x, rep = pcg_solve(op, np.zeros(m.n_n), config=cfg)
+    assert rep.iterations == 0 and rep.converged and rep.final_rel_residual == 0.0
+    assert rep.applications == 0 and np.array_equal(x, np.zeros(m.n_n))
+    # exact start vector: one application, x returned bit-identical
+    xs = O.pcg(m.kn_apply, m.pattern, rel_tol=1e-12, inv_diag=O.jacobi_inverse(m.kn.diagonal())).x
+    b = m.kn @ xs
+    x, rep = pcg_solve(op, b, x0=xs, config=cfg)
+    assert rep.iterations == 0 and rep.applications == 1 and np.array_equal(x, xs)
+    # budget exhaustion: converged False with the last iterate
+    x, rep = pcg_solve(op, m.pattern, config=PcgConfig(rel_tol=1e-14, max_iter=3,
+                                                       preconditioner=Preconditioner.JACOBI))
+    ref = O.pcg(m.kn_apply, m.pattern, rel_tol=1e-14, max_iter=3,
+                inv_diag=O.jacobi_inverse(m.kn.diagonal()))
+    assert not rep.converged and rep.iterations == 3 and not ref.converged
+    assert rel(x, ref.x) <= 1e-12
+    assert abs(rep.final_rel_residual - ref.rel) <= 1e-10 * ref.rel
+    # no preconditioner
+    x, rep = pcg_solve(op, m.pattern, config=PcgConfig(rel_tol=1e-8))
+    ref = O.pcg(m.kn_apply, m.pattern, rel_tol=1e-8)
+    assert abs(rep.iterations - ref.iterations) <= 1 and rel(x, ref.x) <= 1e-8
+    # non-finite input rejected like sparse.as_vector
+    bad = m.pattern.copy()
+    bad[3] = np.nan
+    with pytest.raises(ValueError):
+        pcg_solve(op, bad, config=cfg)
+
+
+def test_csr_path_reference_cases(gpu_ok):
+    """The reference's krylov tests, through the general CSR device path."""
+    import scipy.sparse as sp
+
+    from paper_1611_06721_b200 import (IndefiniteOperatorError, JacobiPreconditioner,
+                                       PcgConfig, Preconditioner, pcg_solve)
+    rng = np.random.default_rng(20250819)
+    b = rng.standard_normal(5)
+    x, rep = pcg_solve(sp.identity(5, format="csr"), b)
+    assert rep.converged and rep.iterations == 1 and np.allclose(x, b, rtol=0, atol=1e-14)
+    q = np.linalg.qr(rng.standard_normal((30, 30)))[0]
+    dense = (q * rng.uniform(0.5, 50.0, 30)) @ q.T
+    dense = 0.5 * (dense + dense.T)
+    b = rng.standard_normal(30)
+    for kind in (Preconditioner.NONE, Preconditioner.JACOBI):
+        x, rep = pcg_solve(dense, b, config=PcgConfig(rel_tol=1e-10, max_iter=200,
+                                                     preconditioner=kind))
+        ref = O.pcg(lambda v: sp.csr_matrix(dense) @ v, b, rel_tol=1e-10, max_iter=200,
+                    inv_diag=O.jacobi_inverse(np.diag(dense)) if kind is Preconditioner.JACOBI else None)
+        assert rep.converged and abs(rep.iterations - ref.iterations) <= 1
+        assert np.linalg.norm(dense @ x - b) / np.linalg.norm(b) <= 1e-8
+    lap = np.array([[1.0, -1, 0, 0], [-1, 2, -1, 0], [0, -1, 2, -1], [0, 0, -1, 1]])
+    bb = np.array([1.0, -0.5, 0.25, -0.75])
+    x, rep = pcg_solve(lap, bb, x0=np.zeros(4), config=PcgConfig(rel_tol=1e-12, max_iter=100))
+    assert rep.converged and np.allclose(x, np.linalg.pinv(lap) @ bb, rtol=0, atol=1e-8)
+    with pytest.raises(IndefiniteOperatorError):
+        pcg_solve(np.diag([1.0, -1.0]), np.array([1.0, 1.0]))
+    x, rep = pcg_solve(np.diag([2.0, 2.0]), np.array([2.0, 4.0]),
+                       config=PcgConfig(preconditioner=Preconditioner.JACOBI),
+                       preconditioner=JacobiPreconditioner(np.full(2, 2.0)))
+    assert rep.converged and np.allclose(x, [1.0, 2.0], rtol=0, atol=1e-12)
+    with pytest.raises(TypeError):
+        pcg_solve(lambda v: v, np.ones(2))
+
+
+def test_cspe_strategy_parity(c0, golden):
+    from paper_1611_06721_b200 import DeviceStrategy, RhsFamily
+    spec, m, prob, g = c0
+    inv = O.jacobi_inverse(m.kn.diagonal())
+    rng = np.random.default_rng(11)
+    seq = [O.pcg(m.kn_apply, m.kn @ rng.standard_normal(m.n_n), rel_tol=1e-8, inv_diag=inv).x
+           for _ in range(6)]
+    seq.append(seq[2] * 3.0)      # dependent -> dropped
+    seq.append(np.zeros(m.n_n))   # zero -> dropped
+    strat = DeviceStrategy(g, "cspe", max_cols=5, drop_tol=1e-8)
+    cache = O.SpeCache(m.n_n, m.kn_apply, max_cols=5, drop_tol=1e-8)
+    fam = RhsFamily.SOURCE_CURRENT
+    rhs = m.kn @ rng.standard_normal(m.n_n)
+    assert np.array_equal(strat.start_vector(fam, rhs), np.zeros(m.n_n))  # empty cache
+    for v in seq:
+        strat.observe(fam, v)
+        cache.insert(v)
+        assert strat.basis_size(fam) == cache.k
+        assert strat.basis_size(RhsFamily.COUPLING_FROM_PREVIOUS_STATE) == 0
+    assert strat.maintenance_applies == cache.products
+    U, KU, G = strat.cache_export(fam)
+    assert rel(G, cache.G) <= 1e-10
+    assert np.max(np.abs(U - cache.U)) <= 1e-10 * np.max(np.abs(cache.U))
+    assert rel(KU, cache.KU) <= 1e-10
+    x0 = strat.start_vector(fam, rhs)
+    assert rel(x0, cache.project(rhs)) <= 1e-8
+    # family isolation
+    assert np.array_equal(strat.start_vector(RhsFamily.COUPLING_FROM_CURRENT_STATE, rhs),
+                          np.zeros(m.n_n))
+
+
+def test_pod_strategy_parity(c0):
+    from paper_1611_06721_b200 import DeviceStrategy, RhsFamily
+    spec, m, prob, g = c0
+    inv = O.jacobi_inverse(m.kn.diagonal())
+    rng = np.random.default_rng(12)
+    seq = [O.pcg(m.kn_apply, m.kn @ rng.standard_normal(m.n_n), rel_tol=1e-8, inv_diag=inv).x
+           for _ in range(5)]
+    seq += [seq[0] + 1e-3 * seq[1], seq[3] * 0.5, seq[1] - 1e-6 * seq[2]]
+    strat = DeviceStrategy(g, "pod", n_pod=6, eps_pod=1e-4)
+    snap = O.Snapshots(m.n_n, n_pod=6, eps_pod=1e-4)
+    pod = O.PodStrategyOracle(m.n_n, m.kn_apply, n_pod=6, eps_pod=1e-4)
+    fam = RhsFamily.COUPLING_FROM_PREVIOUS_STATE
+    rhs = m.kn @ rng.standard_normal(m.n_n)
+    for i, v in enumerate(seq):
+        strat.observe(fam, v)
+        pod.observe(O.FAM_PREV, v)
+        x_dev = strat.start_vector(fam, rhs)
+        x_ref = pod.start(O.FAM_PREV, rhs)
+        d = strat.diagnostics()
+        assert d["pod_k"] == pod.last_k, i
+        assert abs(d["pod_info"] - pod.last_info) <= 1e-12
+        assert d["maintenance_applies"] == pod.applies
+        assert rel(x_dev, x_ref) <= 1e-8, i
+    assert abs(strat.diagnostics()["min_pod_info"] - pod.min_info) <= 1e-12
+
+
+@pytest.mark.parametrize("strategy,nsteps", [("cspe", 100), ("pod", 30), ("previous", 30)])
+def test_transient_config0_device_loop(gpu_ok, strategy, nsteps):
+    """run_explicit twin (device-resident loop, CUDA graph replay) vs oracle."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, run_explicit
+    spec, m = oracle_model(0)
+    prob = C.make_problem(0)
+    tr = O.run(m, O.sinusoid(50.0), spec.dt, nsteps, strategy=strategy, rel_tol=1e-8,
+               max_cols=5, n_pod=20, eps_pod=1e-4)
+    res = run_explicit(prob, t_end=nsteps * spec.dt, dt=spec.dt, strategy=strategy,
+                       pcg=PcgConfig(rel_tol=1e-8, max_iter=5000),
+                       output_period=spec.dt * (1 - 1e-3), max_cols=5, n_pod=20,
+                       eps_pod=1e-4, record_states=True, use_graph=False)
+    hist = res.a_c_history
+    assert hist.shape == (nsteps, m.n_c)
+    worst = max(rel(hist[i], tr.a_c[i + 1]) for i in range(nsteps))
+    assert worst <= REL_FIELD, worst
+    it = res.step_iterations
+    src = np.array(tr.iters[O.FAM_SOURCE][1:]).reshape(nsteps, 2)
+    assert np.max(np.abs(it[:, 0] - src[:, 0])) <= 1
+    assert np.max(np.abs(it[:, 2] - src[:, 1])) <= 1
+    assert np.max(np.abs(it[:, 1] - np.array(tr.iters[O.FAM_PREV]))) <= 1
+    assert np.max(np.abs(it[:, 3] - np.array(tr.iters[O.FAM_CUR][1:]))) <= 1
+    assert rel(res.final_a_n, tr.a_n[-1]) <= REL_FIELD
+    # graph replay gives the same trajectory as eager launches
+    res_g = run_explicit(prob, t_end=nsteps * spec.dt, dt=spec.dt, strategy=strategy,
+                         pcg=PcgConfig(rel_tol=1e-8, max_iter=5000),
+                         output_period=spec.dt * (1 - 1e-3), max_cols=5, n_pod=20,
+                         eps_pod=1e-4, use_graph=True)
+    assert np.array_equal(res_g.final_a_c, hist[-1])
+    assert np.array_equal(res_g.step_iterations, it)
+
+
+def test_single_step_api_matches_oracle(gpu_ok):
+    """explicit_euler_step / recover_an / SchurOperator.solve_kn twins."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import (PcgConfig, RhsFamily, SchurOperator,
+                                       explicit_euler_step, recover_an)
+    spec, m = oracle_model(0)
+    prob = C.make_problem(0)
+    op = SchurOperator(prob, pcg=PcgConfig(rel_tol=1e-8), strategy="cspe", max_cols=5)
+    ref = O.SchurOracle(m, O.sinusoid(50.0), "cspe", 1e-8, 5000, 5)
+    a, a_ref, t = np.zeros(m.n_c), np.zeros(m.n_c), 0.0
+    an, (r1, r2) = recover_an(op, a, t)
+    an_ref, (q1, q2) = ref.recover(a_ref, t)
+    assert rel(an, an_ref) <= REL_FIELD
+    for step in range(1, 6):
+        a, (r1, r2) = explicit_euler_step((a, t), spec.dt, op, step_index=step)
+        a_ref, (q1, q2) = ref.euler(a_ref, t, spec.dt, step)
+        t += spec.dt
+        assert abs(r1.iterations - q1.iterations) <= 1 and abs(r2.iterations - q2.iterations) <= 1
+        assert rel(a, a_ref) <= REL_FIELD
+        an, _ = recover_an(op, a, t)
+        an_ref, _ = ref.recover(a_ref, t)
+        assert rel(an, an_ref) <= REL_FIELD
+    assert op.solve_count(RhsFamily.SOURCE_CURRENT) == 11
+    # dt = 0 reproduces the state bit for bit (schur.py:386-387)
+    a2, _ = explicit_euler_step((a, t), 0.0, op)
+    assert np.array_equal(a2, a)
+    with pytest.raises(ValueError):
+        explicit_euler_step((a, t), -1.0, op)
+
+
+@pytest.mark.slow
+def test_config1_first_steps(gpu_ok, golden):
+    """64^3 Brauer: first two steps against the reference's own numbers."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, run_explicit
+    spec = C.config_spec(1)
+    prob = C.make_problem(1)
+    res = run_explicit(prob, t_end=2 * spec.dt, dt=spec.dt, strategy="cspe",
+                       pcg=PcgConfig(rel_tol=1e-8), output_period=spec.dt * (1 - 1e-3),
+                       max_cols=5, record_states=True)
+    norms = np.linalg.norm(res.a_c_history, axis=1)
+    ref = golden["c1_run_cspe_a_c_norms"][1:]
+    assert np.all(np.abs(norms - ref) <= REL_FIELD * ref)
+    it = golden["c1_run_cspe_iters"]
+    assert np.max(np.abs(res.step_iterations[:, 3] - it[1:, 2])) <= 1
+    assert np.max(np.abs(res.step_iterations[:, 1] - it[1:, 1])) <= 1
