@@ -42,7 +42,7 @@ int ctx_pcg(mq_ctx *ctx, const double *b, double *x, int x0_mode, double rel_tol
     set_error("invalid PCG configuration (rel_tol > 0, abs_tol >= 0, max_iter >= 1)");
     return MQ_INVALID;
   }
-  StencilPcgArgs a;
+  StencilPcgArgs a{};
   a.L = ctx->topo.L;
   a.mask = ctx->d_mask;
   a.dg = ctx->kn_diag;
@@ -359,7 +359,7 @@ int mq_csr_pcg_solve(int32_t device, int64_t n, const int64_t *row_ptr, const in
       if (x0) cudaMemcpy(d_x, x0, sizeof(double) * n, cudaMemcpyHostToDevice);
       if (inv_diag) cudaMemcpy(d_inv, inv_diag, sizeof(double) * n, cudaMemcpyHostToDevice);
     }
-    CsrPcgArgs a;
+    CsrPcgArgs a{};
     a.n = n; a.rp = d_rp; a.ci = d_ci; a.va = d_va; a.inv = d_inv; a.has_x0 = x0 != nullptr;
     a.b = d_b; a.x = d_x; a.r = d_r; a.p = d_p; a.ap = d_ap;
     a.rel_tol = rel_tol; a.abs_tol = abs_tol; a.max_iter = max_iter;

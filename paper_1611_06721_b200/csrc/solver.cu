@@ -702,6 +702,7 @@ struct CondArgs {
 __device__ __forceinline__ double face_flux(const CondArgs &a, int64_t f, const double *x) {
   // c_cond row: cond edges in ascending compact order, csr sum from 0
   double s = 0.0;
+  if (f < 0) return s;  // boundary face of a conductor cell: all edges PEC
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int32_t e = a.f_edge[4 * f + q];
@@ -1013,7 +1014,7 @@ static int solve_enqueue(mq_ctx *ctx, int fam, const double *rhs, double *y) {
   FamDev *f = s->d_fam + fam;
   int rc = start_vector(ctx, fam, rhs, y);
   if (rc) return rc;
-  StencilPcgArgs a;
+  StencilPcgArgs a{};
   a.L = ctx->topo.L;
   a.mask = ctx->d_mask;
   a.dg = ctx->kn_diag;
@@ -1036,11 +1037,11 @@ static int solve_enqueue(mq_ctx *ctx, int fam, const double *rhs, double *y) {
   a.x0_mode_dev = &f->x0_mode;
   a.err_word = &s->d_run->err;
   const bool timed = ctx->pcg_timing && ctx->ev_n < kEvPool;
-  if (timed) MQ_CUDA(cudaEventRecord(ctx->ev_pool[2 * ctx->ev_n], ctx->stream));
+  if (timed) MQ_CUDA(cudaEventRecordWithFlags(ctx->ev_pool[2 * ctx->ev_n], ctx->stream, cudaEventRecordExternal));
   rc = launch_pcg_stencil(a, ctx->pcg_grid, ctx->stream);
   if (rc) return rc;
   if (timed) {
-    MQ_CUDA(cudaEventRecord(ctx->ev_pool[2 * ctx->ev_n + 1], ctx->stream));
+    MQ_CUDA(cudaEventRecordWithFlags(ctx->ev_pool[2 * ctx->ev_n + 1], ctx->stream, cudaEventRecordExternal));
     ctx->ev_n += 1;
   }
   ctx->launches += 1;

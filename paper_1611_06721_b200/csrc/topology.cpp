@@ -154,7 +154,6 @@ int build_topology(const mq_grid_desc &g, Topology &t, std::string &err) {
   // reference's listing order with signs (+,+,-,-).
   const int64_t C = L.C, Si = L.Si, Sj = L.Sj;
   auto pidx = [&](int c, int i, int j, int k) -> int64_t { return c * C + i * Si + j * Sj + k; };
-  struct Face { int64_t fid; int64_t e[4]; int cellA, cellB; };  // cells as flat ids or -1
   auto face_edges = [&](int dir, int i, int j, int k, int64_t out[4]) {
     if (dir == 0) {        // fx(i,j,k): +ey[i,j,k], +ez[i,j+1,k], -ey[i,j,k+1], -ez[i,j,k]
       out[0] = pidx(1, i, j, k); out[1] = pidx(2, i, j + 1, k);
@@ -239,9 +238,9 @@ int build_topology(const mq_grid_desc &g, Topology &t, std::string &err) {
     int64_t f6[6] = {fid_x(d, i, j, k), fid_x(d, i + 1, j, k), fid_y(d, i, j, k),
                      fid_y(d, i, j + 1, k), fid_z(d, i, j, k), fid_z(d, i, j, k + 1)};
     for (int s = 0; s < 6; ++s) {
-      int32_t fi = face_index(f6[s]);
-      if (fi < 0) { err = "internal: conductor cell face without conducting edge"; return MQ_INVALID; }
-      t.cell_face.push_back(fi);
+      // a face with no conducting edge lies in the PEC boundary plane: its
+      // row of c_cond is empty, so its flux is 0 (index -1)
+      t.cell_face.push_back(face_index(f6[s]));
     }
   }
   t.n_cells_c = (int64_t)cells.size();
