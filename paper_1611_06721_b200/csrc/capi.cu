@@ -1,5 +1,6 @@
 // C ABI of libmq_b200: context, device vectors, K_n operator and PCG.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <set>
@@ -63,7 +64,7 @@ int ctx_pcg(mq_ctx *ctx, const double *b, double *x, int x0_mode, double rel_tol
   a.bar = ctx->d_bar;
   a.out = ctx->d_out;
   if (ctx->pcg_timing) MQ_CUDA(cudaEventRecord(ctx->ev_pcg0, ctx->stream));
-  int rc = launch_pcg_stencil(a, ctx->pcg_grid, ctx->stream);
+  int rc = launch_pcg_ctx(ctx, a);
   if (rc) return rc;
   ctx->launches += 1;
   if (ctx->pcg_timing) MQ_CUDA(cudaEventRecord(ctx->ev_pcg1, ctx->stream));
@@ -92,6 +93,11 @@ int ctx_pcg(mq_ctx *ctx, const double *b, double *x, int x0_mode, double rel_tol
     return MQ_CUDA_ERROR;
   }
   return o.status;
+}
+
+int launch_pcg_ctx(mq_ctx *ctx, const StencilPcgArgs &args) {
+  if (ctx->pcg_variant == 1) return launch_pcg_stencil(args, ctx->pcg_grid, ctx->stream);
+  return launch_pcg_brick(args, ctx->geo, ctx->brick_grid, ctx->stream);
 }
 
 }  // namespace mq
@@ -154,6 +160,11 @@ int mq_ctx_create(const mq_grid_desc *desc, int32_t device, mq_ctx **out) {
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_tmp0, sizeof(double) * t.L.total);
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_tmp1, sizeof(double) * t.L.total);
   if (!rc) rc = pcg_stencil_grid(t.L.words, &ctx->pcg_grid);
+  if (!rc) rc = brick_pcg_setup(t.L, t.nx, t.ny, t.nz, &ctx->brick_grid, &ctx->geo);
+  {
+    const char *v = getenv("MQ_PCG_KERNEL");
+    ctx->pcg_variant = (v && std::string(v) == "simple") ? 1 : 0;
+  }
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_partials, sizeof(double) * 8 * (size_t)std::max(ctx->pcg_grid, 1024));
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_bar, sizeof(GridBar));
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_out, sizeof(PcgOut));
@@ -275,7 +286,10 @@ int mq_vec_download(mq_ctx *ctx, const double *dev, double *host) {
 }
 
 int mq_kn_apply_dev(mq_ctx *ctx, const double *x, double *y) {
-  int rc = launch_kn_apply(ctx->topo.L, ctx->d_mask, ctx->kn_diag, ctx->kn_off, x, y, ctx->sms, ctx->stream);
+  int rc = ctx->pcg_variant == 1
+               ? launch_kn_apply(ctx->topo.L, ctx->d_mask, ctx->kn_diag, ctx->kn_off, x, y, ctx->sms, ctx->stream)
+               : launch_kn_apply_brick(ctx->topo.L, ctx->geo, ctx->d_mask, ctx->kn_diag, ctx->kn_off, x, y,
+                                       ctx->sms, ctx->stream);
   if (!rc) ctx->launches += 1;
   return rc;
 }

@@ -80,6 +80,9 @@ struct mq_ctx {
   mq::PcgOut *d_out = nullptr;
   mq::PcgOut *h_out = nullptr;
   int pcg_grid = 1;
+  int pcg_variant = 0;        // 0: brick-tiled kernel, 1: thread-per-row kernel
+  mq::BrickGeo geo{};
+  int brick_grid = 1;
   // conducting block (device)
   int64_t *d_kcn_ptr = nullptr;
   int32_t *d_kcn_col = nullptr;
@@ -132,6 +135,11 @@ int launch_pcg_stencil(const StencilPcgArgs &args, int grid, cudaStream_t s);
 int pcg_stencil_grid(int64_t words, int *out);
 int launch_pcg_csr(const CsrPcgArgs &args, int grid, cudaStream_t s);
 int pcg_csr_grid(int64_t n, int *out);
+int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int *grid, BrickGeo *geo);
+int launch_pcg_brick(const StencilPcgArgs &args, const BrickGeo &geo, int grid, cudaStream_t s);
+int launch_kn_apply_brick(const Lay &L, const BrickGeo &geo, const uint32_t *mask, double dg, double of,
+                          const double *x, double *y, int sms, cudaStream_t s);
+int launch_pcg_ctx(mq_ctx *ctx, const StencilPcgArgs &args);
 int launch_kn_apply(const Lay &L, const uint32_t *mask, double dg, double of, const double *x, double *y, int sms,
                     cudaStream_t s);
 int launch_scatter(int64_t n, const int32_t *idx, const double *src, double *dst, int sms, cudaStream_t s);

@@ -1,10 +1,11 @@
 // Internal declarations of libmq_b200 (not part of the C ABI).
 //
 // Device layout ("padded edge layout"): the three edge components x, y, z
-// each occupy one box of (nx+1)*(ny+1)*(nz+1) doubles, k fastest, the box
-// length rounded up to a multiple of 32 (one 32-bit mask word per warp).
-// Component c starts at c*C.  Inside a box the strides are Sj = nz+1 and
-// Si = (ny+1)*(nz+1).  Within a component the box order is the reference's
+// each occupy one box of nodes i = -1..nx, j = -1..ny, k = -1..nz(+pad),
+// k fastest, the box length rounded up to a multiple of 32 (one 32-bit mask
+// word per warp).  Component c starts at c*C; node (i,j,k) sits at
+// c*C + off + i*Si + j*Sj + k with Sj = nz+2 rounded up to even and
+// Si = (ny+2)*Sj (see topology.cpp).  Within a component the box order is the reference's
 // global edge order (model.py:186-207: ids are C-order with k fastest), so the
 // compact K_n order (ascending global id, model.py:455-464) is exactly the
 // order of active positions in a linear scan of the device layout.  Entries
@@ -25,6 +26,7 @@ namespace mq {
 struct Lay {
   int64_t C;      // padded component length (multiple of 32)
   int64_t Si, Sj; // strides inside a component
+  int64_t off;    // index of node (0,0,0) inside a component (guard layer)
   int64_t total;  // 3*C
   int64_t words;  // total/32 mask words
 };
@@ -62,6 +64,13 @@ struct StencilPcgArgs {
   PcgOut *out;
   const int *x0_mode_dev;      // optional: device-chosen start mode
   const unsigned int *err_word;  // optional: skip the solve if set
+};
+
+// Brick decomposition of the node box [0,nx) x [0,ny) x [0,nz) (pcg_brick.cu)
+struct BrickGeo {
+  int nx, ny, nz;
+  int tiles_k, tiles_j, chunks;
+  int nbricks;
 };
 
 struct CsrPcgArgs {

@@ -1,0 +1,608 @@
+// Brick-tiled fused PCG for the K_n stencil with a TMA pipeline
+// (krylov.py:174-250; same algorithm, stopping rule and bit-level arithmetic
+// as pcg_stencil_kernel in pcg.cu, different work decomposition).
+//
+// K1 (the stencil pass).  Every CTA owns bricks: an 8 (j) x 32 (k) tile of
+// node positions over a chunk of i planes, all three edge components.  It
+// marches along i.  One elected thread streams each plane's (tile + 1-node
+// halo) boxes of r and p_old for the three components into a 5-stage shared
+// memory ring with 4-D TMA bulk tensor loads (cp.async.bulk.tensor, zero fill
+// outside the box = the PEC/grid boundary), two planes ahead of the plane
+// being computed, with mbarrier transaction counts for completion.  The raw
+// r / p_old of a staged plane are converted in place into
+// p_new = M^-1 r + beta p_old; each owner thread writes p_new of its own
+// position and applies the deferred x += alpha_prev p_old.  The K_n rows of
+// plane i are then evaluated from the three staged planes i-1, i, i+1.
+//
+// K2, the initial residual and the final x update are elementwise: flat,
+// 16-byte vectorised, 4-way unrolled grid-stride passes over the padded
+// vectors (entries that are not dofs hold 0 and stay 0).
+//
+// Streams per iteration (fp64, per dof): K1 reads r, p_old, x and writes
+// x, p_new, Ap; K2 reads r, Ap and writes r  ->  9 x 8 B = 72 B.
+#include <cuda.h>
+#include <cstring>
+#include <cudaTypedefs.h>
+
+#include "mq_device.cuh"
+
+namespace mq {
+
+constexpr int TJ = 8, TK = 32;                 // kBlock = TJ * TK threads
+constexpr int HJ = TJ + 2, HK = TK + 2, HP = HJ * HK;  // 10 x 34 box
+constexpr int BOXP = 352;                      // box slot padded to a 128-byte multiple
+constexpr int NST = 5;                         // stages: planes i-1, i, i+1 + 2 in flight
+constexpr int NHALO = 2 * HK + 2 * TJ;         // 84 halo positions per plane
+static_assert(TJ * TK == kBlock, "one thread per tile position");
+static_assert(HP <= BOXP && (BOXP * 8) % 128 == 0, "TMA destination alignment");
+
+struct __align__(128) Stage {
+  double r[3][BOXP];  // raw r, converted in place into p_new (or x0 in the init pass)
+  double p[3][BOXP];  // raw p_old
+};
+
+struct TmaPcgArgs {
+  StencilPcgArgs a;
+  BrickGeo g;
+  CUtensorMap tm_r, tm_pa, tm_pb, tm_x;  // 4-D maps (k, j, i, c), box 34 x 10 x 1 x 1
+};
+
+constexpr size_t kTmaSmem = sizeof(Stage) * NST + 128;
+
+// ---- PTX helpers ----------------------------------------------------------
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(su32(dst)),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void brick_of(const BrickGeo &g, int b, int &i0, int &i1, int &j0, int &k0) {
+  const int tk = b % g.tiles_k;
+  const int r = b / g.tiles_k;
+  const int tj = r % g.tiles_j;
+  const int ic = r / g.tiles_j;
+  k0 = tk * TK;
+  j0 = tj * TJ;
+  i0 = (int)(((int64_t)ic * g.nx) / g.chunks);
+  i1 = (int)(((int64_t)(ic + 1) * g.nx) / g.chunks);
+}
+
+// K_n row in CSR column order on a 3-plane neighbourhood:
+// v(c', di, dj, dk) is the value of component c' at (i+di, j+dj, k+dk).
+// Order and signs are those of stencil_row (mq_device.cuh).
+template <class V>
+__device__ __forceinline__ double stencil3(int c, double dg, double of, V v) {
+  double s;
+  if (c == 0) {
+    s = -mul(of, v(0, 0, -1, 0));
+    s = sub(s, mul(of, v(0, 0, 0, -1)));
+    s = add(s, mul(dg, v(0, 0, 0, 0)));
+    s = sub(s, mul(of, v(0, 0, 0, 1)));
+    s = sub(s, mul(of, v(0, 0, 1, 0)));
+    s = add(s, mul(of, v(1, 0, -1, 0)));
+    s = sub(s, mul(of, v(1, 0, 0, 0)));
+    s = sub(s, mul(of, v(1, 1, -1, 0)));
+    s = add(s, mul(of, v(1, 1, 0, 0)));
+    s = add(s, mul(of, v(2, 0, 0, -1)));
+    s = sub(s, mul(of, v(2, 0, 0, 0)));
+    s = sub(s, mul(of, v(2, 1, 0, -1)));
+    s = add(s, mul(of, v(2, 1, 0, 0)));
+  } else if (c == 1) {
+    s = mul(of, v(0, -1, 0, 0));
+    s = sub(s, mul(of, v(0, -1, 1, 0)));
+    s = sub(s, mul(of, v(0, 0, 0, 0)));
+    s = add(s, mul(of, v(0, 0, 1, 0)));
+    s = sub(s, mul(of, v(1, -1, 0, 0)));
+    s = sub(s, mul(of, v(1, 0, 0, -1)));
+    s = add(s, mul(dg, v(1, 0, 0, 0)));
+    s = sub(s, mul(of, v(1, 0, 0, 1)));
+    s = sub(s, mul(of, v(1, 1, 0, 0)));
+    s = add(s, mul(of, v(2, 0, 0, -1)));
+    s = sub(s, mul(of, v(2, 0, 0, 0)));
+    s = sub(s, mul(of, v(2, 0, 1, -1)));
+    s = add(s, mul(of, v(2, 0, 1, 0)));
+  } else {
+    s = mul(of, v(0, -1, 0, 0));
+    s = sub(s, mul(of, v(0, -1, 0, 1)));
+    s = sub(s, mul(of, v(0, 0, 0, 0)));
+    s = add(s, mul(of, v(0, 0, 0, 1)));
+    s = add(s, mul(of, v(1, 0, -1, 0)));
+    s = sub(s, mul(of, v(1, 0, -1, 1)));
+    s = sub(s, mul(of, v(1, 0, 0, 0)));
+    s = add(s, mul(of, v(1, 0, 0, 1)));
+    s = sub(s, mul(of, v(2, -1, 0, 0)));
+    s = sub(s, mul(of, v(2, 0, -1, 0)));
+    s = add(s, mul(dg, v(2, 0, 0, 0)));
+    s = sub(s, mul(of, v(2, 0, 1, 0)));
+    s = sub(s, mul(of, v(2, 1, 0, 0)));
+  }
+  return s;
+}
+
+__device__ __forceinline__ int stage_of(int q) { return (q + NST) % NST; }  // q >= -1
+
+// One brick of K1 (mode kK1) or of the initial residual r = b - A x0 (mode
+// kInit: the marched field is x0, staged from tm_x).  Uniform per CTA.
+enum { kInit = 0, kK1 = 1 };
+
+struct MarchCtx {
+  Stage *st;
+  uint64_t *bars;
+  uint32_t ph;  // per-stage mbarrier parity (identical in every thread)
+};
+
+template <int MODE, class ROW>
+__device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, const CUtensorMap *mr,
+                                          const CUtensorMap *mp, bool first, double beta, double alpha_prev,
+                                          double *pnew, int i0, int i1, int j0, int k0, ROW row) {
+  const StencilPcgArgs &a = A.a;
+  const BrickGeo &g = A.g;
+  const Lay &L = a.L;
+  const int tid = threadIdx.x, ty = tid >> 5, tx = tid & 31;
+  const int j = j0 + ty, k = k0 + tx;
+  const bool own_ok = j < g.ny && k < g.nz;
+  const int s_own = (ty + 1) * HK + (tx + 1);
+  const int64_t pos_own = L.off + (int64_t)j * L.Sj + k;
+  const bool with_p = (MODE == kK1) && !first;
+  const uint32_t bytes = (with_p ? 6u : 3u) * HP * 8u;
+  // halo slot converted by this thread (threads 0..NHALO-1), besides its own
+  int hs = -1;
+  if (tid < NHALO) {
+    int hj, hk;
+    if (tid < HK) { hj = 0; hk = tid; }
+    else if (tid < 2 * HK) { hj = TJ + 1; hk = tid - HK; }
+    else if (tid < 2 * HK + TJ) { hj = 1 + (tid - 2 * HK); hk = 0; }
+    else { hj = 1 + (tid - 2 * HK - TJ); hk = TK + 1; }
+    hs = hj * HK + hk;
+  }
+  const double inv = a.inv;
+  const bool jac = a.use_jac != 0;
+  const uint32_t *mask = a.mask;
+  double *x = a.x;
+
+  auto issue = [&](int q) {
+    if (tid == 0) {
+      const int s = stage_of(q);
+      fence_proxy_async_smem();
+      mbar_expect_tx(&mc.bars[s], bytes);
+#pragma unroll
+      // box origin (k0-1, j0-1, q) in node coordinates = (k0, j0, q+1) in the
+      // guard-shifted map: never negative
+      for (int c = 0; c < 3; ++c) tma_load_4d(mc.st[s].r[c], mr, &mc.bars[s], k0, j0, q + 1, c);
+      if (with_p) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) tma_load_4d(mc.st[s].p[c], mp, &mc.bars[s], k0, j0, q + 1, c);
+      }
+    }
+  };
+  auto convert = [&](int q, bool own_plane) {
+    const int s = stage_of(q);
+    // own-plane x values are loaded before waiting so the latency overlaps
+    double xo[3] = {0.0, 0.0, 0.0};
+    const bool do_own = MODE == kK1 && own_plane && own_ok;
+    const int64_t qb = (int64_t)q * L.Si;
+    if (do_own && !first) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) xo[c] = x[c * L.C + qb + pos_own];
+    }
+    mbar_wait(&mc.bars[s], (mc.ph >> s) & 1u);
+    mc.ph ^= (1u << s);
+    if (MODE == kInit) return;  // the staged x0 is used as is
+    Stage &S = mc.st[s];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double rq = S.r[c][s_own];
+      const double z = jac ? mul(inv, rq) : rq;
+      double pv = z;
+      if (!first) {
+        const double po = S.p[c][s_own];
+        pv = add(z, mul(beta, po));
+        if (do_own) {
+          const int64_t e = c * L.C + qb + pos_own;
+          if ((mask[e >> 5] >> (e & 31)) & 1u) x[e] = add(xo[c], mul(alpha_prev, po));
+        }
+      }
+      S.r[c][s_own] = pv;
+      if (do_own) {
+        const int64_t e = c * L.C + qb + pos_own;
+        if ((mask[e >> 5] >> (e & 31)) & 1u) pnew[e] = pv;
+      }
+    }
+    if (hs >= 0) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double rq = S.r[c][hs];
+        const double z = jac ? mul(inv, rq) : rq;
+        S.r[c][hs] = first ? z : add(z, mul(beta, S.p[c][hs]));
+      }
+    }
+  };
+
+  // prologue: planes i0-1 .. i0+2 in flight, convert i0-1 and i0
+  const int last = i1;  // planes i0-1 .. i1 are needed
+  for (int q = i0 - 1; q <= i0 + 2 && q <= last; ++q) issue(q);
+  convert(i0 - 1, false);
+  convert(i0, true);
+  for (int i = i0; i < i1; ++i) {
+    convert(i + 1, i + 1 < i1);
+    __syncthreads();
+    if (i + 3 <= last) issue(i + 3);  // into the stage of plane i-2: free after this barrier
+    if (own_ok) {
+      const int64_t qb = (int64_t)i * L.Si;
+      const int sm1 = stage_of(i - 1), s0 = stage_of(i), sp1 = stage_of(i + 1);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        row(c, c * L.C + qb + pos_own, [&](int cc, int di, int dj, int dk) {
+          const int s = di < 0 ? sm1 : (di == 0 ? s0 : sp1);
+          return mc.st[s].r[cc][s_own + dj * HK + dk];
+        });
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// flat 16-byte vectorised grid-stride helper over pairs of padded entries
+template <class F>
+__device__ __forceinline__ void flat_pairs(int64_t total, F f) {
+  const int64_t npair = total >> 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; p + 3 * stride < npair; p += 4 * stride) f(p, stride, 4);
+  for (; p < npair; p += stride) f(p, stride, 1);
+}
+
+__global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constant__ TmaPcgArgs A) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t bars[NST];
+  __shared__ double red[3 * kWarps];
+  __shared__ double tot[4];
+  const StencilPcgArgs &a = A.a;
+  const BrickGeo &g = A.g;
+  const int G = gridDim.x;
+  const Lay &L = a.L;
+  const uint32_t *__restrict__ mask = a.mask;
+  const double dg = a.dg, of = a.of, inv = a.inv;
+  const bool jac = a.use_jac != 0;
+  double *x = a.x, *r = a.r, *ap = a.ap;
+  const double *b = a.b;
+  const int x0_mode = a.x0_mode_dev ? *a.x0_mode_dev : a.x0_mode;
+  if (a.err_word && *((volatile const unsigned int *)a.err_word)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      PcgOut o{};
+      o.status = 99;
+      *a.out = o;
+    }
+    return;
+  }
+  MarchCtx mc;
+  mc.st = reinterpret_cast<Stage *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.bars = bars;
+  mc.ph = 0u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto is_active = [&](int64_t e) { return (mask[e >> 5] >> (e & 31)) & 1u; };
+
+  // ---- initial residual (krylov.py:209-218) ----
+  double v3[3] = {0.0, 0.0, 0.0};
+  if (x0_mode == 1) {
+    for (int bi = blockIdx.x; bi < g.nbricks; bi += G) {
+      int i0, i1, j0, k0;
+      brick_of(g, bi, i0, i1, j0, k0);
+      march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, nullptr, i0, i1, j0, k0,
+                       [&](int c, int64_t e, auto V) {
+                         if (!is_active(e)) return;
+                         const double bv = b[e];
+                         const double rv = sub(bv, stencil3(c, dg, of, V));
+                         r[e] = rv;
+                         const double z = jac ? mul(inv, rv) : rv;
+                         v3[0] = add(v3[0], mul(bv, bv));
+                         v3[1] = add(v3[1], mul(rv, rv));
+                         v3[2] = add(v3[2], mul(rv, z));
+                       });
+    }
+  } else {
+    flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
+      double2 bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (u < n) bv[u] = reinterpret_cast<const double2 *>(b)[p + u * stride];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (u < n) {
+          reinterpret_cast<double2 *>(x)[p + u * stride] = make_double2(0.0, 0.0);
+          reinterpret_cast<double2 *>(r)[p + u * stride] = bv[u];
+          const double z0 = jac ? mul(inv, bv[u].x) : bv[u].x, z1 = jac ? mul(inv, bv[u].y) : bv[u].y;
+          v3[0] = add(v3[0], mul(bv[u].x, bv[u].x));
+          v3[0] = add(v3[0], mul(bv[u].y, bv[u].y));
+          v3[2] = add(v3[2], mul(bv[u].x, z0));
+          v3[2] = add(v3[2], mul(bv[u].y, z1));
+        }
+    });
+    v3[1] = v3[0];
+  }
+  block_sum<3>(v3, red);
+  if (threadIdx.x == 0) {
+    a.partials[0 * G + blockIdx.x] = v3[0];
+    a.partials[1 * G + blockIdx.x] = v3[1];
+    a.partials[2 * G + blockIdx.x] = v3[2];
+  }
+  int status = MQ_OK, iters = 0, converged = 0;
+  double rel = 0.0, bnorm = 0.0, alpha = 0.0, rz = 0.0;
+  bool pold_is_a = true;  // pold = pa, pnew = pb
+  int applies = (x0_mode == 2) ? 0 : 1;
+  if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
+  if (threadIdx.x == 0) fence_proxy_async_global();
+  {
+    double s3[3];
+    grid_partials_sum<3>(a.partials, G, s3, tot);
+    bnorm = sqrt(s3[0]);
+    const double target = fmax(a.rel_tol * bnorm, a.abs_tol);
+    double rnorm = sqrt(s3[1]);
+    rz = jac ? s3[2] : s3[1];
+    auto relf = [&](double res) { return bnorm > 0.0 ? res / bnorm : (res == 0.0 ? 0.0 : INFINITY); };
+    if (rnorm <= target) { converged = 1; rel = relf(rnorm); goto done; }
+    double beta = 0.0, alpha_prev = 0.0;
+    bool first = true;
+    for (int it = 1; it <= a.max_iter; ++it) {
+      double *pnew = pold_is_a ? a.pb : a.pa;
+      const CUtensorMap *mp = pold_is_a ? &A.tm_pa : &A.tm_pb;
+      // ---- K1 ----
+      double v1[1] = {0.0};
+      for (int bi = blockIdx.x; bi < g.nbricks; bi += G) {
+        int i0, i1, j0, k0;
+        brick_of(g, bi, i0, i1, j0, k0);
+        march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, pnew, i0, i1, j0, k0,
+                       [&](int c, int64_t e, auto V) {
+                         if (!is_active(e)) return;
+                         const double av = stencil3(c, dg, of, V);
+                         ap[e] = av;
+                         v1[0] = add(v1[0], mul(V(c, 0, 0, 0), av));
+                       });
+      }
+      block_sum<1>(v1, red);
+      if (threadIdx.x == 0) a.partials[3 * G + blockIdx.x] = v1[0];
+      ++applies;
+      if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
+      double s1[1];
+      grid_partials_sum<1>(a.partials + 3 * G, G, s1, tot);
+      const double pap = s1[0];
+      if (!isfinite(pap) || pap <= 0.0) { status = MQ_INDEFINITE; iters = it; goto done; }
+      alpha = rz / pap;
+      // ---- K2: r -= alpha Ap (flat, all padded entries; non-dofs stay 0) ----
+      double v2[2] = {0.0, 0.0};
+      flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
+        double2 rv[4], av[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < n) {
+            rv[u] = reinterpret_cast<const double2 *>(r)[p + u * stride];
+            av[u] = reinterpret_cast<const double2 *>(ap)[p + u * stride];
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < n) {
+            const double r0 = sub(rv[u].x, mul(alpha, av[u].x));
+            const double r1 = sub(rv[u].y, mul(alpha, av[u].y));
+            reinterpret_cast<double2 *>(r)[p + u * stride] = make_double2(r0, r1);
+            const double z0 = jac ? mul(inv, r0) : r0, z1 = jac ? mul(inv, r1) : r1;
+            v2[0] = add(v2[0], mul(r0, r0));
+            v2[0] = add(v2[0], mul(r1, r1));
+            v2[1] = add(v2[1], mul(r0, z0));
+            v2[1] = add(v2[1], mul(r1, z1));
+          }
+      });
+      block_sum<2>(v2, red);
+      if (threadIdx.x == 0) {
+        a.partials[4 * G + blockIdx.x] = v2[0];
+        a.partials[5 * G + blockIdx.x] = v2[1];
+      }
+      if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
+      if (threadIdx.x == 0) fence_proxy_async_global();
+      double s2[2];
+      grid_partials_sum<2>(a.partials + 4 * G, G, s2, tot);
+      rnorm = sqrt(s2[0]);
+      iters = it;
+      rel = relf(rnorm);
+      const double rz_new = jac ? s2[1] : s2[0];
+      if (rnorm <= target) { converged = 1; break; }
+      if (!isfinite(rz_new)) { status = MQ_INDEFINITE; break; }
+      beta = rz_new / rz;
+      rz = rz_new;
+      alpha_prev = alpha;
+      first = false;
+      pold_is_a = !pold_is_a;
+    }
+    if (status == MQ_OK) {
+      // last direction: p_new of the last iteration (swapped into pold when
+      // the budget ran out)
+      const double *pdir = converged ? (pold_is_a ? a.pb : a.pa) : (pold_is_a ? a.pa : a.pb);
+      flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
+        double2 xv[4], pv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < n) {
+            xv[u] = reinterpret_cast<const double2 *>(x)[p + u * stride];
+            pv[u] = reinterpret_cast<const double2 *>(pdir)[p + u * stride];
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < n)
+            reinterpret_cast<double2 *>(x)[p + u * stride] =
+                make_double2(add(xv[u].x, mul(alpha, pv[u].x)), add(xv[u].y, mul(alpha, pv[u].y)));
+      });
+      if (!converged) status = MQ_NOT_CONVERGED;
+    }
+  }
+done:
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    PcgOut o;
+    o.iterations = iters;
+    o.converged = converged;
+    o.status = status;
+    o.applies = applies;
+    o.rel = rel;
+    o.bnorm = bnorm;
+    o.alpha = alpha;
+    o.rz = rz;
+    *a.out = o;
+  }
+}
+
+// K_n SpMV through the same TMA march (y on active rows only).
+__global__ void __launch_bounds__(kBlock, 2) kn_apply_tma_kernel(const __grid_constant__ TmaPcgArgs A,
+                                                                 double *__restrict__ y) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t bars[NST];
+  MarchCtx mc;
+  mc.st = reinterpret_cast<Stage *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.bars = bars;
+  mc.ph = 0u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t *mask = A.a.mask;
+  for (int bi = blockIdx.x; bi < A.g.nbricks; bi += gridDim.x) {
+    int i0, i1, j0, k0;
+    brick_of(A.g, bi, i0, i1, j0, k0);
+    march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, nullptr, i0, i1, j0, k0,
+                     [&](int c, int64_t e, auto V) {
+                       if ((mask[e >> 5] >> (e & 31)) & 1u) y[e] = stencil3(c, A.a.dg, A.a.of, V);
+                     });
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int get_encoder() {
+  if (g_encode) return MQ_OK;
+  cudaDriverEntryPointQueryResult q;
+  void *fn = nullptr;
+  MQ_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (q != cudaDriverEntryPointSuccess || !fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return MQ_CUDA_ERROR;
+  }
+  g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  return MQ_OK;
+}
+
+// 4-D view (k, j, i, c) of a padded device vector including the guard layer
+// (coordinate 0 = node -1); box = tile + 1-node halo.
+int make_vec_map(const Lay &L, int nx, int ny, int nz, const double *base, CUtensorMap *map) {
+  int rc = get_encoder();
+  if (rc) return rc;
+  cuuint64_t dims[4] = {(cuuint64_t)nz + 2, (cuuint64_t)ny + 2, (cuuint64_t)nx + 2, 3};
+  cuuint64_t strides[3] = {(cuuint64_t)L.Sj * 8, (cuuint64_t)L.Si * 8, (cuuint64_t)L.C * 8};
+  cuuint32_t box[4] = {HK, HJ, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  // the map starts at node (-1,-1,-1) of component 0: index off - Si - Sj - 1 = 0
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return MQ_CUDA_ERROR;
+  }
+  return MQ_OK;
+}
+
+static BrickGeo make_geo(int nx, int ny, int nz, int resident) {
+  BrickGeo g;
+  g.nx = nx;
+  g.ny = ny;
+  g.nz = nz;
+  g.tiles_k = (nz + TK - 1) / TK;
+  g.tiles_j = (ny + TJ - 1) / TJ;
+  const int tiles = g.tiles_k * g.tiles_j;
+  int chunks = resident / tiles;
+  if (chunks < 1) chunks = 1;
+  if (chunks > nx) chunks = nx;
+  g.chunks = chunks;
+  g.nbricks = tiles * chunks;
+  return g;
+}
+
+int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int *grid, BrickGeo *geo) {
+  (void)L;
+  int dev = 0, sms = 0, per = 0;
+  MQ_CUDA(cudaGetDevice(&dev));
+  MQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  MQ_CUDA(cudaFuncSetAttribute(pcg_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+  MQ_CUDA(cudaFuncSetAttribute(kn_apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+  MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pcg_tma_kernel, kBlock, kTmaSmem));
+  if (per < 1) { set_error("TMA PCG kernel cannot be resident"); return MQ_CUDA_ERROR; }
+  const int resident = sms * per;
+  *geo = make_geo(nx, ny, nz, resident);
+  *grid = geo->nbricks < resident ? geo->nbricks : resident;
+  return MQ_OK;
+}
+
+int launch_pcg_brick(const StencilPcgArgs &args, const BrickGeo &geo, int grid, cudaStream_t s) {
+  TmaPcgArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.a = args;
+  A.g = geo;
+  const Lay &L = args.L;
+  int rc = make_vec_map(L, geo.nx, geo.ny, geo.nz, args.r, &A.tm_r);
+  rc = rc ? rc : make_vec_map(L, geo.nx, geo.ny, geo.nz, args.pa, &A.tm_pa);
+  rc = rc ? rc : make_vec_map(L, geo.nx, geo.ny, geo.nz, args.pb, &A.tm_pb);
+  rc = rc ? rc : make_vec_map(L, geo.nx, geo.ny, geo.nz, args.x, &A.tm_x);
+  if (rc) return rc;
+  void *params[] = {&A};
+  MQ_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_tma_kernel, dim3(grid), dim3(kBlock), params, kTmaSmem, s));
+  return MQ_OK;
+}
+
+int launch_kn_apply_brick(const Lay &L, const BrickGeo &geo, const uint32_t *mask, double dg, double of,
+                          const double *x, double *y, int sms, cudaStream_t s) {
+  TmaPcgArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.a.L = L;
+  A.a.mask = mask;
+  A.a.dg = dg;
+  A.a.of = of;
+  A.g = geo;
+  int rc = make_vec_map(L, geo.nx, geo.ny, geo.nz, x, &A.tm_x);
+  if (rc) return rc;
+  const int grid = geo.nbricks < sms * 2 ? geo.nbricks : sms * 2;
+  kn_apply_tma_kernel<<<grid, kBlock, kTmaSmem, s>>>(A, y);
+  MQ_CUDA(cudaGetLastError());
+  return MQ_OK;
+}
+
+}  // namespace mq

@@ -1038,7 +1038,7 @@ static int solve_enqueue(mq_ctx *ctx, int fam, const double *rhs, double *y) {
   a.err_word = &s->d_run->err;
   const bool timed = ctx->pcg_timing && ctx->ev_n < kEvPool;
   if (timed) MQ_CUDA(cudaEventRecordWithFlags(ctx->ev_pool[2 * ctx->ev_n], ctx->stream, cudaEventRecordExternal));
-  rc = launch_pcg_stencil(a, ctx->pcg_grid, ctx->stream);
+  rc = launch_pcg_ctx(ctx, a);
   if (rc) return rc;
   if (timed) {
     MQ_CUDA(cudaEventRecordWithFlags(ctx->ev_pool[2 * ctx->ev_n + 1], ctx->stream, cudaEventRecordExternal));

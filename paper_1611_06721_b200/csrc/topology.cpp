@@ -64,9 +64,15 @@ int build_topology(const mq_grid_desc &g, Topology &t, std::string &err) {
   d.n_fz = (int64_t)nx * ny * (nz + 1);
   t.nx = nx; t.ny = ny; t.nz = nz;
   Lay &L = t.L;
-  L.Sj = nz + 1;
-  L.Si = (int64_t)(ny + 1) * (nz + 1);
-  const int64_t P = (int64_t)(nx + 1) * L.Si;
+  // One guard node on the low side of every axis (node index -1), so that
+  // tile + halo boxes never start at a negative TMA coordinate, and the
+  // k-pitch rounded up to even so that every row starts 16-byte aligned (TMA
+  // global strides must be multiples of 16 B).  Guard / pad entries are never
+  // dofs and hold 0.
+  L.Sj = (nz + 3) & ~1;
+  L.Si = (int64_t)(ny + 2) * L.Sj;
+  L.off = L.Si + L.Sj + 1;
+  const int64_t P = (int64_t)(nx + 2) * L.Si;
   L.C = (P + 31) / 32 * 32;
   L.total = 3 * L.C;
   L.words = L.total / 32;
@@ -131,7 +137,7 @@ int build_topology(const mq_grid_desc &g, Topology &t, std::string &err) {
             gid = gid_z(d, i, j, k);
           }
           if (boundary) continue;
-          const int64_t e = c * L.C + i * L.Si + j * L.Sj + k;
+          const int64_t e = c * L.C + L.off + i * L.Si + j * L.Sj + k;
           if (conducting) {
             pad2cond[e] = (int32_t)t.c_global.size();
             t.c_global.push_back(gid);
@@ -153,7 +159,7 @@ int build_topology(const mq_grid_desc &g, Topology &t, std::string &err) {
   // Each face is described by padded indices of its 4 edges in the
   // reference's listing order with signs (+,+,-,-).
   const int64_t C = L.C, Si = L.Si, Sj = L.Sj;
-  auto pidx = [&](int c, int i, int j, int k) -> int64_t { return c * C + i * Si + j * Sj + k; };
+  auto pidx = [&](int c, int i, int j, int k) -> int64_t { return c * C + L.off + i * Si + j * Sj + k; };
   auto face_edges = [&](int dir, int i, int j, int k, int64_t out[4]) {
     if (dir == 0) {        // fx(i,j,k): +ey[i,j,k], +ez[i,j+1,k], -ey[i,j,k+1], -ez[i,j,k]
       out[0] = pidx(1, i, j, k); out[1] = pidx(2, i, j + 1, k);

@@ -1,0 +1,60 @@
+"""Profiling driver: one fused-PCG solve on a BASELINE config grid.
+
+    python tools/profile_pcg.py --config 2 --iters 20 [--kernel brick|simple]
+
+Runs a warm-up solve, then one solve capped at --iters iterations (so an ncu
+replay stays short), and prints the CUDA-event time per iteration.
+"""
+import argparse
+import ctypes
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--kernel", default=os.environ.get("MQ_PCG_KERNEL", "brick"))
+    ap.add_argument("--spmv", action="store_true", help="also time K_n SpMV launches")
+    args = ap.parse_args()
+    os.environ["MQ_PCG_KERNEL"] = args.kernel
+    from paper_1611_06721_b200 import _lib, configs as C
+    from paper_1611_06721_b200._lib import check
+    from paper_1611_06721_b200.device import DeviceGrid
+    prob = C.make_problem(args.config)
+    g = DeviceGrid(prob)
+    lib = g.lib
+    b, x = g.alloc(), g.alloc()
+    g.upload(prob.pattern, b)
+    rep = _lib.SolveReportC()
+    rc = lib.mq_pcg_solve_dev(g.ctx, ctypes.c_void_p(b), None, ctypes.c_void_p(x), 1e-8, 0.0,
+                              args.iters, 1, ctypes.byref(rep))
+    check(rc, allow=(0, 1))
+    check(lib.mq_pcg_stats(g.ctx, None, None, None, 1))
+    rc = lib.mq_pcg_solve_dev(g.ctx, ctypes.c_void_p(b), None, ctypes.c_void_p(x), 1e-8, 0.0,
+                              args.iters, 1, ctypes.byref(rep))
+    check(rc, allow=(0, 1))
+    ms, it = ctypes.c_double(), ctypes.c_int64()
+    check(lib.mq_pcg_stats(g.ctx, ctypes.byref(ms), ctypes.byref(it), None, 0))
+    n = g.n_n
+    gbs = 72.0 * n * rep.iterations / (ms.value * 1e-3) / 1e9
+    print(f"config {args.config} kernel={args.kernel} n_n={n} iters={rep.iterations} "
+          f"time={ms.value:.3f} ms  {1000*ms.value/max(rep.iterations,1):.1f} us/it  "
+          f"{gbs:.0f} GB/s (72 B/dof/it)")
+    if args.spmv:
+        y = g.alloc()
+        lib.mq_timer_start(g.ctx)
+        for _ in range(20):
+            check(lib.mq_kn_apply_dev(g.ctx, ctypes.c_void_p(b), ctypes.c_void_p(y)))
+        t = ctypes.c_double()
+        lib.mq_timer_stop(g.ctx, ctypes.byref(t))
+        print(f"kn_apply: {1000*t.value/20:.1f} us  ({16.0*n/(t.value/20*1e-3)/1e9:.0f} GB/s at 16 B/dof)")
+    g.close()
+
+
+if __name__ == "__main__":
+    main()
