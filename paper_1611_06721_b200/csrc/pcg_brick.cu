@@ -201,19 +201,32 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       }
     }
   };
-  auto convert = [&](int q, bool own_plane) {
+  // returns the active-dof bits (bit c = component c) of the own position
+  auto convert = [&](int q, bool own_plane) -> uint32_t {
     const int s = stage_of(q);
-    // own-plane x values are loaded before waiting so the latency overlaps
+    // own-plane mask words and x values are loaded before waiting on the
+    // stage so their latency overlaps the TMA transfer
     double xo[3] = {0.0, 0.0, 0.0};
-    const bool do_own = MODE == kK1 && own_plane && own_ok;
+    uint32_t mw[3] = {0u, 0u, 0u};
+    const bool do_own = own_plane && own_ok;
     const int64_t qb = (int64_t)q * L.Si;
-    if (do_own && !first) {
+    if (do_own) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) xo[c] = x[c * L.C + qb + pos_own];
+      for (int c = 0; c < 3; ++c) {
+        const int64_t e = c * L.C + qb + pos_own;
+        mw[c] = __ldg(mask + (e >> 5));
+        if (MODE == kK1 && !first) xo[c] = x[e];
+      }
     }
     mbar_wait(&mc.bars[s], (mc.ph >> s) & 1u);
     mc.ph ^= (1u << s);
-    if (MODE == kInit) return;  // the staged x0 is used as is
+    uint32_t act = 0u;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int64_t e = c * L.C + qb + pos_own;
+      act |= ((mw[c] >> (e & 31)) & 1u) << c;
+    }
+    if (MODE == kInit) return act;  // the staged x0 is used as is
     Stage &S = mc.st[s];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -223,16 +236,10 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       if (!first) {
         const double po = S.p[c][s_own];
         pv = add(z, mul(beta, po));
-        if (do_own) {
-          const int64_t e = c * L.C + qb + pos_own;
-          if ((mask[e >> 5] >> (e & 31)) & 1u) x[e] = add(xo[c], mul(alpha_prev, po));
-        }
+        if ((act >> c) & 1u) x[c * L.C + qb + pos_own] = add(xo[c], mul(alpha_prev, po));
       }
       S.r[c][s_own] = pv;
-      if (do_own) {
-        const int64_t e = c * L.C + qb + pos_own;
-        if ((mask[e >> 5] >> (e & 31)) & 1u) pnew[e] = pv;
-      }
+      if ((act >> c) & 1u) pnew[c * L.C + qb + pos_own] = pv;
     }
     if (hs >= 0) {
 #pragma unroll
@@ -242,39 +249,44 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
         S.r[c][hs] = first ? z : add(z, mul(beta, S.p[c][hs]));
       }
     }
+    return act;
   };
 
   // prologue: planes i0-1 .. i0+2 in flight, convert i0-1 and i0
   const int last = i1;  // planes i0-1 .. i1 are needed
   for (int q = i0 - 1; q <= i0 + 2 && q <= last; ++q) issue(q);
   convert(i0 - 1, false);
-  convert(i0, true);
+  uint32_t act = convert(i0, true);
   for (int i = i0; i < i1; ++i) {
-    convert(i + 1, i + 1 < i1);
+    const uint32_t act_next = convert(i + 1, i + 1 < i1);
     __syncthreads();
     if (i + 3 <= last) issue(i + 3);  // into the stage of plane i-2: free after this barrier
-    if (own_ok) {
+    if (act) {
       const int64_t qb = (int64_t)i * L.Si;
       const int sm1 = stage_of(i - 1), s0 = stage_of(i), sp1 = stage_of(i + 1);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        row(c, c * L.C + qb + pos_own, [&](int cc, int di, int dj, int dk) {
-          const int s = di < 0 ? sm1 : (di == 0 ? s0 : sp1);
-          return mc.st[s].r[cc][s_own + dj * HK + dk];
-        });
+        if ((act >> c) & 1u)
+          row(c, c * L.C + qb + pos_own, [&](int cc, int di, int dj, int dk) {
+            const int s = di < 0 ? sm1 : (di == 0 ? s0 : sp1);
+            return mc.st[s].r[cc][s_own + dj * HK + dk];
+          });
       }
     }
+    act = act_next;
   }
   __syncthreads();
 }
 
 // flat 16-byte vectorised grid-stride helper over pairs of padded entries
+constexpr int kUnroll = 8;  // 8 x 16 B loads per stream in flight per thread
+
 template <class F>
 __device__ __forceinline__ void flat_pairs(int64_t total, F f) {
   const int64_t npair = total >> 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; p + 3 * stride < npair; p += 4 * stride) f(p, stride, 4);
+  for (; p + (kUnroll - 1) * stride < npair; p += kUnroll * stride) f(p, stride, kUnroll);
   for (; p < npair; p += stride) f(p, stride, 1);
 }
 
@@ -287,7 +299,6 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
   const BrickGeo &g = A.g;
   const int G = gridDim.x;
   const Lay &L = a.L;
-  const uint32_t *__restrict__ mask = a.mask;
   const double dg = a.dg, of = a.of, inv = a.inv;
   const bool jac = a.use_jac != 0;
   double *x = a.x, *r = a.r, *ap = a.ap;
@@ -310,8 +321,6 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto is_active = [&](int64_t e) { return (mask[e >> 5] >> (e & 31)) & 1u; };
-
   // ---- initial residual (krylov.py:209-218) ----
   double v3[3] = {0.0, 0.0, 0.0};
   if (x0_mode == 1) {
@@ -320,7 +329,6 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       brick_of(g, bi, i0, i1, j0, k0);
       march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, nullptr, i0, i1, j0, k0,
                        [&](int c, int64_t e, auto V) {
-                         if (!is_active(e)) return;
                          const double bv = b[e];
                          const double rv = sub(bv, stencil3(c, dg, of, V));
                          r[e] = rv;
@@ -332,12 +340,12 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
     }
   } else {
     flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
-      double2 bv[4];
+      double2 bv[kUnroll];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < kUnroll; ++u)
         if (u < n) bv[u] = reinterpret_cast<const double2 *>(b)[p + u * stride];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < kUnroll; ++u)
         if (u < n) {
           reinterpret_cast<double2 *>(x)[p + u * stride] = make_double2(0.0, 0.0);
           reinterpret_cast<double2 *>(r)[p + u * stride] = bv[u];
@@ -383,7 +391,6 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
         brick_of(g, bi, i0, i1, j0, k0);
         march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, pnew, i0, i1, j0, k0,
                        [&](int c, int64_t e, auto V) {
-                         if (!is_active(e)) return;
                          const double av = stencil3(c, dg, of, V);
                          ap[e] = av;
                          v1[0] = add(v1[0], mul(V(c, 0, 0, 0), av));
@@ -401,15 +408,15 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       // ---- K2: r -= alpha Ap (flat, all padded entries; non-dofs stay 0) ----
       double v2[2] = {0.0, 0.0};
       flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
-        double2 rv[4], av[4];
+        double2 rv[kUnroll], av[kUnroll];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kUnroll; ++u)
           if (u < n) {
             rv[u] = reinterpret_cast<const double2 *>(r)[p + u * stride];
             av[u] = reinterpret_cast<const double2 *>(ap)[p + u * stride];
           }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kUnroll; ++u)
           if (u < n) {
             const double r0 = sub(rv[u].x, mul(alpha, av[u].x));
             const double r1 = sub(rv[u].y, mul(alpha, av[u].y));
@@ -447,15 +454,15 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       // the budget ran out)
       const double *pdir = converged ? (pold_is_a ? a.pb : a.pa) : (pold_is_a ? a.pa : a.pb);
       flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
-        double2 xv[4], pv[4];
+        double2 xv[kUnroll], pv[kUnroll];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kUnroll; ++u)
           if (u < n) {
             xv[u] = reinterpret_cast<const double2 *>(x)[p + u * stride];
             pv[u] = reinterpret_cast<const double2 *>(pdir)[p + u * stride];
           }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kUnroll; ++u)
           if (u < n)
             reinterpret_cast<double2 *>(x)[p + u * stride] =
                 make_double2(add(xv[u].x, mul(alpha, pv[u].x)), add(xv[u].y, mul(alpha, pv[u].y)));
@@ -492,14 +499,11 @@ __global__ void __launch_bounds__(kBlock, 2) kn_apply_tma_kernel(const __grid_co
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const uint32_t *mask = A.a.mask;
   for (int bi = blockIdx.x; bi < A.g.nbricks; bi += gridDim.x) {
     int i0, i1, j0, k0;
     brick_of(A.g, bi, i0, i1, j0, k0);
     march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, nullptr, i0, i1, j0, k0,
-                     [&](int c, int64_t e, auto V) {
-                       if ((mask[e >> 5] >> (e & 31)) & 1u) y[e] = stencil3(c, A.a.dg, A.a.of, V);
-                     });
+                     [&](int c, int64_t e, auto V) { y[e] = stencil3(c, A.a.dg, A.a.of, V); });
   }
 }
 
