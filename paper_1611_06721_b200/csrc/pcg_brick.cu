@@ -201,30 +201,44 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       }
     }
   };
-  // returns the active-dof bits (bit c = component c) of the own position
-  auto convert = [&](int q, bool own_plane) -> uint32_t {
-    const int s = stage_of(q);
-    // own-plane mask words and x values are loaded before waiting on the
-    // stage so their latency overlaps the TMA transfer
-    double xo[3] = {0.0, 0.0, 0.0};
-    uint32_t mw[3] = {0u, 0u, 0u};
-    const bool do_own = own_plane && own_ok;
-    const int64_t qb = (int64_t)q * L.Si;
-    if (do_own) {
+  // Own-position mask words and x values are software-pipelined one plane
+  // ahead in registers: they are loaded while the previous plane is
+  // processed, so neither their latency nor the TMA's is exposed.
+  uint32_t mw_nx[3] = {0u, 0u, 0u};
+  double xo_nx[3] = {0.0, 0.0, 0.0};
+  auto prefetch_own = [&](int q, bool own_plane) {
+    if (own_plane && own_ok) {
+      const int64_t qb = (int64_t)q * L.Si;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const int64_t e = c * L.C + qb + pos_own;
-        mw[c] = __ldg(mask + (e >> 5));
-        if (MODE == kK1 && !first) xo[c] = x[e];
+        mw_nx[c] = __ldg(mask + (e >> 5));
+        if (MODE == kK1 && !first) xo_nx[c] = x[e];
       }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) mw_nx[c] = 0u;
     }
+  };
+  // returns the active-dof bits (bit c = component c) of the own position;
+  // next_q/next_own describe the plane whose own data is prefetched now
+  auto convert = [&](int q, bool own_plane, int next_q, bool next_own) -> uint32_t {
+    const int s = stage_of(q);
+    uint32_t mw[3];
+    double xo[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { mw[c] = mw_nx[c]; xo[c] = xo_nx[c]; }
+    prefetch_own(next_q, next_own);
+    const int64_t qb = (int64_t)q * L.Si;
     mbar_wait(&mc.bars[s], (mc.ph >> s) & 1u);
     mc.ph ^= (1u << s);
     uint32_t act = 0u;
+    if (own_plane && own_ok) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const int64_t e = c * L.C + qb + pos_own;
-      act |= ((mw[c] >> (e & 31)) & 1u) << c;
+      for (int c = 0; c < 3; ++c) {
+        const int64_t e = c * L.C + qb + pos_own;
+        act |= ((mw[c] >> (e & 31)) & 1u) << c;
+      }
     }
     if (MODE == kInit) return act;  // the staged x0 is used as is
     Stage &S = mc.st[s];
@@ -255,10 +269,10 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   // prologue: planes i0-1 .. i0+2 in flight, convert i0-1 and i0
   const int last = i1;  // planes i0-1 .. i1 are needed
   for (int q = i0 - 1; q <= i0 + 2 && q <= last; ++q) issue(q);
-  convert(i0 - 1, false);
-  uint32_t act = convert(i0, true);
+  convert(i0 - 1, false, i0, true);
+  uint32_t act = convert(i0, true, i0 + 1, i0 + 1 < i1);
   for (int i = i0; i < i1; ++i) {
-    const uint32_t act_next = convert(i + 1, i + 1 < i1);
+    const uint32_t act_next = convert(i + 1, i + 1 < i1, i + 2, i + 2 < i1);
     __syncthreads();
     if (i + 3 <= last) issue(i + 3);  // into the stage of plane i-2: free after this barrier
     if (act) {
