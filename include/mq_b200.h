@@ -221,6 +221,10 @@ int mq_timer_stop(mq_ctx *ctx, double *ms);
 int mq_pcg_stats(mq_ctx *ctx, double *pcg_ms, int64_t *pcg_iterations,
                  int64_t *launches, int32_t enable);
 int mq_kernel_launches(mq_ctx *ctx, int64_t *count);
+/* %globaltimer stamps of the last PCG launch (CTA 0), when the context was
+ * created with MQ_PCG_TRACE set: [start, then per iteration K1 end, barrier
+ * 1 end, K2 end, barrier 2 end] for the first 64 iterations. */
+int mq_pcg_trace(mq_ctx *ctx, uint64_t *stamps, int32_t n);
 int mq_l2_flush(mq_ctx *ctx);
 
 #ifdef __cplusplus

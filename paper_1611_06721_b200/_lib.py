@@ -128,6 +128,7 @@ SIGNATURES = {
     "mq_timer_stop": (I32, [VP, c_double_p]),
     "mq_pcg_stats": (I32, [VP, c_double_p, c_int64_p, c_int64_p, I32]),
     "mq_kernel_launches": (I32, [VP, c_int64_p]),
+    "mq_pcg_trace": (I32, [VP, ctypes.POINTER(ctypes.c_uint64), I32]),
     "mq_l2_flush": (I32, [VP]),
 }
 

@@ -63,6 +63,7 @@ int ctx_pcg(mq_ctx *ctx, const double *b, double *x, int x0_mode, double rel_tol
   a.partials = ctx->d_partials;
   a.bar = ctx->d_bar;
   a.out = ctx->d_out;
+  a.trace = ctx->d_trace;
   if (ctx->pcg_timing) MQ_CUDA(cudaEventRecord(ctx->ev_pcg0, ctx->stream));
   int rc = launch_pcg_ctx(ctx, a);
   if (rc) return rc;
@@ -168,6 +169,7 @@ int mq_ctx_create(const mq_grid_desc *desc, int32_t device, mq_ctx **out) {
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_partials, sizeof(double) * 8 * (size_t)std::max(ctx->pcg_grid, 1024));
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_bar, sizeof(GridBar));
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_out, sizeof(PcgOut));
+  if (!rc && getenv("MQ_PCG_TRACE")) rc = ctx_alloc(ctx, (void **)&ctx->d_trace, sizeof(unsigned long long) * 4 * 64 + 64);
   if (!rc) {
     e = cudaMallocHost((void **)&ctx->h_out, sizeof(PcgOut));
     if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocHost");
@@ -454,6 +456,12 @@ int mq_pcg_stats(mq_ctx *ctx, double *pcg_ms, int64_t *pcg_iterations, int64_t *
     ctx->pcg_iters = 0;
     ctx->pcg_launches = 0;
   }
+  return MQ_OK;
+}
+
+int mq_pcg_trace(mq_ctx *ctx, uint64_t *stamps, int32_t n) {
+  if (!ctx->d_trace) { set_error("PCG tracing disabled (set MQ_PCG_TRACE)"); return MQ_INVALID; }
+  MQ_CUDA(cudaMemcpy(stamps, ctx->d_trace, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
   return MQ_OK;
 }
 

@@ -79,6 +79,7 @@ struct mq_ctx {
   mq::GridBar *d_bar = nullptr;
   mq::PcgOut *d_out = nullptr;
   mq::PcgOut *h_out = nullptr;
+  unsigned long long *d_trace = nullptr;
   int pcg_grid = 1;
   int pcg_variant = 0;        // 0: brick-tiled kernel, 1: thread-per-row kernel
   mq::BrickGeo geo{};

@@ -70,13 +70,30 @@ __device__ __forceinline__ void grid_partials_sum(const double *partials, int G,
 }
 
 // ---- grid-wide barrier (cooperative launch guarantees co-residency) -------
-// Mirrors the cooperative-groups grid sync: CTA barrier, one thread fences
-// and arrives, spins on the generation word, fences again.  A watchdog
-// (5 s on %globaltimer) turns a lost arrival into an error instead of a hang.
+// One release-atomic arrival per CTA on a monotonic 64-bit counter (zeroed
+// before every launch), then acquire-polling until all G CTAs of this
+// barrier instance arrived: barrier k completes when the counter reaches
+// (k+1)*G.  Cumulativity of the release (after the CTA barrier) publishes
+// every thread's writes; the acquire + CTA barrier makes them visible to the
+// whole CTA.  Data produced by other CTAs is read with L2-only loads (ldcg)
+// or TMA, never through a possibly stale L1 line.  A watchdog (5 s on
+// %globaltimer) turns a lost arrival into an error instead of a hang.
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+__device__ __forceinline__ unsigned long long atom_add_release_gpu(unsigned long long *p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.add.release.gpu.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ bool grid_sync(GridBar *bar) {
@@ -84,31 +101,20 @@ __device__ __forceinline__ bool grid_sync(GridBar *bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
     s_fail = 0;
-    if (*((volatile unsigned int *)&bar->error)) s_fail = 1;
-  }
-  __syncthreads();
-  if (s_fail) return false;
-  if (threadIdx.x == 0) {
-    volatile unsigned int *vgen = &bar->gen;
-    const unsigned int g = *vgen;
-    __threadfence();
-    const unsigned int arrived = atomicAdd(&bar->count, 1u);
-    if (arrived == gridDim.x - 1) {
-      atomicExch(&bar->count, 0u);
-      __threadfence();
-      atomicAdd(&bar->gen, 1u);
-    } else {
+    const unsigned long long G = gridDim.x;
+    const unsigned long long old = atom_add_release_gpu(&bar->count, 1ull);
+    const unsigned long long target = (old / G + 1ull) * G;
+    if (ld_acquire_gpu(&bar->count) < target) {
       const uint64_t t0 = globaltimer_ns();
-      while (*vgen == g) {
-        __nanosleep(64);
-        if (globaltimer_ns() - t0 > 5000000000ull) {
+      unsigned spins = 0;
+      while (ld_acquire_gpu(&bar->count) < target) {
+        if ((++spins & 1023u) == 0u && globaltimer_ns() - t0 > 5000000000ull) {
           atomicExch(&bar->error, 1u);
           s_fail = 1;
           break;
         }
       }
     }
-    __threadfence();
     if (*((volatile unsigned int *)&bar->error)) s_fail = 1;
   }
   __syncthreads();

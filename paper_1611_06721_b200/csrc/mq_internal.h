@@ -32,8 +32,7 @@ struct Lay {
 };
 
 struct GridBar {
-  unsigned int count;
-  unsigned int gen;
+  unsigned long long count;  // monotonic arrivals; zeroed before every launch
   unsigned int error;
   unsigned int pad;
 };
@@ -64,6 +63,7 @@ struct StencilPcgArgs {
   PcgOut *out;
   const int *x0_mode_dev;      // optional: device-chosen start mode
   const unsigned int *err_word;  // optional: skip the solve if set
+  unsigned long long *trace;   // optional: %globaltimer stamps (CTA 0) per phase
 };
 
 // Brick decomposition of the node box [0,nx) x [0,ny) x [0,nz) (pcg_brick.cu)

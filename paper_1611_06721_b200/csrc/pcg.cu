@@ -347,6 +347,7 @@ int coop_grid(const void *kernel, int want_blocks, int *out) {
 }
 
 int launch_pcg_stencil(const StencilPcgArgs &args, int grid, cudaStream_t s) {
+  MQ_CUDA(cudaMemsetAsync(&args.bar->count, 0, sizeof(unsigned long long), s));
   StencilPcgArgs a = args;
   void *params[] = {&a};
   MQ_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_stencil_kernel, dim3(grid), dim3(kBlock), params, 0, s));
@@ -360,6 +361,7 @@ int pcg_stencil_grid(int64_t words, int *out) {
 }
 
 int launch_pcg_csr(const CsrPcgArgs &args, int grid, cudaStream_t s) {
+  MQ_CUDA(cudaMemsetAsync(&args.bar->count, 0, sizeof(unsigned long long), s));
   CsrPcgArgs a = args;
   void *params[] = {&a};
   MQ_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_csr_kernel, dim3(grid), dim3(kBlock), params, 0, s));

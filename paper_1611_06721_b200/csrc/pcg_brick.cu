@@ -21,6 +21,7 @@
 // Streams per iteration (fp64, per dof): K1 reads r, p_old, x and writes
 // x, p_new, Ap; K2 reads r, Ap and writes r  ->  9 x 8 B = 72 B.
 #include <cuda.h>
+#include <cstdlib>
 #include <cstring>
 #include <cudaTypedefs.h>
 
@@ -213,7 +214,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       for (int c = 0; c < 3; ++c) {
         const int64_t e = c * L.C + qb + pos_own;
         mw_nx[c] = __ldg(mask + (e >> 5));
-        if (MODE == kK1 && !first) xo_nx[c] = x[e];
+        if (MODE == kK1 && !first) xo_nx[c] = __ldcg(x + e);
       }
     } else {
 #pragma unroll
@@ -335,6 +336,11 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  unsigned long long *trace = (blockIdx.x == 0 && threadIdx.x == 0) ? a.trace : nullptr;
+  auto stamp = [&](int slot) {
+    if (trace && slot < 4 * 64 + 1) trace[slot] = globaltimer_ns();
+  };
+  stamp(0);
   // ---- initial residual (krylov.py:209-218) ----
   double v3[3] = {0.0, 0.0, 0.0};
   if (x0_mode == 1) {
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       brick_of(g, bi, i0, i1, j0, k0);
       march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, nullptr, i0, i1, j0, k0,
                        [&](int c, int64_t e, auto V) {
-                         const double bv = b[e];
+                         const double bv = __ldcg(b + e);
                          const double rv = sub(bv, stencil3(c, dg, of, V));
                          r[e] = rv;
                          const double z = jac ? mul(inv, rv) : rv;
@@ -357,7 +363,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       double2 bv[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u)
-        if (u < n) bv[u] = reinterpret_cast<const double2 *>(b)[p + u * stride];
+        if (u < n) bv[u] = __ldcg(reinterpret_cast<const double2 *>(b) + p + u * stride);
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u)
         if (u < n) {
@@ -413,7 +419,9 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       block_sum<1>(v1, red);
       if (threadIdx.x == 0) a.partials[3 * G + blockIdx.x] = v1[0];
       ++applies;
+      stamp(4 * (it - 1) + 1);
       if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
+      stamp(4 * (it - 1) + 2);
       double s1[1];
       grid_partials_sum<1>(a.partials + 3 * G, G, s1, tot);
       const double pap = s1[0];
@@ -426,8 +434,8 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
           if (u < n) {
-            rv[u] = reinterpret_cast<const double2 *>(r)[p + u * stride];
-            av[u] = reinterpret_cast<const double2 *>(ap)[p + u * stride];
+            rv[u] = __ldcg(reinterpret_cast<const double2 *>(r) + p + u * stride);
+            av[u] = __ldcg(reinterpret_cast<const double2 *>(ap) + p + u * stride);
           }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
@@ -447,7 +455,9 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
         a.partials[4 * G + blockIdx.x] = v2[0];
         a.partials[5 * G + blockIdx.x] = v2[1];
       }
+      stamp(4 * (it - 1) + 3);
       if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
+      stamp(4 * (it - 1) + 4);
       if (threadIdx.x == 0) fence_proxy_async_global();
       double s2[2];
       grid_partials_sum<2>(a.partials + 4 * G, G, s2, tot);
@@ -472,8 +482,8 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
           if (u < n) {
-            xv[u] = reinterpret_cast<const double2 *>(x)[p + u * stride];
-            pv[u] = reinterpret_cast<const double2 *>(pdir)[p + u * stride];
+            xv[u] = __ldcg(reinterpret_cast<const double2 *>(x) + p + u * stride);
+            pv[u] = __ldcg(reinterpret_cast<const double2 *>(pdir) + p + u * stride);
           }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
@@ -584,6 +594,10 @@ int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int *grid, BrickGeo *g
   MQ_CUDA(cudaFuncSetAttribute(kn_apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
   MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pcg_tma_kernel, kBlock, kTmaSmem));
   if (per < 1) { set_error("TMA PCG kernel cannot be resident"); return MQ_CUDA_ERROR; }
+  if (const char *v = getenv("MQ_BRICK_CTAS_PER_SM")) {
+    const int want = atoi(v);
+    if (want >= 1 && want < per) per = want;
+  }
   const int resident = sms * per;
   *geo = make_geo(nx, ny, nz, resident);
   *grid = geo->nbricks < resident ? geo->nbricks : resident;
@@ -601,6 +615,7 @@ int launch_pcg_brick(const StencilPcgArgs &args, const BrickGeo &geo, int grid, 
   rc = rc ? rc : make_vec_map(L, geo.nx, geo.ny, geo.nz, args.pb, &A.tm_pb);
   rc = rc ? rc : make_vec_map(L, geo.nx, geo.ny, geo.nz, args.x, &A.tm_x);
   if (rc) return rc;
+  MQ_CUDA(cudaMemsetAsync(&args.bar->count, 0, sizeof(unsigned long long), s));
   void *params[] = {&A};
   MQ_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_tma_kernel, dim3(grid), dim3(kBlock), params, kTmaSmem, s));
   return MQ_OK;

@@ -45,6 +45,17 @@ def main():
     print(f"config {args.config} kernel={args.kernel} n_n={n} iters={rep.iterations} "
           f"time={ms.value:.3f} ms  {1000*ms.value/max(rep.iterations,1):.1f} us/it  "
           f"{gbs:.0f} GB/s (72 B/dof/it)")
+    if os.environ.get("MQ_PCG_TRACE"):
+        import numpy as np
+        st = np.zeros(4 * 64 + 1, dtype=np.uint64)
+        check(lib.mq_pcg_trace(g.ctx, st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), st.size))
+        n = min(64, rep.iterations)
+        s = st[1:4 * n + 1].reshape(n, 4).astype(np.float64)
+        prev = np.concatenate([[float(st[0])], s[:-1, 3]])
+        k1, b1, k2, b2 = s[:, 0] - prev, s[:, 1] - s[:, 0], s[:, 2] - s[:, 1], s[:, 3] - s[:, 2]
+        print(f"  per-iteration us (CTA 0, iterations 2..{n}): K1 {k1[1:].mean()/1e3:.2f}  barrier1 "
+              f"{b1[1:].mean()/1e3:.2f}  K2 {k2[1:].mean()/1e3:.2f}  barrier2 {b2[1:].mean()/1e3:.2f}  "
+              f"(init {k1[0]/1e3:.2f})")
     if args.spmv:
         y = g.alloc()
         lib.mq_timer_start(g.ctx)
