@@ -67,6 +67,7 @@ struct SolverHost {
   bool graph_ok = true;
   int64_t launches_per_step = 0;
   bool recover_every_step = true;
+  int kb = 32;  // compile-time basis bound used for the tall-skinny kernels
   int per_step = 4;
   int64_t n_planned = 0, n_enqueued = 0;
 };
@@ -128,80 +129,164 @@ __device__ __forceinline__ void last_block_reduce(double *acc, int nq, double *p
        w_ += (int64_t)gridDim.x * kWarps)                                                    \
     if (((mask)[w_] >> (threadIdx.x & 31)) & 1u)
 
+// Flat passes over pairs of padded entries: every device vector is 0 off the
+// partition, so dots and linear combinations need no mask (the outputs stay
+// 0 there).  KB bounds the number of basis vectors (compile-time register
+// budget), UN pairs per thread are in flight per stream.
+template <int KB>
+struct Unroll {
+  static constexpr int value = KB <= 8 ? 2 : 1;
+};
+
 // d[j] = A_{order[j]} . v  (j < k), d[k] = v . v when selfdot
-__global__ void __launch_bounds__(kBlock) k_mdot(Lay L, const uint32_t *__restrict__ mask, double *const *tab,
-                                                 const int *order, const int *kptr, const double *__restrict__ v,
-                                                 int selfdot, double *out, double *partials, unsigned int *counter) {
-  __shared__ const double *ptr[MAXS];
+template <int KB>
+__global__ void __launch_bounds__(kBlock) k_mdot(int64_t npair, double *const *tab, const int *order,
+                                                 const int *kptr, const double *__restrict__ v, int selfdot,
+                                                 double *out, double *partials, unsigned int *counter) {
+  __shared__ const double2 *ptr[KB];
   const int k = *kptr;
-  if (threadIdx.x < k) ptr[threadIdx.x] = tab[order[threadIdx.x]];
+  if (threadIdx.x < k) ptr[threadIdx.x] = reinterpret_cast<const double2 *>(tab[order[threadIdx.x]]);
   __syncthreads();
-  double acc[RQ];
+  double acc[KB + 2];
 #pragma unroll
-  for (int q = 0; q < RQ; ++q) acc[q] = 0.0;
-  FOR_ACTIVE(L, mask) {
-    const int64_t e = w_ * 32 + (threadIdx.x & 31);
-    const double vv = v[e];
+  for (int q = 0; q < KB + 2; ++q) acc[q] = 0.0;
+  const double2 *v2 = reinterpret_cast<const double2 *>(v);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < npair; p0 += Unroll<KB>::value * stride) {
+    double2 vv[Unroll<KB>::value], uu[Unroll<KB>::value][KB];
 #pragma unroll
-    for (int j = 0; j < MAXS; ++j)
-      if (j < k) acc[j] = add(acc[j], mul(ptr[j][e], vv));
-    if (selfdot) acc[k] = add(acc[k], mul(vv, vv));
+    for (int u = 0; u < Unroll<KB>::value; ++u) {
+      const int64_t p = p0 + u * stride;
+      if (p < npair) {
+        vv[u] = __ldcg(v2 + p);
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+          if (j < k) uu[u][j] = __ldcg(ptr[j] + p);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < Unroll<KB>::value; ++u) {
+      if (p0 + u * stride >= npair) break;
+#pragma unroll
+      for (int j = 0; j < KB; ++j)
+        if (j < k) {
+          acc[j] = add(acc[j], mul(uu[u][j].x, vv[u].x));
+          acc[j] = add(acc[j], mul(uu[u][j].y, vv[u].y));
+        }
+      if (selfdot) {
+        acc[KB] = add(acc[KB], mul(vv[u].x, vv[u].x));
+        acc[KB] = add(acc[KB], mul(vv[u].y, vv[u].y));
+      }
+    }
   }
+  if (selfdot) acc[k] = acc[KB];
   last_block_reduce(acc, k + (selfdot ? 1 : 0), partials, counter, out);
 }
 
 // out = in - sum_j c_j A_{order[j]};  d[j] = A_{order[j]} . out (j < ndot), d[ndot] = out.out
-__global__ void __launch_bounds__(kBlock) k_axpy_dots(Lay L, const uint32_t *__restrict__ mask, double *const *tab,
-                                                      const int *order, const int *kptr, const double *c,
-                                                      const double *in, double *outv, int ndot_is_k, double *dout,
+template <int KB>
+__global__ void __launch_bounds__(kBlock) k_axpy_dots(int64_t npair, double *const *tab, const int *order,
+                                                      const int *kptr, const double *c, const double *in,
+                                                      double *outv, int ndot_is_k, double *dout,
                                                       double *partials, unsigned int *counter, const int *gate) {
   if (gate && !*gate) return;
-  __shared__ const double *ptr[MAXS];
-  __shared__ double cs[MAXS];
+  __shared__ const double2 *ptr[KB];
+  __shared__ double cs[KB];
   const int k = *kptr;
-  if (threadIdx.x < k) { ptr[threadIdx.x] = tab[order[threadIdx.x]]; cs[threadIdx.x] = c[threadIdx.x]; }
+  if (threadIdx.x < k) {
+    ptr[threadIdx.x] = reinterpret_cast<const double2 *>(tab[order[threadIdx.x]]);
+    cs[threadIdx.x] = c[threadIdx.x];
+  }
   __syncthreads();
   const int nd = ndot_is_k ? k : 0;
-  double acc[RQ];
+  double acc[KB + 2];
 #pragma unroll
-  for (int q = 0; q < RQ; ++q) acc[q] = 0.0;
-  FOR_ACTIVE(L, mask) {
-    const int64_t e = w_ * 32 + (threadIdx.x & 31);
-    double u[MAXS];
-    double t = 0.0;
+  for (int q = 0; q < KB + 2; ++q) acc[q] = 0.0;
+  const double2 *in2 = reinterpret_cast<const double2 *>(in);
+  double2 *out2 = reinterpret_cast<double2 *>(outv);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < npair; p0 += Unroll<KB>::value * stride) {
+    double2 iv[Unroll<KB>::value], uu[Unroll<KB>::value][KB];
 #pragma unroll
-    for (int j = 0; j < MAXS; ++j)
-      if (j < k) {
-        u[j] = ptr[j][e];
-        t = (j == 0) ? mul(cs[0], u[0]) : add(t, mul(cs[j], u[j]));
+    for (int u = 0; u < Unroll<KB>::value; ++u) {
+      const int64_t p = p0 + u * stride;
+      if (p < npair) {
+        iv[u] = __ldcg(in2 + p);
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+          if (j < k) uu[u][j] = __ldcg(ptr[j] + p);
       }
-    const double o = sub(in[e], t);
-    outv[e] = o;
+    }
 #pragma unroll
-    for (int j = 0; j < MAXS; ++j)
-      if (j < nd) acc[j] = add(acc[j], mul(u[j], o));
-    acc[nd] = add(acc[nd], mul(o, o));
+    for (int u = 0; u < Unroll<KB>::value; ++u) {
+      const int64_t p = p0 + u * stride;
+      if (p >= npair) break;
+      double tx = 0.0, ty = 0.0;
+#pragma unroll
+      for (int j = 0; j < KB; ++j)
+        if (j < k) {
+          tx = (j == 0) ? mul(cs[0], uu[u][0].x) : add(tx, mul(cs[j], uu[u][j].x));
+          ty = (j == 0) ? mul(cs[0], uu[u][0].y) : add(ty, mul(cs[j], uu[u][j].y));
+        }
+      const double ox = sub(iv[u].x, tx), oy = sub(iv[u].y, ty);
+      out2[p] = make_double2(ox, oy);
+#pragma unroll
+      for (int j = 0; j < KB; ++j)
+        if (j < nd) {
+          acc[j] = add(acc[j], mul(uu[u][j].x, ox));
+          acc[j] = add(acc[j], mul(uu[u][j].y, oy));
+        }
+      acc[KB] = add(acc[KB], mul(ox, ox));
+      acc[KB] = add(acc[KB], mul(oy, oy));
+    }
   }
+  acc[nd] = acc[KB];
   last_block_reduce(acc, nd + 1, partials, counter, dout);
 }
 
 // out = sum_j c_j A_{order[j]} (0 when k == 0)
-__global__ void __launch_bounds__(kBlock) k_comb(Lay L, const uint32_t *__restrict__ mask, double *const *tab,
-                                                 const int *order, const int *kptr, const double *c, double *outv) {
-  __shared__ const double *ptr[MAXS];
-  __shared__ double cs[MAXS];
+template <int KB>
+__global__ void __launch_bounds__(kBlock) k_comb(int64_t npair, double *const *tab, const int *order,
+                                                 const int *kptr, const double *c, double *outv) {
+  __shared__ const double2 *ptr[KB];
+  __shared__ double cs[KB];
   const int k = *kptr;
-  if (threadIdx.x < k) { ptr[threadIdx.x] = tab[order[threadIdx.x]]; cs[threadIdx.x] = c[threadIdx.x]; }
+  if (threadIdx.x < k) {
+    ptr[threadIdx.x] = reinterpret_cast<const double2 *>(tab[order[threadIdx.x]]);
+    cs[threadIdx.x] = c[threadIdx.x];
+  }
   __syncthreads();
-  FOR_ACTIVE(L, mask) {
-    const int64_t e = w_ * 32 + (threadIdx.x & 31);
-    double t = 0.0;
-    for (int j = 0; j < k; ++j) t = (j == 0) ? mul(cs[0], ptr[0][e]) : add(t, mul(cs[j], ptr[j][e]));
-    outv[e] = t;
+  double2 *out2 = reinterpret_cast<double2 *>(outv);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < npair; p0 += Unroll<KB>::value * stride) {
+    double2 uu[Unroll<KB>::value][KB];
+#pragma unroll
+    for (int u = 0; u < Unroll<KB>::value; ++u) {
+      const int64_t p = p0 + u * stride;
+      if (p < npair) {
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+          if (j < k) uu[u][j] = __ldcg(ptr[j] + p);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < Unroll<KB>::value; ++u) {
+      const int64_t p = p0 + u * stride;
+      if (p >= npair) break;
+      double tx = 0.0, ty = 0.0;
+#pragma unroll
+      for (int j = 0; j < KB; ++j)
+        if (j < k) {
+          tx = (j == 0) ? mul(cs[0], uu[u][0].x) : add(tx, mul(cs[j], uu[u][j].x));
+          ty = (j == 0) ? mul(cs[0], uu[u][0].y) : add(ty, mul(cs[j], uu[u][j].y));
+        }
+      out2[p] = make_double2(tx, ty);
+    }
   }
 }
 
 // CSPE: u = w/nrm into U[slot], ku = K u into KU[slot], cross_j = U_{order[j]}.ku (j<kprime), diag = u.ku
+template <int KB>
 __global__ void __launch_bounds__(kBlock) k_cspe_product(Lay L, const uint32_t *__restrict__ mask, double dg,
                                                          double of, FamDev *f, double *const *Utab,
                                                          double *const *KUtab, const double *__restrict__ w,
@@ -214,9 +299,9 @@ __global__ void __launch_bounds__(kBlock) k_cspe_product(Lay L, const uint32_t *
   double *U = Utab[f->new_slot];
   double *KU = KUtab[f->new_slot];
   const double nrm = f->nrm;
-  double acc[RQ];
+  double acc[KB + 2];
 #pragma unroll
-  for (int q = 0; q < RQ; ++q) acc[q] = 0.0;
+  for (int q = 0; q < KB + 2; ++q) acc[q] = 0.0;
   FOR_ACTIVE(L, mask) {
     const int64_t e = w_ * 32 + (threadIdx.x & 31);
     const int c = e < L.C ? 0 : (e < 2 * L.C ? 1 : 2);
@@ -226,10 +311,11 @@ __global__ void __launch_bounds__(kBlock) k_cspe_product(Lay L, const uint32_t *
     U[e] = ue;
     KU[e] = ku;
 #pragma unroll
-    for (int j = 0; j < MAXS; ++j)
-      if (j < kp) acc[j] = add(acc[j], mul(ptr[j][e], ku));
-    acc[kp] = add(acc[kp], mul(ue, ku));
+    for (int j = 0; j < KB; ++j)
+      if (j < kp) acc[j] = add(acc[j], mul(__ldcg(ptr[j] + e), ku));
+    acc[KB] = add(acc[KB], mul(ue, ku));
   }
+  acc[kp] = acc[KB];
   last_block_reduce(acc, kp + 1, partials, counter, f->d + 0);
 }
 
@@ -273,6 +359,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_multi(Lay L, const uint32_t *__
 }
 
 // POD Galerkin: blockIdx.y = j < podk -> Gk[i][j] = B_i . KB_j; j == podk -> d[i] = B_i . rhs
+template <int KB>
 __global__ void __launch_bounds__(kBlock) k_pod_galerkin(Lay L, const uint32_t *__restrict__ mask, FamDev *f,
                                                          double *const *Btab, double *const *KBtab,
                                                          const double *__restrict__ rhs, double *partials,
@@ -284,21 +371,22 @@ __global__ void __launch_bounds__(kBlock) k_pod_galerkin(Lay L, const uint32_t *
   if (threadIdx.x < kk) bp[threadIdx.x] = Btab[threadIdx.x];
   __syncthreads();
   const double *v = (j < kk) ? KBtab[j] : rhs;
-  double acc[RQ];
+  double acc[KB + 2];
 #pragma unroll
-  for (int q = 0; q < RQ; ++q) acc[q] = 0.0;
+  for (int q = 0; q < KB + 2; ++q) acc[q] = 0.0;
   FOR_ACTIVE(L, mask) {
     const int64_t e = w_ * 32 + (threadIdx.x & 31);
-    const double vv = v[e];
+    const double vv = __ldcg(v + e);
 #pragma unroll
-    for (int i = 0; i < MAXS; ++i)
-      if (i < kk) acc[i] = add(acc[i], mul(bp[i][e], vv));
+    for (int i = 0; i < KB; ++i)
+      if (i < kk) acc[i] = add(acc[i], mul(__ldcg(bp[i] + e), vv));
   }
   double *out = (j < kk) ? (f->Gk + (int64_t)j * MAXS) : f->d;  // Gk stored column j contiguous
   last_block_reduce(acc, kk, partials + (int64_t)j * RQ * gridDim.x, counters + j, out);
 }
 
 // POD push: copy y into the ring slot and update the Gram row/column
+template <int KB>
 __global__ void __launch_bounds__(kBlock) k_pod_push(Lay L, const uint32_t *__restrict__ mask, FamDev *f,
                                                      double *const *Xtab, int n_pod, const double *__restrict__ y,
                                                      double *partials, unsigned int *counter) {
@@ -311,18 +399,19 @@ __global__ void __launch_bounds__(kBlock) k_pod_push(Lay L, const uint32_t *__re
   if (threadIdx.x < nother) ptr[threadIdx.x] = Xtab[f->order[first + threadIdx.x]];
   __syncthreads();
   double *X = Xtab[slot];
-  double acc[RQ];
+  double acc[KB + 2];
 #pragma unroll
-  for (int q = 0; q < RQ; ++q) acc[q] = 0.0;
+  for (int q = 0; q < KB + 2; ++q) acc[q] = 0.0;
   FOR_ACTIVE(L, mask) {
     const int64_t e = w_ * 32 + (threadIdx.x & 31);
-    const double yv = y[e];
+    const double yv = __ldcg(y + e);
     X[e] = yv;
 #pragma unroll
-    for (int j = 0; j < MAXS; ++j)
-      if (j < nother) acc[j] = add(acc[j], mul(ptr[j][e], yv));
-    acc[nother] = add(acc[nother], mul(yv, yv));
+    for (int j = 0; j < KB; ++j)
+      if (j < nother) acc[j] = add(acc[j], mul(__ldcg(ptr[j] + e), yv));
+    acc[KB] = add(acc[KB], mul(yv, yv));
   }
+  acc[nother] = acc[KB];
   last_block_reduce(acc, nother + 1, partials, counter, f->d);
 }
 
@@ -905,6 +994,14 @@ static int stream_grid(mq_ctx *ctx) {
   return (int)std::max<int64_t>(1, b);
 }
 
+// dispatch a kernel template on the basis-size bound of the solver
+#define KB_LAUNCH(kb, kern, grid, block, stream, ...)                       \
+  do {                                                                    \
+    if ((kb) <= 8) kern<8><<<(grid), (block), 0, (stream)>>>(__VA_ARGS__);  \
+    else if ((kb) <= 16) kern<16><<<(grid), (block), 0, (stream)>>>(__VA_ARGS__); \
+    else kern<32><<<(grid), (block), 0, (stream)>>>(__VA_ARGS__);          \
+  } while (0)
+
 #define LAUNCH_CHECK()                 \
   do {                                 \
     MQ_CUDA(cudaGetLastError());       \
@@ -930,11 +1027,12 @@ static int start_vector(mq_ctx *ctx, int fam, const double *rhs, double *x0) {
       LAUNCH_CHECK();
       break;
     case MQ_STRAT_CSPE:
-      k_mdot<<<G, kBlock, 0, st>>>(L, ctx->d_mask, s->d_U[fam], f->order, &f->k, rhs, 0, f->d, s->d_red, s->d_cnt);
+      KB_LAUNCH(s->kb, k_mdot, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, rhs, 0, f->d, s->d_red,
+                s->d_cnt);
       LAUNCH_CHECK();
       k_cspe_project_small<<<1, 32, 0, st>>>(f);
       LAUNCH_CHECK();
-      k_comb<<<stream_grid(ctx), kBlock, 0, st>>>(L, ctx->d_mask, s->d_U[fam], f->order, &f->k, f->coef, x0);
+      KB_LAUNCH(s->kb, k_comb, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, f->coef, x0);
       LAUNCH_CHECK();
       break;
     case MQ_STRAT_POD: {
@@ -946,11 +1044,12 @@ static int start_vector(mq_ctx *ctx, int fam, const double *rhs, double *x0) {
       k_spmv_multi<<<g2, kBlock, 0, st>>>(L, ctx->d_mask, ctx->kn_diag, ctx->kn_off, f, s->d_B, s->d_KB);
       LAUNCH_CHECK();
       dim3 g3(G, s->cfg.n_pod + 1);
-      k_pod_galerkin<<<g3, kBlock, 0, st>>>(L, ctx->d_mask, f, s->d_B, s->d_KB, rhs, s->d_red, s->d_cnt + 1);
+      KB_LAUNCH(s->kb, k_pod_galerkin, g3, kBlock, st, L, ctx->d_mask, f, s->d_B, s->d_KB, rhs, s->d_red,
+                s->d_cnt + 1);
       LAUNCH_CHECK();
       k_pod_solve<<<1, 32, 0, st>>>(f, s->d_run);
       LAUNCH_CHECK();
-      k_comb<<<stream_grid(ctx), kBlock, 0, st>>>(L, ctx->d_mask, s->d_B, s->d_iota, &f->podk, f->coef, x0);
+      KB_LAUNCH(s->kb, k_comb, G, kBlock, st, L.total / 2, s->d_B, s->d_iota, &f->podk, f->coef, x0);
       LAUNCH_CHECK();
       break;
     }
@@ -976,30 +1075,31 @@ static int observe(mq_ctx *ctx, int fam, const double *y) {
       break;
     case MQ_STRAT_CSPE:
       // ||v|| and U^T v in one pass
-      k_mdot<<<G, kBlock, 0, st>>>(L, ctx->d_mask, s->d_U[fam], f->order, &f->k, y, 1, f->d, s->d_red, s->d_cnt);
+      KB_LAUNCH(s->kb, k_mdot, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, y, 1, f->d, s->d_red,
+                s->d_cnt);
       LAUNCH_CHECK();
       k_cspe_gate<<<1, 32, 0, st>>>(f);
       LAUNCH_CHECK();
       // CGS pass 1: w1 = v - U c1, c2 = U^T w1
-      k_axpy_dots<<<G, kBlock, 0, st>>>(L, ctx->d_mask, s->d_U[fam], f->order, &f->k, f->coef, y, s->w1, 1, f->d,
+      KB_LAUNCH(s->kb, k_axpy_dots, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, f->coef, y, s->w1, 1, f->d,
                                         s->d_red, s->d_cnt, &f->accept);
       LAUNCH_CHECK();
       k_cspe_gate_c2<<<1, 32, 0, st>>>(f);
       LAUNCH_CHECK();
       // CGS pass 2: w2 = w1 - U c2, ||w2||^2
-      k_axpy_dots<<<G, kBlock, 0, st>>>(L, ctx->d_mask, s->d_U[fam], f->order, &f->k, f->coef, s->w1, s->w2, 0,
+      KB_LAUNCH(s->kb, k_axpy_dots, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, f->coef, s->w1, s->w2, 0,
                                         f->d, s->d_red, s->d_cnt, &f->accept);
       LAUNCH_CHECK();
       k_cspe_decide<<<1, 32, 0, st>>>(f, f->d, s->cfg.max_cols, s->cfg.drop_tol);
       LAUNCH_CHECK();
-      k_cspe_product<<<G, kBlock, 0, st>>>(L, ctx->d_mask, ctx->kn_diag, ctx->kn_off, f, s->d_U[fam], s->d_KU[fam],
+      KB_LAUNCH(s->kb, k_cspe_product, G, kBlock, st, L, ctx->d_mask, ctx->kn_diag, ctx->kn_off, f, s->d_U[fam], s->d_KU[fam],
                                            s->w2, s->d_red, s->d_cnt);
       LAUNCH_CHECK();
       k_cspe_commit<<<1, 32, 0, st>>>(f);
       LAUNCH_CHECK();
       break;
     case MQ_STRAT_POD:
-      k_pod_push<<<G, kBlock, 0, st>>>(L, ctx->d_mask, f, s->d_X[fam], s->cfg.n_pod, y, s->d_red, s->d_cnt);
+      KB_LAUNCH(s->kb, k_pod_push, G, kBlock, st, L, ctx->d_mask, f, s->d_X[fam], s->cfg.n_pod, y, s->d_red, s->d_cnt);
       LAUNCH_CHECK();
       k_pod_push_commit<<<1, 32, 0, st>>>(f, s->cfg.n_pod);
       LAUNCH_CHECK();
@@ -1167,6 +1267,10 @@ int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern)
   SolverHost *s = new SolverHost();
   ctx->solver = s;
   s->cfg = *cfg;
+  {
+    const int bound = cfg->strategy == MQ_STRAT_CSPE ? cfg->max_cols : (cfg->strategy == MQ_STRAT_POD ? cfg->n_pod : 1);
+    s->kb = bound <= 8 ? 8 : (bound <= 16 ? 16 : 32);
+  }
   const Lay &L = ctx->topo.L;
   const size_t vb = sizeof(double) * L.total;
   int rc = 0;
