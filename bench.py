@@ -110,8 +110,8 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # helpers
 # ---------------------------------------------------------------------------
-def schedule(spec, n_steps):
-    dt = spec.dt
+def schedule(spec, n_steps, dt=None):
+    dt = spec.dt if dt is None else dt
     w = 2.0 * np.pi * spec.freq
     tt = [0.0]
     for _ in range(n_steps):
@@ -132,11 +132,14 @@ def pcg_launch_bytes(n_n, iters, modes=None):
 
 
 def member_problem(rank: int):
+    """Rank 0 runs the nominal configs[1] problem; rank r > 0 runs configs[3]
+    ensemble member r (J, kappa factors; dt scaled with kappa)."""
     from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import ensemble as E
     if rank == 0:
-        return C.make_problem(1), (1.0, 1.0)
-    j, k = C.ensemble_factors(256, seed=0)
-    return C.make_problem(1, j_scale=float(j[rank]), kappa_scale=float(k[rank])), (float(j[rank]), float(k[rank]))
+        return C.make_problem(1), (1.0, 1.0), C.config_spec(1).dt
+    prob, jf, kf, dt = E.member_problem(rank)
+    return prob, (jf, kf), dt
 
 
 def dist_init():
@@ -224,7 +227,7 @@ def run_reference_arm(args):
 # ---------------------------------------------------------------------------
 # device arm
 # ---------------------------------------------------------------------------
-def time_device_steps(op, spec, warmup, steps, flush=True):
+def time_device_steps(op, spec, warmup, steps, flush=True, dt=None):
     """W warm-up steps then K timed steps (CUDA events per step on the
     context stream, L2 flushed before each), PCG launches timed inside."""
     import ctypes
@@ -232,7 +235,7 @@ def time_device_steps(op, spec, warmup, steps, flush=True):
     from paper_1611_06721_b200 import _lib
     from paper_1611_06721_b200._lib import check, dptr
     lib, ctx = op.lib, op.grid.ctx
-    dts, wave, _ = schedule(spec, warmup + steps)
+    dts, wave, _ = schedule(spec, warmup + steps, dt)
     op._set_state(np.zeros(op.grid.n_c), 0.0)
     # initial recovery at t = 0 as in the reference loop
     from paper_1611_06721_b200.schur import recover_an
@@ -341,7 +344,7 @@ def run_device_arm(args):
     from paper_1611_06721_b200 import configs as C
     _lib.load()
     spec = C.config_spec(1)
-    problem, factors = member_problem(rank)
+    problem, factors, dt_member = member_problem(rank)
     hbm_peak, peak_kind = peaks()
     op = SchurOperator(problem, pcg=PcgConfig(rel_tol=spec.rel_tol, max_iter=spec.max_iter),
                        strategy="cspe", max_cols=spec.max_cols, device=local)
@@ -349,7 +352,7 @@ def run_device_arm(args):
     barrier(dist)
     with ClockSampler(local) as clk:
         step_ms, pcg_ms, iters, launches = time_device_steps(op, spec, args.warmup, args.steps,
-                                                             flush=not args.no_flush)
+                                                             flush=not args.no_flush, dt=dt_member)
     barrier(dist)
     total_ms = float(step_ms.sum())
     total_ms_max = max_over_ranks(total_ms, dist, local)

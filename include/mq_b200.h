@@ -211,6 +211,13 @@ int mq_run_prepare(mq_ctx *ctx, int64_t n_steps, const double *dt, const double 
 int mq_run_steps(mq_ctx *ctx, int64_t n, int32_t use_graph, double *a_c_hist_dev);
 int mq_run_finish(mq_ctx *ctx, int32_t *iters_out, int64_t *failed_step);
 
+/* Spectral estimate lambda_max(M_c^-1 K_S(a_ref)) by power iteration
+ * (schur.py:327-376): v0 = normalised start vector (host n_c), a_ref NULL = 0.
+ * dt = safety * 2 / lambda. */
+int mq_estimate_cfl(mq_ctx *ctx, const double *a_ref, const double *v0, int32_t power_iters,
+                    double power_tol, double safety, double rel_tol, int32_t max_iter,
+                    double *lambda_out, double *dt_out, int32_t *used_out, int64_t *pcg_applies);
+
 /* ---- timing (CUDA events on the context stream) ------------------------- */
 /* Sum of the device times of the PCG launches of the last step (when PCG
  * timing is enabled with mq_pcg_stats(..., 1)). */

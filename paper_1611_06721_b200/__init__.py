@@ -10,8 +10,8 @@ points mirrored here.
 from .device import AIR, COIL, CONDUCTOR, NU_VACUUM, DeviceGrid, KnOperator, Problem, sinusoid
 from .krylov import (IndefiniteOperatorError, JacobiPreconditioner, PcgConfig, Preconditioner,
                      SolveReport, pcg_solve)
-from .schur import (FAMILIES, SchurOperator, StepFailureError, TransientResult,
-                    explicit_euler_step, recover_an, run_explicit)
+from .schur import (FAMILIES, CflEstimate, SchurOperator, StepFailureError, TransientResult,
+                    estimate_cfl, explicit_euler_step, recover_an, run_explicit)
 from .startvec import DeviceStrategy, RhsFamily
 
 __version__ = "0.1.0"
@@ -21,5 +21,6 @@ __all__ = [
     "IndefiniteOperatorError", "JacobiPreconditioner", "PcgConfig", "Preconditioner",
     "SolveReport", "pcg_solve", "FAMILIES", "SchurOperator", "StepFailureError",
     "TransientResult", "explicit_euler_step", "recover_an", "run_explicit", "DeviceStrategy",
+    "CflEstimate", "estimate_cfl",
     "RhsFamily",
 ]

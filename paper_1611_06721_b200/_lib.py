@@ -124,6 +124,8 @@ SIGNATURES = {
     "mq_run_steps": (I32, [VP, I64, I32, VP]),
     "mq_run_finish": (I32, [VP, c_int32_p, c_int64_p]),
     "mq_pcg_collect": (I32, [VP, c_double_p, c_int32_p]),
+    "mq_estimate_cfl": (I32, [VP, c_double_p, c_double_p, I32, D, D, D, I32, c_double_p,
+                              c_double_p, c_int32_p, c_int64_p]),
     "mq_timer_start": (I32, [VP]),
     "mq_timer_stop": (I32, [VP, c_double_p]),
     "mq_pcg_stats": (I32, [VP, c_double_p, c_int64_p, c_int64_p, I32]),

@@ -100,7 +100,8 @@ def config_spec(index: int) -> ConfigSpec:
         return ConfigSpec("cfg2_128cube_two_blocks_pod30", 128,
                           [(c - 28, c - 4, c - 12, c + 12, c - 12, c + 12),
                            (c + 4, c + 28, c - 12, c + 12, c - 12, c + 12)],
-                          5e6, BRAUER_IRON, 5e6, 200, "pod", n_pod=30)
+                          5e6, BRAUER_IRON, 5e6, 200, "pod", n_pod=30,
+                          dt=5.641670141705834e-05)  # device estimate_cfl, safety 0.9
     if index == 4:
         c = 128
         return ConfigSpec("cfg4_256cube_two_blocks_cspe5", 256,

@@ -1700,6 +1700,87 @@ int mq_run_explicit(mq_ctx *ctx, int64_t n_steps, const double *dt, const double
   return rc;
 }
 
+// Power iteration for lambda_max(M_c^-1 K_S) (schur.py:327-376 with the
+// detached inner solves of schur.py:297-313).  Inner PCG solves run on the
+// device (warm-started from the previous inner solution, no family history);
+// the n_c-sized Rayleigh-quotient algebra runs on the host in the reference's
+// operation order.  v0: the normalised start vector (host, n_c).
+int mq_estimate_cfl(mq_ctx *ctx, const double *a_ref, const double *v0, int32_t power_iters, double power_tol,
+                    double safety, double rel_tol, int32_t max_iter, double *lambda_out, double *dt_out,
+                    int32_t *used_out, int64_t *pcg_applies) {
+  if (!(safety > 0.0 && safety <= 1.0)) { set_error("safety must lie in (0, 1]"); return MQ_INVALID; }
+  if (power_iters < 1) { set_error("power_iters must be at least 1"); return MQ_INVALID; }
+  const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
+  const Lay &L = ctx->topo.L;
+  CondArgs a = cond_args(ctx);
+  cudaStream_t st = ctx->stream;
+  std::vector<double> v(v0, v0 + n_c), w(n_c), kc(n_c), ky(n_c), u(n_c);
+  const std::vector<double> &mc = ctx->topo.mc_diag;
+  std::vector<double> minv(n_c);
+  for (int64_t e = 0; e < n_c; ++e) minv[e] = 1.0 / mc[e];
+  double *d_w = nullptr, *d_y = nullptr;
+  MQ_CUDA(cudaMalloc(&d_w, sizeof(double) * L.total));
+  MQ_CUDA(cudaMalloc(&d_y, sizeof(double) * L.total));
+  MQ_CUDA(cudaMemsetAsync(d_w, 0, sizeof(double) * L.total, st));
+  MQ_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * L.total, st));
+  // nu of the linearisation state (a_ref = 0 when NULL)
+  if (a_ref) MQ_CUDA(cudaMemcpyAsync(ctx->d_ac_next, a_ref, sizeof(double) * n_c, cudaMemcpyHostToDevice, st));
+  else MQ_CUDA(cudaMemsetAsync(ctx->d_ac_next, 0, sizeof(double) * n_c, st));
+  k_cell_nu<<<grid_for(ctx, a.n_cells), 256, 0, st>>>(a, ctx->d_ac_next, ctx->d_cell_nu);
+  int rc = MQ_OK;
+  double lam = 0.0, lam_prev = 0.0;
+  bool have_prev = false;
+  int used = power_iters;
+  int64_t applies = 0;
+  for (int it = 1; it <= power_iters && rc == MQ_OK; ++it) {
+    cudaError_t e = cudaMemcpyAsync(ctx->d_ac_x, v.data(), sizeof(double) * n_c, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "cfl upload"); break; }
+    k_kcnt<<<grid_for(ctx, a.n_rows_t), 256, 0, st>>>(a, ctx->d_ac_x, d_w);
+    mq_solve_report rep{};
+    rc = ctx_pcg(ctx, d_w, d_y, it == 1 ? 2 : 1, rel_tol, 0.0, max_iter, 1, &rep);
+    if (rc == MQ_NOT_CONVERGED) { set_error("spectral probe solve stalled"); break; }
+    if (rc) break;
+    applies += rep.applies;
+    k_kc_apply<<<grid_for(ctx, n_c), 256, 0, st>>>(a, ctx->d_cell_nu, ctx->d_ac_x, ctx->d_yc);
+    e = cudaMemcpyAsync(kc.data(), ctx->d_yc, sizeof(double) * n_c, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) {
+      k_kcn<<<grid_for(ctx, n_c), 256, 0, st>>>(a, d_y, ctx->d_yc);
+      e = cudaMemcpyAsync(ky.data(), ctx->d_yc, sizeof(double) * n_c, cudaMemcpyDeviceToHost, st);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "cfl products"); break; }
+    double den = 0.0, num = 0.0, nu2 = 0.0;
+    for (int64_t q = 0; q < n_c; ++q) {
+      w[q] = kc[q] - ky[q];
+      den += v[q] * (mc[q] * v[q]);
+      num += v[q] * w[q];
+    }
+    lam = num / den;
+    for (int64_t q = 0; q < n_c; ++q) {
+      u[q] = minv[q] * w[q];
+      nu2 += u[q] * u[q];
+    }
+    const double nu = std::sqrt(nu2);
+    if (nu == 0.0) { set_error("power iteration collapsed to the nullspace"); rc = MQ_NOT_CONVERGED; break; }
+    for (int64_t q = 0; q < n_c; ++q) v[q] = u[q] / nu;
+    if (have_prev && std::fabs(lam - lam_prev) <= power_tol * std::fabs(lam)) { used = it; break; }
+    lam_prev = lam;
+    have_prev = true;
+  }
+  cudaFree(d_w);
+  cudaFree(d_y);
+  if (rc) return rc;
+  if (!(lam > 0.0) || !std::isfinite(lam)) {
+    set_error("spectral estimate is not positive");
+    return MQ_NOT_CONVERGED;
+  }
+  *lambda_out = lam;
+  *dt_out = safety * 2.0 / lam;
+  if (used_out) *used_out = used;
+  if (pcg_applies) *pcg_applies = applies;
+  return MQ_OK;
+}
+
 int mq_pcg_collect(mq_ctx *ctx, double *ms, int32_t *n_events) {
   MQ_CUDA(cudaStreamSynchronize(ctx->stream));
   double sum = 0.0;

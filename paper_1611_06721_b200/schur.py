@@ -25,7 +25,8 @@ from .krylov import PcgConfig, Preconditioner, SolveReport
 from .startvec import RhsFamily, family_index, solver_cfg
 
 __all__ = ["StepFailureError", "SchurOperator", "explicit_euler_step", "recover_an",
-           "run_explicit", "TransientResult", "FAMILIES", "step_times"]
+           "run_explicit", "TransientResult", "FAMILIES", "step_times", "CflEstimate",
+           "estimate_cfl"]
 
 FAMILIES = (RhsFamily.SOURCE_CURRENT, RhsFamily.COUPLING_FROM_CURRENT_STATE,
             RhsFamily.COUPLING_FROM_PREVIOUS_STATE)
@@ -146,6 +147,54 @@ class SchurOperator:
         return out
 
 
+@dataclass(frozen=True)
+class CflEstimate:
+    """Largest stable explicit step dt_max = safety * 2 / lambda_max (schur.py:316-324)."""
+
+    lambda_max: float
+    dt_max: float
+    safety: float
+    power_iters: int
+    power_tol: float
+    pcg_applies: int = 0
+
+
+def estimate_cfl(op: SchurOperator, a_c_ref=None, *, power_iters: int = 200,
+                 power_tol: float = 1e-4, safety: float = 0.9, seed: int = 42,
+                 v0=None) -> CflEstimate:
+    """lambda_max(M_c^-1 K_S) by power iteration on the device (schur.py:327-376).
+
+    Same start vector rule as the reference (a valid v0, else
+    ``default_rng(seed).standard_normal``, normalised); the inner K_n solves are
+    device PCG solves warm-started from the previous inner solution.
+    """
+    if not (0.0 < safety <= 1.0):
+        raise ValueError("safety must lie in (0, 1]")
+    if power_iters < 1:
+        raise ValueError("power_iters must be at least 1")
+    n = op.grid.n_c
+    ref = None if a_c_ref is None else f64(a_c_ref, n, "reference state")
+    v = None
+    if v0 is not None:
+        v = np.asarray(v0, dtype=np.float64).copy()
+        if v.shape != (n,) or not np.linalg.norm(v) > 0.0:
+            v = None
+        else:
+            v = v / np.linalg.norm(v)
+    if v is None:
+        v = np.random.default_rng(seed).standard_normal(n)
+        v /= np.linalg.norm(v)
+    v = np.ascontiguousarray(v)
+    lam, dt = ctypes.c_double(), ctypes.c_double()
+    used, applies = ctypes.c_int32(), ctypes.c_int64()
+    rc = op.lib.mq_estimate_cfl(op.grid.ctx, dptr(ref) if ref is not None else None, dptr(v),
+                                int(power_iters), float(power_tol), float(safety),
+                                float(op.pcg.rel_tol), int(op.pcg.max_iter), ctypes.byref(lam),
+                                ctypes.byref(dt), ctypes.byref(used), ctypes.byref(applies))
+    check(rc)
+    return CflEstimate(lam.value, dt.value, safety, int(used.value), power_tol, int(applies.value))
+
+
 def explicit_euler_step(state, dt: float, op: SchurOperator, step_index: int | None = None):
     """One explicit Euler step on the device (schur.py:379-405)."""
     a_c, t = state
@@ -228,24 +277,35 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
                  probe=None, a0=None, max_cols: int = 20, n_pod: int = 10,
                  eps_pod: float = 1e-4, max_steps: int = 2_000_000, device: int = 0,
                  use_graph: bool = True, record_states: bool = False,
-                 op: SchurOperator | None = None) -> TransientResult:
-    """Integrate with explicit Euler on the device (schur.py:474-607), fixed dt.
+                 op: SchurOperator | None = None, safety: float = 0.9,
+                 power_iters: int = 200, power_tol: float = 1e-4,
+                 seed: int = 42) -> TransientResult:
+    """Integrate with explicit Euler on the device (schur.py:474-607).
 
-    ``dt`` must be a number (the spectral estimate runs separately).
+    ``dt="auto"`` runs the device spectral estimate once before the loop
+    (the reference also re-estimates every ``reestimate_every`` steps, which
+    only matters with strong saturation; not done here).
     """
     if t_end <= 0:
         raise ValueError("t_end must be positive")
     if output_period <= 0:
         raise ValueError("output_period must be positive")
-    if isinstance(dt, str):
-        raise ValueError("run_explicit on the device needs a numeric dt")
-    dt = float(dt)
-    if dt <= 0:
-        raise ValueError("dt must be positive")
     wall_start = time.perf_counter()
     if op is None:
         op = SchurOperator(problem, pcg=pcg, strategy=strategy, preconditioner=preconditioner,
                            max_cols=max_cols, n_pod=n_pod, eps_pod=eps_pod, device=device)
+    lambda_max = None
+    if isinstance(dt, str):
+        if dt != "auto":
+            raise ValueError(f"dt must be a number or 'auto', got {dt!r}")
+        # one spectral estimate up front (schur.py:503-510); a fixed dt is
+        # used for the whole run on the device
+        est = estimate_cfl(op, power_iters=power_iters, power_tol=power_tol, safety=safety,
+                           seed=seed)
+        dt, lambda_max = est.dt_max, est.lambda_max
+    dt = float(dt)
+    if dt <= 0:
+        raise ValueError("dt must be positive")
     n_c, n_n = op.grid.n_c, op.grid.n_n
     a_c = np.zeros(n_c) if a0 is None else f64(a0, n_c, "initial state").copy()
     wave = op.problem.waveform
@@ -339,7 +399,7 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
         "strategy": op.strategy_kind,
         "steps": n,
         "dt": dt,
-        "lambda_max": None,
+        "lambda_max": lambda_max,
         "cfl_refreshes": 0,
         "solves": {f.value: op.solve_count(f) for f in FAMILIES},
         "iterations": {f.value: int(sum(op.solve_iterations[f])) for f in FAMILIES},

@@ -349,3 +349,43 @@ def test_config1_first_steps(gpu_ok, golden):
     it = golden["c1_run_cspe_iters"]
     assert np.max(np.abs(res.step_iterations[:, 3] - it[1:, 2])) <= 1
     assert np.max(np.abs(res.step_iterations[:, 1] - it[1:, 1])) <= 1
+
+
+def test_cfl_estimate_matches_oracle_and_reference(gpu_ok, golden):
+    """estimate_cfl (schur.py:327-376) on the device vs the oracle and the
+    reference's own lambda (golden) at config 0."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, SchurOperator, estimate_cfl
+    spec, m = oracle_model(0)
+    op = SchurOperator(C.make_problem(0), pcg=PcgConfig(rel_tol=1e-8), strategy="cspe", max_cols=5)
+    est = estimate_cfl(op, safety=0.9, seed=42)
+    lam_ref, dt_ref, used_ref = golden["c0_cfl"]
+    assert est.power_iters == int(used_ref)
+    assert abs(est.lambda_max - lam_ref) <= 1e-9 * lam_ref
+    assert abs(est.dt_max - dt_ref) <= 1e-9 * dt_ref
+    # zero / wrong-shape start vectors reseed deterministically (schur.py:344-354)
+    est0 = estimate_cfl(op, v0=np.zeros(m.n_c))
+    assert est0.lambda_max == est.lambda_max
+    with pytest.raises(ValueError):
+        estimate_cfl(op, safety=1.5)
+    # a saturated reference state lowers nu... and raises lambda
+    ref = O.SchurOracle(m, O.sinusoid(50.0), "cspe", 1e-8, 5000, 5)
+    a_ref = np.random.default_rng(1).standard_normal(m.n_c) * 1e-4
+    lam_o, dt_o, used_o = ref.estimate_cfl(a_ref=a_ref)
+    est_a = estimate_cfl(op, a_c_ref=a_ref)
+    assert abs(est_a.lambda_max - lam_o) <= 1e-8 * lam_o
+
+
+@pytest.mark.slow
+def test_ensemble_member_first_steps(gpu_ok):
+    """configs[3] member 1 (J, kappa factors, dt scaled with kappa): two
+    device steps against the oracle on the same perturbed problem."""
+    from paper_1611_06721_b200 import PcgConfig, run_explicit
+    from paper_1611_06721_b200 import ensemble as E
+    prob, jf, kf, dt = E.member_problem(1)
+    spec, m = oracle_model(3, j_scale=jf, kappa_scale=kf)
+    tr = O.run(m, O.sinusoid(50.0), dt, 2, strategy="cspe", rel_tol=1e-8, max_cols=5)
+    res = run_explicit(prob, t_end=2 * dt, dt=dt, strategy="cspe", pcg=PcgConfig(rel_tol=1e-8),
+                       output_period=dt * (1 - 1e-3), max_cols=5, record_states=True)
+    for i in range(2):
+        assert rel(res.a_c_history[i], tr.a_c[i + 1]) <= REL_FIELD
