@@ -150,7 +150,7 @@ def load(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("MQ_LIB_PATH", LIB_PATH))
     if not p.exists():
         raise RuntimeError(
             f"{p} is missing: the CUDA extension has not been built "
