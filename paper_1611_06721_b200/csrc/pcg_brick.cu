@@ -580,6 +580,13 @@ static BrickGeo make_geo(int nx, int ny, int nz, int resident) {
   int chunks = resident / tiles;
   if (chunks < 1) chunks = 1;
   if (chunks > nx) chunks = nx;
+  // equal bricks: the largest chunk count <= the budget that divides nx (the
+  // grid barrier waits for the longest brick)
+  for (int c = chunks; c >= 1; --c)
+    if (nx % c == 0) {
+      if (2 * c >= chunks) chunks = c;
+      break;
+    }
   g.chunks = chunks;
   g.nbricks = tiles * chunks;
   return g;
