@@ -98,6 +98,7 @@ int ctx_pcg(mq_ctx *ctx, const double *b, double *x, int x0_mode, double rel_tol
 
 int launch_pcg_ctx(mq_ctx *ctx, const StencilPcgArgs &args) {
   if (ctx->pcg_variant == 1) return launch_pcg_stencil(args, ctx->pcg_grid, ctx->stream);
+  if (ctx->pcg_variant == 2) return launch_pcg_resident(args, ctx->res_geo, ctx->res_grid, ctx->stream);
   return launch_pcg_brick(args, ctx->geo, ctx->brick_grid, ctx->stream);
 }
 
@@ -162,9 +163,16 @@ int mq_ctx_create(const mq_grid_desc *desc, int32_t device, mq_ctx **out) {
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_tmp1, sizeof(double) * t.L.total);
   if (!rc) rc = pcg_stencil_grid(t.L.words, &ctx->pcg_grid);
   if (!rc) rc = brick_pcg_setup(t.L, t.nx, t.ny, t.nz, &ctx->brick_grid, &ctx->geo);
+  if (!rc) rc = resident_pcg_setup(t.nx, t.ny, t.nz, &ctx->res_grid, &ctx->res_geo);
   {
+    // default: shared-memory-resident kernel when the bricks fit on chip,
+    // else the TMA brick kernel; MQ_PCG_KERNEL=simple|brick|resident overrides
     const char *v = getenv("MQ_PCG_KERNEL");
-    ctx->pcg_variant = (v && std::string(v) == "simple") ? 1 : 0;
+    const std::string want = v ? v : "";
+    ctx->pcg_variant = ctx->res_grid > 0 ? 2 : 0;
+    if (want == "simple") ctx->pcg_variant = 1;
+    else if (want == "brick") ctx->pcg_variant = 0;
+    else if (want == "resident" && ctx->res_grid > 0) ctx->pcg_variant = 2;
   }
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_partials, sizeof(double) * 8 * (size_t)std::max(ctx->pcg_grid, 1024));
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_bar, sizeof(GridBar));

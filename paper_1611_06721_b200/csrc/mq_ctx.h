@@ -81,9 +81,11 @@ struct mq_ctx {
   mq::PcgOut *h_out = nullptr;
   unsigned long long *d_trace = nullptr;
   int pcg_grid = 1;
-  int pcg_variant = 0;        // 0: brick-tiled kernel, 1: thread-per-row kernel
+  int pcg_variant = 0;        // 0: TMA brick kernel, 1: thread-per-row, 2: smem-resident
   mq::BrickGeo geo{};
   int brick_grid = 1;
+  mq::BrickGeo res_geo{};
+  int res_grid = 0;
   // conducting block (device)
   int64_t *d_kcn_ptr = nullptr;
   int32_t *d_kcn_col = nullptr;
@@ -141,6 +143,8 @@ int launch_pcg_brick(const StencilPcgArgs &args, const BrickGeo &geo, int grid, 
 int launch_kn_apply_brick(const Lay &L, const BrickGeo &geo, const uint32_t *mask, double dg, double of,
                           const double *x, double *y, int sms, cudaStream_t s);
 int launch_pcg_ctx(mq_ctx *ctx, const StencilPcgArgs &args);
+int resident_pcg_setup(int nx, int ny, int nz, int *grid, BrickGeo *geo);
+int launch_pcg_resident(const StencilPcgArgs &args, const BrickGeo &geo, int grid, cudaStream_t s);
 int launch_kn_apply(const Lay &L, const uint32_t *mask, double dg, double of, const double *x, double *y, int sms,
                     cudaStream_t s);
 int launch_scatter(int64_t n, const int32_t *idx, const double *src, double *dst, int sms, cudaStream_t s);

@@ -1,0 +1,430 @@
+// Shared-memory-resident fused PCG for grids whose bricks fit on chip
+// (krylov.py:174-250; same algorithm, stopping rule and bit-level arithmetic
+// as pcg_stencil_kernel / pcg_tma_kernel).
+//
+// One CTA per SM (512 threads) owns a brick: a 16 (j) x 32 (k) node tile over
+// Li <= 5 i-planes, all three edge components.  For the whole solve the
+// brick's r, Ap and search direction p (the latter with a one-node halo ring)
+// stay in shared memory.  Per iteration:
+//   K1: own p_new = M^-1 r + beta p (in place), halo p_new recomputed from the
+//       neighbours' published r and p_old (L2), own p_new published (ping-pong
+//       buffer), Ap = K_n p_new from shared memory, partial p.Ap
+//   K2: x += alpha p (global, own), r -= alpha Ap (shared), r published,
+//       partials r.r, r.z
+// Global traffic per iteration is the halo ring plus 4 own streams (publish
+// p, publish r, x read/write), all L2-resident at these sizes; the two grid
+// barriers and the shared-memory stencil set the iteration time.
+#include "mq_device.cuh"
+
+namespace mq {
+
+constexpr int RTJ = 16, RTK = 32, RT = RTJ * RTK;      // 512 threads, one position each
+constexpr int RHJ = RTJ + 2, RHK = RTK + 2, RHP = RHJ * RHK;  // 18 x 34 = 612
+constexpr int RW = RT / 32;                              // 16 warps
+constexpr int RRING = 2 * RHK + 2 * RTJ;                 // 100 ring positions per plane
+constexpr int RLI_MAX = 5;                               // planes per brick that fit
+
+struct ResGeo {
+  int nx, ny, nz;
+  int tiles_k, tiles_j, chunks, nbricks, li_max;
+};
+
+struct ResPcgArgs {
+  StencilPcgArgs a;
+  ResGeo g;
+};
+
+__host__ __device__ constexpr size_t res_smem_bytes(int li) {
+  return sizeof(double) * ((size_t)(li + 2) * 3 * RHP + (size_t)2 * li * 3 * RT);
+}
+
+template <int NV>
+__device__ __forceinline__ void block_sum_r(double (&v)[NV], double *smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) smem[q * RW + warp] = v[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    double s = 0.0;
+    for (int w = 0; w < RW; ++w) s = add(s, smem[q * RW + w]);
+    v[q] = s;
+  }
+  __syncthreads();
+}
+
+// same stencil as stencil3 (pcg_brick.cu), CSR column order
+template <class V>
+__device__ __forceinline__ double stencil_r(int c, double dg, double of, V v) {
+  double s;
+  if (c == 0) {
+    s = -mul(of, v(0, 0, -1, 0));
+    s = sub(s, mul(of, v(0, 0, 0, -1)));
+    s = add(s, mul(dg, v(0, 0, 0, 0)));
+    s = sub(s, mul(of, v(0, 0, 0, 1)));
+    s = sub(s, mul(of, v(0, 0, 1, 0)));
+    s = add(s, mul(of, v(1, 0, -1, 0)));
+    s = sub(s, mul(of, v(1, 0, 0, 0)));
+    s = sub(s, mul(of, v(1, 1, -1, 0)));
+    s = add(s, mul(of, v(1, 1, 0, 0)));
+    s = add(s, mul(of, v(2, 0, 0, -1)));
+    s = sub(s, mul(of, v(2, 0, 0, 0)));
+    s = sub(s, mul(of, v(2, 1, 0, -1)));
+    s = add(s, mul(of, v(2, 1, 0, 0)));
+  } else if (c == 1) {
+    s = mul(of, v(0, -1, 0, 0));
+    s = sub(s, mul(of, v(0, -1, 1, 0)));
+    s = sub(s, mul(of, v(0, 0, 0, 0)));
+    s = add(s, mul(of, v(0, 0, 1, 0)));
+    s = sub(s, mul(of, v(1, -1, 0, 0)));
+    s = sub(s, mul(of, v(1, 0, 0, -1)));
+    s = add(s, mul(dg, v(1, 0, 0, 0)));
+    s = sub(s, mul(of, v(1, 0, 0, 1)));
+    s = sub(s, mul(of, v(1, 1, 0, 0)));
+    s = add(s, mul(of, v(2, 0, 0, -1)));
+    s = sub(s, mul(of, v(2, 0, 0, 0)));
+    s = sub(s, mul(of, v(2, 0, 1, -1)));
+    s = add(s, mul(of, v(2, 0, 1, 0)));
+  } else {
+    s = mul(of, v(0, -1, 0, 0));
+    s = sub(s, mul(of, v(0, -1, 0, 1)));
+    s = sub(s, mul(of, v(0, 0, 0, 0)));
+    s = add(s, mul(of, v(0, 0, 0, 1)));
+    s = add(s, mul(of, v(1, 0, -1, 0)));
+    s = sub(s, mul(of, v(1, 0, -1, 1)));
+    s = sub(s, mul(of, v(1, 0, 0, 0)));
+    s = add(s, mul(of, v(1, 0, 0, 1)));
+    s = sub(s, mul(of, v(2, -1, 0, 0)));
+    s = sub(s, mul(of, v(2, 0, -1, 0)));
+    s = add(s, mul(dg, v(2, 0, 0, 0)));
+    s = sub(s, mul(of, v(2, 0, 1, 0)));
+    s = sub(s, mul(of, v(2, 1, 0, 0)));
+  }
+  return s;
+}
+
+__global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
+  extern __shared__ __align__(16) double rsm[];
+  __shared__ double red[3 * RW];
+  __shared__ double tot[4];
+  const StencilPcgArgs &a = A.a;
+  const ResGeo &g = A.g;
+  const Lay &L = a.L;
+  const int G = gridDim.x;
+  const int tid = threadIdx.x, ty = tid >> 5, tx = tid & 31;
+  const double dg = a.dg, of = a.of, inv = a.inv;
+  const bool jac = a.use_jac != 0;
+  const int x0_mode = a.x0_mode_dev ? *a.x0_mode_dev : a.x0_mode;
+  if (a.err_word && *((volatile const unsigned int *)a.err_word)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      PcgOut o{};
+      o.status = 99;
+      *a.out = o;
+    }
+    return;
+  }
+  // brick of this CTA (one per CTA; the launch guarantees nbricks == G)
+  const int b = blockIdx.x;
+  const int tk = b % g.tiles_k, tj = (b / g.tiles_k) % g.tiles_j, ic = b / (g.tiles_k * g.tiles_j);
+  const int k0 = tk * RTK, j0 = tj * RTJ;
+  const int i0 = (int)(((int64_t)ic * g.nx) / g.chunks), i1 = (int)(((int64_t)(ic + 1) * g.nx) / g.chunks);
+  const int li = i1 - i0;
+  double *P = rsm;                                   // [li+2][3][RHP], plane 0 = i0-1
+  double *R = P + (size_t)(g.li_max + 2) * 3 * RHP;  // [li][3][RT]
+  double *AP = R + (size_t)g.li_max * 3 * RT;        // [li][3][RT]
+  const int j = j0 + ty, k = k0 + tx;
+  const bool own_ok = j < g.ny && k < g.nz;
+  const int s_own = (ty + 1) * RHK + (tx + 1);
+  const int64_t pos_own = L.off + (int64_t)j * L.Sj + k;
+  auto Pidx = [&](int l, int c, int s) { return ((size_t)l * 3 + c) * RHP + s; };
+  auto Oidx = [&](int l, int c) { return ((size_t)l * 3 + c) * RT + tid; };
+  const uint32_t *mask = a.mask;
+  // active bits of the own positions, 3 per plane (li <= 5 -> 15 bits)
+  uint32_t act = 0u;
+  if (own_ok)
+    for (int l = 0; l < li; ++l)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int64_t e = c * L.C + (int64_t)(i0 + l) * L.Si + pos_own;
+        act |= ((__ldg(mask + (e >> 5)) >> (e & 31)) & 1u) << (3 * l + c);
+      }
+  auto own_e = [&](int l, int c) { return c * L.C + (int64_t)(i0 + l) * L.Si + pos_own; };
+  auto is_act = [&](int l, int c) { return (act >> (3 * l + c)) & 1u; };
+  auto V = [&](int l, int c) {
+    // neighbourhood accessor of own position at brick plane l (P plane l+1)
+    return [=](int cc, int di, int dj, int dk) { return P[Pidx(l + 1 + di, cc, s_own + dj * RHK + dk)]; };
+  };
+  // halo slots: planes 0 and li+1 in full, ring of the interior planes
+  const int nhalo = 2 * RHP + li * RRING;
+  auto halo_slot = [&](int h, int &l, int &s) {
+    if (h < RHP) { l = 0; s = h; return; }
+    if (h < 2 * RHP) { l = li + 1; s = h - RHP; return; }
+    h -= 2 * RHP;
+    l = 1 + h / RRING;
+    const int q = h % RRING;
+    int jj, kk;
+    if (q < RHK) { jj = 0; kk = q; }
+    else if (q < 2 * RHK) { jj = RHJ - 1; kk = q - RHK; }
+    else if (q < 2 * RHK + RTJ) { jj = 1 + (q - 2 * RHK); kk = 0; }
+    else { jj = 1 + (q - 2 * RHK - RTJ); kk = RHK - 1; }
+    s = jj * RHK + kk;
+  };
+  auto halo_e = [&](int l, int s, int c, bool &ok) {
+    const int jj = s / RHK, kk = s % RHK;
+    const int gi = i0 - 1 + l, gj = j0 - 1 + jj, gk = k0 - 1 + kk;
+    ok = gi >= -1 && gi <= g.nx && gj >= -1 && gj <= g.ny && gk >= -1 && gk <= g.nz;
+    return c * L.C + L.off + (int64_t)gi * L.Si + (int64_t)gj * L.Sj + gk;
+  };
+
+  unsigned long long *trace = (blockIdx.x == 0 && threadIdx.x == 0) ? a.trace : nullptr;
+  auto stamp = [&](int slot) {
+    if (trace && slot < 4 * 64 + 1) trace[slot] = globaltimer_ns();
+  };
+  stamp(0);
+  // ---- initial residual (krylov.py:209-218) ----
+  double v3[3] = {0.0, 0.0, 0.0};
+  {
+    // P <- x0 (own + halo) when x0 is given, own r <- b - A x0
+    if (x0_mode == 1) {
+      for (int h = tid; h < nhalo; h += RT) {
+        int l, s;
+        halo_slot(h, l, s);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          bool ok;
+          const int64_t e = halo_e(l, s, c, ok);
+          P[Pidx(l, c, s)] = ok ? __ldcg(a.x + e) : 0.0;
+        }
+      }
+      for (int l = 0; l < li; ++l)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) P[Pidx(l + 1, c, s_own)] = own_ok ? __ldcg(a.x + own_e(l, c)) : 0.0;
+      __syncthreads();
+    }
+    for (int l = 0; l < li; ++l)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double rv = 0.0;
+        if (own_ok && is_act(l, c)) {
+          const int64_t e = own_e(l, c);
+          const double bv = __ldcg(a.b + e);
+          rv = bv;
+          if (x0_mode == 1) rv = sub(bv, stencil_r(c, dg, of, V(l, c)));
+          else a.x[e] = 0.0;
+          const double z = jac ? mul(inv, rv) : rv;
+          v3[0] = add(v3[0], mul(bv, bv));
+          v3[1] = add(v3[1], mul(rv, rv));
+          v3[2] = add(v3[2], mul(rv, z));
+          a.r[e] = rv;  // published for the neighbours' first halo
+        }
+        R[Oidx(l, c)] = rv;
+        AP[Oidx(l, c)] = 0.0;
+      }
+  }
+  block_sum_r<3>(v3, red);
+  if (threadIdx.x == 0) {
+    a.partials[0 * G + blockIdx.x] = v3[0];
+    a.partials[1 * G + blockIdx.x] = v3[1];
+    a.partials[2 * G + blockIdx.x] = v3[2];
+  }
+  int status = MQ_OK, iters = 0, converged = 0;
+  double rel = 0.0, bnorm = 0.0, alpha = 0.0, rz = 0.0;
+  bool pold_is_a = true;  // published p_old lives in pa, p_new goes to pb
+  int applies = (x0_mode == 2) ? 0 : 1;
+  if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
+  {
+    double s3[3];
+    grid_partials_sum<3>(a.partials, G, s3, tot);
+    bnorm = sqrt(s3[0]);
+    const double target = fmax(a.rel_tol * bnorm, a.abs_tol);
+    double rnorm = sqrt(s3[1]);
+    rz = jac ? s3[2] : s3[1];
+    auto relf = [&](double res) { return bnorm > 0.0 ? res / bnorm : (res == 0.0 ? 0.0 : INFINITY); };
+    if (rnorm <= target) { converged = 1; rel = relf(rnorm); goto done; }
+    double beta = 0.0;
+    bool first = true;
+    for (int it = 1; it <= a.max_iter; ++it) {
+      const double *pold_g = pold_is_a ? a.pa : a.pb;
+      double *pnew_g = pold_is_a ? a.pb : a.pa;
+      // ---- K1: own p_new in place, halo p_new from published r / p_old ----
+      for (int l = 0; l < li; ++l)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double rq = R[Oidx(l, c)];
+          const double z = jac ? mul(inv, rq) : rq;
+          const size_t pi = Pidx(l + 1, c, s_own);
+          const double pv = first ? z : add(z, mul(beta, P[pi]));
+          P[pi] = pv;
+          if (own_ok && is_act(l, c)) pnew_g[own_e(l, c)] = pv;
+        }
+      for (int h0 = tid; h0 < nhalo; h0 += 2 * RT) {
+        double rv[2][3], pv[2][3];
+        int hl[2], hs[2];
+        bool hok[2][3];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int h = h0 + u * RT;
+          hl[u] = -1;
+          if (h < nhalo) {
+            halo_slot(h, hl[u], hs[u]);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              const int64_t e = halo_e(hl[u], hs[u], c, hok[u][c]);
+              rv[u][c] = hok[u][c] ? __ldcg(a.r + e) : 0.0;
+              pv[u][c] = (hok[u][c] && !first) ? __ldcg(pold_g + e) : 0.0;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (hl[u] < 0) continue;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const double z = jac ? mul(inv, rv[u][c]) : rv[u][c];
+            P[Pidx(hl[u], c, hs[u])] = first ? z : add(z, mul(beta, pv[u][c]));
+          }
+        }
+      }
+      __syncthreads();
+      double v1[1] = {0.0};
+      for (int l = 0; l < li; ++l)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (!(own_ok && is_act(l, c))) continue;
+          const double av = stencil_r(c, dg, of, V(l, c));
+          AP[Oidx(l, c)] = av;
+          v1[0] = add(v1[0], mul(P[Pidx(l + 1, c, s_own)], av));
+        }
+      block_sum_r<1>(v1, red);
+      if (threadIdx.x == 0) a.partials[3 * G + blockIdx.x] = v1[0];
+      ++applies;
+      stamp(4 * (it - 1) + 1);
+      if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
+      stamp(4 * (it - 1) + 2);
+      double s1[1];
+      grid_partials_sum<1>(a.partials + 3 * G, G, s1, tot);
+      const double pap = s1[0];
+      if (!isfinite(pap) || pap <= 0.0) { status = MQ_INDEFINITE; iters = it; goto done; }
+      alpha = rz / pap;
+      // ---- K2: x += alpha p, r -= alpha Ap (own), publish r ----
+      double v2[2] = {0.0, 0.0};
+      double xo[RLI_MAX * 3];
+#pragma unroll
+      for (int l = 0; l < RLI_MAX; ++l)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if (l < li && own_ok && is_act(l, c)) xo[3 * l + c] = __ldcg(a.x + own_e(l, c));
+#pragma unroll
+      for (int l = 0; l < RLI_MAX; ++l)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (!(l < li && own_ok && is_act(l, c))) continue;
+          const int64_t e = own_e(l, c);
+          a.x[e] = add(xo[3 * l + c], mul(alpha, P[Pidx(l + 1, c, s_own)]));
+          const double rv = sub(R[Oidx(l, c)], mul(alpha, AP[Oidx(l, c)]));
+          R[Oidx(l, c)] = rv;
+          a.r[e] = rv;
+          const double z = jac ? mul(inv, rv) : rv;
+          v2[0] = add(v2[0], mul(rv, rv));
+          v2[1] = add(v2[1], mul(rv, z));
+        }
+      block_sum_r<2>(v2, red);
+      if (threadIdx.x == 0) {
+        a.partials[4 * G + blockIdx.x] = v2[0];
+        a.partials[5 * G + blockIdx.x] = v2[1];
+      }
+      stamp(4 * (it - 1) + 3);
+      if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
+      stamp(4 * (it - 1) + 4);
+      double s2[2];
+      grid_partials_sum<2>(a.partials + 4 * G, G, s2, tot);
+      rnorm = sqrt(s2[0]);
+      iters = it;
+      rel = relf(rnorm);
+      const double rz_new = jac ? s2[1] : s2[0];
+      if (rnorm <= target) { converged = 1; break; }
+      if (!isfinite(rz_new)) { status = MQ_INDEFINITE; break; }
+      beta = rz_new / rz;
+      rz = rz_new;
+      first = false;
+      pold_is_a = !pold_is_a;
+    }
+    if (status == MQ_OK && !converged) status = MQ_NOT_CONVERGED;
+  }
+done:
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    PcgOut o;
+    o.iterations = iters;
+    o.converged = converged;
+    o.status = status;
+    o.applies = applies;
+    o.rel = rel;
+    o.bnorm = bnorm;
+    o.alpha = alpha;
+    o.rz = rz;
+    *a.out = o;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Returns 0 with *grid = 0 when the grid does not fit the resident scheme.
+int resident_pcg_setup(int nx, int ny, int nz, int *grid, BrickGeo *geo_out) {
+  *grid = 0;
+  int dev = 0, sms = 0;
+  MQ_CUDA(cudaGetDevice(&dev));
+  MQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int tiles_k = (nz + RTK - 1) / RTK, tiles_j = (ny + RTJ - 1) / RTJ;
+  const int tiles = tiles_k * tiles_j;
+  if (tiles > sms) return MQ_OK;
+  // smallest number of i-chunks with <= RLI_MAX planes, dividing nx if possible
+  int best = 0;
+  for (int c = (nx + RLI_MAX - 1) / RLI_MAX; c <= nx && tiles * c <= sms; ++c)
+    if (nx % c == 0) { best = c; break; }
+  if (!best) {
+    const int c = (nx + RLI_MAX - 1) / RLI_MAX;
+    if (tiles * c > sms) return MQ_OK;
+    best = c;
+  }
+  // enough CTAs to be worth it (small grids run faster on the TMA brick
+  // kernel with one plane per CTA)
+  if (2 * tiles * best < sms) return MQ_OK;
+  const int li_max = (nx + best - 1) / best;
+  const size_t smem = res_smem_bytes(li_max);
+  MQ_CUDA(cudaFuncSetAttribute(pcg_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per = 0;
+  MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pcg_resident_kernel, RT, smem));
+  if (per < 1 || tiles * best > sms * per) return MQ_OK;
+  geo_out->nx = nx;
+  geo_out->ny = ny;
+  geo_out->nz = nz;
+  geo_out->tiles_k = tiles_k;
+  geo_out->tiles_j = tiles_j;
+  geo_out->chunks = best;
+  geo_out->nbricks = tiles * best;
+  *grid = tiles * best;
+  return MQ_OK;
+}
+
+int launch_pcg_resident(const StencilPcgArgs &args, const BrickGeo &geo, int grid, cudaStream_t s) {
+  ResPcgArgs A;
+  A.a = args;
+  A.g.nx = geo.nx;
+  A.g.ny = geo.ny;
+  A.g.nz = geo.nz;
+  A.g.tiles_k = geo.tiles_k;
+  A.g.tiles_j = geo.tiles_j;
+  A.g.chunks = geo.chunks;
+  A.g.nbricks = geo.nbricks;
+  A.g.li_max = (geo.nx + geo.chunks - 1) / geo.chunks;
+  const size_t smem = res_smem_bytes(A.g.li_max);
+  MQ_CUDA(cudaMemsetAsync(&args.bar->count, 0, sizeof(unsigned long long), s));
+  void *params[] = {&A};
+  MQ_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_resident_kernel, dim3(grid), dim3(RT), params, smem, s));
+  return MQ_OK;
+}
+
+}  // namespace mq

@@ -389,3 +389,27 @@ def test_ensemble_member_first_steps(gpu_ok):
                        output_period=dt * (1 - 1e-3), max_cols=5, record_states=True)
     for i in range(2):
         assert rel(res.a_c_history[i], tr.a_c[i + 1]) <= REL_FIELD
+
+
+@pytest.mark.parametrize("variant", ["simple", "brick", "resident"])
+def test_pcg_kernel_variants_agree(gpu_ok, variant, monkeypatch):
+    """All three fused-PCG kernels (thread-per-row, TMA brick, shared-memory
+    resident) solve the same system like the oracle; they differ only in the
+    dot-product summation order."""
+    from paper_1611_06721_b200 import PcgConfig, Preconditioner, pcg_solve
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200.device import DeviceGrid
+    monkeypatch.setenv("MQ_PCG_KERNEL", variant)
+    for index in (0, 1):
+        spec, m = oracle_model(index)
+        with DeviceGrid(C.make_problem(index)) as g:
+            rng = np.random.default_rng(17)
+            b = m.kn @ rng.standard_normal(m.n_n)
+            x0 = rng.standard_normal(m.n_n) * 1e-3
+            inv = O.jacobi_inverse(m.kn.diagonal())
+            for start in (None, x0):
+                x, rep = pcg_solve(g.kn_operator(), b, x0=start,
+                                   config=PcgConfig(rel_tol=1e-8, preconditioner=Preconditioner.JACOBI))
+                ref = O.pcg(m.kn_apply, b, x0=start, rel_tol=1e-8, inv_diag=inv)
+                assert rep.converged and abs(rep.iterations - ref.iterations) <= 1
+                assert rel(x, ref.x) <= 1e-8

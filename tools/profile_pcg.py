@@ -18,10 +18,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--kernel", default=os.environ.get("MQ_PCG_KERNEL", "brick"))
+    ap.add_argument("--kernel", default=os.environ.get("MQ_PCG_KERNEL", ""))
     ap.add_argument("--spmv", action="store_true", help="also time K_n SpMV launches")
     args = ap.parse_args()
-    os.environ["MQ_PCG_KERNEL"] = args.kernel
+    if args.kernel:
+        os.environ["MQ_PCG_KERNEL"] = args.kernel
     from paper_1611_06721_b200 import _lib, configs as C
     from paper_1611_06721_b200._lib import check
     from paper_1611_06721_b200.device import DeviceGrid
