@@ -218,6 +218,25 @@ int mq_estimate_cfl(mq_ctx *ctx, const double *a_ref, const double *v0, int32_t 
                     double power_tol, double safety, double rel_tol, int32_t max_iter,
                     double *lambda_out, double *dt_out, int32_t *used_out, int64_t *pcg_applies);
 
+/* ---- i-slab distributed K_n PCG (BASELINE configs[4]) --------------------
+ * A slab context owns node planes [i_lo, i_hi) of the global grid
+ * (partition restricted bit-exactly); local planes -1 and n = i_hi - i_lo
+ * are ghost planes refreshed by the host's halo exchange.  Each phase
+ * returns this rank's partial sums (host); the host allreduces them over the
+ * ranks and drives krylov.py:174-250's control flow (slab.py). */
+int mq_ctx_create_slab(const mq_grid_desc *desc, int32_t i_lo, int32_t i_hi, int32_t device,
+                       mq_ctx **out);
+/* {C, Si, Sj, off, total, n_planes}: plane l of component c occupies
+ * [c*C + (l+1)*Si, c*C + (l+2)*Si) */
+int mq_layout(const mq_ctx *ctx, int64_t *out6);
+int mq_slab_buffers(mq_ctx *ctx, double **r, double **pa, double **pb, double **ap);
+int mq_slab_init(mq_ctx *ctx, const double *b_dev, double *x_dev, int32_t x0_mode,
+                 int32_t use_jacobi, double *part3);
+int mq_slab_k1(mq_ctx *ctx, double *x_dev, int32_t first, double beta, double alpha_prev,
+               int32_t pold_is_a, int32_t use_jacobi, double *part1);
+int mq_slab_k2(mq_ctx *ctx, double alpha, int32_t use_jacobi, double *part2);
+int mq_slab_final(mq_ctx *ctx, double *x_dev, double alpha, int32_t p_is_a);
+
 /* ---- timing (CUDA events on the context stream) ------------------------- */
 /* Sum of the device times of the PCG launches of the last step (when PCG
  * timing is enabled with mq_pcg_stats(..., 1)). */

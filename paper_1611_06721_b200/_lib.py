@@ -126,6 +126,14 @@ SIGNATURES = {
     "mq_pcg_collect": (I32, [VP, c_double_p, c_int32_p]),
     "mq_estimate_cfl": (I32, [VP, c_double_p, c_double_p, I32, D, D, D, I32, c_double_p,
                               c_double_p, c_int32_p, c_int64_p]),
+    "mq_ctx_create_slab": (I32, [ctypes.POINTER(GridDesc), I32, I32, I32, ctypes.POINTER(VP)]),
+    "mq_layout": (I32, [VP, c_int64_p]),
+    "mq_slab_buffers": (I32, [VP, ctypes.POINTER(VP), ctypes.POINTER(VP), ctypes.POINTER(VP),
+                              ctypes.POINTER(VP)]),
+    "mq_slab_init": (I32, [VP, VP, VP, I32, I32, c_double_p]),
+    "mq_slab_k1": (I32, [VP, VP, I32, D, D, I32, I32, c_double_p]),
+    "mq_slab_k2": (I32, [VP, D, I32, c_double_p]),
+    "mq_slab_final": (I32, [VP, VP, D, I32]),
     "mq_timer_start": (I32, [VP]),
     "mq_timer_stop": (I32, [VP, c_double_p]),
     "mq_pcg_stats": (I32, [VP, c_double_p, c_int64_p, c_int64_p, I32]),

@@ -131,5 +131,6 @@ struct Topology {
 };
 
 int build_topology(const mq_grid_desc &d, Topology &t, std::string &err);
+int build_slab_topology(const mq_grid_desc &d, int ilo, int ihi, Topology &t, std::string &err);
 
 }  // namespace mq

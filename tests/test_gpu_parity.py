@@ -413,3 +413,37 @@ def test_pcg_kernel_variants_agree(gpu_ok, variant, monkeypatch):
                 ref = O.pcg(m.kn_apply, b, x0=start, rel_tol=1e-8, inv_diag=inv)
                 assert rep.converged and abs(rep.iterations - ref.iterations) <= 1
                 assert rel(x, ref.x) <= 1e-8
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("x0_given", [False, True])
+def test_slab_pcg_loopback_on_one_gpu(gpu_ok, world, x0_given):
+    """configs[4] i-slab decomposition on one GPU: `world` slab contexts, halo
+    exchange by device copies, fixed-order partial sums (LoopbackComm), the
+    same host loop as the NCCL path.  Partition union bit-exact; solution vs
+    the single-domain oracle."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200.slab import LoopbackComm, SlabGrid, slab_pcg_solve
+    spec, m = oracle_model(0)
+    prob = C.make_problem(0)
+    slabs = [SlabGrid(prob, r, world) for r in range(world)]
+    parts = [s.partition() for s in slabs]
+    allp = np.concatenate(parts)
+    assert allp.size == m.n_n and np.array_equal(np.sort(allp), m.noncond_global)
+    idx = [np.searchsorted(m.noncond_global, p) for p in parts]
+    rng = np.random.default_rng(9)
+    b = m.kn @ rng.standard_normal(m.n_n)
+    x0 = rng.standard_normal(m.n_n) * 1e-3
+    for s, ix in zip(slabs, idx):
+        s.upload(b[ix], s.b)
+        s.upload(x0[ix] if x0_given else np.zeros(ix.size), s.x)
+    it, relres, conv, app = slab_pcg_solve(slabs, LoopbackComm(), x0_given=x0_given, rel_tol=1e-8)
+    ref = O.pcg(m.kn_apply, b, x0=x0 if x0_given else None, rel_tol=1e-8,
+                inv_diag=O.jacobi_inverse(m.kn.diagonal()))
+    x = np.zeros(m.n_n)
+    for s, ix in zip(slabs, idx):
+        x[ix] = s.download(s.x)
+    assert conv and abs(it - ref.iterations) <= 1 and app == ref.applies - (ref.iterations - it)
+    assert rel(x, ref.x) <= 1e-8
+    for s in slabs:
+        s.close()
