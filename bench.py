@@ -330,8 +330,16 @@ def cfg2_pcg_roofline(hbm_peak, reps=2):
     byts = float(pcg_launch_bytes(n_n, iters))
     achieved = byts / (ms * 1e-3) / 1e9
     g.close()
+    # DRAM traffic per launch from the committed ncu --set full capture of the
+    # same kernel on the same grid (per-iteration bytes x this launch's count)
+    traffic = None
+    tj = ROOT / "profiles" / "traffic.json"
+    if tj.exists():
+        t = json.loads(tj.read_text())
+        traffic = float(t["dram_bytes_per_iteration"]) * iters
     return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-            "frac": achieved / hbm_peak, "traffic": None,
+            "frac": achieved / hbm_peak, "traffic": traffic,
+            "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per iteration)",
             "kernel": "pcg_stencil_kernel", "grid": [128, 128, 128], "n_n": n_n,
             "iterations": iters, "launch_ms": ms,
             "us_per_iteration": 1000.0 * ms / max(iters, 1),

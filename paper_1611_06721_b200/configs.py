@@ -171,14 +171,19 @@ def source_pattern(material: np.ndarray, loops) -> np.ndarray:
     flag, idx = noncond_positions(material)
     n_n = int(flag.sum())
     pattern = np.zeros(n_n)
+    touched = np.zeros(n_n, dtype=np.int32)
     for lp in loops:
         ids, sg = loop_edges(material.shape, lp)
         pos = idx[ids]
         if (pos < 0).any():
             raise ValueError("coil loop touches boundary or conducting edges")
-        one = np.zeros(n_n)
-        np.add.at(one, pos, sg * lp.amps)
-        pattern = pattern + one
+        # one closed loop visits an edge at most once
+        pattern[pos] += sg * lp.amps
+        touched[pos] += 1
+    # edge-disjoint loops: every entry is a single term, so the in-place
+    # accumulation equals the reference shim's pattern + one per loop bitwise
+    if touched.max(initial=0) > 1:
+        raise ValueError("coil loops share edges")
     return pattern
 
 
