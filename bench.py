@@ -276,6 +276,7 @@ def time_e2e(problem, spec, warmup, steps):
     from paper_1611_06721_b200 import PcgConfig, SchurOperator, explicit_euler_step, recover_an
     op = SchurOperator(problem, pcg=PcgConfig(rel_tol=spec.rel_tol, max_iter=spec.max_iter),
                        strategy="cspe", max_cols=spec.max_cols)
+    op.set_probe()
     a = np.zeros(op.grid.n_c)
     t = 0.0
     recover_an(op, a, t)
@@ -289,12 +290,31 @@ def time_e2e(problem, spec, warmup, steps):
         a, _ = explicit_euler_step((a, t), spec.dt, op, warmup + s + 1)
         t += spec.dt
         a_n, _ = recover_an(op, a, t)
+        op.probe_b()
     el = time.perf_counter() - t0
     n_c, n_n = op.grid.n_c, op.grid.n_n
-    h2d = 2 * n_c * 8          # a_c uploaded by each of the two calls
-    d2h = n_c * 8 + n_n * 8    # a_c after the step, a_n after the recovery
+    h2d = 2 * n_c * 8              # a_c uploaded by each of the two calls
+    d2h = n_c * 8 + n_n * 8 + 8    # a_c after the step, a_n after the recovery, B_probe
     op.grid.close()
     return steps / el, el, h2d, d2h
+
+
+def cfg2_steps(warmup=3, steps=5):
+    """configs[2] (128^3, two blocks, POD-30) through the same device step
+    loop: steps/s with L2 flushed before each step.  Secondary line; the
+    headline is config 1."""
+    from paper_1611_06721_b200 import PcgConfig, SchurOperator, configs as C
+    spec = C.config_spec(2)
+    op = SchurOperator(C.make_problem(2), pcg=PcgConfig(rel_tol=spec.rel_tol, max_iter=spec.max_iter),
+                       strategy="pod", n_pod=spec.n_pod)
+    op.set_probe()
+    step_ms, pcg_ms, iters, launches = time_device_steps(op, spec, warmup, steps)
+    op.grid.close()
+    return {"workload": spec.name, "grid": [128, 128, 128], "strategy": "pod", "n_pod": spec.n_pod,
+            "dt": spec.dt, "steps_after_warmup": [warmup + 1, warmup + steps],
+            "value": steps / (float(step_ms.sum()) * 1e-3), "unit": UNIT,
+            "ms_per_step": float(step_ms.mean()), "pcg_share_of_step": float(pcg_ms.sum() / step_ms.sum()),
+            "timed_step_iterations": iters.tolist(), "gpu_launches": launches}
 
 
 def cfg2_pcg_roofline(hbm_peak, reps=2):
@@ -356,6 +376,8 @@ def run_device_arm(args):
     hbm_peak, peak_kind = peaks()
     op = SchurOperator(problem, pcg=PcgConfig(rel_tol=spec.rel_tol, max_iter=spec.max_iter),
                        strategy="cspe", max_cols=spec.max_cols, device=local)
+    # B_probe per output row, as the reference bench records (bench.py:371)
+    op.set_probe()
     n_n, n_c = op.grid.n_n, op.grid.n_c
     barrier(dist)
     with ClockSampler(local) as clk:
@@ -379,9 +401,10 @@ def run_device_arm(args):
     line = None
     if rank == 0:
         e2e_v, e2e_s, h2d, d2h = time_e2e(problem, spec, args.warmup, args.steps)
-        roof2 = None
+        roof2 = steps2 = None
         if not args.skip_cfg2:
             roof2 = cfg2_pcg_roofline(hbm_peak)
+            steps2 = cfg2_steps()
         cpu = None
         if world == 1 and not args.skip_cpu:
             v, done, el, _ = cpu_reference(spec, 0, args.cpu_steps, budget_s=30.0)
@@ -404,6 +427,7 @@ def run_device_arm(args):
             "clocks": clk.summary(),
             "roofline": roofline,
             "roofline_cfg2": roof2,
+            "cfg2_steps": steps2,
             "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "explicit_euler_step + recover_an (host arrays)"},
             "gpu_launches": launches,

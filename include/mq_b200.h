@@ -211,6 +211,15 @@ int mq_run_prepare(mq_ctx *ctx, int64_t n_steps, const double *dt, const double 
 int mq_run_steps(mq_ctx *ctx, int64_t n, int32_t use_graph, double *a_c_hist_dev);
 int mq_run_finish(mq_ctx *ctx, int32_t *iters_out, int64_t *failed_step);
 
+/* B probe: mean |B| over probe cells (model.py:415-425 probe_b; default cell
+ * set model.py:562-566, built by the host).  Cells are global cell ids and
+ * must be conductor cells (their B depends on a_c only).  n = 0 clears.
+ * Once set, every step of mq_run_steps also logs B_probe of its new state;
+ * mq_run_probe_log copies the first n entries of the current run. */
+int mq_probe_set(mq_ctx *ctx, const int64_t *cells, int64_t n);
+int mq_probe_b(mq_ctx *ctx, const double *a_c_host /* NULL = current state */, double *out);
+int mq_run_probe_log(mq_ctx *ctx, int64_t n, double *out);
+
 /* Spectral estimate lambda_max(M_c^-1 K_S(a_ref)) by power iteration
  * (schur.py:327-376): v0 = normalised start vector (host n_c), a_ref NULL = 0.
  * dt = safety * 2 / lambda. */

@@ -355,6 +355,29 @@ def cell_b2(model: OracleModel, a_interior) -> np.ndarray:
             + (f[:, 4] ** 2 + f[:, 5] ** 2)) / (2.0 * model.h ** 4)
 
 
+def full_interior(model: OracleModel, a_c, a_n) -> np.ndarray:
+    """model.py:385-391: scatter (a_c, a_n) into the interior vector."""
+    full = np.zeros(model.interior.size)
+    full[model.cond] = a_c
+    full[model.noncond] = a_n
+    return full
+
+
+def default_probe_cells(model: OracleModel, shape) -> np.ndarray:
+    """model.py:562-566: conductor cells in the median k layer (global ids)."""
+    nx, ny, nz = shape
+    ijk = np.stack(np.unravel_index(model.cond_cells, (nx, ny, nz)), axis=1)
+    mid_k = int(np.median(ijk[:, 2]))
+    sel = ijk[ijk[:, 2] == mid_k]
+    return (sel[:, 0] * ny + sel[:, 1]) * nz + sel[:, 2]
+
+
+def probe_b(model: OracleModel, a_interior, cells) -> float:
+    """model.py:415-425: mean |B| over the probe cells."""
+    b2 = cell_b2(model, a_interior)
+    return float(np.sqrt(b2[np.asarray(cells, dtype=np.int64)]).mean())
+
+
 # ---------------------------------------------------------------------------
 # PCG  (krylov.py:82-97, 174-250)
 # ---------------------------------------------------------------------------

@@ -107,7 +107,8 @@ def config_spec(index: int) -> ConfigSpec:
         return ConfigSpec("cfg4_256cube_two_blocks_cspe5", 256,
                           [(c - 56, c - 8, c - 24, c + 24, c - 24, c + 24),
                            (c + 8, c + 56, c - 24, c + 24, c - 24, c + 24)],
-                          5e6, BRAUER_IRON, 5e6, 50, "cspe", max_cols=5)
+                          5e6, BRAUER_IRON, 5e6, 50, "cspe", max_cols=5,
+                          dt=1.4106248992090958e-05)  # device estimate_cfl, safety 0.9
     raise ValueError(f"unknown config {index}")
 
 

@@ -125,6 +125,7 @@ struct Topology {
   std::vector<double> f_base;          // base face weight (air part)
   std::vector<int32_t> f_cell;         // 2 per face: conductor cell list index or -1
   std::vector<int32_t> cell_face;      // 6 per conductor cell: index into faces
+  std::vector<int64_t> cell_ids;       // global cell id per conductor cell (ascending)
   std::vector<int32_t> e_face;         // 4 per cond edge: face index, ascending face id
   std::vector<int8_t> e_sgn;           // 4 per cond edge
   int64_t n_faces_c = 0, n_cells_c = 0;

@@ -70,6 +70,11 @@ struct SolverHost {
   int kb = 32;  // compile-time basis bound used for the tall-skinny kernels
   int per_step = 4;
   int64_t n_planned = 0, n_enqueued = 0;
+  // B probe (model.py:415-425): conductor-cell list indices, per-cell scratch,
+  // per-step log of the current run
+  int32_t *d_probe = nullptr;
+  double *d_probe_vals = nullptr, *d_probe_log = nullptr;
+  int64_t n_probe = 0, probe_cap = 0;
 };
 
 static int s_alloc(mq_ctx *ctx, SolverHost *s, void **p, size_t bytes) {
@@ -84,6 +89,9 @@ void solver_free(mq_ctx *ctx) {
   if (!s) return;
   if (s->graph_exec) cudaGraphExecDestroy(s->graph_exec);
   for (void *p : s->mem) cudaFree(p);
+  cudaFree(s->d_probe);
+  cudaFree(s->d_probe_vals);
+  cudaFree(s->d_probe_log);
   delete s;
   ctx->solver = nullptr;
 }
@@ -800,16 +808,60 @@ __device__ __forceinline__ double face_flux(const CondArgs &a, int64_t f, const 
   return s;
 }
 
+// squared flux density of conductor cell c (model.py:399-407): all edges of
+// its faces are conducting, so the state alone determines it
+__device__ __forceinline__ double cell_b2(const CondArgs &a, int64_t c, const double *state) {
+  double f[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) f[q] = face_flux(a, a.cell_face[6 * c + q], state);
+  return add(add(add(mul(f[0], f[0]), mul(f[1], f[1])), add(mul(f[2], f[2]), mul(f[3], f[3]))),
+             add(mul(f[4], f[4]), mul(f[5], f[5]))) / a.two_h4;
+}
+
 // nu per conductor cell from the state (model.py:496-500, 107-125)
 __global__ void k_cell_nu(CondArgs a, const double *__restrict__ state, double *__restrict__ nu) {
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < a.n_cells; c += (int64_t)gridDim.x * blockDim.x) {
-    double f[6];
-#pragma unroll
-    for (int q = 0; q < 6; ++q) f[q] = face_flux(a, a.cell_face[6 * c + q], state);
-    const double b2 = add(add(add(mul(f[0], f[0]), mul(f[1], f[1])), add(mul(f[2], f[2]), mul(f[3], f[3]))),
-                          add(mul(f[4], f[4]), mul(f[5], f[5]))) / a.two_h4;
+    const double b2 = cell_b2(a, c, state);
     nu[c] = a.linear ? a.k3 : add(mul(a.k1, exp(mul(a.k2, b2))), a.k3);
   }
+}
+
+// numpy's pairwise summation of a float64 array (the add.reduce inner loop
+// behind ndarray.mean): blocks of <= 128 summed with 8 accumulators, larger
+// arrays split at an 8-aligned half.  Recursion depth ~log2(n / 128).
+__device__ double np_pairwise_sum(const double *v, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; ++i) r = add(r, v[i]);
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = v[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = add(r[j], v[i + j]);
+    double res = add(add(add(r[0], r[1]), add(r[2], r[3])), add(add(r[4], r[5]), add(r[6], r[7])));
+    for (; i < n; ++i) res = add(res, v[i]);
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return add(np_pairwise_sum(v, n2), np_pairwise_sum(v + n2, n - n2));
+}
+
+// B_probe = mean(sqrt(b2[cells])) (model.py:415-425); one block.  The value
+// goes to log[par->step - 1] inside a run, else to *out.
+__global__ void k_probe(CondArgs a, const int32_t *__restrict__ cells, int64_t n, const double *__restrict__ state,
+                        double *__restrict__ vals, const StepParams *par, double *log, double *out) {
+  for (int64_t q = threadIdx.x; q < n; q += blockDim.x) vals[q] = sqrt(cell_b2(a, cells[q], state));
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const double v = add(0.0, np_pairwise_sum(vals, n)) / (double)n;
+  if (log) log[par->step - 1] = v;
+  else *out = v;
 }
 
 // y = K_c(state) x with nu precomputed (model.py:502-509)
@@ -1587,9 +1639,76 @@ static int enqueue_step(mq_ctx *ctx, double *hist) {
     rc = recover_enqueue(ctx);
     if (rc) return rc;
   }
+  if (s->n_probe > 0) {
+    k_probe<<<1, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, ctx->d_ac, s->d_probe_vals, s->d_par,
+                                        s->d_probe_log, nullptr);
+    MQ_CUDA(cudaGetLastError());
+    ctx->launches += 1;
+  }
   k_step_done<<<grid_for(ctx, n_c), 256, 0, ctx->stream>>>(s->d_run, s->d_par, ctx->d_ac, hist, n_c);
   MQ_CUDA(cudaGetLastError());
   ctx->launches += 1;
+  return MQ_OK;
+}
+
+int mq_probe_set(mq_ctx *ctx, const int64_t *cells, int64_t n) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  if (n < 0 || (n > 0 && !cells)) { set_error("invalid probe cell list"); return MQ_INVALID; }
+  const std::vector<int64_t> &ids = ctx->topo.cell_ids;
+  std::vector<int32_t> loc((size_t)n);
+  for (int64_t q = 0; q < n; ++q) {
+    auto it = std::lower_bound(ids.begin(), ids.end(), cells[q]);
+    if (it == ids.end() || *it != cells[q]) {
+      set_error("probe cell is not a conductor cell (the device probe reads the conducting state only)");
+      return MQ_INVALID;
+    }
+    loc[q] = (int32_t)(it - ids.begin());
+  }
+  cudaFree(s->d_probe);
+  cudaFree(s->d_probe_vals);
+  s->d_probe = nullptr;
+  s->d_probe_vals = nullptr;
+  s->n_probe = 0;
+  if (n > 0) {
+    MQ_CUDA(cudaMalloc(&s->d_probe, sizeof(int32_t) * n));
+    MQ_CUDA(cudaMalloc(&s->d_probe_vals, sizeof(double) * n));
+    MQ_CUDA(cudaMemcpy(s->d_probe, loc.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  }
+  s->n_probe = n;
+  if (s->graph_exec) { cudaGraphExecDestroy(s->graph_exec); s->graph_exec = nullptr; }
+  return MQ_OK;
+}
+
+int mq_probe_b(mq_ctx *ctx, const double *a_c_host, double *out) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  if (s->n_probe <= 0) { set_error("probe cell set is empty"); return MQ_INVALID; }
+  const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
+  const double *state = ctx->d_ac;
+  if (a_c_host) {
+    MQ_CUDA(cudaMemcpyAsync(ctx->d_ac_x, a_c_host, sizeof(double) * n_c, cudaMemcpyHostToDevice, ctx->stream));
+    state = ctx->d_ac_x;
+  }
+  double *tmp = nullptr;
+  MQ_CUDA(cudaMalloc(&tmp, sizeof(double)));
+  k_probe<<<1, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, state, s->d_probe_vals, nullptr, nullptr,
+                                      tmp);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, tmp, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return cuda_fail(e, "probe");
+  ctx->launches += 1;
+  return MQ_OK;
+}
+
+int mq_run_probe_log(mq_ctx *ctx, int64_t n, double *out) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  if (s->n_probe <= 0) { set_error("probe cell set is empty"); return MQ_INVALID; }
+  if (n < 0 || n > s->n_enqueued) { set_error("more probe rows than steps run"); return MQ_INVALID; }
+  if (n > 0) MQ_CUDA(cudaMemcpy(out, s->d_probe_log, sizeof(double) * n, cudaMemcpyDeviceToHost));
   return MQ_OK;
 }
 
@@ -1612,6 +1731,13 @@ int mq_run_prepare(mq_ctx *ctx, int64_t n_steps, const double *dt, const double 
   if ((recover_every_step != 0) != s->recover_every_step && s->graph_exec) {
     cudaGraphExecDestroy(s->graph_exec);
     s->graph_exec = nullptr;
+  }
+  if (s->n_probe > 0 && s->probe_cap < n_steps) {
+    cudaFree(s->d_probe_log);
+    s->d_probe_log = nullptr;
+    MQ_CUDA(cudaMalloc(&s->d_probe_log, sizeof(double) * n_steps));
+    s->probe_cap = n_steps;
+    if (s->graph_exec) { cudaGraphExecDestroy(s->graph_exec); s->graph_exec = nullptr; }
   }
   s->recover_every_step = recover_every_step != 0;
   s->per_step = per;

@@ -250,6 +250,7 @@ int build_topology(const mq_grid_desc &g, Topology &t, std::string &err) {
     }
   }
   t.n_cells_c = (int64_t)cells.size();
+  t.cell_ids = cells;
   // per cond edge: its faces ascending face id with the incidence sign
   const int64_t n_c = (int64_t)t.c_global.size();
   std::vector<std::vector<std::pair<int32_t, int8_t>>> ef(n_c);

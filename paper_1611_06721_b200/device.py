@@ -208,6 +208,18 @@ class KnOperator:
         return self.grid.kn_apply(x)
 
 
+def default_probe_cells(material) -> np.ndarray:
+    """Conductor cells of the median k layer, global ids (model.py:562-566)."""
+    mat = np.asarray(material)
+    ijk = np.argwhere(mat == CONDUCTOR)
+    if ijk.size == 0:
+        raise ValueError("no conductor cells")
+    mid_k = int(np.median(ijk[:, 2]))
+    sel = ijk[ijk[:, 2] == mid_k]
+    _, ny, nz = mat.shape
+    return ((sel[:, 0] * ny + sel[:, 1]) * nz + sel[:, 2]).astype(np.int64)
+
+
 def sinusoid(freq: float = 50.0) -> Callable[[float], float]:
     """Coil waveform sin(2 pi f t) of the BASELINE configs."""
     w = 2.0 * np.pi * freq

@@ -19,8 +19,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from ._lib import check, dptr, f64
-from .device import DeviceGrid, Problem
+from ._lib import check, dptr, f64, i64ptr
+from .device import DeviceGrid, Problem, default_probe_cells
 from .krylov import PcgConfig, Preconditioner, SolveReport
 from .startvec import RhsFamily, family_index, solver_cfg
 
@@ -145,6 +145,25 @@ class SchurOperator:
         out = np.empty(self.grid.n_c)
         check(self.lib.mq_state_get(self.grid.ctx, dptr(out), None))
         return out
+
+    def set_probe(self, cells=None) -> np.ndarray:
+        """Device B probe over ``cells`` (global conductor-cell ids; default
+        model.py:562-566).  Every later device step logs B_probe."""
+        cells = default_probe_cells(self.problem.material) if cells is None else \
+            np.ascontiguousarray(cells, dtype=np.int64)
+        if cells.size == 0:
+            raise ValueError("probe cell set is empty")
+        check(self.lib.mq_probe_set(self.grid.ctx, i64ptr(cells), int(cells.size)))
+        self.probe_cells = cells
+        return cells
+
+    def probe_b(self, a_c=None) -> float:
+        """Mean |B| over the probe cells of ``a_c`` (default: the device
+        state), model.py:415-425."""
+        out = ctypes.c_double()
+        arg = dptr(f64(a_c, self.grid.n_c, "state")) if a_c is not None else None
+        check(self.lib.mq_probe_b(self.grid.ctx, arg, ctypes.byref(out)))
+        return float(out.value)
 
 
 @dataclass(frozen=True)
@@ -307,6 +326,18 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
     if dt <= 0:
         raise ValueError("dt must be positive")
     n_c, n_n = op.grid.n_c, op.grid.n_n
+    # probe: a host callable (a_c, a_n, t) -> float as in the reference, or
+    # "device" / an array of conductor-cell ids for the device probe, which
+    # logs B_probe inside the step graph
+    host_probe = callable(probe)
+    device_probe = probe is not None and not host_probe
+    if device_probe:
+        if isinstance(probe, str):
+            if probe != "device":
+                raise ValueError(f"probe must be a callable, 'device' or cell ids, got {probe!r}")
+            op.set_probe()
+        else:
+            op.set_probe(probe)
     a_c = np.zeros(n_c) if a0 is None else f64(a0, n_c, "initial state").copy()
     wave = op.problem.waveform
     dts, outs = step_times(t_end, dt, output_period, max_steps)
@@ -314,7 +345,10 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
 
     def emit(t_row, a_c_row, a_n_row, iters_src, iters_prev, iters_cur):
         rows["t"].append(t_row)
-        rows["b"].append(float(probe(a_c_row, a_n_row, t_row)) if probe else 0.0)
+        if host_probe:
+            rows["b"].append(float(probe(a_c_row, a_n_row, t_row)))
+        else:
+            rows["b"].append(op.probe_b(a_c_row) if device_probe else 0.0)
         rows["src"].append(float(np.mean(iters_src)) if len(iters_src) else 0.0)
         rows["prev"].append(float(np.mean(iters_prev)) if len(iters_prev) else 0.0)
         rows["cur"].append(float(np.mean(iters_cur)) if len(iters_cur) else 0.0)
@@ -339,7 +373,7 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
     step_iters = np.zeros((n, 4), dtype=np.int32)
     hist = np.empty((n, n_c)) if record_states else None
     failed = ctypes.c_int64(-1)
-    if all_out and probe is None:
+    if all_out and not host_probe:
         rc = op.lib.mq_run_explicit(op.grid.ctx, n, dptr(dt_tab), dptr(wave_tab), 1,
                                     1 if use_graph else 0, _lib.i32ptr(step_iters),
                                     dptr(hist) if hist is not None else None, ctypes.byref(failed))
@@ -347,10 +381,13 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
             raise StepFailureError(f"non-finite conducting state at step {failed.value}")
         check(rc)
         a_c = op._get_state()
+        blog = np.zeros(n)
+        if device_probe and n > 0:
+            check(op.lib.mq_run_probe_log(op.grid.ctx, n, dptr(blog)))
         # rows: one per step, window means over that step's solves
         for m in range(n):
             rows["t"].append(tt[m + 1])
-            rows["b"].append(0.0)
+            rows["b"].append(float(blog[m]))
             rows["src"].append(float(np.mean(step_iters[m, [0, 2]])))
             rows["prev"].append(float(step_iters[m, 1]))
             rows["cur"].append(float(step_iters[m, 3]))

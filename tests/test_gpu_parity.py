@@ -303,6 +303,50 @@ def test_transient_config0_device_loop(gpu_ok, strategy, nsteps):
     assert np.array_equal(res_g.step_iterations, it)
 
 
+@pytest.mark.parametrize("index", [0, 2])
+def test_device_probe_bitwise_vs_reference(gpu_ok, golden, index):
+    """mq_probe_b (model.py:415-425) on the reference's own probe states:
+    b2 in the reference's operation order and numpy's pairwise mean give the
+    reference's value bit for bit."""
+    from pathlib import Path
+    from tests.golden.make_golden_probe import probe_states
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import SchurOperator
+    ref = np.load(Path(__file__).parent / "golden" / "reference_probe.npz")
+    op = SchurOperator(C.make_problem(index), strategy="previous")
+    cells = op.set_probe()
+    assert np.array_equal(cells, ref[f"c{index}_probe_cells"])
+    vals = [op.probe_b(a_c) for a_c, _ in probe_states(index, op.grid.n_c, op.grid.n_n, golden)]
+    assert np.array_equal(np.array(vals), ref[f"c{index}_probe_values"])
+    with pytest.raises(Exception):
+        op.set_probe(np.array([0], dtype=np.int64))   # an air cell
+
+
+def test_device_probe_in_run(gpu_ok):
+    """run_explicit(probe="device"): B_probe logged inside the step graph
+    equals the oracle's probe of its own trajectory within the field bar."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, run_explicit
+    spec, m = oracle_model(0)
+    nsteps = 20
+    tr = O.run(m, O.sinusoid(50.0), spec.dt, nsteps, strategy="cspe", rel_tol=1e-8, max_cols=5)
+    cells = O.default_probe_cells(m, (spec.N,) * 3)
+    ref_b = np.array([O.probe_b(m, O.full_interior(m, a, b), cells)
+                      for a, b in zip(tr.a_c, tr.a_n)])
+    for use_graph in (False, True):
+        res = run_explicit(C.make_problem(0), t_end=nsteps * spec.dt, dt=spec.dt, strategy="cspe",
+                           pcg=PcgConfig(rel_tol=1e-8), output_period=spec.dt * (1 - 1e-3),
+                           max_cols=5, probe="device", use_graph=use_graph)
+        b = res.probe_b
+        assert b.shape == (nsteps + 1,)
+        assert np.max(np.abs(b - ref_b) / np.abs(ref_b).max()) <= REL_FIELD
+    # segmented loop (outputs every 2nd step) probes the same states
+    res2 = run_explicit(C.make_problem(0), t_end=nsteps * spec.dt, dt=spec.dt, strategy="cspe",
+                        pcg=PcgConfig(rel_tol=1e-8), output_period=2 * spec.dt * (1 - 1e-3),
+                        max_cols=5, probe="device")
+    assert np.max(np.abs(res2.probe_b - ref_b[::2]) / np.abs(ref_b).max()) <= REL_FIELD
+
+
 def test_single_step_api_matches_oracle(gpu_ok):
     """explicit_euler_step / recover_an / SchurOperator.solve_kn twins."""
     from paper_1611_06721_b200 import configs as C

@@ -10,6 +10,7 @@ when numpy/OpenBLAS are the ones the fixtures were produced with).
 from __future__ import annotations
 
 import hashlib
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -152,3 +153,17 @@ def test_config1_first_steps(golden):
     norms = np.array([np.linalg.norm(a) for a in tr.a_c])
     ref = golden["c1_run_cspe_a_c_norms"]
     assert np.all(np.abs(norms - ref) <= 1e-10 * np.maximum(ref, 1e-300))
+
+
+@pytest.mark.parametrize("index", [0, 2])
+def test_probe_b_matches_reference(golden, index):
+    """model.py:415-425 probe_b and the default probe cells (model.py:562-566),
+    against tests/golden/reference_probe.npz (tests/golden/make_golden_probe.py)."""
+    from tests.golden.make_golden_probe import probe_states
+    ref = np.load(Path(__file__).parent / "golden" / "reference_probe.npz")
+    spec, m = oracle_model(index)
+    cells = O.default_probe_cells(m, (spec.N,) * 3)
+    assert np.array_equal(cells, ref[f"c{index}_probe_cells"])
+    vals = [O.probe_b(m, O.full_interior(m, a_c, a_n), cells)
+            for a_c, a_n in probe_states(index, m.n_c, m.n_n, golden)]
+    assert np.array_equal(np.array(vals), ref[f"c{index}_probe_values"])
