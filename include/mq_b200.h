@@ -123,6 +123,10 @@ int mq_map_global_to_noncond(const mq_ctx *ctx, const int64_t *gid, int64_t n, i
 int mq_ctx_sync(mq_ctx *ctx);
 /* optional external stream (cudaStream_t as void*; NULL restores own) */
 int mq_ctx_set_stream(mq_ctx *ctx, void *stream);
+/* Run this context's PCG kernel on a slice of `sms` SMs (0 = whole GPU), so
+ * that several contexts (ensemble members, configs[3]) step concurrently on
+ * their own streams.  No reference counterpart (its members run one by one). */
+int mq_ctx_set_sm_budget(mq_ctx *ctx, int32_t sms);
 
 /* ---- device vectors (padded layout) ------------------------------------- */
 int mq_vec_alloc(mq_ctx *ctx, double **dev);            /* zero-filled */

@@ -86,6 +86,7 @@ SIGNATURES = {
     "mq_map_global_to_noncond": (I32, [VP, c_int64_p, I64, c_int64_p]),
     "mq_ctx_sync": (I32, [VP]),
     "mq_ctx_set_stream": (I32, [VP, VP]),
+    "mq_ctx_set_sm_budget": (I32, [VP, I32]),
     "mq_vec_alloc": (I32, [VP, ctypes.POINTER(VP)]),
     "mq_vec_free": (I32, [VP, VP]),
     "mq_vec_upload": (I32, [VP, c_double_p, VP]),

@@ -162,7 +162,7 @@ int mq_ctx_create(const mq_grid_desc *desc, int32_t device, mq_ctx **out) {
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_tmp0, sizeof(double) * t.L.total);
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_tmp1, sizeof(double) * t.L.total);
   if (!rc) rc = pcg_stencil_grid(t.L.words, &ctx->pcg_grid);
-  if (!rc) rc = brick_pcg_setup(t.L, t.nx, t.ny, t.nz, &ctx->brick_grid, &ctx->geo);
+  if (!rc) rc = brick_pcg_setup(t.L, t.nx, t.ny, t.nz, 0, &ctx->brick_grid, &ctx->geo);
   if (!rc) rc = resident_pcg_setup(t.nx, t.ny, t.nz, &ctx->res_grid, &ctx->res_geo);
   {
     // default: shared-memory-resident kernel when the bricks fit on chip,
@@ -250,6 +250,27 @@ int mq_map_global_to_noncond(const mq_ctx *ctx, const int64_t *gid, int64_t n, i
 
 int mq_ctx_sync(mq_ctx *ctx) {
   MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  return MQ_OK;
+}
+
+int mq_ctx_set_sm_budget(mq_ctx *ctx, int32_t sms) {
+  int dev_sms = 0;
+  MQ_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  if (sms < 0) { set_error("SM budget must be nonnegative"); return MQ_INVALID; }
+  if (sms == 0 || sms >= dev_sms) {
+    int rc = brick_pcg_setup(ctx->topo.L, ctx->topo.nx, ctx->topo.ny, ctx->topo.nz, 0, &ctx->brick_grid, &ctx->geo);
+    if (rc) return rc;
+    ctx->pcg_variant = ctx->res_grid > 0 ? 2 : 0;
+    ctx->sm_budget = 0;
+  } else {
+    // a slice of the GPU: the TMA brick kernel sized for `sms` SMs (the
+    // resident kernel needs one CTA per brick on the whole chip)
+    int rc = brick_pcg_setup(ctx->topo.L, ctx->topo.nx, ctx->topo.ny, ctx->topo.nz, sms, &ctx->brick_grid, &ctx->geo);
+    if (rc) return rc;
+    ctx->pcg_variant = 0;
+    ctx->sm_budget = sms;
+  }
+  solver_graph_reset(ctx);
   return MQ_OK;
 }
 

@@ -118,6 +118,7 @@ struct mq_ctx {
   int64_t launches = 0;
   cudaEvent_t ev_pool[2 * 16] = {};
   int ev_n = 0;
+  int sm_budget = 0;  // 0 = all SMs; else the PCG kernel runs on this many SMs
   void *flush_buf = nullptr;
   unsigned flush_val = 1;
 };
@@ -132,13 +133,14 @@ int ctx_pcg(mq_ctx *ctx, const double *b, double *x, int x0_mode, double rel_tol
             int use_jac, mq_solve_report *rep);
 int conducting_init(mq_ctx *ctx);
 void solver_free(mq_ctx *ctx);
+void solver_graph_reset(mq_ctx *ctx);
 
 int coop_grid(const void *kernel, int want_blocks, int *out);
 int launch_pcg_stencil(const StencilPcgArgs &args, int grid, cudaStream_t s);
 int pcg_stencil_grid(int64_t words, int *out);
 int launch_pcg_csr(const CsrPcgArgs &args, int grid, cudaStream_t s);
 int pcg_csr_grid(int64_t n, int *out);
-int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int *grid, BrickGeo *geo);
+int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int sm_cap, int *grid, BrickGeo *geo);
 int launch_pcg_brick(const StencilPcgArgs &args, const BrickGeo &geo, int grid, cudaStream_t s);
 int launch_kn_apply_brick(const Lay &L, const BrickGeo &geo, const uint32_t *mask, double dg, double of,
                           const double *x, double *y, int sms, cudaStream_t s);

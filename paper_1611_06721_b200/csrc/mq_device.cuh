@@ -49,7 +49,13 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double *smem /* NV*kW
   __syncthreads();
 }
 
-// Sum partials[q*G + 0..G) in a fixed order; identical in every CTA.
+// Sum partials[q*G + 0..G) in a fixed order; identical in every CTA.  Lane l
+// adds b = l, l+32, ... in order; the first kPB loads per lane are issued
+// back to back so the read costs one L2 round trip.
+#ifndef MQ_PSUM_BATCH
+#define MQ_PSUM_BATCH 10
+#endif
+constexpr int kPB = MQ_PSUM_BATCH;  // G <= 32 * kPB in one batch
 template <int NV>
 __device__ __forceinline__ void grid_partials_sum(const double *partials, int G, double (&out)[NV],
                                                   double *smem) {
@@ -57,8 +63,17 @@ __device__ __forceinline__ void grid_partials_sum(const double *partials, int G,
   if (warp == 0) {
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
+      double v[kPB > 0 ? kPB : 1];
+#pragma unroll
+      for (int u = 0; u < kPB; ++u) {
+        const int b = lane + 32 * u;
+        v[u] = b < G ? __ldcg(partials + (int64_t)q * G + b) : 0.0;
+      }
       double s = 0.0;
-      for (int b = lane; b < G; b += 32) s = add(s, __ldcg(partials + (int64_t)q * G + b));
+#pragma unroll
+      for (int u = 0; u < kPB; ++u)
+        if (lane + 32 * u < G) s = add(s, v[u]);
+      for (int b = lane + 32 * kPB; b < G; b += 32) s = add(s, __ldcg(partials + (int64_t)q * G + b));
       s = warp_sum(s);
       if (lane == 0) smem[q] = s;
     }
@@ -96,6 +111,10 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
   return v;
 }
 
+// (An acq_rel arrival that lets the last CTA skip polling, and a failure bit
+// folded into the counter, measured no faster at 64^3 and made the TMA brick
+// kernel's K1 ~30 % slower at 128^3 through its register allocation; kept
+// as is.)
 __device__ __forceinline__ bool grid_sync(GridBar *bar) {
   __shared__ int s_fail;
   __syncthreads();

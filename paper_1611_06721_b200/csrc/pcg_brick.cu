@@ -592,11 +592,12 @@ static BrickGeo make_geo(int nx, int ny, int nz, int resident) {
   return g;
 }
 
-int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int *grid, BrickGeo *geo) {
+int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int sm_cap, int *grid, BrickGeo *geo) {
   (void)L;
   int dev = 0, sms = 0, per = 0;
   MQ_CUDA(cudaGetDevice(&dev));
   MQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (sm_cap > 0 && sm_cap < sms) sms = sm_cap;
   MQ_CUDA(cudaFuncSetAttribute(pcg_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
   MQ_CUDA(cudaFuncSetAttribute(kn_apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
   MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pcg_tma_kernel, kBlock, kTmaSmem));

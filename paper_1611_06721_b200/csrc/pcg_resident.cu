@@ -107,6 +107,10 @@ __device__ __forceinline__ double stencil_r(int c, double dg, double of, V v) {
   return s;
 }
 
+// LI = planes per brick (compile time, so that every row's stencil chain is
+// unrolled and the 3*LI independent chains interleave; bricks of a chunking
+// that does not divide nx have li = LI or LI-1 planes).
+template <int LI>
 __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
   extern __shared__ __align__(16) double rsm[];
   __shared__ double red[3 * RW];
@@ -291,16 +295,33 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
       }
       __syncthreads();
       double v1[1] = {0.0};
-      for (int l = 0; l < li; ++l)
+      {
+        // all LI*3 rows unconditionally (rows past li or inactive read
+        // allocated shared memory and are discarded): independent chains
+        double av[LI * 3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          if (!(own_ok && is_act(l, c))) continue;
-          const double av = stencil_r(c, dg, of, V(l, c));
-          AP[Oidx(l, c)] = av;
-          v1[0] = add(v1[0], mul(P[Pidx(l + 1, c, s_own)], av));
-        }
+        for (int l = 0; l < LI; ++l)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) av[3 * l + c] = stencil_r(c, dg, of, V(l, c));
+#pragma unroll
+        for (int l = 0; l < LI; ++l)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if (l < li && own_ok && is_act(l, c)) {
+              AP[Oidx(l, c)] = av[3 * l + c];
+              v1[0] = add(v1[0], mul(P[Pidx(l + 1, c, s_own)], av[3 * l + c]));
+            }
+          }
+      }
       block_sum_r<1>(v1, red);
       if (threadIdx.x == 0) a.partials[3 * G + blockIdx.x] = v1[0];
+      // own x (written only by this thread) fetched while the barrier drains
+      double xo[LI * 3];
+#pragma unroll
+      for (int l = 0; l < LI; ++l)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if (l < li && own_ok && is_act(l, c)) xo[3 * l + c] = __ldcg(a.x + own_e(l, c));
       ++applies;
       stamp(4 * (it - 1) + 1);
       if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
@@ -312,14 +333,8 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
       alpha = rz / pap;
       // ---- K2: x += alpha p, r -= alpha Ap (own), publish r ----
       double v2[2] = {0.0, 0.0};
-      double xo[RLI_MAX * 3];
 #pragma unroll
-      for (int l = 0; l < RLI_MAX; ++l)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          if (l < li && own_ok && is_act(l, c)) xo[3 * l + c] = __ldcg(a.x + own_e(l, c));
-#pragma unroll
-      for (int l = 0; l < RLI_MAX; ++l)
+      for (int l = 0; l < LI; ++l)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           if (!(l < li && own_ok && is_act(l, c))) continue;
@@ -371,6 +386,16 @@ done:
 }
 
 // ---------------------------------------------------------------------------
+static const void *resident_kernel_for(int li_max) {
+  switch (li_max) {
+    case 1: return (const void *)pcg_resident_kernel<1>;
+    case 2: return (const void *)pcg_resident_kernel<2>;
+    case 3: return (const void *)pcg_resident_kernel<3>;
+    case 4: return (const void *)pcg_resident_kernel<4>;
+    default: return (const void *)pcg_resident_kernel<5>;
+  }
+}
+
 // Returns 0 with *grid = 0 when the grid does not fit the resident scheme.
 int resident_pcg_setup(int nx, int ny, int nz, int *grid, BrickGeo *geo_out) {
   *grid = 0;
@@ -394,9 +419,10 @@ int resident_pcg_setup(int nx, int ny, int nz, int *grid, BrickGeo *geo_out) {
   if (2 * tiles * best < sms) return MQ_OK;
   const int li_max = (nx + best - 1) / best;
   const size_t smem = res_smem_bytes(li_max);
-  MQ_CUDA(cudaFuncSetAttribute(pcg_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const void *fn = resident_kernel_for(li_max);
+  MQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per = 0;
-  MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pcg_resident_kernel, RT, smem));
+  MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, RT, smem));
   if (per < 1 || tiles * best > sms * per) return MQ_OK;
   geo_out->nx = nx;
   geo_out->ny = ny;
@@ -423,7 +449,7 @@ int launch_pcg_resident(const StencilPcgArgs &args, const BrickGeo &geo, int gri
   const size_t smem = res_smem_bytes(A.g.li_max);
   MQ_CUDA(cudaMemsetAsync(&args.bar->count, 0, sizeof(unsigned long long), s));
   void *params[] = {&A};
-  MQ_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_resident_kernel, dim3(grid), dim3(RT), params, smem, s));
+  MQ_CUDA(cudaLaunchCooperativeKernel(resident_kernel_for(A.g.li_max), dim3(grid), dim3(RT), params, smem, s));
   return MQ_OK;
 }
 

@@ -84,6 +84,14 @@ static int s_alloc(mq_ctx *ctx, SolverHost *s, void **p, size_t bytes) {
   return MQ_OK;
 }
 
+void solver_graph_reset(mq_ctx *ctx) {
+  SolverHost *s = ctx->solver;
+  if (s && s->graph_exec) {
+    cudaGraphExecDestroy(s->graph_exec);
+    s->graph_exec = nullptr;
+  }
+}
+
 void solver_free(mq_ctx *ctx) {
   SolverHost *s = ctx->solver;
   if (!s) return;
