@@ -6,14 +6,18 @@
 // Li <= 5 i-planes, all three edge components.  For the whole solve the
 // brick's r, Ap and search direction p (the latter with a one-node halo ring)
 // stay in shared memory.  Per iteration:
-//   K1: own p_new = M^-1 r + beta p (in place), halo p_new recomputed from the
-//       neighbours' published r and p_old (L2), own p_new published (ping-pong
-//       buffer), Ap = K_n p_new from shared memory, partial p.Ap
-//   K2: x += alpha p (global, own), r -= alpha Ap (shared), r published,
-//       partials r.r, r.z
-// Global traffic per iteration is the halo ring plus 4 own streams (publish
-// p, publish r, x read/write), all L2-resident at these sizes; the two grid
-// barriers and the shared-memory stencil set the iteration time.
+//   K1: own p_new = M^-1 r + beta p (in place); halo p_new = M^-1 r + beta p
+//       from the neighbours' published r and the CTA's own halo copy of
+//       p_old (computed by the previous K1 from the owner's inputs with the
+//       owner's arithmetic, hence bit-identical: p is never published);
+//       Ap = K_n p_new from shared memory (all 3*Li row chains unrolled and
+//       interleaved), partial p.Ap
+//   K2: x += alpha p (global, own; x prefetched before the barrier),
+//       r -= alpha Ap (shared), r published, partials r.r, r.z
+// Global traffic per iteration is the r halo ring plus 3 own streams
+// (publish r, x read/write), all L2-resident at these sizes; the two grid
+// barriers (~1.2 us each, tools/barrier_bench.cu), L2 latency of the halo
+// and the shared-memory stencil (128 B/clk/SM) set the iteration time.
 #include "mq_device.cuh"
 
 namespace mq {
@@ -237,7 +241,6 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
   }
   int status = MQ_OK, iters = 0, converged = 0;
   double rel = 0.0, bnorm = 0.0, alpha = 0.0, rz = 0.0;
-  bool pold_is_a = true;  // published p_old lives in pa, p_new goes to pb
   int applies = (x0_mode == 2) ? 0 : 1;
   if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
   {
@@ -252,44 +255,47 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
     double beta = 0.0;
     bool first = true;
     for (int it = 1; it <= a.max_iter; ++it) {
-      const double *pold_g = pold_is_a ? a.pa : a.pb;
-      double *pnew_g = pold_is_a ? a.pb : a.pa;
-      // ---- K1: own p_new in place, halo p_new from published r / p_old ----
+      // ---- K1: own p_new in place; halo p_new = M^-1 r + beta p_old from the
+      // neighbours' published r and this CTA's own copy of the halo p_old
+      // (the previous K1 computed it with the owner's inputs and arithmetic,
+      // so it equals the owner's value bit for bit: p is never published) ----
       for (int l = 0; l < li; ++l)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const double rq = R[Oidx(l, c)];
           const double z = jac ? mul(inv, rq) : rq;
           const size_t pi = Pidx(l + 1, c, s_own);
-          const double pv = first ? z : add(z, mul(beta, P[pi]));
-          P[pi] = pv;
-          if (own_ok && is_act(l, c)) pnew_g[own_e(l, c)] = pv;
+          P[pi] = first ? z : add(z, mul(beta, P[pi]));
         }
-      for (int h0 = tid; h0 < nhalo; h0 += 2 * RT) {
-        double rv[2][3], pv[2][3];
-        int hl[2], hs[2];
-        bool hok[2][3];
+#ifndef MQ_RES_HU
+#define MQ_RES_HU 2
+#endif
+      constexpr int HU = MQ_RES_HU;  // halo positions per thread and round
+      for (int h0 = tid; h0 < nhalo; h0 += HU * RT) {
+        double rv[HU][3];
+        int hl[HU], hs[HU];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < HU; ++u) {
           const int h = h0 + u * RT;
           hl[u] = -1;
           if (h < nhalo) {
             halo_slot(h, hl[u], hs[u]);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-              const int64_t e = halo_e(hl[u], hs[u], c, hok[u][c]);
-              rv[u][c] = hok[u][c] ? __ldcg(a.r + e) : 0.0;
-              pv[u][c] = (hok[u][c] && !first) ? __ldcg(pold_g + e) : 0.0;
+              bool ok;
+              const int64_t e = halo_e(hl[u], hs[u], c, ok);
+              rv[u][c] = ok ? __ldcg(a.r + e) : 0.0;
             }
           }
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < HU; ++u) {
           if (hl[u] < 0) continue;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             const double z = jac ? mul(inv, rv[u][c]) : rv[u][c];
-            P[Pidx(hl[u], c, hs[u])] = first ? z : add(z, mul(beta, pv[u][c]));
+            const size_t pi = Pidx(hl[u], c, hs[u]);
+            P[pi] = first ? z : add(z, mul(beta, P[pi]));
           }
         }
       }
@@ -366,7 +372,6 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
       beta = rz_new / rz;
       rz = rz_new;
       first = false;
-      pold_is_a = !pold_is_a;
     }
     if (status == MQ_OK && !converged) status = MQ_NOT_CONVERGED;
   }
