@@ -84,6 +84,74 @@ __device__ __forceinline__ void grid_partials_sum(const double *partials, int G,
   __syncthreads();
 }
 
+// grid_partials_sum_all split in two: warp 0 issues its loads, other work
+// (other warps' loads) can be issued before warp 0 consumes them.
+template <int NV, int PB>
+__device__ __forceinline__ void psum_issue(const double *partials, int G, double (&v)[NV][PB]) {
+  const int lane = threadIdx.x & 31;
+  if ((threadIdx.x >> 5) == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+#pragma unroll
+      for (int u = 0; u < PB; ++u) {
+        const int b = lane + 32 * u;
+        v[q][u] = b < G ? __ldcg(partials + (int64_t)q * G + b) : 0.0;
+      }
+  }
+}
+
+template <int NV, int PB>
+__device__ __forceinline__ void psum_finish(const double (&v)[NV][PB], int G, double (&out)[NV], double *smem) {
+  const int lane = threadIdx.x & 31;
+  if ((threadIdx.x >> 5) == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int u = 0; u < PB; ++u)
+        if (lane + 32 * u < G) s = add(s, v[q][u]);
+      s = warp_sum(s);
+      if (lane == 0) smem[q] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) out[q] = smem[q];
+  __syncthreads();
+}
+
+// Same sums with every load of all NV rows issued before the first add (one
+// L2 round trip for all NV values); G <= 32 * PB.  Used by kernels with
+// registers to spare.
+template <int NV, int PB>
+__device__ __forceinline__ void grid_partials_sum_all(const double *partials, int G, double (&out)[NV],
+                                                      double *smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    double v[NV][PB];
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+#pragma unroll
+      for (int u = 0; u < PB; ++u) {
+        const int b = lane + 32 * u;
+        v[q][u] = b < G ? __ldcg(partials + (int64_t)q * G + b) : 0.0;
+      }
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int u = 0; u < PB; ++u)
+        if (lane + 32 * u < G) s = add(s, v[q][u]);
+      s = warp_sum(s);
+      if (lane == 0) smem[q] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) out[q] = smem[q];
+  __syncthreads();
+}
+
 // ---- grid-wide barrier (cooperative launch guarantees co-residency) -------
 // One release-atomic arrival per CTA on a monotonic 64-bit counter (zeroed
 // before every launch), then acquire-polling until all G CTAs of this

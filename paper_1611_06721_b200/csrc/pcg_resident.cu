@@ -111,6 +111,55 @@ __device__ __forceinline__ double stencil_r(int c, double dg, double of, V v) {
   return s;
 }
 
+#ifndef MQ_RES_HU
+#define MQ_RES_HU 4
+#endif
+constexpr int HU = MQ_RES_HU;  // halo positions per thread (one round)
+static_assert(2 * RHP + RLI_MAX * RRING <= HU * RT, "halo must fit one round");
+
+#ifndef MQ_RES_SLIDE
+#define MQ_RES_SLIDE 1
+#endif
+
+// The 15 distinct values of one P plane that the three stencil rows of the
+// planes i-1, i, i+1 read around the own position (component, dj, dk).
+struct PlaneVals {
+  double xo, xjm, xjp, xkm, xkp;     // x: own, j-1, j+1, k-1, k+1
+  double yo, yjm, ykm, ykp, yjmkp;   // y: own, j-1, k-1, k+1, (j-1,k+1)
+  double zo, zjm, zjp, zkm, zjpkm;   // z: own, j-1, j+1, k-1, (j+1,k-1)
+};
+
+__device__ __forceinline__ void load_plane(const double *P, int pl, int s, PlaneVals &v) {
+  const double *x = P + ((size_t)pl * 3 + 0) * RHP + s;
+  const double *y = P + ((size_t)pl * 3 + 1) * RHP + s;
+  const double *z = P + ((size_t)pl * 3 + 2) * RHP + s;
+  v.xo = x[0]; v.xjm = x[-RHK]; v.xjp = x[RHK]; v.xkm = x[-1]; v.xkp = x[1];
+  v.yo = y[0]; v.yjm = y[-RHK]; v.ykm = y[-1]; v.ykp = y[1]; v.yjmkp = y[-RHK + 1];
+  v.zo = z[0]; v.zjm = z[-RHK]; v.zjp = z[RHK]; v.zkm = z[-1]; v.zjpkm = z[RHK - 1];
+}
+
+// value (component cc, offset dj, dk) of plane q; arguments are literals in
+// stencil_r, so the selection folds away
+__device__ __forceinline__ double pick(const PlaneVals &q, int cc, int dj, int dk) {
+  if (cc == 0) {
+    if (dj == -1) return q.xjm;
+    if (dj == 1) return q.xjp;
+    if (dk == -1) return q.xkm;
+    if (dk == 1) return q.xkp;
+    return q.xo;
+  }
+  if (cc == 1) {
+    if (dj == -1) return dk == 1 ? q.yjmkp : q.yjm;
+    if (dk == -1) return q.ykm;
+    if (dk == 1) return q.ykp;
+    return q.yo;
+  }
+  if (dj == 1) return dk == -1 ? q.zjpkm : q.zjp;
+  if (dj == -1) return q.zjm;
+  if (dk == -1) return q.zkm;
+  return q.zo;
+}
+
 // LI = planes per brick (compile time, so that every row's stencil chain is
 // unrolled and the 3*LI independent chains interleave; bricks of a chunking
 // that does not divide nx have li = LI or LI-1 planes).
@@ -192,6 +241,16 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
   auto stamp = [&](int slot) {
     if (trace && slot < 4 * 64 + 1) trace[slot] = globaltimer_ns();
   };
+  // fine phase stamps (variant builds with -DMQ_TRACE_FINE): 8 per
+  // iteration for the first 32 iterations at trace[320 + 8 (it-1) + k]
+  auto fstamp = [&](int it, int k) {
+#ifdef MQ_TRACE_FINE
+    if (trace && it <= 32) trace[320 + 8 * (it - 1) + k] = globaltimer_ns();
+#else
+    (void)it;
+    (void)k;
+#endif
+  };
   stamp(0);
   // ---- initial residual (krylov.py:209-218) ----
   double v3[3] = {0.0, 0.0, 0.0};
@@ -242,6 +301,27 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
   int status = MQ_OK, iters = 0, converged = 0;
   double rel = 0.0, bnorm = 0.0, alpha = 0.0, rz = 0.0;
   int applies = (x0_mode == 2) ? 0 : 1;
+  // the halo r values of K1, loaded in one round (issuing them right after
+  // the barrier, ahead of the partial-sum read, measured slower: the partial
+  // loads queue behind them)
+  double hr[HU][3];
+  int hl[HU], hs[HU];
+  auto issue_halo = [&]() {
+#pragma unroll
+    for (int u = 0; u < HU; ++u) {
+      const int h = tid + u * RT;
+      hl[u] = -1;
+      if (h < nhalo) {
+        halo_slot(h, hl[u], hs[u]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          bool ok;
+          const int64_t e = halo_e(hl[u], hs[u], c, ok);
+          hr[u][c] = ok ? __ldcg(a.r + e) : 0.0;
+        }
+      }
+    }
+  };
   if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
   {
     double s3[3];
@@ -255,60 +335,64 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
     double beta = 0.0;
     bool first = true;
     for (int it = 1; it <= a.max_iter; ++it) {
+      fstamp(it, 0);
       // ---- K1: own p_new in place; halo p_new = M^-1 r + beta p_old from the
       // neighbours' published r and this CTA's own copy of the halo p_old
       // (the previous K1 computed it with the owner's inputs and arithmetic,
       // so it equals the owner's value bit for bit: p is never published) ----
-      for (int l = 0; l < li; ++l)
+#pragma unroll
+      for (int l = 0; l < LI; ++l)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const double rq = R[Oidx(l, c)];
-          const double z = jac ? mul(inv, rq) : rq;
-          const size_t pi = Pidx(l + 1, c, s_own);
-          P[pi] = first ? z : add(z, mul(beta, P[pi]));
-        }
-#ifndef MQ_RES_HU
-#define MQ_RES_HU 2
-#endif
-      constexpr int HU = MQ_RES_HU;  // halo positions per thread and round
-      for (int h0 = tid; h0 < nhalo; h0 += HU * RT) {
-        double rv[HU][3];
-        int hl[HU], hs[HU];
-#pragma unroll
-        for (int u = 0; u < HU; ++u) {
-          const int h = h0 + u * RT;
-          hl[u] = -1;
-          if (h < nhalo) {
-            halo_slot(h, hl[u], hs[u]);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              bool ok;
-              const int64_t e = halo_e(hl[u], hs[u], c, ok);
-              rv[u][c] = ok ? __ldcg(a.r + e) : 0.0;
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < HU; ++u) {
-          if (hl[u] < 0) continue;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const double z = jac ? mul(inv, rv[u][c]) : rv[u][c];
-            const size_t pi = Pidx(hl[u], c, hs[u]);
+          if (l < li) {
+            const double rq = R[Oidx(l, c)];
+            const double z = jac ? mul(inv, rq) : rq;
+            const size_t pi = Pidx(l + 1, c, s_own);
             P[pi] = first ? z : add(z, mul(beta, P[pi]));
           }
         }
+      fstamp(it, 1);
+      issue_halo();
+#pragma unroll
+      for (int u = 0; u < HU; ++u) {
+        if (hl[u] < 0) continue;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double z = jac ? mul(inv, hr[u][c]) : hr[u][c];
+          const size_t pi = Pidx(hl[u], c, hs[u]);
+          P[pi] = first ? z : add(z, mul(beta, P[pi]));
+        }
       }
+      fstamp(it, 2);
       __syncthreads();
+      fstamp(it, 3);
       double v1[1] = {0.0};
       {
         // all LI*3 rows unconditionally (rows past li or inactive read
         // allocated shared memory and are discarded): independent chains
         double av[LI * 3];
+#if MQ_RES_SLIDE
+        // march along i keeping the 15 distinct neighbour values of a plane
+        // in registers: each value is read from shared memory once instead
+        // of once per row that uses it (39 -> ~17 loads per plane)
+        PlaneVals pm, p0, pp;
+        load_plane(P, 0, s_own, pm);
+        load_plane(P, 1, s_own, p0);
+#pragma unroll
+        for (int l = 0; l < LI; ++l) {
+          load_plane(P, l + 2, s_own, pp);
+          auto W = [&](int cc, int di, int dj, int dk) { return pick(di < 0 ? pm : (di > 0 ? pp : p0), cc, dj, dk); };
+#pragma unroll
+          for (int c = 0; c < 3; ++c) av[3 * l + c] = stencil_r(c, dg, of, W);
+          pm = p0;
+          p0 = pp;
+        }
+#else
 #pragma unroll
         for (int l = 0; l < LI; ++l)
 #pragma unroll
           for (int c = 0; c < 3; ++c) av[3 * l + c] = stencil_r(c, dg, of, V(l, c));
+#endif
 #pragma unroll
         for (int l = 0; l < LI; ++l)
 #pragma unroll
@@ -319,7 +403,9 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
             }
           }
       }
+      fstamp(it, 4);
       block_sum_r<1>(v1, red);
+      fstamp(it, 5);
       if (threadIdx.x == 0) a.partials[3 * G + blockIdx.x] = v1[0];
       // own x (written only by this thread) fetched while the barrier drains
       double xo[LI * 3];
@@ -333,10 +419,11 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
       if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
       stamp(4 * (it - 1) + 2);
       double s1[1];
-      grid_partials_sum<1>(a.partials + 3 * G, G, s1, tot);
+      grid_partials_sum_all<1, 5>(a.partials + 3 * G, G, s1, tot);
       const double pap = s1[0];
       if (!isfinite(pap) || pap <= 0.0) { status = MQ_INDEFINITE; iters = it; goto done; }
       alpha = rz / pap;
+      fstamp(it, 6);
       // ---- K2: x += alpha p, r -= alpha Ap (own), publish r ----
       double v2[2] = {0.0, 0.0};
 #pragma unroll
@@ -353,6 +440,7 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
           v2[0] = add(v2[0], mul(rv, rv));
           v2[1] = add(v2[1], mul(rv, z));
         }
+      fstamp(it, 7);
       block_sum_r<2>(v2, red);
       if (threadIdx.x == 0) {
         a.partials[4 * G + blockIdx.x] = v2[0];
@@ -362,7 +450,7 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
       if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
       stamp(4 * (it - 1) + 4);
       double s2[2];
-      grid_partials_sum<2>(a.partials + 4 * G, G, s2, tot);
+      grid_partials_sum_all<2, 5>(a.partials + 4 * G, G, s2, tot);
       rnorm = sqrt(s2[0]);
       iters = it;
       rel = relf(rnorm);
@@ -429,6 +517,7 @@ int resident_pcg_setup(int nx, int ny, int nz, int *grid, BrickGeo *geo_out) {
   int per = 0;
   MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, RT, smem));
   if (per < 1 || tiles * best > sms * per) return MQ_OK;
+  if (tiles * best > 32 * 5) return MQ_OK;  // grid_partials_sum_all<*, 5>
   geo_out->nx = nx;
   geo_out->ny = ny;
   geo_out->nz = nz;

@@ -57,6 +57,23 @@ def main():
         print(f"  per-iteration us (CTA 0, iterations 2..{n}): K1 {k1[1:].mean()/1e3:.2f}  barrier1 "
               f"{b1[1:].mean()/1e3:.2f}  K2 {k2[1:].mean()/1e3:.2f}  barrier2 {b2[1:].mean()/1e3:.2f}  "
               f"(init {k1[0]/1e3:.2f})")
+    if os.environ.get("MQ_TRACE_FINE"):
+        import numpy as np
+        st = np.zeros(1024, dtype=np.uint64)
+        check(lib.mq_pcg_trace(g.ctx, st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), st.size))
+        coarse = st[1:4 * 33 + 1].reshape(33, 4).astype(np.float64)
+        fine = st[320:320 + 8 * 32].reshape(32, 8).astype(np.float64)
+        rows = []
+        for it in range(2, 32):   # iteration it+1 (1-based), skip the first
+            f = fine[it]
+            b1s, b1e, k2e, b2e = coarse[it]  # stamps 1..4 of this iteration
+            rows.append([f[1] - f[0], f[2] - f[1], f[3] - f[2], f[4] - f[3], f[5] - f[4],
+                         b1s - f[5], b1e - b1s, f[6] - b1e, f[7] - f[6], k2e - f[7], b2e - k2e,
+                         fine[it + 1][0] - b2e if it + 1 < 32 else np.nan])
+        r = np.nanmean(np.array(rows), axis=0) / 1e3
+        names = ["own_p", "halo", "sync", "stencil", "bsum1", "xpref", "bar1", "psum1", "k2loop",
+                 "bsum2", "bar2", "psum2"]
+        print("  fine us: " + "  ".join(f"{n} {v:.2f}" for n, v in zip(names, r)))
     if args.spmv:
         y = g.alloc()
         lib.mq_timer_start(g.ctx)
