@@ -299,6 +299,20 @@ def time_e2e(problem, spec, warmup, steps):
     return steps / el, el, h2d, d2h
 
 
+def traffic_for(key, iters):
+    """DRAM bytes (read + write) per launch of the PCG kernel, from the
+    committed ncu --set full capture (profiles/traffic.json: bytes per
+    iteration of that kernel on that grid) x this run's iteration counts."""
+    tj = ROOT / "profiles" / "traffic.json"
+    if not tj.exists():
+        return None
+    t = json.loads(tj.read_text()).get(key)
+    if not t:
+        return None
+    its = np.asarray(iters, dtype=np.float64)
+    return float(t["dram_bytes_per_iteration"] * its.mean())
+
+
 def cfg2_steps(warmup=3, steps=5):
     """configs[2] (128^3, two blocks, POD-30) through the same device step
     loop: steps/s with L2 flushed before each step.  Secondary line; the
@@ -347,20 +361,17 @@ def cfg2_pcg_roofline(hbm_peak, reps=2):
             best = (ms.value, int(rep.iterations))
     ms, iters = best
     n_n = g.n_n
+    kname, kgrid = g.pcg_kernel()
     byts = float(pcg_launch_bytes(n_n, iters))
     achieved = byts / (ms * 1e-3) / 1e9
     g.close()
     # DRAM traffic per launch from the committed ncu --set full capture of the
     # same kernel on the same grid (per-iteration bytes x this launch's count)
-    traffic = None
-    tj = ROOT / "profiles" / "traffic.json"
-    if tj.exists():
-        t = json.loads(tj.read_text())
-        traffic = float(t["dram_bytes_per_iteration"]) * iters
+    traffic = traffic_for("cfg2", [iters])
     return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved / hbm_peak, "traffic": traffic,
             "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per iteration)",
-            "kernel": "pcg_stencil_kernel", "grid": [128, 128, 128], "n_n": n_n,
+            "kernel": kname, "kernel_grid": kgrid, "grid": [128, 128, 128], "n_n": n_n,
             "iterations": iters, "launch_ms": ms,
             "us_per_iteration": 1000.0 * ms / max(iters, 1),
             "bytes_per_launch": byts, "bytes_per_iteration": 72.0 * n_n}
@@ -379,6 +390,7 @@ def run_device_arm(args):
     # B_probe per output row, as the reference bench records (bench.py:371)
     op.set_probe()
     n_n, n_c = op.grid.n_n, op.grid.n_c
+    kname, kgrid = op.grid.pcg_kernel()
     barrier(dist)
     with ClockSampler(local) as clk:
         step_ms, pcg_ms, iters, launches = time_device_steps(op, spec, args.warmup, args.steps,
@@ -392,7 +404,8 @@ def run_device_arm(args):
     pcg_total = float(pcg_ms.sum())
     achieved = launch_bytes / (pcg_total * 1e-3) / 1e9 if pcg_total > 0 else 0.0
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "kernel": "pcg_stencil_kernel",
+                "frac": achieved / hbm_peak, "traffic": traffic_for("cfg1", iters.reshape(-1)),
+                "kernel": kname, "kernel_grid": kgrid,
                 "peak_kind": peak_kind, "pcg_share_of_step": pcg_total / total_ms,
                 "pcg_launches": int(iters.size), "pcg_iterations": int(iters.sum()),
                 "note": "config-1 PCG vectors (4 x 5.7 MB) are L2-resident inside a solve; "

@@ -127,6 +127,8 @@ int mq_ctx_set_stream(mq_ctx *ctx, void *stream);
  * that several contexts (ensemble members, configs[3]) step concurrently on
  * their own streams.  No reference counterpart (its members run one by one). */
 int mq_ctx_set_sm_budget(mq_ctx *ctx, int32_t sms);
+/* Which fused PCG kernel this context launches and its grid (diagnostics). */
+int mq_pcg_kernel_info(const mq_ctx *ctx, char *name, int32_t cap, int32_t *grid);
 
 /* ---- device vectors (padded layout) ------------------------------------- */
 int mq_vec_alloc(mq_ctx *ctx, double **dev);            /* zero-filled */

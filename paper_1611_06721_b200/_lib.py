@@ -87,6 +87,7 @@ SIGNATURES = {
     "mq_ctx_sync": (I32, [VP]),
     "mq_ctx_set_stream": (I32, [VP, VP]),
     "mq_ctx_set_sm_budget": (I32, [VP, I32]),
+    "mq_pcg_kernel_info": (I32, [VP, ctypes.c_char_p, I32, c_int32_p]),
     "mq_vec_alloc": (I32, [VP, ctypes.POINTER(VP)]),
     "mq_vec_free": (I32, [VP, VP]),
     "mq_vec_upload": (I32, [VP, c_double_p, VP]),

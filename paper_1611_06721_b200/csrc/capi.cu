@@ -253,6 +253,22 @@ int mq_ctx_sync(mq_ctx *ctx) {
   return MQ_OK;
 }
 
+int mq_pcg_kernel_info(const mq_ctx *ctx, char *name, int32_t cap, int32_t *grid) {
+  std::string n;
+  int g = 0;
+  if (ctx->pcg_variant == 1) { n = "pcg_stencil_kernel"; g = ctx->pcg_grid; }
+  else if (ctx->pcg_variant == 2) {
+    n = "pcg_resident_kernel<" + std::to_string((ctx->res_geo.nx + ctx->res_geo.chunks - 1) / ctx->res_geo.chunks) + ">";
+    g = ctx->res_grid;
+  } else { n = "pcg_tma_kernel"; g = ctx->brick_grid; }
+  if (name && cap > 0) {
+    std::strncpy(name, n.c_str(), (size_t)cap - 1);
+    name[cap - 1] = 0;
+  }
+  if (grid) *grid = g;
+  return MQ_OK;
+}
+
 int mq_ctx_set_sm_budget(mq_ctx *ctx, int32_t sms) {
   int dev_sms = 0;
   MQ_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->device));

@@ -72,8 +72,8 @@ struct SolverHost {
   int64_t n_planned = 0, n_enqueued = 0;
   // B probe (model.py:415-425): conductor-cell list indices, per-cell scratch,
   // per-step log of the current run
-  int32_t *d_probe = nullptr;
-  double *d_probe_vals = nullptr, *d_probe_log = nullptr;
+  int32_t *d_probe = nullptr, *d_probe_plan = nullptr;
+  double *d_probe_vals = nullptr, *d_probe_log = nullptr, *d_probe_leaf = nullptr;
   int64_t n_probe = 0, probe_cap = 0;
 };
 
@@ -100,6 +100,8 @@ void solver_free(mq_ctx *ctx) {
   cudaFree(s->d_probe);
   cudaFree(s->d_probe_vals);
   cudaFree(s->d_probe_log);
+  cudaFree(s->d_probe_plan);
+  cudaFree(s->d_probe_leaf);
   delete s;
   ctx->solver = nullptr;
 }
@@ -836,38 +838,52 @@ __global__ void k_cell_nu(CondArgs a, const double *__restrict__ state, double *
 
 // numpy's pairwise summation of a float64 array (the add.reduce inner loop
 // behind ndarray.mean): blocks of <= 128 summed with 8 accumulators, larger
-// arrays split at an 8-aligned half.  Recursion depth ~log2(n / 128).
-__device__ double np_pairwise_sum(const double *v, int64_t n) {
+// arrays split at an 8-aligned half.  The split tree depends only on n, so
+// the host builds it once (probe_plan): leaves are summed in parallel, then
+// one thread combines them in the tree's postfix order.
+__device__ double np_leaf_sum(const double *v, int n) {
   if (n < 8) {
     double r = 0.0;
-    for (int64_t i = 0; i < n; ++i) r = add(r, v[i]);
+    for (int i = 0; i < n; ++i) r = add(r, v[i]);
     return r;
   }
-  if (n <= 128) {
-    double r[8];
+  double r[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = v[j];
-    int64_t i = 8;
-    for (; i < n - (n % 8); i += 8)
+  for (int j = 0; j < 8; ++j) r[j] = v[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = add(r[j], v[i + j]);
-    double res = add(add(add(r[0], r[1]), add(r[2], r[3])), add(add(r[4], r[5]), add(r[6], r[7])));
-    for (; i < n; ++i) res = add(res, v[i]);
-    return res;
-  }
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return add(np_pairwise_sum(v, n2), np_pairwise_sum(v + n2, n - n2));
+    for (int j = 0; j < 8; ++j) r[j] = add(r[j], v[i + j]);
+  double res = add(add(add(r[0], r[1]), add(r[2], r[3])), add(add(r[4], r[5]), add(r[6], r[7])));
+  for (; i < n; ++i) res = add(res, v[i]);
+  return res;
 }
 
-// B_probe = mean(sqrt(b2[cells])) (model.py:415-425); one block.  The value
-// goes to log[par->step - 1] inside a run, else to *out.
-__global__ void k_probe(CondArgs a, const int32_t *__restrict__ cells, int64_t n, const double *__restrict__ state,
-                        double *__restrict__ vals, const StepParams *par, double *log, double *out) {
+// B_probe = mean(sqrt(b2[cells])) (model.py:415-425); one block.  plan =
+// [n_leaves, n_prog, (start, len) per leaf, postfix program (leaf index or
+// -1 = add)].  The value goes to log[par->step - 1] inside a run, else to *out.
+__global__ void k_probe(CondArgs a, const int32_t *__restrict__ cells, int64_t n, const int32_t *__restrict__ plan,
+                        const double *__restrict__ state, double *__restrict__ vals, double *__restrict__ leaf,
+                        const StepParams *par, double *log, double *out) {
   for (int64_t q = threadIdx.x; q < n; q += blockDim.x) vals[q] = sqrt(cell_b2(a, cells[q], state));
   __syncthreads();
+  const int nl = plan[0], np = plan[1];
+  for (int t = threadIdx.x; t < nl; t += blockDim.x) leaf[t] = np_leaf_sum(vals + plan[2 + 2 * t], plan[3 + 2 * t]);
+  __syncthreads();
   if (threadIdx.x != 0) return;
-  const double v = add(0.0, np_pairwise_sum(vals, n)) / (double)n;
+  double st[64];
+  int sp = 0;
+  for (int i = 0; i < np; ++i) {
+    const int op = plan[2 + 2 * nl + i];
+    if (op >= 0) {
+      st[sp++] = leaf[op];
+    } else {
+      const double rb = st[--sp];
+      const double ra = st[--sp];
+      st[sp++] = add(ra, rb);
+    }
+  }
+  const double v = add(0.0, st[0]) / (double)n;
   if (log) log[par->step - 1] = v;
   else *out = v;
 }
@@ -1648,8 +1664,8 @@ static int enqueue_step(mq_ctx *ctx, double *hist) {
     if (rc) return rc;
   }
   if (s->n_probe > 0) {
-    k_probe<<<1, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, ctx->d_ac, s->d_probe_vals, s->d_par,
-                                        s->d_probe_log, nullptr);
+    k_probe<<<1, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, s->d_probe_plan, ctx->d_ac,
+                                        s->d_probe_vals, s->d_probe_leaf, s->d_par, s->d_probe_log, nullptr);
     MQ_CUDA(cudaGetLastError());
     ctx->launches += 1;
   }
@@ -1657,6 +1673,20 @@ static int enqueue_step(mq_ctx *ctx, double *hist) {
   MQ_CUDA(cudaGetLastError());
   ctx->launches += 1;
   return MQ_OK;
+}
+
+static void probe_plan(int64_t off, int64_t n, std::vector<int32_t> &leaves, std::vector<int32_t> &prog) {
+  if (n <= 128) {
+    prog.push_back((int32_t)(leaves.size() / 2));
+    leaves.push_back((int32_t)off);
+    leaves.push_back((int32_t)n);
+    return;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  probe_plan(off, n2, leaves, prog);
+  probe_plan(off + n2, n - n2, leaves, prog);
+  prog.push_back(-1);
 }
 
 int mq_probe_set(mq_ctx *ctx, const int64_t *cells, int64_t n) {
@@ -1675,13 +1705,25 @@ int mq_probe_set(mq_ctx *ctx, const int64_t *cells, int64_t n) {
   }
   cudaFree(s->d_probe);
   cudaFree(s->d_probe_vals);
+  cudaFree(s->d_probe_plan);
+  cudaFree(s->d_probe_leaf);
   s->d_probe = nullptr;
-  s->d_probe_vals = nullptr;
+  s->d_probe_vals = s->d_probe_leaf = nullptr;
+  s->d_probe_plan = nullptr;
   s->n_probe = 0;
   if (n > 0) {
+    if (n > (int64_t)1 << 30) { set_error("probe cell set too large"); return MQ_INVALID; }
+    std::vector<int32_t> leaves, prog;
+    probe_plan(0, n, leaves, prog);
+    std::vector<int32_t> plan = {(int32_t)(leaves.size() / 2), (int32_t)prog.size()};
+    plan.insert(plan.end(), leaves.begin(), leaves.end());
+    plan.insert(plan.end(), prog.begin(), prog.end());
     MQ_CUDA(cudaMalloc(&s->d_probe, sizeof(int32_t) * n));
     MQ_CUDA(cudaMalloc(&s->d_probe_vals, sizeof(double) * n));
+    MQ_CUDA(cudaMalloc(&s->d_probe_leaf, sizeof(double) * (leaves.size() / 2)));
+    MQ_CUDA(cudaMalloc(&s->d_probe_plan, sizeof(int32_t) * plan.size()));
     MQ_CUDA(cudaMemcpy(s->d_probe, loc.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    MQ_CUDA(cudaMemcpy(s->d_probe_plan, plan.data(), sizeof(int32_t) * plan.size(), cudaMemcpyHostToDevice));
   }
   s->n_probe = n;
   if (s->graph_exec) { cudaGraphExecDestroy(s->graph_exec); s->graph_exec = nullptr; }
@@ -1700,8 +1742,8 @@ int mq_probe_b(mq_ctx *ctx, const double *a_c_host, double *out) {
   }
   double *tmp = nullptr;
   MQ_CUDA(cudaMalloc(&tmp, sizeof(double)));
-  k_probe<<<1, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, state, s->d_probe_vals, nullptr, nullptr,
-                                      tmp);
+  k_probe<<<1, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, s->d_probe_plan, state,
+                                      s->d_probe_vals, s->d_probe_leaf, nullptr, nullptr, tmp);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaMemcpyAsync(out, tmp, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);

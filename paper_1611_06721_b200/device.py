@@ -124,6 +124,17 @@ class DeviceGrid:
         check(self.lib.mq_map_global_to_noncond(self.ctx, i64ptr(g), g.size, i64ptr(out)))
         return out
 
+    def pcg_kernel(self) -> tuple[str, int]:
+        """(name, grid) of the fused PCG kernel this context launches."""
+        buf = ctypes.create_string_buffer(64)
+        grid = ctypes.c_int32()
+        check(self.lib.mq_pcg_kernel_info(self.ctx, buf, 64, ctypes.byref(grid)))
+        return buf.value.decode(), int(grid.value)
+
+    def set_sm_budget(self, sms: int) -> None:
+        """Confine the PCG kernel to ``sms`` SMs (0 = whole GPU)."""
+        check(self.lib.mq_ctx_set_sm_budget(self.ctx, int(sms)))
+
     def mc_diag(self) -> np.ndarray:
         out = np.empty(self.n_c)
         check(self.lib.mq_mc_diag(self.ctx, dptr(out)))
