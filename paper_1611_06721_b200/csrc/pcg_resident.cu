@@ -4,20 +4,20 @@
 //
 // One CTA per SM (512 threads) owns a brick: a 16 (j) x 32 (k) node tile over
 // Li <= 5 i-planes, all three edge components.  For the whole solve the
-// brick's r, Ap and search direction p (the latter with a one-node halo ring)
-// stay in shared memory.  Per iteration:
+// brick's r, x and search direction p (the latter with a one-node halo ring)
+// stay in shared memory, Ap in registers.  Per iteration:
 //   K1: own p_new = M^-1 r + beta p (in place); halo p_new = M^-1 r + beta p
 //       from the neighbours' published r and the CTA's own halo copy of
 //       p_old (computed by the previous K1 from the owner's inputs with the
 //       owner's arithmetic, hence bit-identical: p is never published);
-//       Ap = K_n p_new from shared memory (all 3*Li row chains unrolled and
-//       interleaved), partial p.Ap
-//   K2: x += alpha p (global, own; x prefetched before the barrier),
-//       r -= alpha Ap (shared), r published, partials r.r, r.z
-// Global traffic per iteration is the r halo ring plus 3 own streams
-// (publish r, x read/write), all L2-resident at these sizes; the two grid
-// barriers (~1.2 us each, tools/barrier_bench.cu), L2 latency of the halo
-// and the shared-memory stencil (128 B/clk/SM) set the iteration time.
+//       Ap = K_n p_new from shared memory (plane values cached in registers,
+//       all 3*Li row chains interleaved), partial p.Ap
+//   K2: x += alpha p and r -= alpha Ap (shared / registers), r published,
+//       partials r.r, r.z
+// x leaves shared memory once, at the end.  Global traffic per iteration is
+// the r halo ring (L2) and the r publication; the two grid barriers
+// (~1.2 us each, tools/barrier_bench.cu), the L2 latency of the halo and the
+// shared-memory stencil set the iteration time.
 #include "mq_device.cuh"
 
 namespace mq {
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
   const int li = i1 - i0;
   double *P = rsm;                                   // [li+2][3][RHP], plane 0 = i0-1
   double *R = P + (size_t)(g.li_max + 2) * 3 * RHP;  // [li][3][RT]
-  double *AP = R + (size_t)g.li_max * 3 * RT;        // [li][3][RT]
+  double *X = R + (size_t)g.li_max * 3 * RT;         // [li][3][RT] own x for the whole solve
   const int j = j0 + ty, k = k0 + tx;
   const bool own_ok = j < g.ny && k < g.nz;
   const int s_own = (ty + 1) * RHK + (tx + 1);
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
           a.r[e] = rv;  // published for the neighbours' first halo
         }
         R[Oidx(l, c)] = rv;
-        AP[Oidx(l, c)] = 0.0;
+        X[Oidx(l, c)] = (x0_mode == 1 && own_ok) ? P[Pidx(l + 1, c, s_own)] : 0.0;
       }
   }
   block_sum_r<3>(v3, red);
@@ -367,10 +367,11 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
       __syncthreads();
       fstamp(it, 3);
       double v1[1] = {0.0};
+      // Ap of the own rows stays in registers until K2
+      double av[LI * 3];
       {
         // all LI*3 rows unconditionally (rows past li or inactive read
         // allocated shared memory and are discarded): independent chains
-        double av[LI * 3];
 #if MQ_RES_SLIDE
         // march along i keeping the 15 distinct neighbour values of a plane
         // in registers: each value is read from shared memory once instead
@@ -398,7 +399,6 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             if (l < li && own_ok && is_act(l, c)) {
-              AP[Oidx(l, c)] = av[3 * l + c];
               v1[0] = add(v1[0], mul(P[Pidx(l + 1, c, s_own)], av[3 * l + c]));
             }
           }
@@ -407,13 +407,6 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
       block_sum_r<1>(v1, red);
       fstamp(it, 5);
       if (threadIdx.x == 0) a.partials[3 * G + blockIdx.x] = v1[0];
-      // own x (written only by this thread) fetched while the barrier drains
-      double xo[LI * 3];
-#pragma unroll
-      for (int l = 0; l < LI; ++l)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          if (l < li && own_ok && is_act(l, c)) xo[3 * l + c] = __ldcg(a.x + own_e(l, c));
       ++applies;
       stamp(4 * (it - 1) + 1);
       if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
@@ -424,7 +417,7 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
       if (!isfinite(pap) || pap <= 0.0) { status = MQ_INDEFINITE; iters = it; goto done; }
       alpha = rz / pap;
       fstamp(it, 6);
-      // ---- K2: x += alpha p, r -= alpha Ap (own), publish r ----
+      // ---- K2: x += alpha p (shared), r -= alpha Ap (own), publish r ----
       double v2[2] = {0.0, 0.0};
 #pragma unroll
       for (int l = 0; l < LI; ++l)
@@ -432,8 +425,8 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
         for (int c = 0; c < 3; ++c) {
           if (!(l < li && own_ok && is_act(l, c))) continue;
           const int64_t e = own_e(l, c);
-          a.x[e] = add(xo[3 * l + c], mul(alpha, P[Pidx(l + 1, c, s_own)]));
-          const double rv = sub(R[Oidx(l, c)], mul(alpha, AP[Oidx(l, c)]));
+          X[Oidx(l, c)] = add(X[Oidx(l, c)], mul(alpha, P[Pidx(l + 1, c, s_own)]));
+          const double rv = sub(R[Oidx(l, c)], mul(alpha, av[3 * l + c]));
           R[Oidx(l, c)] = rv;
           a.r[e] = rv;
           const double z = jac ? mul(inv, rv) : rv;
@@ -462,6 +455,12 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
       first = false;
     }
     if (status == MQ_OK && !converged) status = MQ_NOT_CONVERGED;
+    // the iterate leaves shared memory once (converged or budget exhausted)
+#pragma unroll
+    for (int l = 0; l < LI; ++l)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        if (l < li && own_ok && is_act(l, c)) a.x[own_e(l, c)] = X[Oidx(l, c)];
   }
 done:
   if (blockIdx.x == 0 && threadIdx.x == 0) {

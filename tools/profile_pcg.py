@@ -71,7 +71,7 @@ def main():
                          b1s - f[5], b1e - b1s, f[6] - b1e, f[7] - f[6], k2e - f[7], b2e - k2e,
                          fine[it + 1][0] - b2e if it + 1 < 32 else np.nan])
         r = np.nanmean(np.array(rows), axis=0) / 1e3
-        names = ["own_p", "halo", "sync", "stencil", "bsum1", "xpref", "bar1", "psum1", "k2loop",
+        names = ["own_p", "halo", "sync", "stencil", "bsum1", "pstore", "bar1", "psum1", "k2loop",
                  "bsum2", "bar2", "psum2"]
         print("  fine us: " + "  ".join(f"{n} {v:.2f}" for n, v in zip(names, r)))
     if args.spmv:
