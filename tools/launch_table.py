@@ -16,7 +16,7 @@ seq = []
 for r in rows:
     t = float(r[vi].replace(",", ""))
     u = r[unit_i]
-    t_us = t / 1000.0 if u == "nsecond" else (t * 1000.0 if u == "msecond" else t)
+    t_us = t / 1000.0 if u in ("ns", "nsecond") else (t * 1000.0 if u in ("ms", "msecond") else t)
     name = r[ki].split("(")[0].replace("void ", "").replace("mq::", "")
     seq.append((name, t_us))
 agg, cnt = collections.defaultdict(float), collections.Counter()
