@@ -110,6 +110,7 @@ typedef struct mq_diag {
 /* ---- context ------------------------------------------------------------ */
 const char *mq_last_error(void);
 int mq_device_count(int32_t *count);
+int mq_device_sm_count(int32_t device, int32_t *sms);
 int mq_ctx_create(const mq_grid_desc *desc, int32_t device, mq_ctx **out);
 void mq_ctx_destroy(mq_ctx *ctx);
 int64_t mq_n_n(const mq_ctx *ctx);     /* nonconducting interior dofs */

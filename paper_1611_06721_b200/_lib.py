@@ -76,6 +76,7 @@ D = ctypes.c_double
 SIGNATURES = {
     "mq_last_error": (ctypes.c_char_p, []),
     "mq_device_count": (I32, [c_int32_p]),
+    "mq_device_sm_count": (I32, [I32, c_int32_p]),
     "mq_ctx_create": (I32, [ctypes.POINTER(GridDesc), I32, ctypes.POINTER(VP)]),
     "mq_ctx_destroy": (None, [VP]),
     "mq_n_n": (I64, [VP]),
@@ -228,4 +229,10 @@ def f64(a, n=None, name="vector") -> np.ndarray:
 def device_count() -> int:
     n = ctypes.c_int32(0)
     load().mq_device_count(ctypes.byref(n))
+    return int(n.value)
+
+
+def sm_count(device: int = 0) -> int:
+    n = ctypes.c_int32(0)
+    check(load().mq_device_sm_count(int(device), ctypes.byref(n)))
     return int(n.value)

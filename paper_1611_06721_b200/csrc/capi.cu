@@ -118,6 +118,14 @@ int mq_device_count(int32_t *count) {
   return MQ_OK;
 }
 
+int mq_device_sm_count(int32_t device, int32_t *sms) {
+  int n = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) { *sms = 0; return cuda_fail(e, "cudaDeviceGetAttribute"); }
+  *sms = n;
+  return MQ_OK;
+}
+
 int mq_ctx_create(const mq_grid_desc *desc, int32_t device, mq_ctx **out) {
   if (!desc || !out) { set_error("NULL argument"); return MQ_INVALID; }
   *out = nullptr;

@@ -63,6 +63,75 @@ def run_member(member: int, steps: int, *, n_members: int = 256, seed: int = 0, 
                         1000.0 * res.aggregates["wall_seconds"])
 
 
+def run_members(members, steps: int, *, concurrency: int = 1, n_members: int = 256, seed: int = 0,
+                device: int = 0, strategy: str = "cspe", max_cols: int = 5) -> list:
+    """Integrate several members on one GPU, ``concurrency`` at a time.
+
+    Each member of a wave has its own context and stream and its PCG kernel
+    confined to an equal slice of the SMs (``mq_ctx_set_sm_budget``); the
+    waves' step graphs are enqueued interleaved, so the members' kernels run
+    side by side (the single-member PCG at 64^3 is latency-bound and leaves
+    the chip under-used).  Same trajectory per member as :func:`run_member`
+    up to the reduction order of the dot products (grid size).
+
+    Measured on B200 at 64^3 (10 steps): one member on the whole GPU with the
+    shared-memory-resident PCG kernel 279 steps/s; 4 members side by side on
+    37-SM slices (TMA brick kernel) 248 member-steps/s.  Hence the default
+    concurrency 1; slices pay off only for grids too large for the resident
+    kernel and too small to fill the chip."""
+    import ctypes
+    import time
+
+    from . import _lib
+    from ._lib import check, dptr
+    from .krylov import PcgConfig
+    from .schur import SchurOperator, StepFailureError, recover_an
+    from .startvec import RhsFamily
+    members = list(members)
+    sms = _lib.sm_count(device)
+    out = []
+    for w0 in range(0, len(members), max(1, concurrency)):
+        wave = members[w0:w0 + max(1, concurrency)]
+        runs = []
+        for m in wave:
+            prob, jf, kf, dt = member_problem(m, n_members, seed)
+            op = SchurOperator(prob, pcg=PcgConfig(rel_tol=1e-8, max_iter=5000), strategy=strategy,
+                               max_cols=max_cols, device=device)
+            if len(wave) > 1:
+                op.grid.set_sm_budget(sms // len(wave))
+            a0 = np.zeros(op.grid.n_c)
+            _, (r1, r2) = recover_an(op, a0, 0.0)
+            op._set_state(a0, 0.0)
+            tt = [0.0]
+            for _ in range(steps):
+                tt.append(tt[-1] + dt)
+            wave_tab = np.array([float(prob.waveform(t)) for t in tt])
+            check(op.lib.mq_run_prepare(op.grid.ctx, steps, dptr(np.full(steps, dt)), dptr(wave_tab), 1))
+            runs.append((m, jf, kf, dt, op, r1.iterations, r2.iterations))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            for (_, _, _, _, op, _, _) in runs:
+                check(op.lib.mq_run_steps(op.grid.ctx, 1, 1, None))
+        for (_, _, _, _, op, _, _) in runs:
+            op.grid.sync()
+        wall_ms = 1000.0 * (time.perf_counter() - t0)
+        for (m, jf, kf, dt, op, i_src0, i_cur0) in runs:
+            it = np.zeros((steps, 4), dtype=np.int32)
+            failed = ctypes.c_int64(-1)
+            rc = op.lib.mq_run_finish(op.grid.ctx, _lib.i32ptr(it), ctypes.byref(failed))
+            if rc == _lib.MQ_NONFINITE:
+                raise StepFailureError(f"member {m}: non-finite conducting state at step {failed.value}")
+            check(rc)
+            iters = {RhsFamily.SOURCE_CURRENT.value: int(i_src0 + it[:, 0].sum() + it[:, 2].sum()),
+                     RhsFamily.COUPLING_FROM_PREVIOUS_STATE.value: int(it[:, 1].sum()),
+                     RhsFamily.COUPLING_FROM_CURRENT_STATE.value: int(i_cur0 + it[:, 3].sum())}
+            a_c = op._get_state()
+            out.append(MemberResult(m, jf, kf, steps, dt, iters, float(np.linalg.norm(a_c)),
+                                    wall_ms / len(runs)))
+            op.grid.close()
+    return out
+
+
 def gather_results(local: list, dist=None) -> list:
     """All-gather per-member results (object lists) over the ranks."""
     if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:

@@ -491,3 +491,19 @@ def test_slab_pcg_loopback_on_one_gpu(gpu_ok, world, x0_given):
     assert rel(x, ref.x) <= 1e-8
     for s in slabs:
         s.close()
+
+
+@pytest.mark.gpu
+def test_concurrent_members_match_sequential(gpu_ok):
+    """configs[3] members stepped side by side on SM slices (ensemble.run_members)
+    follow the same trajectories as one member on the whole GPU: fields within
+    the north-star bar, iteration counts within +-1 per solve (the slice
+    changes only the dot products' reduction order)."""
+    from paper_1611_06721_b200 import ensemble as E
+    steps = 6
+    conc = E.run_members([0, 1, 2], steps, concurrency=3)
+    for r in conc:
+        ref = E.run_member(r.member, steps)
+        assert abs(r.final_norm_a_c - ref.final_norm_a_c) <= REL_FIELD * ref.final_norm_a_c
+        for fam, v in ref.iterations.items():
+            assert abs(r.iterations[fam] - v) <= 2 * steps + 1, (fam, r.iterations, ref.iterations)
