@@ -33,13 +33,25 @@ __device__ __forceinline__ void slab_reduce(double (&v)[NV], double *partials, u
     last = atomicAdd(counter, 1u) == (unsigned)G - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x < NV) {
+  if (last) {
+    // strided share per thread, fixed-order warp and block sums
     __threadfence();
-    double s = 0.0;
-    for (int b = 0; b < G; ++b) s = add(s, __ldcg(partials + threadIdx.x * G + b));
-    out[threadIdx.x] = s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = 0.0;
+      for (int b = threadIdx.x; b < G; b += blockDim.x) s = add(s, __ldcg(partials + q * G + b));
+      s = warp_sum(s);
+      if (lane == 0) sm[q * kWarps + warp] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < NV) {
+      double s = 0.0;
+      for (int w = 0; w < kWarps; ++w) s = add(s, sm[threadIdx.x * kWarps + w]);
+      out[threadIdx.x] = s;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
   }
-  if (last && threadIdx.x == 0) *counter = 0u;
 }
 
 #define SLAB_ROWS(L, mask)                                                                     \

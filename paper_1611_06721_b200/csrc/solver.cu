@@ -132,10 +132,20 @@ __device__ __forceinline__ void last_block_reduce(double *acc, int nq, double *p
   if (threadIdx.x == 0) is_last = (atomicAdd(counter, 1u) == (unsigned)G - 1);
   __syncthreads();
   if (is_last) {
+    // every thread of the last block takes a strided share of each row of
+    // partials; fixed-order warp and block sums (deterministic).  A serial
+    // sum of G partials per value by one thread costs G dependent L2 loads.
     __threadfence();
+    for (int q = 0; q < nq; ++q) {
+      double s = 0.0;
+      for (int b = threadIdx.x; b < G; b += blockDim.x) s = add(s, __ldcg(partials + (int64_t)q * G + b));
+      s = warp_sum(s);
+      if (lane == 0) sm[q * kWarps + warp] = s;
+    }
+    __syncthreads();
     if (threadIdx.x < nq) {
       double s = 0.0;
-      for (int b = 0; b < G; ++b) s = add(s, __ldcg(partials + (int64_t)threadIdx.x * G + b));
+      for (int w = 0; w < kWarps; ++w) s = add(s, sm[threadIdx.x * kWarps + w]);
       out[threadIdx.x] = s;
     }
     if (threadIdx.x == 0) *counter = 0u;
