@@ -313,32 +313,35 @@ def traffic_for(key, iters):
     return float(t["dram_bytes_per_iteration"] * its.mean())
 
 
-def cfg2_steps(warmup=3, steps=5):
-    """configs[2] (128^3, two blocks, POD-30) through the same device step
-    loop: steps/s with L2 flushed before each step.  Secondary line; the
-    headline is config 1."""
+def cfg_steps(index, warmup=3, steps=5):
+    """configs[2] (128^3, POD-30) or configs[4] (256^3, CSPE k=5, one GPU)
+    through the same device step loop: steps/s with L2 flushed before each
+    step.  Secondary lines; the headline is config 1."""
     from paper_1611_06721_b200 import PcgConfig, SchurOperator, configs as C
-    spec = C.config_spec(2)
-    op = SchurOperator(C.make_problem(2), pcg=PcgConfig(rel_tol=spec.rel_tol, max_iter=spec.max_iter),
-                       strategy="pod", n_pod=spec.n_pod)
+    spec = C.config_spec(index)
+    op = SchurOperator(C.make_problem(index), pcg=PcgConfig(rel_tol=spec.rel_tol, max_iter=spec.max_iter),
+                       strategy=spec.strategy, n_pod=spec.n_pod, max_cols=spec.max_cols)
     op.set_probe()
     step_ms, pcg_ms, iters, launches = time_device_steps(op, spec, warmup, steps)
     op.grid.close()
-    return {"workload": spec.name, "grid": [128, 128, 128], "strategy": "pod", "n_pod": spec.n_pod,
+    n = spec.N
+    return {"workload": spec.name, "grid": [n, n, n], "strategy": spec.strategy,
+            "n_pod" if spec.strategy == "pod" else "max_cols": spec.n_pod if spec.strategy == "pod" else spec.max_cols,
             "dt": spec.dt, "steps_after_warmup": [warmup + 1, warmup + steps],
             "value": steps / (float(step_ms.sum()) * 1e-3), "unit": UNIT,
             "ms_per_step": float(step_ms.mean()), "pcg_share_of_step": float(pcg_ms.sum() / step_ms.sum()),
             "timed_step_iterations": iters.tolist(), "gpu_launches": launches}
 
 
-def cfg2_pcg_roofline(hbm_peak, reps=2):
-    """Fused PCG kernel on the 128^3 grid of configs[2]: cold source solve."""
+def cfg_pcg_roofline(index, hbm_peak, reps=2):
+    """Fused PCG kernel on the grid of configs[index] (2: 128^3, 4: 256^3):
+    cold source solve, one launch timed with CUDA events."""
     import ctypes
 
     from paper_1611_06721_b200 import _lib, configs as C
     from paper_1611_06721_b200._lib import check
     from paper_1611_06721_b200.device import DeviceGrid
-    prob = C.make_problem(2)
+    prob = C.make_problem(index)
     g = DeviceGrid(prob)
     lib = g.lib
     b = g.alloc()
@@ -367,11 +370,11 @@ def cfg2_pcg_roofline(hbm_peak, reps=2):
     g.close()
     # DRAM traffic per launch from the committed ncu --set full capture of the
     # same kernel on the same grid (per-iteration bytes x this launch's count)
-    traffic = traffic_for("cfg2", [iters])
+    traffic = traffic_for(f"cfg{index}", [iters])
     return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved / hbm_peak, "traffic": traffic,
             "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per iteration)",
-            "kernel": kname, "kernel_grid": kgrid, "grid": [128, 128, 128], "n_n": n_n,
+            "kernel": kname, "kernel_grid": kgrid, "grid": [prob.material.shape[0]] * 3, "n_n": n_n,
             "iterations": iters, "launch_ms": ms,
             "us_per_iteration": 1000.0 * ms / max(iters, 1),
             "bytes_per_launch": byts, "bytes_per_iteration": 72.0 * n_n}
@@ -414,10 +417,13 @@ def run_device_arm(args):
     line = None
     if rank == 0:
         e2e_v, e2e_s, h2d, d2h = time_e2e(problem, spec, args.warmup, args.steps)
-        roof2 = steps2 = None
+        roof2 = steps2 = roof4 = steps4 = None
         if not args.skip_cfg2:
-            roof2 = cfg2_pcg_roofline(hbm_peak)
-            steps2 = cfg2_steps()
+            roof2 = cfg_pcg_roofline(2, hbm_peak)
+            steps2 = cfg_steps(2)
+        if not args.skip_cfg4:
+            roof4 = cfg_pcg_roofline(4, hbm_peak, reps=1)
+            steps4 = cfg_steps(4, warmup=1, steps=2)
         cpu = None
         if world == 1 and not args.skip_cpu:
             v, done, el, _ = cpu_reference(spec, 0, args.cpu_steps, budget_s=30.0)
@@ -441,6 +447,8 @@ def run_device_arm(args):
             "roofline": roofline,
             "roofline_cfg2": roof2,
             "cfg2_steps": steps2,
+            "roofline_cfg4_1gpu": roof4,
+            "cfg4_steps_1gpu": steps4,
             "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "explicit_euler_step + recover_an (host arrays)"},
             "gpu_launches": launches,
@@ -462,6 +470,7 @@ def main():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--skip-cfg2", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-cfg4", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -161,9 +161,12 @@ __device__ __forceinline__ void last_block_reduce(double *acc, int nq, double *p
 // partition, so dots and linear combinations need no mask (the outputs stay
 // 0 there).  KB bounds the number of basis vectors (compile-time register
 // budget), UN pairs per thread are in flight per stream.
+#ifndef MQ_TS_UNROLL
+#define MQ_TS_UNROLL 2
+#endif
 template <int KB>
 struct Unroll {
-  static constexpr int value = KB <= 8 ? 2 : 1;
+  static constexpr int value = KB <= 8 ? MQ_TS_UNROLL : 1;
 };
 
 // d[j] = A_{order[j]} . v  (j < k), d[k] = v . v when selfdot
@@ -1395,7 +1398,10 @@ int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern)
   vec(&s->rhs_cpl);
   vec(&s->y_src);
   vec(&s->y_cpl);
-  s->red_grid = std::max(1, std::min<int>(ctx->sms * 2, (int)((L.words + kWarps - 1) / kWarps)));
+#ifndef MQ_RED_MULT
+#define MQ_RED_MULT 2
+#endif
+  s->red_grid = std::max(1, std::min<int>(ctx->sms * MQ_RED_MULT, (int)((L.words + kWarps - 1) / kWarps)));
   rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_red, sizeof(double) * RQ * (size_t)s->red_grid * (MAXS + 2));
   rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_cnt, sizeof(unsigned int) * (MAXS + 4));
   // sparse source pattern on its support
