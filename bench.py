@@ -313,12 +313,17 @@ def traffic_for(key, iters):
     return float(t["dram_bytes_per_iteration"] * its.mean())
 
 
-def cfg_steps(index, warmup=3, steps=5):
-    """configs[2] (128^3, POD-30) or configs[4] (256^3, CSPE k=5, one GPU)
-    through the same device step loop: steps/s with L2 flushed before each
-    step.  Secondary lines; the headline is config 1."""
+def cfg_steps(index, warmup=3, steps=5, strategy=None):
+    """configs[2] (128^3, POD-30), configs[4] (256^3, CSPE k=5, one GPU) or
+    configs[1] with its second start-vector strategy (POD-20) through the
+    same device step loop: steps/s with L2 flushed before each step.
+    Secondary lines; the headline is config 1 with CSPE."""
+    from dataclasses import replace
+
     from paper_1611_06721_b200 import PcgConfig, SchurOperator, configs as C
     spec = C.config_spec(index)
+    if strategy is not None:
+        spec = replace(spec, strategy=strategy, name=f"{spec.name.split('_cspe')[0]}_{strategy}{spec.n_pod}")
     op = SchurOperator(C.make_problem(index), pcg=PcgConfig(rel_tol=spec.rel_tol, max_iter=spec.max_iter),
                        strategy=spec.strategy, n_pod=spec.n_pod, max_cols=spec.max_cols)
     op.set_probe()
@@ -418,6 +423,7 @@ def run_device_arm(args):
     if rank == 0:
         e2e_v, e2e_s, h2d, d2h = time_e2e(problem, spec, args.warmup, args.steps)
         roof2 = steps2 = roof4 = steps4 = None
+        pod1 = cfg_steps(1, warmup=args.warmup, steps=args.steps, strategy="pod")
         if not args.skip_cfg2:
             roof2 = cfg_pcg_roofline(2, hbm_peak)
             steps2 = cfg_steps(2)
@@ -446,6 +452,7 @@ def run_device_arm(args):
             "clocks": clk.summary(),
             "roofline": roofline,
             "roofline_cfg2": roof2,
+            "cfg1_pod_steps": pod1,
             "cfg2_steps": steps2,
             "roofline_cfg4_1gpu": roof4,
             "cfg4_steps_1gpu": steps4,

@@ -395,6 +395,25 @@ def test_config1_first_steps(gpu_ok, golden):
     assert np.max(np.abs(res.step_iterations[:, 1] - it[1:, 1])) <= 1
 
 
+@pytest.mark.slow
+def test_config1_pod_first_steps(gpu_ok):
+    """64^3 Brauer with POD-20 start vectors (configs[1]'s second run): the
+    first steps against the oracle, per-step fields within the bar."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, run_explicit
+    spec, m = oracle_model(1)
+    nsteps = 3
+    tr = O.run(m, O.sinusoid(50.0), spec.dt, nsteps, strategy="pod", rel_tol=1e-8, n_pod=20, eps_pod=1e-4)
+    res = run_explicit(C.make_problem(1), t_end=nsteps * spec.dt, dt=spec.dt, strategy="pod",
+                       pcg=PcgConfig(rel_tol=1e-8), output_period=spec.dt * (1 - 1e-3), n_pod=20,
+                       eps_pod=1e-4, record_states=True)
+    worst = max(rel(res.a_c_history[i], tr.a_c[i + 1]) for i in range(nsteps))
+    assert worst <= REL_FIELD, worst
+    it = res.step_iterations
+    assert np.max(np.abs(it[:, 1] - np.array(tr.iters[O.FAM_PREV]))) <= 1
+    assert np.max(np.abs(it[:, 3] - np.array(tr.iters[O.FAM_CUR][1:]))) <= 1
+
+
 def test_cfl_estimate_matches_oracle_and_reference(gpu_ok, golden):
     """estimate_cfl (schur.py:327-376) on the device vs the oracle and the
     reference's own lambda (golden) at config 0."""
