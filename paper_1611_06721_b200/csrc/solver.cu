@@ -631,20 +631,24 @@ __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
     A[r * MAXS + c] = v;
     V[r * MAXS + c] = (r == c) ? 1.0 : 0.0;
   }
+  __shared__ double s_tr;
+  __shared__ int s_rot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tr = 0.0;
+    for (int r = 0; r < m; ++r) tr += fabs(A[r * MAXS + r]);
+    s_tr = tr;
+  }
   __syncthreads();
   const int npair = mm / 2;
+  // cyclic sweeps until a sweep rotates nothing: a pair is skipped when its
+  // coupling is negligible relative to its diagonal entries (1e-15) or to
+  // the trace (1e-18) -- the Gram matrices of nearly dependent snapshots
+  // carry noise-level eigenvalues whose couplings never fall below a
+  // relative threshold
   for (int sweep = 0; sweep < 40; ++sweep) {
-    if (threadIdx.x == 0) {
-      double off = 0.0, dia = 0.0;
-      for (int r = 0; r < m; ++r)
-        for (int c = 0; c < m; ++c) {
-          if (r == c) dia += A[r * MAXS + c] * A[r * MAXS + c];
-          else off += A[r * MAXS + c] * A[r * MAXS + c];
-        }
-      s_done = (off <= 1e-32 * dia) || off == 0.0;
-    }
+    if (threadIdx.x == 0) s_rot = 0;
     __syncthreads();
-    if (s_done) break;
     for (int round = 0; round < mm - 1; ++round) {
       if (threadIdx.x < npair) {
         // round-robin pairing: player mm-1 fixed, others rotate
@@ -657,7 +661,9 @@ __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
         qq[t] = q;
         const double apq = A[p * MAXS + q];
         double c = 1.0, s = 0.0;
-        if (apq != 0.0) {
+        const double app = A[p * MAXS + p], aqq = A[q * MAXS + q];
+        if (apq != 0.0 && fabs(apq) > 1e-15 * sqrt(fabs(app * aqq)) && fabs(apq) > 1e-18 * s_tr) {
+          atomicAdd(&s_rot, 1);
           const double th = (A[q * MAXS + q] - A[p * MAXS + p]) / (2.0 * apq);
           const double tt = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
           c = 1.0 / sqrt(tt * tt + 1.0);
@@ -691,6 +697,9 @@ __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
       }
       __syncthreads();
     }
+    if (threadIdx.x == 0) s_done = s_rot == 0;
+    __syncthreads();
+    if (s_done) break;
   }
   if (threadIdx.x == 0) {
     // sort descending (startvec.py:287-289), sigma = sqrt(clip(lambda, 0))
