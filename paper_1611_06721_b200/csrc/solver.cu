@@ -610,6 +610,9 @@ __global__ void k_pod_push_commit(FamDev *f, int n_pod) {
 // POD: eigen-decomposition of the logical Gram matrix by parallel cyclic
 // Jacobi (replaces LAPACK syevd, startvec.py:285-294), truncation, basis
 // combination W = V_k (divided by sigma in k_pod_basis).
+#ifndef MQ_EIG_ABS
+#define MQ_EIG_ABS 1e-16
+#endif
 __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
   __shared__ double A[MAXS * MAXS];
   __shared__ double V[MAXS * MAXS];
@@ -662,7 +665,7 @@ __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
         const double apq = A[p * MAXS + q];
         double c = 1.0, s = 0.0;
         const double app = A[p * MAXS + p], aqq = A[q * MAXS + q];
-        if (apq != 0.0 && fabs(apq) > 1e-15 * sqrt(fabs(app * aqq)) && fabs(apq) > 1e-18 * s_tr) {
+        if (apq != 0.0 && fabs(apq) > 1e-15 * sqrt(fabs(app * aqq)) && fabs(apq) > MQ_EIG_ABS * s_tr) {
           atomicAdd(&s_rot, 1);
           const double th = (A[q * MAXS + q] - A[p * MAXS + p]) / (2.0 * apq);
           const double tt = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
