@@ -111,8 +111,22 @@ void solver_free(mq_ctx *ctx) {
 // ---------------------------------------------------------------------------
 constexpr int RQ = MAXS + 2;  // max values reduced by one kernel
 
+// Single-thread family bookkeeping run by thread 0 of the last block of the
+// reduction that produced its inputs (one kernel boundary less per step of
+// the CSPE/POD chains): the CSPE projection solve, the insert gates and
+// decision, the Galerkin commit, the POD push commit.
+enum PostKind : int { POST_NONE = 0, POST_PROJECT, POST_GATE, POST_GATE_C2, POST_DECIDE, POST_COMMIT, POST_POD_PUSH };
+struct Post {
+  int kind = POST_NONE;
+  FamDev *f = nullptr;
+  int max_cols = 0;
+  int n_pod = 0;
+  double drop_tol = 0.0;
+};
+__device__ void run_post(const Post &p);
+
 __device__ __forceinline__ void last_block_reduce(double *acc, int nq, double *partials, unsigned int *counter,
-                                                  double *out) {
+                                                  double *out, const Post &post = Post()) {
   __shared__ double sm[RQ * kWarps];
   __shared__ bool is_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -149,6 +163,10 @@ __device__ __forceinline__ void last_block_reduce(double *acc, int nq, double *p
       out[threadIdx.x] = s;
     }
     if (threadIdx.x == 0) *counter = 0u;
+    if (post.kind != POST_NONE) {
+      __syncthreads();
+      if (threadIdx.x == 0) run_post(post);
+    }
   }
 }
 
@@ -173,7 +191,8 @@ struct Unroll {
 template <int KB>
 __global__ void __launch_bounds__(kBlock) k_mdot(int64_t npair, double *const *tab, const int *order,
                                                  const int *kptr, const double *__restrict__ v, int selfdot,
-                                                 double *out, double *partials, unsigned int *counter) {
+                                                 double *out, double *partials, unsigned int *counter,
+                                                 Post post) {
   __shared__ const double2 *ptr[KB];
   const int k = *kptr;
   if (threadIdx.x < k) ptr[threadIdx.x] = reinterpret_cast<const double2 *>(tab[order[threadIdx.x]]);
@@ -211,7 +230,7 @@ __global__ void __launch_bounds__(kBlock) k_mdot(int64_t npair, double *const *t
     }
   }
   if (selfdot) acc[k] = acc[KB];
-  last_block_reduce(acc, k + (selfdot ? 1 : 0), partials, counter, out);
+  last_block_reduce(acc, k + (selfdot ? 1 : 0), partials, counter, out, post);
 }
 
 // out = in - sum_j c_j A_{order[j]};  d[j] = A_{order[j]} . out (j < ndot), d[ndot] = out.out
@@ -219,7 +238,8 @@ template <int KB>
 __global__ void __launch_bounds__(kBlock) k_axpy_dots(int64_t npair, double *const *tab, const int *order,
                                                       const int *kptr, const double *c, const double *in,
                                                       double *outv, int ndot_is_k, double *dout,
-                                                      double *partials, unsigned int *counter, const int *gate) {
+                                                      double *partials, unsigned int *counter, const int *gate,
+                                                      Post post) {
   if (gate && !*gate) return;
   __shared__ const double2 *ptr[KB];
   __shared__ double cs[KB];
@@ -272,7 +292,7 @@ __global__ void __launch_bounds__(kBlock) k_axpy_dots(int64_t npair, double *con
     }
   }
   acc[nd] = acc[KB];
-  last_block_reduce(acc, nd + 1, partials, counter, dout);
+  last_block_reduce(acc, nd + 1, partials, counter, dout, post);
 }
 
 // out = sum_j c_j A_{order[j]} (0 when k == 0)
@@ -321,7 +341,7 @@ template <int KB>
 __global__ void __launch_bounds__(kBlock) k_cspe_product(Lay L, const uint32_t *__restrict__ mask, double dg,
                                                          double of, FamDev *f, double *const *Utab,
                                                          double *const *KUtab, const double *__restrict__ w,
-                                                         double *partials, unsigned int *counter) {
+                                                         double *partials, unsigned int *counter, Post post) {
   if (!f->accept) return;
   __shared__ const double *ptr[MAXS];
   const int kp = f->kprime;
@@ -347,7 +367,7 @@ __global__ void __launch_bounds__(kBlock) k_cspe_product(Lay L, const uint32_t *
     acc[KB] = add(acc[KB], mul(ue, ku));
   }
   acc[kp] = acc[KB];
-  last_block_reduce(acc, kp + 1, partials, counter, f->d + 0);
+  last_block_reduce(acc, kp + 1, partials, counter, f->d + 0, post);
 }
 
 // POD: B_j = (sum_l X_{order[l]} W[l][j]) / sigma_j  for j < podk
@@ -420,7 +440,7 @@ __global__ void __launch_bounds__(kBlock) k_pod_galerkin(Lay L, const uint32_t *
 template <int KB>
 __global__ void __launch_bounds__(kBlock) k_pod_push(Lay L, const uint32_t *__restrict__ mask, FamDev *f,
                                                      double *const *Xtab, int n_pod, const double *__restrict__ y,
-                                                     double *partials, unsigned int *counter) {
+                                                     double *partials, unsigned int *counter, Post post) {
   __shared__ const double *ptr[MAXS];
   const int m = f->k;
   const int slot = (m < n_pod) ? m : f->order[0];
@@ -443,7 +463,7 @@ __global__ void __launch_bounds__(kBlock) k_pod_push(Lay L, const uint32_t *__re
     acc[KB] = add(acc[KB], mul(yv, yv));
   }
   acc[nother] = acc[KB];
-  last_block_reduce(acc, nother + 1, partials, counter, f->d);
+  last_block_reduce(acc, nother + 1, partials, counter, f->d, post);
 }
 
 // ---------------------------------------------------------------------------
@@ -504,8 +524,7 @@ __device__ void drop_logical(FamDev *f, int j, double *beta) {
 }
 
 // CSPE project (startvec.py:207-225): f->d holds beta = U^T rhs
-__global__ void k_cspe_project_small(FamDev *f) {
-  if (threadIdx.x != 0) return;
+__device__ void cspe_project_small(FamDev *f) {
   __shared__ double low[MAXS * MAXS];
   double beta[MAXS];
   for (int j = 0; j < f->k; ++j) beta[j] = f->d[j];
@@ -523,8 +542,7 @@ __global__ void k_cspe_project_small(FamDev *f) {
 }
 
 // CSPE observe, after ||v||: reject zero / non-finite (startvec.py:166-170)
-__global__ void k_cspe_gate(FamDev *f) {
-  if (threadIdx.x != 0) return;
+__device__ void cspe_gate(FamDev *f) {
   const double nv = sqrt(f->d[f->k]);
   f->nv2 = nv;
   if (nv == 0.0 || !isfinite(nv)) {
@@ -537,14 +555,14 @@ __global__ void k_cspe_gate(FamDev *f) {
 }
 
 // CGS pass 2 uses the coefficients of pass 1's dot products
-__global__ void k_cspe_gate_c2(FamDev *f) {
-  if (threadIdx.x != 0 || !f->accept) return;
+__device__ void cspe_gate_c2(FamDev *f) {
+  if (!f->accept) return;
   for (int j = 0; j < f->k; ++j) f->coef[j] = f->d[j];
 }
 
 // after the second CGS pass: drop test, FIFO eviction, slot choice (startvec.py:175-186)
-__global__ void k_cspe_decide(FamDev *f, const double *nw2, int max_cols, double drop_tol) {
-  if (threadIdx.x != 0 || !f->accept) return;
+__device__ void cspe_decide(FamDev *f, const double *nw2, int max_cols, double drop_tol) {
+  if (!f->accept) return;
   const double nw = sqrt(*nw2);
   if (nw < drop_tol * f->nv2) {
     f->accept = 0;
@@ -569,8 +587,8 @@ __global__ void k_cspe_decide(FamDev *f, const double *nw2, int max_cols, double
 }
 
 // bordered Galerkin update (startvec.py:187-199); f->d = [cross..., diag]
-__global__ void k_cspe_commit(FamDev *f) {
-  if (threadIdx.x != 0 || !f->accept) return;
+__device__ void cspe_commit(FamDev *f) {
+  if (!f->accept) return;
   const int k = f->kprime;
   for (int j = 0; j < k; ++j) {
     f->G[k * MAXS + j] = f->d[j];
@@ -585,8 +603,7 @@ __global__ void k_cspe_commit(FamDev *f) {
 
 // POD push bookkeeping: Gram row/column from f->d (logical order of the
 // remaining snapshots, then the new one)
-__global__ void k_pod_push_commit(FamDev *f, int n_pod) {
-  if (threadIdx.x != 0) return;
+__device__ void pod_push_commit(FamDev *f, int n_pod) {
   const int m = f->k;
   int slot;
   if (m < n_pod) {
@@ -605,6 +622,18 @@ __global__ void k_pod_push_commit(FamDev *f, int n_pod) {
     f->G[sj * MAXS + slot] = f->d[j];
   }
   f->G[slot * MAXS + slot] = f->d[nother];
+}
+
+__device__ void run_post(const Post &p) {
+  switch (p.kind) {
+    case POST_PROJECT: cspe_project_small(p.f); break;
+    case POST_GATE: cspe_gate(p.f); break;
+    case POST_GATE_C2: cspe_gate_c2(p.f); break;
+    case POST_DECIDE: cspe_decide(p.f, p.f->d, p.max_cols, p.drop_tol); break;
+    case POST_COMMIT: cspe_commit(p.f); break;
+    case POST_POD_PUSH: pod_push_commit(p.f, p.n_pod); break;
+    default: break;
+  }
 }
 
 // POD: eigen-decomposition of the logical Gram matrix by parallel cyclic
@@ -1127,15 +1156,18 @@ static int start_vector(mq_ctx *ctx, int fam, const double *rhs, double *x0) {
       k_copy_if<<<stream_grid(ctx), kBlock, 0, st>>>(L, ctx->d_mask, f, s->last[fam], x0);
       LAUNCH_CHECK();
       break;
-    case MQ_STRAT_CSPE:
+    case MQ_STRAT_CSPE: {
+      // beta = U^T rhs; the last block then solves the projected system
+      Post post;
+      post.kind = POST_PROJECT;
+      post.f = f;
       KB_LAUNCH(s->kb, k_mdot, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, rhs, 0, f->d, s->d_red,
-                s->d_cnt);
-      LAUNCH_CHECK();
-      k_cspe_project_small<<<1, 32, 0, st>>>(f);
+                s->d_cnt, post);
       LAUNCH_CHECK();
       KB_LAUNCH(s->kb, k_comb, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, f->coef, x0);
       LAUNCH_CHECK();
       break;
+    }
     case MQ_STRAT_POD: {
       k_pod_eig<<<1, 256, 0, st>>>(f, s->cfg.eps_pod);
       LAUNCH_CHECK();
@@ -1174,37 +1206,43 @@ static int observe(mq_ctx *ctx, int fam, const double *y) {
       k_prev_mark<<<1, 32, 0, st>>>(f);
       LAUNCH_CHECK();
       break;
-    case MQ_STRAT_CSPE:
-      // ||v|| and U^T v in one pass
+    case MQ_STRAT_CSPE: {
+      Post post;
+      post.f = f;
+      post.max_cols = s->cfg.max_cols;
+      post.drop_tol = s->cfg.drop_tol;
+      // ||v|| and U^T v in one pass, then the zero / non-finite gate
+      post.kind = POST_GATE;
       KB_LAUNCH(s->kb, k_mdot, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, y, 1, f->d, s->d_red,
-                s->d_cnt);
-      LAUNCH_CHECK();
-      k_cspe_gate<<<1, 32, 0, st>>>(f);
+                s->d_cnt, post);
       LAUNCH_CHECK();
       // CGS pass 1: w1 = v - U c1, c2 = U^T w1
+      post.kind = POST_GATE_C2;
       KB_LAUNCH(s->kb, k_axpy_dots, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, f->coef, y, s->w1, 1, f->d,
-                                        s->d_red, s->d_cnt, &f->accept);
+                                        s->d_red, s->d_cnt, &f->accept, post);
       LAUNCH_CHECK();
-      k_cspe_gate_c2<<<1, 32, 0, st>>>(f);
-      LAUNCH_CHECK();
-      // CGS pass 2: w2 = w1 - U c2, ||w2||^2
+      // CGS pass 2: w2 = w1 - U c2, ||w2||^2, then drop test / eviction / slot
+      post.kind = POST_DECIDE;
       KB_LAUNCH(s->kb, k_axpy_dots, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, f->coef, s->w1, s->w2, 0,
-                                        f->d, s->d_red, s->d_cnt, &f->accept);
+                                        f->d, s->d_red, s->d_cnt, &f->accept, post);
       LAUNCH_CHECK();
-      k_cspe_decide<<<1, 32, 0, st>>>(f, f->d, s->cfg.max_cols, s->cfg.drop_tol);
-      LAUNCH_CHECK();
+      // u, K u, cross products, diagonal, then the bordered Galerkin commit
+      post.kind = POST_COMMIT;
       KB_LAUNCH(s->kb, k_cspe_product, G, kBlock, st, L, ctx->d_mask, ctx->kn_diag, ctx->kn_off, f, s->d_U[fam], s->d_KU[fam],
-                                           s->w2, s->d_red, s->d_cnt);
-      LAUNCH_CHECK();
-      k_cspe_commit<<<1, 32, 0, st>>>(f);
+                                           s->w2, s->d_red, s->d_cnt, post);
       LAUNCH_CHECK();
       break;
-    case MQ_STRAT_POD:
-      KB_LAUNCH(s->kb, k_pod_push, G, kBlock, st, L, ctx->d_mask, f, s->d_X[fam], s->cfg.n_pod, y, s->d_red, s->d_cnt);
-      LAUNCH_CHECK();
-      k_pod_push_commit<<<1, 32, 0, st>>>(f, s->cfg.n_pod);
+    }
+    case MQ_STRAT_POD: {
+      Post post;
+      post.kind = POST_POD_PUSH;
+      post.f = f;
+      post.n_pod = s->cfg.n_pod;
+      KB_LAUNCH(s->kb, k_pod_push, G, kBlock, st, L, ctx->d_mask, f, s->d_X[fam], s->cfg.n_pod, y, s->d_red, s->d_cnt,
+                post);
       LAUNCH_CHECK();
       break;
+    }
   }
   return MQ_OK;
 }
