@@ -205,7 +205,9 @@ def run_reference_arm(args):
         return 0
     from paper_1611_06721_b200 import configs as C
     spec = C.config_spec(1)
-    v, done, el, n_n = cpu_reference(spec, args.warmup, args.steps)
+    # each step is a full step of the trajectory (~7 s on 16 cores); the
+    # timed loop stops after ~150 s so that any --steps ends in a few minutes
+    v, done, el, n_n = cpu_reference(spec, args.warmup, args.steps, budget_s=150.0)
     cores = os.cpu_count()
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference",
