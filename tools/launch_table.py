@@ -1,6 +1,6 @@
 """Summarise an ncu --metrics gpu__time_duration.sum --csv launch list.
 
-    python tools/launch_table.py profiles/r01_launches.csv
+    python tools/launch_table.py profiles/r01_launches.csv [STEP]
 prints a markdown table (kernel, launches, total us, share) and the
 per-step breakdown of the last complete step (k_load_params to k_load_params).
 """
@@ -29,8 +29,9 @@ print("| kernel | launches | total µs | share |\n|---|---|---|---|")
 for n, t in sorted(agg.items(), key=lambda x: -x[1]):
     print(f"| {n} | {cnt[n]} | {t:.1f} | {100 * t / tot:.1f}% |")
 idx = [i for i, (n, _) in enumerate(seq) if n == "k_load_params"]
+which = int(sys.argv[2]) if len(sys.argv) > 2 else -2   # step boundary index (default: last complete step)
 if len(idx) >= 2:
-    a, b = idx[-2], idx[-1]
+    a, b = idx[which], idx[which + 1]
     step = collections.defaultdict(float)
     sc = collections.Counter()
     for n, t in seq[a:b]:
