@@ -253,6 +253,17 @@ int mq_slab_k1(mq_ctx *ctx, double *x_dev, int32_t first, double beta, double al
 int mq_slab_k2(mq_ctx *ctx, double alpha, int32_t use_jacobi, double *part2);
 int mq_slab_final(mq_ctx *ctx, double *x_dev, double alpha, int32_t p_is_a);
 
+/* Fused slab PCG (configs[4]): one persistent kernel per rank runs the
+ * stencil passes, the ghost-plane stores into the neighbour ranks and the
+ * cross-rank all-reduce (mailbox + arrival counter in every rank's memory)
+ * with no host round trip per iteration (krylov.py:174-250 per iteration).
+ * _local: all nranks slab contexts of this process on one GPU, emulated as
+ * the CTA groups of one cooperative launch.  b/x: per rank device vectors in
+ * the slab layout (x is also the start vector when x0_given). */
+int mq_slab_fused_solve_local(mq_ctx **ctxs, int32_t nranks, const double *const *b, double *const *x,
+                              int32_t x0_given, double rel_tol, double abs_tol, int32_t max_iter,
+                              int32_t use_jacobi, mq_solve_report *report);
+
 /* ---- timing (CUDA events on the context stream) ------------------------- */
 /* Sum of the device times of the PCG launches of the last step (when PCG
  * timing is enabled with mq_pcg_stats(..., 1)). */

@@ -77,6 +77,8 @@ struct mq_ctx {
   double *d_tmp0 = nullptr, *d_tmp1 = nullptr;
   double *d_partials = nullptr;
   mq::GridBar *d_bar = nullptr;
+  double *d_mbox = nullptr;              // fused slab PCG: rank mailbox
+  unsigned long long *d_mcount = nullptr; // [arrival counter, epoch]
   mq::PcgOut *d_out = nullptr;
   mq::PcgOut *h_out = nullptr;
   unsigned long long *d_trace = nullptr;

@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include "mq_device.cuh"
+#include "slab_rank.cuh"
 
 namespace mq {
 
@@ -158,10 +159,17 @@ struct MarchCtx {
   uint32_t ph;  // per-stage mbarrier parity (identical in every thread)
 };
 
-template <int MODE, class ROW>
+struct NoPush {
+  __device__ __forceinline__ void operator()(int, int, int64_t, double) const {}
+};
+
+// push(q, c, jk, v): p_new of an own active position of plane q (jk = its
+// offset inside the padded plane), for the slab kernel's ghost stores
+template <int MODE, class ROW, class PUSH = NoPush>
 __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, const CUtensorMap *mr,
                                           const CUtensorMap *mp, bool first, double beta, double alpha_prev,
-                                          double *pnew, int i0, int i1, int j0, int k0, ROW row) {
+                                          double *pnew, int i0, int i1, int j0, int k0, ROW row,
+                                          PUSH push = PUSH()) {
   const StencilPcgArgs &a = A.a;
   const BrickGeo &g = A.g;
   const Lay &L = a.L;
@@ -254,7 +262,10 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
         if ((act >> c) & 1u) x[c * L.C + qb + pos_own] = add(xo[c], mul(alpha_prev, po));
       }
       S.r[c][s_own] = pv;
-      if ((act >> c) & 1u) pnew[c * L.C + qb + pos_own] = pv;
+      if ((act >> c) & 1u) {
+        pnew[c * L.C + qb + pos_own] = pv;
+        push(q, c, pos_own - L.Si, pv);
+      }
     }
     if (hs >= 0) {
 #pragma unroll
@@ -509,6 +520,261 @@ done:
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused slab variant (configs[4]): the kernel above on one i-slab per rank,
+// its grid barriers replaced by the rank all-reduce of slab_rank.cuh, and
+// the planes 0 / n-1 of r and p_new stored into the neighbour ranks' ghost
+// planes (p_new from the TMA march, r after the flat K2 pass by the thread
+// that updated it).  Ranks are CTA groups: one group per launch on a GPU of
+// its own, or all ranks as the groups of one launch when emulated.
+// ---------------------------------------------------------------------------
+struct TmaSlabGroup {
+  TmaPcgArgs t;
+  SlabRank rk;
+};
+
+struct TmaSlabArgs {
+  TmaSlabGroup grp[kMaxRanks];
+  int ngroups, nranks, rank0;
+};
+
+// flat pass by the Gr CTAs of one group over the pairs of the OWNED planes
+// (padded planes 1..n of each component): the ghost planes are written by
+// the neighbour ranks concurrently and must not be touched
+template <class F>
+__device__ __forceinline__ void flat_pairs_owned(const Lay &L, int n, int lb, int Gr, F f) {
+  const int64_t stride = (int64_t)Gr * blockDim.x;
+  const int64_t p0 = (int64_t)lb * blockDim.x + threadIdx.x;
+  for (int c = 0; c < 3; ++c) {
+    const int64_t a = (c * L.C + L.Si) >> 1, b = (c * L.C + (int64_t)(n + 1) * L.Si) >> 1;
+    int64_t p = a + p0;
+    for (; p + (kUnroll - 1) * stride < b; p += kUnroll * stride) f(p, stride, kUnroll);
+    for (; p < b; p += stride) f(p, stride, 1);
+  }
+}
+
+// the pairs of planes 0 and n-1 (padded planes 1 and n) of vector v owned by
+// this thread in flat_pairs_owned's mapping, stored into the neighbours'
+// ghost planes
+__device__ __forceinline__ void push_planes_group(const SlabRank &me, const double *v, double *lo, double *hi, int lb,
+                                                  int Gr) {
+  const Lay &L = me.L;
+  const int64_t stride = (int64_t)Gr * blockDim.x;
+  const int64_t p0 = (int64_t)lb * blockDim.x + threadIdx.x;
+  const int64_t half = L.Si >> 1;  // pairs per padded plane (Si is even)
+  for (int side = 0; side < 2; ++side) {
+    double *dst = side == 0 ? lo : hi;
+    if (!dst) continue;
+    const int64_t plane = side == 0 ? 1 : me.n;
+    for (int c = 0; c < 3; ++c) {
+      const int64_t a = (c * L.C + L.Si) >> 1;               // start of the owned pairs
+      const int64_t pa = (c * L.C + plane * L.Si) >> 1, pb = pa + half;
+      const int64_t d = pa - a - p0;
+      int64_t p = a + p0 + (d > 0 ? (d + stride - 1) / stride : 0) * stride;
+      const int64_t dbase = side == 0 ? (c * me.lo_C + me.lo_top) : (c * me.hi_C);
+      for (; p < pb; p += stride) {
+        const double2 w = __ldcg(reinterpret_cast<const double2 *>(v) + p);
+        const int64_t jk = 2 * p - (c * L.C + plane * L.Si);
+        dst[dbase + jk] = w.x;
+        dst[dbase + jk + 1] = w.y;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock, 2) pcg_tma_slab_kernel(const __grid_constant__ TmaSlabArgs S) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t bars[NST];
+  __shared__ double red[3 * kWarps];
+  __shared__ double tot[4];
+  const int Gr = gridDim.x / S.ngroups;
+  const int gi = blockIdx.x / Gr, lb = blockIdx.x % Gr;
+  const TmaPcgArgs &A = S.grp[gi].t;
+  const SlabRank &me = S.grp[gi].rk;
+  const int rank = S.rank0 + gi, R = S.nranks;
+  const StencilPcgArgs &a = A.a;
+  const BrickGeo &g = A.g;
+  const Lay &L = a.L;
+  const double dg = a.dg, of = a.of, inv = a.inv;
+  const bool jac = a.use_jac != 0;
+  double *x = a.x, *r = a.r, *ap = a.ap;
+  const double *b = a.b;
+  const int x0_mode = a.x0_mode;
+  MarchCtx mc;
+  mc.st = reinterpret_cast<Stage *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.bars = bars;
+  mc.ph = 0u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned long long inst = *me.epoch;
+  int status = MQ_OK, iters = 0, converged = 0;
+  double rel = 0.0, bnorm = 0.0, alpha = 0.0, rz = 0.0;
+  bool pold_is_a = true;
+  int applies = (x0_mode == 2) ? 0 : 1;
+  double v3[3] = {0.0, 0.0, 0.0};
+  auto push_r = [&](int64_t e, double v) {  // own row e of r (init pass)
+    const int c = e < L.C ? 0 : (e < 2 * L.C ? 1 : 2);
+    const int64_t rel_e = e - c * L.C, plane = rel_e / L.Si, jk = rel_e - plane * L.Si;
+    if (plane == 1 && me.lo_r) me.lo_r[c * me.lo_C + me.lo_top + jk] = v;
+    if (plane == me.n && me.hi_r) me.hi_r[c * me.hi_C + jk] = v;
+  };
+  // ---- initial residual (krylov.py:209-218) ----
+  if (x0_mode == 1) {
+    // x0 ghost planes first (the march stages planes -1 and n)
+    push_planes_group(me, x, me.lo_x, me.hi_x, lb, Gr);
+    double v0[1] = {0.0};
+    if (!rank_allreduce<1>(me, R, rank, lb, Gr, inst++, v0, red, tot)) { status = MQ_CUDA_ERROR; goto done; }
+    if (threadIdx.x == 0) fence_proxy_async_global();
+    for (int bi = lb; bi < g.nbricks; bi += Gr) {
+      int i0, i1, j0, k0;
+      brick_of(g, bi, i0, i1, j0, k0);
+      march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, nullptr, i0, i1, j0, k0,
+                       [&](int c, int64_t e, auto V) {
+                         const double bv = __ldcg(b + e);
+                         const double rv = sub(bv, stencil3(c, dg, of, V));
+                         r[e] = rv;
+                         push_r(e, rv);
+                         const double z = jac ? mul(inv, rv) : rv;
+                         v3[0] = add(v3[0], mul(bv, bv));
+                         v3[1] = add(v3[1], mul(rv, rv));
+                         v3[2] = add(v3[2], mul(rv, z));
+                       });
+    }
+  } else {
+    flat_pairs_owned(L, me.n, lb, Gr, [&](int64_t p, int64_t stride, int n) {
+      double2 bv[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (u < n) bv[u] = __ldcg(reinterpret_cast<const double2 *>(b) + p + u * stride);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (u < n) {
+          reinterpret_cast<double2 *>(x)[p + u * stride] = make_double2(0.0, 0.0);
+          reinterpret_cast<double2 *>(r)[p + u * stride] = bv[u];
+          const double z0 = jac ? mul(inv, bv[u].x) : bv[u].x, z1 = jac ? mul(inv, bv[u].y) : bv[u].y;
+          v3[0] = add(v3[0], mul(bv[u].x, bv[u].x));
+          v3[0] = add(v3[0], mul(bv[u].y, bv[u].y));
+          v3[2] = add(v3[2], mul(bv[u].x, z0));
+          v3[2] = add(v3[2], mul(bv[u].y, z1));
+        }
+    });
+    v3[1] = v3[0];
+    push_planes_group(me, r, me.lo_r, me.hi_r, lb, Gr);
+  }
+  if (!rank_allreduce<3>(me, R, rank, lb, Gr, inst++, v3, red, tot)) { status = MQ_CUDA_ERROR; goto done; }
+  if (threadIdx.x == 0) fence_proxy_async_global();
+  {
+    bnorm = sqrt(v3[0]);
+    const double target = fmax(a.rel_tol * bnorm, a.abs_tol);
+    double rnorm = sqrt(v3[1]);
+    rz = jac ? v3[2] : v3[1];
+    auto relf = [&](double res) { return bnorm > 0.0 ? res / bnorm : (res == 0.0 ? 0.0 : INFINITY); };
+    if (rnorm <= target) { converged = 1; rel = relf(rnorm); goto done; }
+    double beta = 0.0, alpha_prev = 0.0;
+    bool first = true;
+    for (int it = 1; it <= a.max_iter; ++it) {
+      double *pnew = pold_is_a ? a.pb : a.pa;
+      double *lo_pn = pold_is_a ? me.lo_pb : me.lo_pa, *hi_pn = pold_is_a ? me.hi_pb : me.hi_pa;
+      const CUtensorMap *mp = pold_is_a ? &A.tm_pa : &A.tm_pb;
+      const int nmax = me.n - 1;
+      auto push_p = [&](int q, int c, int64_t jk, double v) {
+        if (q == 0 && lo_pn) lo_pn[c * me.lo_C + me.lo_top + jk] = v;
+        if (q == nmax && hi_pn) hi_pn[c * me.hi_C + jk] = v;
+      };
+      // ---- K1 ----
+      double v1[1] = {0.0};
+      for (int bi = lb; bi < g.nbricks; bi += Gr) {
+        int i0, i1, j0, k0;
+        brick_of(g, bi, i0, i1, j0, k0);
+        march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, pnew, i0, i1, j0, k0,
+                       [&](int c, int64_t e, auto V) {
+                         const double av = stencil3(c, dg, of, V);
+                         ap[e] = av;
+                         v1[0] = add(v1[0], mul(V(c, 0, 0, 0), av));
+                       },
+                       push_p);
+      }
+      ++applies;
+      if (!rank_allreduce<1>(me, R, rank, lb, Gr, inst++, v1, red, tot)) { status = MQ_CUDA_ERROR; goto done; }
+      const double pap = v1[0];
+      if (!isfinite(pap) || pap <= 0.0) { status = MQ_INDEFINITE; iters = it; goto done; }
+      alpha = rz / pap;
+      // ---- K2 ----
+      double v2[2] = {0.0, 0.0};
+      flat_pairs_owned(L, me.n, lb, Gr, [&](int64_t p, int64_t stride, int n) {
+        double2 rv[kUnroll], av[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+          if (u < n) {
+            rv[u] = __ldcg(reinterpret_cast<const double2 *>(r) + p + u * stride);
+            av[u] = __ldcg(reinterpret_cast<const double2 *>(ap) + p + u * stride);
+          }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+          if (u < n) {
+            const double r0 = sub(rv[u].x, mul(alpha, av[u].x));
+            const double r1 = sub(rv[u].y, mul(alpha, av[u].y));
+            reinterpret_cast<double2 *>(r)[p + u * stride] = make_double2(r0, r1);
+            const double z0 = jac ? mul(inv, r0) : r0, z1 = jac ? mul(inv, r1) : r1;
+            v2[0] = add(v2[0], mul(r0, r0));
+            v2[0] = add(v2[0], mul(r1, r1));
+            v2[1] = add(v2[1], mul(r0, z0));
+            v2[1] = add(v2[1], mul(r1, z1));
+          }
+      });
+      push_planes_group(me, r, me.lo_r, me.hi_r, lb, Gr);
+      if (!rank_allreduce<2>(me, R, rank, lb, Gr, inst++, v2, red, tot)) { status = MQ_CUDA_ERROR; goto done; }
+      if (threadIdx.x == 0) fence_proxy_async_global();
+      rnorm = sqrt(v2[0]);
+      iters = it;
+      rel = relf(rnorm);
+      const double rz_new = jac ? v2[1] : v2[0];
+      if (rnorm <= target) { converged = 1; break; }
+      if (!isfinite(rz_new)) { status = MQ_INDEFINITE; break; }
+      beta = rz_new / rz;
+      rz = rz_new;
+      alpha_prev = alpha;
+      first = false;
+      pold_is_a = !pold_is_a;
+    }
+    if (status == MQ_OK) {
+      const double *pdir = converged ? (pold_is_a ? a.pb : a.pa) : (pold_is_a ? a.pa : a.pb);
+      flat_pairs_owned(L, me.n, lb, Gr, [&](int64_t p, int64_t stride, int n) {
+        double2 xv[kUnroll], pv[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+          if (u < n) {
+            xv[u] = __ldcg(reinterpret_cast<const double2 *>(x) + p + u * stride);
+            pv[u] = __ldcg(reinterpret_cast<const double2 *>(pdir) + p + u * stride);
+          }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+          if (u < n)
+            reinterpret_cast<double2 *>(x)[p + u * stride] =
+                make_double2(add(xv[u].x, mul(alpha, pv[u].x)), add(xv[u].y, mul(alpha, pv[u].y)));
+      });
+      if (!converged) status = MQ_NOT_CONVERGED;
+    }
+  }
+done:
+  if (lb == 0 && threadIdx.x == 0) {
+    *me.epoch = inst;
+    PcgOut o;
+    o.iterations = iters;
+    o.converged = converged;
+    o.status = status;
+    o.applies = applies;
+    o.rel = rel;
+    o.bnorm = bnorm;
+    o.alpha = alpha;
+    o.rz = rz;
+    *a.out = o;
+  }
+}
+
 // K_n SpMV through the same TMA march (y on active rows only).
 __global__ void __launch_bounds__(kBlock, 2) kn_apply_tma_kernel(const __grid_constant__ TmaPcgArgs A,
                                                                  double *__restrict__ y) {
@@ -627,6 +893,53 @@ int launch_pcg_brick(const StencilPcgArgs &args, const BrickGeo &geo, int grid, 
   void *params[] = {&A};
   MQ_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_tma_kernel, dim3(grid), dim3(kBlock), params, kTmaSmem, s));
   return MQ_OK;
+}
+
+// groups[q] = (PCG arguments, rank description) of the q-th group of this
+// launch; nplanes[q] its owned planes.  Tensor maps and brick geometry are
+// built here; grid = the co-resident CTA count split evenly over the groups.
+int launch_pcg_tma_slab(const StencilPcgArgs *args, const SlabRank *ranks, const int *nplanes, int ngroups,
+                        int nranks, int rank0, int ny, int nz, cudaStream_t s) {
+  if (ngroups < 1 || ngroups > kMaxRanks) { set_error("1..8 rank groups per launch"); return MQ_INVALID; }
+  int dev = 0, sms = 0, per = 0;
+  MQ_CUDA(cudaGetDevice(&dev));
+  MQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  MQ_CUDA(cudaFuncSetAttribute(pcg_tma_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+  MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pcg_tma_slab_kernel, kBlock, kTmaSmem));
+  if (per < 1) { set_error("TMA slab PCG kernel cannot be resident"); return MQ_CUDA_ERROR; }
+  const int Gr = (sms * per) / ngroups;
+  if (Gr < 1) { set_error("too many rank groups for one GPU"); return MQ_INVALID; }
+  TmaSlabArgs *S = new TmaSlabArgs;
+  std::memset(S, 0, sizeof(TmaSlabArgs));
+  S->ngroups = ngroups;
+  S->nranks = nranks;
+  S->rank0 = rank0;
+  int rc = MQ_OK;
+  for (int q = 0; q < ngroups && rc == MQ_OK; ++q) {
+    TmaPcgArgs &t = S->grp[q].t;
+    t.a = args[q];
+    t.g = make_geo(nplanes[q], ny, nz, Gr);
+    const Lay &L = args[q].L;
+    rc = make_vec_map(L, nplanes[q], ny, nz, args[q].r, &t.tm_r);
+    rc = rc ? rc : make_vec_map(L, nplanes[q], ny, nz, args[q].pa, &t.tm_pa);
+    rc = rc ? rc : make_vec_map(L, nplanes[q], ny, nz, args[q].pb, &t.tm_pb);
+    rc = rc ? rc : make_vec_map(L, nplanes[q], ny, nz, args[q].x, &t.tm_x);
+    S->grp[q].rk = ranks[q];
+  }
+  if (rc == MQ_OK) {
+    for (int q = 0; q < ngroups; ++q) {
+      cudaError_t e = cudaMemsetAsync(&args[q].bar->count, 0, sizeof(unsigned long long), s);
+      if (e != cudaSuccess) { rc = cuda_fail(e, "slab barrier reset"); break; }
+    }
+  }
+  if (rc == MQ_OK) {
+    void *params[] = {S};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void *)pcg_tma_slab_kernel, dim3(Gr * ngroups), dim3(kBlock),
+                                                params, kTmaSmem, s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "TMA slab PCG launch");
+  }
+  delete S;
+  return rc;
 }
 
 int launch_kn_apply_brick(const Lay &L, const BrickGeo &geo, const uint32_t *mask, double dg, double of,

@@ -27,7 +27,7 @@ import numpy as np
 from . import _lib
 from ._lib import check, dptr, f64
 
-__all__ = ["slab_range", "SlabGrid", "TorchComm", "LoopbackComm", "slab_pcg_solve"]
+__all__ = ["slab_range", "SlabGrid", "TorchComm", "LoopbackComm", "slab_pcg_solve", "fused_slab_pcg_solve_local"]
 
 
 def slab_range(nx: int, world: int, rank: int) -> tuple[int, int]:
@@ -272,3 +272,27 @@ def slab_pcg_solve(slabs, comm, *, x0_given: bool, rel_tol=1e-8, abs_tol=0.0, ma
     for s in slabs:
         s.final(alpha, pold_is_a)
     return max_iter, rel(r_norm), False, applies
+
+
+def fused_slab_pcg_solve_local(slabs, *, x0_given: bool, rel_tol=1e-8, abs_tol=0.0, max_iter=5000,
+                               jacobi=True):
+    """krylov.py:174-250 over the slabs of this process with the fused kernel
+    (csrc/slab_fused.cu): ghost planes stored straight into the neighbour
+    slab and the rank all-reduce through device mailboxes, one cooperative
+    launch whose CTA groups are the ranks (the one-GPU form of the per-GPU
+    kernel).  Right-hand sides in ``s.b``, start vectors in ``s.x``; the
+    solution is left in ``s.x``.  Returns (iterations, final_rel_residual,
+    converged, applications)."""
+    from .krylov import IndefiniteOperatorError
+    lib = slabs[0].lib
+    n = len(slabs)
+    ctxs = (ctypes.c_void_p * n)(*[s.ctx.value for s in slabs])
+    bs = (ctypes.c_void_p * n)(*[s.b for s in slabs])
+    xs = (ctypes.c_void_p * n)(*[s.x for s in slabs])
+    rep = _lib.SolveReportC()
+    rc = lib.mq_slab_fused_solve_local(ctxs, n, bs, xs, int(bool(x0_given)), float(rel_tol), float(abs_tol),
+                                       int(max_iter), int(bool(jacobi)), ctypes.byref(rep))
+    if rc == _lib.MQ_INDEFINITE:
+        raise IndefiniteOperatorError(_lib.last_error())
+    check(rc, allow=(0, 1))
+    return int(rep.iterations), float(rep.final_rel_residual), bool(rep.converged), int(rep.applies)

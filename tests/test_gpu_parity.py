@@ -512,6 +512,64 @@ def test_slab_pcg_loopback_on_one_gpu(gpu_ok, world, x0_given):
         s.close()
 
 
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+@pytest.mark.parametrize("x0_given", [False, True])
+def test_fused_slab_pcg_on_one_gpu(gpu_ok, world, x0_given):
+    """The fused per-rank slab kernel (ghost stores into the neighbour slab,
+    rank all-reduce through device mailboxes), its ranks emulated as the CTA
+    groups of one cooperative launch: solution vs the single-domain oracle,
+    iterations within +-1; repeated solves reuse the mailboxes (epochs)."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200.slab import SlabGrid, fused_slab_pcg_solve_local
+    spec, m = oracle_model(0)
+    prob = C.make_problem(0)
+    slabs = [SlabGrid(prob, r, world) for r in range(world)]
+    idx = [np.searchsorted(m.noncond_global, s.partition()) for s in slabs]
+    rng = np.random.default_rng(11)
+    inv = O.jacobi_inverse(m.kn.diagonal())
+    for rep in range(3):
+        b = m.kn @ rng.standard_normal(m.n_n)
+        x0 = rng.standard_normal(m.n_n) * 1e-3
+        for s, ix in zip(slabs, idx):
+            s.upload(b[ix], s.b)
+            s.upload(x0[ix] if x0_given else np.zeros(ix.size), s.x)
+        it, relres, conv, app = fused_slab_pcg_solve_local(slabs, x0_given=x0_given, rel_tol=1e-8)
+        ref = O.pcg(m.kn_apply, b, x0=x0 if x0_given else None, rel_tol=1e-8, inv_diag=inv)
+        x = np.zeros(m.n_n)
+        for s, ix in zip(slabs, idx):
+            x[ix] = s.download(s.x)
+        assert conv and abs(it - ref.iterations) <= 1, (it, ref.iterations)
+        assert app == ref.applies - (ref.iterations - it)
+        assert rel(x, ref.x) <= 1e-8
+    for s in slabs:
+        s.close()
+
+
+@pytest.mark.slow
+def test_fused_slab_pcg_config1_grid(gpu_ok):
+    """64^3 (configs[1] grid) split over 4 emulated ranks: the cold source
+    solve against the single-context device solve."""
+    from paper_1611_06721_b200 import PcgConfig, configs as C, pcg_solve
+    from paper_1611_06721_b200.device import DeviceGrid
+    from paper_1611_06721_b200.slab import SlabGrid, fused_slab_pcg_solve_local
+    prob = C.make_problem(1)
+    with DeviceGrid(prob) as g:
+        nc_all = g.partition()[0]
+        x_ref, rep_ref = pcg_solve(g.kn_operator(), prob.pattern, config=PcgConfig(rel_tol=1e-8))
+    slabs = [SlabGrid(prob, r, 4) for r in range(4)]
+    idx = [np.searchsorted(nc_all, s.partition()) for s in slabs]
+    for s, ix in zip(slabs, idx):
+        s.upload(prob.pattern[ix], s.b)
+    it, relres, conv, app = fused_slab_pcg_solve_local(slabs, x0_given=False, rel_tol=1e-8)
+    x = np.zeros(nc_all.size)
+    for s, ix in zip(slabs, idx):
+        x[ix] = s.download(s.x)
+    assert conv and abs(it - rep_ref.iterations) <= 1
+    assert rel(x, x_ref) <= 1e-8
+    for s in slabs:
+        s.close()
+
+
 @pytest.mark.gpu
 def test_concurrent_members_match_sequential(gpu_ok):
     """configs[3] members stepped side by side on SM slices (ensemble.run_members)
