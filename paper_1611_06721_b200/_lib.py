@@ -140,6 +140,9 @@ SIGNATURES = {
     "mq_slab_k1": (I32, [VP, VP, I32, D, D, I32, I32, c_double_p]),
     "mq_slab_k2": (I32, [VP, D, I32, c_double_p]),
     "mq_slab_final": (I32, [VP, VP, D, I32]),
+    "mq_slab_ipc_export": (I32, [VP, VP, VP]),
+    "mq_slab_ipc_import": (I32, [VP, I32, I32, VP, c_int32_p, VP]),
+    "mq_slab_fused_solve_peer": (I32, [VP, VP, I32, D, D, I32, I32, ctypes.POINTER(SolveReportC)]),
     "mq_slab_fused_solve_local": (I32, [ctypes.POINTER(VP), I32, ctypes.POINTER(VP), ctypes.POINTER(VP), I32, D, D, I32, I32,
                                         ctypes.POINTER(SolveReportC)]),
     "mq_timer_start": (I32, [VP]),

@@ -56,6 +56,7 @@ struct RunDev {
 };
 
 struct SolverHost;
+struct SlabPeer;
 
 }  // namespace mq
 
@@ -110,6 +111,7 @@ struct mq_ctx {
   double t_now = 0;
   // solver
   mq::SolverHost *solver = nullptr;
+  mq::SlabPeer *peer = nullptr;  // fused slab PCG across processes (IPC-mapped neighbours)
   // bookkeeping
   std::vector<void *> allocs;
   std::set<double *> vecs;
@@ -135,6 +137,7 @@ int ctx_pcg(mq_ctx *ctx, const double *b, double *x, int x0_mode, double rel_tol
             int use_jac, mq_solve_report *rep);
 int conducting_init(mq_ctx *ctx);
 void solver_free(mq_ctx *ctx);
+void slab_peer_free(mq_ctx *ctx);
 void solver_graph_reset(mq_ctx *ctx);
 
 int coop_grid(const void *kernel, int want_blocks, int *out);

@@ -34,6 +34,7 @@
 // must be co-resident: one launch, never several).
 #include <algorithm>
 #include <string>
+#include <vector>
 
 #include "mq_ctx.h"
 #include "mq_device.cuh"
@@ -241,6 +242,23 @@ static void fill_rank(SlabRank &s, mq_ctx *ctx, const double *b, double *x) {
   s.epoch = ctx->d_mcount + 1;
 }
 
+// ---- one rank per process: IPC-mapped neighbour buffers ------------------
+constexpr int kIpcBufs = 6;  // r, pa, pb, x, mailbox, counter
+
+struct SlabPeer {
+  SlabRank rk{};
+  int rank = 0, nranks = 1;
+  double *x = nullptr;
+  std::vector<void *> opened;  // IPC mappings to close
+};
+
+void slab_peer_free(mq_ctx *ctx) {
+  if (!ctx->peer) return;
+  for (void *p : ctx->peer->opened) cudaIpcCloseMemHandle(p);
+  delete ctx->peer;
+  ctx->peer = nullptr;
+}
+
 }  // namespace mq
 
 using namespace mq;
@@ -357,6 +375,117 @@ int mq_slab_fused_solve_local(mq_ctx **ctxs, int32_t nranks, const double *const
   if (e != cudaSuccess) return cuda_fail(e, "fused slab PCG");
   if (rc) return rc;
   return finish_report(c0, rep);
+}
+
+
+// Handles of this rank's r, p_a, p_b, x (x_dev), mailbox and counter,
+// kIpcBufs x sizeof(cudaIpcMemHandle_t) bytes, to be exchanged between the
+// ranks (torch.distributed all_gather on the host).
+int mq_slab_ipc_export(mq_ctx *ctx, const double *x_dev, void *handles_out) {
+  int rc = fused_ready(ctx);
+  if (rc) return rc;
+  const void *bufs[kIpcBufs] = {ctx->d_r, ctx->d_p0, ctx->d_p1, x_dev, ctx->d_mbox, ctx->d_mcount};
+  cudaIpcMemHandle_t *h = reinterpret_cast<cudaIpcMemHandle_t *>(handles_out);
+  for (int q = 0; q < kIpcBufs; ++q) MQ_CUDA(cudaIpcGetMemHandle(&h[q], const_cast<void *>(bufs[q])));
+  return MQ_OK;
+}
+
+// all_handles: nranks x kIpcBufs handles in rank order; nplanes: owned
+// planes per rank.  Maps the neighbours' r/p/x and every rank's mailbox and
+// counter into this process (NVLink peer access), and remembers x_dev as the
+// solution buffer of mq_slab_fused_solve_peer.
+int mq_slab_ipc_import(mq_ctx *ctx, int32_t rank, int32_t nranks, const void *all_handles, const int32_t *nplanes,
+                       double *x_dev) {
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks) { set_error("invalid rank layout"); return MQ_INVALID; }
+  int rc = fused_ready(ctx);
+  if (rc) return rc;
+  slab_peer_free(ctx);
+  SlabPeer *P = new SlabPeer;
+  P->rank = rank;
+  P->nranks = nranks;
+  P->x = x_dev;
+  const cudaIpcMemHandle_t *h = reinterpret_cast<const cudaIpcMemHandle_t *>(all_handles);
+  auto open = [&](int q, int k, void **out) -> int {
+    if (q == rank) {
+      void *own[kIpcBufs] = {ctx->d_r, ctx->d_p0, ctx->d_p1, x_dev, ctx->d_mbox, ctx->d_mcount};
+      *out = own[k];
+      return MQ_OK;
+    }
+    cudaError_t e = cudaIpcOpenMemHandle(out, h[q * kIpcBufs + k], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    P->opened.push_back(*out);
+    return MQ_OK;
+  };
+  SlabRank &s = P->rk;
+  const Lay &L = ctx->topo.L;
+  auto comp_stride = [&](int n) { return ((int64_t)(n + 2) * L.Si + 31) / 32 * 32; };
+  for (int q = 0; q < nranks && rc == MQ_OK; ++q) {
+    void *mb = nullptr, *mc = nullptr;
+    rc = open(q, 4, &mb);
+    rc = rc ? rc : open(q, 5, &mc);
+    s.mbox[q] = (double *)mb;
+    s.mcount[q] = (unsigned long long *)mc;
+  }
+  if (rc == MQ_OK && rank > 0) {
+    void *v[4];
+    for (int k = 0; k < 4 && rc == MQ_OK; ++k) rc = open(rank - 1, k, &v[k]);
+    s.lo_r = (double *)v[0];
+    s.lo_pa = (double *)v[1];
+    s.lo_pb = (double *)v[2];
+    s.lo_x = (double *)v[3];
+    s.lo_C = comp_stride(nplanes[rank - 1]);
+    s.lo_top = (int64_t)(nplanes[rank - 1] + 1) * L.Si;
+  }
+  if (rc == MQ_OK && rank + 1 < nranks) {
+    void *v[4];
+    for (int k = 0; k < 4 && rc == MQ_OK; ++k) rc = open(rank + 1, k, &v[k]);
+    s.hi_r = (double *)v[0];
+    s.hi_pa = (double *)v[1];
+    s.hi_pb = (double *)v[2];
+    s.hi_x = (double *)v[3];
+    s.hi_C = comp_stride(nplanes[rank + 1]);
+  }
+  ctx->peer = P;
+  if (rc) { slab_peer_free(ctx); return rc; }
+  return MQ_OK;
+}
+
+// This rank's part of the distributed solve (one CTA group on this GPU); all
+// ranks call it with the same arguments.  b: this slab's right-hand side.
+int mq_slab_fused_solve_peer(mq_ctx *ctx, const double *b, int32_t x0_given, double rel_tol, double abs_tol,
+                             int32_t max_iter, int32_t use_jacobi, mq_solve_report *rep) {
+  SlabPeer *P = ctx->peer;
+  if (!P) { set_error("mq_slab_ipc_import first"); return MQ_INVALID; }
+  if (!(rel_tol >= 0.0) || !(abs_tol >= 0.0) || max_iter < 0) { set_error("invalid PCG configuration"); return MQ_INVALID; }
+  SlabRank rk = P->rk;
+  fill_rank(rk, ctx, b, P->x);
+  StencilPcgArgs t{};
+  t.L = ctx->topo.L;
+  t.mask = ctx->d_mask;
+  t.dg = ctx->kn_diag;
+  t.of = ctx->kn_off;
+  t.inv = ctx->jac_inv;
+  t.use_jac = use_jacobi ? 1 : 0;
+  t.x0_mode = x0_given ? 1 : 2;
+  t.b = b;
+  t.x = P->x;
+  t.r = ctx->d_r;
+  t.pa = ctx->d_p0;
+  t.pb = ctx->d_p1;
+  t.ap = ctx->d_ap;
+  t.rel_tol = rel_tol;
+  t.abs_tol = abs_tol;
+  t.max_iter = max_iter;
+  t.partials = ctx->d_partials;
+  t.bar = ctx->d_bar;
+  t.out = ctx->d_out;
+  const int np = ctx->topo.nx;
+  int rc = launch_pcg_tma_slab(&t, &rk, &np, 1, P->nranks, P->rank, ctx->topo.ny, ctx->topo.nz, ctx->stream);
+  if (rc) return rc;
+  ctx->launches += 1;
+  MQ_CUDA(cudaMemcpyAsync(ctx->h_out, ctx->d_out, sizeof(PcgOut), cudaMemcpyDeviceToHost, ctx->stream));
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  return finish_report(ctx, rep);
 }
 
 }  // extern "C"

@@ -27,7 +27,10 @@ import numpy as np
 from . import _lib
 from ._lib import check, dptr, f64
 
-__all__ = ["slab_range", "SlabGrid", "TorchComm", "LoopbackComm", "slab_pcg_solve", "fused_slab_pcg_solve_local"]
+__all__ = ["slab_range", "SlabGrid", "TorchComm", "LoopbackComm", "slab_pcg_solve", "fused_slab_pcg_solve_local",
+           "gather_ipc_tables", "fused_peer_setup", "fused_peer_solve"]
+
+IPC_HANDLE_BYTES = 6 * 64  # r, p_a, p_b, x, mailbox, counter (cudaIpcMemHandle_t = 64 B)
 
 
 def slab_range(nx: int, world: int, rank: int) -> tuple[int, int]:
@@ -292,6 +295,45 @@ def fused_slab_pcg_solve_local(slabs, *, x0_given: bool, rel_tol=1e-8, abs_tol=0
     rep = _lib.SolveReportC()
     rc = lib.mq_slab_fused_solve_local(ctxs, n, bs, xs, int(bool(x0_given)), float(rel_tol), float(abs_tol),
                                        int(max_iter), int(bool(jacobi)), ctypes.byref(rep))
+    if rc == _lib.MQ_INDEFINITE:
+        raise IndefiniteOperatorError(_lib.last_error())
+    check(rc, allow=(0, 1))
+    return int(rep.iterations), float(rep.final_rel_residual), bool(rep.converged), int(rep.applies)
+
+
+def gather_ipc_tables(local_handles: bytes, local_planes: int, dist=None):
+    """All-gather every rank's IPC handle block and owned plane count, in
+    rank order (torch.distributed all_gather_object; identity for 1 rank)."""
+    if len(local_handles) != IPC_HANDLE_BYTES:
+        raise ValueError("unexpected IPC handle block size")
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return [local_handles], [int(local_planes)]
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, (local_handles, int(local_planes)))
+    return [h for h, _ in out], [n for _, n in out]
+
+
+def fused_peer_setup(slab: SlabGrid, dist=None):
+    """Map the neighbour ranks' buffers (one rank per process and GPU) for
+    :func:`fused_peer_solve` (mq_slab_ipc_export / import)."""
+    rank = dist.get_rank() if dist is not None and dist.is_initialized() else 0
+    world = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
+    buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    check(slab.lib.mq_slab_ipc_export(slab.ctx, ctypes.c_void_p(slab.x), buf))
+    handles, planes = gather_ipc_tables(buf.raw, slab.n_planes, dist)
+    allb = ctypes.create_string_buffer(b"".join(handles), IPC_HANDLE_BYTES * world)
+    np_arr = (ctypes.c_int32 * world)(*planes)
+    check(slab.lib.mq_slab_ipc_import(slab.ctx, rank, world, allb, np_arr, ctypes.c_void_p(slab.x)))
+
+
+def fused_peer_solve(slab: SlabGrid, *, x0_given: bool, rel_tol=1e-8, abs_tol=0.0, max_iter=5000, jacobi=True):
+    """This rank's part of the fused distributed solve (every rank calls it):
+    right-hand side in ``slab.b``, start vector / solution in ``slab.x``.
+    Returns (iterations, final_rel_residual, converged, applications)."""
+    from .krylov import IndefiniteOperatorError
+    rep = _lib.SolveReportC()
+    rc = slab.lib.mq_slab_fused_solve_peer(slab.ctx, ctypes.c_void_p(slab.b), int(bool(x0_given)), float(rel_tol),
+                                           float(abs_tol), int(max_iter), int(bool(jacobi)), ctypes.byref(rep))
     if rc == _lib.MQ_INDEFINITE:
         raise IndefiniteOperatorError(_lib.last_error())
     check(rc, allow=(0, 1))

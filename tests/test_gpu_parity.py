@@ -545,6 +545,30 @@ def test_fused_slab_pcg_on_one_gpu(gpu_ok, world, x0_given):
         s.close()
 
 
+def test_fused_slab_peer_path_single_rank(gpu_ok):
+    """The one-rank-per-process entry points (IPC export/import, the kernel
+    launched as a single CTA group) at one rank: same answer as the oracle.
+    (More ranks need more GPUs; the protocol is the one the emulated
+    multi-group launches above exercise.)"""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200.slab import SlabGrid, fused_peer_setup, fused_peer_solve
+    spec, m = oracle_model(0)
+    s = SlabGrid(C.make_problem(0), 0, 1)
+    fused_peer_setup(s)
+    rng = np.random.default_rng(13)
+    inv = O.jacobi_inverse(m.kn.diagonal())
+    for x0_given in (False, True, False):
+        b = m.kn @ rng.standard_normal(m.n_n)
+        x0 = rng.standard_normal(m.n_n) * 1e-3
+        s.upload(b, s.b)
+        s.upload(x0 if x0_given else np.zeros(m.n_n), s.x)
+        it, relres, conv, app = fused_peer_solve(s, x0_given=x0_given, rel_tol=1e-8)
+        ref = O.pcg(m.kn_apply, b, x0=x0 if x0_given else None, rel_tol=1e-8, inv_diag=inv)
+        assert conv and abs(it - ref.iterations) <= 1
+        assert rel(s.download(s.x), ref.x) <= 1e-8
+    s.close()
+
+
 @pytest.mark.slow
 def test_fused_slab_pcg_config1_grid(gpu_ok):
     """64^3 (configs[1] grid) split over 4 emulated ranks: the cold source

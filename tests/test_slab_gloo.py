@@ -96,3 +96,39 @@ def test_distributed_pcg_gloo_matches_single_domain(x0_given):
     assert np.all(owned == 1)                      # the slabs partition the dofs
     assert its == {ref.iterations}                 # every rank took the same decisions
     assert np.linalg.norm(x - ref.x) <= 1e-12 * np.linalg.norm(ref.x)
+
+
+def _ipc_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_1611_06721_b200.slab import IPC_HANDLE_BYTES, gather_ipc_tables
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = bytes([rank + 1]) * IPC_HANDLE_BYTES   # stand-in handle block
+        handles, planes = gather_ipc_tables(mine, 10 + rank, dist)
+        q.put((rank, [h[0] for h in handles], [len(h) for h in handles], planes))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_peer_ipc_tables_gloo():
+    """Host side of the fused slab kernel's setup: every rank ends up with all
+    ranks' IPC handle blocks and plane counts in rank order."""
+    import torch.multiprocessing as mp
+    from paper_1611_06721_b200.slab import IPC_HANDLE_BYTES, gather_ipc_tables
+    with pytest.raises(ValueError):
+        gather_ipc_tables(b"x", 1)
+    assert gather_ipc_tables(b"\0" * IPC_HANDLE_BYTES, 7) == ([b"\0" * IPC_HANDLE_BYTES], [7])
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, first_bytes, sizes, planes in out:
+        assert first_bytes == [1, 2, 3] and sizes == [IPC_HANDLE_BYTES] * 3 and planes == [10, 11, 12]
