@@ -93,6 +93,7 @@ __device__ bool rank_allreduce(const SlabRank &me, int nranks, int rank, int lb,
   if (!group_sync(me.bar, Gr)) return false;
   grid_partials_sum<NV>(me.partials, Gr, v, tot);  // rank total, identical in the group
   const int R = nranks;
+  if (R == 1) return true;  // a single rank: the group total is the total
   const int slot = (int)(inst % kRing);
   if (lb == 0 && threadIdx.x == 0) {
     for (int q = 0; q < R; ++q)
@@ -119,10 +120,17 @@ __device__ bool rank_allreduce(const SlabRank &me, int nranks, int rank, int lb,
   if (threadIdx.x == 0) {
     fence_acq_rel_sys();
     const double *box = me.mbox[rank] + (int64_t)slot * kMaxRanks * 4;
+    double val[kMaxRanks][NV];  // all loads in flight, then the rank-order sums
+#pragma unroll
+    for (int q = 0; q < kMaxRanks; ++q)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) val[q][k] = q < R ? ld_relaxed_sys_f64(box + q * 4 + k) : 0.0;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       double s = 0.0;
-      for (int q = 0; q < R; ++q) s = add(s, ld_relaxed_sys_f64(box + q * 4 + k));
+#pragma unroll
+      for (int q = 0; q < kMaxRanks; ++q)
+        if (q < R) s = add(s, val[q][k]);
       tot[k] = s;
     }
   }
