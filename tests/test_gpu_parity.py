@@ -267,6 +267,49 @@ def test_pod_strategy_parity(c0):
     assert abs(strat.diagnostics()["min_pod_info"] - pod.min_info) <= 1e-7
 
 
+def test_strategy_edge_cases(c0):
+    """startvec.py edge cases the reference tests (test_startvec.py: zero and
+    non-finite columns, rank-one and all-zero snapshot buffers, empty
+    buffers): device strategies vs the oracle's."""
+    from paper_1611_06721_b200 import DeviceStrategy, RhsFamily
+    spec, m, prob, g = c0
+    inv = O.jacobi_inverse(m.kn.diagonal())
+    rng = np.random.default_rng(21)
+    rhs = m.kn @ rng.standard_normal(m.n_n)
+    v = O.pcg(m.kn_apply, m.kn @ rng.standard_normal(m.n_n), rel_tol=1e-8, inv_diag=inv).x
+    fam = RhsFamily.SOURCE_CURRENT
+    # CSPE: zero / non-finite columns are dropped, the cache is unchanged
+    strat = DeviceStrategy(g, "cspe", max_cols=3, drop_tol=1e-8)
+    cache = O.SpeCache(m.n_n, m.kn_apply, max_cols=3, drop_tol=1e-8)
+    bad = v.copy()
+    bad[7] = np.nan
+    for col in (np.zeros(m.n_n), v, bad, v * np.inf):
+        strat.observe(fam, col)
+        cache.insert(col)
+        assert strat.basis_size(fam) == cache.k
+    assert strat.maintenance_applies == cache.products == 1
+    assert rel(strat.start_vector(fam, rhs), cache.project(rhs)) <= 1e-8
+    # POD: empty buffer -> zero start; all-zero snapshots -> zero start, k = 0
+    pstrat = DeviceStrategy(g, "pod", n_pod=4, eps_pod=1e-4)
+    pod = O.PodStrategyOracle(m.n_n, m.kn_apply, n_pod=4, eps_pod=1e-4)
+    assert np.array_equal(pstrat.start_vector(fam, rhs), np.zeros(m.n_n))
+    for _ in range(2):
+        pstrat.observe(fam, np.zeros(m.n_n))
+        pod.observe(O.FAM_SOURCE, np.zeros(m.n_n))
+    x_dev, x_ref = pstrat.start_vector(fam, rhs), pod.start(O.FAM_SOURCE, rhs)
+    assert np.array_equal(x_dev, np.zeros(m.n_n)) and np.array_equal(x_ref, np.zeros(m.n_n))
+    assert pstrat.diagnostics()["pod_k"] == pod.last_k == 0
+    # rank-one snapshots: one retained mode, start = its Galerkin projection
+    pstrat = DeviceStrategy(g, "pod", n_pod=4, eps_pod=1e-4)
+    pod = O.PodStrategyOracle(m.n_n, m.kn_apply, n_pod=4, eps_pod=1e-4)
+    for a in (1.0, -2.0, 0.5, 3.0, 4.0):  # more than n_pod: the ring wraps
+        pstrat.observe(fam, a * v)
+        pod.observe(O.FAM_SOURCE, a * v)
+    x_dev, x_ref = pstrat.start_vector(fam, rhs), pod.start(O.FAM_SOURCE, rhs)
+    assert pstrat.diagnostics()["pod_k"] == pod.last_k == 1
+    assert rel(x_dev, x_ref) <= 1e-8
+
+
 @pytest.mark.parametrize("strategy,nsteps", [("cspe", 100), ("pod", 30), ("previous", 30)])
 def test_transient_config0_device_loop(gpu_ok, strategy, nsteps):
     """run_explicit twin (device-resident loop, CUDA graph replay) vs oracle."""
