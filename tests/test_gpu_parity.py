@@ -390,6 +390,44 @@ def test_device_probe_in_run(gpu_ok):
     assert np.max(np.abs(res2.probe_b - ref_b[::2]) / np.abs(ref_b).max()) <= REL_FIELD
 
 
+def test_schur_loop_semantics(gpu_ok):
+    """test_schur.py cases on the device loop: a zero source from a zero state
+    stays exactly zero with zero iterations; the final state does not depend
+    on the start-vector strategy; output rows, validation and the step
+    budget; a non-finite state names the failing step."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, SchurOperator, StepFailureError, run_explicit
+    from paper_1611_06721_b200.schur import explicit_euler_step
+    spec, m = oracle_model(0)
+    quiet = C.make_problem(0)
+    quiet.pattern = np.zeros_like(quiet.pattern)
+    res = run_explicit(quiet, t_end=5 * spec.dt, dt=spec.dt, strategy="previous",
+                       pcg=PcgConfig(rel_tol=1e-8))
+    assert not res.final_a_c.any() and not res.final_a_n.any()
+    assert res.aggregates["iterations"] == {"source": 0, "coupling_current": 0, "coupling_previous": 0}
+    finals = {}
+    for strategy in ("previous", "cspe", "pod", "zero"):
+        finals[strategy] = run_explicit(C.make_problem(0), t_end=12 * spec.dt, dt=spec.dt, strategy=strategy,
+                                        pcg=PcgConfig(rel_tol=1e-10), max_cols=5, n_pod=6).final_a_c
+    for strategy in ("cspe", "pod", "zero"):
+        assert rel(finals[strategy], finals["previous"]) <= 1e-8, strategy
+    res = run_explicit(C.make_problem(0), t_end=10 * spec.dt, dt=spec.dt, strategy="cspe",
+                       pcg=PcgConfig(rel_tol=1e-8), max_cols=5, output_period=2 * spec.dt, probe="device")
+    assert res.times[0] == 0.0 and res.times[-1] == pytest.approx(10 * spec.dt, rel=1e-12)
+    assert np.all(np.diff(res.times) > 0) and len(res.times) == len(res.probe_b) == 6
+    assert res.aggregates["steps"] == 10 and res.aggregates["solves"]["source"] >= 10
+    prob = C.make_problem(0)
+    for kw in ({"t_end": 0.0, "dt": spec.dt}, {"t_end": 1.0, "dt": "sideways"}, {"t_end": 1.0, "dt": -1e-3},
+               {"t_end": 1.0, "dt": spec.dt, "output_period": 0.0}):
+        with pytest.raises(ValueError):
+            run_explicit(prob, **kw)
+    with pytest.raises(StepFailureError):
+        run_explicit(prob, t_end=1.0, dt=1e-6, strategy="previous", max_steps=10)
+    op = SchurOperator(C.make_problem(0), pcg=PcgConfig(rel_tol=1e-8), strategy="previous")
+    with pytest.raises(StepFailureError, match="7"):
+        explicit_euler_step((np.full(m.n_c, 1e300), 0.0), 1e9, op, step_index=7)
+
+
 def test_single_step_api_matches_oracle(gpu_ok):
     """explicit_euler_step / recover_an / SchurOperator.solve_kn twins."""
     from paper_1611_06721_b200 import configs as C
