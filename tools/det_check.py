@@ -1,3 +1,9 @@
+"""Determinism check of the device loop: the same configs[0] POD run twice
+eager and twice as graph replays must give bit-identical states and
+iteration counts.
+
+    python tools/det_check.py
+"""
 import numpy as np, sys
 sys.path.insert(0, '/root/repo')
 from paper_1611_06721_b200 import configs as C, PcgConfig, run_explicit
