@@ -111,6 +111,9 @@ typedef struct mq_diag {
 const char *mq_last_error(void);
 int mq_device_count(int32_t *count);
 int mq_device_sm_count(int32_t device, int32_t *sms);
+/* page-locked host memory (result arrays of the Python mirror) */
+int mq_host_alloc(int64_t bytes, void **out);
+int mq_host_free(void *p);
 int mq_ctx_create(const mq_grid_desc *desc, int32_t device, mq_ctx **out);
 void mq_ctx_destroy(mq_ctx *ctx);
 int64_t mq_n_n(const mq_ctx *ctx);     /* nonconducting interior dofs */

@@ -77,6 +77,8 @@ SIGNATURES = {
     "mq_last_error": (ctypes.c_char_p, []),
     "mq_device_count": (I32, [c_int32_p]),
     "mq_device_sm_count": (I32, [I32, c_int32_p]),
+    "mq_host_alloc": (I32, [I64, ctypes.POINTER(VP)]),
+    "mq_host_free": (I32, [VP]),
     "mq_ctx_create": (I32, [ctypes.POINTER(GridDesc), I32, ctypes.POINTER(VP)]),
     "mq_ctx_destroy": (None, [VP]),
     "mq_n_n": (I64, [VP]),
@@ -241,3 +243,51 @@ def sm_count(device: int = 0) -> int:
     n = ctypes.c_int32(0)
     check(load().mq_device_sm_count(int(device), ctypes.byref(n)))
     return int(n.value)
+
+
+class PinnedPool:
+    """Page-locked float64 result arrays (mq_host_alloc), recycled by size.
+
+    ``empty(n)`` returns a numpy array backed by pinned memory; when the
+    array (and every view of it) is garbage collected, its buffer goes back
+    to the pool instead of being freed, so steady-state calls allocate
+    nothing and the device-to-host copy into it runs at DMA speed."""
+
+    def __init__(self, max_free_per_size: int = 8):
+        import threading
+        self._free: dict[int, list[int]] = {}
+        self._lock = threading.Lock()
+        self._max = max_free_per_size
+
+    def _release(self, n: int, ptr: int):
+        with self._lock:
+            lst = self._free.setdefault(n, [])
+            if len(lst) < self._max:
+                lst.append(ptr)
+                return
+        load().mq_host_free(ctypes.c_void_p(ptr))
+
+    def empty(self, n: int) -> np.ndarray:
+        import weakref
+        with self._lock:
+            lst = self._free.get(n)
+            ptr = lst.pop() if lst else None
+        if ptr is None:
+            p = ctypes.c_void_p()
+            check(load().mq_host_alloc(8 * max(n, 1), ctypes.byref(p)))
+            ptr = p.value
+        buf = (ctypes.c_double * max(n, 1)).from_address(ptr)
+        arr = np.frombuffer(buf, dtype=np.float64, count=n)
+        weakref.finalize(arr, self._release, n, ptr)
+        return arr
+
+
+_PINNED = None
+
+
+def pinned_empty(n: int) -> np.ndarray:
+    """float64 array of length n in recycled page-locked memory."""
+    global _PINNED
+    if _PINNED is None:
+        _PINNED = PinnedPool()
+    return _PINNED.empty(n)

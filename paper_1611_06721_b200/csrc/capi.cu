@@ -118,6 +118,19 @@ int mq_device_count(int32_t *count) {
   return MQ_OK;
 }
 
+// Page-locked host memory for result arrays: device-to-host copies into it
+// run at DMA speed instead of through the driver's pageable staging.
+int mq_host_alloc(int64_t bytes, void **out) {
+  if (bytes <= 0 || !out) { set_error("invalid host allocation"); return MQ_INVALID; }
+  MQ_CUDA(cudaMallocHost(out, (size_t)bytes));
+  return MQ_OK;
+}
+
+int mq_host_free(void *p) {
+  if (p) MQ_CUDA(cudaFreeHost(p));
+  return MQ_OK;
+}
+
 int mq_device_sm_count(int32_t device, int32_t *sms) {
   int n = 0;
   cudaError_t e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);

@@ -154,7 +154,7 @@ class DeviceGrid:
         check(self.lib.mq_vec_upload(self.ctx, dptr(v), ctypes.c_void_p(dev)))
 
     def download(self, dev: int) -> np.ndarray:
-        out = np.empty(self.n_n)
+        out = _lib.pinned_empty(self.n_n)
         check(self.lib.mq_vec_download(self.ctx, ctypes.c_void_p(dev), dptr(out)))
         return out
 

@@ -237,7 +237,7 @@ def explicit_euler_step(state, dt: float, op: SchurOperator, step_index: int | N
 def recover_an(op: SchurOperator, a_c, t: float):
     """a_n = K_n^+ j_n(t) - K_n^+ K_cn^T a_c (schur.py:408-419)."""
     op._set_state(a_c, t)
-    a_n = np.empty(op.grid.n_n)
+    a_n = _lib.pinned_empty(op.grid.n_n)
     r1, r2 = _lib.SolveReportC(), _lib.SolveReportC()
     rc = op.lib.mq_recover_an(op.grid.ctx, float(op.problem.waveform(t)), dptr(a_n),
                               ctypes.byref(r1), ctypes.byref(r2))
