@@ -643,8 +643,12 @@ __device__ void run_post(const Post &p) {
 #define MQ_EIG_ABS 1e-16
 #endif
 __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
-  __shared__ double A[MAXS * MAXS];
-  __shared__ double V[MAXS * MAXS];
+  // rows padded to an odd number of doubles: the column updates walk a
+  // column with consecutive threads, which a 32-double row stride would put
+  // in one shared-memory bank
+  constexpr int LDA = MAXS + 1;
+  __shared__ double A[MAXS * LDA];
+  __shared__ double V[MAXS * LDA];
   __shared__ double cs[MAXS / 2], sn[MAXS / 2];
   __shared__ int pp[MAXS / 2], qq[MAXS / 2];
   __shared__ int perm[MAXS];
@@ -660,15 +664,15 @@ __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
     const int r = q / mm, c = q % mm;
     double v = 0.0;
     if (r < m && c < m) v = f->G[f->order[r] * MAXS + f->order[c]];
-    A[r * MAXS + c] = v;
-    V[r * MAXS + c] = (r == c) ? 1.0 : 0.0;
+    A[r * LDA + c] = v;
+    V[r * LDA + c] = (r == c) ? 1.0 : 0.0;
   }
   __shared__ double s_tr;
   __shared__ int s_rot;
   __syncthreads();
   if (threadIdx.x == 0) {
     double tr = 0.0;
-    for (int r = 0; r < m; ++r) tr += fabs(A[r * MAXS + r]);
+    for (int r = 0; r < m; ++r) tr += fabs(A[r * LDA + r]);
     s_tr = tr;
   }
   __syncthreads();
@@ -691,12 +695,12 @@ __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
         const int p = a < b ? a : b, q = a < b ? b : a;
         pp[t] = p;
         qq[t] = q;
-        const double apq = A[p * MAXS + q];
+        const double apq = A[p * LDA + q];
         double c = 1.0, s = 0.0;
-        const double app = A[p * MAXS + p], aqq = A[q * MAXS + q];
+        const double app = A[p * LDA + p], aqq = A[q * LDA + q];
         if (apq != 0.0 && fabs(apq) > 1e-15 * sqrt(fabs(app * aqq)) && fabs(apq) > MQ_EIG_ABS * s_tr) {
           atomicAdd(&s_rot, 1);
-          const double th = (A[q * MAXS + q] - A[p * MAXS + p]) / (2.0 * apq);
+          const double th = (A[q * LDA + q] - A[p * LDA + p]) / (2.0 * apq);
           const double tt = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
           c = 1.0 / sqrt(tt * tt + 1.0);
           s = tt * c;
@@ -710,9 +714,9 @@ __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
         const int t = it / mm, col = it % mm;
         const int p = pp[t], q = qq[t];
         const double c = cs[t], s = sn[t];
-        const double ap = A[p * MAXS + col], aq = A[q * MAXS + col];
-        A[p * MAXS + col] = c * ap - s * aq;
-        A[q * MAXS + col] = s * ap + c * aq;
+        const double ap = A[p * LDA + col], aq = A[q * LDA + col];
+        A[p * LDA + col] = c * ap - s * aq;
+        A[q * LDA + col] = s * ap + c * aq;
       }
       __syncthreads();
       // columns of A and V
@@ -720,22 +724,25 @@ __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
         const int t = it / mm, row = it % mm;
         const int p = pp[t], q = qq[t];
         const double c = cs[t], s = sn[t];
-        const double ap = A[row * MAXS + p], aq = A[row * MAXS + q];
-        A[row * MAXS + p] = c * ap - s * aq;
-        A[row * MAXS + q] = s * ap + c * aq;
-        const double vp = V[row * MAXS + p], vq = V[row * MAXS + q];
-        V[row * MAXS + p] = c * vp - s * vq;
-        V[row * MAXS + q] = s * vp + c * vq;
+        const double ap = A[row * LDA + p], aq = A[row * LDA + q];
+        A[row * LDA + p] = c * ap - s * aq;
+        A[row * LDA + q] = s * ap + c * aq;
+        const double vp = V[row * LDA + p], vq = V[row * LDA + q];
+        V[row * LDA + p] = c * vp - s * vq;
+        V[row * LDA + q] = s * vp + c * vq;
       }
       __syncthreads();
     }
     if (threadIdx.x == 0) s_done = s_rot == 0;
     __syncthreads();
+#ifdef MQ_EIG_DEBUG
+    if (threadIdx.x == 0 && s_done) printf("EIGSWEEPS m=%d sweeps=%d\n", m, sweep + 1);
+#endif
     if (s_done) break;
   }
   if (threadIdx.x == 0) {
     // sort descending (startvec.py:287-289), sigma = sqrt(clip(lambda, 0))
-    for (int i = 0; i < m; ++i) { perm[i] = i; lam[i] = A[i * MAXS + i]; }
+    for (int i = 0; i < m; ++i) { perm[i] = i; lam[i] = A[i * LDA + i]; }
     for (int i = 0; i < m; ++i)
       for (int j = i + 1; j < m; ++j)
         if (lam[perm[j]] > lam[perm[i]]) { int t = perm[i]; perm[i] = perm[j]; perm[j] = t; }
@@ -754,7 +761,7 @@ __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
     }
     f->podk = k;
     for (int l = 0; l < m; ++l)
-      for (int j = 0; j < k; ++j) f->W[l * MAXS + j] = V[l * MAXS + perm[j]];
+      for (int j = 0; j < k; ++j) f->W[l * MAXS + j] = V[l * LDA + perm[j]];
     f->x0_mode = 0;
   }
 }
