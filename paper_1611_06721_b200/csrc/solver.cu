@@ -652,7 +652,8 @@ __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
   __shared__ double cs[MAXS / 2], sn[MAXS / 2];
   __shared__ int pp[MAXS / 2], qq[MAXS / 2];
   __shared__ int perm[MAXS];
-  __shared__ double lam[MAXS];
+  __shared__ double lam[MAXS], sig[MAXS];
+  __shared__ int s_k;
   __shared__ int s_done;
   const int m = f->k;
   if (m == 0) {
@@ -741,7 +742,8 @@ __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
     if (s_done) break;
   }
   if (threadIdx.x == 0) {
-    // sort descending (startvec.py:287-289), sigma = sqrt(clip(lambda, 0))
+    // sort descending (startvec.py:287-289), sigma = sqrt(clip(lambda, 0));
+    // shared-memory work only: the family state is written after the barrier
     for (int i = 0; i < m; ++i) { perm[i] = i; lam[i] = A[i * LDA + i]; }
     for (int i = 0; i < m; ++i)
       for (int j = i + 1; j < m; ++j)
@@ -749,20 +751,23 @@ __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
     double total = 0.0;
     for (int i = 0; i < m; ++i) {
       const double l = lam[perm[i]];
-      f->pod_sigma[i] = sqrt(l > 0.0 ? l : 0.0);
-      total += f->pod_sigma[i];
+      sig[i] = sqrt(l > 0.0 ? l : 0.0);
+      total += sig[i];
     }
-    f->nrm = total;
     int k = 0;
-    if (f->pod_sigma[0] == 0.0) {
-      k = 0;
-    } else {
-      for (int i = 0; i < m; ++i) k += (f->pod_sigma[i] / f->pod_sigma[0] > eps_pod) ? 1 : 0;
-    }
+    if (sig[0] != 0.0)
+      for (int i = 0; i < m; ++i) k += (sig[i] / sig[0] > eps_pod) ? 1 : 0;
+    s_k = k;
+    f->nrm = total;
     f->podk = k;
-    for (int l = 0; l < m; ++l)
-      for (int j = 0; j < k; ++j) f->W[l * MAXS + j] = V[l * LDA + perm[j]];
     f->x0_mode = 0;
+  }
+  __syncthreads();
+  const int k = s_k;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) f->pod_sigma[i] = sig[i];
+  for (int q = threadIdx.x; q < m * k; q += blockDim.x) {
+    const int l = q / k, j = q % k;
+    f->W[l * MAXS + j] = V[l * LDA + perm[j]];
   }
 }
 
