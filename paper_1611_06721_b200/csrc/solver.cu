@@ -64,6 +64,9 @@ struct SolverHost {
   std::vector<void *> mem;
   int *d_iota = nullptr;  // identity order 0..MAXS-1
   cudaGraphExec_t graph_exec = nullptr;
+  // one-call graphs of the host-facing mq_euler_step / mq_recover_an
+  cudaGraphExec_t euler_graph = nullptr, recover_graph = nullptr;
+  int64_t euler_launches = 0, recover_launches = 0;
   bool graph_ok = true;
   int64_t launches_per_step = 0;
   bool recover_every_step = true;
@@ -86,16 +89,25 @@ static int s_alloc(mq_ctx *ctx, SolverHost *s, void **p, size_t bytes) {
 
 void solver_graph_reset(mq_ctx *ctx) {
   SolverHost *s = ctx->solver;
-  if (s && s->graph_exec) {
+  if (!s) return;
+  if (s->graph_exec) {
     cudaGraphExecDestroy(s->graph_exec);
     s->graph_exec = nullptr;
+  }
+  if (s->euler_graph) {
+    cudaGraphExecDestroy(s->euler_graph);
+    s->euler_graph = nullptr;
+  }
+  if (s->recover_graph) {
+    cudaGraphExecDestroy(s->recover_graph);
+    s->recover_graph = nullptr;
   }
 }
 
 void solver_free(mq_ctx *ctx) {
   SolverHost *s = ctx->solver;
   if (!s) return;
-  if (s->graph_exec) cudaGraphExecDestroy(s->graph_exec);
+  solver_graph_reset(ctx);
   for (void *p : s->mem) cudaFree(p);
   cudaFree(s->d_probe);
   cudaFree(s->d_probe_vals);
@@ -1673,7 +1685,36 @@ static int ensure_log(mq_ctx *ctx, int64_t n) {
   s->d_log = nullptr;
   MQ_CUDA(cudaMalloc(&s->d_log, sizeof(int32_t) * n));
   s->log_cap = n;
-  if (s->graph_exec) { cudaGraphExecDestroy(s->graph_exec); s->graph_exec = nullptr; }
+  solver_graph_reset(ctx);
+  return MQ_OK;
+}
+
+// Enqueue fn once into a graph and replay it afterwards (the kernels read
+// their per-call scalars from device memory, so the graph is call-invariant);
+// eager launches while PCG timing events are recorded.
+static int run_cached(mq_ctx *ctx, cudaGraphExec_t *g, int64_t *nlaunch, int (*fn)(mq_ctx *)) {
+  SolverHost *s = ctx->solver;
+  if (ctx->pcg_timing || !s->graph_ok) return fn(ctx);
+  if (!*g) {
+    cudaGraph_t gr = nullptr;
+    const int64_t l0 = ctx->launches;
+    cudaError_t e = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      int r2 = fn(ctx);
+      e = cudaStreamEndCapture(ctx->stream, &gr);
+      if (r2 == MQ_OK && e == cudaSuccess) e = cudaGraphInstantiate(g, gr, 0);
+      if (gr) cudaGraphDestroy(gr);
+    }
+    *nlaunch = ctx->launches - l0;
+    ctx->launches = l0;
+    if (e != cudaSuccess || !*g) {
+      cudaGetLastError();
+      *g = nullptr;
+      return fn(ctx);
+    }
+  }
+  MQ_CUDA(cudaGraphLaunch(*g, ctx->stream));
+  ctx->launches += *nlaunch;
   return MQ_OK;
 }
 
@@ -1688,7 +1729,7 @@ int mq_euler_step(mq_ctx *ctx, double dt, double wave_new, int64_t step_index, m
   if (rc) return rc;
   StepParams p{dt, wave_new, wave_new, (long long)step_index};
   MQ_CUDA(cudaMemcpyAsync(s->d_par, &p, sizeof(p), cudaMemcpyHostToDevice, ctx->stream));
-  rc = euler_enqueue(ctx);
+  rc = run_cached(ctx, &s->euler_graph, &s->euler_launches, euler_enqueue);
   if (rc) return rc;
   int64_t failed = -1;
   rc = check_run(ctx, &failed);
@@ -1707,7 +1748,7 @@ int mq_recover_an(mq_ctx *ctx, double wave_now, double *a_n_host, mq_solve_repor
   if (rc) return rc;
   StepParams p{0.0, wave_now, wave_now, -1};
   MQ_CUDA(cudaMemcpyAsync(s->d_par, &p, sizeof(p), cudaMemcpyHostToDevice, ctx->stream));
-  rc = recover_enqueue(ctx);
+  rc = run_cached(ctx, &s->recover_graph, &s->recover_launches, recover_enqueue);
   if (rc) return rc;
   rc = check_run(ctx, nullptr);
   read_report(ctx, 0, rep_src, rep_cpl);
