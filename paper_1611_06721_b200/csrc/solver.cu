@@ -748,9 +748,6 @@ __global__ void __launch_bounds__(256) k_pod_eig(FamDev *f, double eps_pod) {
     }
     if (threadIdx.x == 0) s_done = s_rot == 0;
     __syncthreads();
-#ifdef MQ_EIG_DEBUG
-    if (threadIdx.x == 0 && s_done) printf("EIGSWEEPS m=%d sweeps=%d\n", m, sweep + 1);
-#endif
     if (s_done) break;
   }
   if (threadIdx.x == 0) {
