@@ -272,23 +272,45 @@ class TransientResult:
 
 def step_times(t_end: float, dt: float, output_period: float, max_steps: int = 2_000_000):
     """The reference loop's (step_dt list, output-after-step flags)
-    (schur.py:546-572), evaluated on the host in the same float order."""
-    eps = 1e-12 * t_end
-    t = 0.0
-    next_output = output_period
-    dts, outs = [], []
-    while t < t_end - eps:
-        step_dt = min(dt, t_end - t)
-        t += step_dt
-        dts.append(step_dt)
-        if len(dts) > max_steps:
-            raise StepFailureError(f"step budget exceeded ({max_steps})")
-        out = t >= next_output - eps or t >= t_end - eps
-        outs.append(out)
-        if out:
-            while next_output <= t + eps:
-                next_output += output_period
+    (schur.py:546-572) for a fixed dt."""
+    dts, outs, _ = _Schedule(t_end, output_period, max_steps).take(dt)
     return dts, outs
+
+
+class _Schedule:
+    """The reference loop's step sizes and output flags (schur.py:546-572),
+    produced on the host in the same float order, a phase at a time (the
+    step size may shrink between phases when dt="auto" re-estimates)."""
+
+    def __init__(self, t_end: float, output_period: float, max_steps: int):
+        self.t_end, self.period, self.max_steps = t_end, output_period, max_steps
+        self.eps = 1e-12 * t_end
+        self.t = 0.0
+        self.next_output = output_period
+        self.count = 0
+
+    @property
+    def done(self) -> bool:
+        return not (self.t < self.t_end - self.eps)
+
+    def take(self, dt: float, nmax=None):
+        """(step sizes, output flags, node times incl. the start) of up to
+        nmax further steps of size dt."""
+        dts, outs, tt = [], [], [self.t]
+        while not self.done and (nmax is None or len(dts) < nmax):
+            step_dt = min(dt, self.t_end - self.t)
+            self.t += step_dt
+            self.count += 1
+            if self.count > self.max_steps:
+                raise StepFailureError(f"step budget exceeded ({self.max_steps})")
+            out = self.t >= self.next_output - self.eps or self.t >= self.t_end - self.eps
+            if out:
+                while self.next_output <= self.t + self.eps:
+                    self.next_output += self.period
+            dts.append(step_dt)
+            outs.append(out)
+            tt.append(self.t)
+        return dts, outs, tt
 
 
 def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig | None = None,
@@ -296,14 +318,16 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
                  probe=None, a0=None, max_cols: int = 20, n_pod: int = 10,
                  eps_pod: float = 1e-4, max_steps: int = 2_000_000, device: int = 0,
                  use_graph: bool = True, record_states: bool = False,
-                 op: SchurOperator | None = None, safety: float = 0.9,
+                 op: SchurOperator | None = None, reestimate_every: int = 500, safety: float = 0.9,
                  power_iters: int = 200, power_tol: float = 1e-4,
                  seed: int = 42) -> TransientResult:
     """Integrate with explicit Euler on the device (schur.py:474-607).
 
-    ``dt="auto"`` runs the device spectral estimate once before the loop
-    (the reference also re-estimates every ``reestimate_every`` steps, which
-    only matters with strong saturation; not done here).
+    ``dt="auto"`` runs the device spectral estimate before the loop and again
+    every ``reestimate_every`` steps at the current state, shrinking the step
+    when the bound tightened (a fixed dt is never adjusted), as the reference.
+    The steps between outputs run as one device-resident sequence (one CUDA
+    graph per step).
     """
     if t_end <= 0:
         raise ValueError("t_end must be positive")
@@ -314,18 +338,16 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
         op = SchurOperator(problem, pcg=pcg, strategy=strategy, preconditioner=preconditioner,
                            max_cols=max_cols, n_pod=n_pod, eps_pod=eps_pod, device=device)
     lambda_max = None
-    if isinstance(dt, str):
+    auto = isinstance(dt, str)
+    if auto:
         if dt != "auto":
             raise ValueError(f"dt must be a number or 'auto', got {dt!r}")
-        # one spectral estimate up front (schur.py:503-510); a fixed dt is
-        # used for the whole run on the device
-        est = estimate_cfl(op, power_iters=power_iters, power_tol=power_tol, safety=safety,
-                           seed=seed)
+        est = estimate_cfl(op, power_iters=power_iters, power_tol=power_tol, safety=safety, seed=seed)
         dt, lambda_max = est.dt_max, est.lambda_max
     dt = float(dt)
     if dt <= 0:
         raise ValueError("dt must be positive")
-    n_c, n_n = op.grid.n_c, op.grid.n_n
+    n_c = op.grid.n_c
     # probe: a host callable (a_c, a_n, t) -> float as in the reference, or
     # "device" / an array of conductor-cell ids for the device probe, which
     # logs B_probe inside the step graph
@@ -340,7 +362,6 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
             op.set_probe(probe)
     a_c = np.zeros(n_c) if a0 is None else f64(a0, n_c, "initial state").copy()
     wave = op.problem.waveform
-    dts, outs = step_times(t_end, dt, output_period, max_steps)
     rows = {k: [] for k in ("t", "b", "src", "prev", "cur", "basis", "k", "info")}
 
     def emit(t_row, a_c_row, a_n_row, iters_src, iters_prev, iters_cur):
@@ -361,24 +382,85 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
     a_n, (r1, r2) = recover_an(op, a_c, 0.0)
     emit(0.0, a_c, a_n, [r1.iterations], [], [r2.iterations])
     op._set_state(a_c, 0.0)
+    sched = _Schedule(t_end, output_period, max_steps)
+    phase_len = reestimate_every if (auto and reestimate_every > 0) else None
+    iters_parts, hist_parts = [], []
+    all_out_all = True
+    refreshes = 0
+    while not sched.done:
+        if phase_len is not None and sched.count > 0 and sched.count % phase_len == 0:
+            # schur.py:548-557: re-estimate at the current state, shrink only
+            est = estimate_cfl(op, a_c_ref=a_c, power_iters=power_iters, power_tol=power_tol,
+                               safety=safety, seed=seed)
+            refreshes += 1
+            lambda_max = est.lambda_max
+            dt = min(dt, est.dt_max)
+            op._set_state(a_c, sched.t)
+        base = sched.count
+        dts, outs, tt = sched.take(dt, phase_len)
+        a_c, a_n_ph, step_iters, hist, all_out = _run_phase(
+            op, dts, outs, tt, wave, emit, rows, base, host_probe, device_probe, use_graph, record_states)
+        if a_n_ph is not None:
+            a_n = a_n_ph
+        all_out_all = all_out_all and all_out
+        iters_parts.append(step_iters)
+        if hist is not None:
+            hist_parts.append(hist)
+    n = sched.count
+    wall = time.perf_counter() - wall_start
+    d = op.diagnostics()
+    aggregates = {
+        "integrator": "explicit",
+        "strategy": op.strategy_kind,
+        "steps": n,
+        "dt": dt,
+        "lambda_max": lambda_max,
+        "cfl_refreshes": refreshes,
+        "solves": {f.value: op.solve_count(f) for f in FAMILIES},
+        "iterations": {f.value: int(sum(op.solve_iterations[f])) for f in FAMILIES},
+        "mean_iterations": {f.value: (float(np.mean(op.solve_iterations[f]))
+                                      if op.solve_iterations[f] else 0.0) for f in FAMILIES},
+        "pcg_applies": int(d.pcg_applies),
+        "maintenance_applies": int(d.maintenance_applies),
+        "operator_applies": int(d.pcg_applies + d.maintenance_applies),
+        "wall_seconds": wall,
+        "min_pod_info": float(d.min_pod_info),
+        "max_basis_cols": int(max(d.basis_cols)),
+        "aborted": False,
+    }
+    step_iters = (np.concatenate(iters_parts) if iters_parts else np.zeros((0, 4), dtype=np.int32))
+    return TransientResult(times=np.asarray(rows["t"]), probe_b=np.asarray(rows["b"]),
+                           iters_src=np.asarray(rows["src"]), iters_cpl_prev=np.asarray(rows["prev"]),
+                           iters_cpl_cur=np.asarray(rows["cur"]),
+                           basis_cols=np.asarray(rows["basis"], dtype=np.int64),
+                           pod_k=np.asarray(rows["k"], dtype=np.int64),
+                           pod_info=np.asarray(rows["info"]), final_a_c=a_c, final_a_n=a_n,
+                           aggregates=aggregates,
+                           step_iterations=step_iters if all_out_all and not host_probe else None,
+                           a_c_history=np.concatenate(hist_parts) if record_states and hist_parts else
+                           (np.empty((0, n_c)) if record_states else None))
+
+
+def _run_phase(op, dts, outs, tt, wave, emit, rows, base, host_probe, device_probe, use_graph,
+               record_states):
+    """Run the steps dts (node times tt, output flags outs) on the device from
+    the state held there; returns (a_c, a_n or None, per-step iterations,
+    a_c history or None, all steps had outputs)."""
     n = len(dts)
-    # exact host float sequence of t (t += step_dt)
-    tt = [0.0]
-    for d in dts:
-        tt.append(tt[-1] + d)
-    t_nodes = np.array(tt)
-    wave_tab = np.array([float(wave(x)) for x in t_nodes])
+    n_c = op.grid.n_c
+    wave_tab = np.array([float(wave(x)) for x in tt])
     dt_tab = np.array(dts, dtype=np.float64)
     all_out = all(outs)
     step_iters = np.zeros((n, 4), dtype=np.int32)
     hist = np.empty((n, n_c)) if record_states else None
     failed = ctypes.c_int64(-1)
+    a_n = None
     if all_out and not host_probe:
         rc = op.lib.mq_run_explicit(op.grid.ctx, n, dptr(dt_tab), dptr(wave_tab), 1,
                                     1 if use_graph else 0, _lib.i32ptr(step_iters),
                                     dptr(hist) if hist is not None else None, ctypes.byref(failed))
         if rc == _lib.MQ_NONFINITE:
-            raise StepFailureError(f"non-finite conducting state at step {failed.value}")
+            raise StepFailureError(f"non-finite conducting state at step {base + failed.value}")
         check(rc)
         a_c = op._get_state()
         blog = np.zeros(n)
@@ -413,11 +495,13 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
             it = np.zeros((seg, 4), dtype=np.int32)
             rc = op.lib.mq_run_explicit(op.grid.ctx, seg, dptr(dt_tab[m:m + seg]),
                                         dptr(wave_tab[m:m + seg + 1].copy()), 0,
-                                        1 if use_graph else 0, _lib.i32ptr(it), None,
+                                        1 if use_graph else 0, _lib.i32ptr(it),
+                                        dptr(hist[m:m + seg]) if hist is not None else None,
                                         ctypes.byref(failed))
             if rc == _lib.MQ_NONFINITE:
-                raise StepFailureError(f"non-finite conducting state at step {m + failed.value}")
+                raise StepFailureError(f"non-finite conducting state at step {base + m + failed.value}")
             check(rc)
+            step_iters[m:m + seg, :2] = it[:, :2]
             win_src.extend(int(v) for v in it[:, 0])
             win_prev.extend(int(v) for v in it[:, 1])
             op.solve_iterations[RhsFamily.SOURCE_CURRENT].extend(int(v) for v in it[:, 0])
@@ -426,39 +510,11 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
             if outs[m - 1]:
                 a_c = op._get_state()
                 a_n, (r1, r2) = recover_an(op, a_c, tt[m])
+                step_iters[m - 1, 2:] = (r1.iterations, r2.iterations)
                 emit(tt[m], a_c, a_n, win_src + [r1.iterations], win_prev, [r2.iterations])
                 win_src, win_prev = [], []
         a_c = op._get_state()
-    wall = time.perf_counter() - wall_start
-    d = op.diagnostics()
-    aggregates = {
-        "integrator": "explicit",
-        "strategy": op.strategy_kind,
-        "steps": n,
-        "dt": dt,
-        "lambda_max": lambda_max,
-        "cfl_refreshes": 0,
-        "solves": {f.value: op.solve_count(f) for f in FAMILIES},
-        "iterations": {f.value: int(sum(op.solve_iterations[f])) for f in FAMILIES},
-        "mean_iterations": {f.value: (float(np.mean(op.solve_iterations[f]))
-                                      if op.solve_iterations[f] else 0.0) for f in FAMILIES},
-        "pcg_applies": int(d.pcg_applies),
-        "maintenance_applies": int(d.maintenance_applies),
-        "operator_applies": int(d.pcg_applies + d.maintenance_applies),
-        "wall_seconds": wall,
-        "min_pod_info": float(d.min_pod_info),
-        "max_basis_cols": int(max(d.basis_cols)),
-        "aborted": False,
-    }
-    return TransientResult(times=np.asarray(rows["t"]), probe_b=np.asarray(rows["b"]),
-                           iters_src=np.asarray(rows["src"]), iters_cpl_prev=np.asarray(rows["prev"]),
-                           iters_cpl_cur=np.asarray(rows["cur"]),
-                           basis_cols=np.asarray(rows["basis"], dtype=np.int64),
-                           pod_k=np.asarray(rows["k"], dtype=np.int64),
-                           pod_info=np.asarray(rows["info"]), final_a_c=a_c, final_a_n=a_n,
-                           aggregates=aggregates,
-                           step_iterations=step_iters if all_out and probe is None else None,
-                           a_c_history=hist)
+    return a_c, a_n, step_iters, hist, all_out
 
 
 def _final_an(op: SchurOperator) -> np.ndarray:

@@ -428,6 +428,25 @@ def test_schur_loop_semantics(gpu_ok):
         explicit_euler_step((np.full(m.n_c, 1e300), 0.0), 1e9, op, step_index=7)
 
 
+def test_auto_dt_reestimation(gpu_ok):
+    """dt="auto" re-estimates every reestimate_every steps (schur.py:548-557):
+    with linear iron the bound does not move, so the run equals the one with
+    a single estimate bit for bit and counts its refreshes."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, run_explicit
+    spec, m = oracle_model(0)
+    kw = dict(strategy="cspe", pcg=PcgConfig(rel_tol=1e-8), max_cols=5, power_iters=60)
+    once = run_explicit(C.make_problem(0), t_end=8.5 * spec.dt, dt="auto", reestimate_every=0,
+                        output_period=spec.dt * (1 - 1e-3), **kw)
+    again = run_explicit(C.make_problem(0), t_end=8.5 * spec.dt, dt="auto", reestimate_every=3,
+                         output_period=spec.dt * (1 - 1e-3), **kw)
+    assert once.aggregates["steps"] == again.aggregates["steps"] == 9
+    assert once.aggregates["cfl_refreshes"] == 0 and again.aggregates["cfl_refreshes"] == 2
+    assert again.aggregates["dt"] == once.aggregates["dt"]
+    assert np.array_equal(again.final_a_c, once.final_a_c)
+    assert np.array_equal(again.times, once.times)
+
+
 def test_single_step_api_matches_oracle(gpu_ok):
     """explicit_euler_step / recover_an / SchurOperator.solve_kn twins."""
     from paper_1611_06721_b200 import configs as C
