@@ -25,7 +25,7 @@ from .krylov import PcgConfig, Preconditioner, SolveReport
 from .startvec import RhsFamily, family_index, solver_cfg
 
 __all__ = ["StepFailureError", "SchurOperator", "explicit_euler_step", "recover_an",
-           "run_explicit", "TransientResult", "FAMILIES", "step_times", "CflEstimate",
+           "run_explicit", "TransientResult", "FAMILIES", "step_times", "CflEstimate", "trace_bytes",
            "estimate_cfl"]
 
 FAMILIES = (RhsFamily.SOURCE_CURRENT, RhsFamily.COUPLING_FROM_CURRENT_STATE,
@@ -515,6 +515,23 @@ def _run_phase(op, dts, outs, tt, wave, emit, rows, base, host_probe, device_pro
                 win_src, win_prev = [], []
         a_c = op._get_state()
     return a_c, a_n, step_iters, hist, all_out
+
+
+TRACE_HEADER = "t,B_probe,iters_src,iters_cpl_prev,iters_cpl_cur,basis_cols,pod_k,pod_info"
+
+
+def trace_bytes(result: TransientResult) -> bytes:
+    """The reference's trace CSV of a transient result (bench.py:42, 341-357):
+    one row per output time, floats by repr, counts as integers."""
+    if result.n_rows == 0:
+        raise ValueError("refusing to write an empty trace")
+    out = [TRACE_HEADER]
+    for i in range(result.n_rows):
+        out.append(",".join([repr(float(result.times[i])), repr(float(result.probe_b[i])),
+                             repr(float(result.iters_src[i])), repr(float(result.iters_cpl_prev[i])),
+                             repr(float(result.iters_cpl_cur[i])), str(int(result.basis_cols[i])),
+                             str(int(result.pod_k[i])), repr(float(result.pod_info[i]))]))
+    return ("\n".join(out) + "\n").encode("ascii")
 
 
 def _final_an(op: SchurOperator) -> np.ndarray:

@@ -447,6 +447,23 @@ def test_auto_dt_reestimation(gpu_ok):
     assert np.array_equal(again.times, once.times)
 
 
+def test_trace_csv_deterministic(gpu_ok):
+    """The reference's trace CSV (bench.py:341-357) from two identical device
+    runs is byte-identical (test_bench.py: test_benchmark_is_deterministic)."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, run_explicit
+    from paper_1611_06721_b200.schur import TRACE_HEADER, trace_bytes
+    spec, m = oracle_model(0)
+    runs = [run_explicit(C.make_problem(0), t_end=6 * spec.dt, dt=spec.dt, strategy=strat,
+                         pcg=PcgConfig(rel_tol=1e-8), max_cols=5, n_pod=6, probe="device",
+                         output_period=2 * spec.dt * (1 - 1e-3))
+            for strat in ("pod", "pod")]
+    a, b = (trace_bytes(r) for r in runs)
+    assert a == b
+    lines = a.decode().splitlines()
+    assert lines[0] == TRACE_HEADER and len(lines) == 1 + runs[0].n_rows == 5
+
+
 def test_single_step_api_matches_oracle(gpu_ok):
     """explicit_euler_step / recover_an / SchurOperator.solve_kn twins."""
     from paper_1611_06721_b200 import configs as C
