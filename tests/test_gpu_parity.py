@@ -207,6 +207,22 @@ def test_csr_path_reference_cases(gpu_ok):
         pcg_solve(lambda v: v, np.ones(2))
 
 
+def test_csr_path_on_assembled_kn(c0):
+    """An externally supplied CSR K_n (non-FIT models) on
+    the general CSR device PCG: the configs[0] matrix as scipy CSR against
+    the matrix-free stencil path and the oracle."""
+    import scipy.sparse as sp
+
+    from paper_1611_06721_b200 import PcgConfig, Preconditioner, pcg_solve
+    spec, m, prob, g = c0
+    cfg = PcgConfig(rel_tol=1e-8, preconditioner=Preconditioner.JACOBI)
+    x_csr, rep_csr = pcg_solve(sp.csr_matrix(m.kn), m.pattern, config=cfg)
+    x_st, rep_st = pcg_solve(g.kn_operator(), m.pattern, config=cfg)
+    ref = O.pcg(m.kn_apply, m.pattern, rel_tol=1e-8, inv_diag=O.jacobi_inverse(m.kn.diagonal()))
+    assert rep_csr.converged and abs(rep_csr.iterations - ref.iterations) <= 1
+    assert rel(x_csr, ref.x) <= 1e-8 and rel(x_csr, x_st) <= 1e-8
+
+
 def test_cspe_strategy_parity(c0, golden):
     from paper_1611_06721_b200 import DeviceStrategy, RhsFamily
     spec, m, prob, g = c0
