@@ -73,6 +73,15 @@ struct SolverHost {
   int kb = 32;  // compile-time basis bound used for the tall-skinny kernels
   int per_step = 4;
   int64_t n_planned = 0, n_enqueued = 0;
+  // overlap: the source family's cache update runs on a side stream on the
+  // SMs the shared-memory-resident PCG kernel leaves idle, while the coupling
+  // solve runs (own reduction scratch and CGS vectors)
+  bool overlap = false;
+  int side_grid = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join[2] = {nullptr, nullptr};
+  double *d_red2 = nullptr, *w1b = nullptr, *w2b = nullptr;
+  unsigned int *d_cnt2 = nullptr;
   // B probe (model.py:415-425): conductor-cell list indices, per-cell scratch,
   // per-step log of the current run
   int32_t *d_probe = nullptr, *d_probe_plan = nullptr;
@@ -108,6 +117,11 @@ void solver_free(mq_ctx *ctx) {
   SolverHost *s = ctx->solver;
   if (!s) return;
   solver_graph_reset(ctx);
+  if (s->side) cudaStreamDestroy(s->side);
+  for (int q = 0; q < 2; ++q) {
+    if (s->ev_fork[q]) cudaEventDestroy(s->ev_fork[q]);
+    if (s->ev_join[q]) cudaEventDestroy(s->ev_join[q]);
+  }
   for (void *p : s->mem) cudaFree(p);
   cudaFree(s->d_probe);
   cudaFree(s->d_probe_vals);
@@ -1212,17 +1226,31 @@ static int start_vector(mq_ctx *ctx, int fam, const double *rhs, double *x0) {
 }
 
 // ---- observe ------------------------------------------------------------
-static int observe(mq_ctx *ctx, int fam, const double *y) {
+// where a family's cache update runs: stream, reduction scratch, CGS vectors
+struct ObsRes {
+  cudaStream_t st;
+  double *red;
+  unsigned int *cnt;
+  double *w1, *w2;
+  int grid;
+};
+
+static ObsRes main_res(mq_ctx *ctx) {
+  SolverHost *s = ctx->solver;
+  return ObsRes{ctx->stream, s->d_red, s->d_cnt, s->w1, s->w2, s->red_grid};
+}
+
+static int observe(mq_ctx *ctx, int fam, const double *y, const ObsRes &o) {
   SolverHost *s = ctx->solver;
   FamDev *f = s->d_fam + fam;
   const Lay &L = ctx->topo.L;
-  cudaStream_t st = ctx->stream;
-  const int G = s->red_grid;
+  cudaStream_t st = o.st;
+  const int G = o.grid;
   switch (s->cfg.strategy) {
     case MQ_STRAT_ZERO:
       break;
     case MQ_STRAT_PREVIOUS:
-      k_copy<<<stream_grid(ctx), kBlock, 0, st>>>(L, ctx->d_mask, y, s->last[fam]);
+      k_copy<<<G, kBlock, 0, st>>>(L, ctx->d_mask, y, s->last[fam]);
       LAUNCH_CHECK();
       k_prev_mark<<<1, 32, 0, st>>>(f);
       LAUNCH_CHECK();
@@ -1234,23 +1262,23 @@ static int observe(mq_ctx *ctx, int fam, const double *y) {
       post.drop_tol = s->cfg.drop_tol;
       // ||v|| and U^T v in one pass, then the zero / non-finite gate
       post.kind = POST_GATE;
-      KB_LAUNCH(s->kb, k_mdot, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, y, 1, f->d, s->d_red,
-                s->d_cnt, post);
+      KB_LAUNCH(s->kb, k_mdot, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, y, 1, f->d, o.red,
+                o.cnt, post);
       LAUNCH_CHECK();
       // CGS pass 1: w1 = v - U c1, c2 = U^T w1
       post.kind = POST_GATE_C2;
-      KB_LAUNCH(s->kb, k_axpy_dots, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, f->coef, y, s->w1, 1, f->d,
-                                        s->d_red, s->d_cnt, &f->accept, post);
+      KB_LAUNCH(s->kb, k_axpy_dots, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, f->coef, y, o.w1, 1, f->d,
+                                        o.red, o.cnt, &f->accept, post);
       LAUNCH_CHECK();
       // CGS pass 2: w2 = w1 - U c2, ||w2||^2, then drop test / eviction / slot
       post.kind = POST_DECIDE;
-      KB_LAUNCH(s->kb, k_axpy_dots, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, f->coef, s->w1, s->w2, 0,
-                                        f->d, s->d_red, s->d_cnt, &f->accept, post);
+      KB_LAUNCH(s->kb, k_axpy_dots, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, f->coef, o.w1, o.w2, 0,
+                                        f->d, o.red, o.cnt, &f->accept, post);
       LAUNCH_CHECK();
       // u, K u, cross products, diagonal, then the bordered Galerkin commit
       post.kind = POST_COMMIT;
       KB_LAUNCH(s->kb, k_cspe_product, G, kBlock, st, L, ctx->d_mask, ctx->kn_diag, ctx->kn_off, f, s->d_U[fam], s->d_KU[fam],
-                                           s->w2, s->d_red, s->d_cnt, post);
+                                           o.w2, o.red, o.cnt, post);
       LAUNCH_CHECK();
       break;
     }
@@ -1259,7 +1287,7 @@ static int observe(mq_ctx *ctx, int fam, const double *y) {
       post.kind = POST_POD_PUSH;
       post.f = f;
       post.n_pod = s->cfg.n_pod;
-      KB_LAUNCH(s->kb, k_pod_push, G, kBlock, st, L, ctx->d_mask, f, s->d_X[fam], s->cfg.n_pod, y, s->d_red, s->d_cnt,
+      KB_LAUNCH(s->kb, k_pod_push, G, kBlock, st, L, ctx->d_mask, f, s->d_X[fam], s->cfg.n_pod, y, o.red, o.cnt,
                 post);
       LAUNCH_CHECK();
       break;
@@ -1269,7 +1297,7 @@ static int observe(mq_ctx *ctx, int fam, const double *y) {
 }
 
 // ---- one solve_kn (schur.py:239-264), device only ------------------------
-static int solve_enqueue(mq_ctx *ctx, int fam, const double *rhs, double *y) {
+static int solve_enqueue(mq_ctx *ctx, int fam, const double *rhs, double *y, bool observe_now = true) {
   SolverHost *s = ctx->solver;
   FamDev *f = s->d_fam + fam;
   int rc = start_vector(ctx, fam, rhs, y);
@@ -1307,7 +1335,25 @@ static int solve_enqueue(mq_ctx *ctx, int fam, const double *rhs, double *y) {
   ctx->launches += 1;
   k_post_solve<<<1, 32, 0, ctx->stream>>>(ctx->d_out, s->d_run, s->d_fam, fam, s->d_log, s->log_cap, s->d_par);
   LAUNCH_CHECK();
-  return observe(ctx, fam, y);
+  return observe_now ? observe(ctx, fam, y, main_res(ctx)) : MQ_OK;
+}
+
+// the source family's cache update on the side stream (fork), joined back
+// into the main stream by join_side()
+static int fork_observe(mq_ctx *ctx, int slot, int fam, const double *y) {
+  SolverHost *s = ctx->solver;
+  MQ_CUDA(cudaEventRecord(s->ev_fork[slot], ctx->stream));
+  MQ_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork[slot], 0));
+  int rc = observe(ctx, fam, y, ObsRes{s->side, s->d_red2, s->d_cnt2, s->w1b, s->w2b, s->side_grid});
+  if (rc) return rc;
+  MQ_CUDA(cudaEventRecord(s->ev_join[slot], s->side));
+  return MQ_OK;
+}
+
+static int join_side(mq_ctx *ctx, int slot) {
+  SolverHost *s = ctx->solver;
+  MQ_CUDA(cudaStreamWaitEvent(ctx->stream, s->ev_join[slot], 0));
+  return MQ_OK;
 }
 
 static int euler_enqueue(mq_ctx *ctx) {
@@ -1319,13 +1365,21 @@ static int euler_enqueue(mq_ctx *ctx) {
   // SOURCE at t + dt
   k_src_rhs<<<grid_for(ctx, s->n_pat), 256, 0, st>>>(s->n_pat, s->d_pat_idx, s->d_pat_val, s->d_par, 0, s->rhs_src);
   LAUNCH_CHECK();
-  int rc = solve_enqueue(ctx, MQ_FAM_SOURCE, s->rhs_src, s->y_src);
+  int rc = solve_enqueue(ctx, MQ_FAM_SOURCE, s->rhs_src, s->y_src, !s->overlap);
   if (rc) return rc;
+  if (s->overlap) {
+    rc = fork_observe(ctx, 0, MQ_FAM_SOURCE, s->y_src);
+    if (rc) return rc;
+  }
   // COUPLING_FROM_PREVIOUS_STATE with w = K_cn^T a_c
   k_kcnt<<<grid_for(ctx, a.n_rows_t), 256, 0, st>>>(a, ctx->d_ac, s->rhs_cpl);
   LAUNCH_CHECK();
   rc = solve_enqueue(ctx, MQ_FAM_COUPLING_PREVIOUS, s->rhs_cpl, s->y_cpl);
   if (rc) return rc;
+  if (s->overlap) {
+    rc = join_side(ctx, 0);
+    if (rc) return rc;
+  }
   // Brauer + Euler update
   k_cell_nu<<<grid_for(ctx, a.n_cells), 256, 0, st>>>(a, ctx->d_ac, ctx->d_cell_nu);
   LAUNCH_CHECK();
@@ -1343,11 +1397,17 @@ static int recover_enqueue(mq_ctx *ctx) {
   cudaStream_t st = ctx->stream;
   k_src_rhs<<<grid_for(ctx, s->n_pat), 256, 0, st>>>(s->n_pat, s->d_pat_idx, s->d_pat_val, s->d_par, 1, s->rhs_src);
   LAUNCH_CHECK();
-  int rc = solve_enqueue(ctx, MQ_FAM_SOURCE, s->rhs_src, s->y_src);
+  int rc = solve_enqueue(ctx, MQ_FAM_SOURCE, s->rhs_src, s->y_src, !s->overlap);
   if (rc) return rc;
+  if (s->overlap) {
+    rc = fork_observe(ctx, 1, MQ_FAM_SOURCE, s->y_src);
+    if (rc) return rc;
+  }
   k_kcnt<<<grid_for(ctx, a.n_rows_t), 256, 0, st>>>(a, ctx->d_ac, s->rhs_cpl);
   LAUNCH_CHECK();
-  return solve_enqueue(ctx, MQ_FAM_COUPLING_CURRENT, s->rhs_cpl, s->y_cpl);
+  rc = solve_enqueue(ctx, MQ_FAM_COUPLING_CURRENT, s->rhs_cpl, s->y_cpl);
+  if (rc) return rc;
+  return s->overlap ? join_side(ctx, 1) : MQ_OK;
 }
 
 static int check_run(mq_ctx *ctx, int64_t *failed_step) {
@@ -1475,6 +1535,28 @@ int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern)
   s->red_grid = std::max(1, std::min<int>(ctx->sms * MQ_RED_MULT, (int)((L.words + kWarps - 1) / kWarps)));
   rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_red, sizeof(double) * RQ * (size_t)s->red_grid * (MAXS + 2));
   rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_cnt, sizeof(unsigned int) * (MAXS + 4));
+  // side stream for the overlapped source-family update: only with the
+  // resident PCG kernel, which leaves SMs idle (MQ_OVERLAP=0 disables)
+  {
+    const char *ov = getenv("MQ_OVERLAP");
+    const int idle = ctx->sms - ctx->res_grid;
+    if (!rc && ctx->pcg_variant == 2 && idle >= 4 && !(ov && ov[0] == '0')) {
+      s->side_grid = idle;
+      vec(&s->w1b);
+      vec(&s->w2b);
+      rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_red2, sizeof(double) * RQ * (size_t)s->red_grid * (MAXS + 2));
+      rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_cnt2, sizeof(unsigned int) * (MAXS + 4));
+      if (!rc) {
+        cudaError_t e = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
+        for (int q = 0; q < 2 && e == cudaSuccess; ++q) {
+          e = cudaEventCreateWithFlags(&s->ev_fork[q], cudaEventDisableTiming);
+          if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_join[q], cudaEventDisableTiming);
+        }
+        if (e != cudaSuccess) rc = cuda_fail(e, "overlap stream");
+        else s->overlap = true;
+      }
+    }
+  }
   // sparse source pattern on its support
   if (!rc && pattern) {
     std::vector<int32_t> idx;
@@ -1551,7 +1633,7 @@ int mq_strategy_start(mq_ctx *ctx, int32_t family, const double *rhs, double *x0
 
 int mq_strategy_observe(mq_ctx *ctx, int32_t family, const double *y) {
   if (!ctx->solver) { set_error("solver not initialised"); return MQ_INVALID; }
-  int rc = observe(ctx, family, y);
+  int rc = observe(ctx, family, y, main_res(ctx));
   if (rc) return rc;
   MQ_CUDA(cudaStreamSynchronize(ctx->stream));
   return MQ_OK;

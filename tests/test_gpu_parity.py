@@ -529,6 +529,30 @@ def test_config1_first_steps(gpu_ok, golden):
 
 
 @pytest.mark.slow
+def test_overlapped_source_update(gpu_ok, monkeypatch):
+    """64^3 (resident PCG kernel): the source family's cache update on the
+    side stream (its reductions run on the idle SMs' smaller grid, so the
+    summation tree differs) is deterministic — graph replay and eager
+    launches agree bit for bit — and stays within the field bar of the
+    serial order."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, run_explicit
+    spec = C.config_spec(1)
+    runs = {}
+    for ov in ("0", "1"):
+        monkeypatch.setenv("MQ_OVERLAP", ov)
+        for graph in (True, False):
+            runs[ov, graph] = run_explicit(C.make_problem(1), t_end=4 * spec.dt, dt=spec.dt, strategy="cspe",
+                                           pcg=PcgConfig(rel_tol=1e-8), max_cols=5,
+                                           output_period=spec.dt * (1 - 1e-3), use_graph=graph)
+    for ov in ("0", "1"):
+        assert np.array_equal(runs[ov, True].final_a_c, runs[ov, False].final_a_c), ov
+        assert np.array_equal(runs[ov, True].step_iterations, runs[ov, False].step_iterations), ov
+    assert rel(runs["1", True].final_a_c, runs["0", True].final_a_c) <= REL_FIELD
+    assert np.max(np.abs(runs["1", True].step_iterations - runs["0", True].step_iterations)) <= 1
+
+
+@pytest.mark.slow
 def test_config1_pod_first_steps(gpu_ok):
     """64^3 Brauer with POD-20 start vectors (configs[1]'s second run): the
     first steps against the oracle, per-step fields within the bar."""
