@@ -48,6 +48,7 @@ struct SolverHost {
   double *last[3] = {nullptr, nullptr, nullptr};
   double *w1 = nullptr, *w2 = nullptr;
   double *rhs_src = nullptr, *rhs_cpl = nullptr, *y_src = nullptr, *y_cpl = nullptr;
+  double *y_cur = nullptr;  // recovery's coupling solution (y_cpl may still be read by the side stream)
   // source pattern (sparse: padded index + value)
   int32_t *d_pat_idx = nullptr;
   double *d_pat_val = nullptr;
@@ -79,7 +80,8 @@ struct SolverHost {
   bool overlap = false;
   int side_grid = 0;
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork[3] = {}, ev_join[3] = {};
+  bool pend[3] = {false, false, false};  // forks not yet joined (host-side, per enqueue sequence)
   double *d_red2 = nullptr, *w1b = nullptr, *w2b = nullptr;
   unsigned int *d_cnt2 = nullptr;
   // B probe (model.py:415-425): conductor-cell list indices, per-cell scratch,
@@ -118,7 +120,7 @@ void solver_free(mq_ctx *ctx) {
   if (!s) return;
   solver_graph_reset(ctx);
   if (s->side) cudaStreamDestroy(s->side);
-  for (int q = 0; q < 2; ++q) {
+  for (int q = 0; q < 3; ++q) {
     if (s->ev_fork[q]) cudaEventDestroy(s->ev_fork[q]);
     if (s->ev_join[q]) cudaEventDestroy(s->ev_join[q]);
   }
@@ -1347,16 +1349,35 @@ static int fork_observe(mq_ctx *ctx, int slot, int fam, const double *y) {
   int rc = observe(ctx, fam, y, ObsRes{s->side, s->d_red2, s->d_cnt2, s->w1b, s->w2b, s->side_grid});
   if (rc) return rc;
   MQ_CUDA(cudaEventRecord(s->ev_join[slot], s->side));
+  s->pend[slot] = true;
   return MQ_OK;
 }
 
+// main stream waits for the side stream up to fork `slot` (side work is in
+// issue order, so this also covers earlier forks)
 static int join_side(mq_ctx *ctx, int slot) {
   SolverHost *s = ctx->solver;
+  if (!s->pend[slot]) return MQ_OK;
   MQ_CUDA(cudaStreamWaitEvent(ctx->stream, s->ev_join[slot], 0));
+  s->pend[slot] = false;
   return MQ_OK;
 }
 
-static int euler_enqueue(mq_ctx *ctx) {
+static int join_all(mq_ctx *ctx) {
+  SolverHost *s = ctx->solver;
+  for (int q = 0; q < 3; ++q) {
+    int rc = join_side(ctx, q);
+    if (rc) return rc;
+  }
+  return MQ_OK;
+}
+
+static int euler_enqueue(mq_ctx *ctx, bool join_tail);
+static int euler_enqueue_joined(mq_ctx *ctx) { return euler_enqueue(ctx, true); }
+
+// join_tail: leave no side work pending (standalone calls); the stepper
+// passes false and lets the recovery absorb the coupling family's update
+static int euler_enqueue(mq_ctx *ctx, bool join_tail) {
   SolverHost *s = ctx->solver;
   const Topology &t = ctx->topo;
   CondArgs a = cond_args(ctx);
@@ -1374,10 +1395,14 @@ static int euler_enqueue(mq_ctx *ctx) {
   // COUPLING_FROM_PREVIOUS_STATE with w = K_cn^T a_c
   k_kcnt<<<grid_for(ctx, a.n_rows_t), 256, 0, st>>>(a, ctx->d_ac, s->rhs_cpl);
   LAUNCH_CHECK();
-  rc = solve_enqueue(ctx, MQ_FAM_COUPLING_PREVIOUS, s->rhs_cpl, s->y_cpl);
+  // the coupling family's update overlaps the Euler update and the recovery
+  // when one follows in the same sequence; alone it would only trail the
+  // call on the small side grid
+  const bool fork_cpl = s->overlap && !join_tail;
+  rc = solve_enqueue(ctx, MQ_FAM_COUPLING_PREVIOUS, s->rhs_cpl, s->y_cpl, !fork_cpl);
   if (rc) return rc;
-  if (s->overlap) {
-    rc = join_side(ctx, 0);
+  if (fork_cpl) {
+    rc = fork_observe(ctx, 2, MQ_FAM_COUPLING_PREVIOUS, s->y_cpl);
     if (rc) return rc;
   }
   // Brauer + Euler update
@@ -1388,16 +1413,19 @@ static int euler_enqueue(mq_ctx *ctx) {
   LAUNCH_CHECK();
   k_copy_n<<<grid_for(ctx, n_c), 256, 0, st>>>(n_c, ctx->d_ac_next, ctx->d_ac, s->d_run);
   LAUNCH_CHECK();
-  return MQ_OK;
+  return join_tail ? join_all(ctx) : MQ_OK;
 }
 
 static int recover_enqueue(mq_ctx *ctx) {
   SolverHost *s = ctx->solver;
   CondArgs a = cond_args(ctx);
   cudaStream_t st = ctx->stream;
+  // the source family's cache must be final before its projection
+  int rc = join_side(ctx, 0);
+  if (rc) return rc;
   k_src_rhs<<<grid_for(ctx, s->n_pat), 256, 0, st>>>(s->n_pat, s->d_pat_idx, s->d_pat_val, s->d_par, 1, s->rhs_src);
   LAUNCH_CHECK();
-  int rc = solve_enqueue(ctx, MQ_FAM_SOURCE, s->rhs_src, s->y_src, !s->overlap);
+  rc = solve_enqueue(ctx, MQ_FAM_SOURCE, s->rhs_src, s->y_src, !s->overlap);
   if (rc) return rc;
   if (s->overlap) {
     rc = fork_observe(ctx, 1, MQ_FAM_SOURCE, s->y_src);
@@ -1405,9 +1433,9 @@ static int recover_enqueue(mq_ctx *ctx) {
   }
   k_kcnt<<<grid_for(ctx, a.n_rows_t), 256, 0, st>>>(a, ctx->d_ac, s->rhs_cpl);
   LAUNCH_CHECK();
-  rc = solve_enqueue(ctx, MQ_FAM_COUPLING_CURRENT, s->rhs_cpl, s->y_cpl);
+  rc = solve_enqueue(ctx, MQ_FAM_COUPLING_CURRENT, s->rhs_cpl, s->y_cur);
   if (rc) return rc;
-  return s->overlap ? join_side(ctx, 1) : MQ_OK;
+  return join_all(ctx);
 }
 
 static int check_run(mq_ctx *ctx, int64_t *failed_step) {
@@ -1529,6 +1557,7 @@ int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern)
   vec(&s->rhs_cpl);
   vec(&s->y_src);
   vec(&s->y_cpl);
+  vec(&s->y_cur);
 #ifndef MQ_RED_MULT
 #define MQ_RED_MULT 2
 #endif
@@ -1548,7 +1577,7 @@ int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern)
       rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_cnt2, sizeof(unsigned int) * (MAXS + 4));
       if (!rc) {
         cudaError_t e = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
-        for (int q = 0; q < 2 && e == cudaSuccess; ++q) {
+        for (int q = 0; q < 3 && e == cudaSuccess; ++q) {
           e = cudaEventCreateWithFlags(&s->ev_fork[q], cudaEventDisableTiming);
           if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_join[q], cudaEventDisableTiming);
         }
@@ -1808,7 +1837,7 @@ int mq_euler_step(mq_ctx *ctx, double dt, double wave_new, int64_t step_index, m
   if (rc) return rc;
   StepParams p{dt, wave_new, wave_new, (long long)step_index};
   MQ_CUDA(cudaMemcpyAsync(s->d_par, &p, sizeof(p), cudaMemcpyHostToDevice, ctx->stream));
-  rc = run_cached(ctx, &s->euler_graph, &s->euler_launches, euler_enqueue);
+  rc = run_cached(ctx, &s->euler_graph, &s->euler_launches, euler_enqueue_joined);
   if (rc) return rc;
   int64_t failed = -1;
   rc = check_run(ctx, &failed);
@@ -1833,7 +1862,7 @@ int mq_recover_an(mq_ctx *ctx, double wave_now, double *a_n_host, mq_solve_repor
   read_report(ctx, 0, rep_src, rep_cpl);
   if (rc) return rc;
   if (a_n_host) {
-    k_sub<<<stream_grid(ctx), kBlock, 0, ctx->stream>>>(ctx->topo.L, ctx->d_mask, s->y_src, s->y_cpl, ctx->d_tmp1);
+    k_sub<<<stream_grid(ctx), kBlock, 0, ctx->stream>>>(ctx->topo.L, ctx->d_mask, s->y_src, s->y_cur, ctx->d_tmp1);
     LAUNCH_CHECK();
     return mq_vec_download(ctx, ctx->d_tmp1, a_n_host);
   }
@@ -1843,7 +1872,7 @@ int mq_recover_an(mq_ctx *ctx, double wave_now, double *a_n_host, mq_solve_repor
 int mq_last_an(mq_ctx *ctx, double *a_n_host) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
-  k_sub<<<stream_grid(ctx), kBlock, 0, ctx->stream>>>(ctx->topo.L, ctx->d_mask, s->y_src, s->y_cpl, ctx->d_tmp1);
+  k_sub<<<stream_grid(ctx), kBlock, 0, ctx->stream>>>(ctx->topo.L, ctx->d_mask, s->y_src, s->y_cur, ctx->d_tmp1);
   LAUNCH_CHECK();
   return mq_vec_download(ctx, ctx->d_tmp1, a_n_host);
 }
@@ -1855,7 +1884,7 @@ static int enqueue_step(mq_ctx *ctx, double *hist) {
   k_load_params<<<1, 32, 0, ctx->stream>>>(s->d_par, s->d_dt_tab, s->d_wave_tab, s->d_run);
   MQ_CUDA(cudaGetLastError());
   ctx->launches += 1;
-  int rc = euler_enqueue(ctx);
+  int rc = euler_enqueue(ctx, !s->recover_every_step);
   if (rc) return rc;
   if (s->recover_every_step) {
     rc = recover_enqueue(ctx);
