@@ -11,7 +11,7 @@ from .device import AIR, COIL, CONDUCTOR, NU_VACUUM, DeviceGrid, KnOperator, Pro
 from .krylov import (IndefiniteOperatorError, JacobiPreconditioner, PcgConfig, Preconditioner,
                      SolveReport, pcg_solve)
 from .schur import (FAMILIES, CflEstimate, SchurOperator, StepFailureError, TransientResult,
-                    estimate_cfl, explicit_euler_step, recover_an, run_explicit)
+                    estimate_cfl, explicit_euler_step, recover_an, run_explicit, trace_bytes)
 from .startvec import DeviceStrategy, RhsFamily
 
 __version__ = "0.1.0"
@@ -21,6 +21,6 @@ __all__ = [
     "IndefiniteOperatorError", "JacobiPreconditioner", "PcgConfig", "Preconditioner",
     "SolveReport", "pcg_solve", "FAMILIES", "SchurOperator", "StepFailureError",
     "TransientResult", "explicit_euler_step", "recover_an", "run_explicit", "DeviceStrategy",
-    "CflEstimate", "estimate_cfl",
+    "CflEstimate", "estimate_cfl", "trace_bytes",
     "RhsFamily",
 ]
