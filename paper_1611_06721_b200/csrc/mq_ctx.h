@@ -27,7 +27,8 @@ struct FamDev {
   int x0_mode;           // PCG start mode chosen by the last start vector
   int podk;              // POD: retained modes of the last projection
   int has_last;          // previous strategy
-  int pad0;
+  int pending;           // CSPE: a deferred insert of the last recovery's solution waits
+  int skip;              // CSPE: the current (gated) insert is a no-op
   double nv2, nw2;       // CSPE: squared norms of the raw / orthogonalised vector
   double nrm;            // CSPE: ||w|| used to normalise
   double pod_info;       // POD: kept information of the last projection

@@ -80,8 +80,11 @@ struct SolverHost {
   bool overlap = false;
   int side_grid = 0;
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork[3] = {}, ev_join[3] = {};
-  bool pend[3] = {false, false, false};  // forks not yet joined (host-side, per enqueue sequence)
+  cudaEvent_t ev_fork[4] = {}, ev_join[4] = {};
+  bool pend[4] = {false, false, false, false};  // forks not yet joined (host-side, per enqueue sequence)
+  // CSPE: the stepper defers the recovery's coupling-family insert into the
+  // next step's side stream; maybe_pending = one may wait on the device
+  bool defer_cur = false, maybe_pending = false;
   double *d_red2 = nullptr, *w1b = nullptr, *w2b = nullptr;
   unsigned int *d_cnt2 = nullptr;
   // B probe (model.py:415-425): conductor-cell list indices, per-cell scratch,
@@ -120,7 +123,7 @@ void solver_free(mq_ctx *ctx) {
   if (!s) return;
   solver_graph_reset(ctx);
   if (s->side) cudaStreamDestroy(s->side);
-  for (int q = 0; q < 3; ++q) {
+  for (int q = 0; q < 4; ++q) {
     if (s->ev_fork[q]) cudaEventDestroy(s->ev_fork[q]);
     if (s->ev_join[q]) cudaEventDestroy(s->ev_join[q]);
   }
@@ -220,7 +223,8 @@ template <int KB>
 __global__ void __launch_bounds__(kBlock) k_mdot(int64_t npair, double *const *tab, const int *order,
                                                  const int *kptr, const double *__restrict__ v, int selfdot,
                                                  double *out, double *partials, unsigned int *counter,
-                                                 Post post) {
+                                                 Post post, const int *skip) {
+  if (skip && *skip) return;  // gated deferred insert with nothing pending
   __shared__ const double2 *ptr[KB];
   const int k = *kptr;
   if (threadIdx.x < k) ptr[threadIdx.x] = reinterpret_cast<const double2 *>(tab[order[threadIdx.x]]);
@@ -1199,7 +1203,7 @@ static int start_vector(mq_ctx *ctx, int fam, const double *rhs, double *x0) {
       post.kind = POST_PROJECT;
       post.f = f;
       KB_LAUNCH(s->kb, k_mdot, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, rhs, 0, f->d, s->d_red,
-                s->d_cnt, post);
+                s->d_cnt, post, nullptr);
       LAUNCH_CHECK();
       KB_LAUNCH(s->kb, k_comb, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, f->coef, x0);
       LAUNCH_CHECK();
@@ -1228,6 +1232,22 @@ static int start_vector(mq_ctx *ctx, int fam, const double *rhs, double *x0) {
 }
 
 // ---- observe ------------------------------------------------------------
+// deferred CSPE insert (the recovery's coupling family, see enqueue_step)
+__global__ void k_obs_gate(FamDev *f) {
+  if (threadIdx.x != 0) return;
+  if (f->pending) {
+    f->pending = 0;
+    f->skip = 0;
+  } else {
+    f->skip = 1;
+    f->accept = 0;  // the chain's later kernels test accept
+  }
+}
+
+__global__ void k_set_pending(FamDev *f) {
+  if (threadIdx.x == 0) f->pending = 1;
+}
+
 // where a family's cache update runs: stream, reduction scratch, CGS vectors
 struct ObsRes {
   cudaStream_t st;
@@ -1242,7 +1262,9 @@ static ObsRes main_res(mq_ctx *ctx) {
   return ObsRes{ctx->stream, s->d_red, s->d_cnt, s->w1, s->w2, s->red_grid};
 }
 
-static int observe(mq_ctx *ctx, int fam, const double *y, const ObsRes &o) {
+// gated: the insert runs only if the family has a deferred one pending
+// (k_obs_gate); CSPE only
+static int observe(mq_ctx *ctx, int fam, const double *y, const ObsRes &o, bool gated = false) {
   SolverHost *s = ctx->solver;
   FamDev *f = s->d_fam + fam;
   const Lay &L = ctx->topo.L;
@@ -1258,6 +1280,10 @@ static int observe(mq_ctx *ctx, int fam, const double *y, const ObsRes &o) {
       LAUNCH_CHECK();
       break;
     case MQ_STRAT_CSPE: {
+      if (gated) {
+        k_obs_gate<<<1, 32, 0, st>>>(f);
+        LAUNCH_CHECK();
+      }
       Post post;
       post.f = f;
       post.max_cols = s->cfg.max_cols;
@@ -1265,7 +1291,7 @@ static int observe(mq_ctx *ctx, int fam, const double *y, const ObsRes &o) {
       // ||v|| and U^T v in one pass, then the zero / non-finite gate
       post.kind = POST_GATE;
       KB_LAUNCH(s->kb, k_mdot, G, kBlock, st, L.total / 2, s->d_U[fam], f->order, &f->k, y, 1, f->d, o.red,
-                o.cnt, post);
+                o.cnt, post, gated ? &f->skip : nullptr);
       LAUNCH_CHECK();
       // CGS pass 1: w1 = v - U c1, c2 = U^T w1
       post.kind = POST_GATE_C2;
@@ -1342,11 +1368,11 @@ static int solve_enqueue(mq_ctx *ctx, int fam, const double *rhs, double *y, boo
 
 // the source family's cache update on the side stream (fork), joined back
 // into the main stream by join_side()
-static int fork_observe(mq_ctx *ctx, int slot, int fam, const double *y) {
+static int fork_observe(mq_ctx *ctx, int slot, int fam, const double *y, bool gated = false) {
   SolverHost *s = ctx->solver;
   MQ_CUDA(cudaEventRecord(s->ev_fork[slot], ctx->stream));
   MQ_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork[slot], 0));
-  int rc = observe(ctx, fam, y, ObsRes{s->side, s->d_red2, s->d_cnt2, s->w1b, s->w2b, s->side_grid});
+  int rc = observe(ctx, fam, y, ObsRes{s->side, s->d_red2, s->d_cnt2, s->w1b, s->w2b, s->side_grid}, gated);
   if (rc) return rc;
   MQ_CUDA(cudaEventRecord(s->ev_join[slot], s->side));
   s->pend[slot] = true;
@@ -1365,7 +1391,7 @@ static int join_side(mq_ctx *ctx, int slot) {
 
 static int join_all(mq_ctx *ctx) {
   SolverHost *s = ctx->solver;
-  for (int q = 0; q < 3; ++q) {
+  for (int q = 0; q < 4; ++q) {
     int rc = join_side(ctx, q);
     if (rc) return rc;
   }
@@ -1416,7 +1442,9 @@ static int euler_enqueue(mq_ctx *ctx, bool join_tail) {
   return join_tail ? join_all(ctx) : MQ_OK;
 }
 
-static int recover_enqueue(mq_ctx *ctx) {
+// defer: leave the coupling family's insert pending for the next step's
+// side stream (stepper only)
+static int recover_enqueue(mq_ctx *ctx, bool defer) {
   SolverHost *s = ctx->solver;
   CondArgs a = cond_args(ctx);
   cudaStream_t st = ctx->stream;
@@ -1433,9 +1461,28 @@ static int recover_enqueue(mq_ctx *ctx) {
   }
   k_kcnt<<<grid_for(ctx, a.n_rows_t), 256, 0, st>>>(a, ctx->d_ac, s->rhs_cpl);
   LAUNCH_CHECK();
-  rc = solve_enqueue(ctx, MQ_FAM_COUPLING_CURRENT, s->rhs_cpl, s->y_cur);
+  // a deferred insert of the previous recovery must finish before this
+  // family projects and before y_cur is overwritten
+  rc = join_side(ctx, 3);
   if (rc) return rc;
+  rc = solve_enqueue(ctx, MQ_FAM_COUPLING_CURRENT, s->rhs_cpl, s->y_cur, !defer);
+  if (rc) return rc;
+  if (defer) {
+    k_set_pending<<<1, 32, 0, st>>>(s->d_fam + MQ_FAM_COUPLING_CURRENT);
+    LAUNCH_CHECK();
+  }
   return join_all(ctx);
+}
+
+static int recover_enqueue_now(mq_ctx *ctx) { return recover_enqueue(ctx, false); }
+
+// a deferred insert left by the stepper, run now (before any host-visible
+// use of the families); a gated no-op if none is pending on the device
+static int flush_deferred(mq_ctx *ctx) {
+  SolverHost *s = ctx->solver;
+  if (!s || !s->maybe_pending) return MQ_OK;
+  s->maybe_pending = false;
+  return observe(ctx, MQ_FAM_COUPLING_CURRENT, s->y_cur, main_res(ctx), true);
 }
 
 static int check_run(mq_ctx *ctx, int64_t *failed_step) {
@@ -1577,12 +1624,15 @@ int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern)
       rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_cnt2, sizeof(unsigned int) * (MAXS + 4));
       if (!rc) {
         cudaError_t e = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
-        for (int q = 0; q < 3 && e == cudaSuccess; ++q) {
+        for (int q = 0; q < 4 && e == cudaSuccess; ++q) {
           e = cudaEventCreateWithFlags(&s->ev_fork[q], cudaEventDisableTiming);
           if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_join[q], cudaEventDisableTiming);
         }
         if (e != cudaSuccess) rc = cuda_fail(e, "overlap stream");
-        else s->overlap = true;
+        else {
+          s->overlap = true;
+          s->defer_cur = cfg->strategy == MQ_STRAT_CSPE;
+        }
       }
     }
   }
@@ -1622,12 +1672,17 @@ int mq_solver_reset(mq_ctx *ctx) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
   MQ_CUDA(cudaMemsetAsync(s->d_fam, 0, sizeof(FamDev) * 3, ctx->stream));
+  s->maybe_pending = false;  // the memset cleared any deferred insert
   return init_run(ctx);
 }
 
 int mq_solve_kn(mq_ctx *ctx, int32_t family, const double *rhs, double *y, mq_solve_report *rep) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  {
+    const int frc = flush_deferred(ctx);
+    if (frc) return frc;
+  }
   if (family < 0 || family > 2) { set_error("unknown family"); return MQ_INVALID; }
   int rc = reset_run(ctx);
   if (rc) return rc;
@@ -1649,6 +1704,10 @@ int mq_solve_kn(mq_ctx *ctx, int32_t family, const double *rhs, double *y, mq_so
 int mq_strategy_start(mq_ctx *ctx, int32_t family, const double *rhs, double *x0) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  {
+    const int frc = flush_deferred(ctx);
+    if (frc) return frc;
+  }
   int rc = start_vector(ctx, family, rhs, x0);
   if (rc) return rc;
   // materialise zero start vectors
@@ -1662,6 +1721,10 @@ int mq_strategy_start(mq_ctx *ctx, int32_t family, const double *rhs, double *x0
 
 int mq_strategy_observe(mq_ctx *ctx, int32_t family, const double *y) {
   if (!ctx->solver) { set_error("solver not initialised"); return MQ_INVALID; }
+  {
+    const int frc = flush_deferred(ctx);
+    if (frc) return frc;
+  }
   int rc = observe(ctx, family, y, main_res(ctx));
   if (rc) return rc;
   MQ_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1671,6 +1734,10 @@ int mq_strategy_observe(mq_ctx *ctx, int32_t family, const double *y) {
 int mq_diagnostics(mq_ctx *ctx, mq_diag *out) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  {
+    const int frc = flush_deferred(ctx);
+    if (frc) return frc;
+  }
   FamDev f[3];
   RunDev r;
   MQ_CUDA(cudaMemcpyAsync(f, s->d_fam, sizeof(FamDev) * 3, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1830,6 +1897,14 @@ int mq_euler_step(mq_ctx *ctx, double dt, double wave_new, int64_t step_index, m
                   mq_solve_report *rep_cpl) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  {
+    const int frc = flush_deferred(ctx);
+    if (frc) return frc;
+  }
+  {
+    const int frc = flush_deferred(ctx);
+    if (frc) return frc;
+  }
   if (dt < 0) { set_error("dt must be nonnegative"); return MQ_INVALID; }
   int rc = ensure_log(ctx, 4);
   if (rc) return rc;
@@ -1850,13 +1925,17 @@ int mq_recover_an(mq_ctx *ctx, double wave_now, double *a_n_host, mq_solve_repor
                   mq_solve_report *rep_cpl) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  {
+    const int frc = flush_deferred(ctx);
+    if (frc) return frc;
+  }
   int rc = ensure_log(ctx, 4);
   if (rc) return rc;
   rc = reset_run(ctx);
   if (rc) return rc;
   StepParams p{0.0, wave_now, wave_now, -1};
   MQ_CUDA(cudaMemcpyAsync(s->d_par, &p, sizeof(p), cudaMemcpyHostToDevice, ctx->stream));
-  rc = run_cached(ctx, &s->recover_graph, &s->recover_launches, recover_enqueue);
+  rc = run_cached(ctx, &s->recover_graph, &s->recover_launches, recover_enqueue_now);
   if (rc) return rc;
   rc = check_run(ctx, nullptr);
   read_report(ctx, 0, rep_src, rep_cpl);
@@ -1884,11 +1963,19 @@ static int enqueue_step(mq_ctx *ctx, double *hist) {
   k_load_params<<<1, 32, 0, ctx->stream>>>(s->d_par, s->d_dt_tab, s->d_wave_tab, s->d_run);
   MQ_CUDA(cudaGetLastError());
   ctx->launches += 1;
+  const bool defer = s->defer_cur && s->recover_every_step;
+  if (defer) {
+    // the previous recovery's coupling-family insert, under this step's
+    // source and coupling solves (a no-op if none is pending)
+    int r0 = fork_observe(ctx, 3, MQ_FAM_COUPLING_CURRENT, s->y_cur, true);
+    if (r0) return r0;
+  }
   int rc = euler_enqueue(ctx, !s->recover_every_step);
   if (rc) return rc;
   if (s->recover_every_step) {
-    rc = recover_enqueue(ctx);
+    rc = recover_enqueue(ctx, defer);
     if (rc) return rc;
+    if (defer) s->maybe_pending = true;
   }
   if (s->n_probe > 0) {
     k_probe<<<1, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, s->d_probe_plan, ctx->d_ac,
@@ -2074,6 +2161,10 @@ int mq_run_steps(mq_ctx *ctx, int64_t n, int32_t use_graph, double *a_c_hist_dev
 int mq_run_finish(mq_ctx *ctx, int32_t *iters_out, int64_t *failed_step) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  {
+    const int frc = flush_deferred(ctx);
+    if (frc) return frc;
+  }
   int rc = check_run(ctx, failed_step);
   const int64_t n = s->n_enqueued;
   if (iters_out && n > 0)

@@ -542,7 +542,7 @@ def test_overlapped_source_update(gpu_ok, monkeypatch):
     for ov in ("0", "1"):
         monkeypatch.setenv("MQ_OVERLAP", ov)
         for graph in (True, False):
-            runs[ov, graph] = run_explicit(C.make_problem(1), t_end=4 * spec.dt, dt=spec.dt, strategy="cspe",
+            runs[ov, graph] = run_explicit(C.make_problem(1), t_end=12 * spec.dt, dt=spec.dt, strategy="cspe",
                                            pcg=PcgConfig(rel_tol=1e-8), max_cols=5,
                                            output_period=spec.dt * (1 - 1e-3), use_graph=graph)
     for ov in ("0", "1"):
@@ -550,6 +550,11 @@ def test_overlapped_source_update(gpu_ok, monkeypatch):
         assert np.array_equal(runs[ov, True].step_iterations, runs[ov, False].step_iterations), ov
     assert rel(runs["1", True].final_a_c, runs["0", True].final_a_c) <= REL_FIELD
     assert np.max(np.abs(runs["1", True].step_iterations - runs["0", True].step_iterations)) <= 1
+    # every insert happened (the deferred one of the last recovery included)
+    ag1, ag0 = runs["1", True].aggregates, runs["0", True].aggregates
+    assert ag1["maintenance_applies"] == ag0["maintenance_applies"]
+    assert abs(ag1["pcg_applies"] - ag0["pcg_applies"]) <= 4 * ag0["steps"]   # +-1 per solve
+    assert np.array_equal(runs["1", True].basis_cols, runs["0", True].basis_cols)
 
 
 @pytest.mark.slow
