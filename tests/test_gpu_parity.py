@@ -558,6 +558,35 @@ def test_overlapped_source_update(gpu_ok, monkeypatch):
 
 
 @pytest.mark.slow
+def test_config2_first_steps_vs_oracle(gpu_ok):
+    """configs[2] (128^3, two iron blocks, POD-30, TMA brick PCG): the first
+    two steps against the CPU oracle's run (tests/golden/oracle_cfg2.npz,
+    made by tests/golden/make_oracle_cfg2.py): per-step field norms and 512
+    sampled entries within the bar, iteration counts within +-1."""
+    from pathlib import Path
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, run_explicit
+    ref = np.load(Path(__file__).parent / "golden" / "oracle_cfg2.npz")
+    spec = C.config_spec(2)
+    steps = len(ref["a_c_norm"]) - 1
+    res = run_explicit(C.make_problem(2), t_end=steps * spec.dt, dt=spec.dt, strategy="pod",
+                       pcg=PcgConfig(rel_tol=spec.rel_tol), n_pod=spec.n_pod, eps_pod=1e-4,
+                       output_period=spec.dt * (1 - 1e-3), record_states=True)
+    for i in range(steps):
+        a = res.a_c_history[i]
+        nref = ref["a_c_norm"][i + 1]
+        assert abs(np.linalg.norm(a) - nref) <= REL_FIELD * nref
+        assert np.max(np.abs(a[ref["idx_c"]] - ref["a_c_sample"][i + 1])) <= REL_FIELD * nref
+    an = res.final_a_n
+    assert abs(np.linalg.norm(an) - ref["a_n_norm"][-1]) <= AN_FLOOR * ref["a_n_norm"][-1]
+    it = res.step_iterations
+    src = ref["iters_src"][1:].reshape(steps, 2)
+    assert np.max(np.abs(it[:, 0] - src[:, 0])) <= 1 and np.max(np.abs(it[:, 2] - src[:, 1])) <= 1
+    assert np.max(np.abs(it[:, 1] - ref["iters_prev"])) <= 1
+    assert np.max(np.abs(it[:, 3] - ref["iters_cur"][1:])) <= 1
+
+
+@pytest.mark.slow
 def test_config1_pod_first_steps(gpu_ok):
     """64^3 Brauer with POD-20 start vectors (configs[1]'s second run): the
     first steps against the oracle, per-step fields within the bar."""
