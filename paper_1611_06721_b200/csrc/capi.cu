@@ -198,7 +198,7 @@ int mq_ctx_create(const mq_grid_desc *desc, int32_t device, mq_ctx **out) {
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_partials, sizeof(double) * 8 * (size_t)std::max(ctx->pcg_grid, 1024));
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_bar, sizeof(GridBar));
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_out, sizeof(PcgOut));
-  if (!rc && getenv("MQ_PCG_TRACE")) rc = ctx_alloc(ctx, (void **)&ctx->d_trace, sizeof(unsigned long long) * 1024);
+  if (!rc && getenv("MQ_PCG_TRACE")) rc = ctx_alloc(ctx, (void **)&ctx->d_trace, sizeof(unsigned long long) * 2048);
   if (!rc) {
     e = cudaMallocHost((void **)&ctx->h_out, sizeof(PcgOut));
     if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocHost");

@@ -431,6 +431,9 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       if (threadIdx.x == 0) a.partials[3 * G + blockIdx.x] = v1[0];
       ++applies;
       stamp(4 * (it - 1) + 1);
+#ifdef MQ_TRACE_SPREAD
+      if (a.trace && threadIdx.x == 0 && it == 10 && blockIdx.x < 1024) a.trace[1024 + blockIdx.x] = globaltimer_ns();
+#endif
       if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
       stamp(4 * (it - 1) + 2);
       double s1[1];
