@@ -199,6 +199,14 @@ int mq_euler_step(mq_ctx *ctx, double dt, double wave_new, int64_t step_index,
 /* recover_an at the current state (schur.py:408-419); a_n to host if non-NULL */
 int mq_recover_an(mq_ctx *ctx, double wave_now, double *a_n_host,
                   mq_solve_report *rep_src, mq_solve_report *rep_cpl);
+/* One-call host forms of explicit_euler_step((a_c, t), dt, op) and
+ * recover_an(op, a_c, t) (schur.py:379-419): upload a_c (compact host order),
+ * run, return a_c_next / a_n; a single stream synchronisation per call. */
+int mq_euler_step_host(mq_ctx *ctx, const double *a_c, double t, double dt, double wave_new,
+                       int64_t step_index, double *a_c_next,
+                       mq_solve_report *rep_src, mq_solve_report *rep_cpl);
+int mq_recover_an_host(mq_ctx *ctx, const double *a_c, double t, double wave_now, double *a_n_host,
+                       mq_solve_report *rep_src, mq_solve_report *rep_cpl);
 
 /* a_n = y_src - y_cpl of the most recent recovery / step solves (host n_n) */
 int mq_last_an(mq_ctx *ctx, double *a_n_host);

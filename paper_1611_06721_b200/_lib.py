@@ -122,6 +122,10 @@ SIGNATURES = {
                             ctypes.POINTER(SolveReportC)]),
     "mq_recover_an": (I32, [VP, D, c_double_p, ctypes.POINTER(SolveReportC),
                             ctypes.POINTER(SolveReportC)]),
+    "mq_euler_step_host": (I32, [VP, c_double_p, D, D, D, I64, c_double_p, ctypes.POINTER(SolveReportC),
+                                 ctypes.POINTER(SolveReportC)]),
+    "mq_recover_an_host": (I32, [VP, c_double_p, D, D, c_double_p, ctypes.POINTER(SolveReportC),
+                                 ctypes.POINTER(SolveReportC)]),
     "mq_last_an": (I32, [VP, c_double_p]),
     "mq_run_explicit": (I32, [VP, I64, c_double_p, c_double_p, I32, I32, c_int32_p,
                               c_double_p, c_int64_p]),

@@ -80,11 +80,16 @@ struct SolverHost {
   bool overlap = false;
   int side_grid = 0;
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork[4] = {}, ev_join[4] = {};
-  bool pend[4] = {false, false, false, false};  // forks not yet joined (host-side, per enqueue sequence)
-  // CSPE: the stepper defers the recovery's coupling-family insert into the
-  // next step's side stream; maybe_pending = one may wait on the device
-  bool defer_cur = false, maybe_pending = false;
+  // fork slots: 0/1 source update in the step / recovery, 2 coupling-previous
+  // update, 3 deferred coupling-current insert, 4 deferred coupling-previous
+  // insert (host-facing calls)
+  static constexpr int kSlots = 5;
+  cudaEvent_t ev_fork[kSlots] = {}, ev_join[kSlots] = {};
+  bool pend[kSlots] = {};  // forks not yet joined (host-side, per enqueue sequence)
+  // CSPE: a coupling family's insert is deferred into the next call's (or
+  // step's) side stream; maybe_pending[fam] = one may wait on the device
+  bool defer_cur = false;
+  bool maybe_pending[3] = {false, false, false};
   double *d_red2 = nullptr, *w1b = nullptr, *w2b = nullptr;
   unsigned int *d_cnt2 = nullptr;
   // B probe (model.py:415-425): conductor-cell list indices, per-cell scratch,
@@ -92,6 +97,15 @@ struct SolverHost {
   int32_t *d_probe = nullptr, *d_probe_plan = nullptr;
   double *d_probe_vals = nullptr, *d_probe_log = nullptr, *d_probe_leaf = nullptr;
   int64_t n_probe = 0, probe_cap = 0;
+  double *d_probe_out = nullptr;
+  // page-locked landing block of the host-facing calls: run status, the two
+  // iteration counts and the probe value come back in one copy batch and one
+  // stream synchronisation per call
+  struct HostStage {
+    RunDev run;
+    int32_t it[2];
+    double probe;
+  } *h_st = nullptr;
 };
 
 static int s_alloc(mq_ctx *ctx, SolverHost *s, void **p, size_t bytes) {
@@ -123,7 +137,7 @@ void solver_free(mq_ctx *ctx) {
   if (!s) return;
   solver_graph_reset(ctx);
   if (s->side) cudaStreamDestroy(s->side);
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < SolverHost::kSlots; ++q) {
     if (s->ev_fork[q]) cudaEventDestroy(s->ev_fork[q]);
     if (s->ev_join[q]) cudaEventDestroy(s->ev_join[q]);
   }
@@ -133,6 +147,7 @@ void solver_free(mq_ctx *ctx) {
   cudaFree(s->d_probe_log);
   cudaFree(s->d_probe_plan);
   cudaFree(s->d_probe_leaf);
+  if (s->h_st) cudaFreeHost(s->h_st);
   delete s;
   ctx->solver = nullptr;
 }
@@ -1391,19 +1406,20 @@ static int join_side(mq_ctx *ctx, int slot) {
 
 static int join_all(mq_ctx *ctx) {
   SolverHost *s = ctx->solver;
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < SolverHost::kSlots; ++q) {
     int rc = join_side(ctx, q);
     if (rc) return rc;
   }
   return MQ_OK;
 }
 
-static int euler_enqueue(mq_ctx *ctx, bool join_tail);
-static int euler_enqueue_joined(mq_ctx *ctx) { return euler_enqueue(ctx, true); }
+static int euler_enqueue(mq_ctx *ctx, bool join_tail, bool defer_cpl = false);
 
 // join_tail: leave no side work pending (standalone calls); the stepper
 // passes false and lets the recovery absorb the coupling family's update
-static int euler_enqueue(mq_ctx *ctx, bool join_tail) {
+// defer_cpl: leave the coupling family's insert pending on the device for
+// the next call's side stream (host-facing calls, CSPE)
+static int euler_enqueue(mq_ctx *ctx, bool join_tail, bool defer_cpl) {
   SolverHost *s = ctx->solver;
   const Topology &t = ctx->topo;
   CondArgs a = cond_args(ctx);
@@ -1424,12 +1440,16 @@ static int euler_enqueue(mq_ctx *ctx, bool join_tail) {
   // the coupling family's update overlaps the Euler update and the recovery
   // when one follows in the same sequence; alone it would only trail the
   // call on the small side grid
-  const bool fork_cpl = s->overlap && !join_tail;
-  rc = solve_enqueue(ctx, MQ_FAM_COUPLING_PREVIOUS, s->rhs_cpl, s->y_cpl, !fork_cpl);
+  const bool fork_cpl = s->overlap && !join_tail && !defer_cpl;
+  rc = solve_enqueue(ctx, MQ_FAM_COUPLING_PREVIOUS, s->rhs_cpl, s->y_cpl, !fork_cpl && !defer_cpl);
   if (rc) return rc;
   if (fork_cpl) {
     rc = fork_observe(ctx, 2, MQ_FAM_COUPLING_PREVIOUS, s->y_cpl);
     if (rc) return rc;
+  }
+  if (defer_cpl) {
+    k_set_pending<<<1, 32, 0, st>>>(s->d_fam + MQ_FAM_COUPLING_PREVIOUS);
+    LAUNCH_CHECK();
   }
   // Brauer + Euler update
   k_cell_nu<<<grid_for(ctx, a.n_cells), 256, 0, st>>>(a, ctx->d_ac, ctx->d_cell_nu);
@@ -1474,22 +1494,58 @@ static int recover_enqueue(mq_ctx *ctx, bool defer) {
   return join_all(ctx);
 }
 
-static int recover_enqueue_now(mq_ctx *ctx) { return recover_enqueue(ctx, false); }
+// The cached graphs of the host-facing calls.  With deferral (CSPE + overlap)
+// each call starts with the other call's pending coupling insert on the side
+// stream (gated: a no-op when nothing is pending on the device), under its own
+// solves, and leaves its own coupling insert pending; otherwise every cache
+// update completes inside the call.
+static bool host_defer(const SolverHost *s) { return s->defer_cur && s->overlap; }
+
+static int euler_enqueue_host(mq_ctx *ctx) {
+  SolverHost *s = ctx->solver;
+  if (!host_defer(s)) return euler_enqueue(ctx, true);
+  int rc = fork_observe(ctx, 3, MQ_FAM_COUPLING_CURRENT, s->y_cur, true);
+  if (rc) return rc;
+  return euler_enqueue(ctx, true, true);
+}
+
+static int recover_enqueue_host(mq_ctx *ctx) {
+  SolverHost *s = ctx->solver;
+  if (!host_defer(s)) return recover_enqueue(ctx, false);
+  int rc = fork_observe(ctx, 4, MQ_FAM_COUPLING_PREVIOUS, s->y_cpl, true);
+  if (rc) return rc;
+  return recover_enqueue(ctx, true);
+}
 
 // a deferred insert left by the stepper, run now (before any host-visible
 // use of the families); a gated no-op if none is pending on the device
-static int flush_deferred(mq_ctx *ctx) {
-  SolverHost *s = ctx->solver;
-  if (!s || !s->maybe_pending) return MQ_OK;
-  s->maybe_pending = false;
-  return observe(ctx, MQ_FAM_COUPLING_CURRENT, s->y_cur, main_res(ctx), true);
+static const double *deferred_vec(SolverHost *s, int fam) {
+  return fam == MQ_FAM_COUPLING_CURRENT ? s->y_cur : s->y_cpl;
 }
 
-static int check_run(mq_ctx *ctx, int64_t *failed_step) {
+static int flush_deferred(mq_ctx *ctx, unsigned keep = 0u) {
   SolverHost *s = ctx->solver;
-  RunDev r;
-  MQ_CUDA(cudaMemcpyAsync(&r, s->d_run, sizeof(RunDev), cudaMemcpyDeviceToHost, ctx->stream));
-  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (!s) return MQ_OK;
+  for (int fam = MQ_FAM_COUPLING_CURRENT; fam <= MQ_FAM_COUPLING_PREVIOUS; ++fam) {
+    if (!s->maybe_pending[fam] || (keep >> fam & 1u)) continue;
+    s->maybe_pending[fam] = false;
+    const int rc = observe(ctx, fam, deferred_vec(s, fam), main_res(ctx), true);
+    if (rc) return rc;
+  }
+  return MQ_OK;
+}
+
+static int stage_status(mq_ctx *ctx, int64_t log_first) {
+  SolverHost *s = ctx->solver;
+  MQ_CUDA(cudaMemcpyAsync(&s->h_st->run, s->d_run, sizeof(RunDev), cudaMemcpyDeviceToHost, ctx->stream));
+  if (log_first >= 0)
+    MQ_CUDA(cudaMemcpyAsync(s->h_st->it, s->d_log + log_first, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  return MQ_OK;
+}
+
+static int staged_run_status(mq_ctx *ctx, int64_t *failed_step) {
+  const RunDev &r = ctx->solver->h_st->run;
   if (failed_step) *failed_step = r.err ? r.err_step : -1;
   if (r.err == 0) return MQ_OK;
   static const char *fam_name[3] = {"source", "coupling_current", "coupling_previous"};
@@ -1505,6 +1561,13 @@ static int check_run(mq_ctx *ctx, int64_t *failed_step) {
   else
     set_error("device failure (grid barrier watchdog)" + where);
   return (int)r.err;
+}
+
+static int check_run(mq_ctx *ctx, int64_t *failed_step) {
+  int rc = stage_status(ctx, -1);
+  if (rc) return rc;
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  return staged_run_status(ctx, failed_step);
 }
 
 __global__ void k_reset_run(RunDev *run) {
@@ -1572,6 +1635,11 @@ int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern)
   rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_fam, sizeof(FamDev) * 3);
   rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_run, sizeof(RunDev));
   rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_par, sizeof(StepParams));
+  rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_probe_out, sizeof(double));
+  if (!rc) {
+    cudaError_t e = cudaMallocHost((void **)&s->h_st, sizeof(SolverHost::HostStage));
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocHost");
+  }
   auto vec = [&](double **p) { return rc ? rc : (rc = s_alloc(ctx, s, (void **)p, vb)); };
   auto table = [&](double ***tab, std::vector<double *> &h, int n) {
     if (rc) return rc;
@@ -1624,7 +1692,7 @@ int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern)
       rc = rc ? rc : s_alloc(ctx, s, (void **)&s->d_cnt2, sizeof(unsigned int) * (MAXS + 4));
       if (!rc) {
         cudaError_t e = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
-        for (int q = 0; q < 4 && e == cudaSuccess; ++q) {
+        for (int q = 0; q < SolverHost::kSlots && e == cudaSuccess; ++q) {
           e = cudaEventCreateWithFlags(&s->ev_fork[q], cudaEventDisableTiming);
           if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_join[q], cudaEventDisableTiming);
         }
@@ -1672,7 +1740,7 @@ int mq_solver_reset(mq_ctx *ctx) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
   MQ_CUDA(cudaMemsetAsync(s->d_fam, 0, sizeof(FamDev) * 3, ctx->stream));
-  s->maybe_pending = false;  // the memset cleared any deferred insert
+  for (bool &m : s->maybe_pending) m = false;  // the memset cleared any deferred insert
   return init_run(ctx);
 }
 
@@ -1843,14 +1911,10 @@ int mq_state_get(mq_ctx *ctx, double *a_c, double *t) {
   return MQ_OK;
 }
 
-static int read_report(mq_ctx *ctx, int64_t first, mq_solve_report *a, mq_solve_report *b) {
-  SolverHost *s = ctx->solver;
-  int32_t it[2] = {0, 0};
-  MQ_CUDA(cudaMemcpyAsync(it, s->d_log + first, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, ctx->stream));
-  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+static void staged_report(mq_ctx *ctx, mq_solve_report *a, mq_solve_report *b) {
+  const int32_t *it = ctx->solver->h_st->it;
   if (a) { a->iterations = it[0]; a->converged = 1; a->final_rel_residual = 0; a->applies = it[0] + 1; }
   if (b) { b->iterations = it[1]; b->converged = 1; b->final_rel_residual = 0; b->applies = it[1] + 1; }
-  return MQ_OK;
 }
 
 static int ensure_log(mq_ctx *ctx, int64_t n) {
@@ -1893,59 +1957,111 @@ static int run_cached(mq_ctx *ctx, cudaGraphExec_t *g, int64_t *nlaunch, int (*f
   return MQ_OK;
 }
 
-int mq_euler_step(mq_ctx *ctx, double dt, double wave_new, int64_t step_index, mq_solve_report *rep_src,
-                  mq_solve_report *rep_cpl) {
+// Host-facing step and recovery.  Everything a call needs is enqueued on the
+// context stream and the call synchronises once: state upload, parameters, the
+// cached one-call graph, then the run status, the two iteration counts and the
+// host result (a_c or a_n) come back in one batch of copies.
+static int euler_call(mq_ctx *ctx, const double *a_c_in, double t, double dt, double wave_new, int64_t step_index,
+                      double *a_c_out, mq_solve_report *rep_src, mq_solve_report *rep_cpl) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
-  {
-    const int frc = flush_deferred(ctx);
-    if (frc) return frc;
-  }
-  {
-    const int frc = flush_deferred(ctx);
-    if (frc) return frc;
-  }
   if (dt < 0) { set_error("dt must be nonnegative"); return MQ_INVALID; }
+  {
+    const int frc = flush_deferred(ctx, host_defer(s) ? 1u << MQ_FAM_COUPLING_CURRENT : 0u);
+    if (frc) return frc;
+  }
   int rc = ensure_log(ctx, 4);
   if (rc) return rc;
+  const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
+  if (a_c_in) {
+    MQ_CUDA(cudaMemcpyAsync(ctx->d_ac, a_c_in, sizeof(double) * n_c, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->t_now = t;
+  }
   rc = reset_run(ctx);
   if (rc) return rc;
   StepParams p{dt, wave_new, wave_new, (long long)step_index};
   MQ_CUDA(cudaMemcpyAsync(s->d_par, &p, sizeof(p), cudaMemcpyHostToDevice, ctx->stream));
-  rc = run_cached(ctx, &s->euler_graph, &s->euler_launches, euler_enqueue_joined);
+  rc = run_cached(ctx, &s->euler_graph, &s->euler_launches, euler_enqueue_host);
   if (rc) return rc;
+  if (host_defer(s)) {
+    s->maybe_pending[MQ_FAM_COUPLING_CURRENT] = false;
+    s->maybe_pending[MQ_FAM_COUPLING_PREVIOUS] = true;
+  }
+  rc = stage_status(ctx, 0);
+  if (rc) return rc;
+  if (a_c_out) MQ_CUDA(cudaMemcpyAsync(a_c_out, ctx->d_ac, sizeof(double) * n_c, cudaMemcpyDeviceToHost, ctx->stream));
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
   int64_t failed = -1;
-  rc = check_run(ctx, &failed);
-  read_report(ctx, 0, rep_src, rep_cpl);
+  rc = staged_run_status(ctx, &failed);
+  staged_report(ctx, rep_src, rep_cpl);
   if (!rc) ctx->t_now += dt;
   return rc;
 }
 
-int mq_recover_an(mq_ctx *ctx, double wave_now, double *a_n_host, mq_solve_report *rep_src,
-                  mq_solve_report *rep_cpl) {
+static int recover_call(mq_ctx *ctx, const double *a_c_in, double t, double wave_now, double *a_n_host,
+                        mq_solve_report *rep_src, mq_solve_report *rep_cpl) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
   {
-    const int frc = flush_deferred(ctx);
+    const int frc = flush_deferred(ctx, host_defer(s) ? 1u << MQ_FAM_COUPLING_PREVIOUS : 0u);
     if (frc) return frc;
   }
   int rc = ensure_log(ctx, 4);
   if (rc) return rc;
+  if (a_c_in) {
+    const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
+    MQ_CUDA(cudaMemcpyAsync(ctx->d_ac, a_c_in, sizeof(double) * n_c, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->t_now = t;
+  }
   rc = reset_run(ctx);
   if (rc) return rc;
   StepParams p{0.0, wave_now, wave_now, -1};
   MQ_CUDA(cudaMemcpyAsync(s->d_par, &p, sizeof(p), cudaMemcpyHostToDevice, ctx->stream));
-  rc = run_cached(ctx, &s->recover_graph, &s->recover_launches, recover_enqueue_now);
+  rc = run_cached(ctx, &s->recover_graph, &s->recover_launches, recover_enqueue_host);
   if (rc) return rc;
-  rc = check_run(ctx, nullptr);
-  read_report(ctx, 0, rep_src, rep_cpl);
+  if (host_defer(s)) {
+    s->maybe_pending[MQ_FAM_COUPLING_PREVIOUS] = false;
+    s->maybe_pending[MQ_FAM_COUPLING_CURRENT] = true;
+  }
+  rc = stage_status(ctx, 0);
   if (rc) return rc;
   if (a_n_host) {
+    // a_n = y_src - y_cur, gathered to the compact order; a failed run is
+    // reported below and the copied values are then meaningless
     k_sub<<<stream_grid(ctx), kBlock, 0, ctx->stream>>>(ctx->topo.L, ctx->d_mask, s->y_src, s->y_cur, ctx->d_tmp1);
     LAUNCH_CHECK();
-    return mq_vec_download(ctx, ctx->d_tmp1, a_n_host);
+    const int64_t n = (int64_t)ctx->topo.nc_pad.size();
+    rc = launch_gather(n, ctx->d_nc_pad, ctx->d_tmp1, ctx->d_stage, ctx->sms, ctx->stream);
+    if (rc) return rc;
+    ctx->launches += 1;
+    MQ_CUDA(cudaMemcpyAsync(a_n_host, ctx->d_stage, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
   }
-  return MQ_OK;
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  rc = staged_run_status(ctx, nullptr);
+  staged_report(ctx, rep_src, rep_cpl);
+  return rc;
+}
+
+int mq_euler_step(mq_ctx *ctx, double dt, double wave_new, int64_t step_index, mq_solve_report *rep_src,
+                  mq_solve_report *rep_cpl) {
+  return euler_call(ctx, nullptr, 0.0, dt, wave_new, step_index, nullptr, rep_src, rep_cpl);
+}
+
+int mq_euler_step_host(mq_ctx *ctx, const double *a_c, double t, double dt, double wave_new, int64_t step_index,
+                       double *a_c_next, mq_solve_report *rep_src, mq_solve_report *rep_cpl) {
+  if (!a_c || !a_c_next) { set_error("NULL state array"); return MQ_INVALID; }
+  return euler_call(ctx, a_c, t, dt, wave_new, step_index, a_c_next, rep_src, rep_cpl);
+}
+
+int mq_recover_an(mq_ctx *ctx, double wave_now, double *a_n_host, mq_solve_report *rep_src,
+                  mq_solve_report *rep_cpl) {
+  return recover_call(ctx, nullptr, 0.0, wave_now, a_n_host, rep_src, rep_cpl);
+}
+
+int mq_recover_an_host(mq_ctx *ctx, const double *a_c, double t, double wave_now, double *a_n_host,
+                       mq_solve_report *rep_src, mq_solve_report *rep_cpl) {
+  if (!a_c) { set_error("NULL state array"); return MQ_INVALID; }
+  return recover_call(ctx, a_c, t, wave_now, a_n_host, rep_src, rep_cpl);
 }
 
 int mq_last_an(mq_ctx *ctx, double *a_n_host) {
@@ -1975,7 +2091,7 @@ static int enqueue_step(mq_ctx *ctx, double *hist) {
   if (s->recover_every_step) {
     rc = recover_enqueue(ctx, defer);
     if (rc) return rc;
-    if (defer) s->maybe_pending = true;
+    if (defer) s->maybe_pending[MQ_FAM_COUPLING_CURRENT] = true;
   }
   if (s->n_probe > 0) {
     k_probe<<<1, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, s->d_probe_plan, ctx->d_ac,
@@ -2054,16 +2170,12 @@ int mq_probe_b(mq_ctx *ctx, const double *a_c_host, double *out) {
     MQ_CUDA(cudaMemcpyAsync(ctx->d_ac_x, a_c_host, sizeof(double) * n_c, cudaMemcpyHostToDevice, ctx->stream));
     state = ctx->d_ac_x;
   }
-  double *tmp = nullptr;
-  MQ_CUDA(cudaMalloc(&tmp, sizeof(double)));
   k_probe<<<1, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, s->d_probe_plan, state,
-                                      s->d_probe_vals, s->d_probe_leaf, nullptr, nullptr, tmp);
-  cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaMemcpyAsync(out, tmp, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  cudaFree(tmp);
-  if (e != cudaSuccess) return cuda_fail(e, "probe");
-  ctx->launches += 1;
+                                      s->d_probe_vals, s->d_probe_leaf, nullptr, nullptr, s->d_probe_out);
+  LAUNCH_CHECK();
+  MQ_CUDA(cudaMemcpyAsync(&s->h_st->probe, s->d_probe_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  *out = s->h_st->probe;
   return MQ_OK;
 }
 
@@ -2081,6 +2193,13 @@ int mq_run_prepare(mq_ctx *ctx, int64_t n_steps, const double *dt, const double 
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
   if (n_steps < 0) { set_error("n_steps must be nonnegative"); return MQ_INVALID; }
+  {
+    // a host call's deferred insert: the coupling-current one is absorbed by
+    // the first step's side stream when the steps recover, the other runs now
+    const bool absorb = s->defer_cur && recover_every_step;
+    const int frc = flush_deferred(ctx, absorb ? 1u << MQ_FAM_COUPLING_CURRENT : 0u);
+    if (frc) return frc;
+  }
   const int per = recover_every_step ? 4 : 2;
   int rc = ensure_log(ctx, std::max<int64_t>(4, per * n_steps));
   if (rc) return rc;

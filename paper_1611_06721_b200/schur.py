@@ -219,28 +219,32 @@ def explicit_euler_step(state, dt: float, op: SchurOperator, step_index: int | N
     a_c, t = state
     if dt < 0:
         raise ValueError("dt must be nonnegative")
-    op._set_state(a_c, t)
+    v = f64(a_c, op.grid.n_c, "state")
     t_new = t + dt
+    a_next = _lib.pinned_empty(op.grid.n_c)
     r1, r2 = _lib.SolveReportC(), _lib.SolveReportC()
-    rc = op.lib.mq_euler_step(op.grid.ctx, float(dt), float(op.problem.waveform(t_new)),
-                              int(step_index if step_index is not None else -1),
-                              ctypes.byref(r1), ctypes.byref(r2))
+    rc = op.lib.mq_euler_step_host(op.grid.ctx, dptr(v), float(t), float(dt), float(op.problem.waveform(t_new)),
+                                   int(step_index if step_index is not None else -1), dptr(a_next),
+                                   ctypes.byref(r1), ctypes.byref(r2))
+    op.t = float(t)
     if rc == _lib.MQ_NONFINITE:
         where = f" at step {step_index}" if step_index is not None else ""
         raise StepFailureError(f"non-finite conducting state{where} (t = {t_new:.6e})")
     check(rc)
     op.solve_iterations[RhsFamily.SOURCE_CURRENT].append(int(r1.iterations))
     op.solve_iterations[RhsFamily.COUPLING_FROM_PREVIOUS_STATE].append(int(r2.iterations))
-    return op._get_state(), (_report(r1), _report(r2))
+    op.t = float(t_new)
+    return a_next, (_report(r1), _report(r2))
 
 
 def recover_an(op: SchurOperator, a_c, t: float):
     """a_n = K_n^+ j_n(t) - K_n^+ K_cn^T a_c (schur.py:408-419)."""
-    op._set_state(a_c, t)
+    v = f64(a_c, op.grid.n_c, "state")
     a_n = _lib.pinned_empty(op.grid.n_n)
     r1, r2 = _lib.SolveReportC(), _lib.SolveReportC()
-    rc = op.lib.mq_recover_an(op.grid.ctx, float(op.problem.waveform(t)), dptr(a_n),
-                              ctypes.byref(r1), ctypes.byref(r2))
+    rc = op.lib.mq_recover_an_host(op.grid.ctx, dptr(v), float(t), float(op.problem.waveform(t)), dptr(a_n),
+                                   ctypes.byref(r1), ctypes.byref(r2))
+    op.t = float(t)
     check(rc)
     op.solve_iterations[RhsFamily.SOURCE_CURRENT].append(int(r1.iterations))
     op.solve_iterations[RhsFamily.COUPLING_FROM_CURRENT_STATE].append(int(r2.iterations))

@@ -558,6 +558,39 @@ def test_overlapped_source_update(gpu_ok, monkeypatch):
 
 
 @pytest.mark.slow
+def test_host_step_api_matches_device_loop(gpu_ok):
+    """64^3: explicit_euler_step + recover_an from the host (each call leaves
+    its coupling-family insert pending on the device for the next call's side
+    stream) reproduce the device-resident loop bit for bit, and every insert
+    is accounted for."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, SchurOperator, explicit_euler_step, recover_an, run_explicit
+    from paper_1611_06721_b200.schur import step_times
+    spec = C.config_spec(1)
+    n = 6
+    res = run_explicit(C.make_problem(1), t_end=n * spec.dt, dt=spec.dt, strategy="cspe",
+                       pcg=PcgConfig(rel_tol=1e-8), max_cols=5, output_period=spec.dt * (1 - 1e-3))
+    dts, _ = step_times(n * spec.dt, spec.dt, spec.dt * (1 - 1e-3))   # the loop's own step sizes
+    assert len(dts) == n
+    op = SchurOperator(C.make_problem(1), pcg=PcgConfig(rel_tol=1e-8), strategy="cspe", max_cols=5)
+    a, t = np.zeros(op.grid.n_c), 0.0
+    recover_an(op, a, t)
+    its = []
+    for s, dt in enumerate(dts):
+        a, (r1, r2) = explicit_euler_step((a, t), dt, op, s + 1)
+        t += dt
+        a_n, (q1, q2) = recover_an(op, a, t)
+        its.append([r1.iterations, r2.iterations, q1.iterations, q2.iterations])
+    assert np.array_equal(np.asarray(its), res.step_iterations)
+    assert np.array_equal(a, res.final_a_c)
+    assert np.array_equal(a_n, res.final_a_n)
+    d = op.diagnostics()
+    assert d.maintenance_applies == res.aggregates["maintenance_applies"]
+    assert d.pcg_applies == res.aggregates["pcg_applies"]
+    op.grid.close()
+
+
+@pytest.mark.slow
 def test_config2_first_steps_vs_oracle(gpu_ok):
     """configs[2] (128^3, two iron blocks, POD-30, TMA brick PCG): the first
     two steps against the CPU oracle's run (tests/golden/oracle_cfg2.npz,
