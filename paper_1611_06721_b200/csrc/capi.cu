@@ -280,7 +280,9 @@ int mq_pcg_kernel_info(const mq_ctx *ctx, char *name, int32_t cap, int32_t *grid
   int g = 0;
   if (ctx->pcg_variant == 1) { n = "pcg_stencil_kernel"; g = ctx->pcg_grid; }
   else if (ctx->pcg_variant == 2) {
-    n = "pcg_resident_kernel<" + std::to_string((ctx->res_geo.nx + ctx->res_geo.chunks - 1) / ctx->res_geo.chunks) + ">";
+    const int li = (ctx->res_geo.nx + ctx->res_geo.chunks - 1) / ctx->res_geo.chunks;
+    n = std::string(resident_single_reduction(li) ? "pcg_resident1_kernel<" : "pcg_resident_kernel<") +
+        std::to_string(li) + ">";
     g = ctx->res_grid;
   } else { n = "pcg_tma_kernel"; g = ctx->brick_grid; }
   if (name && cap > 0) {

@@ -153,6 +153,7 @@ int launch_kn_apply_brick(const Lay &L, const BrickGeo &geo, const uint32_t *mas
 int launch_pcg_ctx(mq_ctx *ctx, const StencilPcgArgs &args);
 int resident_pcg_setup(int nx, int ny, int nz, int *grid, BrickGeo *geo);
 int launch_pcg_resident(const StencilPcgArgs &args, const BrickGeo &geo, int grid, cudaStream_t s);
+bool resident_single_reduction(int li_max);
 int launch_kn_apply(const Lay &L, const uint32_t *mask, double dg, double of, const double *x, double *y, int sms,
                     cudaStream_t s);
 int launch_scatter(int64_t n, const int32_t *idx, const double *src, double *dst, int sms, cudaStream_t s);

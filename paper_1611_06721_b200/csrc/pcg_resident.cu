@@ -478,6 +478,466 @@ done:
 }
 
 // ---------------------------------------------------------------------------
+// One grid reduction per iteration (pcg_resident1_kernel).  The reference's
+// iteration (krylov.py:231-249) needs p.Ap before alpha and r.z after the
+// r update: two reductions, two grid barriers.  With the scalar Jacobi
+// preconditioner (z = inv * r) the next r.z follows from scalars of the
+// current iteration,
+//   |r - alpha Ap|^2 = r.r - 2 alpha r.Ap + alpha^2 Ap.Ap,
+// so K1 reduces [p.Ap, r.Ap, Ap.Ap, r.r, r.z] in one barrier (D'Azevedo,
+// Eijkhout & Romine's reduced-synchronisation CG).  Only beta uses the
+// extrapolated value; alpha uses r.z, and the stopping test |r| <= target
+// uses r.r, both summed directly from the vector, one barrier later: the
+// test of iteration it is read at the barrier of it+1, whose K1 pass is then
+// discarded (x, the iteration count and the reported residual are the
+// reference's).  Exact-arithmetic iterates are unchanged; in fp64 they differ
+// from the two-barrier kernel in the last bits (PCG parity bar: 1e-8 field,
+// +-1 iteration).
+// Halo exchange without a second barrier: owners publish Ap (instead of r);
+// every CTA keeps the r of its halo ring in shared memory (HR) and advances
+// it with alpha and the neighbours' published Ap, bit-identical to the
+// owners' own update; halo p follows from HR and the CTA's halo p_old as
+// before.  Only for li_max <= 4 (the HR ring needs 39 KB next to the 186 KB
+// of P, R and X).
+// halo Ap loads issued right after the barrier, ahead of the partial-sum
+// read, by warps 1..15 only (2; measured 9.4 us/iteration at 64^3), by all
+// warps (1; 9.5 us) or after alpha (0; 10.4 us)
+#ifndef MQ_RES1_EARLY
+#define MQ_RES1_EARLY 2
+#endif
+#ifndef MQ_RES1_APSURF
+#define MQ_RES1_APSURF 0
+#endif
+template <int LI>
+__global__ void __launch_bounds__(RT, 1) pcg_resident1_kernel(ResPcgArgs A) {
+  extern __shared__ __align__(16) double rsm[];
+  __shared__ double red[5 * RW];
+  __shared__ double tot[5];
+  const StencilPcgArgs &a = A.a;
+  const ResGeo &g = A.g;
+  const Lay &L = a.L;
+  const int G = gridDim.x;
+  const int tid = threadIdx.x, ty = tid >> 5, tx = tid & 31;
+  const double dg = a.dg, of = a.of, inv = a.inv;
+  const bool jac = a.use_jac != 0;
+  const int x0_mode = a.x0_mode_dev ? *a.x0_mode_dev : a.x0_mode;
+  if (a.err_word && *((volatile const unsigned int *)a.err_word)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      PcgOut o{};
+      o.status = 99;
+      *a.out = o;
+    }
+    return;
+  }
+  const int b = blockIdx.x;
+  const int tk = b % g.tiles_k, tj = (b / g.tiles_k) % g.tiles_j, ic = b / (g.tiles_k * g.tiles_j);
+  const int k0 = tk * RTK, j0 = tj * RTJ;
+  const int i0 = (int)(((int64_t)ic * g.nx) / g.chunks), i1 = (int)(((int64_t)(ic + 1) * g.nx) / g.chunks);
+  const int li = i1 - i0;
+  const int NH = 2 * RHP + g.li_max * RRING;
+  double *P = rsm;                                   // [li+2][3][RHP], plane 0 = i0-1
+  double *R = P + (size_t)(g.li_max + 2) * 3 * RHP;  // [li][3][RT]
+  double *X = R + (size_t)g.li_max * 3 * RT;         // [li][3][RT]
+  double *HR = X + (size_t)g.li_max * 3 * RT;        // [3][NH] r of the halo slots
+  const int j = j0 + ty, k = k0 + tx;
+  const bool own_ok = j < g.ny && k < g.nz;
+  const int s_own = (ty + 1) * RHK + (tx + 1);
+  const int64_t pos_own = L.off + (int64_t)j * L.Sj + k;
+  auto Pidx = [&](int l, int c, int s) { return ((size_t)l * 3 + c) * RHP + s; };
+  auto Oidx = [&](int l, int c) { return ((size_t)l * 3 + c) * RT + tid; };
+  const uint32_t *mask = a.mask;
+  uint32_t act = 0u;
+  if (own_ok)
+    for (int l = 0; l < li; ++l)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int64_t e = c * L.C + (int64_t)(i0 + l) * L.Si + pos_own;
+        act |= ((__ldg(mask + (e >> 5)) >> (e & 31)) & 1u) << (3 * l + c);
+      }
+  auto own_e = [&](int l, int c) { return c * L.C + (int64_t)(i0 + l) * L.Si + pos_own; };
+  auto is_act = [&](int l, int c) { return (act >> (3 * l + c)) & 1u; };
+  auto V = [&](int l, int c) {
+    return [=](int cc, int di, int dj, int dk) { return P[Pidx(l + 1 + di, cc, s_own + dj * RHK + dk)]; };
+  };
+  const int nhalo = 2 * RHP + li * RRING;
+  auto halo_slot = [&](int h, int &l, int &s) {
+    if (h < RHP) { l = 0; s = h; return; }
+    if (h < 2 * RHP) { l = li + 1; s = h - RHP; return; }
+    h -= 2 * RHP;
+    l = 1 + h / RRING;
+    const int q = h % RRING;
+    int jj, kk;
+    if (q < RHK) { jj = 0; kk = q; }
+    else if (q < 2 * RHK) { jj = RHJ - 1; kk = q - RHK; }
+    else if (q < 2 * RHK + RTJ) { jj = 1 + (q - 2 * RHK); kk = 0; }
+    else { jj = 1 + (q - 2 * RHK - RTJ); kk = RHK - 1; }
+    s = jj * RHK + kk;
+  };
+  auto halo_e = [&](int l, int s, int c, bool &ok) {
+    const int jj = s / RHK, kk = s % RHK;
+    const int gi = i0 - 1 + l, gj = j0 - 1 + jj, gk = k0 - 1 + kk;
+    ok = gi >= -1 && gi <= g.nx && gj >= -1 && gj <= g.ny && gk >= -1 && gk <= g.nz;
+    return c * L.C + L.off + (int64_t)gi * L.Si + (int64_t)gj * L.Sj + gk;
+  };
+  unsigned long long *trace = (blockIdx.x == 0 && threadIdx.x == 0) ? a.trace : nullptr;
+  auto stamp = [&](int slot) {
+    if (trace && slot < 4 * 64 + 1) trace[slot] = globaltimer_ns();
+  };
+  auto fstamp = [&](int it, int k) {
+#ifdef MQ_TRACE_FINE
+    if (trace && it <= 32) trace[320 + 8 * (it - 1) + k] = globaltimer_ns();
+#else
+    (void)it;
+    (void)k;
+#endif
+  };
+  stamp(0);
+  // ---- initial residual (krylov.py:209-218), as pcg_resident_kernel ----
+  double v3[3] = {0.0, 0.0, 0.0};
+  {
+    if (x0_mode == 1) {
+      for (int h = tid; h < nhalo; h += RT) {
+        int l, s;
+        halo_slot(h, l, s);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          bool ok;
+          const int64_t e = halo_e(l, s, c, ok);
+          P[Pidx(l, c, s)] = ok ? __ldcg(a.x + e) : 0.0;
+        }
+      }
+      for (int l = 0; l < li; ++l)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) P[Pidx(l + 1, c, s_own)] = own_ok ? __ldcg(a.x + own_e(l, c)) : 0.0;
+      __syncthreads();
+    }
+    for (int l = 0; l < li; ++l)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double rv = 0.0;
+        if (own_ok && is_act(l, c)) {
+          const int64_t e = own_e(l, c);
+          const double bv = __ldcg(a.b + e);
+          rv = bv;
+          if (x0_mode == 1) rv = sub(bv, stencil_r(c, dg, of, V(l, c)));
+          else a.x[e] = 0.0;
+          const double z = jac ? mul(inv, rv) : rv;
+          v3[0] = add(v3[0], mul(bv, bv));
+          v3[1] = add(v3[1], mul(rv, rv));
+          v3[2] = add(v3[2], mul(rv, z));
+          a.r[e] = rv;  // the neighbours' initial halo r
+        }
+        R[Oidx(l, c)] = rv;
+        X[Oidx(l, c)] = (x0_mode == 1 && own_ok) ? P[Pidx(l + 1, c, s_own)] : 0.0;
+      }
+  }
+  block_sum_r<3>(v3, red);
+  if (threadIdx.x == 0) {
+    a.partials[0 * G + blockIdx.x] = v3[0];
+    a.partials[1 * G + blockIdx.x] = v3[1];
+    a.partials[2 * G + blockIdx.x] = v3[2];
+  }
+  int status = MQ_OK, iters = 0, converged = 0;
+  double rel = 0.0, bnorm = 0.0, alpha = 0.0, rz = 0.0;
+  const int applies0 = (x0_mode == 2) ? 0 : 1;
+  // activity of this thread's halo slots h = hbase + u * hstride (slot u,
+  // component c -> bit 3u+c): inactive and out-of-box slots keep r = 0 and
+  // never read Ap.  With MQ_RES1_EARLY == 2 warp 0 has no halo slots (it
+  // reads the partial sums while the other warps' halo loads are in flight).
+  uint32_t hact = 0u;
+#if MQ_RES1_EARLY == 2
+  const int hbase = tid - 32, hstride = RT - 32;
+#else
+  const int hbase = tid, hstride = RT;
+#endif
+  static_assert(2 * RHP + 4 * RRING <= HU * (RT - 32), "halo slots of li <= 4 fit one round");
+  if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
+  {
+    double s3[3];
+    grid_partials_sum<3>(a.partials, G, s3, tot);
+#pragma unroll
+    for (int u = 0; u < HU; ++u) {
+      const int h = hbase + u * hstride;
+      if (hbase >= 0 && h < nhalo) {
+        int l, s;
+        halo_slot(h, l, s);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          bool ok;
+          const int64_t e = halo_e(l, s, c, ok);
+          const bool on = ok && ((__ldg(mask + (e >> 5)) >> (e & 31)) & 1u);
+          hact |= (uint32_t)on << (3 * u + c);
+          HR[c * NH + h] = on ? __ldcg(a.r + e) : 0.0;
+        }
+      }
+    }
+    bnorm = sqrt(s3[0]);
+    const double target = fmax(a.rel_tol * bnorm, a.abs_tol);
+    double rnorm = sqrt(s3[1]);
+    rz = jac ? s3[2] : s3[1];
+    auto relf = [&](double res) { return bnorm > 0.0 ? res / bnorm : (res == 0.0 ? 0.0 : INFINITY); };
+    rel = relf(rnorm);
+    if (rnorm <= target) { converged = 1; goto done; }
+    double beta = 0.0;
+    bool first = true;
+    // this thread's halo slots: P index of component 0 (components are RHP
+    // apart) and padded element of component 0 (components L.C apart)
+    int hp[HU], he[HU];
+#pragma unroll
+    for (int u = 0; u < HU; ++u) {
+      const int h = hbase + u * hstride;
+      hp[u] = -1;
+      he[u] = 0;
+      if (hbase >= 0 && h < nhalo) {
+        int l, s;
+        halo_slot(h, l, s);
+        bool ok;
+        hp[u] = (int)Pidx(l, 0, s);
+        he[u] = (int)halo_e(l, s, 0, ok);
+      }
+    }
+    // the neighbours' published Ap at this thread's active halo slots, all
+    // loads in flight before the first use (one L2 round trip)
+    double hq[HU][3];
+    auto issue_ap_halo = [&]() {
+#pragma unroll
+      for (int u = 0; u < HU; ++u)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          hq[u][c] = ((hact >> (3 * u + c)) & 1u) ? __ldcg(a.ap + he[u] + c * L.C) : 0.0;
+    };
+    for (int it = 1;; ++it) {
+      fstamp(it, 0);
+      // ---- K1: p_new (own and halo) from r; Ap; partials of p.Ap, r.Ap,
+      // Ap.Ap and of r.r, r.z of the current r.  Shared-memory operands are
+      // loaded in batches ahead of the stores (the compiler cannot reorder
+      // loads past stores into the same array) ----
+      double v5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      {
+        double rq[LI * 3], po[LI * 3];
+#pragma unroll
+        for (int l = 0; l < LI; ++l)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            rq[3 * l + c] = l < li ? R[Oidx(l, c)] : 0.0;
+            po[3 * l + c] = (l < li && !first) ? P[Pidx(l + 1, c, s_own)] : 0.0;
+          }
+#pragma unroll
+        for (int l = 0; l < LI; ++l)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if (l < li) {
+              const double r0 = rq[3 * l + c];
+              const double z = jac ? mul(inv, r0) : r0;
+              P[Pidx(l + 1, c, s_own)] = first ? z : add(z, mul(beta, po[3 * l + c]));
+              if (own_ok && is_act(l, c)) {
+                v5[3] = add(v5[3], mul(r0, r0));
+                v5[4] = add(v5[4], mul(r0, z));
+              }
+            }
+          }
+      }
+      {
+        double hv[HU][3], ho[HU][3];
+#pragma unroll
+        for (int u = 0; u < HU; ++u)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const int h = hbase + u * hstride;
+            hv[u][c] = hp[u] >= 0 ? HR[c * NH + h] : 0.0;
+            ho[u][c] = (hp[u] >= 0 && !first) ? P[hp[u] + c * RHP] : 0.0;
+          }
+#pragma unroll
+        for (int u = 0; u < HU; ++u)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if (hp[u] < 0) continue;
+            const double z = jac ? mul(inv, hv[u][c]) : hv[u][c];
+            P[hp[u] + c * RHP] = first ? z : add(z, mul(beta, ho[u][c]));
+          }
+      }
+      fstamp(it, 1);
+      __syncthreads();
+      double av[LI * 3];
+      {
+        PlaneVals pm, p0, pp;
+        load_plane(P, 0, s_own, pm);
+        load_plane(P, 1, s_own, p0);
+#pragma unroll
+        for (int l = 0; l < LI; ++l) {
+          load_plane(P, l + 2, s_own, pp);
+          auto W = [&](int cc, int di, int dj, int dk) { return pick(di < 0 ? pm : (di > 0 ? pp : p0), cc, dj, dk); };
+#pragma unroll
+          for (int c = 0; c < 3; ++c) av[3 * l + c] = stencil_r(c, dg, of, W);
+          pm = p0;
+          p0 = pp;
+        }
+      }
+#pragma unroll
+      for (int l = 0; l < LI; ++l)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (l < li && own_ok && is_act(l, c)) {
+            const double apv = av[3 * l + c];
+            v5[0] = add(v5[0], mul(P[Pidx(l + 1, c, s_own)], apv));
+            v5[1] = add(v5[1], mul(R[Oidx(l, c)], apv));
+            v5[2] = add(v5[2], mul(apv, apv));
+#if MQ_RES1_APSURF
+            // only the brick surface is anyone's halo
+            if (l == 0 || l == li - 1 || ty == 0 || ty == RTJ - 1 || tx == 0 || tx == RTK - 1)
+#endif
+            a.ap[own_e(l, c)] = apv;  // the neighbours' halo r update
+          }
+        }
+      fstamp(it, 2);
+      // block sums: warp sums to shared memory, lane q of warp 0 adds value
+      // q over the 16 warps in order and stores this CTA's partial (only
+      // the partials leave the CTA; one CTA barrier)
+      double *pt = a.partials + 3 * G + (it & 1) * 5 * G;  // alternating sets: a fast CTA's
+#pragma unroll                                              // next partials never race a
+      for (int q = 0; q < 5; ++q) v5[q] = warp_sum(v5[q]);  // slow CTA's read of these
+      if (tx == 0) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) red[q * RW + ty] = v5[q];
+      }
+      __syncthreads();
+      if (ty == 0 && tx < 5) {
+        double sacc = 0.0;
+        for (int w = 0; w < RW; ++w) sacc = add(sacc, red[tx * RW + w]);
+        pt[tx * G + blockIdx.x] = sacc;
+      }
+      stamp(4 * (it - 1) + 1);
+      if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
+      stamp(4 * (it - 1) + 2);
+      double s5[5];
+#if MQ_RES1_EARLY
+      issue_ap_halo();
+#endif
+      {
+        // warp q < 5 reads partial row q (G <= 160: five loads per lane in
+        // flight), fixed-order lane sums then the warp tree: identical in
+        // every CTA
+        if (ty < 5) {
+          double pv[5];
+#pragma unroll
+          for (int u = 0; u < 5; ++u) {
+            const int bb = tx + 32 * u;
+            pv[u] = bb < G ? __ldcg(pt + (int64_t)ty * G + bb) : 0.0;
+          }
+          double sacc = 0.0;
+#pragma unroll
+          for (int u = 0; u < 5; ++u)
+            if (tx + 32 * u < G) sacc = add(sacc, pv[u]);
+          sacc = warp_sum(sacc);
+          if (tx == 0) tot[ty] = sacc;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 5; ++q) s5[q] = tot[q];
+      }
+      fstamp(it, 3);
+      if (!first) {
+        // the previous iteration's stopping test and r.z (krylov.py:239-246)
+        rnorm = sqrt(s5[3]);
+        rel = relf(rnorm);
+        if (rnorm <= target) { converged = 1; break; }
+        const double rz_d = jac ? s5[4] : s5[3];
+        if (!isfinite(rz_d)) { status = MQ_INDEFINITE; break; }
+        rz = rz_d;
+      }
+      if (it > a.max_iter) break;  // budget: iters == max_iter, not converged
+      const double pap = s5[0];
+      if (!isfinite(pap) || pap <= 0.0) { status = MQ_INDEFINITE; iters = it; break; }
+      alpha = rz / pap;
+      // ---- K2: x += alpha p, r -= alpha Ap (own), halo r -= alpha Ap ----
+#if !MQ_RES1_EARLY
+      issue_ap_halo();
+#endif
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        constexpr int LH = (LI + 1) / 2;
+        double xo[LH * 3], pv[LH * 3], ro[LH * 3];
+#pragma unroll
+        for (int l2 = 0; l2 < LH; ++l2)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const int l = h2 * LH + l2;
+            const bool on = l < LI && l < li;
+            xo[3 * l2 + c] = on ? X[Oidx(l, c)] : 0.0;
+            pv[3 * l2 + c] = on ? P[Pidx(l + 1, c, s_own)] : 0.0;
+            ro[3 * l2 + c] = on ? R[Oidx(l, c)] : 0.0;
+          }
+#pragma unroll
+        for (int l2 = 0; l2 < LH; ++l2)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const int l = h2 * LH + l2;
+            if (!(l < LI && l < li && own_ok && is_act(l, c))) continue;
+            X[Oidx(l, c)] = add(xo[3 * l2 + c], mul(alpha, pv[3 * l2 + c]));
+            R[Oidx(l, c)] = sub(ro[3 * l2 + c], mul(alpha, av[3 * l + c]));
+          }
+      }
+      {
+        double hv[HU][3];
+#pragma unroll
+        for (int u = 0; u < HU; ++u)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) hv[u][c] = hp[u] >= 0 ? HR[c * NH + hbase + u * hstride] : 0.0;
+#pragma unroll
+        for (int u = 0; u < HU; ++u)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            if ((hact >> (3 * u + c)) & 1u) HR[c * NH + hbase + u * hstride] = sub(hv[u][c], mul(alpha, hq[u][c]));
+      }
+      iters = it;
+      fstamp(it, 4);
+      // beta from the extrapolated r.z of the updated r
+      const double rr_new = add(sub(s5[3], mul(mul(2.0, alpha), s5[1])), mul(mul(alpha, alpha), s5[2]));
+      const double rz_new = jac ? mul(inv, rr_new) : rr_new;
+      beta = rz_new > 0.0 ? rz_new / rz : 0.0;
+      first = false;
+    }
+    if (status == MQ_OK && !converged) status = MQ_NOT_CONVERGED;
+#pragma unroll
+    for (int l = 0; l < LI; ++l)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        if (l < li && own_ok && is_act(l, c)) a.x[own_e(l, c)] = X[Oidx(l, c)];
+  }
+done:
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    PcgOut o;
+    o.iterations = iters;
+    o.converged = converged;
+    o.status = status;
+    o.applies = applies0 + iters;
+    o.rel = rel;
+    o.bnorm = bnorm;
+    o.alpha = alpha;
+    o.rz = rz;
+    *a.out = o;
+  }
+}
+
+static const void *resident1_kernel_for(int li_max) {
+  switch (li_max) {
+    case 1: return (const void *)pcg_resident1_kernel<1>;
+    case 2: return (const void *)pcg_resident1_kernel<2>;
+    case 3: return (const void *)pcg_resident1_kernel<3>;
+    default: return (const void *)pcg_resident1_kernel<4>;
+  }
+}
+
+__host__ __device__ constexpr size_t res1_smem_bytes(int li) {
+  return res_smem_bytes(li) + sizeof(double) * 3 * (size_t)(2 * RHP + li * RRING);
+}
+
+// single-reduction kernel unless MQ_PCG_SYNC=2 or the HR ring does not fit
+static bool use_resident1(int li_max) {
+  const char *v = getenv("MQ_PCG_SYNC");
+  return !(v && v[0] == '2') && li_max <= 4;
+}
+
 static const void *resident_kernel_for(int li_max) {
   switch (li_max) {
     case 1: return (const void *)pcg_resident_kernel<1>;
@@ -487,6 +947,8 @@ static const void *resident_kernel_for(int li_max) {
     default: return (const void *)pcg_resident_kernel<5>;
   }
 }
+
+bool resident_single_reduction(int li_max) { return use_resident1(li_max); }
 
 // Returns 0 with *grid = 0 when the grid does not fit the resident scheme.
 int resident_pcg_setup(int nx, int ny, int nz, int *grid, BrickGeo *geo_out) {
@@ -510,9 +972,15 @@ int resident_pcg_setup(int nx, int ny, int nz, int *grid, BrickGeo *geo_out) {
   // kernel with one plane per CTA)
   if (2 * tiles * best < sms) return MQ_OK;
   const int li_max = (nx + best - 1) / best;
-  const size_t smem = res_smem_bytes(li_max);
-  const void *fn = resident_kernel_for(li_max);
-  MQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const bool one = use_resident1(li_max);
+  const size_t smem = one ? res1_smem_bytes(li_max) : res_smem_bytes(li_max);
+  const void *fn = one ? resident1_kernel_for(li_max) : resident_kernel_for(li_max);
+  // both variants launchable (MQ_PCG_SYNC is read per launch)
+  MQ_CUDA(cudaFuncSetAttribute(resident_kernel_for(li_max), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)res_smem_bytes(li_max)));
+  if (li_max <= 4)
+    MQ_CUDA(cudaFuncSetAttribute(resident1_kernel_for(li_max), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)res1_smem_bytes(li_max)));
   int per = 0;
   MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, RT, smem));
   if (per < 1 || tiles * best > sms * per) return MQ_OK;
@@ -539,10 +1007,12 @@ int launch_pcg_resident(const StencilPcgArgs &args, const BrickGeo &geo, int gri
   A.g.chunks = geo.chunks;
   A.g.nbricks = geo.nbricks;
   A.g.li_max = (geo.nx + geo.chunks - 1) / geo.chunks;
-  const size_t smem = res_smem_bytes(A.g.li_max);
+  const bool one = use_resident1(A.g.li_max);
+  const size_t smem = one ? res1_smem_bytes(A.g.li_max) : res_smem_bytes(A.g.li_max);
   MQ_CUDA(cudaMemsetAsync(&args.bar->count, 0, sizeof(unsigned long long), s));
   void *params[] = {&A};
-  MQ_CUDA(cudaLaunchCooperativeKernel(resident_kernel_for(A.g.li_max), dim3(grid), dim3(RT), params, smem, s));
+  const void *fn = one ? resident1_kernel_for(A.g.li_max) : resident_kernel_for(A.g.li_max);
+  MQ_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(RT), params, smem, s));
   return MQ_OK;
 }
 

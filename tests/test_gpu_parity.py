@@ -678,15 +678,18 @@ def test_ensemble_member_first_steps(gpu_ok):
         assert rel(res.a_c_history[i], tr.a_c[i + 1]) <= REL_FIELD
 
 
-@pytest.mark.parametrize("variant", ["simple", "brick", "resident"])
+@pytest.mark.parametrize("variant", ["simple", "brick", "resident", "resident2"])
 def test_pcg_kernel_variants_agree(gpu_ok, variant, monkeypatch):
-    """All three fused-PCG kernels (thread-per-row, TMA brick, shared-memory
-    resident) solve the same system like the oracle; they differ only in the
-    dot-product summation order."""
+    """All fused-PCG kernels (thread-per-row, TMA brick, shared-memory
+    resident with one or -- MQ_PCG_SYNC=2 -- two grid reductions per
+    iteration) solve the same system like the oracle; they differ only in the
+    dot-product summation order (and, single-reduction, beta from the
+    extrapolated r.z)."""
     from paper_1611_06721_b200 import PcgConfig, Preconditioner, pcg_solve
     from paper_1611_06721_b200 import configs as C
     from paper_1611_06721_b200.device import DeviceGrid
-    monkeypatch.setenv("MQ_PCG_KERNEL", variant)
+    monkeypatch.setenv("MQ_PCG_KERNEL", variant.rstrip("2"))
+    monkeypatch.setenv("MQ_PCG_SYNC", "2" if variant.endswith("2") else "1")
     for index in (0, 1):
         spec, m = oracle_model(index)
         with DeviceGrid(C.make_problem(index)) as g:
@@ -700,6 +703,43 @@ def test_pcg_kernel_variants_agree(gpu_ok, variant, monkeypatch):
                 ref = O.pcg(m.kn_apply, b, x0=start, rel_tol=1e-8, inv_diag=inv)
                 assert rep.converged and abs(rep.iterations - ref.iterations) <= 1
                 assert rel(x, ref.x) <= 1e-8
+
+
+@pytest.mark.parametrize("sync", ["1", "2"])
+def test_resident_pcg_semantics(gpu_ok, sync, monkeypatch):
+    """64^3 (shared-memory resident kernel, one or two reductions per
+    iteration): krylov.py's budget exhaustion, exact start vector, zero rhs and
+    application counts, against the oracle.  The single-reduction kernel reads
+    the stopping test one barrier late; the counts must not see it."""
+    from paper_1611_06721_b200 import PcgConfig, Preconditioner, pcg_solve
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200.device import DeviceGrid
+    monkeypatch.setenv("MQ_PCG_KERNEL", "resident")
+    monkeypatch.setenv("MQ_PCG_SYNC", sync)
+    spec, m = oracle_model(1)
+    inv = O.jacobi_inverse(m.kn.diagonal())
+    with DeviceGrid(C.make_problem(1)) as g:
+        name, _ = g.pcg_kernel()
+        assert name.startswith("pcg_resident1_kernel" if sync == "1" else "pcg_resident_kernel"), name
+        op = g.kn_operator()
+        jac = Preconditioner.JACOBI
+        for budget in (1, 2, 3):
+            x, rep = pcg_solve(op, m.pattern, config=PcgConfig(rel_tol=1e-14, max_iter=budget, preconditioner=jac))
+            ref = O.pcg(m.kn_apply, m.pattern, rel_tol=1e-14, max_iter=budget, inv_diag=inv)
+            assert not rep.converged and rep.iterations == budget and rep.applications == ref.applies
+            assert rel(x, ref.x) <= 1e-12
+            assert abs(rep.final_rel_residual - ref.rel) <= 1e-10 * ref.rel
+        x, rep = pcg_solve(op, np.zeros(m.n_n), config=PcgConfig(rel_tol=1e-8, preconditioner=jac))
+        assert rep.iterations == 0 and rep.converged and rep.applications == 0
+        assert np.array_equal(x, np.zeros(m.n_n))
+        ref = O.pcg(m.kn_apply, m.pattern, rel_tol=1e-8, inv_diag=inv)
+        x, rep = pcg_solve(op, m.pattern, config=PcgConfig(rel_tol=1e-8, preconditioner=jac))
+        assert rep.converged and abs(rep.iterations - ref.iterations) <= 1
+        assert rep.applications == rep.iterations and rel(x, ref.x) <= 1e-8
+        # warm start from the converged solution: 0 iterations, x unchanged
+        b = m.kn @ x
+        x2, rep2 = pcg_solve(op, b, x0=x, config=PcgConfig(rel_tol=1e-8, preconditioner=jac))
+        assert rep2.iterations == 0 and rep2.applications == 1 and np.array_equal(x2, x)
 
 
 @pytest.mark.parametrize("world", [1, 2, 3])
