@@ -505,6 +505,9 @@ done:
 #ifndef MQ_RES1_EARLY
 #define MQ_RES1_EARLY 2
 #endif
+#ifndef MQ_RES1_LH
+#define MQ_RES1_LH 1  // planes per batch of the own update's shared-memory loads
+#endif
 #ifndef MQ_RES1_APSURF
 #define MQ_RES1_APSURF 0
 #endif
@@ -706,58 +709,36 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident1_kernel(ResPcgArgs A) {
         for (int c = 0; c < 3; ++c)
           hq[u][c] = ((hact >> (3 * u + c)) & 1u) ? __ldcg(a.ap + he[u] + c * L.C) : 0.0;
     };
+    // p_0 = z_0 (own and halo); r.r and r.z of r_0 ride on the first
+    // reduction (krylov.py:228-230)
+    double v5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int l = 0; l < LI; ++l)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (l < li) {
+          const double r0 = R[Oidx(l, c)];
+          const double z = jac ? mul(inv, r0) : r0;
+          P[Pidx(l + 1, c, s_own)] = z;
+          if (own_ok && is_act(l, c)) {
+            v5[3] = add(v5[3], mul(r0, r0));
+            v5[4] = add(v5[4], mul(r0, z));
+          }
+        }
+      }
+#pragma unroll
+    for (int u = 0; u < HU; ++u)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        if (hp[u] >= 0) {
+          const double hv = HR[c * NH + hbase + u * hstride];
+          P[hp[u] + c * RHP] = jac ? mul(inv, hv) : hv;
+        }
     for (int it = 1;; ++it) {
       fstamp(it, 0);
-      // ---- K1: p_new (own and halo) from r; Ap; partials of p.Ap, r.Ap,
-      // Ap.Ap and of r.r, r.z of the current r.  Shared-memory operands are
-      // loaded in batches ahead of the stores (the compiler cannot reorder
-      // loads past stores into the same array) ----
-      double v5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-      {
-        double rq[LI * 3], po[LI * 3];
-#pragma unroll
-        for (int l = 0; l < LI; ++l)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            rq[3 * l + c] = l < li ? R[Oidx(l, c)] : 0.0;
-            po[3 * l + c] = (l < li && !first) ? P[Pidx(l + 1, c, s_own)] : 0.0;
-          }
-#pragma unroll
-        for (int l = 0; l < LI; ++l)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            if (l < li) {
-              const double r0 = rq[3 * l + c];
-              const double z = jac ? mul(inv, r0) : r0;
-              P[Pidx(l + 1, c, s_own)] = first ? z : add(z, mul(beta, po[3 * l + c]));
-              if (own_ok && is_act(l, c)) {
-                v5[3] = add(v5[3], mul(r0, r0));
-                v5[4] = add(v5[4], mul(r0, z));
-              }
-            }
-          }
-      }
-      {
-        double hv[HU][3], ho[HU][3];
-#pragma unroll
-        for (int u = 0; u < HU; ++u)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const int h = hbase + u * hstride;
-            hv[u][c] = hp[u] >= 0 ? HR[c * NH + h] : 0.0;
-            ho[u][c] = (hp[u] >= 0 && !first) ? P[hp[u] + c * RHP] : 0.0;
-          }
-#pragma unroll
-        for (int u = 0; u < HU; ++u)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            if (hp[u] < 0) continue;
-            const double z = jac ? mul(inv, hv[u][c]) : hv[u][c];
-            P[hp[u] + c * RHP] = first ? z : add(z, mul(beta, ho[u][c]));
-          }
-      }
-      fstamp(it, 1);
       __syncthreads();
+      // ---- Ap = K_n p from shared memory; partials p.Ap, r.Ap, Ap.Ap per
+      // plane as the march passes it; Ap published for the neighbours' halo
       double av[LI * 3];
       {
         PlaneVals pm, p0, pp;
@@ -769,27 +750,21 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident1_kernel(ResPcgArgs A) {
           auto W = [&](int cc, int di, int dj, int dk) { return pick(di < 0 ? pm : (di > 0 ? pp : p0), cc, dj, dk); };
 #pragma unroll
           for (int c = 0; c < 3; ++c) av[3 * l + c] = stencil_r(c, dg, of, W);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if (l < li && own_ok && is_act(l, c)) {
+              const double apv = av[3 * l + c];
+              v5[0] = add(v5[0], mul(pick(p0, c, 0, 0), apv));
+              v5[1] = add(v5[1], mul(R[Oidx(l, c)], apv));
+              v5[2] = add(v5[2], mul(apv, apv));
+              a.ap[own_e(l, c)] = apv;
+            }
+          }
           pm = p0;
           p0 = pp;
         }
       }
-#pragma unroll
-      for (int l = 0; l < LI; ++l)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          if (l < li && own_ok && is_act(l, c)) {
-            const double apv = av[3 * l + c];
-            v5[0] = add(v5[0], mul(P[Pidx(l + 1, c, s_own)], apv));
-            v5[1] = add(v5[1], mul(R[Oidx(l, c)], apv));
-            v5[2] = add(v5[2], mul(apv, apv));
-#if MQ_RES1_APSURF
-            // only the brick surface is anyone's halo
-            if (l == 0 || l == li - 1 || ty == 0 || ty == RTJ - 1 || tx == 0 || tx == RTK - 1)
-#endif
-            a.ap[own_e(l, c)] = apv;  // the neighbours' halo r update
-          }
-        }
-      fstamp(it, 2);
+      fstamp(it, 1);
       // block sums: warp sums to shared memory, lane q of warp 0 adds value
       // q over the 16 warps in order and stores this CTA's partial (only
       // the partials leave the CTA; one CTA barrier)
@@ -835,7 +810,7 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident1_kernel(ResPcgArgs A) {
 #pragma unroll
         for (int q = 0; q < 5; ++q) s5[q] = tot[q];
       }
-      fstamp(it, 3);
+      fstamp(it, 2);
       if (!first) {
         // the previous iteration's stopping test and r.z (krylov.py:239-246)
         rnorm = sqrt(s5[3]);
@@ -849,13 +824,23 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident1_kernel(ResPcgArgs A) {
       const double pap = s5[0];
       if (!isfinite(pap) || pap <= 0.0) { status = MQ_INDEFINITE; iters = it; break; }
       alpha = rz / pap;
-      // ---- K2: x += alpha p, r -= alpha Ap (own), halo r -= alpha Ap ----
+      // beta from the extrapolated r.z of the updated r
+      {
+        const double rr_new = add(sub(s5[3], mul(mul(2.0, alpha), s5[1])), mul(mul(alpha, alpha), s5[2]));
+        const double rz_new = jac ? mul(inv, rr_new) : rr_new;
+        beta = rz_new > 0.0 ? rz_new / rz : 0.0;
+      }
 #if !MQ_RES1_EARLY
       issue_ap_halo();
 #endif
+      // ---- own: x += alpha p, r -= alpha Ap, p = z + beta p, and r.r, r.z
+      // of the new r for the next reduction (the halo work, which waits on
+      // the neighbours' Ap, comes last) ----
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        constexpr int LH = (LI + 1) / 2;
+      for (int q = 0; q < 5; ++q) v5[q] = 0.0;
+#pragma unroll
+      for (int h2 = 0; h2 < (LI + MQ_RES1_LH - 1) / MQ_RES1_LH; ++h2) {
+        constexpr int LH = MQ_RES1_LH;
         double xo[LH * 3], pv[LH * 3], ro[LH * 3];
 #pragma unroll
         for (int l2 = 0; l2 < LH; ++l2)
@@ -874,28 +859,39 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident1_kernel(ResPcgArgs A) {
             const int l = h2 * LH + l2;
             if (!(l < LI && l < li && own_ok && is_act(l, c))) continue;
             X[Oidx(l, c)] = add(xo[3 * l2 + c], mul(alpha, pv[3 * l2 + c]));
-            R[Oidx(l, c)] = sub(ro[3 * l2 + c], mul(alpha, av[3 * l + c]));
+            const double rn = sub(ro[3 * l2 + c], mul(alpha, av[3 * l + c]));
+            R[Oidx(l, c)] = rn;
+            const double z = jac ? mul(inv, rn) : rn;
+            P[Pidx(l + 1, c, s_own)] = add(z, mul(beta, pv[3 * l2 + c]));
+            v5[3] = add(v5[3], mul(rn, rn));
+            v5[4] = add(v5[4], mul(rn, z));
           }
       }
+      // ---- halo: r -= alpha Ap (the owners' update, bit for bit), p = z + beta p
       {
-        double hv[HU][3];
+        double hv[HU][3], ho[HU][3];
 #pragma unroll
         for (int u = 0; u < HU; ++u)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) hv[u][c] = hp[u] >= 0 ? HR[c * NH + hbase + u * hstride] : 0.0;
+          for (int c = 0; c < 3; ++c) {
+            const bool on = (hact >> (3 * u + c)) & 1u;
+            hv[u][c] = on ? HR[c * NH + hbase + u * hstride] : 0.0;
+            ho[u][c] = on ? P[hp[u] + c * RHP] : 0.0;
+          }
 #pragma unroll
         for (int u = 0; u < HU; ++u)
 #pragma unroll
           for (int c = 0; c < 3; ++c)
-            if ((hact >> (3 * u + c)) & 1u) HR[c * NH + hbase + u * hstride] = sub(hv[u][c], mul(alpha, hq[u][c]));
+            if ((hact >> (3 * u + c)) & 1u) {
+              const double rn = sub(hv[u][c], mul(alpha, hq[u][c]));
+              HR[c * NH + hbase + u * hstride] = rn;
+              const double z = jac ? mul(inv, rn) : rn;
+              P[hp[u] + c * RHP] = add(z, mul(beta, ho[u][c]));
+            }
       }
       iters = it;
-      fstamp(it, 4);
-      // beta from the extrapolated r.z of the updated r
-      const double rr_new = add(sub(s5[3], mul(mul(2.0, alpha), s5[1])), mul(mul(alpha, alpha), s5[2]));
-      const double rz_new = jac ? mul(inv, rr_new) : rr_new;
-      beta = rz_new > 0.0 ? rz_new / rz : 0.0;
       first = false;
+      fstamp(it, 3);
     }
     if (status == MQ_OK && !converged) status = MQ_NOT_CONVERGED;
 #pragma unroll

@@ -58,9 +58,9 @@ def main():
               f"{b1[1:].mean()/1e3:.2f}  K2 {k2[1:].mean()/1e3:.2f}  barrier2 {b2[1:].mean()/1e3:.2f}  "
               f"(init {k1[0]/1e3:.2f})")
     if os.environ.get("MQ_TRACE_FINE") and g.pcg_kernel()[0].startswith("pcg_resident1"):
-        # single-reduction kernel: fine stamps 0..4 = start, p done, stencil +
-        # dots + Ap stores done, partial sums read, K2 done; coarse 1/2 =
-        # before / after the barrier
+        # single-reduction kernel: fine stamps 0..3 = loop top, stencil + dots
+        # + Ap stores done, partial sums read, own + halo update done;
+        # coarse 1/2 = before / after the barrier
         import numpy as np
         st = np.zeros(1024, dtype=np.uint64)
         check(lib.mq_pcg_trace(g.ctx, st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), st.size))
@@ -69,11 +69,10 @@ def main():
         rows = []
         for it in range(2, 31):
             f, c = fine[it], coarse[it]
-            rows.append([f[1] - f[0], f[2] - f[1], c[0] - f[2], c[1] - c[0], f[3] - c[1], f[4] - f[3],
-                         fine[it + 1][0] - f[4]])
+            rows.append([f[1] - f[0], c[0] - f[1], c[1] - c[0], f[2] - c[1], f[3] - f[2], fine[it + 1][0] - f[3]])
         r = np.mean(np.array(rows), axis=0) / 1e3
-        names = ["p_own_halo", "stencil_dots_apstore", "bsum5_pstore", "barrier", "psum", "k2_halo", "tail"]
-        print("  fine us: " + "  ".join(f"{n} {v:.2f}" for n, v in zip(names, r)))
+        names = ["sync_stencil_dots", "bsum_pstore", "barrier", "psum", "update_own_halo", "tail"]
+        print("  fine us: " + "  ".join(f"{n} {v:.2f}" for n, v in zip(names, r)) + f"  total {r.sum():.2f}")
     elif os.environ.get("MQ_TRACE_FINE"):
         import numpy as np
         st = np.zeros(1024, dtype=np.uint64)
