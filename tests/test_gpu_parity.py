@@ -742,6 +742,40 @@ def test_resident_pcg_semantics(gpu_ok, sync, monkeypatch):
         assert rep2.iterations == 0 and rep2.applications == 1 and np.array_equal(x2, x)
 
 
+@pytest.mark.parametrize("shape,li", [((33, 64, 64), 3), ((26, 64, 64), 2), ((48, 64, 48), 4),
+                                      ((20, 128, 128), 5)])
+@pytest.mark.parametrize("sync", ["1", "2"])
+def test_resident_pcg_other_brick_depths(gpu_ok, shape, li, sync, monkeypatch):
+    """Non-cubic grids whose resident bricks hold 2, 3, 4 or 5 i-planes (the
+    kernel templates LI; 5 planes only fit the two-barrier kernel) and tiles
+    cut by the grid edge: PCG against the oracle, cold and warm start."""
+    from paper_1611_06721_b200 import PcgConfig, Preconditioner, pcg_solve
+    from paper_1611_06721_b200.device import DeviceGrid, Problem
+    monkeypatch.setenv("MQ_PCG_KERNEL", "resident")
+    monkeypatch.setenv("MQ_PCG_SYNC", sync)
+    mat = np.zeros(shape, np.int8)
+    nx, ny, nz = shape
+    mat[nx // 3:nx // 3 + 6, ny // 3:ny // 3 + 9, nz // 4:nz // 4 + 7] = 1
+    h = 1.0 / max(shape)
+    m = O.assemble(mat, h, O.Conductor(5e6, 3.8, 2.17, 396.2), [])
+    inv = O.jacobi_inverse(m.kn.diagonal())
+    rng = np.random.default_rng(sum(shape))
+    b = m.kn @ rng.standard_normal(m.n_n)
+    x0 = rng.standard_normal(m.n_n) * 1e-3
+    with DeviceGrid(Problem(material=mat, h=h, kappa=5e6, brauer=(3.8, 2.17, 396.2),
+                            pattern=np.zeros(m.n_n))) as g:
+        name, _ = g.pcg_kernel()
+        one = sync == "1" and li <= 4
+        assert name == (f"pcg_resident1_kernel<{li}>" if one else f"pcg_resident_kernel<{li}>"), name
+        for start in (None, x0):
+            x, rep = pcg_solve(g.kn_operator(), b, x0=start,
+                               config=PcgConfig(rel_tol=1e-8, preconditioner=Preconditioner.JACOBI))
+            ref = O.pcg(m.kn_apply, b, x0=start, rel_tol=1e-8, inv_diag=inv)
+            assert rep.converged and abs(rep.iterations - ref.iterations) <= 1
+            assert rep.applications == ref.applies + (rep.iterations - ref.iterations)
+            assert rel(x, ref.x) <= 1e-8
+
+
 @pytest.mark.parametrize("world", [1, 2, 3])
 @pytest.mark.parametrize("x0_given", [False, True])
 def test_slab_pcg_loopback_on_one_gpu(gpu_ok, world, x0_given):

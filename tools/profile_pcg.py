@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--kernel", default=os.environ.get("MQ_PCG_KERNEL", ""))
     ap.add_argument("--spmv", action="store_true", help="also time K_n SpMV launches")
+    ap.add_argument("--zero", action="store_true", help="also time zero-iteration solves")
     args = ap.parse_args()
     if args.kernel:
         os.environ["MQ_PCG_KERNEL"] = args.kernel
@@ -90,6 +91,16 @@ def main():
         names = ["own_p", "halo", "sync", "stencil", "bsum1", "pstore", "bar1", "psum1", "k2loop",
                  "bsum2", "bar2", "psum2"]
         print("  fine us: " + "  ".join(f"{n} {v:.2f}" for n, v in zip(names, r)))
+    if args.zero:
+        # launch cost of a solve that converges at its initial residual (the
+        # SOURCE-family solves of every step): x0 = the solution just found
+        check(lib.mq_pcg_stats(g.ctx, None, None, None, 1))
+        for _ in range(20):
+            rc = lib.mq_pcg_solve_dev(g.ctx, ctypes.c_void_p(b), ctypes.c_void_p(x), ctypes.c_void_p(x), 1e-6,
+                                      0.0, 10, 1, ctypes.byref(rep))
+            check(rc, allow=(0, 1))
+        check(lib.mq_pcg_stats(g.ctx, ctypes.byref(ms), ctypes.byref(it), None, 0))
+        print(f"  zero-iteration solve (x0 exact, iters={rep.iterations}): {1000 * ms.value / 20:.1f} us per launch")
     if args.spmv:
         y = g.alloc()
         lib.mq_timer_start(g.ctx)
