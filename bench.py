@@ -423,7 +423,10 @@ def run_device_arm(args):
     op.grid.close()
     line = None
     if rank == 0:
-        e2e_v, e2e_s, h2d, d2h = time_e2e(problem, spec, args.warmup, args.steps)
+        # a longer host-timed sample than the device leg: a host hiccup in a
+        # 10-step (30 ms) window moved the number by up to 20 %
+        e2e_steps = max(args.steps, 40)
+        e2e_v, e2e_s, h2d, d2h = time_e2e(problem, spec, args.warmup, e2e_steps)
         roof2 = steps2 = roof4 = steps4 = None
         pod1 = cfg_steps(1, warmup=args.warmup, steps=args.steps, strategy="pod")
         if not args.skip_cfg2:
@@ -459,7 +462,7 @@ def run_device_arm(args):
             "roofline_cfg4_1gpu": roof4,
             "cfg4_steps_1gpu": steps4,
             "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "explicit_euler_step + recover_an (host arrays)"},
+                    "api": "explicit_euler_step + recover_an + probe_b (host arrays)", "steps": e2e_steps},
             "gpu_launches": launches,
             "cpu_baseline": cpu,
         }

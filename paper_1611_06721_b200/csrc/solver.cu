@@ -96,6 +96,8 @@ struct SolverHost {
   // per-step log of the current run
   int32_t *d_probe = nullptr, *d_probe_plan = nullptr;
   double *d_probe_vals = nullptr, *d_probe_log = nullptr, *d_probe_leaf = nullptr;
+  unsigned int *d_probe_ctr = nullptr;  // k_probe's last-block ticket
+  int probe_grid = 1;
   int64_t n_probe = 0, probe_cap = 0;
   double *d_probe_out = nullptr;
   // page-locked landing block of the host-facing calls: run status, the two
@@ -106,6 +108,12 @@ struct SolverHost {
     int32_t it[2];
     double probe;
   } *h_st = nullptr;
+  // B probe of the device state, computed by the host-facing recovery call
+  // with its results (same kernel, same state, same cells as mq_probe_b) so
+  // that the probe_b() that follows needs no device round trip; cleared by
+  // every call that writes the state or the probe cells
+  bool probe_cached = false;
+  double probe_cache = 0.0;
 };
 
 static int s_alloc(mq_ctx *ctx, SolverHost *s, void **p, size_t bytes) {
@@ -147,6 +155,7 @@ void solver_free(mq_ctx *ctx) {
   cudaFree(s->d_probe_log);
   cudaFree(s->d_probe_plan);
   cudaFree(s->d_probe_leaf);
+  cudaFree(s->d_probe_ctr);
   if (s->h_st) cudaFreeHost(s->h_st);
   delete s;
   ctx->solver = nullptr;
@@ -951,36 +960,47 @@ __global__ void k_cell_nu(CondArgs a, const double *__restrict__ state, double *
 // arrays split at an 8-aligned half.  The split tree depends only on n, so
 // the host builds it once (probe_plan): leaves are summed in parallel, then
 // one thread combines them in the tree's postfix order.
-__device__ double np_leaf_sum(const double *v, int n) {
+// (values written by other blocks: L2 loads)
+__device__ double np_leaf_sum_cg(const double *v, int n) {
   if (n < 8) {
     double r = 0.0;
-    for (int i = 0; i < n; ++i) r = add(r, v[i]);
+    for (int i = 0; i < n; ++i) r = add(r, __ldcg(v + i));
     return r;
   }
   double r[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = v[j];
+  for (int j = 0; j < 8; ++j) r[j] = __ldcg(v + j);
   int i = 8;
   for (; i < n - (n % 8); i += 8)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = add(r[j], v[i + j]);
+    for (int j = 0; j < 8; ++j) r[j] = add(r[j], __ldcg(v + i + j));
   double res = add(add(add(r[0], r[1]), add(r[2], r[3])), add(add(r[4], r[5]), add(r[6], r[7])));
-  for (; i < n; ++i) res = add(res, v[i]);
+  for (; i < n; ++i) res = add(res, __ldcg(v + i));
   return res;
 }
 
-// B_probe = mean(sqrt(b2[cells])) (model.py:415-425); one block.  plan =
-// [n_leaves, n_prog, (start, len) per leaf, postfix program (leaf index or
-// -1 = add)].  The value goes to log[par->step - 1] inside a run, else to *out.
+// B_probe = mean(sqrt(b2[cells])) (model.py:415-425).  Every block computes
+// |B| of a strided share of the cells; the last block to finish (ticket)
+// sums the leaves in parallel and runs the tree.  plan = [n_leaves, n_prog,
+// (start, len) per leaf, postfix program (leaf index or -1 = add)].  The value
+// goes to log[par->step - 1] inside a run, else to *out.
 __global__ void k_probe(CondArgs a, const int32_t *__restrict__ cells, int64_t n, const int32_t *__restrict__ plan,
                         const double *__restrict__ state, double *__restrict__ vals, double *__restrict__ leaf,
-                        const StepParams *par, double *log, double *out) {
-  for (int64_t q = threadIdx.x; q < n; q += blockDim.x) vals[q] = sqrt(cell_b2(a, cells[q], state));
+                        unsigned int *ctr, const StepParams *par, double *log, double *out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    vals[q] = sqrt(cell_b2(a, cells[q], state));
+  __shared__ bool is_last;
+  __threadfence();
   __syncthreads();
+  if (threadIdx.x == 0) is_last = (atomicAdd(ctr, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
   const int nl = plan[0], np = plan[1];
-  for (int t = threadIdx.x; t < nl; t += blockDim.x) leaf[t] = np_leaf_sum(vals + plan[2 + 2 * t], plan[3 + 2 * t]);
+  for (int t = threadIdx.x; t < nl; t += blockDim.x) leaf[t] = np_leaf_sum_cg(vals + plan[2 + 2 * t], plan[3 + 2 * t]);
   __syncthreads();
   if (threadIdx.x != 0) return;
+  *ctr = 0u;
   double st[64];
   int sp = 0;
   for (int i = 0; i < np; ++i) {
@@ -1741,6 +1761,7 @@ int mq_solver_reset(mq_ctx *ctx) {
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
   MQ_CUDA(cudaMemsetAsync(s->d_fam, 0, sizeof(FamDev) * 3, ctx->stream));
   for (bool &m : s->maybe_pending) m = false;  // the memset cleared any deferred insert
+  s->probe_cached = false;
   return init_run(ctx);
 }
 
@@ -1896,6 +1917,7 @@ int mq_mc_diag(mq_ctx *ctx, double *mc_diag) {
 
 int mq_state_set(mq_ctx *ctx, const double *a_c, double t) {
   const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
+  if (ctx->solver) ctx->solver->probe_cached = false;
   if (a_c) MQ_CUDA(cudaMemcpyAsync(ctx->d_ac, a_c, sizeof(double) * n_c, cudaMemcpyHostToDevice, ctx->stream));
   else MQ_CUDA(cudaMemsetAsync(ctx->d_ac, 0, sizeof(double) * n_c, ctx->stream));
   ctx->t_now = t;
@@ -1966,6 +1988,7 @@ static int euler_call(mq_ctx *ctx, const double *a_c_in, double t, double dt, do
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
   if (dt < 0) { set_error("dt must be nonnegative"); return MQ_INVALID; }
+  s->probe_cached = false;
   {
     const int frc = flush_deferred(ctx, host_defer(s) ? 1u << MQ_FAM_COUPLING_CURRENT : 0u);
     if (frc) return frc;
@@ -2002,6 +2025,7 @@ static int recover_call(mq_ctx *ctx, const double *a_c_in, double t, double wave
                         mq_solve_report *rep_src, mq_solve_report *rep_cpl) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  s->probe_cached = false;
   {
     const int frc = flush_deferred(ctx, host_defer(s) ? 1u << MQ_FAM_COUPLING_PREVIOUS : 0u);
     if (frc) return frc;
@@ -2036,9 +2060,21 @@ static int recover_call(mq_ctx *ctx, const double *a_c_in, double t, double wave
     ctx->launches += 1;
     MQ_CUDA(cudaMemcpyAsync(a_n_host, ctx->d_stage, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
   }
+  const bool probe = s->n_probe > 0;
+  if (probe) {
+    k_probe<<<s->probe_grid, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, s->d_probe_plan,
+                                                    ctx->d_ac, s->d_probe_vals, s->d_probe_leaf, s->d_probe_ctr,
+                                                    nullptr, nullptr, s->d_probe_out);
+    LAUNCH_CHECK();
+    MQ_CUDA(cudaMemcpyAsync(&s->h_st->probe, s->d_probe_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  }
   MQ_CUDA(cudaStreamSynchronize(ctx->stream));
   rc = staged_run_status(ctx, nullptr);
   staged_report(ctx, rep_src, rep_cpl);
+  if (probe && rc == MQ_OK) {
+    s->probe_cache = s->h_st->probe;
+    s->probe_cached = true;
+  }
   return rc;
 }
 
@@ -2094,8 +2130,9 @@ static int enqueue_step(mq_ctx *ctx, double *hist) {
     if (defer) s->maybe_pending[MQ_FAM_COUPLING_CURRENT] = true;
   }
   if (s->n_probe > 0) {
-    k_probe<<<1, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, s->d_probe_plan, ctx->d_ac,
-                                        s->d_probe_vals, s->d_probe_leaf, s->d_par, s->d_probe_log, nullptr);
+    k_probe<<<s->probe_grid, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, s->d_probe_plan,
+                                                    ctx->d_ac, s->d_probe_vals, s->d_probe_leaf, s->d_probe_ctr,
+                                                    s->d_par, s->d_probe_log, nullptr);
     MQ_CUDA(cudaGetLastError());
     ctx->launches += 1;
   }
@@ -2122,6 +2159,7 @@ static void probe_plan(int64_t off, int64_t n, std::vector<int32_t> &leaves, std
 int mq_probe_set(mq_ctx *ctx, const int64_t *cells, int64_t n) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  s->probe_cached = false;
   if (n < 0 || (n > 0 && !cells)) { set_error("invalid probe cell list"); return MQ_INVALID; }
   const std::vector<int64_t> &ids = ctx->topo.cell_ids;
   std::vector<int32_t> loc((size_t)n);
@@ -2137,7 +2175,9 @@ int mq_probe_set(mq_ctx *ctx, const int64_t *cells, int64_t n) {
   cudaFree(s->d_probe_vals);
   cudaFree(s->d_probe_plan);
   cudaFree(s->d_probe_leaf);
+  cudaFree(s->d_probe_ctr);
   s->d_probe = nullptr;
+  s->d_probe_ctr = nullptr;
   s->d_probe_vals = s->d_probe_leaf = nullptr;
   s->d_probe_plan = nullptr;
   s->n_probe = 0;
@@ -2152,6 +2192,9 @@ int mq_probe_set(mq_ctx *ctx, const int64_t *cells, int64_t n) {
     MQ_CUDA(cudaMalloc(&s->d_probe_vals, sizeof(double) * n));
     MQ_CUDA(cudaMalloc(&s->d_probe_leaf, sizeof(double) * (leaves.size() / 2)));
     MQ_CUDA(cudaMalloc(&s->d_probe_plan, sizeof(int32_t) * plan.size()));
+    MQ_CUDA(cudaMalloc(&s->d_probe_ctr, sizeof(unsigned int)));
+    MQ_CUDA(cudaMemset(s->d_probe_ctr, 0, sizeof(unsigned int)));
+    s->probe_grid = (int)std::min<int64_t>((n + 255) / 256, ctx->sms);
     MQ_CUDA(cudaMemcpy(s->d_probe, loc.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
     MQ_CUDA(cudaMemcpy(s->d_probe_plan, plan.data(), sizeof(int32_t) * plan.size(), cudaMemcpyHostToDevice));
   }
@@ -2164,14 +2207,19 @@ int mq_probe_b(mq_ctx *ctx, const double *a_c_host, double *out) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
   if (s->n_probe <= 0) { set_error("probe cell set is empty"); return MQ_INVALID; }
+  if (!a_c_host && s->probe_cached) {
+    *out = s->probe_cache;
+    return MQ_OK;
+  }
   const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
   const double *state = ctx->d_ac;
   if (a_c_host) {
     MQ_CUDA(cudaMemcpyAsync(ctx->d_ac_x, a_c_host, sizeof(double) * n_c, cudaMemcpyHostToDevice, ctx->stream));
     state = ctx->d_ac_x;
   }
-  k_probe<<<1, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, s->d_probe_plan, state,
-                                      s->d_probe_vals, s->d_probe_leaf, nullptr, nullptr, s->d_probe_out);
+  k_probe<<<s->probe_grid, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, s->d_probe_plan, state,
+                                                  s->d_probe_vals, s->d_probe_leaf, s->d_probe_ctr, nullptr, nullptr,
+                                                  s->d_probe_out);
   LAUNCH_CHECK();
   MQ_CUDA(cudaMemcpyAsync(&s->h_st->probe, s->d_probe_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   MQ_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -2192,6 +2240,7 @@ int mq_run_prepare(mq_ctx *ctx, int64_t n_steps, const double *dt, const double 
                    int32_t recover_every_step) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  s->probe_cached = false;
   if (n_steps < 0) { set_error("n_steps must be nonnegative"); return MQ_INVALID; }
   {
     // a host call's deferred insert: the coupling-current one is absorbed by
@@ -2323,6 +2372,7 @@ int mq_estimate_cfl(mq_ctx *ctx, const double *a_ref, const double *v0, int32_t 
                     int32_t *used_out, int64_t *pcg_applies) {
   if (!(safety > 0.0 && safety <= 1.0)) { set_error("safety must lie in (0, 1]"); return MQ_INVALID; }
   if (power_iters < 1) { set_error("power_iters must be at least 1"); return MQ_INVALID; }
+  if (ctx->solver) ctx->solver->probe_cached = false;
   const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
   const Lay &L = ctx->topo.L;
   CondArgs a = cond_args(ctx);

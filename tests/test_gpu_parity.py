@@ -590,6 +590,39 @@ def test_host_step_api_matches_device_loop(gpu_ok):
     op.grid.close()
 
 
+def test_probe_after_host_calls(gpu_ok):
+    """probe_b() after a host recovery call returns the value that call
+    computed with its results (no device round trip); after an Euler call,
+    a state upload or new probe cells it is computed afresh.  Every value
+    equals probe_b(state) on the same state bit for bit."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, SchurOperator, explicit_euler_step, recover_an
+    spec = C.config_spec(0)
+    op = SchurOperator(C.make_problem(0), pcg=PcgConfig(rel_tol=1e-8), strategy="cspe", max_cols=5)
+    op.set_probe()
+    a, t = np.zeros(op.grid.n_c), 0.0
+    recover_an(op, a, t)
+    for s in range(4):
+        a, _ = explicit_euler_step((a, t), spec.dt, op, s + 1)
+        t += spec.dt
+        after_euler = op.probe_b()
+        assert after_euler == op.probe_b(a)
+        recover_an(op, a, t)
+        cached = op.probe_b()
+        assert cached == op.probe_b(a) == after_euler and cached > 0.0
+    other = np.random.default_rng(5).standard_normal(op.grid.n_c)
+    recover_an(op, a, t)
+    assert op.probe_b() == op.probe_b(a)
+    op._set_state(other, t)                        # the device state changed: recomputed
+    assert op.probe_b() == op.probe_b(other) != op.probe_b(a)
+    recover_an(op, a, t)
+    cells = op.set_probe(op.probe_cells[:3])       # new cells: recomputed
+    assert cells.size == 3 and op.probe_b(a) == op.probe_b(a)
+    recover_an(op, a, t)
+    assert op.probe_b() == op.probe_b(a)
+    op.grid.close()
+
+
 @pytest.mark.slow
 def test_config2_first_steps_vs_oracle(gpu_ok):
     """configs[2] (128^3, two iron blocks, POD-30, TMA brick PCG): the first

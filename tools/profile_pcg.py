@@ -99,8 +99,18 @@ def main():
             rc = lib.mq_pcg_solve_dev(g.ctx, ctypes.c_void_p(b), ctypes.c_void_p(x), ctypes.c_void_p(x), 1e-6,
                                       0.0, 10, 1, ctypes.byref(rep))
             check(rc, allow=(0, 1))
-        check(lib.mq_pcg_stats(g.ctx, ctypes.byref(ms), ctypes.byref(it), None, 0))
+        ms0, it0 = ctypes.c_double(), ctypes.c_int64()
+        check(lib.mq_pcg_stats(g.ctx, ctypes.byref(ms0), ctypes.byref(it0), None, 0))
+        ms = ms0
         print(f"  zero-iteration solve (x0 exact, iters={rep.iterations}): {1000 * ms.value / 20:.1f} us per launch")
+        if os.environ.get("MQ_TRACE_FINE") and os.environ.get("MQ_PCG_TRACE"):
+            import numpy as np
+            st = np.zeros(320, dtype=np.uint64)
+            check(lib.mq_pcg_trace(g.ctx, st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), st.size))
+            t = st[[0, 301, 302, 303, 304, 305, 306]].astype(np.float64)
+            d = np.diff(t) / 1e3
+            names = ["residual", "bsum_pstore", "barrier", "psum", "halo_r", "tail"]
+            print("  init us (CTA 0, last launch): " + "  ".join(f"{n} {v:.2f}" for n, v in zip(names, d)))
     if args.spmv:
         y = g.alloc()
         lib.mq_timer_start(g.ctx)
