@@ -149,6 +149,13 @@ def dist_init():
     if world > 1:
         import torch
         import torch.distributed as dist
+        if os.environ.get("MQ_BENCH_PLUMBING_TEST"):
+            # functional check of the multi-rank path on a one-GPU box (every
+            # rank on cuda:0, gloo): never a measurement
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+            return world, rank, local, dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         return world, rank, local, dist
@@ -159,7 +166,8 @@ def max_over_ranks(x: float, dist, local):
     if dist is None:
         return x
     import torch
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dev = "cpu" if dist.get_backend() == "gloo" else f"cuda:{local}"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -57,6 +57,7 @@ int ctx_pcg(mq_ctx *ctx, const double *b, double *x, int x0_mode, double rel_tol
   a.pa = ctx->d_p0;
   a.pb = ctx->d_p1;
   a.ap = ctx->d_ap;
+  a.ap2 = ctx->d_ap2;
   a.rel_tol = rel_tol;
   a.abs_tol = abs_tol;
   a.max_iter = max_iter;
@@ -185,6 +186,10 @@ int mq_ctx_create(const mq_grid_desc *desc, int32_t device, mq_ctx **out) {
   if (!rc) rc = pcg_stencil_grid(t.L.words, &ctx->pcg_grid);
   if (!rc) rc = brick_pcg_setup(t.L, t.nx, t.ny, t.nz, 0, &ctx->brick_grid, &ctx->geo);
   if (!rc) rc = resident_pcg_setup(t.nx, t.ny, t.nz, &ctx->res_grid, &ctx->res_geo);
+  // Ap of odd iterations: the single-reduction resident kernel publishes Ap
+  // double-buffered (a CTA's next Ap must not overwrite the values a slower
+  // neighbour still has to load after the barrier)
+  if (!rc && ctx->res_grid > 0) rc = ctx_alloc(ctx, (void **)&ctx->d_ap2, sizeof(double) * t.L.total);
   {
     // default: shared-memory-resident kernel when the bricks fit on chip,
     // else the TMA brick kernel; MQ_PCG_KERNEL=simple|brick|resident overrides

@@ -76,6 +76,7 @@ struct mq_ctx {
   double *d_stage = nullptr;
   // PCG scratch
   double *d_r = nullptr, *d_p0 = nullptr, *d_p1 = nullptr, *d_ap = nullptr;
+  double *d_ap2 = nullptr;  // Ap of odd iterations (pcg_resident1_kernel)
   double *d_tmp0 = nullptr, *d_tmp1 = nullptr;
   double *d_partials = nullptr;
   mq::GridBar *d_bar = nullptr;

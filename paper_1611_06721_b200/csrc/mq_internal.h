@@ -64,6 +64,7 @@ struct StencilPcgArgs {
   const int *x0_mode_dev;      // optional: device-chosen start mode
   const unsigned int *err_word;  // optional: skip the solve if set
   unsigned long long *trace;   // optional: %globaltimer stamps (CTA 0) per phase
+  double *ap2;                 // second Ap buffer (pcg_resident1_kernel publishes Ap double-buffered)
 };
 
 // Brick decomposition of the node box [0,nx) x [0,ny) x [0,nz) (pcg_brick.cu)

@@ -702,12 +702,17 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident1_kernel(ResPcgArgs A) {
     // the neighbours' published Ap at this thread's active halo slots, all
     // loads in flight before the first use (one L2 round trip)
     double hq[HU][3];
+    // Ap of iteration it goes to buffer it & 1: a CTA writes Ap_{it+1} before
+    // the barrier of it+1, possibly while a slower neighbour is still to load
+    // Ap_it after the barrier of it; Ap_{it+2} is written only after every
+    // CTA passed the barrier of it+1, i.e. after all loads of Ap_it
+    const double *apb = a.ap;
     auto issue_ap_halo = [&]() {
 #pragma unroll
       for (int u = 0; u < HU; ++u)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-          hq[u][c] = ((hact >> (3 * u + c)) & 1u) ? __ldcg(a.ap + he[u] + c * L.C) : 0.0;
+          hq[u][c] = ((hact >> (3 * u + c)) & 1u) ? __ldcg(apb + he[u] + c * L.C) : 0.0;
     };
     // p_0 = z_0 (own and halo); r.r and r.z of r_0 ride on the first
     // reduction (krylov.py:228-230)
@@ -736,6 +741,8 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident1_kernel(ResPcgArgs A) {
         }
     for (int it = 1;; ++it) {
       fstamp(it, 0);
+      double *const apw = (it & 1) ? a.ap2 : a.ap;
+      apb = apw;
       __syncthreads();
       // ---- Ap = K_n p from shared memory; partials p.Ap, r.Ap, Ap.Ap per
       // plane as the march passes it; Ap published for the neighbours' halo
@@ -757,7 +764,7 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident1_kernel(ResPcgArgs A) {
               v5[0] = add(v5[0], mul(pick(p0, c, 0, 0), apv));
               v5[1] = add(v5[1], mul(R[Oidx(l, c)], apv));
               v5[2] = add(v5[2], mul(apv, apv));
-              a.ap[own_e(l, c)] = apv;
+              apw[own_e(l, c)] = apv;
             }
           }
           pm = p0;
@@ -1003,7 +1010,7 @@ int launch_pcg_resident(const StencilPcgArgs &args, const BrickGeo &geo, int gri
   A.g.chunks = geo.chunks;
   A.g.nbricks = geo.nbricks;
   A.g.li_max = (geo.nx + geo.chunks - 1) / geo.chunks;
-  const bool one = use_resident1(A.g.li_max);
+  const bool one = use_resident1(A.g.li_max) && args.ap2 != nullptr;
   const size_t smem = one ? res1_smem_bytes(A.g.li_max) : res_smem_bytes(A.g.li_max);
   MQ_CUDA(cudaMemsetAsync(&args.bar->count, 0, sizeof(unsigned long long), s));
   void *params[] = {&A};
