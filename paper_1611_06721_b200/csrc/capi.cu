@@ -58,6 +58,7 @@ int ctx_pcg(mq_ctx *ctx, const double *b, double *x, int x0_mode, double rel_tol
   a.pb = ctx->d_p1;
   a.ap = ctx->d_ap;
   a.ap2 = ctx->d_ap2;
+  a.stress_ns = pcg_stress_ns();
   a.rel_tol = rel_tol;
   a.abs_tol = abs_tol;
   a.max_iter = max_iter;

@@ -155,6 +155,9 @@ int launch_pcg_ctx(mq_ctx *ctx, const StencilPcgArgs &args);
 int resident_pcg_setup(int nx, int ny, int nz, int *grid, BrickGeo *geo);
 int launch_pcg_resident(const StencilPcgArgs &args, const BrickGeo &geo, int grid, cudaStream_t s);
 bool resident_single_reduction(int li_max);
+// MQ_PCG_STRESS=<ns>: test-only delay of some CTAs after every grid barrier of
+// the resident kernels (results must not change: they depend on no timing)
+int pcg_stress_ns();
 int launch_kn_apply(const Lay &L, const uint32_t *mask, double dg, double of, const double *x, double *y, int sms,
                     cudaStream_t s);
 int launch_scatter(int64_t n, const int32_t *idx, const double *src, double *dst, int sms, cudaStream_t s);

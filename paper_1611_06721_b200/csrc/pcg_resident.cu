@@ -28,6 +28,12 @@ constexpr int RW = RT / 32;                              // 16 warps
 constexpr int RRING = 2 * RHK + 2 * RTJ;                 // 100 ring positions per plane
 constexpr int RLI_MAX = 5;                               // planes per brick that fit
 
+// test-only: a pseudo-random subset of CTAs sleeps right after a grid barrier
+// (MQ_PCG_STRESS; the results depend on no timing and must not change)
+__device__ __forceinline__ void stress_after_barrier(int ns, int it) {
+  if (ns && ((blockIdx.x * 37 + it * 11) % 29 == 0)) __nanosleep((unsigned)ns);
+}
+
 struct ResGeo {
   int nx, ny, nz;
   int tiles_k, tiles_j, chunks, nbricks, li_max;
@@ -411,6 +417,7 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
       stamp(4 * (it - 1) + 1);
       if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
       stamp(4 * (it - 1) + 2);
+      stress_after_barrier(a.stress_ns, 2 * it);
       double s1[1];
       grid_partials_sum_all<1, 5>(a.partials + 3 * G, G, s1, tot);
       const double pap = s1[0];
@@ -442,6 +449,7 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident_kernel(ResPcgArgs A) {
       stamp(4 * (it - 1) + 3);
       if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
       stamp(4 * (it - 1) + 4);
+      stress_after_barrier(a.stress_ns, 2 * it + 1);
       double s2[2];
       grid_partials_sum_all<2, 5>(a.partials + 4 * G, G, s2, tot);
       rnorm = sqrt(s2[0]);
@@ -741,7 +749,11 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident1_kernel(ResPcgArgs A) {
         }
     for (int it = 1;; ++it) {
       fstamp(it, 0);
+#ifdef MQ_RES1_AP_SINGLE  // the racy single buffer, for the stress test's negative control only
+      double *const apw = a.ap;
+#else
       double *const apw = (it & 1) ? a.ap2 : a.ap;
+#endif
       apb = apw;
       __syncthreads();
       // ---- Ap = K_n p from shared memory; partials p.Ap, r.Ap, Ap.Ap per
@@ -791,6 +803,7 @@ __global__ void __launch_bounds__(RT, 1) pcg_resident1_kernel(ResPcgArgs A) {
       stamp(4 * (it - 1) + 1);
       if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
       stamp(4 * (it - 1) + 2);
+      stress_after_barrier(a.stress_ns, it);
       double s5[5];
 #if MQ_RES1_EARLY
       issue_ap_halo();
@@ -952,6 +965,12 @@ static const void *resident_kernel_for(int li_max) {
 }
 
 bool resident_single_reduction(int li_max) { return use_resident1(li_max); }
+
+int pcg_stress_ns() {
+  const char *v = getenv("MQ_PCG_STRESS");
+  const int ns = v ? atoi(v) : 0;
+  return ns > 0 ? (ns < 1000000 ? ns : 1000000) : 0;
+}
 
 // Returns 0 with *grid = 0 when the grid does not fit the resident scheme.
 int resident_pcg_setup(int nx, int ny, int nz, int *grid, BrickGeo *geo_out) {

@@ -1380,6 +1380,7 @@ static int solve_enqueue(mq_ctx *ctx, int fam, const double *rhs, double *y, boo
   a.pb = ctx->d_p1;
   a.ap = ctx->d_ap;
   a.ap2 = ctx->d_ap2;
+  a.stress_ns = pcg_stress_ns();
   a.rel_tol = s->cfg.rel_tol;
   a.abs_tol = s->cfg.abs_tol;
   a.max_iter = s->cfg.max_iter;

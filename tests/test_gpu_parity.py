@@ -775,6 +775,35 @@ def test_resident_pcg_semantics(gpu_ok, sync, monkeypatch):
         assert rep2.iterations == 0 and rep2.applications == 1 and np.array_equal(x2, x)
 
 
+@pytest.mark.parametrize("sync", ["1", "2"])
+def test_resident_pcg_barrier_stress(gpu_ok, sync, monkeypatch):
+    """Race check of the resident kernels' halo exchange: with MQ_PCG_STRESS a
+    pseudo-random subset of CTAs sleeps 20 us after every grid barrier, so
+    their neighbours run ahead into the next iteration's publication.  The
+    solve depends on no timing: x and the iteration count are bit-identical
+    to the unstressed solve (the single-reduction kernel once overwrote the
+    Ap a delayed neighbour still had to load)."""
+    from paper_1611_06721_b200 import PcgConfig, Preconditioner, pcg_solve
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200.device import DeviceGrid
+    monkeypatch.setenv("MQ_PCG_KERNEL", "resident")
+    monkeypatch.setenv("MQ_PCG_SYNC", sync)
+    prob = C.make_problem(1)
+    with DeviceGrid(prob) as g:
+        op = g.kn_operator()
+        rng = np.random.default_rng(11)
+        b = g.kn_apply(rng.standard_normal(g.n_n))
+        x0 = rng.standard_normal(g.n_n) * 1e-3
+        cfg = PcgConfig(rel_tol=1e-8, preconditioner=Preconditioner.JACOBI)
+        for start in (None, x0):
+            monkeypatch.delenv("MQ_PCG_STRESS", raising=False)
+            x, rep = pcg_solve(op, b, x0=start, config=cfg)
+            monkeypatch.setenv("MQ_PCG_STRESS", "20000")
+            xs, reps = pcg_solve(op, b, x0=start, config=cfg)
+            assert rep.converged and reps.iterations == rep.iterations
+            assert np.array_equal(xs, x)
+
+
 @pytest.mark.parametrize("shape,li", [((33, 64, 64), 3), ((26, 64, 64), 2), ((48, 64, 48), 4),
                                       ((20, 128, 128), 5)])
 @pytest.mark.parametrize("sync", ["1", "2"])
