@@ -208,6 +208,12 @@ __device__ __forceinline__ bool grid_sync(GridBar *bar) {
   return s_fail == 0;
 }
 
+// test-only: a pseudo-random subset of CTAs sleeps right after a grid barrier
+// (MQ_PCG_STRESS; the results depend on no timing and must not change)
+__device__ __forceinline__ void stress_after_barrier(int ns, int it) {
+  if (ns && ((blockIdx.x * 37 + it * 11) % 29 == 0)) __nanosleep((unsigned)ns);
+}
+
 // ---- the K_n stencil -------------------------------------------------------
 // Row of K_n = (nu0/h) * S at padded index e of component c, evaluated as the
 // CSR row sum in ascending column order with separately rounded products and

@@ -436,6 +436,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
 #endif
       if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
       stamp(4 * (it - 1) + 2);
+      stress_after_barrier(a.stress_ns, 2 * it);
       double s1[1];
       grid_partials_sum<1>(a.partials + 3 * G, G, s1, tot);
       const double pap = s1[0];
@@ -472,6 +473,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       stamp(4 * (it - 1) + 3);
       if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
       stamp(4 * (it - 1) + 4);
+      stress_after_barrier(a.stress_ns, 2 * it + 1);
       if (threadIdx.x == 0) fence_proxy_async_global();
       double s2[2];
       grid_partials_sum<2>(a.partials + 4 * G, G, s2, tot);

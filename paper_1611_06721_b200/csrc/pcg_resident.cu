@@ -28,12 +28,6 @@ constexpr int RW = RT / 32;                              // 16 warps
 constexpr int RRING = 2 * RHK + 2 * RTJ;                 // 100 ring positions per plane
 constexpr int RLI_MAX = 5;                               // planes per brick that fit
 
-// test-only: a pseudo-random subset of CTAs sleeps right after a grid barrier
-// (MQ_PCG_STRESS; the results depend on no timing and must not change)
-__device__ __forceinline__ void stress_after_barrier(int ns, int it) {
-  if (ns && ((blockIdx.x * 37 + it * 11) % 29 == 0)) __nanosleep((unsigned)ns);
-}
-
 struct ResGeo {
   int nx, ny, nz;
   int tiles_k, tiles_j, chunks, nbricks, li_max;

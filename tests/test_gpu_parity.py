@@ -775,9 +775,9 @@ def test_resident_pcg_semantics(gpu_ok, sync, monkeypatch):
         assert rep2.iterations == 0 and rep2.applications == 1 and np.array_equal(x2, x)
 
 
-@pytest.mark.parametrize("sync", ["1", "2"])
-def test_resident_pcg_barrier_stress(gpu_ok, sync, monkeypatch):
-    """Race check of the resident kernels' halo exchange: with MQ_PCG_STRESS a
+@pytest.mark.parametrize("kernel,sync", [("resident", "1"), ("resident", "2"), ("brick", "2")])
+def test_pcg_barrier_stress(gpu_ok, kernel, sync, monkeypatch):
+    """Race check of the persistent kernels' halo exchange: with MQ_PCG_STRESS a
     pseudo-random subset of CTAs sleeps 20 us after every grid barrier, so
     their neighbours run ahead into the next iteration's publication.  The
     solve depends on no timing: x and the iteration count are bit-identical
@@ -786,10 +786,11 @@ def test_resident_pcg_barrier_stress(gpu_ok, sync, monkeypatch):
     from paper_1611_06721_b200 import PcgConfig, Preconditioner, pcg_solve
     from paper_1611_06721_b200 import configs as C
     from paper_1611_06721_b200.device import DeviceGrid
-    monkeypatch.setenv("MQ_PCG_KERNEL", "resident")
+    monkeypatch.setenv("MQ_PCG_KERNEL", kernel)
     monkeypatch.setenv("MQ_PCG_SYNC", sync)
     prob = C.make_problem(1)
     with DeviceGrid(prob) as g:
+        assert g.pcg_kernel()[0].startswith({"resident": "pcg_resident", "brick": "pcg_tma"}[kernel])
         op = g.kn_operator()
         rng = np.random.default_rng(11)
         b = g.kn_apply(rng.standard_normal(g.n_n))
