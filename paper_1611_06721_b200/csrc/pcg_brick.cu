@@ -704,6 +704,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_slab_kernel(const __grid_co
       }
       ++applies;
       if (!rank_allreduce<1>(me, R, rank, lb, Gr, inst++, v1, red, tot)) { status = MQ_CUDA_ERROR; goto done; }
+      stress_after_barrier(a.stress_ns, 2 * it);
       const double pap = v1[0];
       if (!isfinite(pap) || pap <= 0.0) { status = MQ_INDEFINITE; iters = it; goto done; }
       alpha = rz / pap;
@@ -732,6 +733,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_slab_kernel(const __grid_co
       });
       push_planes_group(me, r, me.lo_r, me.hi_r, lb, Gr);
       if (!rank_allreduce<2>(me, R, rank, lb, Gr, inst++, v2, red, tot)) { status = MQ_CUDA_ERROR; goto done; }
+      stress_after_barrier(a.stress_ns, 2 * it + 1);
       if (threadIdx.x == 0) fence_proxy_async_global();
       rnorm = sqrt(v2[0]);
       iters = it;

@@ -338,6 +338,7 @@ int mq_slab_fused_solve_local(mq_ctx **ctxs, int32_t nranks, const double *const
       t.pb = c->d_p1;
       t.ap = c->d_ap;
       t.rel_tol = rel_tol;
+      t.stress_ns = pcg_stress_ns();
       t.abs_tol = abs_tol;
       t.max_iter = max_iter;
       t.partials = c->d_partials;
@@ -474,6 +475,7 @@ int mq_slab_fused_solve_peer(mq_ctx *ctx, const double *b, int32_t x0_given, dou
   t.pb = ctx->d_p1;
   t.ap = ctx->d_ap;
   t.rel_tol = rel_tol;
+  t.stress_ns = pcg_stress_ns();
   t.abs_tol = abs_tol;
   t.max_iter = max_iter;
   t.partials = ctx->d_partials;

@@ -906,6 +906,40 @@ def test_fused_slab_pcg_on_one_gpu(gpu_ok, world, x0_given):
         s.close()
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_slab_barrier_stress(gpu_ok, world, monkeypatch):
+    """The fused slab kernel with some CTAs of every rank group delayed after
+    each rank all-reduce (MQ_PCG_STRESS): ghost stores into the neighbours'
+    slabs and the mailbox protocol depend on no timing, so x and the
+    iteration count are bit-identical to the unstressed solve."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200.slab import SlabGrid, fused_slab_pcg_solve_local
+    spec, m = oracle_model(0)
+    prob = C.make_problem(0)
+    slabs = [SlabGrid(prob, r, world) for r in range(world)]
+    idx = [np.searchsorted(m.noncond_global, s.partition()) for s in slabs]
+    rng = np.random.default_rng(19)
+    b = m.kn @ rng.standard_normal(m.n_n)
+    out = []
+    for stress in (None, "20000"):
+        if stress:
+            monkeypatch.setenv("MQ_PCG_STRESS", stress)
+        else:
+            monkeypatch.delenv("MQ_PCG_STRESS", raising=False)
+        for s, ix in zip(slabs, idx):
+            s.upload(b[ix], s.b)
+            s.upload(np.zeros(ix.size), s.x)
+        it, relres, conv, app = fused_slab_pcg_solve_local(slabs, x0_given=False, rel_tol=1e-8)
+        x = np.zeros(m.n_n)
+        for s, ix in zip(slabs, idx):
+            x[ix] = s.download(s.x)
+        assert conv
+        out.append((it, x))
+    assert out[0][0] == out[1][0] and np.array_equal(out[0][1], out[1][1])
+    for s in slabs:
+        s.close()
+
+
 def test_fused_slab_peer_path_single_rank(gpu_ok):
     """The one-rank-per-process entry points (IPC export/import, the kernel
     launched as a single CTA group) at one rank: same answer as the oracle.
