@@ -557,6 +557,33 @@ def test_overlapped_source_update(gpu_ok, monkeypatch):
     assert np.array_equal(runs["1", True].basis_cols, runs["0", True].basis_cols)
 
 
+@pytest.mark.parametrize("strategy", ["cspe", "pod"])
+def test_step_graph_under_barrier_stress(gpu_ok, strategy, monkeypatch):
+    """64^3 step graphs (resident PCG on the main stream, cache updates forked
+    onto the side stream under it, deferred inserts) with the PCG kernels'
+    CTAs delayed after every grid barrier (MQ_PCG_STRESS): the side-stream
+    work now overlaps different parts of the solves, yet the trajectory,
+    iteration counts and basis sizes are bit-identical to the unstressed run
+    (the fork/join edges order every shared buffer)."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, run_explicit
+    spec = C.config_spec(1)
+    runs = []
+    for stress in (None, "20000"):
+        if stress:
+            monkeypatch.setenv("MQ_PCG_STRESS", stress)
+        else:
+            monkeypatch.delenv("MQ_PCG_STRESS", raising=False)
+        runs.append(run_explicit(C.make_problem(1), t_end=6 * spec.dt, dt=spec.dt, strategy=strategy,
+                                 pcg=PcgConfig(rel_tol=1e-8), max_cols=5, n_pod=20,
+                                 output_period=spec.dt * (1 - 1e-3)))
+    assert np.array_equal(runs[0].final_a_c, runs[1].final_a_c)
+    assert np.array_equal(runs[0].final_a_n, runs[1].final_a_n)
+    assert np.array_equal(runs[0].step_iterations, runs[1].step_iterations)
+    assert np.array_equal(runs[0].basis_cols, runs[1].basis_cols)
+    assert np.array_equal(runs[0].pod_k, runs[1].pod_k)
+
+
 @pytest.mark.slow
 def test_host_step_api_matches_device_loop(gpu_ok):
     """64^3: explicit_euler_step + recover_an from the host (each call leaves
