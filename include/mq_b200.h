@@ -165,6 +165,24 @@ int mq_csr_spmv(int32_t device, int64_t nrows, int64_t ncols,
                 const int64_t *row_ptr, const int32_t *col_idx,
                 const double *values, const double *x, double *y);
 
+/* ---- device-resident CSR operator (models given as matrices) -----------
+ * The reference's manifest path (bench.py:228-313 load_model, model.py:640-689
+ * export_model) gives a PartitionedSystem of CSR blocks with no grid behind
+ * it.  mq_csr_op uploads one block once (K_n, K_cn, its transpose or K_c);
+ * PCG solves (krylov.py:174-250, replaces pcg_solve(a=CsrMatrix) at
+ * mq/schur.py:253 through the module-global rebinding) and SpMVs
+ * (sparse.py:179-184, CsrMatrix.matvec) reuse it.  inv_diag: the Jacobi
+ * inverse (krylov.py:90-94), NULL if never used.  Host vectors. */
+typedef struct mq_csr_op mq_csr_op;
+int mq_csr_op_create(int32_t device, int64_t nrows, int64_t ncols,
+                     const int64_t *row_ptr, const int32_t *col_idx,
+                     const double *values, const double *inv_diag, mq_csr_op **out);
+int mq_csr_op_destroy(mq_csr_op *op);
+int mq_csr_op_pcg(mq_csr_op *op, const double *b, const double *x0, double *x,
+                  int32_t use_inv, double rel_tol, double abs_tol, int32_t max_iter,
+                  mq_solve_report *rep);
+int mq_csr_op_spmv(mq_csr_op *op, const double *x, double *y);
+
 /* ---- solver: strategy + families + conducting block ---------------------
  * One solver per context.  pattern: compact source pattern (n_n). */
 int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern);

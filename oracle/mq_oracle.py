@@ -733,6 +733,32 @@ def make_strategy(kind, n, apply_a, *, max_cols=20, n_pod=10, eps_pod=1e-4,
 # ---------------------------------------------------------------------------
 
 
+@dataclass
+class CsrModel:
+    """PartitionedSystem.linear (schur.py:85-160) of CSR blocks, as
+    bench.py:228-313 loads a manifest without builtin parameters: the fields
+    SchurOracle reads.  K_c is the stored (frozen) matrix."""
+    kn: sp.csr_matrix
+    kcn: sp.csr_matrix
+    kc: sp.csr_matrix
+    mc_diag: np.ndarray
+    pattern: np.ndarray
+
+    @property
+    def n_c(self):
+        return int(self.kcn.shape[0])
+
+    @property
+    def n_n(self):
+        return int(self.kcn.shape[1])
+
+    def kn_apply(self, x):
+        return self.kn @ x
+
+    def kc_apply(self, state, x):
+        return self.kc @ x
+
+
 class SchurOracle:
     """Owns the strategy and bookkeeping of every K_n solve."""
 

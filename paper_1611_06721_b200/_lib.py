@@ -100,6 +100,11 @@ SIGNATURES = {
     "mq_pcg_solve_dev": (I32, [VP, VP, VP, VP, D, D, I32, I32, ctypes.POINTER(SolveReportC)]),
     "mq_pcg_solve_host": (I32, [VP, c_double_p, c_double_p, c_double_p, D, D, I32, I32,
                                 ctypes.POINTER(SolveReportC)]),
+    "mq_csr_op_create": (I32, [I32, I64, I64, c_int64_p, c_int32_p, c_double_p, c_double_p, ctypes.POINTER(VP)]),
+    "mq_csr_op_destroy": (I32, [VP]),
+    "mq_csr_op_pcg": (I32, [VP, c_double_p, c_double_p, c_double_p, I32, D, D, I32,
+                            ctypes.POINTER(SolveReportC)]),
+    "mq_csr_op_spmv": (I32, [VP, c_double_p, c_double_p]),
     "mq_csr_pcg_solve": (I32, [I32, I64, c_int64_p, c_int32_p, c_double_p, c_double_p,
                                c_double_p, c_double_p, c_double_p, D, D, I32,
                                ctypes.POINTER(SolveReportC)]),

@@ -161,6 +161,18 @@ def pcg_solve(a, b, x0=None, config: PcgConfig | None = None, preconditioner=Non
         a.count += int(rep.applies)
         return x, SolveReport(int(rep.iterations), float(rep.final_rel_residual),
                               bool(rep.converged), int(rep.applies))
+    from .csrsys import CsrOperator
+    if isinstance(a, CsrOperator):
+        # a block resident on the device (models given as matrices)
+        use_jac = config.preconditioner is Preconditioner.JACOBI
+        if preconditioner is not None:
+            inv = _inverse_of(preconditioner, a.n)
+            if a.inverse is None or not np.array_equal(inv, a.inverse):
+                raise NotImplementedError("a resident CSR block solves with its own Jacobi inverse only")
+            use_jac = True
+        elif config.preconditioner is Preconditioner.IC0:
+            raise NotImplementedError("IC(0) is not part of the device path")
+        return a.solve(b, x0=x0, config=config, use_jacobi=use_jac)
     csr = _csr_of(a)
     if csr is None:
         if callable(a):
