@@ -276,6 +276,17 @@ class PinnedPool:
                 return
         load().mq_host_free(ctypes.c_void_p(ptr))
 
+    def reserve(self, n: int, count: int) -> None:
+        """Have ``count`` free buffers of length n ready (page-locking costs
+        milliseconds per buffer; a stepping loop should not pay it)."""
+        with self._lock:
+            have = len(self._free.get(n, []))
+        for _ in range(max(0, min(count, self._max) - have)):
+            p = ctypes.c_void_p()
+            check(load().mq_host_alloc(8 * max(n, 1), ctypes.byref(p)))
+            with self._lock:
+                self._free.setdefault(n, []).append(p.value)
+
     def empty(self, n: int) -> np.ndarray:
         import weakref
         with self._lock:
@@ -294,9 +305,18 @@ class PinnedPool:
 _PINNED = None
 
 
-def pinned_empty(n: int) -> np.ndarray:
-    """float64 array of length n in recycled page-locked memory."""
+def _pool() -> PinnedPool:
     global _PINNED
     if _PINNED is None:
         _PINNED = PinnedPool()
-    return _PINNED.empty(n)
+    return _PINNED
+
+
+def pinned_empty(n: int) -> np.ndarray:
+    """float64 array of length n in recycled page-locked memory."""
+    return _pool().empty(n)
+
+
+def pinned_reserve(n: int, count: int = 4) -> None:
+    """Pre-allocate ``count`` recycled page-locked buffers of length n."""
+    _pool().reserve(n, count)

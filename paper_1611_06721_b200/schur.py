@@ -68,6 +68,10 @@ class SchurOperator:
         self._y = self.grid.alloc()
         self._minv_diag = 1.0 / self.grid.mc_diag()
         self.t = 0.0
+        # page-locked result arrays of the host-facing step / recovery calls,
+        # allocated now rather than inside the first steps
+        _lib.pinned_reserve(self.grid.n_c, 4)
+        _lib.pinned_reserve(self.grid.n_n, 4)
 
     @property
     def system_n_c(self):
