@@ -1,6 +1,10 @@
 // Shared-memory-resident fused PCG for grids whose bricks fit on chip
-// (krylov.py:174-250; same algorithm, stopping rule and bit-level arithmetic
-// as pcg_stencil_kernel / pcg_tma_kernel).
+// (krylov.py:174-250).  Two kernels:
+//  * pcg_resident1_kernel<LI> (default for li <= 4): one grid reduction per
+//    iteration (reduced-synchronisation recurrence, see its comment below);
+//  * pcg_resident_kernel<LI> (MQ_PCG_SYNC=2, and li = 5): the reference's two
+//    reductions per iteration, same algorithm, stopping rule and bit-level
+//    arithmetic as pcg_stencil_kernel / pcg_tma_kernel; described here.
 //
 // One CTA per SM (512 threads) owns a brick: a 16 (j) x 32 (k) node tile over
 // Li <= 5 i-planes, all three edge components.  For the whole solve the
