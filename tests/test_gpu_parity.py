@@ -680,6 +680,40 @@ def test_config2_first_steps_vs_oracle(gpu_ok):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("strategy", ["cspe", "pod"])
+def test_config1_twenty_steps_vs_oracle(gpu_ok, strategy):
+    """configs[1] (64^3, Brauer, the bench workload; single-reduction resident
+    PCG): the first 20 steps with CSPE (k = 5) and with POD-20 against the CPU
+    oracle's run (tests/golden/oracle_cfg1.npz, made by
+    tests/golden/make_oracle_cfg1.py): every step's a_c norm and 512 sampled
+    entries within the field bar, the final a_c within the bar, every solve's
+    iteration count within +-1, the recovered a_n within its floor."""
+    from pathlib import Path
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, run_explicit
+    ref = np.load(Path(__file__).parent / "golden" / "oracle_cfg1.npz")
+    spec = C.config_spec(1)
+    steps = int(ref["steps"])
+    res = run_explicit(C.make_problem(1), t_end=steps * spec.dt, dt=spec.dt, strategy=strategy,
+                       pcg=PcgConfig(rel_tol=spec.rel_tol), max_cols=5, n_pod=20, eps_pod=1e-4,
+                       output_period=spec.dt * (1 - 1e-3), record_states=True)
+    k = strategy
+    for i in range(steps):
+        a = res.a_c_history[i]
+        nref = ref[f"{k}_a_c_norm"][i + 1]
+        assert abs(np.linalg.norm(a) - nref) <= REL_FIELD * nref, i
+        assert np.max(np.abs(a[ref["idx_c"]] - ref[f"{k}_a_c_sample"][i + 1])) <= REL_FIELD * nref, i
+    assert rel(res.final_a_c, ref[f"{k}_a_c_final"]) <= REL_FIELD
+    an = res.final_a_n
+    assert abs(np.linalg.norm(an) - ref[f"{k}_a_n_norm"][-1]) <= AN_FLOOR * ref[f"{k}_a_n_norm"][-1]
+    it = res.step_iterations
+    src = ref[f"{k}_iters_src"][1:].reshape(steps, 2)
+    assert np.max(np.abs(it[:, 0] - src[:, 0])) <= 1 and np.max(np.abs(it[:, 2] - src[:, 1])) <= 1
+    assert np.max(np.abs(it[:, 1] - ref[f"{k}_iters_prev"])) <= 1
+    assert np.max(np.abs(it[:, 3] - ref[f"{k}_iters_cur"][1:])) <= 1
+
+
+@pytest.mark.slow
 def test_config1_pod_first_steps(gpu_ok):
     """64^3 Brauer with POD-20 start vectors (configs[1]'s second run): the
     first steps against the oracle, per-step fields within the bar."""
