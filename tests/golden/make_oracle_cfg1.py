@@ -6,6 +6,9 @@ the GPU parity test: per-step norms of a_c and a_n, per-solve iteration
 counts, 512 fixed sample entries of a_c and a_n per step, the final a_c.
 
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_oracle_cfg1.py
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_oracle_cfg1.py --long
+
+--long: 100 CSPE steps into oracle_cfg1_long.npz (about 15 minutes here).
 """
 
 from __future__ import annotations
@@ -22,8 +25,10 @@ sys.path.insert(0, str(ROOT))
 from oracle import mq_oracle as O  # noqa: E402
 from tests.conftest import oracle_model  # noqa: E402
 
-OUT = Path(__file__).resolve().parent / "oracle_cfg1.npz"
-STEPS = 20
+LONG = "--long" in sys.argv
+OUT = Path(__file__).resolve().parent / ("oracle_cfg1_long.npz" if LONG else "oracle_cfg1.npz")
+STEPS = 100 if LONG else 20
+STRATEGIES = ("cspe",) if LONG else ("cspe", "pod")
 
 
 def main():
@@ -33,7 +38,7 @@ def main():
     ic = np.sort(rng.choice(m.n_c, 512, replace=False))
     inn = np.sort(rng.choice(m.n_n, 512, replace=False))
     out = {"idx_c": ic, "idx_n": inn, "steps": np.array(STEPS), "dt": np.array(spec.dt)}
-    for strat in ("cspe", "pod"):
+    for strat in STRATEGIES:
         tr = O.run(m, O.sinusoid(spec.freq), spec.dt, STEPS, strategy=strat, rel_tol=spec.rel_tol,
                    max_cols=5, n_pod=20, eps_pod=1e-4)
         out.update({

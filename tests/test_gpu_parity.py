@@ -680,18 +680,20 @@ def test_config2_first_steps_vs_oracle(gpu_ok):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("strategy", ["cspe", "pod"])
-def test_config1_twenty_steps_vs_oracle(gpu_ok, strategy):
+@pytest.mark.parametrize("strategy,fixture", [("cspe", "oracle_cfg1.npz"), ("pod", "oracle_cfg1.npz"),
+                                              ("cspe", "oracle_cfg1_long.npz")])
+def test_config1_twenty_steps_vs_oracle(gpu_ok, strategy, fixture):
     """configs[1] (64^3, Brauer, the bench workload; single-reduction resident
     PCG): the first 20 steps with CSPE (k = 5) and with POD-20 against the CPU
     oracle's run (tests/golden/oracle_cfg1.npz, made by
     tests/golden/make_oracle_cfg1.py): every step's a_c norm and 512 sampled
     entries within the field bar, the final a_c within the bar, every solve's
-    iteration count within +-1, the recovered a_n within its floor."""
+    iteration count within +-1, the recovered a_n within its floor.
+    oracle_cfg1_long.npz: the same for 100 CSPE steps."""
     from pathlib import Path
     from paper_1611_06721_b200 import configs as C
     from paper_1611_06721_b200 import PcgConfig, run_explicit
-    ref = np.load(Path(__file__).parent / "golden" / "oracle_cfg1.npz")
+    ref = np.load(Path(__file__).parent / "golden" / fixture)
     spec = C.config_spec(1)
     steps = int(ref["steps"])
     res = run_explicit(C.make_problem(1), t_end=steps * spec.dt, dt=spec.dt, strategy=strategy,
