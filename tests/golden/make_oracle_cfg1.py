@@ -8,7 +8,9 @@ counts, 512 fixed sample entries of a_c and a_n per step, the final a_c.
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_oracle_cfg1.py
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_oracle_cfg1.py --long
 
---long: 100 CSPE steps into oracle_cfg1_long.npz (about 15 minutes here).
+--long: 100 CSPE steps into oracle_cfg1_long.npz (about 15 minutes here);
+--long-pod: 60 POD-20 steps (every family's ring full and evicting) into
+oracle_cfg1_pod_long.npz.
 """
 
 from __future__ import annotations
@@ -26,9 +28,11 @@ from oracle import mq_oracle as O  # noqa: E402
 from tests.conftest import oracle_model  # noqa: E402
 
 LONG = "--long" in sys.argv
-OUT = Path(__file__).resolve().parent / ("oracle_cfg1_long.npz" if LONG else "oracle_cfg1.npz")
-STEPS = 100 if LONG else 20
-STRATEGIES = ("cspe",) if LONG else ("cspe", "pod")
+LONG_POD = "--long-pod" in sys.argv
+OUT = Path(__file__).resolve().parent / ("oracle_cfg1_long.npz" if LONG else
+                                         "oracle_cfg1_pod_long.npz" if LONG_POD else "oracle_cfg1.npz")
+STEPS = 100 if LONG else (60 if LONG_POD else 20)
+STRATEGIES = ("cspe",) if LONG else (("pod",) if LONG_POD else ("cspe", "pod"))
 
 
 def main():

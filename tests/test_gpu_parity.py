@@ -681,7 +681,8 @@ def test_config2_first_steps_vs_oracle(gpu_ok):
 
 @pytest.mark.slow
 @pytest.mark.parametrize("strategy,fixture", [("cspe", "oracle_cfg1.npz"), ("pod", "oracle_cfg1.npz"),
-                                              ("cspe", "oracle_cfg1_long.npz")])
+                                              ("cspe", "oracle_cfg1_long.npz"),
+                                              ("pod", "oracle_cfg1_pod_long.npz")])
 def test_config1_twenty_steps_vs_oracle(gpu_ok, strategy, fixture):
     """configs[1] (64^3, Brauer, the bench workload; single-reduction resident
     PCG): the first 20 steps with CSPE (k = 5) and with POD-20 against the CPU
@@ -689,7 +690,8 @@ def test_config1_twenty_steps_vs_oracle(gpu_ok, strategy, fixture):
     tests/golden/make_oracle_cfg1.py): every step's a_c norm and 512 sampled
     entries within the field bar, the final a_c within the bar, every solve's
     iteration count within +-1, the recovered a_n within its floor.
-    oracle_cfg1_long.npz: the same for 100 CSPE steps."""
+    oracle_cfg1_long.npz: the same for 100 CSPE steps; oracle_cfg1_pod_long.npz
+    for 60 POD-20 steps (every family's snapshot ring full and evicting)."""
     from pathlib import Path
     from paper_1611_06721_b200 import configs as C
     from paper_1611_06721_b200 import PcgConfig, run_explicit
