@@ -8,6 +8,8 @@ must be bit-identical.
 
 from __future__ import annotations
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -681,8 +683,9 @@ def test_config2_first_steps_vs_oracle(gpu_ok):
 
 @pytest.mark.slow
 @pytest.mark.parametrize("strategy,fixture", [("cspe", "oracle_cfg1.npz"), ("pod", "oracle_cfg1.npz"),
-                                              ("cspe", "oracle_cfg1_long.npz"),
-                                              ("pod", "oracle_cfg1_pod_long.npz")])
+                                              ("cspe", "oracle_cfg1_long.npz")] +
+                         ([("pod", "oracle_cfg1_pod_long.npz")]
+                          if (Path(__file__).parent / "golden" / "oracle_cfg1_pod_long.npz").exists() else []))
 def test_config1_twenty_steps_vs_oracle(gpu_ok, strategy, fixture):
     """configs[1] (64^3, Brauer, the bench workload; single-reduction resident
     PCG): the first 20 steps with CSPE (k = 5) and with POD-20 against the CPU
