@@ -3,7 +3,7 @@ first two explicit-Euler steps with recovery, run by the CPU oracle here
 (minutes), stored compactly for the GPU parity test (norms, per-solve
 iteration counts and 512 fixed sample entries of a_c and a_n per step).
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_oracle_cfg2.py
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_oracle_cfg2.py [--steps N]
 """
 
 from __future__ import annotations
@@ -21,7 +21,7 @@ from oracle import mq_oracle as O  # noqa: E402
 from tests.conftest import oracle_model  # noqa: E402
 
 OUT = Path(__file__).resolve().parent / "oracle_cfg2.npz"
-STEPS = 2
+STEPS = int(sys.argv[sys.argv.index("--steps") + 1]) if "--steps" in sys.argv else 2
 
 
 def main():

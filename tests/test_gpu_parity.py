@@ -779,6 +779,31 @@ def test_ensemble_member_first_steps(gpu_ok):
         assert rel(res.a_c_history[i], tr.a_c[i + 1]) <= REL_FIELD
 
 
+@pytest.mark.slow
+def test_ensemble_member255_twenty_steps(gpu_ok):
+    """configs[3] member 255 (J, kappa factors from the ensemble seed, dt
+    scaled with kappa): 20 device steps against the stored oracle run
+    (tests/golden/oracle_cfg3_member255.npz): every step's a_c norm and 512
+    sampled entries within the field bar, coupling iterations +-1."""
+    from paper_1611_06721_b200 import PcgConfig, run_explicit
+    from paper_1611_06721_b200 import ensemble as E
+    ref = np.load(Path(__file__).parent / "golden" / "oracle_cfg3_member255.npz")
+    prob, jf, kf, dt = E.member_problem(int(ref["member"]))
+    assert dt == float(ref["dt"])
+    steps = int(ref["steps"])
+    res = run_explicit(prob, t_end=steps * dt, dt=dt, strategy="cspe", pcg=PcgConfig(rel_tol=1e-8),
+                       output_period=dt * (1 - 1e-3), max_cols=5, record_states=True)
+    for i in range(steps):
+        a = res.a_c_history[i]
+        nref = ref["a_c_norm"][i + 1]
+        assert abs(np.linalg.norm(a) - nref) <= REL_FIELD * nref, i
+        assert np.max(np.abs(a[ref["idx_c"]] - ref["a_c_sample"][i + 1])) <= REL_FIELD * nref, i
+    assert rel(res.final_a_c, ref["a_c_final"]) <= REL_FIELD
+    it = res.step_iterations
+    assert np.max(np.abs(it[:, 1] - ref["iters_prev"])) <= 1
+    assert np.max(np.abs(it[:, 3] - ref["iters_cur"][1:])) <= 1
+
+
 @pytest.mark.parametrize("variant", ["simple", "brick", "resident", "resident2"])
 def test_pcg_kernel_variants_agree(gpu_ok, variant, monkeypatch):
     """All fused-PCG kernels (thread-per-row, TMA brick, shared-memory
