@@ -655,7 +655,7 @@ def test_probe_after_host_calls(gpu_ok):
 @pytest.mark.slow
 def test_config2_first_steps_vs_oracle(gpu_ok):
     """configs[2] (128^3, two iron blocks, POD-30, TMA brick PCG): the first
-    two steps against the CPU oracle's run (tests/golden/oracle_cfg2.npz,
+    five steps against the CPU oracle's run (tests/golden/oracle_cfg2.npz,
     made by tests/golden/make_oracle_cfg2.py): per-step field norms and 512
     sampled entries within the bar, iteration counts within +-1."""
     from pathlib import Path
