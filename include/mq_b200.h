@@ -240,6 +240,14 @@ int mq_run_explicit(mq_ctx *ctx, int64_t n_steps, const double *dt,
                     int32_t use_graph, int32_t *iters_out, double *a_c_hist,
                     int64_t *failed_step);
 
+/* mq_run_explicit that also records a_n = y_src - y_cpl of every step's
+ * recovery (a_n_hist, n_steps*n_n, compact order; needs
+ * recover_every_step != 0): the per-step A-field (a_c, a_n) of the run. */
+int mq_run_explicit_states(mq_ctx *ctx, int64_t n_steps, const double *dt,
+                           const double *wave, int32_t recover_every_step,
+                           int32_t use_graph, int32_t *iters_out, double *a_c_hist,
+                           double *a_n_hist, int64_t *failed_step);
+
 /* The same loop in three calls: prepare (tables, counters), enqueue n steps
  * (asynchronous), finish (sync, error check, iteration log). */
 int mq_run_prepare(mq_ctx *ctx, int64_t n_steps, const double *dt, const double *wave,
@@ -255,6 +263,14 @@ int mq_run_finish(mq_ctx *ctx, int32_t *iters_out, int64_t *failed_step);
 int mq_probe_set(mq_ctx *ctx, const int64_t *cells, int64_t n);
 int mq_probe_b(mq_ctx *ctx, const double *a_c_host /* NULL = current state */, double *out);
 int mq_run_probe_log(mq_ctx *ctx, int64_t n, double *out);
+/* Per-step strategy diagnostics of the current run, 8 doubles per step:
+ * [0..2] CSPE basis size of families SOURCE, COUPLING_CURRENT,
+ * COUPLING_PREVIOUS after that step's inserts; [3,4] POD (last_k, last_info)
+ * after the Euler step's solves; [5,6] the same after the recovery's solves;
+ * [7] unused.  The host folds them into the trace columns basis_cols, pod_k,
+ * pod_info as the reference's _WindowStats / emit_row (schur.py:448-467,
+ * 524-538). */
+int mq_run_diag_log(mq_ctx *ctx, int64_t n, double *out);
 
 /* Spectral estimate lambda_max(M_c^-1 K_S(a_ref)) by power iteration
  * (schur.py:327-376): v0 = normalised start vector (host n_c), a_ref NULL = 0.

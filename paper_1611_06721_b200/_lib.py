@@ -134,12 +134,15 @@ SIGNATURES = {
     "mq_last_an": (I32, [VP, c_double_p]),
     "mq_run_explicit": (I32, [VP, I64, c_double_p, c_double_p, I32, I32, c_int32_p,
                               c_double_p, c_int64_p]),
+    "mq_run_explicit_states": (I32, [VP, I64, c_double_p, c_double_p, I32, I32, c_int32_p,
+                                     c_double_p, c_double_p, c_int64_p]),
     "mq_run_prepare": (I32, [VP, I64, c_double_p, c_double_p, I32]),
     "mq_run_steps": (I32, [VP, I64, I32, VP]),
     "mq_run_finish": (I32, [VP, c_int32_p, c_int64_p]),
     "mq_probe_set": (I32, [VP, c_int64_p, I64]),
     "mq_probe_b": (I32, [VP, c_double_p, c_double_p]),
     "mq_run_probe_log": (I32, [VP, I64, c_double_p]),
+    "mq_run_diag_log": (I32, [VP, I64, c_double_p]),
     "mq_pcg_collect": (I32, [VP, c_double_p, c_int32_p]),
     "mq_estimate_cfl": (I32, [VP, c_double_p, c_double_p, I32, D, D, D, I32, c_double_p,
                               c_double_p, c_int32_p, c_int64_p]),

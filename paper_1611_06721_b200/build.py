@@ -31,15 +31,32 @@ def newest_source_mtime() -> float:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if OUT.exists() and not force and OUT.stat().st_mtime >= newest_source_mtime():
         return OUT
-    cmd = [nvcc(), "-O3", "-lineinfo", "-std=c++17", *ARCH, "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-O3", "-shared", "-diag-suppress", "177",
-           *[str(CSRC / s) for s in SOURCES], "-o", str(OUT) + ".tmp"]
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    flags = [nvcc(), "-O3", "-lineinfo", "-std=c++17", *ARCH, "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
+             "-diag-suppress", "177"]
+
+    def compile_one(src: str):
+        obj = objdir / (src + ".o")
+        cmd = [*flags, "-c", str(CSRC / src), "-o", str(obj)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for obj, res in results:
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError(f"nvcc failed compiling {obj.name[:-2]}")
+    cmd = [nvcc(), *ARCH, "-shared", *[str(o) for o, _ in results], "-o", str(OUT) + ".tmp"]
     if verbose:
-        print(" ".join(cmd))
+        print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libmq_b200.so")
+        raise RuntimeError("nvcc failed linking libmq_b200.so")
     os.replace(str(OUT) + ".tmp", OUT)
     return OUT
 

@@ -99,6 +99,11 @@ struct SolverHost {
   unsigned int *d_probe_ctr = nullptr;  // k_probe's last-block ticket
   int probe_grid = 1;
   int64_t n_probe = 0, probe_cap = 0;
+  // per-step strategy diagnostics of the current run (trace columns
+  // basis_cols / pod_k / pod_info, schur.py:448-467,524-538): kDiagW doubles
+  // per step, see k_dlog_k / k_dlog_pod
+  double *d_dlog = nullptr;
+  int64_t dlog_cap = 0;
   double *d_probe_out = nullptr;
   // page-locked landing block of the host-facing calls: run status, the two
   // iteration counts and the probe value come back in one copy batch and one
@@ -153,6 +158,7 @@ void solver_free(mq_ctx *ctx) {
   cudaFree(s->d_probe);
   cudaFree(s->d_probe_vals);
   cudaFree(s->d_probe_log);
+  cudaFree(s->d_dlog);
   cudaFree(s->d_probe_plan);
   cudaFree(s->d_probe_leaf);
   cudaFree(s->d_probe_ctr);
@@ -913,6 +919,30 @@ __global__ void k_post_solve(const PcgOut *o, RunDev *run, FamDev *fams, int fam
   run->pcg_applies += r.applies;
 }
 
+// ---- per-step diagnostics log ---------------------------------------------
+// Row m (0-based step of the run) of the log, kDiagW doubles:
+//   [0..2] CSPE basis size of each family after that step's inserts
+//   [3,4]  POD (last_k, last_info) sampled after the Euler step's solves
+//   [5,6]  POD (last_k, last_info) sampled after the recovery's solves
+// The host reduces them as the reference's _WindowStats and emit_row do.
+constexpr int kDiagW = 8;
+
+// row = par->step - shift (a deferred insert runs one step late)
+__global__ void k_dlog_k(const FamDev *f, int fam, const StepParams *par, double *log, long long cap, int shift) {
+  if (threadIdx.x != 0 || !log) return;
+  const long long m = par->step - shift;
+  if (m >= 0 && m < cap) log[m * kDiagW + fam] = (double)f->k;
+}
+
+__global__ void k_dlog_pod(const RunDev *run, const StepParams *par, double *log, long long cap, int col) {
+  if (threadIdx.x != 0 || !log) return;
+  const long long m = par->step - 1;
+  if (m >= 0 && m < cap) {
+    log[m * kDiagW + col] = (double)run->pod_last_k;
+    log[m * kDiagW + col + 1] = run->pod_last_info;
+  }
+}
+
 // ---- conducting block ---------------------------------------------------
 struct CondArgs {
   int64_t n_c, n_cells, n_rows_t;
@@ -1299,7 +1329,7 @@ static ObsRes main_res(mq_ctx *ctx) {
 
 // gated: the insert runs only if the family has a deferred one pending
 // (k_obs_gate); CSPE only
-static int observe(mq_ctx *ctx, int fam, const double *y, const ObsRes &o, bool gated = false) {
+static int observe(mq_ctx *ctx, int fam, const double *y, const ObsRes &o, bool gated = false, int dlog_shift = 1) {
   SolverHost *s = ctx->solver;
   FamDev *f = s->d_fam + fam;
   const Lay &L = ctx->topo.L;
@@ -1342,6 +1372,8 @@ static int observe(mq_ctx *ctx, int fam, const double *y, const ObsRes &o, bool 
       post.kind = POST_COMMIT;
       KB_LAUNCH(s->kb, k_cspe_product, G, kBlock, st, L, ctx->d_mask, ctx->kn_diag, ctx->kn_off, f, s->d_U[fam], s->d_KU[fam],
                                            o.w2, o.red, o.cnt, post);
+      LAUNCH_CHECK();
+      k_dlog_k<<<1, 32, 0, st>>>(f, fam, s->d_par, s->d_dlog, s->dlog_cap, dlog_shift);
       LAUNCH_CHECK();
       break;
     }
@@ -1405,11 +1437,12 @@ static int solve_enqueue(mq_ctx *ctx, int fam, const double *rhs, double *y, boo
 
 // the source family's cache update on the side stream (fork), joined back
 // into the main stream by join_side()
-static int fork_observe(mq_ctx *ctx, int slot, int fam, const double *y, bool gated = false) {
+static int fork_observe(mq_ctx *ctx, int slot, int fam, const double *y, bool gated = false, int dlog_shift = 1) {
   SolverHost *s = ctx->solver;
   MQ_CUDA(cudaEventRecord(s->ev_fork[slot], ctx->stream));
   MQ_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork[slot], 0));
-  int rc = observe(ctx, fam, y, ObsRes{s->side, s->d_red2, s->d_cnt2, s->w1b, s->w2b, s->side_grid}, gated);
+  int rc = observe(ctx, fam, y, ObsRes{s->side, s->d_red2, s->d_cnt2, s->w1b, s->w2b, s->side_grid}, gated,
+                   dlog_shift);
   if (rc) return rc;
   MQ_CUDA(cudaEventRecord(s->ev_join[slot], s->side));
   s->pend[slot] = true;
@@ -1473,6 +1506,8 @@ static int euler_enqueue(mq_ctx *ctx, bool join_tail, bool defer_cpl) {
     k_set_pending<<<1, 32, 0, st>>>(s->d_fam + MQ_FAM_COUPLING_PREVIOUS);
     LAUNCH_CHECK();
   }
+  k_dlog_pod<<<1, 32, 0, st>>>(s->d_run, s->d_par, s->d_dlog, s->dlog_cap, 3);
+  LAUNCH_CHECK();
   // Brauer + Euler update
   k_cell_nu<<<grid_for(ctx, a.n_cells), 256, 0, st>>>(a, ctx->d_ac, ctx->d_cell_nu);
   LAUNCH_CHECK();
@@ -1509,6 +1544,8 @@ static int recover_enqueue(mq_ctx *ctx, bool defer) {
   if (rc) return rc;
   rc = solve_enqueue(ctx, MQ_FAM_COUPLING_CURRENT, s->rhs_cpl, s->y_cur, !defer);
   if (rc) return rc;
+  k_dlog_pod<<<1, 32, 0, st>>>(s->d_run, s->d_par, s->d_dlog, s->dlog_cap, 5);
+  LAUNCH_CHECK();
   if (defer) {
     k_set_pending<<<1, 32, 0, st>>>(s->d_fam + MQ_FAM_COUPLING_CURRENT);
     LAUNCH_CHECK();
@@ -2110,7 +2147,19 @@ int mq_last_an(mq_ctx *ctx, double *a_n_host) {
   return mq_vec_download(ctx, ctx->d_tmp1, a_n_host);
 }
 
-static int enqueue_step(mq_ctx *ctx, double *hist) {
+// a_n = y_src - y_cur of the step's recovery in compact order (schur.py:416-419)
+__global__ void k_an_record(int64_t n, const int32_t *__restrict__ idx, const double *__restrict__ y_src,
+                            const double *__restrict__ y_cur, const StepParams *par, const RunDev *run,
+                            double *__restrict__ out) {
+  if (run->err) return;
+  const long long m = par->step - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t e = idx[i];
+    out[m * n + i] = sub(y_src[e], y_cur[e]);
+  }
+}
+
+static int enqueue_step(mq_ctx *ctx, double *hist, double *hist_n = nullptr) {
   SolverHost *s = ctx->solver;
   const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
   ctx->ev_n = 0;
@@ -2121,7 +2170,7 @@ static int enqueue_step(mq_ctx *ctx, double *hist) {
   if (defer) {
     // the previous recovery's coupling-family insert, under this step's
     // source and coupling solves (a no-op if none is pending)
-    int r0 = fork_observe(ctx, 3, MQ_FAM_COUPLING_CURRENT, s->y_cur, true);
+    int r0 = fork_observe(ctx, 3, MQ_FAM_COUPLING_CURRENT, s->y_cur, true, 2);
     if (r0) return r0;
   }
   int rc = euler_enqueue(ctx, !s->recover_every_step);
@@ -2130,6 +2179,13 @@ static int enqueue_step(mq_ctx *ctx, double *hist) {
     rc = recover_enqueue(ctx, defer);
     if (rc) return rc;
     if (defer) s->maybe_pending[MQ_FAM_COUPLING_CURRENT] = true;
+    if (hist_n) {
+      const int64_t n_n = (int64_t)ctx->topo.nc_pad.size();
+      k_an_record<<<grid_for(ctx, n_n), 256, 0, ctx->stream>>>(n_n, ctx->d_nc_pad, s->y_src, s->y_cur, s->d_par,
+                                                               s->d_run, hist_n);
+      MQ_CUDA(cudaGetLastError());
+      ctx->launches += 1;
+    }
   }
   if (s->n_probe > 0) {
     k_probe<<<s->probe_grid, 256, 0, ctx->stream>>>(cond_args(ctx), s->d_probe, s->n_probe, s->d_probe_plan,
@@ -2238,6 +2294,14 @@ int mq_run_probe_log(mq_ctx *ctx, int64_t n, double *out) {
   return MQ_OK;
 }
 
+int mq_run_diag_log(mq_ctx *ctx, int64_t n, double *out) {
+  SolverHost *s = ctx->solver;
+  if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  if (n < 0 || n > s->n_enqueued || n > s->dlog_cap) { set_error("more diagnostics rows than steps run"); return MQ_INVALID; }
+  if (n > 0) MQ_CUDA(cudaMemcpy(out, s->d_dlog, sizeof(double) * kDiagW * n, cudaMemcpyDeviceToHost));
+  return MQ_OK;
+}
+
 int mq_run_prepare(mq_ctx *ctx, int64_t n_steps, const double *dt, const double *wave,
                    int32_t recover_every_step) {
   SolverHost *s = ctx->solver;
@@ -2266,6 +2330,14 @@ int mq_run_prepare(mq_ctx *ctx, int64_t n_steps, const double *dt, const double 
     cudaGraphExecDestroy(s->graph_exec);
     s->graph_exec = nullptr;
   }
+  if (s->dlog_cap < n_steps) {
+    cudaFree(s->d_dlog);
+    s->d_dlog = nullptr;
+    MQ_CUDA(cudaMalloc(&s->d_dlog, sizeof(double) * kDiagW * n_steps));
+    MQ_CUDA(cudaMemset(s->d_dlog, 0, sizeof(double) * kDiagW * n_steps));
+    s->dlog_cap = n_steps;
+    solver_graph_reset(ctx);  // every cached graph holds the log pointer
+  }
   if (s->n_probe > 0 && s->probe_cap < n_steps) {
     cudaFree(s->d_probe_log);
     s->d_probe_log = nullptr;
@@ -2286,7 +2358,13 @@ int mq_run_prepare(mq_ctx *ctx, int64_t n_steps, const double *dt, const double 
   return MQ_OK;
 }
 
+static int run_steps(mq_ctx *ctx, int64_t n, int32_t use_graph, double *a_c_hist_dev, double *a_n_hist_dev);
+
 int mq_run_steps(mq_ctx *ctx, int64_t n, int32_t use_graph, double *a_c_hist_dev) {
+  return run_steps(ctx, n, use_graph, a_c_hist_dev, nullptr);
+}
+
+static int run_steps(mq_ctx *ctx, int64_t n, int32_t use_graph, double *a_c_hist_dev, double *a_n_hist_dev) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
   if (s->n_enqueued + n > s->n_planned) { set_error("more steps than prepared"); return MQ_INVALID; }
@@ -2320,7 +2398,7 @@ int mq_run_steps(mq_ctx *ctx, int64_t n, int32_t use_graph, double *a_c_hist_dev
   }
   if (!graphed) {
     for (int64_t m = 0; m < n; ++m) {
-      int rc = enqueue_step(ctx, a_c_hist_dev);
+      int rc = enqueue_step(ctx, a_c_hist_dev, a_n_hist_dev);
       if (rc) return rc;
     }
   }
@@ -2342,19 +2420,33 @@ int mq_run_finish(mq_ctx *ctx, int32_t *iters_out, int64_t *failed_step) {
   return rc;
 }
 
-int mq_run_explicit(mq_ctx *ctx, int64_t n_steps, const double *dt, const double *wave, int32_t recover_every_step,
-                    int32_t use_graph, int32_t *iters_out, double *a_c_hist, int64_t *failed_step) {
+int mq_run_explicit_states(mq_ctx *ctx, int64_t n_steps, const double *dt, const double *wave,
+                           int32_t recover_every_step, int32_t use_graph, int32_t *iters_out, double *a_c_hist,
+                           double *a_n_hist, int64_t *failed_step) {
+  if (a_n_hist && !recover_every_step) { set_error("a_n history needs a recovery every step"); return MQ_INVALID; }
   int rc = mq_run_prepare(ctx, n_steps, dt, wave, recover_every_step);
   if (rc) return rc;
   const int64_t n_c = (int64_t)ctx->topo.c_pad.size();
-  double *hist = nullptr;
+  const int64_t n_n = (int64_t)ctx->topo.nc_pad.size();
+  double *hist = nullptr, *hist_n = nullptr;
   if (a_c_hist && n_steps > 0) MQ_CUDA(cudaMalloc(&hist, sizeof(double) * n_c * n_steps));
-  rc = mq_run_steps(ctx, n_steps, use_graph, hist);
+  if (a_n_hist && n_steps > 0) {
+    const cudaError_t e = cudaMalloc(&hist_n, sizeof(double) * n_n * n_steps);
+    if (e != cudaSuccess) {
+      cudaFree(hist);
+      MQ_CUDA(e);
+    }
+  }
+  rc = run_steps(ctx, n_steps, use_graph, hist, hist_n);
   int rc2 = mq_run_finish(ctx, iters_out, failed_step);
   if (rc == MQ_OK) rc = rc2;
   if (hist) {
     cudaMemcpy(a_c_hist, hist, sizeof(double) * n_c * n_steps, cudaMemcpyDeviceToHost);
     cudaFree(hist);
+  }
+  if (hist_n) {
+    cudaMemcpy(a_n_hist, hist_n, sizeof(double) * n_n * n_steps, cudaMemcpyDeviceToHost);
+    cudaFree(hist_n);
   }
   if (rc == MQ_OK) {
     double t = ctx->t_now;
@@ -2362,6 +2454,12 @@ int mq_run_explicit(mq_ctx *ctx, int64_t n_steps, const double *dt, const double
     ctx->t_now = t;
   }
   return rc;
+}
+
+int mq_run_explicit(mq_ctx *ctx, int64_t n_steps, const double *dt, const double *wave, int32_t recover_every_step,
+                    int32_t use_graph, int32_t *iters_out, double *a_c_hist, int64_t *failed_step) {
+  return mq_run_explicit_states(ctx, n_steps, dt, wave, recover_every_step, use_graph, iters_out, a_c_hist, nullptr,
+                                failed_step);
 }
 
 // Power iteration for lambda_max(M_c^-1 K_S) (schur.py:327-376 with the

@@ -271,7 +271,8 @@ class TransientResult:
     final_a_n: np.ndarray | None
     aggregates: dict = field(default_factory=dict)
     step_iterations: np.ndarray | None = None   # per step [src, prev, src_rec, cur]
-    a_c_history: np.ndarray | None = None
+    a_c_history: np.ndarray | None = None       # record_states: a_c after every step
+    a_n_history: np.ndarray | None = None       # record_states: a_n recovered after every step
 
     @property
     def n_rows(self) -> int:
@@ -372,7 +373,9 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
     wave = op.problem.waveform
     rows = {k: [] for k in ("t", "b", "src", "prev", "cur", "basis", "k", "info")}
 
-    def emit(t_row, a_c_row, a_n_row, iters_src, iters_prev, iters_cur):
+    def emit(t_row, a_c_row, a_n_row, iters_src, iters_prev, iters_cur, pod_window=()):
+        # pod_window: the (pod_k, pod_info) samples the reference's
+        # _WindowStats.note_pod took after each Euler step since the last row
         rows["t"].append(t_row)
         if host_probe:
             rows["b"].append(float(probe(a_c_row, a_n_row, t_row)))
@@ -383,8 +386,13 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
         rows["cur"].append(float(np.mean(iters_cur)) if len(iters_cur) else 0.0)
         diag = op.strategy_diagnostics()
         rows["basis"].append(op.basis_size())
-        rows["k"].append(diag.get("pod_k", 0))
-        rows["info"].append(diag.get("min_pod_info", 1.0) if op.strategy_kind == "pod" else 1.0)
+        if op.strategy_kind == "pod":
+            samples = list(pod_window) + [(diag["pod_k"], diag["pod_info"])]
+            rows["k"].append(max(k for k, _ in samples))
+            rows["info"].append(min([1.0] + [i for _, i in samples]))
+        else:
+            rows["k"].append(0)
+            rows["info"].append(1.0)
 
     # initial recovery at t = 0 (schur.py:540-541)
     a_n, (r1, r2) = recover_an(op, a_c, 0.0)
@@ -392,7 +400,7 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
     op._set_state(a_c, 0.0)
     sched = _Schedule(t_end, output_period, max_steps)
     phase_len = reestimate_every if (auto and reestimate_every > 0) else None
-    iters_parts, hist_parts = [], []
+    iters_parts, hist_parts, hist_n_parts = [], [], []
     all_out_all = True
     refreshes = 0
     while not sched.done:
@@ -413,7 +421,8 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
         all_out_all = all_out_all and all_out
         iters_parts.append(step_iters)
         if hist is not None:
-            hist_parts.append(hist)
+            hist_parts.append(hist[0])
+            hist_n_parts.append(hist[1])
     n = sched.count
     wall = time.perf_counter() - wall_start
     d = op.diagnostics()
@@ -446,7 +455,9 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
                            aggregates=aggregates,
                            step_iterations=step_iters if all_out_all and not host_probe else None,
                            a_c_history=np.concatenate(hist_parts) if record_states and hist_parts else
-                           (np.empty((0, n_c)) if record_states else None))
+                           (np.empty((0, n_c)) if record_states else None),
+                           a_n_history=np.concatenate(hist_n_parts) if record_states and hist_n_parts else
+                           (np.empty((0, op.grid.n_n)) if record_states else None))
 
 
 def _run_phase(op, dts, outs, tt, wave, emit, rows, base, host_probe, device_probe, use_graph,
@@ -463,10 +474,13 @@ def _run_phase(op, dts, outs, tt, wave, emit, rows, base, host_probe, device_pro
     hist = np.empty((n, n_c)) if record_states else None
     failed = ctypes.c_int64(-1)
     a_n = None
+    hist_n = None
     if all_out and not host_probe:
-        rc = op.lib.mq_run_explicit(op.grid.ctx, n, dptr(dt_tab), dptr(wave_tab), 1,
-                                    1 if use_graph else 0, _lib.i32ptr(step_iters),
-                                    dptr(hist) if hist is not None else None, ctypes.byref(failed))
+        hist_n = np.empty((n, op.grid.n_n)) if record_states else None
+        rc = op.lib.mq_run_explicit_states(op.grid.ctx, n, dptr(dt_tab), dptr(wave_tab), 1,
+                                           1 if use_graph else 0, _lib.i32ptr(step_iters),
+                                           dptr(hist) if hist is not None else None,
+                                           dptr(hist_n) if hist_n is not None else None, ctypes.byref(failed))
         if rc == _lib.MQ_NONFINITE:
             raise StepFailureError(f"non-finite conducting state at step {base + failed.value}")
         check(rc)
@@ -481,18 +495,31 @@ def _run_phase(op, dts, outs, tt, wave, emit, rows, base, host_probe, device_pro
             rows["src"].append(float(np.mean(step_iters[m, [0, 2]])))
             rows["prev"].append(float(step_iters[m, 1]))
             rows["cur"].append(float(step_iters[m, 3]))
-        diag = op.strategy_diagnostics()
-        nb = op.basis_size()
-        rows["basis"].extend([nb] * n)
-        rows["k"].extend([diag.get("pod_k", 0)] * n)
-        rows["info"].extend([diag.get("min_pod_info", 1.0) if op.strategy_kind == "pod" else 1.0] * n)
+        if n > 0:
+            # per-row strategy columns from the device log (schur.py:448-467,
+            # 524-538): the window of a row is one Euler step + its recovery
+            dlog = np.zeros((n, 8))
+            check(op.lib.mq_run_diag_log(op.grid.ctx, n, dptr(dlog)))
+            if op.strategy_kind == "cspe":
+                rows["basis"].extend(int(v) for v in dlog[:, 0:3].max(axis=1))
+                rows["k"].extend([0] * n)
+                rows["info"].extend([1.0] * n)
+            elif op.strategy_kind == "pod":
+                rows["basis"].extend(int(v) for v in dlog[:, 5])
+                rows["k"].extend(int(v) for v in np.maximum(dlog[:, 3], dlog[:, 5]))
+                rows["info"].extend(float(min(1.0, a, b)) for a, b in zip(dlog[:, 4], dlog[:, 6]))
+            else:
+                rows["basis"].extend([0] * n)
+                rows["k"].extend([0] * n)
+                rows["info"].extend([1.0] * n)
         op.solve_iterations[RhsFamily.SOURCE_CURRENT].extend(
             int(v) for pair in step_iters[:, [0, 2]] for v in pair)
         op.solve_iterations[RhsFamily.COUPLING_FROM_PREVIOUS_STATE].extend(int(v) for v in step_iters[:, 1])
         op.solve_iterations[RhsFamily.COUPLING_FROM_CURRENT_STATE].extend(int(v) for v in step_iters[:, 3])
         a_n = _final_an(op)
     else:
-        win_src, win_prev = [], []
+        win_src, win_prev, win_pod = [], [], []
+        an_rows = []
         m = 0
         while m < n:
             seg = 0
@@ -500,7 +527,7 @@ def _run_phase(op, dts, outs, tt, wave, emit, rows, base, host_probe, device_pro
                 seg += 1
             seg += 1 if m + seg < n else 0
             seg = min(seg, n - m)
-            it = np.zeros((seg, 4), dtype=np.int32)
+            it = np.zeros((seg, 2), dtype=np.int32)   # [src, cpl_prev] per step (no recovery)
             rc = op.lib.mq_run_explicit(op.grid.ctx, seg, dptr(dt_tab[m:m + seg]),
                                         dptr(wave_tab[m:m + seg + 1].copy()), 0,
                                         1 if use_graph else 0, _lib.i32ptr(it),
@@ -510,6 +537,10 @@ def _run_phase(op, dts, outs, tt, wave, emit, rows, base, host_probe, device_pro
                 raise StepFailureError(f"non-finite conducting state at step {base + m + failed.value}")
             check(rc)
             step_iters[m:m + seg, :2] = it[:, :2]
+            if op.strategy_kind == "pod" and seg > 0:
+                dlog = np.zeros((seg, 8))
+                check(op.lib.mq_run_diag_log(op.grid.ctx, seg, dptr(dlog)))
+                win_pod.extend((int(a), float(b)) for a, b in dlog[:, 3:5])
             win_src.extend(int(v) for v in it[:, 0])
             win_prev.extend(int(v) for v in it[:, 1])
             op.solve_iterations[RhsFamily.SOURCE_CURRENT].extend(int(v) for v in it[:, 0])
@@ -518,11 +549,17 @@ def _run_phase(op, dts, outs, tt, wave, emit, rows, base, host_probe, device_pro
             if outs[m - 1]:
                 a_c = op._get_state()
                 a_n, (r1, r2) = recover_an(op, a_c, tt[m])
+                if record_states:
+                    an_rows.append((m - 1, np.array(a_n)))
                 step_iters[m - 1, 2:] = (r1.iterations, r2.iterations)
-                emit(tt[m], a_c, a_n, win_src + [r1.iterations], win_prev, [r2.iterations])
-                win_src, win_prev = [], []
+                emit(tt[m], a_c, a_n, win_src + [r1.iterations], win_prev, [r2.iterations], win_pod)
+                win_src, win_prev, win_pod = [], [], []
         a_c = op._get_state()
-    return a_c, a_n, step_iters, hist, all_out
+        if record_states:
+            hist_n = np.full((n, op.grid.n_n), np.nan)
+            for row, v in an_rows:
+                hist_n[row] = v
+    return a_c, a_n, step_iters, (hist, hist_n) if record_states else None, all_out
 
 
 TRACE_HEADER = "t,B_probe,iters_src,iters_cpl_prev,iters_cpl_cur,basis_cols,pod_k,pod_info"
