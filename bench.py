@@ -1,26 +1,28 @@
 #!/usr/bin/env python
 """Benchmark: explicit-Euler steps/s of the semi-explicit MQS scheme on B200.
 
-Workload (BASELINE.json configs[1]): 64^3 cells, Brauer iron block 24^3,
-annular coil J = 5e6 sin(2 pi 50 t), fp64, PCG (Jacobi, rel_tol 1e-8), CSPE
-start vectors (k = 5), output (recover_an) every step: 4 K_n solves per step.
-A "step" is one explicit-Euler step plus the recovery of a_n.  W warm-up
-steps (untimed; they also build the CSPE bases) precede K timed steps of the
-same trajectory.  L2 is flushed (256 MB write) before every timed step and
-the flush is outside the timed events.
+Headline workload (BASELINE.json configs[2], the largest single-GPU config and
+the north star's HBM case): 128^3 cells, two Brauer iron blocks of 24^3,
+annular coil J = 5e6 sin(2 pi 50 t), fp64, PCG (Jacobi, rel_tol 1e-8), POD
+start vectors from a 30-snapshot ring, output (recover_an + B probe) every
+step: 4 K_n solves per step.  A "step" is one explicit-Euler step plus the
+recovery of a_n.  W warm-up steps (untimed; they also fill the snapshot
+rings) precede K timed steps of the same trajectory.  L2 is flushed (256 MB
+write) before every timed step, outside the timed events.
 
 Outputs one JSON line (rank 0).  `value` is device-timed with the inputs
 resident in HBM; `e2e` is the same metric through the host-facing API
-(explicit_euler_step + recover_an with host arrays, copies inside the timed
-region); `roofline` is the fused PCG kernel measured inside the timed region
-(config 1) and `roofline_cfg2` the same kernel on the 128^3 grid of
-configs[2] (the north star's HBM target).  `cpu_baseline` times the CPU port
-of the reference (oracle/, numpy/scipy) on a bounded sample.
+(explicit_euler_step + recover_an + probe_b with host arrays, copies inside
+the timed region); `roofline` is the fused PCG kernel (pcg_tma_kernel)
+measured with CUDA events inside the timed region.  Secondary keys: configs[1]
+(64^3) with CSPE and with POD-20, configs[4] (256^3) on one GPU.
+`cpu_baseline` times the CPU port of the reference (oracle/, numpy/scipy) on
+a bounded sample of the same steps (see cpu_sampled_steps).
 
 --impl reference runs the CPU port of the reference on the same workload and
 prints the same metric.  With torchrun (N > 1) every rank runs an
-independent ensemble member (configs[3] factors): weak scaling, no
-collective on the data path; the timing is the max over ranks.
+independent replica of the workload (configs 0-2 do not shard: SURVEY.md
+8(e)), no collective on the data path; the timing is the max over ranks.
 """
 
 from __future__ import annotations
@@ -38,7 +40,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "explicit-Euler steps/s (config 1: 64^3 Brauer, CSPE k=5, recover every step)"
+METRIC = "explicit-Euler steps/s (config 2: 128^3 two Brauer blocks, POD-30, recover every step)"
 UNIT = "steps/s"
 
 
@@ -131,17 +133,6 @@ def pcg_launch_bytes(n_n, iters, modes=None):
     return 8.0 * n_n * (9.0 * iters + 4.0 + 3.0 * (iters > 0))
 
 
-def member_problem(rank: int):
-    """Rank 0 runs the nominal configs[1] problem; rank r > 0 runs configs[3]
-    ensemble member r (J, kappa factors; dt scaled with kappa)."""
-    from paper_1611_06721_b200 import configs as C
-    from paper_1611_06721_b200 import ensemble as E
-    if rank == 0:
-        return C.make_problem(1), (1.0, 1.0), C.config_spec(1).dt
-    prob, jf, kf, dt = E.member_problem(rank)
-    return prob, (jf, kf), dt
-
-
 def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -180,54 +171,177 @@ def barrier(dist):
 # ---------------------------------------------------------------------------
 # CPU port of the reference (oracle) on the same workload
 # ---------------------------------------------------------------------------
-def cpu_reference(spec, warmup, steps, *, budget_s=None):
+FIELDS = ROOT / "tests" / "golden"
+
+
+def oracle_iterations(index: int, strategy: str):
+    """The oracle's own per-step iteration counts [src, prev, src_rec, cur]
+    (tests/golden/fields_*.npz, made by running the oracle on the config)."""
+    name = {(1, "cspe"): "cfg1_cspe", (1, "pod"): "cfg1_pod", (2, "pod"): "cfg2"}[(index, strategy)]
+    f = np.load(FIELDS / f"fields_{name}.npz")
+    n = int(f["steps"])
+    src = f["iters_src"][1:].reshape(n, 2)
+    return np.stack([src[:, 0], f["iters_prev"], src[:, 1], f["iters_cur"][1:]], axis=1), name
+
+
+def cpu_sampled_steps(index: int, strategy: str, warmup: int, steps: int, *, iters=(4, 24)):
+    """steps/s of the CPU port (oracle/mq_oracle.py, a numpy/scipy restatement
+    of mqsolve) on steps warmup+1 .. warmup+steps, from a bounded sample.
+
+    Running those steps takes minutes each at 128^3 (0.36 s per PCG
+    iteration), so the sample measures, on this host and on the config's own
+    assembled matrices, the parts a step is made of and adds them up for
+    every timed step:
+      * t_it: one PCG iteration of the oracle's pcg loop (SpMV, dots, axpys),
+        from two truncated solves of iters[0] and iters[1] iterations;
+      * t_init: the initial residual of a warm-started solve;
+      * t_start(m): one start vector of the strategy with m columns in the
+        family's history (POD: Gram of the ring, eigh, basis, k SpMVs, the
+        Galerkin solve; CSPE: the projection) measured at two history sizes and
+        interpolated linearly in m, plus one observe (POD push / CSPE insert);
+      * t_rest: the step's remaining work (K_cn^T products, the Euler update
+        with the Brauer K_c, the recovery's subtraction, the B probe).
+    Per step: sum over its 4 solves of (t_init + its iteration count * t_it +
+    t_start(m) + t_observe) + t_rest, with the oracle's own iteration counts of
+    exactly those steps (oracle_iterations) and the history sizes the
+    reference's ring / FIFO rules give at that step.  The model is checked
+    against timed oracle steps in DESIGN.md."""
     from oracle import mq_oracle as O
     from paper_1611_06721_b200 import configs as C
+    spec = C.config_spec(index)
+    t0 = time.perf_counter()
     mat = C.material_map(spec)
     loops = C.coil_loops(spec.N, spec.J)
     m = O.assemble(mat, spec.h, O.Conductor(spec.kappa, *spec.brauer),
                    [O.Loop(lp.i0, lp.i1, lp.j0, lp.j1, lp.k0, lp.amps) for lp in loops])
-    op = O.SchurOracle(m, O.sinusoid(spec.freq), "cspe", spec.rel_tol, spec.max_iter, spec.max_cols)
-    a = np.zeros(m.n_c)
-    t = 0.0
-    op.recover(a, t)
-    for s in range(warmup):
-        a, _ = op.euler(a, t, spec.dt, s + 1)
-        t += spec.dt
-        op.recover(a, t)
-    done, t0 = 0, time.perf_counter()
-    for s in range(steps):
-        a, _ = op.euler(a, t, spec.dt, warmup + s + 1)
-        t += spec.dt
-        op.recover(a, t)
-        done += 1
-        if budget_s is not None and time.perf_counter() - t0 > budget_s:
-            break
-    el = time.perf_counter() - t0
-    return done / el, done, el, m.n_n
+    t_asm = time.perf_counter() - t0
+    inv = O.jacobi_inverse(m.kn.diagonal())
+    n = m.n_n
+    b = m.pattern.copy()
+    x0 = np.zeros(n)
+
+    def truncated(k):
+        ts = time.perf_counter()
+        O.pcg(m.kn_apply, b, x0=x0, rel_tol=1e-300, max_iter=k, inv_diag=inv)
+        return time.perf_counter() - ts
+    ta, tb = truncated(iters[0]), truncated(iters[1])
+    t_it = (tb - ta) / (iters[1] - iters[0])
+    t_init = max(ta - iters[0] * t_it, 0.0)
+    # history columns: Krylov vectors of the Jacobi-scaled K_n (smooth, close
+    # to dependent like successive solutions)
+    cap = spec.n_pod if strategy == "pod" else spec.max_cols
+    v = b / np.linalg.norm(b)
+    hist = []
+    for _ in range(cap):
+        v = inv * m.kn_apply(v)
+        v = v / np.linalg.norm(v)
+        hist.append(v)
+    lo_m = max(1, cap // 3)
+
+    def start_cost(mm):
+        if strategy == "pod":
+            snap = O.Snapshots(n, spec.n_pod, 1e-4)
+            for u in hist[:mm]:
+                snap.push(u)
+            ts = time.perf_counter()
+            _, k, _, _ = O.pod_start(snap, b, m.kn_apply)
+            return time.perf_counter() - ts, k
+        cache = O.SpeCache(n, m.kn_apply, spec.max_cols, spec.rel_tol)
+        for u in hist[:mm]:
+            cache.insert(u)
+        ts = time.perf_counter()
+        cache.project(b)
+        return time.perf_counter() - ts, cache.k
+    (t_lo, _), (t_hi, k_hi) = start_cost(lo_m), start_cost(cap)
+    # one observe with a full history
+    if strategy == "pod":
+        snap = O.Snapshots(n, spec.n_pod, 1e-4)
+        for u in hist:
+            snap.push(u)
+        ts = time.perf_counter()
+        snap.push(b)
+        t_obs = time.perf_counter() - ts
+    else:
+        cache = O.SpeCache(n, m.kn_apply, spec.max_cols, spec.rel_tol)
+        for u in hist:
+            cache.insert(u)
+        ts = time.perf_counter()
+        cache.insert(b / np.linalg.norm(b) + hist[0])
+        t_obs = time.perf_counter() - ts
+    # the step's remaining work (schur.py:379-419, model.py:415-425)
+    rng = np.random.default_rng(0)
+    a_c = rng.standard_normal(m.n_c) * 1e-4
+    y1, y2 = rng.standard_normal(n), rng.standard_normal(n)
+    cells = O.default_probe_cells(m, (spec.N,) * 3)
+    minv = 1.0 / m.mc_diag
+    ts = time.perf_counter()
+    m.kcn.T @ a_c
+    m.kcn.T @ a_c
+    rate = m.kcn @ (y1 - y2) - m.kc_apply(a_c, a_c)
+    a_next = a_c + spec.dt * (minv * rate)
+    np.isfinite(a_next).all()
+    a_n = y1 - y2
+    O.probe_b(m, O.full_interior(m, a_next, a_n), cells)
+    t_rest = time.perf_counter() - ts
+
+    def t_start(mm):
+        if mm <= 0:
+            return 0.0
+        return t_lo + (t_hi - t_lo) * (min(mm, cap) - lo_m) / max(cap - lo_m, 1)
+
+    its, fixture = oracle_iterations(index, strategy)
+    tail = its[-10:].mean(axis=0)
+    total = 0.0
+    for s in range(warmup + 1, warmup + steps + 1):
+        row = its[s - 1] if s <= len(its) else tail
+        # history sizes before each solve (one record per solve, FIFO/ring cap)
+        hsz = [min(cap, 2 * s - 1), min(cap, s - 1), min(cap, 2 * s), min(cap, s)]
+        total += sum(t_init + float(row[q]) * t_it + t_start(hsz[q]) + t_obs for q in range(4)) + t_rest
+    covered = min(warmup + steps, len(its)) - warmup
+    sample = (f"config {index} ({spec.N}^3, {strategy}) steps {warmup + 1}..{warmup + steps}: oracle/mq_oracle.py "
+              f"(numpy/scipy port of mqsolve) on this host, per-part timing x the oracle's own iteration counts "
+              f"of those steps (tests/golden/fields_{fixture}.npz covers {max(covered, 0)} of them, the rest at "
+              f"the mean of its last 10 steps): PCG iteration {t_it * 1e3:.1f} ms, initial residual "
+              f"{t_init * 1e3:.1f} ms, start vector {t_lo * 1e3:.0f} ms ({lo_m} columns) .. {t_hi * 1e3:.0f} ms "
+              f"({cap} columns, k = {k_hi}), observe {t_obs * 1e3:.0f} ms, rest {t_rest * 1e3:.0f} ms; "
+              f"assembly {t_asm:.0f} s not counted; scipy csr_matvec single-threaded, numpy BLAS on all cores")
+    parts = {"pcg_iteration_ms": t_it * 1e3, "initial_residual_ms": t_init * 1e3,
+             "start_vector_ms": [t_lo * 1e3, t_hi * 1e3], "start_vector_columns": [lo_m, cap],
+             "observe_ms": t_obs * 1e3, "rest_ms": t_rest * 1e3,
+             "timed_step_iterations": its[warmup:warmup + steps].tolist()}
+    return steps / total, total, sample, parts, n
+
+
+def host_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cores": os.cpu_count(), "cpu_model": model,
+            "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS", "default (all cores)")}
 
 
 def run_reference_arm(args):
-    world, rank, local, dist = 1, int(os.environ.get("RANK", "0")), 0, None
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from paper_1611_06721_b200 import configs as C
-    spec = C.config_spec(1)
-    # each step is a full step of the trajectory (~7 s on 16 cores); the
-    # timed loop stops after ~150 s so that any --steps ends in a few minutes
-    v, done, el, n_n = cpu_reference(spec, args.warmup, args.steps, budget_s=150.0)
-    cores = os.cpu_count()
+    spec = C.config_spec(2)
+    v, el, sample, parts, n_n = cpu_sampled_steps(2, "pod", args.warmup, args.steps, iters=(5, 45))
+    hi = host_info()
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference",
-        "n_gpus": args.gpus, "steps": done, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * el / max(done, 1), "higher_is_better": True,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * el / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg1_64cube_brauer_cspe5", "grid": [64, 64, 64], "n_n": n_n,
-                   "strategy": "cspe", "max_cols": 5, "rel_tol": 1e-8, "dt": spec.dt},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"steps {args.warmup + 1}..{args.warmup + done} of config 1 "
-                                   "(oracle/mq_oracle.py: numpy/scipy port of mqsolve; scipy "
-                                   "csr_matvec single-threaded, OpenBLAS dots on all cores)"},
+        "config": {"workload": "cfg2_128cube_two_blocks_pod30", "grid": [128, 128, 128], "n_n": n_n,
+                   "strategy": "pod", "n_pod": 30, "rel_tol": 1e-8, "dt": spec.dt},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": hi["cores"], "kind": "port", "sample": sample,
+                         "host": hi, "parts": parts},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -282,10 +396,10 @@ def time_device_steps(op, spec, warmup, steps, flush=True, dt=None):
 
 def time_e2e(problem, spec, warmup, steps):
     """Same steps through the host-facing API (explicit_euler_step +
-    recover_an with host arrays; copies inside the timed region)."""
+    recover_an + probe_b with host arrays; copies inside the timed region)."""
     from paper_1611_06721_b200 import PcgConfig, SchurOperator, explicit_euler_step, recover_an
     op = SchurOperator(problem, pcg=PcgConfig(rel_tol=spec.rel_tol, max_iter=spec.max_iter),
-                       strategy="cspe", max_cols=spec.max_cols)
+                       strategy=spec.strategy, max_cols=spec.max_cols, n_pod=spec.n_pod)
     op.set_probe()
     a = np.zeros(op.grid.n_c)
     t = 0.0
@@ -323,11 +437,13 @@ def traffic_for(key, iters):
     return float(t["dram_bytes_per_iteration"] * its.mean())
 
 
-def cfg_steps(index, warmup=3, steps=5, strategy=None):
-    """configs[2] (128^3, POD-30), configs[4] (256^3, CSPE k=5, one GPU) or
-    configs[1] with its second start-vector strategy (POD-20) through the
-    same device step loop: steps/s with L2 flushed before each step.
-    Secondary lines; the headline is config 1 with CSPE."""
+def cfg_steps(index, warmup=3, steps=5, strategy=None, with_roofline=None):
+    """configs[1] (64^3, CSPE k=5 or POD-20) or configs[4] (256^3, CSPE k=5,
+    one GPU) through the same device step loop: steps/s with L2 flushed before
+    each step.  Secondary keys; the headline is configs[2].
+    with_roofline=<HBM peak>: the PCG kernel's bytes/s inside the timed steps,
+    labelled by what bounds it (configs[1]: every PCG vector fits in L2 and
+    shared memory, so it is not an HBM figure)."""
     from dataclasses import replace
 
     from paper_1611_06721_b200 import PcgConfig, SchurOperator, configs as C
@@ -337,15 +453,29 @@ def cfg_steps(index, warmup=3, steps=5, strategy=None):
     op = SchurOperator(C.make_problem(index), pcg=PcgConfig(rel_tol=spec.rel_tol, max_iter=spec.max_iter),
                        strategy=spec.strategy, n_pod=spec.n_pod, max_cols=spec.max_cols)
     op.set_probe()
+    kname, kgrid = op.grid.pcg_kernel()
+    n_n = op.grid.n_n
     step_ms, pcg_ms, iters, launches = time_device_steps(op, spec, warmup, steps)
     op.grid.close()
     n = spec.N
-    return {"workload": spec.name, "grid": [n, n, n], "strategy": spec.strategy,
-            "n_pod" if spec.strategy == "pod" else "max_cols": spec.n_pod if spec.strategy == "pod" else spec.max_cols,
-            "dt": spec.dt, "steps_after_warmup": [warmup + 1, warmup + steps],
-            "value": steps / (float(step_ms.sum()) * 1e-3), "unit": UNIT,
-            "ms_per_step": float(step_ms.mean()), "pcg_share_of_step": float(pcg_ms.sum() / step_ms.sum()),
-            "timed_step_iterations": iters.tolist(), "gpu_launches": launches}
+    out = {"workload": spec.name, "grid": [n, n, n], "strategy": spec.strategy,
+           "n_pod" if spec.strategy == "pod" else "max_cols": spec.n_pod if spec.strategy == "pod" else spec.max_cols,
+           "dt": spec.dt, "steps_after_warmup": [warmup + 1, warmup + steps],
+           "value": steps / (float(step_ms.sum()) * 1e-3), "unit": UNIT,
+           "ms_per_step": float(step_ms.mean()), "pcg_share_of_step": float(pcg_ms.sum() / step_ms.sum()),
+           "timed_step_iterations": iters.tolist(), "gpu_launches": launches}
+    if with_roofline:
+        byts = pcg_launch_bytes(n_n, iters.reshape(-1)).sum()
+        ach = byts / (float(pcg_ms.sum()) * 1e-3) / 1e9
+        out["roofline"] = {
+            "bound": "latency (L2/shared-memory resident)", "achieved": ach, "unit": "GB/s",
+            "frac_of_hbm_peak": ach / with_roofline, "kernel": kname, "kernel_grid": kgrid,
+            "us_per_iteration": 1000.0 * float(pcg_ms.sum()) / max(int(iters.sum()), 1),
+            "traffic": traffic_for(f"cfg{index}", iters.reshape(-1)),
+            "note": "72 B/dof/iteration convention; the 64^3 vectors (5.7 MB) stay in shared memory and L2, "
+                    "DRAM traffic is ~0.3 % of it: the kernel is bound by its grid barriers and "
+                    "shared-memory passes, not by HBM"}
+    return out
 
 
 def cfg_pcg_roofline(index, hbm_peak, reps=2):
@@ -400,11 +530,11 @@ def run_device_arm(args):
     from paper_1611_06721_b200 import PcgConfig, SchurOperator, _lib
     from paper_1611_06721_b200 import configs as C
     _lib.load()
-    spec = C.config_spec(1)
-    problem, factors, dt_member = member_problem(rank)
+    spec = C.config_spec(2)
+    problem = C.make_problem(2)
     hbm_peak, peak_kind = peaks()
     op = SchurOperator(problem, pcg=PcgConfig(rel_tol=spec.rel_tol, max_iter=spec.max_iter),
-                       strategy="cspe", max_cols=spec.max_cols, device=local)
+                       strategy=spec.strategy, n_pod=spec.n_pod, device=local)
     # B_probe per output row, as the reference bench records (bench.py:371)
     op.set_probe()
     n_n, n_c = op.grid.n_n, op.grid.n_c
@@ -412,64 +542,66 @@ def run_device_arm(args):
     barrier(dist)
     with ClockSampler(local) as clk:
         step_ms, pcg_ms, iters, launches = time_device_steps(op, spec, args.warmup, args.steps,
-                                                             flush=not args.no_flush, dt=dt_member)
+                                                             flush=not args.no_flush)
     barrier(dist)
     total_ms = float(step_ms.sum())
     total_ms_max = max_over_ranks(total_ms, dist, local)
     value = world * args.steps / (total_ms_max * 1e-3)
-    # roofline of the dominant kernel inside the timed region
+    # roofline of the dominant kernel inside the timed region: algorithmic
+    # bytes of every PCG launch of the timed steps / their CUDA-event time
     launch_bytes = pcg_launch_bytes(n_n, iters.reshape(-1)).sum()
     pcg_total = float(pcg_ms.sum())
     achieved = launch_bytes / (pcg_total * 1e-3) / 1e9 if pcg_total > 0 else 0.0
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": traffic_for("cfg1", iters.reshape(-1)),
+                "frac": achieved / hbm_peak, "traffic": traffic_for("cfg2", iters.reshape(-1)),
+                "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per iteration) x this "
+                                  "run's mean iterations per launch",
                 "kernel": kname, "kernel_grid": kgrid,
                 "peak_kind": peak_kind, "pcg_share_of_step": pcg_total / total_ms,
                 "pcg_launches": int(iters.size), "pcg_iterations": int(iters.sum()),
-                "note": "config-1 PCG vectors (4 x 5.7 MB) are L2-resident inside a solve; "
-                        "see roofline_cfg2 for the HBM-bound 128^3 case"}
+                "bytes_per_iteration": 72.0 * n_n,
+                "us_per_iteration": 1000.0 * pcg_total / max(int(iters.sum()), 1),
+                "algorithmic_bytes": "72 B per dof per iteration (9 fp64 streams) + 32 B/dof initial residual "
+                                     "+ 24 B/dof final x update per launch (pcg_launch_bytes)"}
     op.grid.close()
     line = None
     if rank == 0:
         # the device leg's steps, host-timed three times from a fresh
-        # operator: a host hiccup in one 10-step (30 ms) window moved a single
-        # run by up to 20 %, so the median run is reported
+        # operator; the median run is reported
         e2e_runs = [time_e2e(problem, spec, args.warmup, args.steps) for _ in range(3)]
         e2e_vals = [r[0] for r in e2e_runs]
         e2e_v = float(np.median(e2e_vals))
         _, e2e_s, h2d, d2h = e2e_runs[int(np.argsort(e2e_vals)[1])]
-        roof2 = steps2 = roof4 = steps4 = None
-        pod1 = cfg_steps(1, warmup=args.warmup, steps=args.steps, strategy="pod")
-        if not args.skip_cfg2:
-            roof2 = cfg_pcg_roofline(2, hbm_peak)
-            steps2 = cfg_steps(2)
+        cfg1 = cfg1_pod = roof4 = steps4 = None
+        if not args.skip_secondary:
+            cfg1 = cfg_steps(1, warmup=args.warmup, steps=args.steps, with_roofline=hbm_peak)
+            cfg1_pod = cfg_steps(1, warmup=args.warmup, steps=args.steps, strategy="pod")
         if not args.skip_cfg4:
             roof4 = cfg_pcg_roofline(4, hbm_peak, reps=1)
             steps4 = cfg_steps(4, warmup=1, steps=2)
         cpu = None
         if world == 1 and not args.skip_cpu:
-            v, done, el, _ = cpu_reference(spec, 0, args.cpu_steps, budget_s=30.0)
-            cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                   "sample": f"first {done} steps of config 1 ({el:.1f} s; oracle/mq_oracle.py, "
-                             "numpy/scipy port of mqsolve; csr_matvec single-threaded)"}
+            v, el, sample, parts, _ = cpu_sampled_steps(2, "pod", args.warmup, args.steps)
+            hi = host_info()
+            cpu = {"value": v, "unit": UNIT, "cores": hi["cores"], "kind": "port", "sample": sample,
+                   "host": hi, "parts": parts}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (SURVEY 8(d) geometry: iron block + annular coil, seeded ensemble factors)",
-            "config": {"workload": "cfg1_64cube_brauer_cspe5", "grid": [64, 64, 64],
-                       "n_n": n_n, "n_c": n_c, "strategy": "cspe", "max_cols": 5,
+            "data": "synthetic (SURVEY 8(d) geometry: two iron blocks + annular coil)",
+            "config": {"workload": "cfg2_128cube_two_blocks_pod30", "grid": [128, 128, 128],
+                       "n_n": n_n, "n_c": n_c, "strategy": "pod", "n_pod": spec.n_pod, "eps_pod": 1e-4,
                        "rel_tol": spec.rel_tol, "dt": spec.dt,
+                       "steps_timed": [args.warmup + 1, args.warmup + args.steps],
                        "l2": "flushed (256 MB write) before every timed step" if not args.no_flush else "not flushed",
-                       "parallelism": f"replicas{world} (ensemble members, no collectives)",
-                       "member_factors": factors},
+                       "parallelism": f"replicas{world} (configs 0-2 do not shard; no collectives)"},
             "timed_step_iterations": iters.tolist(),
             "clocks": clk.summary(),
             "roofline": roofline,
-            "roofline_cfg2": roof2,
-            "cfg1_pod_steps": pod1,
-            "cfg2_steps": steps2,
+            "cfg1_cspe_steps": cfg1,
+            "cfg1_pod_steps": cfg1_pod,
             "roofline_cfg4_1gpu": roof4,
             "cfg4_steps_1gpu": steps4,
             "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -488,14 +620,13 @@ def run_device_arm(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-flush", action="store_true")
-    ap.add_argument("--skip-cfg2", action="store_true")
+    ap.add_argument("--skip-secondary", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-cfg4", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -21,6 +21,7 @@
 // Streams per iteration (fp64, per dof): K1 reads r, p_old, x and writes
 // x, p_new, Ap; K2 reads r, Ap and writes r  ->  9 x 8 B = 72 B.
 #include <cuda.h>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <cudaTypedefs.h>
@@ -33,7 +34,10 @@ namespace mq {
 constexpr int TJ = 8, TK = 32;                 // kBlock = TJ * TK threads
 constexpr int HJ = TJ + 2, HK = TK + 2, HP = HJ * HK;  // 10 x 34 box
 constexpr int BOXP = 352;                      // box slot padded to a 128-byte multiple
-constexpr int NST = 5;                         // stages: planes i-1, i, i+1 + 2 in flight
+#ifndef MQ_NST
+#define MQ_NST 5
+#endif
+constexpr int NST = MQ_NST;                    // stages: planes i-1, i, i+1 + NST-3 in flight
 constexpr int NHALO = 2 * HK + 2 * TJ;         // 84 halo positions per plane
 static_assert(TJ * TK == kBlock, "one thread per tile position");
 static_assert(HP <= BOXP && (BOXP * 8) % 128 == 0, "TMA destination alignment");
@@ -157,6 +161,9 @@ struct MarchCtx {
   Stage *st;
   uint64_t *bars;
   uint32_t ph;  // per-stage mbarrier parity (identical in every thread)
+#ifdef MQ_TRACE_MARCH
+  unsigned long long *tr = nullptr;  // CTA 0 thread 0, one iteration: 4 stamps per plane step
+#endif
 };
 
 struct NoPush {
@@ -180,14 +187,18 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   const int64_t pos_own = L.off + (int64_t)j * L.Sj + k;
   const bool with_p = (MODE == kK1) && !first;
   const uint32_t bytes = (with_p ? 6u : 3u) * HP * 8u;
-  // halo slot converted by this thread (threads 0..NHALO-1), besides its own
-  int hs = -1;
-  if (tid < NHALO) {
+  // halo (slot, component) converted by this thread besides its own
+  // position: the 84 halo positions x 3 components are spread over threads
+  // 0..251, one each, so that no warp carries three times the work
+  int hs = -1, hc = 0;
+  if (tid < 3 * NHALO) {
+    const int h = tid % NHALO;
+    hc = tid / NHALO;
     int hj, hk;
-    if (tid < HK) { hj = 0; hk = tid; }
-    else if (tid < 2 * HK) { hj = TJ + 1; hk = tid - HK; }
-    else if (tid < 2 * HK + TJ) { hj = 1 + (tid - 2 * HK); hk = 0; }
-    else { hj = 1 + (tid - 2 * HK - TJ); hk = TK + 1; }
+    if (h < HK) { hj = 0; hk = h; }
+    else if (h < 2 * HK) { hj = TJ + 1; hk = h - HK; }
+    else if (h < 2 * HK + TJ) { hj = 1 + (h - 2 * HK); hk = 0; }
+    else { hj = 1 + (h - 2 * HK - TJ); hk = TK + 1; }
     hs = hj * HK + hk;
   }
   const double inv = a.inv;
@@ -239,8 +250,14 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     for (int c = 0; c < 3; ++c) { mw[c] = mw_nx[c]; xo[c] = xo_nx[c]; }
     prefetch_own(next_q, next_own);
     const int64_t qb = (int64_t)q * L.Si;
+#ifdef MQ_TRACE_MARCH
+    if (mc.tr && q - i0 >= 1 && q - i0 < 33) mc.tr[4 * (q - i0 - 1) + 0] = globaltimer_ns();
+#endif
     mbar_wait(&mc.bars[s], (mc.ph >> s) & 1u);
     mc.ph ^= (1u << s);
+#ifdef MQ_TRACE_MARCH
+    if (mc.tr && q - i0 >= 1 && q - i0 < 33) mc.tr[4 * (q - i0 - 1) + 1] = globaltimer_ns();
+#endif
     uint32_t act = 0u;
     if (own_plane && own_ok) {
 #pragma unroll
@@ -268,25 +285,28 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       }
     }
     if (hs >= 0) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double rq = S.r[c][hs];
-        const double z = jac ? mul(inv, rq) : rq;
-        S.r[c][hs] = first ? z : add(z, mul(beta, S.p[c][hs]));
-      }
+      const double rq = S.r[hc][hs];
+      const double z = jac ? mul(inv, rq) : rq;
+      S.r[hc][hs] = first ? z : add(z, mul(beta, S.p[hc][hs]));
     }
     return act;
   };
 
   // prologue: planes i0-1 .. i0+2 in flight, convert i0-1 and i0
   const int last = i1;  // planes i0-1 .. i1 are needed
-  for (int q = i0 - 1; q <= i0 + 2 && q <= last; ++q) issue(q);
+  for (int q = i0 - 1; q <= i0 + NST - 3 && q <= last; ++q) issue(q);
   convert(i0 - 1, false, i0, true);
   uint32_t act = convert(i0, true, i0 + 1, i0 + 1 < i1);
   for (int i = i0; i < i1; ++i) {
     const uint32_t act_next = convert(i + 1, i + 1 < i1, i + 2, i + 2 < i1);
+#ifdef MQ_TRACE_MARCH
+    if (mc.tr) mc.tr[4 * (i - i0) + 2] = globaltimer_ns();
+#endif
     __syncthreads();
-    if (i + 3 <= last) issue(i + 3);  // into the stage of plane i-2: free after this barrier
+#ifdef MQ_TRACE_MARCH
+    if (mc.tr) mc.tr[4 * (i - i0) + 3] = globaltimer_ns();
+#endif
+    if (i + NST - 2 <= last) issue(i + NST - 2);  // into the stage of plane i-2: free after this barrier
     if (act) {
       const int64_t qb = (int64_t)i * L.Si;
       const int sm1 = stage_of(i - 1), s0 = stage_of(i), sp1 = stage_of(i + 1);
@@ -417,6 +437,9 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       const CUtensorMap *mp = pold_is_a ? &A.tm_pa : &A.tm_pb;
       // ---- K1 ----
       double v1[1] = {0.0};
+#ifdef MQ_TRACE_MARCH
+      mc.tr = (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && it == 10) ? a.trace + 1300 : nullptr;
+#endif
       for (int bi = blockIdx.x; bi < g.nbricks; bi += G) {
         int i0, i1, j0, k0;
         brick_of(g, bi, i0, i1, j0, k0);
@@ -824,12 +847,12 @@ static int get_encoder() {
 
 // 4-D view (k, j, i, c) of a padded device vector including the guard layer
 // (coordinate 0 = node -1); box = tile + 1-node halo.
-int make_vec_map(const Lay &L, int nx, int ny, int nz, const double *base, CUtensorMap *map) {
+int make_vec_map(const Lay &L, int nx, int ny, int nz, const double *base, CUtensorMap *map, int bk = HK, int bj = HJ) {
   int rc = get_encoder();
   if (rc) return rc;
   cuuint64_t dims[4] = {(cuuint64_t)nz + 2, (cuuint64_t)ny + 2, (cuuint64_t)nx + 2, 3};
   cuuint64_t strides[3] = {(cuuint64_t)L.Sj * 8, (cuuint64_t)L.Si * 8, (cuuint64_t)L.C * 8};
-  cuuint32_t box[4] = {HK, HJ, 1, 1};
+  cuuint32_t box[4] = {(cuuint32_t)bk, (cuuint32_t)bj, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   // the map starts at node (-1,-1,-1) of component 0: index off - Si - Sj - 1 = 0
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)base, dims, strides, box, estr,
@@ -865,6 +888,26 @@ static BrickGeo make_geo(int nx, int ny, int nz, int resident) {
   return g;
 }
 
+// Shared-memory carveout of the TMA kernels: the smallest preference at which
+// the occupancy calculator places two CTAs per SM, so the rest stays L1.  The
+// L1 share matters: with the largest carveout (28 KB L1) the global loads and
+// stores of K1 throttle (ncu stall_lg 0.61 -> 1.53 per issue) and an iteration
+// at 128^3 takes 104 instead of 94 us; left to the driver the carveout
+// sometimes fits only one CTA per SM (118 us).  MQ_PCG_CARVEOUT overrides.
+static cudaError_t two_cta_carveout(const void *fn) {
+  int pct = 100;
+  for (int c = 50; c <= 100; ++c) {
+    int per2 = 0;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, fn, kBlock, kTmaSmem);
+    if (e != cudaSuccess) return e;
+    if (per2 >= 2) { pct = c; break; }
+  }
+  if (const char *v = getenv("MQ_PCG_CARVEOUT")) pct = atoi(v);
+  if (getenv("MQ_PCG_VERBOSE")) fprintf(stderr, "TMA kernel carveout preference %d %%\n", pct);
+  return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct < 100 ? pct : 100);
+}
+
 int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int sm_cap, int *grid, BrickGeo *geo) {
   (void)L;
   int dev = 0, sms = 0, per = 0;
@@ -873,7 +916,10 @@ int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int sm_cap, int *grid,
   if (sm_cap > 0 && sm_cap < sms) sms = sm_cap;
   MQ_CUDA(cudaFuncSetAttribute(pcg_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
   MQ_CUDA(cudaFuncSetAttribute(kn_apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+  MQ_CUDA(two_cta_carveout((const void *)pcg_tma_kernel));
+  MQ_CUDA(two_cta_carveout((const void *)kn_apply_tma_kernel));
   MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pcg_tma_kernel, kBlock, kTmaSmem));
+  if (getenv("MQ_PCG_VERBOSE")) fprintf(stderr, "pcg_tma_kernel: %d CTAs per SM, %zu B smem\n", per, kTmaSmem);
   if (per < 1) { set_error("TMA PCG kernel cannot be resident"); return MQ_CUDA_ERROR; }
   if (const char *v = getenv("MQ_BRICK_CTAS_PER_SM")) {
     const int want = atoi(v);
@@ -912,6 +958,7 @@ int launch_pcg_tma_slab(const StencilPcgArgs *args, const SlabRank *ranks, const
   MQ_CUDA(cudaGetDevice(&dev));
   MQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   MQ_CUDA(cudaFuncSetAttribute(pcg_tma_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+  MQ_CUDA(two_cta_carveout((const void *)pcg_tma_slab_kernel));
   MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pcg_tma_slab_kernel, kBlock, kTmaSmem));
   if (per < 1) { set_error("TMA slab PCG kernel cannot be resident"); return MQ_CUDA_ERROR; }
   const int Gr = (sms * per) / ngroups;

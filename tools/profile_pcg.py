@@ -58,6 +58,21 @@ def main():
         print(f"  per-iteration us (CTA 0, iterations 2..{n}): K1 {k1[1:].mean()/1e3:.2f}  barrier1 "
               f"{b1[1:].mean()/1e3:.2f}  K2 {k2[1:].mean()/1e3:.2f}  barrier2 {b2[1:].mean()/1e3:.2f}  "
               f"(init {k1[0]/1e3:.2f})")
+    if os.environ.get("MQ_TRACE_MARCH"):
+        # pcg_tma_kernel built with -DMQ_TRACE_MARCH: CTA 0, iteration 10, per
+        # plane step i: [before TMA wait of plane i+1, after it, after the
+        # convert, after the __syncthreads]; the stencil of plane i follows
+        import numpy as np
+        st = np.zeros(1300 + 4 * 33, dtype=np.uint64)
+        check(lib.mq_pcg_trace(g.ctx, st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), st.size))
+        m = st[1300:1300 + 4 * 31].reshape(31, 4).astype(np.float64)
+        wait = m[:, 1] - m[:, 0]
+        conv = m[:, 2] - m[:, 1]
+        sync = m[:, 3] - m[:, 2]
+        sten = m[1:, 0] - m[:-1, 3]
+        print(f"  march us per plane step (CTA 0): TMA wait {wait[2:].mean()/1e3:.3f}  convert {conv[2:].mean()/1e3:.3f}  "
+              f"syncthreads {sync[2:].mean()/1e3:.3f}  stencil+prefetch {sten[2:].mean()/1e3:.3f}  "
+              f"step {np.diff(m[:, 0])[2:].mean()/1e3:.3f}")
     if os.environ.get("MQ_TRACE_FINE") and g.pcg_kernel()[0].startswith("pcg_resident1"):
         # single-reduction kernel: fine stamps 0..3 = loop top, stencil + dots
         # + Ap stores done, partial sums read, own + halo update done;
