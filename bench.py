@@ -184,7 +184,7 @@ def oracle_iterations(index: int, strategy: str):
     return np.stack([src[:, 0], f["iters_prev"], src[:, 1], f["iters_cur"][1:]], axis=1), name
 
 
-def cpu_sampled_steps(index: int, strategy: str, warmup: int, steps: int, *, iters=(4, 24)):
+def cpu_sampled_steps(index: int, strategy: str, warmup: int, steps: int, *, iters=(35, 105), kept_modes=4):
     """steps/s of the CPU port (oracle/mq_oracle.py, a numpy/scipy restatement
     of mqsolve) on steps warmup+1 .. warmup+steps, from a bounded sample.
 
@@ -193,8 +193,10 @@ def cpu_sampled_steps(index: int, strategy: str, warmup: int, steps: int, *, ite
     assembled matrices, the parts a step is made of and adds them up for
     every timed step:
       * t_it: one PCG iteration of the oracle's pcg loop (SpMV, dots, axpys),
-        from two truncated solves of iters[0] and iters[1] iterations;
-      * t_init: the initial residual of a warm-started solve;
+        from two truncated solves of iters[0] and iters[1] iterations (the
+        per-iteration cost falls over the first tens of iterations of a solve
+        as numpy's allocations warm up: 0.27 s at 5, 0.22 s at 105 at 128^3);
+      * t_init: a solve that ends at its initial residual (x0 given);
       * t_start(m): one start vector of the strategy with m columns in the
         family's history (POD: Gram of the ring, eigh, basis, k SpMVs, the
         Galerkin solve; CSPE: the projection) measured at two history sizes and
@@ -219,23 +221,35 @@ def cpu_sampled_steps(index: int, strategy: str, warmup: int, steps: int, *, ite
     n = m.n_n
     b = m.pattern.copy()
     x0 = np.zeros(n)
+    rng0 = np.random.default_rng(1)
 
     def truncated(k):
         ts = time.perf_counter()
         O.pcg(m.kn_apply, b, x0=x0, rel_tol=1e-300, max_iter=k, inv_diag=inv)
         return time.perf_counter() - ts
+    truncated(3)  # first touch of the matrix and of the allocator's pages
     ta, tb = truncated(iters[0]), truncated(iters[1])
     t_it = (tb - ta) / (iters[1] - iters[0])
-    t_init = max(ta - iters[0] * t_it, 0.0)
-    # history columns: Krylov vectors of the Jacobi-scaled K_n (smooth, close
-    # to dependent like successive solutions)
+    # a solve that ends at its initial residual (x0 given, ||r|| <= target)
+    ts = time.perf_counter()
+    for _ in range(3):
+        O.pcg(m.kn_apply, b, x0=x0, rel_tol=1.0, max_iter=1, inv_diag=inv)
+    t_init = (time.perf_counter() - ts) / 3
+    # history columns: successive solutions of one family are smooth and
+    # nearly dependent (POD keeps about kept_modes of them): mixtures of that
+    # many Krylov vectors of the Jacobi-scaled K_n plus a 1e-7 perturbation
     cap = spec.n_pod if strategy == "pod" else spec.max_cols
     v = b / np.linalg.norm(b)
-    hist = []
-    for _ in range(cap):
+    base = []
+    for _ in range(kept_modes):
         v = inv * m.kn_apply(v)
         v = v / np.linalg.norm(v)
-        hist.append(v)
+        base.append(v)
+    hist = []
+    for jj in range(cap):
+        h = sum(np.cos(0.3 * (ii + 1) * jj) * base[ii] for ii in range(kept_modes))
+        h = h + 1e-7 * np.linalg.norm(h) / np.sqrt(n) * rng0.standard_normal(n)
+        hist.append(h)
     lo_m = max(1, cap // 3)
 
     def start_cost(mm):
@@ -270,7 +284,7 @@ def cpu_sampled_steps(index: int, strategy: str, warmup: int, steps: int, *, ite
         t_obs = time.perf_counter() - ts
     # the step's remaining work (schur.py:379-419, model.py:415-425)
     rng = np.random.default_rng(0)
-    a_c = rng.standard_normal(m.n_c) * 1e-4
+    a_c = rng.standard_normal(m.n_c) * 1e-9
     y1, y2 = rng.standard_normal(n), rng.standard_normal(n)
     cells = O.default_probe_cells(m, (spec.N,) * 3)
     minv = 1.0 / m.mc_diag
@@ -331,7 +345,7 @@ def run_reference_arm(args):
         return 0
     from paper_1611_06721_b200 import configs as C
     spec = C.config_spec(2)
-    v, el, sample, parts, n_n = cpu_sampled_steps(2, "pod", args.warmup, args.steps, iters=(5, 45))
+    v, el, sample, parts, n_n = cpu_sampled_steps(2, "pod", args.warmup, args.steps)
     hi = host_info()
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference",
