@@ -34,17 +34,25 @@ namespace mq {
 constexpr int TJ = 8, TK = 32;                 // kBlock = TJ * TK threads
 constexpr int HJ = TJ + 2, HK = TK + 2, HP = HJ * HK;  // 10 x 34 box
 constexpr int BOXP = 352;                      // box slot padded to a 128-byte multiple
-#ifndef MQ_NST
-#define MQ_NST 5
+#ifndef MQ_XDEFER
+#define MQ_XDEFER 1
 #endif
-constexpr int NST = MQ_NST;                    // stages: planes i-1, i, i+1 + NST-3 in flight
+#ifndef MQ_NAHEAD
+#define MQ_NAHEAD 3
+#endif
+// Two shared-memory rings: the r ring holds planes i-1, i, i+1 (converted
+// in place into p_new, read by the stencil) plus NA planes in flight; the
+// p_old ring only the NA in-flight planes (p_old is dead once its plane is
+// converted).  Same bytes as a 5-stage (r, p) ring, one more plane ahead.
+constexpr int NA = MQ_NAHEAD;                  // planes in flight ahead of i+1
+constexpr int NR = NA + 3, NP = NA;            // r-ring and p-ring slots
 constexpr int NHALO = 2 * HK + 2 * TJ;         // 84 halo positions per plane
 static_assert(TJ * TK == kBlock, "one thread per tile position");
 static_assert(HP <= BOXP && (BOXP * 8) % 128 == 0, "TMA destination alignment");
+static_assert(NA >= 1 && NR <= 32, "ring sizes");
 
-struct __align__(128) Stage {
-  double r[3][BOXP];  // raw r, converted in place into p_new (or x0 in the init pass)
-  double p[3][BOXP];  // raw p_old
+struct __align__(128) Box3 {
+  double v[3][BOXP];  // one staged plane of one field, three components
 };
 
 struct TmaPcgArgs {
@@ -53,7 +61,7 @@ struct TmaPcgArgs {
   CUtensorMap tm_r, tm_pa, tm_pb, tm_x;  // 4-D maps (k, j, i, c), box 34 x 10 x 1 x 1
 };
 
-constexpr size_t kTmaSmem = sizeof(Stage) * NST + 128;
+constexpr size_t kTmaSmem = sizeof(Box3) * (NR + NP) + 128;
 
 // ---- PTX helpers ----------------------------------------------------------
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -151,16 +159,18 @@ __device__ __forceinline__ double stencil3(int c, double dg, double of, V v) {
   return s;
 }
 
-__device__ __forceinline__ int stage_of(int q) { return (q + NST) % NST; }  // q >= -1
+__device__ __forceinline__ int rslot(int q) { return (q + NR) % NR; }  // q >= -1
+__device__ __forceinline__ int pslot(int q) { return (q + NP) % NP; }
 
 // One brick of K1 (mode kK1) or of the initial residual r = b - A x0 (mode
 // kInit: the marched field is x0, staged from tm_x).  Uniform per CTA.
 enum { kInit = 0, kK1 = 1 };
 
 struct MarchCtx {
-  Stage *st;
+  Box3 *sr;        // NR slots of r (-> p_new); bars[] is indexed by r slot
+  Box3 *sp;        // NP slots of p_old
   uint64_t *bars;
-  uint32_t ph;  // per-stage mbarrier parity (identical in every thread)
+  uint32_t ph;  // per-slot mbarrier parity (identical in every thread)
 #ifdef MQ_TRACE_MARCH
   unsigned long long *tr = nullptr;  // CTA 0 thread 0, one iteration: 4 stamps per plane step
 #endif
@@ -175,7 +185,8 @@ struct NoPush {
 template <int MODE, class ROW, class PUSH = NoPush>
 __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, const CUtensorMap *mr,
                                           const CUtensorMap *mp, bool first, double beta, double alpha_prev,
-                                          double *pnew, int i0, int i1, int j0, int k0, ROW row,
+                                          int xmode, double alpha_prev2, double *pnew, int i0, int i1, int j0,
+                                          int k0, ROW row,
                                           PUSH push = PUSH()) {
   const StencilPcgArgs &a = A.a;
   const BrickGeo &g = A.g;
@@ -186,6 +197,10 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   const int s_own = (ty + 1) * HK + (tx + 1);
   const int64_t pos_own = L.off + (int64_t)j * L.Sj + k;
   const bool with_p = (MODE == kK1) && !first;
+  // x update of this pass (kK1, !first): 0 none (deferred), 1 x += a1 p_old,
+  // 2 x = (x + a2 p_prev2) + a1 p_old with p_prev2 read from the p_new buffer
+  // at the own position just before it is overwritten
+  const int xm = (MODE == kK1 && !first) ? xmode : 0;
   const uint32_t bytes = (with_p ? 6u : 3u) * HP * 8u;
   // halo (slot, component) converted by this thread besides its own
   // position: the 84 halo positions x 3 components are spread over threads
@@ -208,16 +223,16 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 
   auto issue = [&](int q) {
     if (tid == 0) {
-      const int s = stage_of(q);
+      const int s = rslot(q), sp = pslot(q);
       fence_proxy_async_smem();
       mbar_expect_tx(&mc.bars[s], bytes);
 #pragma unroll
       // box origin (k0-1, j0-1, q) in node coordinates = (k0, j0, q+1) in the
       // guard-shifted map: never negative
-      for (int c = 0; c < 3; ++c) tma_load_4d(mc.st[s].r[c], mr, &mc.bars[s], k0, j0, q + 1, c);
+      for (int c = 0; c < 3; ++c) tma_load_4d(mc.sr[s].v[c], mr, &mc.bars[s], k0, j0, q + 1, c);
       if (with_p) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) tma_load_4d(mc.st[s].p[c], mp, &mc.bars[s], k0, j0, q + 1, c);
+        for (int c = 0; c < 3; ++c) tma_load_4d(mc.sp[sp].v[c], mp, &mc.bars[s], k0, j0, q + 1, c);
       }
     }
   };
@@ -226,6 +241,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   // processed, so neither their latency nor the TMA's is exposed.
   uint32_t mw_nx[3] = {0u, 0u, 0u};
   double xo_nx[3] = {0.0, 0.0, 0.0};
+  double p2_nx[3] = {0.0, 0.0, 0.0};
   auto prefetch_own = [&](int q, bool own_plane) {
     if (own_plane && own_ok) {
       const int64_t qb = (int64_t)q * L.Si;
@@ -233,7 +249,8 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       for (int c = 0; c < 3; ++c) {
         const int64_t e = c * L.C + qb + pos_own;
         mw_nx[c] = __ldg(mask + (e >> 5));
-        if (MODE == kK1 && !first) xo_nx[c] = __ldcg(x + e);
+        if (xm >= 1) xo_nx[c] = __ldcg(x + e);
+        if (xm == 2) p2_nx[c] = __ldcg(pnew + e);
       }
     } else {
 #pragma unroll
@@ -243,11 +260,11 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   // returns the active-dof bits (bit c = component c) of the own position;
   // next_q/next_own describe the plane whose own data is prefetched now
   auto convert = [&](int q, bool own_plane, int next_q, bool next_own) -> uint32_t {
-    const int s = stage_of(q);
+    const int s = rslot(q);
     uint32_t mw[3];
-    double xo[3];
+    double xo[3], p2[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) { mw[c] = mw_nx[c]; xo[c] = xo_nx[c]; }
+    for (int c = 0; c < 3; ++c) { mw[c] = mw_nx[c]; xo[c] = xo_nx[c]; p2[c] = p2_nx[c]; }
     prefetch_own(next_q, next_own);
     const int64_t qb = (int64_t)q * L.Si;
 #ifdef MQ_TRACE_MARCH
@@ -267,36 +284,45 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       }
     }
     if (MODE == kInit) return act;  // the staged x0 is used as is
-    Stage &S = mc.st[s];
+    double (&Sr)[3][BOXP] = mc.sr[s].v;
+    const double (&Sp)[3][BOXP] = mc.sp[pslot(q)].v;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const double rq = S.r[c][s_own];
+      const double rq = Sr[c][s_own];
       const double z = jac ? mul(inv, rq) : rq;
       double pv = z;
       if (!first) {
-        const double po = S.p[c][s_own];
+        const double po = Sp[c][s_own];
         pv = add(z, mul(beta, po));
-        if ((act >> c) & 1u) x[c * L.C + qb + pos_own] = add(xo[c], mul(alpha_prev, po));
+        if (xm >= 1 && ((act >> c) & 1u)) {
+          const double xv = xm == 2 ? add(xo[c], mul(alpha_prev2, p2[c])) : xo[c];
+          x[c * L.C + qb + pos_own] = add(xv, mul(alpha_prev, po));
+        }
       }
-      S.r[c][s_own] = pv;
+      Sr[c][s_own] = pv;
       if ((act >> c) & 1u) {
         pnew[c * L.C + qb + pos_own] = pv;
         push(q, c, pos_own - L.Si, pv);
       }
     }
     if (hs >= 0) {
-      const double rq = S.r[hc][hs];
+      const double rq = Sr[hc][hs];
       const double z = jac ? mul(inv, rq) : rq;
-      S.r[hc][hs] = first ? z : add(z, mul(beta, S.p[hc][hs]));
+      Sr[hc][hs] = first ? z : add(z, mul(beta, Sp[hc][hs]));
     }
     return act;
   };
 
-  // prologue: planes i0-1 .. i0+2 in flight, convert i0-1 and i0
+  // prologue: planes i0-1 .. i0+NA-2 in flight, then convert i0-1 and i0,
+  // each followed by the issue of the plane that takes over its p slot
   const int last = i1;  // planes i0-1 .. i1 are needed
-  for (int q = i0 - 1; q <= i0 + NST - 3 && q <= last; ++q) issue(q);
+  for (int q = i0 - 1; q <= i0 + NA - 2 && q <= last; ++q) issue(q);
   convert(i0 - 1, false, i0, true);
+  __syncthreads();
+  if (i0 + NA - 1 <= last) issue(i0 + NA - 1);
   uint32_t act = convert(i0, true, i0 + 1, i0 + 1 < i1);
+  __syncthreads();
+  if (i0 + NA <= last) issue(i0 + NA);
   for (int i = i0; i < i1; ++i) {
     const uint32_t act_next = convert(i + 1, i + 1 < i1, i + 2, i + 2 < i1);
 #ifdef MQ_TRACE_MARCH
@@ -306,16 +332,18 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 #ifdef MQ_TRACE_MARCH
     if (mc.tr) mc.tr[4 * (i - i0) + 3] = globaltimer_ns();
 #endif
-    if (i + NST - 2 <= last) issue(i + NST - 2);  // into the stage of plane i-2: free after this barrier
+    // r slot of plane i-2 (its last stencil was before this barrier), p slot
+    // of plane i+1 (converted before this barrier)
+    if (i + NA + 1 <= last) issue(i + NA + 1);
     if (act) {
       const int64_t qb = (int64_t)i * L.Si;
-      const int sm1 = stage_of(i - 1), s0 = stage_of(i), sp1 = stage_of(i + 1);
+      const int sm1 = rslot(i - 1), s0 = rslot(i), sp1 = rslot(i + 1);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         if ((act >> c) & 1u)
           row(c, c * L.C + qb + pos_own, [&](int cc, int di, int dj, int dk) {
             const int s = di < 0 ? sm1 : (di == 0 ? s0 : sp1);
-            return mc.st[s].r[cc][s_own + dj * HK + dk];
+            return mc.sr[s].v[cc][s_own + dj * HK + dk];
           });
       }
     }
@@ -338,7 +366,7 @@ __device__ __forceinline__ void flat_pairs(int64_t total, F f) {
 
 __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constant__ TmaPcgArgs A) {
   extern __shared__ __align__(128) unsigned char dsm[];
-  __shared__ __align__(8) uint64_t bars[NST];
+  __shared__ __align__(8) uint64_t bars[NR];
   __shared__ double red[3 * kWarps];
   __shared__ double tot[4];
   const StencilPcgArgs &a = A.a;
@@ -359,11 +387,12 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
     return;
   }
   MarchCtx mc;
-  mc.st = reinterpret_cast<Stage *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sr = reinterpret_cast<Box3 *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sp = mc.sr + NR;
   mc.bars = bars;
   mc.ph = 0u;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NR; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -378,7 +407,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
     for (int bi = blockIdx.x; bi < g.nbricks; bi += G) {
       int i0, i1, j0, k0;
       brick_of(g, bi, i0, i1, j0, k0);
-      march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, nullptr, i0, i1, j0, k0,
+      march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
                        [&](int c, int64_t e, auto V) {
                          const double bv = __ldcg(b + e);
                          const double rv = sub(bv, stencil3(c, dg, of, V));
@@ -430,12 +459,25 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
     rz = jac ? s3[2] : s3[1];
     auto relf = [&](double res) { return bnorm > 0.0 ? res / bnorm : (res == 0.0 ? 0.0 : INFINITY); };
     if (rnorm <= target) { converged = 1; rel = relf(rnorm); goto done; }
-    double beta = 0.0, alpha_prev = 0.0;
+    double beta = 0.0, alpha_prev = 0.0, alpha_prev2 = 0.0;
     bool first = true;
+    // deferred x update: x += alpha_{it-1} p_{it-1} is applied every second
+    // K1 together with the pending alpha_{it-2} p_{it-2} (same roundings in
+    // the same order, one x read/write per two iterations)
+    bool pend = false;
     for (int it = 1; it <= a.max_iter; ++it) {
       double *pnew = pold_is_a ? a.pb : a.pa;
       const CUtensorMap *mp = pold_is_a ? &A.tm_pa : &A.tm_pb;
       // ---- K1 ----
+      int xmode = 0;
+      if (!first) {
+#if MQ_XDEFER
+        xmode = pend ? 2 : 0;
+        pend = !pend;
+#else
+        xmode = 1;
+#endif
+      }
       double v1[1] = {0.0};
 #ifdef MQ_TRACE_MARCH
       mc.tr = (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && it == 10) ? a.trace + 1300 : nullptr;
@@ -443,7 +485,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       for (int bi = blockIdx.x; bi < g.nbricks; bi += G) {
         int i0, i1, j0, k0;
         brick_of(g, bi, i0, i1, j0, k0);
-        march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, pnew, i0, i1, j0, k0,
+        march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0,
                        [&](int c, int64_t e, auto V) {
                          const double av = stencil3(c, dg, of, V);
                          ap[e] = av;
@@ -508,6 +550,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       if (!isfinite(rz_new)) { status = MQ_INDEFINITE; break; }
       beta = rz_new / rz;
       rz = rz_new;
+      alpha_prev2 = alpha_prev;
       alpha_prev = alpha;
       first = false;
       pold_is_a = !pold_is_a;
@@ -516,20 +559,42 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       // last direction: p_new of the last iteration (swapped into pold when
       // the budget ran out)
       const double *pdir = converged ? (pold_is_a ? a.pb : a.pa) : (pold_is_a ? a.pa : a.pb);
-      flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
-        double2 xv[kUnroll], pv[kUnroll];
+      // the pending alpha_{K-1} p_{K-1} (deferred x update), applied first
+      const double *pdir2 = converged ? (pold_is_a ? a.pa : a.pb) : (pold_is_a ? a.pb : a.pa);
+      const double alpha2 = converged ? alpha_prev : alpha_prev2;
+      if (pend) {
+        flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
+          double2 xv[kUnroll], pv[kUnroll], qv[kUnroll];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
-          if (u < n) {
-            xv[u] = __ldcg(reinterpret_cast<const double2 *>(x) + p + u * stride);
-            pv[u] = __ldcg(reinterpret_cast<const double2 *>(pdir) + p + u * stride);
-          }
+          for (int u = 0; u < kUnroll; ++u)
+            if (u < n) {
+              xv[u] = __ldcg(reinterpret_cast<const double2 *>(x) + p + u * stride);
+              qv[u] = __ldcg(reinterpret_cast<const double2 *>(pdir2) + p + u * stride);
+              pv[u] = __ldcg(reinterpret_cast<const double2 *>(pdir) + p + u * stride);
+            }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
-          if (u < n)
-            reinterpret_cast<double2 *>(x)[p + u * stride] =
-                make_double2(add(xv[u].x, mul(alpha, pv[u].x)), add(xv[u].y, mul(alpha, pv[u].y)));
-      });
+          for (int u = 0; u < kUnroll; ++u)
+            if (u < n)
+              reinterpret_cast<double2 *>(x)[p + u * stride] =
+                  make_double2(add(add(xv[u].x, mul(alpha2, qv[u].x)), mul(alpha, pv[u].x)),
+                               add(add(xv[u].y, mul(alpha2, qv[u].y)), mul(alpha, pv[u].y)));
+        });
+      } else {
+        flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
+          double2 xv[kUnroll], pv[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u)
+            if (u < n) {
+              xv[u] = __ldcg(reinterpret_cast<const double2 *>(x) + p + u * stride);
+              pv[u] = __ldcg(reinterpret_cast<const double2 *>(pdir) + p + u * stride);
+            }
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u)
+            if (u < n)
+              reinterpret_cast<double2 *>(x)[p + u * stride] =
+                  make_double2(add(xv[u].x, mul(alpha, pv[u].x)), add(xv[u].y, mul(alpha, pv[u].y)));
+        });
+      }
       if (!converged) status = MQ_NOT_CONVERGED;
     }
   }
@@ -612,7 +677,7 @@ __device__ __forceinline__ void push_planes_group(const SlabRank &me, const doub
 
 __global__ void __launch_bounds__(kBlock, 2) pcg_tma_slab_kernel(const __grid_constant__ TmaSlabArgs S) {
   extern __shared__ __align__(128) unsigned char dsm[];
-  __shared__ __align__(8) uint64_t bars[NST];
+  __shared__ __align__(8) uint64_t bars[NR];
   __shared__ double red[3 * kWarps];
   __shared__ double tot[4];
   const int Gr = gridDim.x / S.ngroups;
@@ -629,11 +694,12 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_slab_kernel(const __grid_co
   const double *b = a.b;
   const int x0_mode = a.x0_mode;
   MarchCtx mc;
-  mc.st = reinterpret_cast<Stage *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sr = reinterpret_cast<Box3 *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sp = mc.sr + NR;
   mc.bars = bars;
   mc.ph = 0u;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NR; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -659,7 +725,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_slab_kernel(const __grid_co
     for (int bi = lb; bi < g.nbricks; bi += Gr) {
       int i0, i1, j0, k0;
       brick_of(g, bi, i0, i1, j0, k0);
-      march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, nullptr, i0, i1, j0, k0,
+      march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
                        [&](int c, int64_t e, auto V) {
                          const double bv = __ldcg(b + e);
                          const double rv = sub(bv, stencil3(c, dg, of, V));
@@ -717,7 +783,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_slab_kernel(const __grid_co
       for (int bi = lb; bi < g.nbricks; bi += Gr) {
         int i0, i1, j0, k0;
         brick_of(g, bi, i0, i1, j0, k0);
-        march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, pnew, i0, i1, j0, k0,
+        march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, 1, 0.0, pnew, i0, i1, j0, k0,
                        [&](int c, int64_t e, auto V) {
                          const double av = stencil3(c, dg, of, V);
                          ap[e] = av;
@@ -809,20 +875,21 @@ done:
 __global__ void __launch_bounds__(kBlock, 2) kn_apply_tma_kernel(const __grid_constant__ TmaPcgArgs A,
                                                                  double *__restrict__ y) {
   extern __shared__ __align__(128) unsigned char dsm[];
-  __shared__ __align__(8) uint64_t bars[NST];
+  __shared__ __align__(8) uint64_t bars[NR];
   MarchCtx mc;
-  mc.st = reinterpret_cast<Stage *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sr = reinterpret_cast<Box3 *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sp = mc.sr + NR;
   mc.bars = bars;
   mc.ph = 0u;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NR; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   for (int bi = blockIdx.x; bi < A.g.nbricks; bi += gridDim.x) {
     int i0, i1, j0, k0;
     brick_of(A.g, bi, i0, i1, j0, k0);
-    march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, nullptr, i0, i1, j0, k0,
+    march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
                      [&](int c, int64_t e, auto V) { y[e] = stencil3(c, A.a.dg, A.a.of, V); });
   }
 }
