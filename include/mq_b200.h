@@ -319,6 +319,45 @@ int mq_slab_ipc_import(mq_ctx *ctx, int32_t rank, int32_t nranks, const void *al
 int mq_slab_fused_solve_peer(mq_ctx *ctx, const double *b_dev, int32_t x0_given, double rel_tol,
                              double abs_tol, int32_t max_iter, int32_t use_jacobi, mq_solve_report *report);
 
+/* ---- sharded explicit step over i-slabs (BASELINE configs[4]) -----------
+ * The SchurOperator step (schur.py:379-419) with the K_n-sized vectors of a
+ * slab context (mq_ctx_create_slab) and the CSPE / previous / zero start
+ * vectors (startvec.py:158-225, 345-431).  Every reduction leaves this rank's
+ * partial sums (MQ_SS_NPART doubles) in `part`; the host sums them over the
+ * ranks in rank order and hands the totals back as `tot`, so every rank takes
+ * the same decisions on the same scalars.  The conducting state a_c (full
+ * grid, compact order) is replicated on every rank; each rank integrates the
+ * conducting edges whose node plane it owns (mq_ss_owned).  The host drives
+ * the sequence (paper_1611_06721_b200/slabstep.py), the halo exchanges and
+ * the PCG (mq_slab_fused_solve_local / _peer). */
+#define MQ_SS_NPART 34
+/* pattern_local: the source pattern on the slab's own dofs (slab compact order) */
+int mq_ss_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern_local);
+/* {n_c of the grid, owned conducting edges, conductor cells, K_cn^T rows of the slab} */
+int mq_ss_info(mq_ctx *ctx, int64_t *out4);
+int mq_ss_owned(mq_ctx *ctx, int64_t *idx);
+/* 0 rhs_src, 1 rhs_cpl, 2 y_src, 3 y_cpl, 4 y_cur, 5 w2 (CGS vector), 6 y_cpl - y_src */
+int mq_ss_vec(mq_ctx *ctx, int32_t which, double **out);
+int mq_ss_state_set(mq_ctx *ctx, const double *a_c);
+int mq_ss_state_get(mq_ctx *ctx, double *a_c);
+/* which 0: rhs_src = pattern * wave (schur.py:81-82); 1: rhs_cpl = K_cn^T a_c (schur.py:394) */
+int mq_ss_rhs(mq_ctx *ctx, int32_t which, double wave);
+/* SubspaceCache.project (startvec.py:207-225) in two halves around the all-reduce */
+int mq_ss_project(mq_ctx *ctx, int32_t family, int32_t rhs_which, double *part);
+int mq_ss_start(mq_ctx *ctx, int32_t family, const double *tot, double *x_dev);
+/* solution x (slab vector) -> the family's solution vector; rep counted in diagnostics */
+int mq_ss_store(mq_ctx *ctx, int32_t family, const double *x_dev, const mq_solve_report *rep);
+/* SubspaceCache.insert (startvec.py:158-199), phases 0..5 (solver_slab.cuh) */
+int mq_ss_observe(mq_ctx *ctx, int32_t family, int32_t phase, const double *tot, double *part, int32_t *flag);
+/* Euler update (schur.py:392-404): prep forms y_cpl - y_src (halo next), then
+ * the owned conducting edges' new values (owned order); MQ_NONFINITE on a
+ * non-finite state */
+int mq_ss_euler_prep(mq_ctx *ctx);
+int mq_ss_euler(mq_ctx *ctx, double dt, double *owned_out);
+/* a_n = y_src - y_cur of the last recovery on the slab's dofs (schur.py:408-419) */
+int mq_ss_an(mq_ctx *ctx, double *a_n_local);
+int mq_ss_diag(mq_ctx *ctx, mq_diag *out);
+
 /* ---- timing (CUDA events on the context stream) ------------------------- */
 /* Sum of the device times of the PCG launches of the last step (when PCG
  * timing is enabled with mq_pcg_stats(..., 1)). */

@@ -157,6 +157,21 @@ SIGNATURES = {
     "mq_slab_ipc_export": (I32, [VP, VP, VP]),
     "mq_slab_ipc_import": (I32, [VP, I32, I32, VP, c_int32_p, VP]),
     "mq_slab_fused_solve_peer": (I32, [VP, VP, I32, D, D, I32, I32, ctypes.POINTER(SolveReportC)]),
+    "mq_ss_init": (I32, [VP, ctypes.POINTER(SolverCfg), c_double_p]),
+    "mq_ss_info": (I32, [VP, c_int64_p]),
+    "mq_ss_owned": (I32, [VP, c_int64_p]),
+    "mq_ss_vec": (I32, [VP, I32, ctypes.POINTER(VP)]),
+    "mq_ss_state_set": (I32, [VP, c_double_p]),
+    "mq_ss_state_get": (I32, [VP, c_double_p]),
+    "mq_ss_rhs": (I32, [VP, I32, D]),
+    "mq_ss_project": (I32, [VP, I32, I32, c_double_p]),
+    "mq_ss_start": (I32, [VP, I32, c_double_p, VP]),
+    "mq_ss_store": (I32, [VP, I32, VP, ctypes.POINTER(SolveReportC)]),
+    "mq_ss_observe": (I32, [VP, I32, I32, c_double_p, c_double_p, c_int32_p]),
+    "mq_ss_euler_prep": (I32, [VP]),
+    "mq_ss_euler": (I32, [VP, D, c_double_p]),
+    "mq_ss_an": (I32, [VP, c_double_p]),
+    "mq_ss_diag": (I32, [VP, ctypes.POINTER(Diag)]),
     "mq_slab_fused_solve_local": (I32, [ctypes.POINTER(VP), I32, ctypes.POINTER(VP), ctypes.POINTER(VP), I32, D, D, I32, I32,
                                         ctypes.POINTER(SolveReportC)]),
     "mq_timer_start": (I32, [VP]),

@@ -232,6 +232,7 @@ void mq_ctx_destroy(mq_ctx *ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   solver_free(ctx);
+  slab_step_free(ctx);
   slab_peer_free(ctx);
   for (void *p : ctx->allocs) cudaFree(p);
   for (double *p : ctx->vecs) cudaFree(p);

@@ -58,6 +58,7 @@ struct RunDev {
 
 struct SolverHost;
 struct SlabPeer;
+struct SlabStepHost;
 
 }  // namespace mq
 
@@ -114,6 +115,8 @@ struct mq_ctx {
   // solver
   mq::SolverHost *solver = nullptr;
   mq::SlabPeer *peer = nullptr;  // fused slab PCG across processes (IPC-mapped neighbours)
+  mq::SlabStepHost *sstep = nullptr;  // sharded explicit step on a slab context (solver_slab.cuh)
+  int slab_lo = 0, slab_hi = 0;       // node planes [lo, hi) of a slab context (0, 0: whole grid)
   // bookkeeping
   std::vector<void *> allocs;
   std::set<double *> vecs;
@@ -140,6 +143,7 @@ int ctx_pcg(mq_ctx *ctx, const double *b, double *x, int x0_mode, double rel_tol
 int conducting_init(mq_ctx *ctx);
 void solver_free(mq_ctx *ctx);
 void slab_peer_free(mq_ctx *ctx);
+void slab_step_free(mq_ctx *ctx);
 void solver_graph_reset(mq_ctx *ctx);
 
 int coop_grid(const void *kernel, int want_blocks, int *out);

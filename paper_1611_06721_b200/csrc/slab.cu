@@ -162,6 +162,8 @@ int mq_ctx_create_slab(const mq_grid_desc *desc, int32_t i_lo, int32_t i_hi, int
   int rc = build_slab_topology(ctx->desc, i_lo, i_hi, ctx->topo, err);
   if (rc) { set_error(err); delete ctx; return rc; }
   ctx->device = device;
+  ctx->slab_lo = i_lo;
+  ctx->slab_hi = i_hi;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "cudaSetDevice"); }
   e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);

@@ -2558,3 +2558,5 @@ int mq_pcg_collect(mq_ctx *ctx, double *ms, int32_t *n_events) {
 }
 
 }  // extern "C"
+
+#include "solver_slab.cuh"

@@ -8,6 +8,16 @@ families, their start-vector histories and every PCG solve stay on the GPU.
 ``run_explicit`` runs the whole time loop on the device (one CUDA graph per
 step, replayed) and synchronises with the host only at output rows that need
 host data, or once at the end.
+
+The reference's other ``SchurOperator`` options are honoured as it defines
+them: ``strategy=<StartVectorStrategy object>`` (any object with the
+protocol of startvec.py:315-342, e.g. the reference's own ``CspeStrategy``;
+schur.py:198-199), ``cache_source_solve`` (one pattern solve rescaled per
+call, schur.py:266-278) and ``projection_target`` (schur.py:244-250).  With
+a host-side strategy object or a cached source solve the step is composed on
+the host from device operations (PCG, K_cn, K_cn^T, K_c products), exactly
+the reference's sequence (schur.py:379-419, 474-607); otherwise the whole
+step runs on the device.
 """
 
 from __future__ import annotations
@@ -21,8 +31,8 @@ import numpy as np
 from . import _lib
 from ._lib import check, dptr, f64, i64ptr
 from .device import DeviceGrid, Problem, default_probe_cells
-from .krylov import PcgConfig, Preconditioner, SolveReport
-from .startvec import RhsFamily, family_index, solver_cfg
+from .krylov import JacobiPreconditioner, PcgConfig, Preconditioner, SolveReport, pcg_solve
+from .startvec import DeviceStrategy, RhsFamily, family_index, solver_cfg
 
 __all__ = ["StepFailureError", "SchurOperator", "explicit_euler_step", "recover_an",
            "run_explicit", "TransientResult", "FAMILIES", "step_times", "CflEstimate", "trace_bytes",
@@ -41,37 +51,89 @@ def _report(r: _lib.SolveReportC) -> SolveReport:
                        int(r.applies))
 
 
+class _DeviceStrategyView:
+    """``op.strategy`` of an operator whose strategy runs on the device:
+    the reference's strategy queries (startvec.py:315-342) answered from the
+    device diagnostics."""
+
+    def __init__(self, op):
+        self._op = op
+        self.kind = op.strategy_kind
+
+    def basis_size(self, family=None) -> int:
+        if family is not None and self.kind == "cspe":
+            return int(self._op.diagnostics().basis_cols[family_index(family)])
+        return self._op.basis_size()
+
+    @property
+    def maintenance_applies(self) -> int:
+        return self._op.maintenance_applies
+
+    def diagnostics(self) -> dict:
+        return self._op.strategy_diagnostics()
+
+
 class SchurOperator:
     """Device-resident eliminated-block operator (schur.py:168-313)."""
 
     def __init__(self, problem, pcg: PcgConfig | None = None, strategy="previous", *,
-                 preconditioner=Preconditioner.JACOBI, max_cols: int = 20,
+                 preconditioner=Preconditioner.JACOBI, cache_source_solve: bool = False,
+                 projection_target: str = "assembled-rhs", max_cols: int = 20,
                  n_pod: int = 10, eps_pod: float = 1e-4, device: int = 0):
+        if projection_target not in ("assembled-rhs", "composed-coupling"):
+            raise ValueError(f"unknown projection target {projection_target!r}")
         if Preconditioner(preconditioner) is not Preconditioner.JACOBI:
             raise NotImplementedError("the device K_n path uses the reference's Jacobi preconditioner")
         self.grid = problem if isinstance(problem, DeviceGrid) else DeviceGrid(problem, device)
         self.problem = self.grid.problem
         self.pcg = pcg or PcgConfig()
-        self.strategy_kind = str(strategy).lower()
+        self.projection_target = projection_target
+        self.cache_source_solve = bool(cache_source_solve)
+        self._cached_pattern_solution = None
+        # strategy: a name (device solver), a DeviceStrategy on this grid (its
+        # device solver and parameters), or any StartVectorStrategy-protocol
+        # object, which stays on the host (schur.py:198-199)
+        self.host_strategy = None
+        if isinstance(strategy, DeviceStrategy) and strategy.grid is self.grid:
+            max_cols, n_pod, eps_pod = strategy.max_cols, strategy.n_pod, strategy.eps_pod
+            self.strategy_kind = strategy.kind
+        elif isinstance(strategy, str):
+            self.strategy_kind = strategy.lower()
+        else:
+            if not (hasattr(strategy, "start_vector") and hasattr(strategy, "observe")):
+                raise ValueError(f"strategy must be a name or a StartVectorStrategy, got {strategy!r}")
+            self.host_strategy = strategy
+            self.strategy_kind = str(getattr(strategy, "kind", "custom"))
+        # composed: the step is built on the host from device operations
+        self.composed = self.host_strategy is not None or self.cache_source_solve
         if self.problem.pattern is None:
             raise ValueError("problem has no source pattern")
         pat = f64(self.problem.pattern, self.grid.n_n, "source pattern")
-        cfg = solver_cfg(self.strategy_kind, max_cols=max_cols, n_pod=n_pod, eps_pod=eps_pod,
-                         rel_tol=self.pcg.rel_tol, abs_tol=self.pcg.abs_tol,
+        cfg = solver_cfg("zero" if self.host_strategy is not None else self.strategy_kind, max_cols=max_cols,
+                         n_pod=n_pod, eps_pod=eps_pod, rel_tol=self.pcg.rel_tol, abs_tol=self.pcg.abs_tol,
                          max_iter=self.pcg.max_iter, drop_tol=self.pcg.rel_tol)
         self.cfg = cfg
         self.lib = self.grid.lib
         check(self.lib.mq_solver_init(self.grid.ctx, ctypes.byref(cfg), dptr(pat)))
         self.solve_iterations = {f: [] for f in FAMILIES}
         self.solver_seconds = 0.0
+        self._host_applies = 0
         self._rhs = self.grid.alloc()
         self._y = self.grid.alloc()
+        self._kn = self.grid.kn_operator()
+        self._jac = JacobiPreconditioner(self._kn.diagonal())   # schur.py:193-197
         self._minv_diag = 1.0 / self.grid.mc_diag()
         self.t = 0.0
         # page-locked result arrays of the host-facing step / recovery calls,
         # allocated now rather than inside the first steps
         _lib.pinned_reserve(self.grid.n_c, 4)
         _lib.pinned_reserve(self.grid.n_n, 4)
+
+    @property
+    def strategy(self):
+        """The host strategy object, or a DeviceStrategy-like view of the
+        device solver (basis_size / diagnostics)."""
+        return self.host_strategy if self.host_strategy is not None else _DeviceStrategyView(self)
 
     @property
     def system_n_c(self):
@@ -84,10 +146,12 @@ class SchurOperator:
 
     @property
     def pcg_applies(self) -> int:
-        return int(self.diagnostics().pcg_applies)
+        return int(self.diagnostics().pcg_applies) + self._host_applies
 
     @property
     def maintenance_applies(self) -> int:
+        if self.host_strategy is not None:
+            return int(getattr(self.host_strategy, "maintenance_applies", 0))
         return int(self.diagnostics().maintenance_applies)
 
     def solve_count(self, family) -> int:
@@ -100,6 +164,8 @@ class SchurOperator:
         return sum(sum(v) for v in self.solve_iterations.values())
 
     def basis_size(self) -> int:
+        if self.host_strategy is not None:
+            return int(self.host_strategy.basis_size())
         d = self.diagnostics()
         if self.strategy_kind == "cspe":
             return int(max(d.basis_cols))
@@ -108,6 +174,9 @@ class SchurOperator:
         return 0
 
     def strategy_diagnostics(self) -> dict:
+        if self.host_strategy is not None:
+            diag = getattr(self.host_strategy, "diagnostics", None)
+            return dict(diag()) if diag else {}
         d = self.diagnostics()
         if self.strategy_kind == "cspe":
             return {"basis_cols": int(max(d.basis_cols)),
@@ -118,24 +187,67 @@ class SchurOperator:
                     "maintenance_applies": int(d.maintenance_applies)}
         return {}
 
-    def solve_kn(self, rhs, family) -> tuple[np.ndarray, SolveReport]:
+    def solve_kn(self, rhs, family, raw_state=None) -> tuple[np.ndarray, SolveReport]:
         """One pseudo-inverse action K_n^+ rhs for the family (schur.py:239-264)."""
         started = time.perf_counter()
-        self.grid.upload(f64(rhs, self.grid.n_n, "rhs"), self._rhs)
-        rep = _lib.SolveReportC()
-        rc = self.lib.mq_solve_kn(self.grid.ctx, family_index(family), ctypes.c_void_p(self._rhs),
-                                  ctypes.c_void_p(self._y), ctypes.byref(rep))
-        check(rc)
-        y = self.grid.download(self._y)
         fam = family if isinstance(family, RhsFamily) else RhsFamily(getattr(family, "value", family))
+        if self.host_strategy is not None:
+            target = rhs
+            if (self.projection_target == "composed-coupling" and raw_state is not None
+                    and fam is not RhsFamily.SOURCE_CURRENT):
+                # schur.py:244-250: the target recomposed from the coupling operator
+                target = self.grid.kcn_t_apply(raw_state)
+            x0 = self.host_strategy.start_vector(family, target)
+            y, rep = pcg_solve(self._kn, rhs, x0=x0, config=self.pcg, preconditioner=self._jac)
+            if not rep.converged:
+                raise StepFailureError(f"inner solve ({fam.value}) stalled at relative residual "
+                                       f"{rep.final_rel_residual:.3e} after {rep.iterations} iterations")
+            self._host_applies += rep.applications
+            self.host_strategy.observe(family, y)
+        else:
+            # the device solver projects onto the assembled rhs; the composed
+            # coupling target is the same vector (K_cn^T a_c, schur.py:246-249)
+            self.grid.upload(f64(rhs, self.grid.n_n, "rhs"), self._rhs)
+            r = _lib.SolveReportC()
+            rc = self.lib.mq_solve_kn(self.grid.ctx, family_index(family), ctypes.c_void_p(self._rhs),
+                                      ctypes.c_void_p(self._y), ctypes.byref(r))
+            check(rc)
+            y = self.grid.download(self._y)
+            rep = _report(r)
         self.solve_iterations[fam].append(int(rep.iterations))
         self.solver_seconds += time.perf_counter() - started
-        return y, _report(rep)
+        return y, rep
 
     def source_solution(self, t: float):
-        """K_n^+ j_n(t) (schur.py:266-278, cache_source_solve=False)."""
+        """K_n^+ j_n(t); with cache_source_solve one pattern solve, rescaled
+        per call (schur.py:266-278)."""
         scale = float(self.problem.waveform(t))
+        if self.cache_source_solve:
+            if self._cached_pattern_solution is None:
+                y, rep = self.solve_kn(self.problem.pattern, RhsFamily.SOURCE_CURRENT)
+                self._cached_pattern_solution = y
+            else:
+                rep = SolveReport(0, 0.0, True)
+            return self._cached_pattern_solution * scale, rep
         return self.solve_kn(self.problem.pattern * scale, RhsFamily.SOURCE_CURRENT)
+
+    def apply(self, x, lin_state, family=RhsFamily.COUPLING_FROM_PREVIOUS_STATE) -> np.ndarray:
+        """K_S(lin_state) x, charging the inner solve to ``family`` (schur.py:289-296)."""
+        w = self.grid.kcn_t_apply(x)
+        y, _ = self.solve_kn(w, family, raw_state=x)
+        return self.grid.kc_apply(lin_state, x) - self.grid.kcn_apply(y)
+
+    def apply_detached(self, x, lin_state, inner_start=None):
+        """K_S x with an explicit inner start vector and no family history
+        (schur.py:298-313); returns (K_S x, inner solution)."""
+        started = time.perf_counter()
+        w = self.grid.kcn_t_apply(x)
+        y, rep = pcg_solve(self._kn, w, x0=inner_start, config=self.pcg, preconditioner=self._jac)
+        if not rep.converged:
+            raise StepFailureError("spectral probe solve stalled")
+        self._host_applies += rep.applications
+        self.solver_seconds += time.perf_counter() - started
+        return self.grid.kc_apply(lin_state, x) - self.grid.kcn_apply(y), y
 
     def minv(self, x):
         return self._minv_diag * x
@@ -218,11 +330,42 @@ def estimate_cfl(op: SchurOperator, a_c_ref=None, *, power_iters: int = 200,
     return CflEstimate(lam.value, dt.value, safety, int(used.value), power_tol, int(applies.value))
 
 
+def _composed_euler_step(state, dt, op, step_index):
+    """schur.py:379-405 composed on the host from device operations (a host
+    strategy object or a cached source solve)."""
+    a_c, t = state
+    a_c = f64(a_c, op.grid.n_c, "state")
+    t_new = t + dt
+    y_src, rep_src = op.source_solution(t_new)
+    w = op.grid.kcn_t_apply(a_c)
+    y_cpl, rep_cpl = op.solve_kn(w, RhsFamily.COUPLING_FROM_PREVIOUS_STATE, raw_state=a_c)
+    rate = op.grid.kcn_apply(y_cpl - y_src) - op.grid.kc_apply(a_c, a_c)
+    a_next = a_c + dt * op.minv(rate)
+    if not np.isfinite(a_next).all():
+        where = f" at step {step_index}" if step_index is not None else ""
+        raise StepFailureError(f"non-finite conducting state{where} (t = {t_new:.6e})")
+    op.t = float(t_new)
+    return a_next, (rep_src, rep_cpl)
+
+
+def _composed_recover_an(op, a_c, t):
+    """schur.py:408-419 composed on the host from device operations."""
+    a_c = f64(a_c, op.grid.n_c, "state")
+    y_src, rep_src = op.source_solution(t)
+    w = op.grid.kcn_t_apply(a_c)
+    y_cpl, rep_cpl = op.solve_kn(w, RhsFamily.COUPLING_FROM_CURRENT_STATE, raw_state=a_c)
+    op.t = float(t)
+    return y_src - y_cpl, (rep_src, rep_cpl)
+
+
 def explicit_euler_step(state, dt: float, op: SchurOperator, step_index: int | None = None):
     """One explicit Euler step on the device (schur.py:379-405)."""
     a_c, t = state
     if dt < 0:
         raise ValueError("dt must be nonnegative")
+    if op.composed:
+        return _composed_euler_step(state, dt, op, step_index)
+    started = time.perf_counter()
     v = f64(a_c, op.grid.n_c, "state")
     t_new = t + dt
     a_next = _lib.pinned_empty(op.grid.n_c)
@@ -238,11 +381,15 @@ def explicit_euler_step(state, dt: float, op: SchurOperator, step_index: int | N
     op.solve_iterations[RhsFamily.SOURCE_CURRENT].append(int(r1.iterations))
     op.solve_iterations[RhsFamily.COUPLING_FROM_PREVIOUS_STATE].append(int(r2.iterations))
     op.t = float(t_new)
+    op.solver_seconds += time.perf_counter() - started
     return a_next, (_report(r1), _report(r2))
 
 
 def recover_an(op: SchurOperator, a_c, t: float):
     """a_n = K_n^+ j_n(t) - K_n^+ K_cn^T a_c (schur.py:408-419)."""
+    if op.composed:
+        return _composed_recover_an(op, a_c, t)
+    started = time.perf_counter()
     v = f64(a_c, op.grid.n_c, "state")
     a_n = _lib.pinned_empty(op.grid.n_n)
     r1, r2 = _lib.SolveReportC(), _lib.SolveReportC()
@@ -252,6 +399,7 @@ def recover_an(op: SchurOperator, a_c, t: float):
     check(rc)
     op.solve_iterations[RhsFamily.SOURCE_CURRENT].append(int(r1.iterations))
     op.solve_iterations[RhsFamily.COUPLING_FROM_CURRENT_STATE].append(int(r2.iterations))
+    op.solver_seconds += time.perf_counter() - started
     return a_n, (_report(r1), _report(r2))
 
 
@@ -329,7 +477,8 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
                  use_graph: bool = True, record_states: bool = False,
                  op: SchurOperator | None = None, reestimate_every: int = 500, safety: float = 0.9,
                  power_iters: int = 200, power_tol: float = 1e-4,
-                 seed: int = 42) -> TransientResult:
+                 seed: int = 42, cache_source_solve: bool = False,
+                 projection_target: str = "assembled-rhs") -> TransientResult:
     """Integrate with explicit Euler on the device (schur.py:474-607).
 
     ``dt="auto"`` runs the device spectral estimate before the loop and again
@@ -345,7 +494,12 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
     wall_start = time.perf_counter()
     if op is None:
         op = SchurOperator(problem, pcg=pcg, strategy=strategy, preconditioner=preconditioner,
+                           cache_source_solve=cache_source_solve, projection_target=projection_target,
                            max_cols=max_cols, n_pod=n_pod, eps_pod=eps_pod, device=device)
+    if op.composed:
+        return _run_composed(op, t_end, dt, output_period=output_period, probe=probe, a0=a0,
+                             max_steps=max_steps, reestimate_every=reestimate_every, safety=safety,
+                             power_iters=power_iters, power_tol=power_tol, seed=seed, wall_start=wall_start)
     lambda_max = None
     auto = isinstance(dt, str)
     if auto:
@@ -414,8 +568,12 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
             op._set_state(a_c, sched.t)
         base = sched.count
         dts, outs, tt = sched.take(dt, phase_len)
+        ph0 = time.perf_counter()
         a_c, a_n_ph, step_iters, hist, all_out = _run_phase(
             op, dts, outs, tt, wave, emit, rows, base, host_probe, device_probe, use_graph, record_states)
+        # the device phases are solver work (every step is its inner solves
+        # plus the n_c-sized Euler update)
+        op.solver_seconds += time.perf_counter() - ph0
         if a_n_ph is not None:
             a_n = a_n_ph
         all_out_all = all_out_all and all_out
@@ -441,6 +599,7 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
         "maintenance_applies": int(d.maintenance_applies),
         "operator_applies": int(d.pcg_applies + d.maintenance_applies),
         "wall_seconds": wall,
+        "solver_seconds": op.solver_seconds,
         "min_pod_info": float(d.min_pod_info),
         "max_basis_cols": int(max(d.basis_cols)),
         "aborted": False,
@@ -458,6 +617,110 @@ def run_explicit(problem, t_end: float, dt, *, strategy="cspe", pcg: PcgConfig |
                            (np.empty((0, n_c)) if record_states else None),
                            a_n_history=np.concatenate(hist_n_parts) if record_states and hist_n_parts else
                            (np.empty((0, op.grid.n_n)) if record_states else None))
+
+
+def _run_composed(op, t_end, dt, *, output_period, probe, a0, max_steps, reestimate_every, safety,
+                  power_iters, power_tol, seed, wall_start):
+    """The reference's loop (schur.py:474-607, _WindowStats 448-467) over the
+    composed step, for operators with a host strategy object or a cached
+    source solve."""
+    auto = isinstance(dt, str)
+    lambda_max = None
+    if auto:
+        if dt != "auto":
+            raise ValueError(f"dt must be a number or 'auto', got {dt!r}")
+        est = estimate_cfl(op, power_iters=power_iters, power_tol=power_tol, safety=safety, seed=seed)
+        dt_val, lambda_max = est.dt_max, est.lambda_max
+    else:
+        dt_val = float(dt)
+        if dt_val <= 0:
+            raise ValueError("dt must be positive")
+    n_c = op.grid.n_c
+    a_c = np.zeros(n_c) if a0 is None else f64(a0, n_c, "initial state").copy()
+    t = 0.0
+    rows = {k: [] for k in ("t", "b", "src", "prev", "cur", "basis", "k", "info")}
+    win = {f: [] for f in FAMILIES}
+    pod = {"k": 0, "info": 1.0}
+
+    def note_pod():
+        diag = op.strategy_diagnostics()
+        if "pod_k" in diag:
+            pod["k"] = max(pod["k"], diag["pod_k"])
+            pod["info"] = min(pod["info"], diag.get("pod_info", 1.0))
+
+    def mean(f):
+        return float(np.mean(win[f])) if win[f] else 0.0
+
+    def emit_row(t_row, a_n, reps):
+        if reps is not None:
+            win[RhsFamily.SOURCE_CURRENT].append(reps[0].iterations)
+            win[RhsFamily.COUPLING_FROM_CURRENT_STATE].append(reps[1].iterations)
+        note_pod()
+        rows["t"].append(t_row)
+        rows["b"].append(float(probe(a_c, a_n, t_row)) if probe else 0.0)
+        rows["src"].append(mean(RhsFamily.SOURCE_CURRENT))
+        rows["prev"].append(mean(RhsFamily.COUPLING_FROM_PREVIOUS_STATE))
+        rows["cur"].append(mean(RhsFamily.COUPLING_FROM_CURRENT_STATE))
+        rows["basis"].append(op.basis_size())
+        rows["k"].append(max(pod["k"], op.strategy_diagnostics().get("pod_k", 0)))
+        rows["info"].append(pod["info"])
+        for f in FAMILIES:
+            win[f] = []
+        pod["k"], pod["info"] = 0, 1.0
+
+    a_n, reps = recover_an(op, a_c, t)
+    emit_row(t, a_n, reps)
+    next_output = output_period
+    steps = refreshes = 0
+    eps = 1e-12 * t_end
+    while t < t_end - eps:
+        if auto and reestimate_every > 0 and steps > 0 and steps % reestimate_every == 0:
+            est = estimate_cfl(op, a_c_ref=a_c, power_iters=power_iters, power_tol=power_tol,
+                               safety=safety, seed=seed)
+            refreshes += 1
+            lambda_max = est.lambda_max
+            dt_val = min(dt_val, est.dt_max)
+        step_dt = min(dt_val, t_end - t)
+        a_c, sreps = explicit_euler_step((a_c, t), step_dt, op, step_index=steps + 1)
+        win[RhsFamily.SOURCE_CURRENT].append(sreps[0].iterations)
+        win[RhsFamily.COUPLING_FROM_PREVIOUS_STATE].append(sreps[1].iterations)
+        note_pod()
+        t += step_dt
+        steps += 1
+        if steps > max_steps:
+            raise StepFailureError(f"step budget exceeded ({max_steps})")
+        if t >= next_output - eps or t >= t_end - eps:
+            a_n, reps = recover_an(op, a_c, t)
+            emit_row(t, a_n, reps)
+            while next_output <= t + eps:
+                next_output += output_period
+    diag = op.strategy_diagnostics()
+    aggregates = {
+        "integrator": "explicit",
+        "strategy": op.strategy_kind,
+        "steps": steps,
+        "dt": dt_val,
+        "lambda_max": lambda_max,
+        "cfl_refreshes": refreshes,
+        "solves": {f.value: op.solve_count(f) for f in FAMILIES},
+        "iterations": {f.value: int(sum(op.solve_iterations[f])) for f in FAMILIES},
+        "mean_iterations": {f.value: (float(np.mean(op.solve_iterations[f]))
+                                      if op.solve_iterations[f] else 0.0) for f in FAMILIES},
+        "pcg_applies": op.pcg_applies,
+        "maintenance_applies": op.maintenance_applies,
+        "operator_applies": op.pcg_applies + op.maintenance_applies,
+        "wall_seconds": time.perf_counter() - wall_start,
+        "solver_seconds": op.solver_seconds,
+        "min_pod_info": diag.get("min_pod_info", 1.0),
+        "max_basis_cols": diag.get("basis_cols", 0),
+        "aborted": False,
+    }
+    return TransientResult(times=np.asarray(rows["t"]), probe_b=np.asarray(rows["b"]),
+                           iters_src=np.asarray(rows["src"]), iters_cpl_prev=np.asarray(rows["prev"]),
+                           iters_cpl_cur=np.asarray(rows["cur"]),
+                           basis_cols=np.asarray(rows["basis"], dtype=np.int64),
+                           pod_k=np.asarray(rows["k"], dtype=np.int64), pod_info=np.asarray(rows["info"]),
+                           final_a_c=a_c, final_a_n=a_n, aggregates=aggregates)
 
 
 def _run_phase(op, dts, outs, tt, wave, emit, rows, base, host_probe, device_probe, use_graph,
