@@ -539,6 +539,59 @@ def cfg_pcg_roofline(index, hbm_peak, reps=2):
             "bytes_per_launch": byts, "bytes_per_iteration": 72.0 * n_n}
 
 
+def cfg4_sharded(dist, world, local, hbm_peak, warmup=1, steps=2):
+    """configs[4] (256^3, Brauer, CSPE k = 5) with the sharded step over the
+    ranks of this job (slabstep.py: one i-slab per rank and GPU, fused slab
+    PCG over CUDA-IPC-mapped neighbour buffers, NCCL all-gathers of the rank
+    partials and the owned conducting values).  Strong scaling: the same grid
+    at every N.  Every call of a step synchronises the host (reductions), so
+    steps are timed by the host clock after a device synchronisation, max
+    over ranks."""
+    import torch
+
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200.slabstep import SlabStepper
+    spec = C.config_spec(4)
+    prob = C.make_problem(4)
+    t0 = time.perf_counter()
+    st = SlabStepper(prob, world, dist=dist, device=local, strategy="cspe", max_cols=spec.max_cols,
+                     rel_tol=spec.rel_tol, max_iter=spec.max_iter)
+    setup = time.perf_counter() - t0
+    try:
+        st.recover(gather=False)
+        for _ in range(warmup):
+            st.step(spec.dt)
+            st.recover(gather=False)
+        torch.cuda.synchronize(local)
+        barrier(dist)
+        its, secs = [], []
+        pcg0 = st.pcg_seconds
+        for _ in range(steps):
+            ts = time.perf_counter()
+            r1, r2 = st.step(spec.dt)
+            _, (r3, r4) = st.recover(gather=False)
+            torch.cuda.synchronize(local)
+            secs.append(time.perf_counter() - ts)
+            its.append([r1.iterations, r2.iterations, r3.iterations, r4.iterations])
+        pcg_s = st.pcg_seconds - pcg0
+        n_n = st.n_n
+    finally:
+        st.close()
+    total = max_over_ranks(float(sum(secs)), dist, local)
+    pcg_max = max_over_ranks(pcg_s, dist, local)
+    byts = float(pcg_launch_bytes(n_n, np.asarray(its).reshape(-1)).sum())
+    agg = byts / pcg_max / 1e9
+    return {"workload": "cfg4_256cube_two_blocks_cspe5_sharded", "grid": [256, 256, 256], "n_n": n_n,
+            "ranks": world, "scaling": "strong", "decomposition": "i-slabs, one per rank/GPU",
+            "dt": spec.dt, "steps_after_warmup": [warmup + 1, warmup + steps],
+            "value": steps / total, "unit": UNIT, "ms_per_step": 1e3 * total / steps,
+            "pcg_share_of_step": pcg_max / total, "timed_step_iterations": its,
+            "pcg_GBps_aggregate": agg, "pcg_GBps_per_gpu": agg / world,
+            "frac_of_N_hbm": agg / (hbm_peak * world), "setup_s": setup,
+            "timing": "host clock around each step after cuda synchronize (the step synchronises at every "
+                      "reduction), max over ranks"}
+
+
 def run_device_arm(args):
     world, rank, local, dist = dist_init()
     from paper_1611_06721_b200 import PcgConfig, SchurOperator, _lib
@@ -578,6 +631,13 @@ def run_device_arm(args):
                 "algorithmic_bytes": "72 B per dof per iteration (9 fp64 streams) + 32 B/dof initial residual "
                                      "+ 24 B/dof final x update per launch (pcg_launch_bytes)"}
     op.grid.close()
+    sharded = None
+    if not args.skip_cfg4:
+        try:
+            sharded = cfg4_sharded(dist, world, local, hbm_peak)
+        except Exception as exc:  # noqa: BLE001  (reported, never silently dropped)
+            sharded = {"workload": "cfg4_256cube_two_blocks_cspe5_sharded", "ranks": world,
+                       "error": f"{type(exc).__name__}: {exc}"}
     line = None
     if rank == 0:
         # the device leg's steps, host-timed three times from a fresh
@@ -618,6 +678,7 @@ def run_device_arm(args):
             "cfg1_pod_steps": cfg1_pod,
             "roofline_cfg4_1gpu": roof4,
             "cfg4_steps_1gpu": steps4,
+            "cfg4_sharded": sharded,
             "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "explicit_euler_step + recover_an + probe_b (host arrays)",
                     "runs": e2e_vals, "estimator": "median of 3 runs of the timed steps"},

@@ -638,6 +638,10 @@ def _run_composed(op, t_end, dt, *, output_period, probe, a0, max_steps, reestim
     n_c = op.grid.n_c
     a_c = np.zeros(n_c) if a0 is None else f64(a0, n_c, "initial state").copy()
     t = 0.0
+    if probe is not None and not callable(probe):
+        # "device" or conductor-cell ids: the device B probe of each row's state
+        op.set_probe(None if isinstance(probe, str) else probe)
+        probe = (lambda a, _n, _t: op.probe_b(a))
     rows = {k: [] for k in ("t", "b", "src", "prev", "cur", "basis", "k", "info")}
     win = {f: [] for f in FAMILIES}
     pod = {"k": 0, "info": 1.0}

@@ -133,6 +133,16 @@ class SlabStepGrid(SlabGrid):
         check(self.lib.mq_ss_diag(self.ctx, ctypes.byref(d)))
         return d
 
+    def stage_b(self, which: str):
+        """Copy the named rhs into this slab's PCG ``b`` (host-driven PCG)."""
+        import torch
+        n = self.total
+        src = torch.as_tensor(_DevArray(self.vecs[which], n), device=f"cuda:{self.device}")
+        dst = torch.as_tensor(_DevArray(self.b, n), device=f"cuda:{self.device}")
+        self.sync()
+        dst.copy_(src)
+        torch.cuda.synchronize(self.device)
+
 
 def _sum_rank_order(parts):
     tot = np.array(parts[0], dtype=np.float64, copy=True)
@@ -216,32 +226,43 @@ class SlabStepper:
     over IPC-mapped neighbours with ``dist``)."""
 
     def __init__(self, problem, world: int, *, dist=None, device: int = 0, strategy: str = "cspe",
-                 max_cols: int = 5, rel_tol: float = 1e-8, abs_tol: float = 0.0, max_iter: int = 5000):
+                 max_cols: int = 5, rel_tol: float = 1e-8, abs_tol: float = 0.0, max_iter: int = 5000,
+                 pcg: str = "fused", slabs=None, comm=None):
         if strategy not in ("zero", "previous", "cspe"):
             raise ValueError("the sharded step supports the zero / previous / cspe strategies")
+        if pcg not in ("fused", "host"):
+            raise ValueError("pcg must be 'fused' (one persistent kernel per rank) or 'host' (phase loop)")
         self.problem = problem
         self.world = int(world)
         self.strategy = strategy
+        self.pcg_mode = pcg
         self.rel_tol, self.abs_tol, self.max_iter = float(rel_tol), float(abs_tol), int(max_iter)
         cfg = _lib.SolverCfg(_lib.STRAT[strategy], int(max_cols), 1, int(max_iter), 1e-4, float(rel_tol),
                              float(abs_tol), float(rel_tol))
         gidx_all = global_compact_index(problem.material)
         self.n_n = int((gidx_all >= 0).sum())
         self.dist = dist
-        if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
-            if dist.get_world_size() != self.world:
-                raise ValueError("world size disagrees with torch.distributed")
-            ranks = [dist.get_rank()]
+        distributed = dist is not None and dist.is_initialized() and dist.get_world_size() > 1
+        if distributed and dist.get_world_size() != self.world:
+            raise ValueError("world size disagrees with torch.distributed")
+        if comm is not None:
+            self.comm = comm
+        elif distributed:
             import torch
             dev = torch.device("cuda", device) if dist.get_backend() == "nccl" else None
             self.comm = _Torch(dist, dev)
         else:
-            ranks = list(range(self.world))
             self.comm = _Loopback()
-        self.slabs = [SlabStepGrid(problem, r, self.world, device, cfg=cfg, gidx_all=gidx_all) for r in ranks]
-        self.lib = self.slabs[0].lib
+        if slabs is not None:
+            # prebuilt slab objects with the SlabStepGrid phase methods (tests
+            # drive numpy slabs through the same host sequence under gloo)
+            self.slabs = list(slabs)
+        else:
+            ranks = [dist.get_rank()] if distributed else list(range(self.world))
+            self.slabs = [SlabStepGrid(problem, r, self.world, device, cfg=cfg, gidx_all=gidx_all) for r in ranks]
+        self.lib = getattr(self.slabs[0], "lib", None)
         self.n_c = self.slabs[0].n_c
-        self.peer = len(self.slabs) == 1 and self.world > 1
+        self.peer = pcg == "fused" and len(self.slabs) == 1 and self.world > 1
         if self.peer:
             fused_peer_setup(self.slabs[0], dist)
         # owned conducting edges of every rank (rank order), for the all-gather
@@ -278,8 +299,19 @@ class SlabStepper:
         return self.comm.allreduce(parts)
 
     def _pcg(self, which: str) -> _lib.SolveReportC:
+        """krylov.py:174-250 on the slabs: b = the named rhs, x0 and the
+        solution in each slab's x."""
         rep = _lib.SolveReportC()
         t0 = time.perf_counter()
+        if self.pcg_mode == "host":
+            from .slab import slab_pcg_solve
+            for s in self.slabs:
+                s.stage_b(which)
+            it, relres, conv, app = slab_pcg_solve(self.slabs, self.comm.halo, x0_given=True, rel_tol=self.rel_tol,
+                                                   abs_tol=self.abs_tol, max_iter=self.max_iter, jacobi=True)
+            rep.iterations, rep.final_rel_residual, rep.converged, rep.applies = it, relres, int(conv), app
+            self.pcg_seconds += time.perf_counter() - t0
+            return rep
         if self.peer:
             s = self.slabs[0]
             rc = self.lib.mq_slab_fused_solve_peer(s.ctx, ctypes.c_void_p(s.vecs[which]), 1, self.rel_tol,

@@ -157,3 +157,54 @@ def test_sharded_step_128_matches_single_context(gpu_ok):
         e = rel(_field(res.a_c_history[i], res.a_n_history[i]), _field(one.a_c_history[i], one.a_n_history[i]))
         assert e <= REL_FIELD, (i, e)
     assert np.max(np.abs(res.step_iterations - one.step_iterations)) <= 1
+
+
+def _two_gpu_worker(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200.slabstep import run_explicit_sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        spec = C.config_spec(0)
+        res = run_explicit_sharded(C.make_problem(0), 10, spec.dt, world=world, dist=dist, device=rank,
+                                   strategy="cspe", max_cols=5, record_states=True)
+        q.put((rank, res.step_iterations, res.a_c_history, res.a_n_history))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_step_two_processes(gpu_ok, oracle_c0_runs):
+    """One rank per process and GPU (NCCL all-gathers, fused slab PCG over
+    CUDA-IPC-mapped neighbour buffers).  Runs wherever two GPUs exist."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs (one rank per GPU; ranks that wait on one another never share one)")
+    spec, m, runs = oracle_c0_runs
+    tr = runs["cspe"]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_two_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=300) for _ in procs], key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, it0, ac0, an0), (_, it1, ac1, an1) = out
+    assert np.array_equal(it0, it1) and np.array_equal(ac0, ac1) and np.array_equal(an0, an1)
+    for i in range(10):
+        assert rel(_field(ac0[i], an0[i]), _field(tr.a_c[i + 1], tr.a_n[i + 1])) <= REL_FIELD
