@@ -40,6 +40,7 @@ struct FamDev {
   double Gk[MAXS * MAXS];// POD Galerkin scratch
   long long products, accepted, dropped, evictions, pod_applies;
   long long proj_count;
+  double gs[MAXS + 2];   // POD: one-pass Galerkin sums before the scatter into Gk / d
 };
 
 // Device-wide run state of the stepper.

@@ -176,7 +176,8 @@ constexpr int RQ = MAXS + 2;  // max values reduced by one kernel
 // reduction that produced its inputs (one kernel boundary less per step of
 // the CSPE/POD chains): the CSPE projection solve, the insert gates and
 // decision, the Galerkin commit, the POD push commit.
-enum PostKind : int { POST_NONE = 0, POST_PROJECT, POST_GATE, POST_GATE_C2, POST_DECIDE, POST_COMMIT, POST_POD_PUSH };
+enum PostKind : int { POST_NONE = 0, POST_PROJECT, POST_GATE, POST_GATE_C2, POST_DECIDE, POST_COMMIT, POST_POD_PUSH,
+                      POST_GAL_SCATTER };
 struct Post {
   int kind = POST_NONE;
   FamDev *f = nullptr;
@@ -359,11 +360,10 @@ __global__ void __launch_bounds__(kBlock) k_axpy_dots(int64_t npair, double *con
 
 // out = sum_j c_j A_{order[j]} (0 when k == 0)
 template <int KB>
-__global__ void __launch_bounds__(kBlock) k_comb(int64_t npair, double *const *tab, const int *order,
-                                                 const int *kptr, const double *c, double *outv) {
+__device__ __forceinline__ void comb_body(int64_t npair, double *const *tab, const int *order, int k,
+                                          const double *c, double *outv) {
   __shared__ const double2 *ptr[KB];
   __shared__ double cs[KB];
-  const int k = *kptr;
   if (threadIdx.x < k) {
     ptr[threadIdx.x] = reinterpret_cast<const double2 *>(tab[order[threadIdx.x]]);
     cs[threadIdx.x] = c[threadIdx.x];
@@ -396,6 +396,22 @@ __global__ void __launch_bounds__(kBlock) k_comb(int64_t npair, double *const *t
       out2[p] = make_double2(tx, ty);
     }
   }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kBlock) k_comb(int64_t npair, double *const *tab, const int *order,
+                                                 const int *kptr, const double *c, double *outv) {
+  comb_body<KB>(npair, tab, order, *kptr, c, outv);
+}
+
+// the same for lo < k <= KB only (k read on the device: a small-k and a
+// large-k instance are both launched, exactly one of them runs)
+template <int KB>
+__global__ void __launch_bounds__(kBlock) k_comb_range(int64_t npair, double *const *tab, const int *order,
+                                                       const int *kptr, const double *c, double *outv, int lo) {
+  const int k = *kptr;
+  if (k <= lo || k > KB) return;
+  comb_body<KB>(npair, tab, order, k, c, outv);
 }
 
 // CSPE: u = w/nrm into U[slot], ku = K u into KU[slot], cross_j = U_{order[j]}.ku (j<kprime), diag = u.ku
@@ -432,6 +448,154 @@ __global__ void __launch_bounds__(kBlock) k_cspe_product(Lay L, const uint32_t *
   last_block_reduce(acc, kp + 1, partials, counter, f->d + 0, post);
 }
 
+// POD basis for podk <= KMAX as one flat 16-byte pass (snapshots are 0
+// off the partition, so B is too): B_j = (sum_l X_{order[l]} W[l][j]) /
+// sigma_j in the order of k_pod_basis (l ascending from l = 0)
+constexpr int kBasisFlatMax = 8;
+
+template <int KMAX>
+__global__ void __launch_bounds__(kBlock) k_pod_basis_flat(int64_t npair, FamDev *f, double *const *Xtab,
+                                                           double *const *Btab) {
+  __shared__ const double2 *xp[MAXS];
+  __shared__ double2 *bp[KMAX];
+  __shared__ double Wt[MAXS * KMAX];
+  __shared__ double sg[KMAX];
+  const int m = f->k, kk = f->podk;
+  if (kk == 0 || kk > KMAX) return;
+  if (threadIdx.x < m) xp[threadIdx.x] = reinterpret_cast<const double2 *>(Xtab[f->order[threadIdx.x]]);
+  if (threadIdx.x < kk) {
+    bp[threadIdx.x] = reinterpret_cast<double2 *>(Btab[threadIdx.x]);
+    sg[threadIdx.x] = f->pod_sigma[threadIdx.x];
+  }
+  for (int q = threadIdx.x; q < MAXS * KMAX; q += blockDim.x) {
+    const int l = q / KMAX, j = q % KMAX;
+    Wt[q] = (l < MAXS && j < MAXS) ? f->W[l * MAXS + j] : 0.0;
+  }
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npair; p += stride) {
+    double tx[KMAX], ty[KMAX];
+    {
+      const double2 x0 = __ldcg(xp[0] + p);
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) {
+        tx[j] = mul(x0.x, Wt[j]);
+        ty[j] = mul(x0.y, Wt[j]);
+      }
+    }
+#pragma unroll 4
+    for (int l = 1; l < m; ++l) {
+      const double2 xv = __ldcg(xp[l] + p);
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) {
+        tx[j] = add(tx[j], mul(xv.x, Wt[l * KMAX + j]));
+        ty[j] = add(ty[j], mul(xv.y, Wt[l * KMAX + j]));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+      if (j < kk) bp[j][p] = make_double2(tx[j] / sg[j], ty[j] / sg[j]);
+  }
+}
+
+// POD Galerkin for podk <= 5 in one flat pass over B, K B and the rhs (all 0
+// off the partition): gs[j*k + i] = B_i . KB_j, gs[k*k + i] = B_i . rhs,
+// scattered into Gk / d by the last block (POST_GAL_SCATTER)
+template <int K>
+__device__ __forceinline__ void gal_body(int64_t npair, double *const *Btab, double *const *KBtab,
+                                         const double *rhs, double *acc) {
+  const double2 *B[K], *KB[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    B[i] = reinterpret_cast<const double2 *>(Btab[i]);
+    KB[i] = reinterpret_cast<const double2 *>(KBtab[i]);
+  }
+  const double2 *R = reinterpret_cast<const double2 *>(rhs);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npair; p += stride) {
+    double2 b[K], kb[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      b[i] = __ldcg(B[i] + p);
+      kb[i] = __ldcg(KB[i] + p);
+    }
+    const double2 r = __ldcg(R + p);
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        acc[j * K + i] = add(acc[j * K + i], mul(b[i].x, kb[j].x));
+        acc[j * K + i] = add(acc[j * K + i], mul(b[i].y, kb[j].y));
+      }
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      acc[K * K + i] = add(acc[K * K + i], mul(b[i].x, r.x));
+      acc[K * K + i] = add(acc[K * K + i], mul(b[i].y, r.y));
+    }
+  }
+}
+
+constexpr int kGalFusedMax = 5;  // k*k + k <= RQ
+
+__global__ void __launch_bounds__(kBlock) k_pod_galerkin_fused(int64_t npair, FamDev *f, double *const *Btab,
+                                                               double *const *KBtab, const double *__restrict__ rhs,
+                                                               double *partials, unsigned int *counter) {
+  const int kk = f->podk;
+  if (kk == 0 || kk > kGalFusedMax) return;
+  double acc[kGalFusedMax * kGalFusedMax + kGalFusedMax];
+#pragma unroll
+  for (int q = 0; q < kGalFusedMax * kGalFusedMax + kGalFusedMax; ++q) acc[q] = 0.0;
+  switch (kk) {
+    case 1: gal_body<1>(npair, Btab, KBtab, rhs, acc); break;
+    case 2: gal_body<2>(npair, Btab, KBtab, rhs, acc); break;
+    case 3: gal_body<3>(npair, Btab, KBtab, rhs, acc); break;
+    case 4: gal_body<4>(npair, Btab, KBtab, rhs, acc); break;
+    default: gal_body<5>(npair, Btab, KBtab, rhs, acc); break;
+  }
+  Post post;
+  post.kind = POST_GAL_SCATTER;
+  post.f = f;
+  last_block_reduce(acc, kk * kk + kk, partials, counter, f->gs, post);
+}
+
+// POD push as one flat 16-byte pass: the snapshot copy and its Gram row
+template <int KB>
+__global__ void __launch_bounds__(kBlock) k_pod_push_flat(int64_t npair, FamDev *f, double *const *Xtab, int n_pod,
+                                                          const double *__restrict__ y, double *partials,
+                                                          unsigned int *counter, Post post) {
+  __shared__ const double2 *ptr[MAXS];
+  const int m = f->k;
+  const int slot = (m < n_pod) ? m : f->order[0];
+  const int first = (m < n_pod) ? 0 : 1;
+  const int nother = m - first;
+  if (threadIdx.x < nother) ptr[threadIdx.x] = reinterpret_cast<const double2 *>(Xtab[f->order[first + threadIdx.x]]);
+  __syncthreads();
+  double2 *X = reinterpret_cast<double2 *>(Xtab[slot]);
+  const double2 *Y = reinterpret_cast<const double2 *>(y);
+  double acc[KB + 2];
+#pragma unroll
+  for (int q = 0; q < KB + 2; ++q) acc[q] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npair; p += stride) {
+    const double2 yv = __ldcg(Y + p);
+    double2 u[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < nother) u[j] = __ldcg(ptr[j] + p);
+    X[p] = yv;
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < nother) {
+        acc[j] = add(acc[j], mul(u[j].x, yv.x));
+        acc[j] = add(acc[j], mul(u[j].y, yv.y));
+      }
+    acc[KB] = add(acc[KB], mul(yv.x, yv.x));
+    acc[KB] = add(acc[KB], mul(yv.y, yv.y));
+  }
+  acc[nother] = acc[KB];
+  last_block_reduce(acc, nother + 1, partials, counter, f->d, post);
+}
+
 // POD: B_j = (sum_l X_{order[l]} W[l][j]) / sigma_j  for j < podk
 __global__ void __launch_bounds__(kBlock) k_pod_basis(Lay L, const uint32_t *__restrict__ mask, FamDev *f,
                                                       double *const *Xtab, double *const *Btab) {
@@ -440,7 +604,7 @@ __global__ void __launch_bounds__(kBlock) k_pod_basis(Lay L, const uint32_t *__r
   __shared__ double Wt[MAXS * MAXS];
   __shared__ double sg[MAXS];
   const int m = f->k, kk = f->podk;
-  if (kk == 0) return;
+  if (kk <= kBasisFlatMax) return;  // k_pod_basis_flat did it (or nothing to do)
   if (threadIdx.x < m) xp[threadIdx.x] = Xtab[f->order[threadIdx.x]];
   if (threadIdx.x < kk) { bp[threadIdx.x] = Btab[threadIdx.x]; sg[threadIdx.x] = f->pod_sigma[threadIdx.x]; }
   for (int q = threadIdx.x; q < MAXS * MAXS; q += blockDim.x) Wt[q] = f->W[q];
@@ -479,7 +643,7 @@ __global__ void __launch_bounds__(kBlock) k_pod_galerkin(Lay L, const uint32_t *
                                                          unsigned int *counters) {
   const int j = blockIdx.y;
   const int kk = f->podk;
-  if (j > kk) return;
+  if (j > kk || kk <= kGalFusedMax) return;  // k_pod_galerkin_fused did it
   __shared__ const double *bp[MAXS];
   if (threadIdx.x < kk) bp[threadIdx.x] = Btab[threadIdx.x];
   __syncthreads();
@@ -686,8 +850,17 @@ __device__ void pod_push_commit(FamDev *f, int n_pod) {
   f->G[slot * MAXS + slot] = f->d[nother];
 }
 
+// one-pass Galerkin sums -> Gk (column j contiguous) and d
+__device__ void gal_scatter(FamDev *f) {
+  const int k = f->podk;
+  for (int j = 0; j < k; ++j)
+    for (int i = 0; i < k; ++i) f->Gk[j * MAXS + i] = f->gs[j * k + i];
+  for (int i = 0; i < k; ++i) f->d[i] = f->gs[k * k + i];
+}
+
 __device__ void run_post(const Post &p) {
   switch (p.kind) {
+    case POST_GAL_SCATTER: gal_scatter(p.f); break;
     case POST_PROJECT: cspe_project_small(p.f); break;
     case POST_GATE: cspe_gate(p.f); break;
     case POST_GATE_C2: cspe_gate_c2(p.f); break;
@@ -1277,18 +1450,25 @@ static int start_vector(mq_ctx *ctx, int fam, const double *rhs, double *x0) {
     case MQ_STRAT_POD: {
       k_pod_eig<<<1, 256, 0, st>>>(f, s->cfg.eps_pod);
       LAUNCH_CHECK();
+      k_pod_basis_flat<kBasisFlatMax><<<G, kBlock, 0, st>>>(L.total / 2, f, s->d_X[fam], s->d_B);
+      LAUNCH_CHECK();
       k_pod_basis<<<stream_grid(ctx), kBlock, 0, st>>>(L, ctx->d_mask, f, s->d_X[fam], s->d_B);
       LAUNCH_CHECK();
       dim3 g2(stream_grid(ctx), s->cfg.n_pod);
       k_spmv_multi<<<g2, kBlock, 0, st>>>(L, ctx->d_mask, ctx->kn_diag, ctx->kn_off, f, s->d_B, s->d_KB);
       LAUNCH_CHECK();
       dim3 g3(G, s->cfg.n_pod + 1);
+      k_pod_galerkin_fused<<<G, kBlock, 0, st>>>(L.total / 2, f, s->d_B, s->d_KB, rhs, s->d_red, s->d_cnt + 1);
+      LAUNCH_CHECK();
       KB_LAUNCH(s->kb, k_pod_galerkin, g3, kBlock, st, L, ctx->d_mask, f, s->d_B, s->d_KB, rhs, s->d_red,
                 s->d_cnt + 1);
       LAUNCH_CHECK();
       k_pod_solve<<<1, 32, 0, st>>>(f, s->d_run);
       LAUNCH_CHECK();
-      KB_LAUNCH(s->kb, k_comb, G, kBlock, st, L.total / 2, s->d_B, s->d_iota, &f->podk, f->coef, x0);
+      // small-k and large-k instances, exactly one runs (podk is on the device)
+      k_comb_range<4><<<G, kBlock, 0, st>>>(L.total / 2, s->d_B, s->d_iota, &f->podk, f->coef, x0, -1);
+      LAUNCH_CHECK();
+      KB_LAUNCH(s->kb, k_comb_range, G, kBlock, st, L.total / 2, s->d_B, s->d_iota, &f->podk, f->coef, x0, 4);
       LAUNCH_CHECK();
       break;
     }
@@ -1382,7 +1562,7 @@ static int observe(mq_ctx *ctx, int fam, const double *y, const ObsRes &o, bool 
       post.kind = POST_POD_PUSH;
       post.f = f;
       post.n_pod = s->cfg.n_pod;
-      KB_LAUNCH(s->kb, k_pod_push, G, kBlock, st, L, ctx->d_mask, f, s->d_X[fam], s->cfg.n_pod, y, o.red, o.cnt,
+      KB_LAUNCH(s->kb, k_pod_push_flat, G, kBlock, st, L.total / 2, f, s->d_X[fam], s->cfg.n_pod, y, o.red, o.cnt,
                 post);
       LAUNCH_CHECK();
       break;
