@@ -592,6 +592,40 @@ def cfg4_sharded(dist, world, local, hbm_peak, warmup=1, steps=2):
                       "reduction), max over ranks"}
 
 
+def ensemble_members(dist, world, rank, local, members_per_rank=2, warmup=3, steps=5):
+    """configs[3] (256 independent 64^3 members, CSPE k = 5): the members are
+    sharded over the ranks (ensemble.shard, weak scaling, no collective); each
+    rank times the first ``members_per_rank`` members of its shard through the
+    device step loop (CUDA events per step, L2 flushed before each), one member
+    at a time on the whole GPU (the resident single-member PCG is
+    faster per member-iteration than a batched or sliced one at 64^3)."""
+    from paper_1611_06721_b200 import PcgConfig, SchurOperator, configs as C
+    from paper_1611_06721_b200 import ensemble as E
+    spec = C.config_spec(3)
+    mine = list(E.shard(256, world, rank))[:members_per_rank]
+    total_ms, per, its = 0.0, [], []
+    for m in mine:
+        prob, jf, kf, dt = E.member_problem(m)
+        op = SchurOperator(prob, pcg=PcgConfig(rel_tol=spec.rel_tol, max_iter=spec.max_iter),
+                           strategy="cspe", max_cols=spec.max_cols, device=local)
+        op.set_probe()
+        step_ms, _, iters, _ = time_device_steps(op, spec, warmup, steps, dt=dt)
+        op.grid.close()
+        total_ms += float(step_ms.sum())
+        per.append({"member": m, "j_factor": jf, "kappa_factor": kf, "dt": dt,
+                    "steps_per_s": steps / (float(step_ms.sum()) * 1e-3)})
+        its.append(iters.tolist())
+    t_max = max_over_ranks(total_ms, dist, local)
+    value = world * len(mine) * steps / (t_max * 1e-3)
+    return {"workload": "cfg3_ensemble_64cube_cspe5", "scaling": "weak",
+            "sharding": "256 members in contiguous blocks over the ranks, no data-path collective",
+            "members_per_rank_timed": len(mine), "members_per_rank_total": len(E.shard(256, world, rank)),
+            "steps_after_warmup": [warmup + 1, warmup + steps],
+            "value": value, "unit": "member-steps/s",
+            "projected_s_for_256x200_steps": 256 * 200 / value, "members_rank0": per,
+            "timed_step_iterations_rank0": its}
+
+
 def run_device_arm(args):
     world, rank, local, dist = dist_init()
     from paper_1611_06721_b200 import PcgConfig, SchurOperator, _lib
@@ -638,6 +672,9 @@ def run_device_arm(args):
         except Exception as exc:  # noqa: BLE001  (reported, never silently dropped)
             sharded = {"workload": "cfg4_256cube_two_blocks_cspe5_sharded", "ranks": world,
                        "error": f"{type(exc).__name__}: {exc}"}
+    ens = None
+    if not args.skip_secondary:
+        ens = ensemble_members(dist, world, rank, local)
     line = None
     if rank == 0:
         # the device leg's steps, host-timed three times from a fresh
@@ -679,6 +716,7 @@ def run_device_arm(args):
             "roofline_cfg4_1gpu": roof4,
             "cfg4_steps_1gpu": steps4,
             "cfg4_sharded": sharded,
+            "cfg3_ensemble": ens,
             "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "explicit_euler_step + recover_an + probe_b (host arrays)",
                     "runs": e2e_vals, "estimator": "median of 3 runs of the timed steps"},

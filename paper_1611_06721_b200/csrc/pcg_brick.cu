@@ -364,6 +364,42 @@ __device__ __forceinline__ void flat_pairs(int64_t total, F f) {
   for (; p < npair; p += stride) f(p, stride, 1);
 }
 
+#ifndef MQ_K2_BRICK
+#define MQ_K2_BRICK 0
+#endif
+// K2 over this CTA's own bricks, planes in reverse order: the rows of r and
+// Ap that K1 touched last are the first ones K2 reads back (still in L2), and
+// the planes K2 writes last are the ones the next K1 reads first.  Every
+// active dof lies in a brick (node positions j < ny, k < nz, i < nx); the
+// entries outside the bricks are 0 in r and Ap and stay 0.  f(e) per own
+// position, one warp per (plane, component, row) of 32 k positions.
+template <class F>
+__device__ __forceinline__ void brick_rows_reverse(const BrickGeo &g, const Lay &L, int G, F f) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int U = 4;  // rows in flight per warp
+  for (int bi = blockIdx.x; bi < g.nbricks; bi += G) {
+    int i0, i1, j0, k0;
+    brick_of(g, bi, i0, i1, j0, k0);
+    const int k = k0 + lane;
+    const bool kok = k < g.nz;
+    const int nrows = (i1 - i0) * 3 * TJ;
+    for (int q0 = warp * U; q0 < nrows; q0 += kWarps * U) {
+      int64_t e[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + u;
+        const int plane = i1 - 1 - q / (3 * TJ);
+        const int rem = q % (3 * TJ);
+        const int c = rem / TJ, jj = j0 + rem % TJ;
+        ok[u] = q < nrows && kok && jj < g.ny;
+        e[u] = c * L.C + L.off + (int64_t)plane * L.Si + (int64_t)jj * L.Sj + k;
+      }
+      f(e, ok);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constant__ TmaPcgArgs A) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t bars[NR];
@@ -509,6 +545,27 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       alpha = rz / pap;
       // ---- K2: r -= alpha Ap (flat, all padded entries; non-dofs stay 0) ----
       double v2[2] = {0.0, 0.0};
+#if MQ_K2_BRICK
+      brick_rows_reverse(g, L, G, [&](const int64_t *e, const bool *ok) {
+        double rv[4], av[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (ok[u]) {
+            rv[u] = __ldcg(r + e[u]);
+            av[u] = __ldcg(ap + e[u]);
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (ok[u]) {
+            const double r0 = sub(rv[u], mul(alpha, av[u]));
+            r[e[u]] = r0;
+            const double z0 = jac ? mul(inv, r0) : r0;
+            v2[0] = add(v2[0], mul(r0, r0));
+            v2[1] = add(v2[1], mul(r0, z0));
+          }
+      });
+      if (false)
+#endif
       flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
         double2 rv[kUnroll], av[kUnroll];
 #pragma unroll
