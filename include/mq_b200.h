@@ -358,6 +358,14 @@ int mq_ss_euler(mq_ctx *ctx, double dt, double *owned_out);
 int mq_ss_an(mq_ctx *ctx, double *a_n_local);
 int mq_ss_diag(mq_ctx *ctx, mq_diag *out);
 
+/* Guard check: count the off-partition entries (boundary, conducting, guard
+ * and padding positions; a slab's ghost planes excepted) that are not 0 in
+ * every device vector the context owns (PCG scratch, user vectors, the
+ * solver's caches and work vectors).  The stencils read those entries as
+ * boundary values, so any stray write there shows; tests run it after runs
+ * (memory-safety evidence on a pool where compute-sanitizer is closed). */
+int mq_guard_check(mq_ctx *ctx, int64_t *bad_entries, int32_t *bad_vectors, int32_t *checked);
+
 /* ---- timing (CUDA events on the context stream) ------------------------- */
 /* Sum of the device times of the PCG launches of the last step (when PCG
  * timing is enabled with mq_pcg_stats(..., 1)). */

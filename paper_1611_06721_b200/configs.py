@@ -198,6 +198,39 @@ def make_problem(index: int, *, j_scale: float = 1.0, kappa_scale: float = 1.0) 
                    meta={"spec": spec, "loops": loops})
 
 
+def builtin_problem(cells: int = 8, h: float = 5e-3, kappa: float = 5e6,
+                    brauer: tuple = (49.4, 1.46, 520.6), amps: float = 50000.0, tau: float = 0.5, *,
+                    linear: bool = False) -> Problem:
+    """The reference's benchmark model (model.py:582-622) as a Problem: a
+    2 x 2 x (cells - 2) conductor bar at the grid centre, threaded by one
+    square edge loop one cell in from the boundary at mid height, carrying
+    ``amps`` with the exponential ramp 1 - exp(-t/tau); COIL cells mark the
+    two cell layers around the loop; ``linear`` freezes the bar reluctivity
+    at its unsaturated value k1 + k3."""
+    import math
+    if cells < 6:
+        raise ValueError("builtin model needs at least 6 cells per direction")
+    n = int(cells)
+    mat = np.zeros((n, n, n), dtype=np.int8)
+    b0, b1 = n // 2 - 1, n // 2
+    mat[b0:b1 + 1, b0:b1 + 1, 1:n - 1] = CONDUCTOR
+    lp = LoopSpec(1, n - 1, 1, n - 1, n // 2, float(amps))
+    coil = np.zeros((n, n, n), dtype=bool)
+    for kk in (lp.k0 - 1, lp.k0):
+        if 0 <= kk < n:
+            coil[lp.i0:lp.i1, lp.j0 - 1:lp.j0 + 1, kk] = True
+            coil[lp.i0:lp.i1, lp.j1 - 1:lp.j1 + 1, kk] = True
+            coil[lp.i0 - 1:lp.i0 + 1, lp.j0:lp.j1, kk] = True
+            coil[lp.i1 - 1:lp.i1 + 1, lp.j0:lp.j1, kk] = True
+    mat[coil & (mat == AIR)] = COIL
+    k1, k2, k3 = (float(v) for v in brauer)
+    nu = (0.0, 0.0, k1 + k3) if linear else (k1, k2, k3)
+    tau = float(tau)
+    return Problem(material=mat, h=float(h), kappa=float(kappa), brauer=nu, nu_air=NU_VACUUM,
+                   pattern=source_pattern(mat, [lp]), waveform=lambda t: 1.0 - math.exp(-t / tau),
+                   name=f"builtin_{n}", meta={"loops": [lp], "linear": bool(linear)})
+
+
 def ensemble_factors(n_members: int = 256, seed: int = 0):
     """Config 3: J then kappa factors, each U(0.8, 1.2)."""
     rng = np.random.default_rng(seed)

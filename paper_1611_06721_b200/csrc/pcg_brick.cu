@@ -44,8 +44,16 @@ constexpr int BOXP = 352;                      // box slot padded to a 128-byte 
 // in place into p_new, read by the stencil) plus NA planes in flight; the
 // p_old ring only the NA in-flight planes (p_old is dead once its plane is
 // converted).  Same bytes as a 5-stage (r, p) ring, one more plane ahead.
+#ifndef MQ_MARCH2
+#define MQ_MARCH2 0
+#endif
+// K1 stages of * p_new (the off-diagonal product of every staged value,
+// formed once) instead of p_new: stencil3s, bit-identical rows
+#ifndef MQ_PRESCALE
+#define MQ_PRESCALE 0
+#endif
 constexpr int NA = MQ_NAHEAD;                  // planes in flight ahead of i+1
-constexpr int NR = NA + 3, NP = NA;            // r-ring and p-ring slots
+constexpr int NR = NA + 3 + MQ_MARCH2, NP = NA;  // r-ring and p-ring slots
 constexpr int NHALO = 2 * HK + 2 * TJ;         // 84 halo positions per plane
 static_assert(TJ * TK == kBlock, "one thread per tile position");
 static_assert(HP <= BOXP && (BOXP * 8) % 128 == 0, "TMA destination alignment");
@@ -91,6 +99,61 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, u
       "[%6];" ::"r"(su32(dst)),
       "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
       : "memory");
+}
+
+// L2 residency hints (MQ_L2HINT): r and Ap are each read twice per
+// iteration (r: K1's TMA march and K2; Ap: written by K1, read by K2), 106 MB
+// at 128^3 against a 126 MB L2.  Their loads and stores carry an evict_last
+// policy, the streams touched once per iteration (p_old, p_new, x) evict_first,
+// so that K2 and the next K1 find r and Ap in L2.
+#ifndef MQ_L2HINT
+#define MQ_L2HINT 0
+#endif
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+  uint64_t p;
+  if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_hint(double *a, double v, uint64_t pol) {
+#if MQ_L2HINT
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+#else
+  (void)pol;
+  *a = v;
+#endif
+}
+__device__ __forceinline__ double2 ld2_hint(const double2 *a, uint64_t pol) {
+#if MQ_L2HINT
+  double2 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+#else
+  (void)pol;
+  return __ldcg(a);
+#endif
+}
+__device__ __forceinline__ void st2_hint(double2 *a, double2 v, uint64_t pol) {
+#if MQ_L2HINT
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y), "l"(pol)
+               : "memory");
+#else
+  (void)pol;
+  *a = v;
+#endif
+}
+__device__ __forceinline__ void tma_load_4d_hint(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                                 int c2, int c3, uint64_t pol) {
+#if MQ_L2HINT
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(su32(dst)),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar)), "l"(pol)
+      : "memory");
+#else
+  (void)pol;
+  tma_load_4d(dst, map, bar, c0, c1, c2, c3);
+#endif
 }
 
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
@@ -159,6 +222,60 @@ __device__ __forceinline__ double stencil3(int c, double dg, double of, V v) {
   return s;
 }
 
+// stencil3 with every off-diagonal product precomputed: v(c', di, dj, dk)
+// returns of * p of that position (formed once per staged value when it is
+// converted, the same rounding as forming it in every row that uses it), own
+// is the raw p of the row's own position for the diagonal term.  Identical
+// bits to stencil3 on the raw values; 13 -> 1 multiplication per row.
+template <class V>
+__device__ __forceinline__ double stencil3s(int c, double dg, double own, V v) {
+  double s;
+  if (c == 0) {
+    s = -v(0, 0, -1, 0);
+    s = sub(s, v(0, 0, 0, -1));
+    s = add(s, mul(dg, own));
+    s = sub(s, v(0, 0, 0, 1));
+    s = sub(s, v(0, 0, 1, 0));
+    s = add(s, v(1, 0, -1, 0));
+    s = sub(s, v(1, 0, 0, 0));
+    s = sub(s, v(1, 1, -1, 0));
+    s = add(s, v(1, 1, 0, 0));
+    s = add(s, v(2, 0, 0, -1));
+    s = sub(s, v(2, 0, 0, 0));
+    s = sub(s, v(2, 1, 0, -1));
+    s = add(s, v(2, 1, 0, 0));
+  } else if (c == 1) {
+    s = v(0, -1, 0, 0);
+    s = sub(s, v(0, -1, 1, 0));
+    s = sub(s, v(0, 0, 0, 0));
+    s = add(s, v(0, 0, 1, 0));
+    s = sub(s, v(1, -1, 0, 0));
+    s = sub(s, v(1, 0, 0, -1));
+    s = add(s, mul(dg, own));
+    s = sub(s, v(1, 0, 0, 1));
+    s = sub(s, v(1, 1, 0, 0));
+    s = add(s, v(2, 0, 0, -1));
+    s = sub(s, v(2, 0, 0, 0));
+    s = sub(s, v(2, 0, 1, -1));
+    s = add(s, v(2, 0, 1, 0));
+  } else {
+    s = v(0, -1, 0, 0);
+    s = sub(s, v(0, -1, 0, 1));
+    s = sub(s, v(0, 0, 0, 0));
+    s = add(s, v(0, 0, 0, 1));
+    s = add(s, v(1, 0, -1, 0));
+    s = sub(s, v(1, 0, -1, 1));
+    s = sub(s, v(1, 0, 0, 0));
+    s = add(s, v(1, 0, 0, 1));
+    s = sub(s, v(2, -1, 0, 0));
+    s = sub(s, v(2, 0, -1, 0));
+    s = add(s, mul(dg, own));
+    s = sub(s, v(2, 0, 1, 0));
+    s = sub(s, v(2, 1, 0, 0));
+  }
+  return s;
+}
+
 __device__ __forceinline__ int rslot(int q) { return (q + NR) % NR; }  // q >= -1
 __device__ __forceinline__ int pslot(int q) { return (q + NP) % NP; }
 
@@ -221,6 +338,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   const uint32_t *mask = a.mask;
   double *x = a.x;
 
+  const uint64_t pol_keep = l2_policy(true), pol_drop = l2_policy(false);
   auto issue = [&](int q) {
     if (tid == 0) {
       const int s = rslot(q), sp = pslot(q);
@@ -229,43 +347,38 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 #pragma unroll
       // box origin (k0-1, j0-1, q) in node coordinates = (k0, j0, q+1) in the
       // guard-shifted map: never negative
-      for (int c = 0; c < 3; ++c) tma_load_4d(mc.sr[s].v[c], mr, &mc.bars[s], k0, j0, q + 1, c);
+      for (int c = 0; c < 3; ++c) tma_load_4d_hint(mc.sr[s].v[c], mr, &mc.bars[s], k0, j0, q + 1, c, pol_keep);
       if (with_p) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) tma_load_4d(mc.sp[sp].v[c], mp, &mc.bars[s], k0, j0, q + 1, c);
+        for (int c = 0; c < 3; ++c) tma_load_4d_hint(mc.sp[sp].v[c], mp, &mc.bars[s], k0, j0, q + 1, c, pol_drop);
       }
     }
   };
-  // Own-position mask words and x values are software-pipelined one plane
-  // ahead in registers: they are loaded while the previous plane is
-  // processed, so neither their latency nor the TMA's is exposed.
-  uint32_t mw_nx[3] = {0u, 0u, 0u};
-  double xo_nx[3] = {0.0, 0.0, 0.0};
-  double p2_nx[3] = {0.0, 0.0, 0.0};
-  auto prefetch_own = [&](int q, bool own_plane) {
+  // Own-position mask words and x values are software-pipelined ahead in
+  // registers: they are loaded while earlier planes are processed, so neither
+  // their latency nor the TMA's is exposed.
+  struct OwnPre {
+    uint32_t mw[3];
+    double xo[3], p2[3];
+  };
+  auto prefetch_own = [&](OwnPre &o, int q, bool own_plane) {
     if (own_plane && own_ok) {
       const int64_t qb = (int64_t)q * L.Si;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const int64_t e = c * L.C + qb + pos_own;
-        mw_nx[c] = __ldg(mask + (e >> 5));
-        if (xm >= 1) xo_nx[c] = __ldcg(x + e);
-        if (xm == 2) p2_nx[c] = __ldcg(pnew + e);
+        o.mw[c] = __ldg(mask + (e >> 5));
+        if (xm >= 1) o.xo[c] = __ldcg(x + e);
+        if (xm == 2) o.p2[c] = __ldcg(pnew + e);
       }
     } else {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) mw_nx[c] = 0u;
+      for (int c = 0; c < 3; ++c) o.mw[c] = 0u;
     }
   };
-  // returns the active-dof bits (bit c = component c) of the own position;
-  // next_q/next_own describe the plane whose own data is prefetched now
-  auto convert = [&](int q, bool own_plane, int next_q, bool next_own) -> uint32_t {
+  // returns the active-dof bits (bit c = component c) of the own position
+  auto convert = [&](int q, bool own_plane, const OwnPre &o, double (&raw)[3]) -> uint32_t {
     const int s = rslot(q);
-    uint32_t mw[3];
-    double xo[3], p2[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) { mw[c] = mw_nx[c]; xo[c] = xo_nx[c]; p2[c] = p2_nx[c]; }
-    prefetch_own(next_q, next_own);
     const int64_t qb = (int64_t)q * L.Si;
 #ifdef MQ_TRACE_MARCH
     if (mc.tr && q - i0 >= 1 && q - i0 < 33) mc.tr[4 * (q - i0 - 1) + 0] = globaltimer_ns();
@@ -280,10 +393,14 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const int64_t e = c * L.C + qb + pos_own;
-        act |= ((mw[c] >> (e & 31)) & 1u) << c;
+        act |= ((o.mw[c] >> (e & 31)) & 1u) << c;
       }
     }
-    if (MODE == kInit) return act;  // the staged x0 is used as is
+    if (MODE == kInit) {  // the staged x0 is used as is
+#pragma unroll
+      for (int c = 0; c < 3; ++c) raw[c] = mc.sr[s].v[c][s_own];
+      return act;
+    }
     double (&Sr)[3][BOXP] = mc.sr[s].v;
     const double (&Sp)[3][BOXP] = mc.sp[pslot(q)].v;
 #pragma unroll
@@ -295,36 +412,88 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
         const double po = Sp[c][s_own];
         pv = add(z, mul(beta, po));
         if (xm >= 1 && ((act >> c) & 1u)) {
-          const double xv = xm == 2 ? add(xo[c], mul(alpha_prev2, p2[c])) : xo[c];
-          x[c * L.C + qb + pos_own] = add(xv, mul(alpha_prev, po));
+          const double xv = xm == 2 ? add(o.xo[c], mul(alpha_prev2, o.p2[c])) : o.xo[c];
+          st_hint(x + c * L.C + qb + pos_own, add(xv, mul(alpha_prev, po)), pol_drop);
         }
       }
-      Sr[c][s_own] = pv;
+      raw[c] = pv;
+      Sr[c][s_own] = (MODE == kK1 && MQ_PRESCALE) ? mul(a.of, pv) : pv;
       if ((act >> c) & 1u) {
-        pnew[c * L.C + qb + pos_own] = pv;
+        st_hint(pnew + c * L.C + qb + pos_own, pv, pol_drop);
         push(q, c, pos_own - L.Si, pv);
       }
     }
     if (hs >= 0) {
       const double rq = Sr[hc][hs];
       const double z = jac ? mul(inv, rq) : rq;
-      Sr[hc][hs] = first ? z : add(z, mul(beta, Sp[hc][hs]));
+      const double ph = first ? z : add(z, mul(beta, Sp[hc][hs]));
+      Sr[hc][hs] = (MODE == kK1 && MQ_PRESCALE) ? mul(a.of, ph) : ph;
     }
     return act;
+  };
+  auto stencil_plane = [&](int i, uint32_t act, const double (&raw)[3]) {
+    if (!act) return;
+    const int64_t qb = (int64_t)i * L.Si;
+    const int sm1 = rslot(i - 1), s0 = rslot(i), sp1 = rslot(i + 1);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if ((act >> c) & 1u)
+        row(c, c * L.C + qb + pos_own, [&](int cc, int di, int dj, int dk) {
+          const int s = di < 0 ? sm1 : (di == 0 ? s0 : sp1);
+          return mc.sr[s].v[cc][s_own + dj * HK + dk];
+        }, raw[c]);
+    }
   };
 
   // prologue: planes i0-1 .. i0+NA-2 in flight, then convert i0-1 and i0,
   // each followed by the issue of the plane that takes over its p slot
   const int last = i1;  // planes i0-1 .. i1 are needed
+  OwnPre pa, pb;
+  double rw[3], rw1[3], rw2[3];
   for (int q = i0 - 1; q <= i0 + NA - 2 && q <= last; ++q) issue(q);
-  convert(i0 - 1, false, i0, true);
+  prefetch_own(pa, i0, true);
+  prefetch_own(pb, i0 - 1, false);
+  convert(i0 - 1, false, pb, rw1);
   __syncthreads();
   if (i0 + NA - 1 <= last) issue(i0 + NA - 1);
-  uint32_t act = convert(i0, true, i0 + 1, i0 + 1 < i1);
+#if MQ_MARCH2
+  // two planes per step: converts of planes i+1, i+2, one __syncthreads, the
+  // stencils of planes i, i+1 (twice the independent work per barrier); the
+  // own-position data of the two planes of the next step is prefetched here
+  const OwnPre c0 = pa;
+  prefetch_own(pb, i0 + 1, i0 + 1 < i1);
+  prefetch_own(pa, i0 + 2, i0 + 2 < i1);
+  uint32_t act = convert(i0, true, c0, rw);
+  __syncthreads();
+  if (i0 + NA <= last) issue(i0 + NA);
+  for (int i = i0; i < i1; i += 2) {
+    const bool two = i + 1 < i1;
+    const OwnPre c1 = pb, c2 = pa;
+    prefetch_own(pb, i + 3, i + 3 < i1);
+    prefetch_own(pa, i + 4, i + 4 < i1);
+    const uint32_t a1 = convert(i + 1, i + 1 < i1, c1, rw1);
+    const uint32_t a2 = two ? convert(i + 2, i + 2 < i1, c2, rw2) : 0u;
+    __syncthreads();
+    // r slots of planes i-3, i-2 (last read by the previous step's
+    // stencils), p slots of planes i+1, i+2 (converted before the barrier)
+    if (i + NA + 1 <= last) issue(i + NA + 1);
+    if (two && i + NA + 2 <= last) issue(i + NA + 2);
+    stencil_plane(i, act, rw);
+    if (two) stencil_plane(i + 1, a1, rw1);
+    act = a2;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) rw[c] = rw2[c];
+  }
+#else
+  const OwnPre c0 = pa;
+  prefetch_own(pa, i0 + 1, i0 + 1 < i1);
+  uint32_t act = convert(i0, true, c0, rw);
   __syncthreads();
   if (i0 + NA <= last) issue(i0 + NA);
   for (int i = i0; i < i1; ++i) {
-    const uint32_t act_next = convert(i + 1, i + 1 < i1, i + 2, i + 2 < i1);
+    const OwnPre cur = pa;
+    prefetch_own(pa, i + 2, i + 2 < i1);
+    const uint32_t act_next = convert(i + 1, i + 1 < i1, cur, rw1);
 #ifdef MQ_TRACE_MARCH
     if (mc.tr) mc.tr[4 * (i - i0) + 2] = globaltimer_ns();
 #endif
@@ -335,20 +504,12 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     // r slot of plane i-2 (its last stencil was before this barrier), p slot
     // of plane i+1 (converted before this barrier)
     if (i + NA + 1 <= last) issue(i + NA + 1);
-    if (act) {
-      const int64_t qb = (int64_t)i * L.Si;
-      const int sm1 = rslot(i - 1), s0 = rslot(i), sp1 = rslot(i + 1);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        if ((act >> c) & 1u)
-          row(c, c * L.C + qb + pos_own, [&](int cc, int di, int dj, int dk) {
-            const int s = di < 0 ? sm1 : (di == 0 ? s0 : sp1);
-            return mc.sr[s].v[cc][s_own + dj * HK + dk];
-          });
-      }
-    }
+    stencil_plane(i, act, rw);
     act = act_next;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) rw[c] = rw1[c];
   }
+#endif
   __syncthreads();
 }
 
@@ -400,7 +561,10 @@ __device__ __forceinline__ void brick_rows_reverse(const BrickGeo &g, const Lay 
   }
 }
 
-__global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constant__ TmaPcgArgs A) {
+#ifndef MQ_TMA_MINB
+#define MQ_TMA_MINB 2
+#endif
+__global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __grid_constant__ TmaPcgArgs A) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t bars[NR];
   __shared__ double red[3 * kWarps];
@@ -413,6 +577,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
   const bool jac = a.use_jac != 0;
   double *x = a.x, *r = a.r, *ap = a.ap;
   const double *b = a.b;
+  const uint64_t pol_keep = l2_policy(true), pol_drop = l2_policy(false);
   const int x0_mode = a.x0_mode_dev ? *a.x0_mode_dev : a.x0_mode;
   if (a.err_word && *((volatile const unsigned int *)a.err_word)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -444,7 +609,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
       int i0, i1, j0, k0;
       brick_of(g, bi, i0, i1, j0, k0);
       march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
-                       [&](int c, int64_t e, auto V) {
+                       [&](int c, int64_t e, auto V, double) {
                          const double bv = __ldcg(b + e);
                          const double rv = sub(bv, stencil3(c, dg, of, V));
                          r[e] = rv;
@@ -522,10 +687,19 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
         int i0, i1, j0, k0;
         brick_of(g, bi, i0, i1, j0, k0);
         march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0,
-                       [&](int c, int64_t e, auto V) {
+                       [&](int c, int64_t e, auto V, double own) {
+#ifdef MQ_DIAG_NOSTENCIL
+                         // timing diagnostic only: a 5-point in-plane operator (SPD), 5 of 13 terms
+                         const double av = sub(mul(dg, V(c, 0, 0, 0)),
+                                               mul(of, add(add(V(c, 0, -1, 0), V(c, 0, 1, 0)),
+                                                           add(V(c, 0, 0, -1), V(c, 0, 0, 1)))));
+#elif MQ_PRESCALE
+                         const double av = stencil3s(c, dg, own, V);
+#else
                          const double av = stencil3(c, dg, of, V);
-                         ap[e] = av;
-                         v1[0] = add(v1[0], mul(V(c, 0, 0, 0), av));
+#endif
+                         st_hint(ap + e, av, pol_keep);
+                         v1[0] = add(v1[0], mul(own, av));
                        });
       }
       block_sum<1>(v1, red);
@@ -571,15 +745,15 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_kernel(const __grid_constan
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
           if (u < n) {
-            rv[u] = __ldcg(reinterpret_cast<const double2 *>(r) + p + u * stride);
-            av[u] = __ldcg(reinterpret_cast<const double2 *>(ap) + p + u * stride);
+            rv[u] = ld2_hint(reinterpret_cast<const double2 *>(r) + p + u * stride, pol_keep);
+            av[u] = ld2_hint(reinterpret_cast<const double2 *>(ap) + p + u * stride, pol_drop);
           }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
           if (u < n) {
             const double r0 = sub(rv[u].x, mul(alpha, av[u].x));
             const double r1 = sub(rv[u].y, mul(alpha, av[u].y));
-            reinterpret_cast<double2 *>(r)[p + u * stride] = make_double2(r0, r1);
+            st2_hint(reinterpret_cast<double2 *>(r) + p + u * stride, make_double2(r0, r1), pol_keep);
             const double z0 = jac ? mul(inv, r0) : r0, z1 = jac ? mul(inv, r1) : r1;
             v2[0] = add(v2[0], mul(r0, r0));
             v2[0] = add(v2[0], mul(r1, r1));
@@ -783,7 +957,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_slab_kernel(const __grid_co
       int i0, i1, j0, k0;
       brick_of(g, bi, i0, i1, j0, k0);
       march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
-                       [&](int c, int64_t e, auto V) {
+                       [&](int c, int64_t e, auto V, double) {
                          const double bv = __ldcg(b + e);
                          const double rv = sub(bv, stencil3(c, dg, of, V));
                          r[e] = rv;
@@ -841,10 +1015,14 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_slab_kernel(const __grid_co
         int i0, i1, j0, k0;
         brick_of(g, bi, i0, i1, j0, k0);
         march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, 1, 0.0, pnew, i0, i1, j0, k0,
-                       [&](int c, int64_t e, auto V) {
+                       [&](int c, int64_t e, auto V, double own) {
+#if MQ_PRESCALE
+                         const double av = stencil3s(c, dg, own, V);
+#else
                          const double av = stencil3(c, dg, of, V);
+#endif
                          ap[e] = av;
-                         v1[0] = add(v1[0], mul(V(c, 0, 0, 0), av));
+                         v1[0] = add(v1[0], mul(own, av));
                        },
                        push_p);
       }
@@ -947,7 +1125,7 @@ __global__ void __launch_bounds__(kBlock, 2) kn_apply_tma_kernel(const __grid_co
     int i0, i1, j0, k0;
     brick_of(A.g, bi, i0, i1, j0, k0);
     march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
-                     [&](int c, int64_t e, auto V) { y[e] = stencil3(c, A.a.dg, A.a.of, V); });
+                     [&](int c, int64_t e, auto V, double own) { y[e] = stencil3(c, A.a.dg, A.a.of, V); });
   }
 }
 
@@ -1007,6 +1185,10 @@ static BrickGeo make_geo(int nx, int ny, int nz, int resident) {
       if (2 * c >= chunks) chunks = c;
       break;
     }
+  if (const char *v = getenv("MQ_BRICK_CHUNKS")) {  // experiments: fixed i-chunk count
+    const int c = atoi(v);
+    if (c >= 1 && c <= nx) chunks = c;
+  }
   g.chunks = chunks;
   g.nbricks = tiles * chunks;
   return g;
@@ -1018,14 +1200,14 @@ static BrickGeo make_geo(int nx, int ny, int nz, int resident) {
 // stores of K1 throttle (ncu stall_lg 0.61 -> 1.53 per issue) and an iteration
 // at 128^3 takes 104 instead of 94 us; left to the driver the carveout
 // sometimes fits only one CTA per SM (118 us).  MQ_PCG_CARVEOUT overrides.
-static cudaError_t two_cta_carveout(const void *fn) {
+static cudaError_t two_cta_carveout(const void *fn, int want = 2) {
   int pct = 100;
   for (int c = 50; c <= 100; ++c) {
     int per2 = 0;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, c);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, fn, kBlock, kTmaSmem);
     if (e != cudaSuccess) return e;
-    if (per2 >= 2) { pct = c; break; }
+    if (per2 >= want) { pct = c; break; }
   }
   if (const char *v = getenv("MQ_PCG_CARVEOUT")) pct = atoi(v);
   if (getenv("MQ_PCG_VERBOSE")) fprintf(stderr, "TMA kernel carveout preference %d %%\n", pct);
@@ -1040,7 +1222,7 @@ int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int sm_cap, int *grid,
   if (sm_cap > 0 && sm_cap < sms) sms = sm_cap;
   MQ_CUDA(cudaFuncSetAttribute(pcg_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
   MQ_CUDA(cudaFuncSetAttribute(kn_apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
-  MQ_CUDA(two_cta_carveout((const void *)pcg_tma_kernel));
+  MQ_CUDA(two_cta_carveout((const void *)pcg_tma_kernel, MQ_TMA_MINB));
   MQ_CUDA(two_cta_carveout((const void *)kn_apply_tma_kernel));
   MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pcg_tma_kernel, kBlock, kTmaSmem));
   if (getenv("MQ_PCG_VERBOSE")) fprintf(stderr, "pcg_tma_kernel: %d CTAs per SM, %zu B smem\n", per, kTmaSmem);

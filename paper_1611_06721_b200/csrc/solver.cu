@@ -2740,3 +2740,76 @@ int mq_pcg_collect(mq_ctx *ctx, double *ms, int32_t *n_events) {
 }  // extern "C"
 
 #include "solver_slab.cuh"
+
+// ---- guard check (memory-safety evidence without compute-sanitizer) ------
+// Every device vector of a context holds exact zeros off the partition
+// (boundary, conducting, guard and padding entries): the stencils read them as
+// boundary values, so a stray write there changes results.  This counts the
+// off-partition entries that are not 0 in every vector the context owns.
+// Slab contexts: the ghost planes (neighbour values) are skipped.
+namespace mq {
+__global__ void k_guard(Lay L, const uint32_t *__restrict__ mask, const double *__restrict__ v, int64_t skip_lo,
+                        int64_t skip_hi, unsigned long long *bad) {
+  unsigned long long n = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L.total; e += (int64_t)gridDim.x * blockDim.x) {
+    if ((mask[e >> 5] >> (e & 31)) & 1u) continue;
+    const int64_t rel = e % L.C;  // position inside the component box
+    if (rel < skip_lo || rel >= skip_hi) continue;
+    if (v[e] != 0.0) ++n;
+  }
+  if (n) atomicAdd(bad, n);
+}
+}  // namespace mq
+
+extern "C" int mq_guard_check(mq_ctx *ctx, int64_t *bad_entries, int32_t *bad_vectors, int32_t *checked) {
+  if (!ctx || !bad_entries || !bad_vectors) { set_error("NULL argument"); return MQ_INVALID; }
+  MQ_CUDA(cudaSetDevice(ctx->device));
+  std::vector<const double *> vs = {ctx->d_r, ctx->d_p0, ctx->d_p1, ctx->d_ap, ctx->d_ap2};
+  for (double *p : ctx->vecs) vs.push_back(p);
+  if (SolverHost *s = ctx->solver) {
+    for (int f = 0; f < 3; ++f) {
+      for (double *p : s->h_U[f]) vs.push_back(p);
+      for (double *p : s->h_KU[f]) vs.push_back(p);
+      for (double *p : s->h_X[f]) vs.push_back(p);
+      vs.push_back(s->last[f]);
+    }
+    for (double *p : s->h_B) vs.push_back(p);
+    for (double *p : s->h_KB) vs.push_back(p);
+    for (double *p : {s->w1, s->w2, s->w1b, s->w2b, s->rhs_src, s->rhs_cpl, s->y_src, s->y_cpl, s->y_cur})
+      vs.push_back(p);
+  }
+  if (SlabStepHost *s = ctx->sstep) {
+    for (int f = 0; f < 3; ++f) {
+      for (double *p : s->h_U[f]) vs.push_back(p);
+      for (double *p : s->h_KU[f]) vs.push_back(p);
+      vs.push_back(s->last[f]);
+    }
+    for (double *p : {s->rhs_src, s->rhs_cpl, s->y_src, s->y_cpl, s->y_cur, s->w1, s->w2, s->dvec}) vs.push_back(p);
+  }
+  const Lay &L = ctx->topo.L;
+  // slab: owned planes are padded planes 1..n of each component box
+  const bool slab = ctx->slab_hi > ctx->slab_lo;
+  const int64_t lo = slab ? L.Si : 0, hi = slab ? (int64_t)(ctx->topo.nx + 1) * L.Si : L.C;
+  unsigned long long *d_bad = nullptr;
+  MQ_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
+  int64_t total = 0;
+  int nbad = 0, n = 0;
+  for (const double *v : vs) {
+    if (!v) continue;
+    ++n;
+    cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), ctx->stream);
+    k_guard<<<ctx->sms * 4, 256, 0, ctx->stream>>>(L, ctx->d_mask, v, lo, hi, d_bad);
+    unsigned long long h = 0;
+    cudaMemcpyAsync(&h, d_bad, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) { cudaFree(d_bad); return cuda_fail(e, "guard check"); }
+    total += (int64_t)h;
+    nbad += h ? 1 : 0;
+  }
+  cudaFree(d_bad);
+  *bad_entries = total;
+  *bad_vectors = nbad;
+  if (checked) *checked = n;
+  return MQ_OK;
+}
+

@@ -33,7 +33,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import check, dptr
-from .krylov import JacobiPreconditioner, PcgConfig, SolveReport
+from .krylov import JacobiPreconditioner, PcgConfig, Preconditioner, SolveReport
 from .startvec import RhsFamily
 
 
@@ -108,6 +108,7 @@ class CsrSystem:
     pattern: np.ndarray
     waveform: Callable[[float], float]
     manifest: dict = field(default_factory=dict)
+    builtin: object = None   # Problem rebuilt from the manifest's "builtin" section (FIT grid)
 
     @property
     def n_c(self) -> int:
@@ -138,10 +139,16 @@ def _require(d, key, where):
 
 
 def load_manifest(path) -> CsrSystem:
-    """bench.py:228-313 for the stored blocks (a frozen-linear system).  A
-    manifest's ``builtin`` section (the reference rebuilds its FIT model from
-    it) is kept in ``manifest``; FIT grids run on the stencil path
-    (``Problem.from_reference_model``)."""
+    """bench.py:228-313 for the stored blocks (a frozen-linear system).
+
+    A ``builtin`` section (bench.py:283-306: the reference rebuilds its FIT
+    model from it and refuses stored blocks that disagree) rebuilds the model
+    as a :class:`~paper_1611_06721_b200.device.Problem` in ``system.builtin``
+    (configs.builtin_problem) — the stencil path, which also carries the
+    Brauer nonlinearity — and checks the stored source pattern against it
+    here; the stored matrix blocks are checked against the rebuilt model on
+    the device when a :class:`CsrSchurOperator` is made (verify_builtin),
+    which also refuses to step a nonlinear builtin model as frozen-linear."""
     path = Path(path)
     mpath = path / "manifest.json" if path.is_dir() else path
     if not mpath.exists():
@@ -176,8 +183,59 @@ def load_manifest(path) -> CsrSystem:
         raise ConfigError(f"unknown waveform kind {kind!r}")
     system = CsrSystem(mc=loaded["m_c"], kc=loaded["k_c"], kcn=loaded["k_cn"], kn=loaded["k_n"],
                        pattern=loaded["source_pattern"], waveform=waveform, manifest=manifest)
+    builtin = manifest.get("builtin")
+    if builtin:
+        from .configs import builtin_problem
+        try:
+            prob = builtin_problem(cells=int(builtin["cells"]), h=float(builtin["h"]),
+                                   kappa=float(builtin["kappa"]), brauer=tuple(builtin["brauer"]),
+                                   amps=float(builtin["amps"]), tau=float(builtin["tau"]),
+                                   linear=bool(builtin["linear"]))
+        except (KeyError, TypeError, ValueError) as err:
+            raise ConfigError(f"builtin section cannot be rebuilt: {err}")
+        if prob.pattern.shape != system.pattern.shape or not np.array_equal(prob.pattern, system.pattern):
+            raise ConfigError("stored source pattern disagrees with the builtin parameters in the manifest")
+        system.builtin = prob
+        system.waveform = prob.waveform
     system.validate()
     return system
+
+
+def is_diagonal(m) -> bool:
+    """CsrMatrix.is_diagonal (sparse.py:166-173)."""
+    c = _csr_arrays(m)
+    if c.shape[0] != c.shape[1]:
+        return False
+    counts = np.diff(c.indptr)
+    if (counts > 1).any():
+        return False
+    rows = np.repeat(np.arange(c.shape[0]), counts)
+    return bool((c.indices == rows).all())
+
+
+def verify_builtin(system: CsrSystem, device: int = 0, seed: int = 0) -> None:
+    """bench.py:291-306 on the device: the stored M_c, K_c(0), K_cn and K_n
+    must be the rebuilt builtin model's blocks.  Compared through their
+    products with random vectors, which the device forms in the reference's
+    summation order (bit-exact), so any stored entry that differs shows."""
+    from .device import DeviceGrid
+    prob = system.builtin
+    if prob is None:
+        return
+    rng = np.random.default_rng(seed)
+    with DeviceGrid(prob, device) as g:
+        if (g.n_c, g.n_n) != (system.n_c, system.n_n):
+            raise ConfigError("stored block 'k_cn' disagrees with the builtin parameters in the manifest")
+        xn = rng.standard_normal(g.n_n)
+        xc = rng.standard_normal(g.n_c)
+        checks = (("m_c", is_diagonal(system.mc) and np.array_equal(system.mc.diagonal(), g.mc_diag())),
+                  ("k_c", np.array_equal(system.kc @ xc, g.kc_apply(np.zeros(g.n_c), xc))),
+                  ("k_cn", np.array_equal(system.kcn @ xn, g.kcn_apply(xn))
+                   and np.array_equal(system.kcn.T @ xc, g.kcn_t_apply(xc))),
+                  ("k_n", np.array_equal(system.kn @ xn, g.kn_apply(xn))))
+        for name, ok in checks:
+            if not ok:
+                raise ConfigError(f"stored block {name!r} disagrees with the builtin parameters in the manifest")
 
 
 class CsrOperator:
@@ -302,15 +360,32 @@ class CsrSchurOperator:
     K_cn^T and K_c resident on the device."""
 
     def __init__(self, system: CsrSystem, pcg: PcgConfig | None = None, strategy="previous",
-                 device: int = 0):
+                 device: int = 0, preconditioner=Preconditioner.JACOBI):
         system.validate()
+        if system.builtin is not None:
+            verify_builtin(system, device)
+            if not system.builtin.meta.get("linear", False):
+                raise ConfigError("the manifest's builtin model is nonlinear (Brauer K_c); its blocks hold K_c "
+                                  "at the zero state only: step it on the stencil path, "
+                                  "SchurOperator(system.builtin)")
+        pre = Preconditioner(preconditioner)
+        if pre is Preconditioner.IC0:
+            raise NotImplementedError("IC(0) is not part of the device path (the reference falls back to "
+                                      "Jacobi when it breaks down on the singular block)")
+        self.use_jacobi = pre is Preconditioner.JACOBI   # schur.py:193-197
         self.system = system
         self.pcg = pcg or PcgConfig()
         self.kn = CsrOperator(system.kn, device)
         self.kcn = CsrOperator(system.kcn, device, jacobi=False)
         self.kcn_t = CsrOperator(system.kcn.T, device, jacobi=False)
         self.kc = CsrOperator(system.kc, device, jacobi=False)
-        self.minv_diag = 1.0 / system.mc.diagonal()          # schur.py:212
+        # schur.py:210-218: 1/diag for a diagonal M_c, else a Jacobi-PCG mass solve
+        if is_diagonal(system.mc):
+            self.minv_diag = 1.0 / system.mc.diagonal()
+            self.mc = None
+        else:
+            self.minv_diag = None
+            self.mc = CsrOperator(system.mc, device)
         n = system.n_n
         if isinstance(strategy, str):
             s = strategy.lower()
@@ -327,7 +402,7 @@ class CsrSchurOperator:
     def solve_kn(self, rhs, family: RhsFamily):
         """schur.py:239-264."""
         x0 = self.strategy.start_vector(family, rhs)
-        y, rep = self.kn.solve(rhs, x0=x0, config=self.pcg)
+        y, rep = self.kn.solve(rhs, x0=x0, config=self.pcg, use_jacobi=self.use_jacobi)
         if not rep.converged:
             raise StepFailureError(f"K_n solve ({family.value}) did not converge: "
                                    f"rel. residual {rep.final_rel_residual:.3e}")
@@ -340,8 +415,17 @@ class CsrSchurOperator:
         """schur.py:266-278."""
         return self.solve_kn(self.system.pattern * float(self.system.waveform(t)), RhsFamily.SOURCE_CURRENT)
 
+    def minv(self, x) -> np.ndarray:
+        """schur.py:280-287."""
+        if self.minv_diag is not None:
+            return self.minv_diag * x
+        y, rep = self.mc.solve(np.ascontiguousarray(x, dtype=np.float64), config=self.pcg, use_jacobi=True)
+        if not rep.converged:
+            raise StepFailureError("conductivity mass solve stalled")
+        return y
+
     def close(self):
-        for op in (self.kn, self.kcn, self.kcn_t, self.kc):
+        for op in (self.kn, self.kcn, self.kcn_t, self.kc) + ((self.mc,) if self.mc is not None else ()):
             op.close()
 
 
@@ -355,7 +439,7 @@ def explicit_euler_step(state, dt: float, op: CsrSchurOperator, step_index: int 
     y_src, r1 = op.source_solution(t_new)
     y_cpl, r2 = op.solve_kn(op.kcn_t(a_c), RhsFamily.COUPLING_FROM_PREVIOUS_STATE)
     rate = op.kcn(y_cpl - y_src) - op.kc(a_c)
-    a_next = a_c + dt * (op.minv_diag * rate)
+    a_next = a_c + dt * op.minv(rate)
     if not np.isfinite(a_next).all():
         where = f" at step {step_index}" if step_index is not None else ""
         raise StepFailureError(f"non-finite conducting state{where} (t = {t_new:.6e})")

@@ -78,3 +78,22 @@ def test_load_manifest_rejects(tmp_path, case):
         scipy.io.mmwrite(str(f), k, symmetry="general")
     with pytest.raises(ConfigError):
         load_manifest(d)
+
+
+def test_builtin_section_rebuilds_and_checks_pattern(tmp_path):
+    """bench.py:283-306 on the host side: the builtin section rebuilds the
+    model (configs.builtin_problem, model.py:582-622) and a stored pattern
+    that disagrees with it is refused."""
+    from paper_1611_06721_b200.csrsys import ConfigError, is_diagonal, load_manifest
+    d, mf = _copy(tmp_path / "a")
+    mf["builtin"] = {"cells": 6, "h": 5e-3, "kappa": 5e6, "brauer": [49.4, 1.46, 520.6], "amps": 50000.0,
+                     "tau": 0.5, "linear": False}
+    (d / "manifest.json").write_text(json.dumps(mf))
+    s = load_manifest(d)
+    assert s.builtin is not None and s.builtin.material.shape == (6, 6, 6)
+    assert np.array_equal(s.builtin.pattern, s.pattern)
+    assert is_diagonal(s.mc)
+    mf["builtin"]["amps"] = 40000.0
+    (d / "manifest.json").write_text(json.dumps(mf))
+    with pytest.raises(ConfigError, match="pattern"):
+        load_manifest(d)

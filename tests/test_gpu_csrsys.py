@@ -125,3 +125,64 @@ def test_csr_strategy_object(gpu_ok):
     assert op.solve_iterations[RhsFamily.SOURCE_CURRENT][-1] <= 1
     assert cspe.basis_size() > 0
     op.close()
+
+
+def _with_builtin(tmp_path, **over):
+    import json
+    import shutil
+    d = tmp_path / "m"
+    shutil.copytree(GOLD / "manifest_c6", d)
+    mf = json.loads((d / "manifest.json").read_text())
+    mf["builtin"] = {"cells": 6, "h": 5e-3, "kappa": 5e6, "brauer": [49.4, 1.46, 520.6], "amps": 50000.0,
+                     "tau": 0.5, "linear": False, "probe_cells": None, **over}
+    (d / "manifest.json").write_text(json.dumps(mf))
+    return d
+
+
+def test_builtin_manifest_blocks_checked_on_device(gpu_ok, tmp_path):
+    """bench.py:283-306: a manifest's builtin section rebuilds the FIT model;
+    stored blocks that disagree are refused, and the nonlinear model is not
+    stepped as frozen-linear (its stencil-path Problem is system.builtin)."""
+    import scipy.io
+    from paper_1611_06721_b200.csrsys import ConfigError, CsrSchurOperator, load_manifest, verify_builtin
+    s = load_manifest(_with_builtin(tmp_path / "a"))
+    verify_builtin(s)                                    # the stored blocks are builtin_model(6)'s
+    with pytest.raises(ConfigError, match="nonlinear"):
+        CsrSchurOperator(s)
+    op = CsrSchurOperator(load_manifest(_with_builtin(tmp_path / "b", linear=True)))  # K_c(0) is the linear K_c
+    op.close()
+    d = _with_builtin(tmp_path / "c", linear=True)
+    kn = scipy.io.mmread(str(d / "k_n.mtx")).tocsr()
+    kn.data[0] *= 1.0 + 1e-12
+    scipy.io.mmwrite(str(d / "k_n.mtx"), kn, symmetry="general")
+    with pytest.raises(ConfigError, match="'k_n'"):
+        CsrSchurOperator(load_manifest(d))
+
+
+def test_consistent_mass_solve(gpu_ok):
+    """A non-diagonal M_c takes the reference's Jacobi-PCG mass solve
+    (schur.py:210-218, 280-287) instead of 1/diag."""
+    from paper_1611_06721_b200 import PcgConfig
+    from paper_1611_06721_b200.csrsys import CsrSchurOperator, CsrSystem, explicit_euler_step
+    base = fixture_system()
+    d = base.mc.diagonal()
+    off = 0.1 * np.minimum(d[:-1], d[1:])
+    mc = sp.diags([off, d, off], [-1, 0, 1]).tocsr()
+    s = CsrSystem(mc=mc, kc=base.kc, kcn=base.kcn, kn=base.kn, pattern=base.pattern, waveform=base.waveform)
+    op = CsrSchurOperator(s, pcg=PcgConfig(rel_tol=1e-10), strategy="zero")
+    try:
+        assert op.minv_diag is None
+        rng = np.random.default_rng(2)
+        a = rng.standard_normal(s.n_c) * 1e-3
+        inv_kn = O.jacobi_inverse(s.kn.diagonal())
+        dt = 2e-4
+        y_src = O.pcg(lambda v: s.kn @ v, s.pattern * s.waveform(dt), rel_tol=1e-10, inv_diag=inv_kn).x
+        y_cpl = O.pcg(lambda v: s.kn @ v, s.kcn.T @ a, rel_tol=1e-10, inv_diag=inv_kn).x
+        rate = s.kcn @ (y_cpl - y_src) - s.kc @ a
+        ref = a + dt * O.pcg(lambda v: mc @ v, rate, rel_tol=1e-10, inv_diag=O.jacobi_inverse(d)).x
+        got, _ = explicit_euler_step((a, 0.0), dt, op)
+        assert rel(got, ref) <= 1e-9
+        # 1/diag would be visibly different
+        assert rel(a + dt * rate / d, ref) > 1e-6
+    finally:
+        op.close()

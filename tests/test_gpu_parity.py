@@ -1089,3 +1089,45 @@ def test_concurrent_members_match_sequential(gpu_ok):
         assert abs(r.final_norm_a_c - ref.final_norm_a_c) <= REL_FIELD * ref.final_norm_a_c
         for fam, v in ref.iterations.items():
             assert abs(r.iterations[fam] - v) <= 2 * steps + 1, (fam, r.iterations, ref.iterations)
+
+
+def _guard(lib, ctx):
+    import ctypes
+    bad, nv, chk = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32()
+    from paper_1611_06721_b200._lib import check
+    check(lib.mq_guard_check(ctx, ctypes.byref(bad), ctypes.byref(nv), ctypes.byref(chk)))
+    return bad.value, nv.value, chk.value
+
+
+@pytest.mark.parametrize("index,strategy,steps", [(0, "cspe", 20), (0, "pod", 20), (0, "previous", 10),
+                                                  (1, "cspe", 4), (1, "pod", 4), (2, "pod", 2)])
+def test_guard_entries_stay_zero(gpu_ok, index, strategy, steps):
+    """Memory-safety evidence in place of compute-sanitizer (closed on this
+    pool): after a run, every off-partition entry of every device vector of
+    the context (PCG scratch, CSPE / POD caches, work vectors) is still 0 —
+    the stencils read them as boundary values, so a stray or out-of-range
+    write into the padded layout would show here (and in the results)."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, SchurOperator, run_explicit
+    spec = C.config_spec(index)
+    op = SchurOperator(C.make_problem(index), pcg=PcgConfig(rel_tol=1e-8), strategy=strategy, max_cols=5,
+                       n_pod=20 if index < 2 else 30)
+    run_explicit(op.problem, t_end=steps * spec.dt, dt=spec.dt, output_period=spec.dt * (1 - 1e-3), op=op)
+    bad, nv, chk = _guard(op.lib, op.grid.ctx)
+    assert chk > 10 and bad == 0, (bad, nv, chk)
+    op.grid.close()
+
+
+def test_guard_entries_stay_zero_on_slabs(gpu_ok):
+    """The same on the slabs of the sharded step (ghost planes excepted)."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200.slabstep import SlabStepper, run_explicit_sharded
+    spec = C.config_spec(0)
+    st = SlabStepper(C.make_problem(0), 3, strategy="cspe", max_cols=5)
+    try:
+        run_explicit_sharded(st.problem, 8, spec.dt, world=3, stepper=st)
+        for s in st.slabs:
+            bad, nv, chk = _guard(s.lib, s.ctx)
+            assert chk >= 5 and bad == 0, (bad, nv, chk)
+    finally:
+        st.close()
