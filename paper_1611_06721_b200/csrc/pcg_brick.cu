@@ -50,7 +50,7 @@ constexpr int BOXP = 352;                      // box slot padded to a 128-byte 
 // K1 stages of * p_new (the off-diagonal product of every staged value,
 // formed once) instead of p_new: stencil3s, bit-identical rows
 #ifndef MQ_PRESCALE
-#define MQ_PRESCALE 0
+#define MQ_PRESCALE 1
 #endif
 constexpr int NA = MQ_NAHEAD;                  // planes in flight ahead of i+1
 constexpr int NR = NA + 3 + MQ_MARCH2, NP = NA;  // r-ring and p-ring slots

@@ -213,11 +213,17 @@ def is_diagonal(m) -> bool:
     return bool((c.indices == rows).all())
 
 
+def _close(a, b, tol) -> bool:
+    nb = float(np.linalg.norm(b))
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b))) <= tol * (nb if nb > 0 else 1.0)
+
+
 def verify_builtin(system: CsrSystem, device: int = 0, seed: int = 0) -> None:
     """bench.py:291-306 on the device: the stored M_c, K_c(0), K_cn and K_n
     must be the rebuilt builtin model's blocks.  Compared through their
     products with random vectors, which the device forms in the reference's
-    summation order (bit-exact), so any stored entry that differs shows."""
+    summation order (bit-exact for M_c, K_cn, K_cn^T, K_n; K_c to 1e-12, see
+    below), so any stored entry that differs shows."""
     from .device import DeviceGrid
     prob = system.builtin
     if prob is None:
@@ -229,7 +235,10 @@ def verify_builtin(system: CsrSystem, device: int = 0, seed: int = 0) -> None:
         xn = rng.standard_normal(g.n_n)
         xc = rng.standard_normal(g.n_c)
         checks = (("m_c", is_diagonal(system.mc) and np.array_equal(system.mc.diagonal(), g.mc_diag())),
-                  ("k_c", np.array_equal(system.kc @ xc, g.kc_apply(np.zeros(g.n_c), xc))),
+                  # the device forms K_c x as the reference's kc_apply closure
+                  # (C^T diag(w/h) C x, model.py:507-509), not as the assembled
+                  # matrix's rows: equal to rounding, not bitwise
+                  ("k_c", _close(system.kc @ xc, g.kc_apply(np.zeros(g.n_c), xc), 1e-12)),
                   ("k_cn", np.array_equal(system.kcn @ xn, g.kcn_apply(xn))
                    and np.array_equal(system.kcn.T @ xc, g.kcn_t_apply(xc))),
                   ("k_n", np.array_equal(system.kn @ xn, g.kn_apply(xn))))

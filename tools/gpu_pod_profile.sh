@@ -7,8 +7,8 @@ NCU=/usr/local/cuda/bin/ncu
 python tools/ts_profile.py --config 2 --strategy pod --steps 25 > gpurun_out/pod/run.log 2>&1
 timeout 1200 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/pod/launches.csv \
   python tools/ts_profile.py --config 2 --strategy pod --steps 25 > gpurun_out/pod/ncu_launch.log 2>&1
-KN='regex:k_(comb|pod_push|pod_galerkin|pod_basis|spmv_multi|pod_eig|pod_solve)'
+KN='regex:k_(comb|pod_|spmv_multi)'
 MET=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,launch__grid_size,launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active
-timeout 1200 $NCU --kernel-name "$KN" -s 560 -c 140 --metrics $MET --clock-control none --csv --log-file gpurun_out/pod/pod_metrics.csv \
+timeout 1200 $NCU --kernel-name "$KN" -s 800 -c 200 --metrics $MET --clock-control none --csv --log-file gpurun_out/pod/pod_metrics.csv \
   python tools/ts_profile.py --config 2 --strategy pod --steps 25 > gpurun_out/pod/ncu_pod.log 2>&1
 tail -2 gpurun_out/pod/*.log
