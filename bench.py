@@ -554,8 +554,12 @@ def cfg4_sharded(dist, world, local, hbm_peak, warmup=1, steps=2):
     spec = C.config_spec(4)
     prob = C.make_problem(4)
     t0 = time.perf_counter()
+    # MQ_BENCH_PLUMBING_TEST (every rank on cuda:0, gloo): ranks on one GPU
+    # must never run kernels that wait on one another, so the PCG is the
+    # host-driven phase loop there; on one GPU per rank the fused kernel
+    pcg = "host" if (os.environ.get("MQ_BENCH_PLUMBING_TEST") and world > 1) else "fused"
     st = SlabStepper(prob, world, dist=dist, device=local, strategy="cspe", max_cols=spec.max_cols,
-                     rel_tol=spec.rel_tol, max_iter=spec.max_iter)
+                     rel_tol=spec.rel_tol, max_iter=spec.max_iter, pcg=pcg)
     setup = time.perf_counter() - t0
     try:
         st.recover(gather=False)

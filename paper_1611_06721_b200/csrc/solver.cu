@@ -453,48 +453,65 @@ __global__ void __launch_bounds__(kBlock) k_cspe_product(Lay L, const uint32_t *
 // sigma_j in the order of k_pod_basis (l ascending from l = 0)
 constexpr int kBasisFlatMax = 8;
 
-template <int KMAX>
+template <int K>
+__device__ __forceinline__ void basis_body(int64_t npair, int m, const double2 *const *xp, double2 *const *bp,
+                                           const double *Wt, const double *sg) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npair; p += stride) {
+    double tx[K], ty[K];
+    {
+      const double2 x0 = __ldcg(xp[0] + p);
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        tx[j] = mul(x0.x, Wt[j]);
+        ty[j] = mul(x0.y, Wt[j]);
+      }
+    }
+#pragma unroll 6
+    for (int l = 1; l < m; ++l) {
+      const double2 xv = __ldcg(xp[l] + p);
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        tx[j] = add(tx[j], mul(xv.x, Wt[l * kBasisFlatMax + j]));
+        ty[j] = add(ty[j], mul(xv.y, Wt[l * kBasisFlatMax + j]));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) bp[j][p] = make_double2(tx[j] / sg[j], ty[j] / sg[j]);
+  }
+}
+
+// POD basis for podk <= 8 as one flat 16-byte pass (snapshots are 0 off the
+// partition, so B is too): B_j = (sum_l X_{order[l]} W[l][j]) / sigma_j in
+// the order of k_pod_basis (l ascending from l = 0); the body is instantiated
+// for the exact k (the FP64 work per loaded value is k multiply-adds)
 __global__ void __launch_bounds__(kBlock) k_pod_basis_flat(int64_t npair, FamDev *f, double *const *Xtab,
                                                            double *const *Btab) {
   __shared__ const double2 *xp[MAXS];
-  __shared__ double2 *bp[KMAX];
-  __shared__ double Wt[MAXS * KMAX];
-  __shared__ double sg[KMAX];
+  __shared__ double2 *bp[kBasisFlatMax];
+  __shared__ double Wt[MAXS * kBasisFlatMax];
+  __shared__ double sg[kBasisFlatMax];
   const int m = f->k, kk = f->podk;
-  if (kk == 0 || kk > KMAX) return;
+  if (kk == 0 || kk > kBasisFlatMax) return;
   if (threadIdx.x < m) xp[threadIdx.x] = reinterpret_cast<const double2 *>(Xtab[f->order[threadIdx.x]]);
   if (threadIdx.x < kk) {
     bp[threadIdx.x] = reinterpret_cast<double2 *>(Btab[threadIdx.x]);
     sg[threadIdx.x] = f->pod_sigma[threadIdx.x];
   }
-  for (int q = threadIdx.x; q < MAXS * KMAX; q += blockDim.x) {
-    const int l = q / KMAX, j = q % KMAX;
-    Wt[q] = (l < MAXS && j < MAXS) ? f->W[l * MAXS + j] : 0.0;
+  for (int q = threadIdx.x; q < MAXS * kBasisFlatMax; q += blockDim.x) {
+    const int l = q / kBasisFlatMax, j = q % kBasisFlatMax;
+    Wt[q] = f->W[l * MAXS + j];
   }
   __syncthreads();
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npair; p += stride) {
-    double tx[KMAX], ty[KMAX];
-    {
-      const double2 x0 = __ldcg(xp[0] + p);
-#pragma unroll
-      for (int j = 0; j < KMAX; ++j) {
-        tx[j] = mul(x0.x, Wt[j]);
-        ty[j] = mul(x0.y, Wt[j]);
-      }
-    }
-#pragma unroll 4
-    for (int l = 1; l < m; ++l) {
-      const double2 xv = __ldcg(xp[l] + p);
-#pragma unroll
-      for (int j = 0; j < KMAX; ++j) {
-        tx[j] = add(tx[j], mul(xv.x, Wt[l * KMAX + j]));
-        ty[j] = add(ty[j], mul(xv.y, Wt[l * KMAX + j]));
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j)
-      if (j < kk) bp[j][p] = make_double2(tx[j] / sg[j], ty[j] / sg[j]);
+  switch (kk) {
+    case 1: basis_body<1>(npair, m, xp, bp, Wt, sg); break;
+    case 2: basis_body<2>(npair, m, xp, bp, Wt, sg); break;
+    case 3: basis_body<3>(npair, m, xp, bp, Wt, sg); break;
+    case 4: basis_body<4>(npair, m, xp, bp, Wt, sg); break;
+    case 5: basis_body<5>(npair, m, xp, bp, Wt, sg); break;
+    case 6: basis_body<6>(npair, m, xp, bp, Wt, sg); break;
+    case 7: basis_body<7>(npair, m, xp, bp, Wt, sg); break;
+    default: basis_body<8>(npair, m, xp, bp, Wt, sg); break;
   }
 }
 
@@ -1450,7 +1467,7 @@ static int start_vector(mq_ctx *ctx, int fam, const double *rhs, double *x0) {
     case MQ_STRAT_POD: {
       k_pod_eig<<<1, 256, 0, st>>>(f, s->cfg.eps_pod);
       LAUNCH_CHECK();
-      k_pod_basis_flat<kBasisFlatMax><<<G, kBlock, 0, st>>>(L.total / 2, f, s->d_X[fam], s->d_B);
+      k_pod_basis_flat<<<G, kBlock, 0, st>>>(L.total / 2, f, s->d_X[fam], s->d_B);
       LAUNCH_CHECK();
       k_pod_basis<<<stream_grid(ctx), kBlock, 0, st>>>(L, ctx->d_mask, f, s->d_X[fam], s->d_B);
       LAUNCH_CHECK();

@@ -12,3 +12,5 @@ MET=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_byt
 timeout 1200 $NCU --kernel-name "$KN" -s 800 -c 200 --metrics $MET --clock-control none --csv --log-file gpurun_out/pod/pod_metrics.csv \
   python tools/ts_profile.py --config 2 --strategy pod --steps 25 > gpurun_out/pod/ncu_pod.log 2>&1
 tail -2 gpurun_out/pod/*.log
+timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/pod/bench_launches.csv \
+  python bench.py --steps 3 --warmup 3 --skip-secondary --skip-cpu --skip-cfg4 > gpurun_out/pod/ncu_bench.log 2>&1
