@@ -153,6 +153,16 @@ int mq_pcg_solve_host(mq_ctx *ctx, const double *b, const double *x0, double *x,
                       double rel_tol, double abs_tol, int32_t max_iter,
                       int32_t use_jacobi, mq_solve_report *rep);
 
+/* ---- member-batched PCG on K_n (BASELINE configs[3]) --------
+ * nb = 1, 2, 4 or 8 right-hand sides of the same K_n solved in one launch
+ * (krylov.py:174-250 per member, per-member alpha / beta / stopping test; a
+ * converged member is frozen).  b, x0 (may be NULL), x: host, member-major
+ * (member m's compact vector at offset m * n_n); reports: nb records;
+ * kernel_ms (optional): the launch's device time. */
+int mq_pcg_solve_batched_host(mq_ctx *ctx, int32_t nb, const double *b, const double *x0, double *x,
+                              double rel_tol, double abs_tol, int32_t max_iter, int32_t use_jacobi,
+                              mq_solve_report *reports, double *kernel_ms);
+
 /* ---- PCG on a general CSR operator (krylov.py:161-250) ------------------
  * int32 column indices, int64 row pointers; inv_diag NULL = no
  * preconditioner.  All pointers are HOST; the solve runs on `device`. */

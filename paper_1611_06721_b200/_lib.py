@@ -158,6 +158,8 @@ SIGNATURES = {
     "mq_slab_ipc_import": (I32, [VP, I32, I32, VP, c_int32_p, VP]),
     "mq_slab_fused_solve_peer": (I32, [VP, VP, I32, D, D, I32, I32, ctypes.POINTER(SolveReportC)]),
     "mq_guard_check": (I32, [VP, c_int64_p, c_int32_p, c_int32_p]),
+    "mq_pcg_solve_batched_host": (I32, [VP, I32, c_double_p, c_double_p, c_double_p, D, D, I32, I32,
+                                       ctypes.POINTER(SolveReportC), c_double_p]),
     "mq_ss_init": (I32, [VP, ctypes.POINTER(SolverCfg), c_double_p]),
     "mq_ss_info": (I32, [VP, c_int64_p]),
     "mq_ss_owned": (I32, [VP, c_int64_p]),

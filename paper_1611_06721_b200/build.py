@@ -11,7 +11,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libmq_b200.so"
-SOURCES = ["capi.cu", "csr_op.cu", "pcg.cu", "pcg_brick.cu", "pcg_resident.cu", "slab.cu", "slab_fused.cu", "solver.cu", "topology.cpp"]
+SOURCES = ["capi.cu", "csr_op.cu", "pcg.cu", "pcg_batched.cu", "pcg_brick.cu", "pcg_resident.cu", "slab.cu", "slab_fused.cu", "solver.cu", "topology.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -188,6 +188,25 @@ class DeviceGrid:
         check(self.lib.mq_kcn_apply_host(self.ctx, dptr(v), dptr(y)))
         return y
 
+    def pcg_batched(self, b, x0=None, *, rel_tol=1e-8, abs_tol=0.0, max_iter=5000, jacobi=True):
+        """nb right-hand sides (rows of ``b``, nb in 1, 2, 4, 8) of K_n in one
+        member-batched launch (``mq_pcg_solve_batched_host``); returns
+        (x rows, [(iterations, converged, final_rel_residual, applies)], kernel ms)."""
+        b = np.ascontiguousarray(np.atleast_2d(b), dtype=np.float64)
+        nb = b.shape[0]
+        if b.shape[1] != self.n_n:
+            raise ValueError("rhs rows must have length n_n")
+        x0v = None if x0 is None else np.ascontiguousarray(np.atleast_2d(x0), dtype=np.float64)
+        x = np.empty_like(b)
+        reps = (_lib.SolveReportC * nb)()
+        ms = ctypes.c_double()
+        rc = self.lib.mq_pcg_solve_batched_host(self.ctx, nb, dptr(b), dptr(x0v) if x0v is not None else None,
+                                                 dptr(x), float(rel_tol), float(abs_tol), int(max_iter),
+                                                 int(bool(jacobi)), reps, ctypes.byref(ms))
+        check(rc, allow=(_lib.MQ_OK, _lib.MQ_NOT_CONVERGED))
+        return x, [(int(r.iterations), bool(r.converged), float(r.final_rel_residual), int(r.applies))
+                   for r in reps], float(ms.value)
+
     def kn_operator(self) -> "KnOperator":
         return KnOperator(self)
 
