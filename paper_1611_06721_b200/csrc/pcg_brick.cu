@@ -37,6 +37,9 @@ constexpr int BOXP = 352;                      // box slot padded to a 128-byte 
 #ifndef MQ_XDEFER
 #define MQ_XDEFER 1
 #endif
+#ifndef MQ_XSPLIT
+#define MQ_XSPLIT 0
+#endif
 #ifndef MQ_NAHEAD
 #define MQ_NAHEAD 3
 #endif
@@ -304,7 +307,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
                                           const CUtensorMap *mp, bool first, double beta, double alpha_prev,
                                           int xmode, double alpha_prev2, double *pnew, int i0, int i1, int j0,
                                           int k0, ROW row,
-                                          PUSH push = PUSH()) {
+                                          PUSH push = PUSH(), int xmode_odd = -1) {
   const StencilPcgArgs &a = A.a;
   const BrickGeo &g = A.g;
   const Lay &L = a.L;
@@ -317,7 +320,11 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   // x update of this pass (kK1, !first): 0 none (deferred), 1 x += a1 p_old,
   // 2 x = (x + a2 p_prev2) + a1 p_old with p_prev2 read from the p_new buffer
   // at the own position just before it is overwritten
-  const int xm = (MODE == kK1 && !first) ? xmode : 0;
+  // xmode_odd >= 0: planes of odd index take xmode_odd (MQ_XSPLIT: the
+  // two-step update alternates between the plane parities, so every K1 pass
+  // carries half of the x traffic)
+  const int xm_e = (MODE == kK1 && !first) ? xmode : 0;
+  const int xm_o = (MODE == kK1 && !first) ? (xmode_odd >= 0 ? xmode_odd : xmode) : 0;
   const uint32_t bytes = (with_p ? 6u : 3u) * HP * 8u;
   // halo (slot, component) converted by this thread besides its own
   // position: the 84 halo positions x 3 components are spread over threads
@@ -368,6 +375,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       for (int c = 0; c < 3; ++c) {
         const int64_t e = c * L.C + qb + pos_own;
         o.mw[c] = __ldg(mask + (e >> 5));
+        const int xm = (q & 1) ? xm_o : xm_e;
         if (xm >= 1) o.xo[c] = __ldcg(x + e);
         if (xm == 2) o.p2[c] = __ldcg(pnew + e);
       }
@@ -403,6 +411,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     }
     double (&Sr)[3][BOXP] = mc.sr[s].v;
     const double (&Sp)[3][BOXP] = mc.sp[pslot(q)].v;
+    const int xm = (q & 1) ? xm_o : xm_e;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double rq = Sr[c][s_own];
@@ -450,6 +459,9 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   const int last = i1;  // planes i0-1 .. i1 are needed
   OwnPre pa, pb;
   double rw[3], rw1[3], rw2[3];
+#ifdef MQ_TRACE_MARCH
+  if (mc.tr) mc.tr[128] = globaltimer_ns();  // march entry
+#endif
   for (int q = i0 - 1; q <= i0 + NA - 2 && q <= last; ++q) issue(q);
   prefetch_own(pa, i0, true);
   prefetch_own(pb, i0 - 1, false);
@@ -487,8 +499,14 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 #else
   const OwnPre c0 = pa;
   prefetch_own(pa, i0 + 1, i0 + 1 < i1);
+#ifdef MQ_TRACE_MARCH
+  if (mc.tr) mc.tr[129] = globaltimer_ns();  // planes i0-1 converted
+#endif
   uint32_t act = convert(i0, true, c0, rw);
   __syncthreads();
+#ifdef MQ_TRACE_MARCH
+  if (mc.tr) mc.tr[130] = globaltimer_ns();  // plane i0 converted (prologue done)
+#endif
   if (i0 + NA <= last) issue(i0 + NA);
   for (int i = i0; i < i1; ++i) {
     const OwnPre cur = pa;
@@ -511,6 +529,9 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   }
 #endif
   __syncthreads();
+#ifdef MQ_TRACE_MARCH
+  if (mc.tr) mc.tr[131] = globaltimer_ns();  // march done
+#endif
 }
 
 // flat 16-byte vectorised grid-stride helper over pairs of padded entries
@@ -670,11 +691,16 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __gr
       double *pnew = pold_is_a ? a.pb : a.pa;
       const CUtensorMap *mp = pold_is_a ? &A.tm_pa : &A.tm_pb;
       // ---- K1 ----
-      int xmode = 0;
+      int xmode = 0, xmode_odd = -1;
       if (!first) {
 #if MQ_XDEFER
         xmode = pend ? 2 : 0;
         pend = !pend;
+#if MQ_XSPLIT
+        // odd planes run one iteration ahead: it = 2 applies p_1 alone, then
+        // the two-step update at every even it (even planes: every odd it >= 3)
+        xmode_odd = (it & 1) ? 0 : (it == 2 ? 1 : 2);
+#endif
 #else
         xmode = 1;
 #endif
@@ -700,7 +726,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __gr
 #endif
                          st_hint(ap + e, av, pol_keep);
                          v1[0] = add(v1[0], mul(own, av));
-                       });
+                       }, NoPush(), xmode_odd);
       }
       block_sum<1>(v1, red);
       if (threadIdx.x == 0) a.partials[3 * G + blockIdx.x] = v1[0];
@@ -793,7 +819,40 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __gr
       // the pending alpha_{K-1} p_{K-1} (deferred x update), applied first
       const double *pdir2 = converged ? (pold_is_a ? a.pa : a.pb) : (pold_is_a ? a.pb : a.pa);
       const double alpha2 = converged ? alpha_prev : alpha_prev2;
-      if (pend) {
+      // pending directions per plane parity (MQ_XSPLIT): even planes as the
+      // global toggle (pend), odd planes last updated at even iterations
+      const bool pend_e = pend;
+#if MQ_XSPLIT && MQ_XDEFER
+      const bool pend_o = iters >= 3 && (iters & 1);
+#else
+      const bool pend_o = pend;
+#endif
+      if (pend_e != pend_o) {
+        // mixed: per pair, by the parity of its node plane (a pair never
+        // straddles two planes: C and Si are even)
+        flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
+          double2 xv[kUnroll], pv[kUnroll], qv[kUnroll];
+          bool two[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u)
+            if (u < n) {
+              const int64_t e = 2 * (p + u * stride);
+              const int64_t plane = (e % L.C) / L.Si - 1;
+              two[u] = (plane & 1) ? pend_o : pend_e;
+              xv[u] = __ldcg(reinterpret_cast<const double2 *>(x) + p + u * stride);
+              pv[u] = __ldcg(reinterpret_cast<const double2 *>(pdir) + p + u * stride);
+              if (two[u]) qv[u] = __ldcg(reinterpret_cast<const double2 *>(pdir2) + p + u * stride);
+            }
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u)
+            if (u < n) {
+              double2 xs = xv[u];
+              if (two[u]) xs = make_double2(add(xs.x, mul(alpha2, qv[u].x)), add(xs.y, mul(alpha2, qv[u].y)));
+              reinterpret_cast<double2 *>(x)[p + u * stride] =
+                  make_double2(add(xs.x, mul(alpha, pv[u].x)), add(xs.y, mul(alpha, pv[u].y)));
+            }
+        });
+      } else if (pend_e) {
         flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
           double2 xv[kUnroll], pv[kUnroll], qv[kUnroll];
 #pragma unroll

@@ -63,7 +63,7 @@ def main():
         # plane step i: [before TMA wait of plane i+1, after it, after the
         # convert, after the __syncthreads]; the stencil of plane i follows
         import numpy as np
-        st = np.zeros(1300 + 4 * 33, dtype=np.uint64)
+        st = np.zeros(1300 + 140, dtype=np.uint64)
         check(lib.mq_pcg_trace(g.ctx, st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), st.size))
         m = st[1300:1300 + 4 * 31].reshape(31, 4).astype(np.float64)
         wait = m[:, 1] - m[:, 0]
@@ -73,6 +73,11 @@ def main():
         print(f"  march us per plane step (CTA 0): TMA wait {wait[2:].mean()/1e3:.3f}  convert {conv[2:].mean()/1e3:.3f}  "
               f"syncthreads {sync[2:].mean()/1e3:.3f}  stencil+prefetch {sten[2:].mean()/1e3:.3f}  "
               f"step {np.diff(m[:, 0])[2:].mean()/1e3:.3f}")
+        e = st[1300 + 128:1300 + 132].astype(np.float64)
+        print(f"  march entry -> plane i0-1 converted {(e[1]-e[0])/1e3:.2f} us, -> prologue done "
+              f"{(e[2]-e[0])/1e3:.2f} us, march total {(e[3]-e[0])/1e3:.2f} us")
+        print("  first steps (us): wait " + " ".join(f"{v/1e3:.2f}" for v in wait[:6]) +
+              " | step " + " ".join(f"{v/1e3:.2f}" for v in np.diff(m[:, 0])[:6]))
     if os.environ.get("MQ_TRACE_FINE") and g.pcg_kernel()[0].startswith("pcg_resident1"):
         # single-reduction kernel: fine stamps 0..3 = loop top, stencil + dots
         # + Ap stores done, partial sums read, own + halo update done;
