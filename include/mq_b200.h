@@ -367,6 +367,8 @@ int mq_ss_euler(mq_ctx *ctx, double dt, double *owned_out);
 /* a_n = y_src - y_cur of the last recovery on the slab's dofs (schur.py:408-419) */
 int mq_ss_an(mq_ctx *ctx, double *a_n_local);
 int mq_ss_diag(mq_ctx *ctx, mq_diag *out);
+/* CSPE cache of one family on this slab (as mq_cspe_export, slab compact order) */
+int mq_ss_cspe_export(mq_ctx *ctx, int32_t family, int32_t *k, double *basis, double *products, double *galerkin);
 
 /* Guard check: count the off-partition entries (boundary, conducting, guard
  * and padding positions; a slab's ghost planes excepted) that are not 0 in

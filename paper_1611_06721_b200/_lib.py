@@ -175,6 +175,7 @@ SIGNATURES = {
     "mq_ss_euler": (I32, [VP, D, c_double_p]),
     "mq_ss_an": (I32, [VP, c_double_p]),
     "mq_ss_diag": (I32, [VP, ctypes.POINTER(Diag)]),
+    "mq_ss_cspe_export": (I32, [VP, I32, c_int32_p, c_double_p, c_double_p, c_double_p]),
     "mq_slab_fused_solve_local": (I32, [ctypes.POINTER(VP), I32, ctypes.POINTER(VP), ctypes.POINTER(VP), I32, D, D, I32, I32,
                                         ctypes.POINTER(SolveReportC)]),
     "mq_timer_start": (I32, [VP]),

@@ -154,6 +154,11 @@ int launch_pcg_csr(const CsrPcgArgs &args, int grid, cudaStream_t s);
 int pcg_csr_grid(int64_t n, int *out);
 int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int sm_cap, int *grid, BrickGeo *geo);
 int launch_pcg_brick(const StencilPcgArgs &args, const BrickGeo &geo, int grid, cudaStream_t s);
+struct KnMulti;
+int kn_multi_prepare(const Lay &L, const BrickGeo &geo, const uint32_t *mask, double dg, double of,
+                     double *const *x, double *const *y, int nvec, const int *kptr, int sms, KnMulti **out);
+int kn_multi_launch(const KnMulti *k, cudaStream_t s);
+void kn_multi_free(KnMulti *k);
 int launch_kn_apply_brick(const Lay &L, const BrickGeo &geo, const uint32_t *mask, double dg, double of,
                           const double *x, double *y, int sms, cudaStream_t s);
 int launch_pcg_ctx(mq_ctx *ctx, const StencilPcgArgs &args);

@@ -73,6 +73,7 @@ struct TmaPcgArgs {
 };
 
 constexpr size_t kTmaSmem = sizeof(Box3) * (NR + NP) + 128;
+constexpr int kMaxMultiVec = 32;  // POD basis slots (MAXS)
 
 // ---- PTX helpers ----------------------------------------------------------
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -1188,6 +1189,40 @@ __global__ void __launch_bounds__(kBlock, 2) kn_apply_tma_kernel(const __grid_co
   }
 }
 
+// K_n applied to the POD basis vectors B_j, j < *kptr (the k SpMVs of
+// pod_start_vector, startvec.py:296): blockIdx.y = j, the same TMA march as
+// kn_apply_tma_kernel with one tensor map per basis slot.
+struct KnMultiArgs {
+  TmaPcgArgs A;
+  const int *kptr;
+  double *y[kMaxMultiVec];
+  CUtensorMap tm[kMaxMultiVec];
+};
+
+__global__ void __launch_bounds__(kBlock, 2) kn_apply_tma_multi_kernel(const __grid_constant__ KnMultiArgs M) {
+  const int j = blockIdx.y;
+  if (j >= *M.kptr) return;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t bars[NR];
+  MarchCtx mc;
+  mc.sr = reinterpret_cast<Box3 *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sp = mc.sr + NR;
+  mc.bars = bars;
+  mc.ph = 0u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NR; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double *y = M.y[j];
+  for (int bi = blockIdx.x; bi < M.A.g.nbricks; bi += gridDim.x) {
+    int i0, i1, j0, k0;
+    brick_of(M.A.g, bi, i0, i1, j0, k0);
+    march_tma<kInit>(mc, M.A, &M.tm[j], nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
+                     [&](int c, int64_t e, auto V, double) { y[e] = stencil3(c, M.A.a.dg, M.A.a.of, V); });
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -1377,5 +1412,44 @@ int launch_kn_apply_brick(const Lay &L, const BrickGeo &geo, const uint32_t *mas
   MQ_CUDA(cudaGetLastError());
   return MQ_OK;
 }
+
+// prepared once per solver (tensor maps of the basis slots), launched inside
+// the captured POD start vector
+struct KnMulti {
+  KnMultiArgs M;
+  int grid = 0, nvec = 0;
+};
+
+int kn_multi_prepare(const Lay &L, const BrickGeo &geo, const uint32_t *mask, double dg, double of,
+                     double *const *x, double *const *y, int nvec, const int *kptr, int sms, KnMulti **out) {
+  if (nvec < 1 || nvec > kMaxMultiVec) { set_error("1..32 vectors per multi-SpMV"); return MQ_INVALID; }
+  KnMulti *k = new KnMulti();
+  std::memset(&k->M, 0, sizeof(k->M));
+  k->M.A.a.L = L;
+  k->M.A.a.mask = mask;
+  k->M.A.a.dg = dg;
+  k->M.A.a.of = of;
+  k->M.A.g = geo;
+  k->M.kptr = kptr;
+  for (int j = 0; j < nvec; ++j) {
+    int rc = make_vec_map(L, geo.nx, geo.ny, geo.nz, x[j], &k->M.tm[j]);
+    if (rc) { delete k; return rc; }
+    k->M.y[j] = y[j];
+  }
+  MQ_CUDA(cudaFuncSetAttribute(kn_apply_tma_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+  MQ_CUDA(two_cta_carveout((const void *)kn_apply_tma_multi_kernel));
+  k->grid = geo.nbricks < sms * 2 ? geo.nbricks : sms * 2;
+  k->nvec = nvec;
+  *out = k;
+  return MQ_OK;
+}
+
+int kn_multi_launch(const KnMulti *k, cudaStream_t s) {
+  kn_apply_tma_multi_kernel<<<dim3(k->grid, k->nvec), kBlock, kTmaSmem, s>>>(k->M);
+  MQ_CUDA(cudaGetLastError());
+  return MQ_OK;
+}
+
+void kn_multi_free(KnMulti *k) { delete k; }
 
 }  // namespace mq

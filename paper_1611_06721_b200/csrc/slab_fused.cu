@@ -317,6 +317,10 @@ int mq_slab_fused_solve_local(mq_ctx **ctxs, int32_t nranks, const double *const
   }
   // every rank's epoch must agree (they only ever run together)
   cudaStream_t st = c0->stream;
+  // the launch runs on rank 0's stream: the other ranks' streams may still
+  // hold work writing this solve's inputs (b, x0 -- the sharded step queues
+  // K_cn^T a_c and the start vector there), so they are drained first
+  for (int q = 1; q < nranks; ++q) MQ_CUDA(cudaStreamSynchronize(ctxs[q]->stream));
   if (slab_use_tma()) {
     StencilPcgArgs sa[kMaxRanks];
     int np[kMaxRanks];

@@ -105,6 +105,9 @@ struct SolverHost {
   double *d_dlog = nullptr;
   int64_t dlog_cap = 0;
   double *d_probe_out = nullptr;
+  // POD: K B_j on the TMA brick march (grids run by pcg_tma_kernel), one
+  // tensor map per basis slot per family (the k of the family's projection)
+  KnMulti *kn_multi[3] = {nullptr, nullptr, nullptr};
   // page-locked landing block of the host-facing calls: run status, the two
   // iteration counts and the probe value come back in one copy batch and one
   // stream synchronisation per call
@@ -149,6 +152,7 @@ void solver_free(mq_ctx *ctx) {
   SolverHost *s = ctx->solver;
   if (!s) return;
   solver_graph_reset(ctx);
+  for (int f = 0; f < 3; ++f) kn_multi_free(s->kn_multi[f]);
   if (s->side) cudaStreamDestroy(s->side);
   for (int q = 0; q < SolverHost::kSlots; ++q) {
     if (s->ev_fork[q]) cudaEventDestroy(s->ev_fork[q]);
@@ -1471,9 +1475,15 @@ static int start_vector(mq_ctx *ctx, int fam, const double *rhs, double *x0) {
       LAUNCH_CHECK();
       k_pod_basis<<<stream_grid(ctx), kBlock, 0, st>>>(L, ctx->d_mask, f, s->d_X[fam], s->d_B);
       LAUNCH_CHECK();
-      dim3 g2(stream_grid(ctx), s->cfg.n_pod);
-      k_spmv_multi<<<g2, kBlock, 0, st>>>(L, ctx->d_mask, ctx->kn_diag, ctx->kn_off, f, s->d_B, s->d_KB);
-      LAUNCH_CHECK();
+      if (s->kn_multi[fam]) {
+        int rc2 = kn_multi_launch(s->kn_multi[fam], st);
+        if (rc2) return rc2;
+        ctx->launches += 1;
+      } else {
+        dim3 g2(stream_grid(ctx), s->cfg.n_pod);
+        k_spmv_multi<<<g2, kBlock, 0, st>>>(L, ctx->d_mask, ctx->kn_diag, ctx->kn_off, f, s->d_B, s->d_KB);
+        LAUNCH_CHECK();
+      }
       dim3 g3(G, s->cfg.n_pod + 1);
       k_pod_galerkin_fused<<<G, kBlock, 0, st>>>(L.total / 2, f, s->d_B, s->d_KB, rhs, s->d_red, s->d_cnt + 1);
       LAUNCH_CHECK();
@@ -1921,6 +1931,13 @@ int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern)
   if (cfg->strategy == MQ_STRAT_POD) {
     table(&s->d_B, s->h_B, cfg->n_pod);
     table(&s->d_KB, s->h_KB, cfg->n_pod);
+    // K B_j through the TMA march where the TMA PCG kernel runs (128^3 and
+    // up); MQ_POD_SPMV=flat keeps the thread-per-row k_spmv_multi
+    const char *sp = getenv("MQ_POD_SPMV");
+    if (!rc && ctx->pcg_variant == 0 && !(sp && std::string(sp) == "flat"))
+      for (int fam = 0; fam < 3 && !rc; ++fam)
+        rc = kn_multi_prepare(L, ctx->geo, ctx->d_mask, ctx->kn_diag, ctx->kn_off, s->h_B.data(), s->h_KB.data(),
+                              cfg->n_pod, &s->d_fam[fam].podk, ctx->sms, &s->kn_multi[fam]);
   }
   vec(&s->w1);
   vec(&s->w2);

@@ -651,6 +651,28 @@ int mq_ss_an(mq_ctx *ctx, double *a_n_local) {
   return mq_vec_download(ctx, s->w1, a_n_local);
 }
 
+// CSPE cache of one family on this slab: k, basis / products on the slab's
+// own dofs (slab compact order, column-major n_n x k), the Galerkin matrix
+int mq_ss_cspe_export(mq_ctx *ctx, int32_t family, int32_t *k, double *basis, double *products, double *galerkin) {
+  int rc = ss_check(ctx);
+  if (rc) return rc;
+  SlabStepHost *s = ctx->sstep;
+  if (s->cfg.strategy != MQ_STRAT_CSPE || family < 0 || family > 2) { set_error("CSPE family expected"); return MQ_INVALID; }
+  FamDev f;
+  MQ_CUDA(cudaMemcpyAsync(&f, s->d_fam + family, sizeof(FamDev), cudaMemcpyDeviceToHost, ctx->stream));
+  MQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  *k = f.k;
+  const int64_t n = (int64_t)ctx->topo.nc_pad.size();
+  for (int j = 0; j < f.k; ++j) {
+    if (basis && (rc = mq_vec_download(ctx, s->h_U[family][f.order[j]], basis + j * n))) return rc;
+    if (products && (rc = mq_vec_download(ctx, s->h_KU[family][f.order[j]], products + j * n))) return rc;
+  }
+  if (galerkin)
+    for (int r = 0; r < f.k; ++r)
+      for (int c = 0; c < f.k; ++c) galerkin[r * f.k + c] = f.G[r * MAXS + c];
+  return MQ_OK;
+}
+
 int mq_ss_diag(mq_ctx *ctx, mq_diag *out) {
   int rc = ss_check(ctx);
   if (rc) return rc;

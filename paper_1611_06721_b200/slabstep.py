@@ -133,6 +133,16 @@ class SlabStepGrid(SlabGrid):
         check(self.lib.mq_ss_diag(self.ctx, ctypes.byref(d)))
         return d
 
+    def cspe_export(self, fam: int):
+        """(U, K U) on this slab's own dofs (n_n x k each) and the Galerkin matrix."""
+        k = ctypes.c_int32()
+        U = np.empty((32, self.n_n))
+        KU = np.empty((32, self.n_n))
+        G = np.empty(32 * 32)
+        check(self.lib.mq_ss_cspe_export(self.ctx, int(fam), ctypes.byref(k), dptr(U), dptr(KU), dptr(G)))
+        kk = k.value
+        return U[:kk].T.copy(), KU[:kk].T.copy(), G[:kk * kk].reshape(kk, kk).copy()
+
     def stage_b(self, which: str):
         """Copy the named rhs into this slab's PCG ``b`` (host-driven PCG)."""
         import torch

@@ -208,3 +208,25 @@ def test_sharded_step_two_processes(gpu_ok, oracle_c0_runs):
     assert np.array_equal(it0, it1) and np.array_equal(ac0, ac1) and np.array_equal(an0, an1)
     for i in range(10):
         assert rel(_field(ac0[i], an0[i]), _field(tr.a_c[i + 1], tr.a_n[i + 1])) <= REL_FIELD
+
+
+@pytest.mark.slow
+def test_sharded_step_config4_grid_matches_single_context(gpu_ok):
+    """configs[4] itself (256^3, Brauer, CSPE k = 5): the sharded step on 2
+    emulated ranks against the single-context device loop over 2 steps with
+    recovery (A-field within 1e-8 per step, every solve within +-1
+    iteration).  No oracle run exists at 256^3 (hours of CPU); the
+    single-context loop is the one pinned to the oracle at 16^3-128^3."""
+    from paper_1611_06721_b200 import configs as C
+    from paper_1611_06721_b200 import PcgConfig, run_explicit
+    from paper_1611_06721_b200.slabstep import run_explicit_sharded
+    spec = C.config_spec(4)
+    prob = C.make_problem(4)
+    n = 2
+    one = run_explicit(prob, t_end=n * spec.dt, dt=spec.dt, strategy="cspe", pcg=PcgConfig(rel_tol=1e-8),
+                       max_cols=5, output_period=spec.dt * (1 - 1e-3), record_states=True)
+    res = run_explicit_sharded(prob, n, spec.dt, world=2, strategy="cspe", max_cols=5, record_states=True)
+    for i in range(n):
+        e = rel(_field(res.a_c_history[i], res.a_n_history[i]), _field(one.a_c_history[i], one.a_n_history[i]))
+        assert e <= REL_FIELD, (i, e)
+    assert np.max(np.abs(res.step_iterations - one.step_iterations)) <= 1
