@@ -37,9 +37,6 @@ constexpr int BOXP = 352;                      // box slot padded to a 128-byte 
 #ifndef MQ_XDEFER
 #define MQ_XDEFER 1
 #endif
-#ifndef MQ_XSPLIT
-#define MQ_XSPLIT 0
-#endif
 #ifndef MQ_NAHEAD
 #define MQ_NAHEAD 3
 #endif
@@ -47,16 +44,13 @@ constexpr int BOXP = 352;                      // box slot padded to a 128-byte 
 // in place into p_new, read by the stencil) plus NA planes in flight; the
 // p_old ring only the NA in-flight planes (p_old is dead once its plane is
 // converted).  Same bytes as a 5-stage (r, p) ring, one more plane ahead.
-#ifndef MQ_MARCH2
-#define MQ_MARCH2 0
-#endif
 // K1 stages of * p_new (the off-diagonal product of every staged value,
 // formed once) instead of p_new: stencil3s, bit-identical rows
 #ifndef MQ_PRESCALE
 #define MQ_PRESCALE 1
 #endif
 constexpr int NA = MQ_NAHEAD;                  // planes in flight ahead of i+1
-constexpr int NR = NA + 3 + MQ_MARCH2, NP = NA;  // r-ring and p-ring slots
+constexpr int NR = NA + 3, NP = NA;            // r-ring and p-ring slots
 constexpr int NHALO = 2 * HK + 2 * TJ;         // 84 halo positions per plane
 static_assert(TJ * TK == kBlock, "one thread per tile position");
 static_assert(HP <= BOXP && (BOXP * 8) % 128 == 0, "TMA destination alignment");
@@ -103,61 +97,6 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, u
       "[%6];" ::"r"(su32(dst)),
       "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
       : "memory");
-}
-
-// L2 residency hints (MQ_L2HINT): r and Ap are each read twice per
-// iteration (r: K1's TMA march and K2; Ap: written by K1, read by K2), 106 MB
-// at 128^3 against a 126 MB L2.  Their loads and stores carry an evict_last
-// policy, the streams touched once per iteration (p_old, p_new, x) evict_first,
-// so that K2 and the next K1 find r and Ap in L2.
-#ifndef MQ_L2HINT
-#define MQ_L2HINT 0
-#endif
-__device__ __forceinline__ uint64_t l2_policy(bool keep) {
-  uint64_t p;
-  if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void st_hint(double *a, double v, uint64_t pol) {
-#if MQ_L2HINT
-  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
-#else
-  (void)pol;
-  *a = v;
-#endif
-}
-__device__ __forceinline__ double2 ld2_hint(const double2 *a, uint64_t pol) {
-#if MQ_L2HINT
-  double2 v;
-  asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
-  return v;
-#else
-  (void)pol;
-  return __ldcg(a);
-#endif
-}
-__device__ __forceinline__ void st2_hint(double2 *a, double2 v, uint64_t pol) {
-#if MQ_L2HINT
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y), "l"(pol)
-               : "memory");
-#else
-  (void)pol;
-  *a = v;
-#endif
-}
-__device__ __forceinline__ void tma_load_4d_hint(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
-                                                 int c2, int c3, uint64_t pol) {
-#if MQ_L2HINT
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
-      "[%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(su32(dst)),
-      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar)), "l"(pol)
-      : "memory");
-#else
-  (void)pol;
-  tma_load_4d(dst, map, bar, c0, c1, c2, c3);
-#endif
 }
 
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
@@ -308,7 +247,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
                                           const CUtensorMap *mp, bool first, double beta, double alpha_prev,
                                           int xmode, double alpha_prev2, double *pnew, int i0, int i1, int j0,
                                           int k0, ROW row,
-                                          PUSH push = PUSH(), int xmode_odd = -1) {
+                                          PUSH push = PUSH()) {
   const StencilPcgArgs &a = A.a;
   const BrickGeo &g = A.g;
   const Lay &L = a.L;
@@ -321,11 +260,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   // x update of this pass (kK1, !first): 0 none (deferred), 1 x += a1 p_old,
   // 2 x = (x + a2 p_prev2) + a1 p_old with p_prev2 read from the p_new buffer
   // at the own position just before it is overwritten
-  // xmode_odd >= 0: planes of odd index take xmode_odd (MQ_XSPLIT: the
-  // two-step update alternates between the plane parities, so every K1 pass
-  // carries half of the x traffic)
-  const int xm_e = (MODE == kK1 && !first) ? xmode : 0;
-  const int xm_o = (MODE == kK1 && !first) ? (xmode_odd >= 0 ? xmode_odd : xmode) : 0;
+  const int xm = (MODE == kK1 && !first) ? xmode : 0;
   const uint32_t bytes = (with_p ? 6u : 3u) * HP * 8u;
   // halo (slot, component) converted by this thread besides its own
   // position: the 84 halo positions x 3 components are spread over threads
@@ -346,7 +281,6 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   const uint32_t *mask = a.mask;
   double *x = a.x;
 
-  const uint64_t pol_keep = l2_policy(true), pol_drop = l2_policy(false);
   auto issue = [&](int q) {
     if (tid == 0) {
       const int s = rslot(q), sp = pslot(q);
@@ -355,10 +289,10 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 #pragma unroll
       // box origin (k0-1, j0-1, q) in node coordinates = (k0, j0, q+1) in the
       // guard-shifted map: never negative
-      for (int c = 0; c < 3; ++c) tma_load_4d_hint(mc.sr[s].v[c], mr, &mc.bars[s], k0, j0, q + 1, c, pol_keep);
+      for (int c = 0; c < 3; ++c) tma_load_4d(mc.sr[s].v[c], mr, &mc.bars[s], k0, j0, q + 1, c);
       if (with_p) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) tma_load_4d_hint(mc.sp[sp].v[c], mp, &mc.bars[s], k0, j0, q + 1, c, pol_drop);
+        for (int c = 0; c < 3; ++c) tma_load_4d(mc.sp[sp].v[c], mp, &mc.bars[s], k0, j0, q + 1, c);
       }
     }
   };
@@ -376,7 +310,6 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       for (int c = 0; c < 3; ++c) {
         const int64_t e = c * L.C + qb + pos_own;
         o.mw[c] = __ldg(mask + (e >> 5));
-        const int xm = (q & 1) ? xm_o : xm_e;
         if (xm >= 1) o.xo[c] = __ldcg(x + e);
         if (xm == 2) o.p2[c] = __ldcg(pnew + e);
       }
@@ -412,7 +345,6 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     }
     double (&Sr)[3][BOXP] = mc.sr[s].v;
     const double (&Sp)[3][BOXP] = mc.sp[pslot(q)].v;
-    const int xm = (q & 1) ? xm_o : xm_e;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double rq = Sr[c][s_own];
@@ -423,13 +355,13 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
         pv = add(z, mul(beta, po));
         if (xm >= 1 && ((act >> c) & 1u)) {
           const double xv = xm == 2 ? add(o.xo[c], mul(alpha_prev2, o.p2[c])) : o.xo[c];
-          st_hint(x + c * L.C + qb + pos_own, add(xv, mul(alpha_prev, po)), pol_drop);
+          x[c * L.C + qb + pos_own] = add(xv, mul(alpha_prev, po));
         }
       }
       raw[c] = pv;
       Sr[c][s_own] = (MODE == kK1 && MQ_PRESCALE) ? mul(a.of, pv) : pv;
       if ((act >> c) & 1u) {
-        st_hint(pnew + c * L.C + qb + pos_own, pv, pol_drop);
+        pnew[c * L.C + qb + pos_own] = pv;
         push(q, c, pos_own - L.Si, pv);
       }
     }
@@ -459,7 +391,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   // each followed by the issue of the plane that takes over its p slot
   const int last = i1;  // planes i0-1 .. i1 are needed
   OwnPre pa, pb;
-  double rw[3], rw1[3], rw2[3];
+  double rw[3], rw1[3];
 #ifdef MQ_TRACE_MARCH
   if (mc.tr) mc.tr[128] = globaltimer_ns();  // march entry
 #endif
@@ -469,35 +401,6 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   convert(i0 - 1, false, pb, rw1);
   __syncthreads();
   if (i0 + NA - 1 <= last) issue(i0 + NA - 1);
-#if MQ_MARCH2
-  // two planes per step: converts of planes i+1, i+2, one __syncthreads, the
-  // stencils of planes i, i+1 (twice the independent work per barrier); the
-  // own-position data of the two planes of the next step is prefetched here
-  const OwnPre c0 = pa;
-  prefetch_own(pb, i0 + 1, i0 + 1 < i1);
-  prefetch_own(pa, i0 + 2, i0 + 2 < i1);
-  uint32_t act = convert(i0, true, c0, rw);
-  __syncthreads();
-  if (i0 + NA <= last) issue(i0 + NA);
-  for (int i = i0; i < i1; i += 2) {
-    const bool two = i + 1 < i1;
-    const OwnPre c1 = pb, c2 = pa;
-    prefetch_own(pb, i + 3, i + 3 < i1);
-    prefetch_own(pa, i + 4, i + 4 < i1);
-    const uint32_t a1 = convert(i + 1, i + 1 < i1, c1, rw1);
-    const uint32_t a2 = two ? convert(i + 2, i + 2 < i1, c2, rw2) : 0u;
-    __syncthreads();
-    // r slots of planes i-3, i-2 (last read by the previous step's
-    // stencils), p slots of planes i+1, i+2 (converted before the barrier)
-    if (i + NA + 1 <= last) issue(i + NA + 1);
-    if (two && i + NA + 2 <= last) issue(i + NA + 2);
-    stencil_plane(i, act, rw);
-    if (two) stencil_plane(i + 1, a1, rw1);
-    act = a2;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) rw[c] = rw2[c];
-  }
-#else
   const OwnPre c0 = pa;
   prefetch_own(pa, i0 + 1, i0 + 1 < i1);
 #ifdef MQ_TRACE_MARCH
@@ -528,7 +431,6 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 #pragma unroll
     for (int c = 0; c < 3; ++c) rw[c] = rw1[c];
   }
-#endif
   __syncthreads();
 #ifdef MQ_TRACE_MARCH
   if (mc.tr) mc.tr[131] = globaltimer_ns();  // march done
@@ -547,42 +449,6 @@ __device__ __forceinline__ void flat_pairs(int64_t total, F f) {
   for (; p < npair; p += stride) f(p, stride, 1);
 }
 
-#ifndef MQ_K2_BRICK
-#define MQ_K2_BRICK 0
-#endif
-// K2 over this CTA's own bricks, planes in reverse order: the rows of r and
-// Ap that K1 touched last are the first ones K2 reads back (still in L2), and
-// the planes K2 writes last are the ones the next K1 reads first.  Every
-// active dof lies in a brick (node positions j < ny, k < nz, i < nx); the
-// entries outside the bricks are 0 in r and Ap and stay 0.  f(e) per own
-// position, one warp per (plane, component, row) of 32 k positions.
-template <class F>
-__device__ __forceinline__ void brick_rows_reverse(const BrickGeo &g, const Lay &L, int G, F f) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int U = 4;  // rows in flight per warp
-  for (int bi = blockIdx.x; bi < g.nbricks; bi += G) {
-    int i0, i1, j0, k0;
-    brick_of(g, bi, i0, i1, j0, k0);
-    const int k = k0 + lane;
-    const bool kok = k < g.nz;
-    const int nrows = (i1 - i0) * 3 * TJ;
-    for (int q0 = warp * U; q0 < nrows; q0 += kWarps * U) {
-      int64_t e[U];
-      bool ok[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int q = q0 + u;
-        const int plane = i1 - 1 - q / (3 * TJ);
-        const int rem = q % (3 * TJ);
-        const int c = rem / TJ, jj = j0 + rem % TJ;
-        ok[u] = q < nrows && kok && jj < g.ny;
-        e[u] = c * L.C + L.off + (int64_t)plane * L.Si + (int64_t)jj * L.Sj + k;
-      }
-      f(e, ok);
-    }
-  }
-}
-
 #ifndef MQ_TMA_MINB
 #define MQ_TMA_MINB 2
 #endif
@@ -599,7 +465,6 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __gr
   const bool jac = a.use_jac != 0;
   double *x = a.x, *r = a.r, *ap = a.ap;
   const double *b = a.b;
-  const uint64_t pol_keep = l2_policy(true), pol_drop = l2_policy(false);
   const int x0_mode = a.x0_mode_dev ? *a.x0_mode_dev : a.x0_mode;
   if (a.err_word && *((volatile const unsigned int *)a.err_word)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -692,16 +557,11 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __gr
       double *pnew = pold_is_a ? a.pb : a.pa;
       const CUtensorMap *mp = pold_is_a ? &A.tm_pa : &A.tm_pb;
       // ---- K1 ----
-      int xmode = 0, xmode_odd = -1;
+      int xmode = 0;
       if (!first) {
 #if MQ_XDEFER
         xmode = pend ? 2 : 0;
         pend = !pend;
-#if MQ_XSPLIT
-        // odd planes run one iteration ahead: it = 2 applies p_1 alone, then
-        // the two-step update at every even it (even planes: every odd it >= 3)
-        xmode_odd = (it & 1) ? 0 : (it == 2 ? 1 : 2);
-#endif
 #else
         xmode = 1;
 #endif
@@ -715,19 +575,14 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __gr
         brick_of(g, bi, i0, i1, j0, k0);
         march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0,
                        [&](int c, int64_t e, auto V, double own) {
-#ifdef MQ_DIAG_NOSTENCIL
-                         // timing diagnostic only: a 5-point in-plane operator (SPD), 5 of 13 terms
-                         const double av = sub(mul(dg, V(c, 0, 0, 0)),
-                                               mul(of, add(add(V(c, 0, -1, 0), V(c, 0, 1, 0)),
-                                                           add(V(c, 0, 0, -1), V(c, 0, 0, 1)))));
-#elif MQ_PRESCALE
+#if MQ_PRESCALE
                          const double av = stencil3s(c, dg, own, V);
 #else
                          const double av = stencil3(c, dg, of, V);
 #endif
-                         st_hint(ap + e, av, pol_keep);
+                         ap[e] = av;
                          v1[0] = add(v1[0], mul(own, av));
-                       }, NoPush(), xmode_odd);
+                       });
       }
       block_sum<1>(v1, red);
       if (threadIdx.x == 0) a.partials[3 * G + blockIdx.x] = v1[0];
@@ -746,41 +601,20 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __gr
       alpha = rz / pap;
       // ---- K2: r -= alpha Ap (flat, all padded entries; non-dofs stay 0) ----
       double v2[2] = {0.0, 0.0};
-#if MQ_K2_BRICK
-      brick_rows_reverse(g, L, G, [&](const int64_t *e, const bool *ok) {
-        double rv[4], av[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (ok[u]) {
-            rv[u] = __ldcg(r + e[u]);
-            av[u] = __ldcg(ap + e[u]);
-          }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (ok[u]) {
-            const double r0 = sub(rv[u], mul(alpha, av[u]));
-            r[e[u]] = r0;
-            const double z0 = jac ? mul(inv, r0) : r0;
-            v2[0] = add(v2[0], mul(r0, r0));
-            v2[1] = add(v2[1], mul(r0, z0));
-          }
-      });
-      if (false)
-#endif
       flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
         double2 rv[kUnroll], av[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
           if (u < n) {
-            rv[u] = ld2_hint(reinterpret_cast<const double2 *>(r) + p + u * stride, pol_keep);
-            av[u] = ld2_hint(reinterpret_cast<const double2 *>(ap) + p + u * stride, pol_drop);
+            rv[u] = __ldcg(reinterpret_cast<const double2 *>(r) + p + u * stride);
+            av[u] = __ldcg(reinterpret_cast<const double2 *>(ap) + p + u * stride);
           }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
           if (u < n) {
             const double r0 = sub(rv[u].x, mul(alpha, av[u].x));
             const double r1 = sub(rv[u].y, mul(alpha, av[u].y));
-            st2_hint(reinterpret_cast<double2 *>(r) + p + u * stride, make_double2(r0, r1), pol_keep);
+            reinterpret_cast<double2 *>(r)[p + u * stride] = make_double2(r0, r1);
             const double z0 = jac ? mul(inv, r0) : r0, z1 = jac ? mul(inv, r1) : r1;
             v2[0] = add(v2[0], mul(r0, r0));
             v2[0] = add(v2[0], mul(r1, r1));
@@ -820,40 +654,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __gr
       // the pending alpha_{K-1} p_{K-1} (deferred x update), applied first
       const double *pdir2 = converged ? (pold_is_a ? a.pa : a.pb) : (pold_is_a ? a.pb : a.pa);
       const double alpha2 = converged ? alpha_prev : alpha_prev2;
-      // pending directions per plane parity (MQ_XSPLIT): even planes as the
-      // global toggle (pend), odd planes last updated at even iterations
-      const bool pend_e = pend;
-#if MQ_XSPLIT && MQ_XDEFER
-      const bool pend_o = iters >= 3 && (iters & 1);
-#else
-      const bool pend_o = pend;
-#endif
-      if (pend_e != pend_o) {
-        // mixed: per pair, by the parity of its node plane (a pair never
-        // straddles two planes: C and Si are even)
-        flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
-          double2 xv[kUnroll], pv[kUnroll], qv[kUnroll];
-          bool two[kUnroll];
-#pragma unroll
-          for (int u = 0; u < kUnroll; ++u)
-            if (u < n) {
-              const int64_t e = 2 * (p + u * stride);
-              const int64_t plane = (e % L.C) / L.Si - 1;
-              two[u] = (plane & 1) ? pend_o : pend_e;
-              xv[u] = __ldcg(reinterpret_cast<const double2 *>(x) + p + u * stride);
-              pv[u] = __ldcg(reinterpret_cast<const double2 *>(pdir) + p + u * stride);
-              if (two[u]) qv[u] = __ldcg(reinterpret_cast<const double2 *>(pdir2) + p + u * stride);
-            }
-#pragma unroll
-          for (int u = 0; u < kUnroll; ++u)
-            if (u < n) {
-              double2 xs = xv[u];
-              if (two[u]) xs = make_double2(add(xs.x, mul(alpha2, qv[u].x)), add(xs.y, mul(alpha2, qv[u].y)));
-              reinterpret_cast<double2 *>(x)[p + u * stride] =
-                  make_double2(add(xs.x, mul(alpha, pv[u].x)), add(xs.y, mul(alpha, pv[u].y)));
-            }
-        });
-      } else if (pend_e) {
+      if (pend) {
         flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
           double2 xv[kUnroll], pv[kUnroll], qv[kUnroll];
 #pragma unroll
