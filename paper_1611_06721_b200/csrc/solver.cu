@@ -108,6 +108,15 @@ struct SolverHost {
   // POD: K B_j on the TMA brick march (grids run by pcg_tma_kernel), one
   // tensor map per basis slot per family (the k of the family's projection)
   KnMulti *kn_multi[3] = {nullptr, nullptr, nullptr};
+  // POD: the eigen-decomposition of a family's snapshot Gram matrix depends
+  // only on its ring, final once the family's push is done, so it runs on a
+  // side stream right after the push (one CTA next to the TMA PCG kernel,
+  // which leaves CTA slots free) and is joined before the family's next
+  // projection or at the end of the call (MQ_EIG_AHEAD=0 disables)
+  bool eig_ahead = false;
+  cudaStream_t eig_side = nullptr;
+  cudaEvent_t ev_ef[3] = {}, ev_ej[3] = {};
+  bool eig_pend[3] = {false, false, false};
   // page-locked landing block of the host-facing calls: run status, the two
   // iteration counts and the probe value come back in one copy batch and one
   // stream synchronisation per call
@@ -153,6 +162,14 @@ void solver_free(mq_ctx *ctx) {
   if (!s) return;
   solver_graph_reset(ctx);
   for (int f = 0; f < 3; ++f) kn_multi_free(s->kn_multi[f]);
+  if (s->eig_side) {
+    cudaStreamSynchronize(s->eig_side);
+    cudaStreamDestroy(s->eig_side);
+  }
+  for (int f = 0; f < 3; ++f) {
+    if (s->ev_ef[f]) cudaEventDestroy(s->ev_ef[f]);
+    if (s->ev_ej[f]) cudaEventDestroy(s->ev_ej[f]);
+  }
   if (s->side) cudaStreamDestroy(s->side);
   for (int q = 0; q < SolverHost::kSlots; ++q) {
     if (s->ev_fork[q]) cudaEventDestroy(s->ev_fork[q]);
@@ -1469,8 +1486,17 @@ static int start_vector(mq_ctx *ctx, int fam, const double *rhs, double *x0) {
       break;
     }
     case MQ_STRAT_POD: {
-      k_pod_eig<<<1, 256, 0, st>>>(f, s->cfg.eps_pod);
-      LAUNCH_CHECK();
+      if (s->eig_ahead) {
+        // the eigen-decomposition of this ring ran after the family's last
+        // push (observe); an empty ring has podk = 0 from the reset
+        if (s->eig_pend[fam]) {
+          MQ_CUDA(cudaStreamWaitEvent(st, s->ev_ej[fam], 0));
+          s->eig_pend[fam] = false;
+        }
+      } else {
+        k_pod_eig<<<1, 256, 0, st>>>(f, s->cfg.eps_pod);
+        LAUNCH_CHECK();
+      }
       k_pod_basis_flat<<<G, kBlock, 0, st>>>(L.total / 2, f, s->d_X[fam], s->d_B);
       LAUNCH_CHECK();
       k_pod_basis<<<stream_grid(ctx), kBlock, 0, st>>>(L, ctx->d_mask, f, s->d_X[fam], s->d_B);
@@ -1592,6 +1618,14 @@ static int observe(mq_ctx *ctx, int fam, const double *y, const ObsRes &o, bool 
       KB_LAUNCH(s->kb, k_pod_push_flat, G, kBlock, st, L.total / 2, f, s->d_X[fam], s->cfg.n_pod, y, o.red, o.cnt,
                 post);
       LAUNCH_CHECK();
+      if (s->eig_ahead) {
+        MQ_CUDA(cudaEventRecord(s->ev_ef[fam], st));
+        MQ_CUDA(cudaStreamWaitEvent(s->eig_side, s->ev_ef[fam], 0));
+        k_pod_eig<<<1, 256, 0, s->eig_side>>>(f, s->cfg.eps_pod);
+        LAUNCH_CHECK();
+        MQ_CUDA(cudaEventRecord(s->ev_ej[fam], s->eig_side));
+        s->eig_pend[fam] = true;
+      }
       break;
     }
   }
@@ -1666,13 +1700,23 @@ static int join_side(mq_ctx *ctx, int slot) {
   return MQ_OK;
 }
 
+static int join_eigs(mq_ctx *ctx) {
+  SolverHost *s = ctx->solver;
+  for (int f = 0; f < 3; ++f)
+    if (s->eig_pend[f]) {
+      MQ_CUDA(cudaStreamWaitEvent(ctx->stream, s->ev_ej[f], 0));
+      s->eig_pend[f] = false;
+    }
+  return MQ_OK;
+}
+
 static int join_all(mq_ctx *ctx) {
   SolverHost *s = ctx->solver;
   for (int q = 0; q < SolverHost::kSlots; ++q) {
     int rc = join_side(ctx, q);
     if (rc) return rc;
   }
-  return MQ_OK;
+  return join_eigs(ctx);
 }
 
 static int euler_enqueue(mq_ctx *ctx, bool join_tail, bool defer_cpl = false);
@@ -1933,6 +1977,16 @@ int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern)
     table(&s->d_KB, s->h_KB, cfg->n_pod);
     // K B_j through the TMA march where the TMA PCG kernel runs (128^3 and
     // up); MQ_POD_SPMV=flat keeps the thread-per-row k_spmv_multi
+    const char *ea = getenv("MQ_EIG_AHEAD");
+    if (!rc && ctx->pcg_variant == 0 && ctx->brick_grid < ctx->sms * 2 && !(ea && ea[0] == '0')) {
+      cudaError_t e = cudaStreamCreateWithFlags(&s->eig_side, cudaStreamNonBlocking);
+      for (int f = 0; f < 3 && e == cudaSuccess; ++f) {
+        e = cudaEventCreateWithFlags(&s->ev_ef[f], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_ej[f], cudaEventDisableTiming);
+      }
+      if (e != cudaSuccess) rc = cuda_fail(e, "eig side stream");
+      else s->eig_ahead = true;
+    }
     const char *sp = getenv("MQ_POD_SPMV");
     if (!rc && ctx->pcg_variant == 0 && !(sp && std::string(sp) == "flat"))
       for (int fam = 0; fam < 3 && !rc; ++fam)
@@ -2012,6 +2066,8 @@ int mq_solver_init(mq_ctx *ctx, const mq_solver_cfg *cfg, const double *pattern)
 int mq_solver_reset(mq_ctx *ctx) {
   SolverHost *s = ctx->solver;
   if (!s) { set_error("solver not initialised"); return MQ_INVALID; }
+  int rj = join_eigs(ctx);  // a running eigen-decomposition writes the family state
+  if (rj) return rj;
   MQ_CUDA(cudaMemsetAsync(s->d_fam, 0, sizeof(FamDev) * 3, ctx->stream));
   for (bool &m : s->maybe_pending) m = false;  // the memset cleared any deferred insert
   s->probe_cached = false;
@@ -2068,6 +2124,7 @@ int mq_strategy_observe(mq_ctx *ctx, int32_t family, const double *y) {
     if (frc) return frc;
   }
   int rc = observe(ctx, family, y, main_res(ctx));
+  if (!rc) rc = join_eigs(ctx);
   if (rc) return rc;
   MQ_CUDA(cudaStreamSynchronize(ctx->stream));
   return MQ_OK;
@@ -2079,6 +2136,8 @@ int mq_diagnostics(mq_ctx *ctx, mq_diag *out) {
   {
     const int frc = flush_deferred(ctx);
     if (frc) return frc;
+    const int jrc = join_eigs(ctx);
+    if (jrc) return jrc;
   }
   FamDev f[3];
   RunDev r;
