@@ -31,7 +31,6 @@ CUDA-IPC-mapped neighbour buffers.
 from __future__ import annotations
 
 import ctypes
-import math
 import time
 from dataclasses import dataclass, field
 
