@@ -1,5 +1,5 @@
 """Summarise an ncu --csv metrics log of the tall-skinny start-vector kernels
-(tools/gpu_sanitize_and_ts.sh) per kernel: launches, median duration, DRAM
+(tools/gpu_tallskinny.sh, tools/gpu_pod_profile.sh) per kernel: launches, median duration, DRAM
 and L2 bytes per launch and the achieved GB/s against the measured HBM peak.
 
     python tools/ts_summary.py gpurun_out/ts/cfg2_cspe.csv [...]
