@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <cudaTypedefs.h>
+#include <type_traits>
 
 #include "mq_device.cuh"
 #include "slab_rank.cuh"
@@ -44,6 +45,9 @@ constexpr int BOXP = 352;                      // box slot padded to a 128-byte 
 // in place into p_new, read by the stencil) plus NA planes in flight; the
 // p_old ring only the NA in-flight planes (p_old is dead once its plane is
 // converted).  Same bytes as a 5-stage (r, p) ring, one more plane ahead.
+#ifndef MQ_STENCIL_CSE
+#define MQ_STENCIL_CSE 1
+#endif
 // K1 stages of * p_new (the off-diagonal product of every staged value,
 // formed once) instead of p_new: stencil3s, bit-identical rows
 #ifndef MQ_PRESCALE
@@ -219,6 +223,89 @@ __device__ __forceinline__ double stencil3s(int c, double dg, double own, V v) {
   return s;
 }
 
+// The three K_n rows of one node from pre-scaled staged values (stencil3s),
+// each distinct neighbour value loaded once (24 shared-memory loads instead
+// of 36; identical arithmetic and order per row); own[c] the raw own p.
+template <class V>
+__device__ __forceinline__ void stencil3s_rows(double dg, const double (&own)[3], V v, double (&av)[3]) {
+  const double v0_0m10 = v(0, 0, -1, 0);
+  const double v0_00m1 = v(0, 0, 0, -1);
+  const double v0_001 = v(0, 0, 0, 1);
+  const double v0_010 = v(0, 0, 1, 0);
+  const double v1_0m10 = v(1, 0, -1, 0);
+  const double v1_000 = v(1, 0, 0, 0);
+  const double v1_1m10 = v(1, 1, -1, 0);
+  const double v1_100 = v(1, 1, 0, 0);
+  const double v2_00m1 = v(2, 0, 0, -1);
+  const double v2_000 = v(2, 0, 0, 0);
+  const double v2_10m1 = v(2, 1, 0, -1);
+  const double v2_100 = v(2, 1, 0, 0);
+  const double v0_m100 = v(0, -1, 0, 0);
+  const double v0_m110 = v(0, -1, 1, 0);
+  const double v0_000 = v(0, 0, 0, 0);
+  const double v1_m100 = v(1, -1, 0, 0);
+  const double v1_00m1 = v(1, 0, 0, -1);
+  const double v1_001 = v(1, 0, 0, 1);
+  const double v2_01m1 = v(2, 0, 1, -1);
+  const double v2_010 = v(2, 0, 1, 0);
+  const double v0_m101 = v(0, -1, 0, 1);
+  const double v1_0m11 = v(1, 0, -1, 1);
+  const double v2_m100 = v(2, -1, 0, 0);
+  const double v2_0m10 = v(2, 0, -1, 0);
+  {
+    double s;
+    s = -v0_0m10;
+    s = sub(s, v0_00m1);
+    s = add(s, mul(dg, own[0]));
+    s = sub(s, v0_001);
+    s = sub(s, v0_010);
+    s = add(s, v1_0m10);
+    s = sub(s, v1_000);
+    s = sub(s, v1_1m10);
+    s = add(s, v1_100);
+    s = add(s, v2_00m1);
+    s = sub(s, v2_000);
+    s = sub(s, v2_10m1);
+    s = add(s, v2_100);
+    av[0] = s;
+  }
+  {
+    double s;
+    s = v0_m100;
+    s = sub(s, v0_m110);
+    s = sub(s, v0_000);
+    s = add(s, v0_010);
+    s = sub(s, v1_m100);
+    s = sub(s, v1_00m1);
+    s = add(s, mul(dg, own[1]));
+    s = sub(s, v1_001);
+    s = sub(s, v1_100);
+    s = add(s, v2_00m1);
+    s = sub(s, v2_000);
+    s = sub(s, v2_01m1);
+    s = add(s, v2_010);
+    av[1] = s;
+  }
+  {
+    double s;
+    s = v0_m100;
+    s = sub(s, v0_m101);
+    s = sub(s, v0_000);
+    s = add(s, v0_001);
+    s = add(s, v1_0m10);
+    s = sub(s, v1_0m11);
+    s = sub(s, v1_000);
+    s = add(s, v1_001);
+    s = sub(s, v2_m100);
+    s = sub(s, v2_0m10);
+    s = add(s, mul(dg, own[2]));
+    s = sub(s, v2_010);
+    s = sub(s, v2_100);
+    av[2] = s;
+  }
+}
+
+
 __device__ __forceinline__ int rslot(int q) { return (q + NR) % NR; }  // q >= -1
 __device__ __forceinline__ int pslot(int q) { return (q + NP) % NP; }
 
@@ -377,13 +464,25 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     if (!act) return;
     const int64_t qb = (int64_t)i * L.Si;
     const int sm1 = rslot(i - 1), s0 = rslot(i), sp1 = rslot(i + 1);
+    auto ld = [&](int cc, int di, int dj, int dk) {
+      const int s = di < 0 ? sm1 : (di == 0 ? s0 : sp1);
+      return mc.sr[s].v[cc][s_own + dj * HK + dk];
+    };
+#if MQ_PRESCALE && MQ_STENCIL_CSE
+    if constexpr (MODE == kK1) {
+      // all three rows from the 24 distinct staged values, each loaded once;
+      // the row callback receives the row value
+      double av[3];
+      stencil3s_rows(a.dg, raw, ld, av);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        if ((act >> c) & 1u) row(c, c * L.C + qb + pos_own, av[c], raw[c]);
+      return;
+    }
+#endif
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      if ((act >> c) & 1u)
-        row(c, c * L.C + qb + pos_own, [&](int cc, int di, int dj, int dk) {
-          const int s = di < 0 ? sm1 : (di == 0 ? s0 : sp1);
-          return mc.sr[s].v[cc][s_own + dj * HK + dk];
-        }, raw[c]);
+      if ((act >> c) & 1u) row(c, c * L.C + qb + pos_own, ld, raw[c]);
     }
   };
 
@@ -575,10 +674,12 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __gr
         brick_of(g, bi, i0, i1, j0, k0);
         march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0,
                        [&](int c, int64_t e, auto V, double own) {
+                         double av;
+                         if constexpr (std::is_same_v<decltype(V), double>) av = V;  // stencil3s_rows
 #if MQ_PRESCALE
-                         const double av = stencil3s(c, dg, own, V);
+                         else av = stencil3s(c, dg, own, V);
 #else
-                         const double av = stencil3(c, dg, of, V);
+                         else av = stencil3(c, dg, of, V);
 #endif
                          ap[e] = av;
                          v1[0] = add(v1[0], mul(own, av));
@@ -877,10 +978,12 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_slab_kernel(const __grid_co
         brick_of(g, bi, i0, i1, j0, k0);
         march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, 1, 0.0, pnew, i0, i1, j0, k0,
                        [&](int c, int64_t e, auto V, double own) {
+                         double av;
+                         if constexpr (std::is_same_v<decltype(V), double>) av = V;  // stencil3s_rows
 #if MQ_PRESCALE
-                         const double av = stencil3s(c, dg, own, V);
+                         else av = stencil3s(c, dg, own, V);
 #else
-                         const double av = stencil3(c, dg, of, V);
+                         else av = stencil3(c, dg, of, V);
 #endif
                          ap[e] = av;
                          v1[0] = add(v1[0], mul(own, av));
