@@ -225,32 +225,36 @@ __device__ __forceinline__ double stencil3s(int c, double dg, double own, V v) {
 
 // The three K_n rows of one node from pre-scaled staged values (stencil3s),
 // each distinct neighbour value loaded once (24 shared-memory loads instead
-// of 36; identical arithmetic and order per row); own[c] the raw own p.
+// of 36, 16 with the thread's own staged values of planes i-1, i, i+1 kept
+// in registers;
+// identical arithmetic and order per row); own[c] / own[3+c] the raw /
+// pre-scaled own p of the row's node.
 template <class V>
-__device__ __forceinline__ void stencil3s_rows(double dg, const double (&own)[3], V v, double (&av)[3]) {
+__device__ __forceinline__ void stencil3s_rows(double dg, const double (&prev)[6], const double (&own)[6],
+                                               const double (&next)[6], V v, double (&av)[3]) {
   const double v0_0m10 = v(0, 0, -1, 0);
   const double v0_00m1 = v(0, 0, 0, -1);
   const double v0_001 = v(0, 0, 0, 1);
   const double v0_010 = v(0, 0, 1, 0);
   const double v1_0m10 = v(1, 0, -1, 0);
-  const double v1_000 = v(1, 0, 0, 0);
+  const double v1_000 = own[4];  // own node, plane i: the value this thread staged
   const double v1_1m10 = v(1, 1, -1, 0);
-  const double v1_100 = v(1, 1, 0, 0);
+  const double v1_100 = next[4];  // own node, plane i+1
   const double v2_00m1 = v(2, 0, 0, -1);
-  const double v2_000 = v(2, 0, 0, 0);
+  const double v2_000 = own[5];  // own node, plane i: the value this thread staged
   const double v2_10m1 = v(2, 1, 0, -1);
-  const double v2_100 = v(2, 1, 0, 0);
-  const double v0_m100 = v(0, -1, 0, 0);
+  const double v2_100 = next[5];  // own node, plane i+1
+  const double v0_m100 = prev[3];  // own node, plane i-1
   const double v0_m110 = v(0, -1, 1, 0);
-  const double v0_000 = v(0, 0, 0, 0);
-  const double v1_m100 = v(1, -1, 0, 0);
+  const double v0_000 = own[3];  // own node, plane i: the value this thread staged
+  const double v1_m100 = prev[4];  // own node, plane i-1
   const double v1_00m1 = v(1, 0, 0, -1);
   const double v1_001 = v(1, 0, 0, 1);
   const double v2_01m1 = v(2, 0, 1, -1);
   const double v2_010 = v(2, 0, 1, 0);
   const double v0_m101 = v(0, -1, 0, 1);
   const double v1_0m11 = v(1, 0, -1, 1);
-  const double v2_m100 = v(2, -1, 0, 0);
+  const double v2_m100 = prev[5];  // own node, plane i-1
   const double v2_0m10 = v(2, 0, -1, 0);
   {
     double s;
@@ -406,7 +410,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     }
   };
   // returns the active-dof bits (bit c = component c) of the own position
-  auto convert = [&](int q, bool own_plane, const OwnPre &o, double (&raw)[3]) -> uint32_t {
+  auto convert = [&](int q, bool own_plane, const OwnPre &o, double (&raw)[6]) -> uint32_t {
     const int s = rslot(q);
     const int64_t qb = (int64_t)q * L.Si;
 #ifdef MQ_TRACE_MARCH
@@ -427,7 +431,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     }
     if (MODE == kInit) {  // the staged x0 is used as is
 #pragma unroll
-      for (int c = 0; c < 3; ++c) raw[c] = mc.sr[s].v[c][s_own];
+      for (int c = 0; c < 3; ++c) raw[c] = raw[3 + c] = mc.sr[s].v[c][s_own];
       return act;
     }
     double (&Sr)[3][BOXP] = mc.sr[s].v;
@@ -446,7 +450,8 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
         }
       }
       raw[c] = pv;
-      Sr[c][s_own] = (MODE == kK1 && MQ_PRESCALE) ? mul(a.of, pv) : pv;
+      raw[3 + c] = (MODE == kK1 && MQ_PRESCALE) ? mul(a.of, pv) : pv;
+      Sr[c][s_own] = raw[3 + c];
       if ((act >> c) & 1u) {
         pnew[c * L.C + qb + pos_own] = pv;
         push(q, c, pos_own - L.Si, pv);
@@ -460,7 +465,8 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     }
     return act;
   };
-  auto stencil_plane = [&](int i, uint32_t act, const double (&raw)[3]) {
+  auto stencil_plane = [&](int i, uint32_t act, const double (&prev)[6], const double (&raw)[6],
+                           const double (&next)[6]) {
     if (!act) return;
     const int64_t qb = (int64_t)i * L.Si;
     const int sm1 = rslot(i - 1), s0 = rslot(i), sp1 = rslot(i + 1);
@@ -473,7 +479,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       // all three rows from the 24 distinct staged values, each loaded once;
       // the row callback receives the row value
       double av[3];
-      stencil3s_rows(a.dg, raw, ld, av);
+      stencil3s_rows(a.dg, prev, raw, next, ld, av);
 #pragma unroll
       for (int c = 0; c < 3; ++c)
         if ((act >> c) & 1u) row(c, c * L.C + qb + pos_own, av[c], raw[c]);
@@ -490,14 +496,14 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   // each followed by the issue of the plane that takes over its p slot
   const int last = i1;  // planes i0-1 .. i1 are needed
   OwnPre pa, pb;
-  double rw[3], rw1[3];
+  double rwm[6], rw[6], rw1[6];  // own staged values of planes i-1, i, i+1
 #ifdef MQ_TRACE_MARCH
   if (mc.tr) mc.tr[128] = globaltimer_ns();  // march entry
 #endif
   for (int q = i0 - 1; q <= i0 + NA - 2 && q <= last; ++q) issue(q);
   prefetch_own(pa, i0, true);
   prefetch_own(pb, i0 - 1, false);
-  convert(i0 - 1, false, pb, rw1);
+  convert(i0 - 1, false, pb, rwm);
   __syncthreads();
   if (i0 + NA - 1 <= last) issue(i0 + NA - 1);
   const OwnPre c0 = pa;
@@ -525,10 +531,13 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     // r slot of plane i-2 (its last stencil was before this barrier), p slot
     // of plane i+1 (converted before this barrier)
     if (i + NA + 1 <= last) issue(i + NA + 1);
-    stencil_plane(i, act, rw);
+    stencil_plane(i, act, rwm, rw, rw1);
     act = act_next;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) rw[c] = rw1[c];
+    for (int c = 0; c < 6; ++c) {
+      rwm[c] = rw[c];
+      rw[c] = rw1[c];
+    }
   }
   __syncthreads();
 #ifdef MQ_TRACE_MARCH
