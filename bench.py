@@ -13,7 +13,7 @@ write) before every timed step, outside the timed events.
 Outputs one JSON line (rank 0).  `value` is device-timed with the inputs
 resident in HBM; `e2e` is the same metric through the host-facing API
 (explicit_euler_step + recover_an + probe_b with host arrays, copies inside
-the timed region); `roofline` is the fused PCG kernel (pcg_tma_kernel)
+the timed region); `roofline` is the fused PCG kernel (pcg_tma1_kernel)
 measured with CUDA events inside the timed region.  Secondary keys: configs[1]
 (64^3) with CSPE and with POD-20, configs[4] (256^3) on one GPU.
 `cpu_baseline` times the CPU port of the reference (oracle/, numpy/scipy) on

@@ -58,6 +58,7 @@ int ctx_pcg(mq_ctx *ctx, const double *b, double *x, int x0_mode, double rel_tol
   a.pb = ctx->d_p1;
   a.ap = ctx->d_ap;
   a.ap2 = ctx->d_ap2;
+  a.r2 = ctx->d_r2;
   a.stress_ns = pcg_stress_ns();
   a.rel_tol = rel_tol;
   a.abs_tol = abs_tol;
@@ -190,7 +191,9 @@ int mq_ctx_create(const mq_grid_desc *desc, int32_t device, mq_ctx **out) {
   // Ap of odd iterations: the single-reduction resident kernel publishes Ap
   // double-buffered (a CTA's next Ap must not overwrite the values a slower
   // neighbour still has to load after the barrier)
-  if (!rc && ctx->res_grid > 0) rc = ctx_alloc(ctx, (void **)&ctx->d_ap2, sizeof(double) * t.L.total);
+  // (and so does the one-barrier TMA kernel, which also double-buffers r)
+  if (!rc) rc = ctx_alloc(ctx, (void **)&ctx->d_ap2, sizeof(double) * t.L.total);
+  if (!rc) rc = ctx_alloc(ctx, (void **)&ctx->d_r2, sizeof(double) * t.L.total);
   {
     // default: shared-memory-resident kernel when the bricks fit on chip,
     // else the TMA brick kernel; MQ_PCG_KERNEL=simple|brick|resident overrides
@@ -291,7 +294,7 @@ int mq_pcg_kernel_info(const mq_ctx *ctx, char *name, int32_t cap, int32_t *grid
     n = std::string(resident_single_reduction(li) ? "pcg_resident1_kernel<" : "pcg_resident_kernel<") +
         std::to_string(li) + ">";
     g = ctx->res_grid;
-  } else { n = "pcg_tma_kernel"; g = ctx->brick_grid; }
+  } else { n = tma_single_reduction(ctx->geo) ? "pcg_tma1_kernel" : "pcg_tma_kernel"; g = ctx->brick_grid; }
   if (name && cap > 0) {
     std::strncpy(name, n.c_str(), (size_t)cap - 1);
     name[cap - 1] = 0;

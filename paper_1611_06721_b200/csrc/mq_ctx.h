@@ -78,7 +78,8 @@ struct mq_ctx {
   double *d_stage = nullptr;
   // PCG scratch
   double *d_r = nullptr, *d_p0 = nullptr, *d_p1 = nullptr, *d_ap = nullptr;
-  double *d_ap2 = nullptr;  // Ap of odd iterations (pcg_resident1_kernel)
+  double *d_ap2 = nullptr;  // Ap of odd iterations (pcg_resident1_kernel, pcg_tma1_kernel)
+  double *d_r2 = nullptr;   // r of odd iterations (pcg_tma1_kernel)
   double *d_tmp0 = nullptr, *d_tmp1 = nullptr;
   double *d_partials = nullptr;
   mq::GridBar *d_bar = nullptr;
@@ -153,6 +154,7 @@ int pcg_stencil_grid(int64_t words, int *out);
 int launch_pcg_csr(const CsrPcgArgs &args, int grid, cudaStream_t s);
 int pcg_csr_grid(int64_t n, int *out);
 int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int sm_cap, int *grid, BrickGeo *geo);
+bool tma_single_reduction(const BrickGeo &g);  // pcg_tma1_kernel (one grid barrier per iteration) is launched
 int launch_pcg_brick(const StencilPcgArgs &args, const BrickGeo &geo, int grid, cudaStream_t s);
 struct KnMulti;
 int kn_multi_prepare(const Lay &L, const BrickGeo &geo, const uint32_t *mask, double dg, double of,

@@ -65,6 +65,7 @@ struct StencilPcgArgs {
   const unsigned int *err_word;  // optional: skip the solve if set
   unsigned long long *trace;   // optional: %globaltimer stamps (CTA 0) per phase
   double *ap2;                 // second Ap buffer (pcg_resident1_kernel publishes Ap double-buffered)
+  double *r2;                  // second r buffer (pcg_tma1_kernel keeps r double-buffered)
   int stress_ns;               // test only (MQ_PCG_STRESS): some CTAs sleep after each grid barrier
 };
 

@@ -229,9 +229,9 @@ __device__ __forceinline__ double stencil3s(int c, double dg, double own, V v) {
 // in registers;
 // identical arithmetic and order per row); own[c] / own[3+c] the raw /
 // pre-scaled own p of the row's node.
-template <class V>
-__device__ __forceinline__ void stencil3s_rows(double dg, const double (&prev)[6], const double (&own)[6],
-                                               const double (&next)[6], V v, double (&av)[3]) {
+template <class V, int N>
+__device__ __forceinline__ void stencil3s_rows(double dg, const double (&prev)[N], const double (&own)[N],
+                                               const double (&next)[N], V v, double (&av)[3]) {
   const double v0_0m10 = v(0, 0, -1, 0);
   const double v0_00m1 = v(0, 0, 0, -1);
   const double v0_001 = v(0, 0, 0, 1);
@@ -315,13 +315,24 @@ __device__ __forceinline__ int pslot(int q) { return (q + NP) % NP; }
 
 // One brick of K1 (mode kK1) or of the initial residual r = b - A x0 (mode
 // kInit: the marched field is x0, staged from tm_x).  Uniform per CTA.
-enum { kInit = 0, kK1 = 1 };
+// kK1R: K1 of the one-barrier kernel (pcg_tma1_kernel): the staged r is
+// r_{k-2}, advanced to r_{k-1} = r_{k-2} - alpha_{k-1} Ap_{k-1} with the
+// staged Ap_{k-1} before the conversion (own and halo positions, the same
+// arithmetic as a K2 pass), r_{k-1} stored at the own positions, its r.r and
+// r.z summed into mc.crr / mc.crz.
+enum { kInit = 0, kK1 = 1, kK1R = 2 };
 
 struct MarchCtx {
   Box3 *sr;        // NR slots of r (-> p_new); bars[] is indexed by r slot
   Box3 *sp;        // NP slots of p_old
   uint64_t *bars;
   uint32_t ph;  // per-slot mbarrier parity (identical in every thread)
+  // kK1R only: NP slots of Ap_{k-1}, its map, the r_{k-1} output vector and
+  // the own r.r / r.z partial sums
+  Box3 *sa = nullptr;
+  const CUtensorMap *ma = nullptr;
+  double *rout = nullptr;
+  double crr = 0.0, crz = 0.0;
 #ifdef MQ_TRACE_MARCH
   unsigned long long *tr = nullptr;  // CTA 0 thread 0, one iteration: 4 stamps per plane step
 #endif
@@ -333,7 +344,7 @@ struct NoPush {
 
 // push(q, c, jk, v): p_new of an own active position of plane q (jk = its
 // offset inside the padded plane), for the slab kernel's ghost stores
-template <int MODE, class ROW, class PUSH = NoPush>
+template <int MODE, int NAT = NA, class ROW, class PUSH = NoPush>
 __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, const CUtensorMap *mr,
                                           const CUtensorMap *mp, bool first, double beta, double alpha_prev,
                                           int xmode, double alpha_prev2, double *pnew, int i0, int i1, int j0,
@@ -342,17 +353,21 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   const StencilPcgArgs &a = A.a;
   const BrickGeo &g = A.g;
   const Lay &L = a.L;
+  constexpr int NRT = NAT + 3, NPT = NAT;  // ring slots (the kernel's allocation)
+  auto rsl = [](int q) { return (q + NRT) % NRT; };  // q >= -1
+  auto psl = [](int q) { return (q + NPT) % NPT; };
   const int tid = threadIdx.x, ty = tid >> 5, tx = tid & 31;
   const int j = j0 + ty, k = k0 + tx;
   const bool own_ok = j < g.ny && k < g.nz;
   const int s_own = (ty + 1) * HK + (tx + 1);
   const int64_t pos_own = L.off + (int64_t)j * L.Sj + k;
-  const bool with_p = (MODE == kK1) && !first;
+  constexpr bool K1M = MODE == kK1 || MODE == kK1R;
+  const bool with_p = K1M && !first;
   // x update of this pass (kK1, !first): 0 none (deferred), 1 x += a1 p_old,
   // 2 x = (x + a2 p_prev2) + a1 p_old with p_prev2 read from the p_new buffer
   // at the own position just before it is overwritten
-  const int xm = (MODE == kK1 && !first) ? xmode : 0;
-  const uint32_t bytes = (with_p ? 6u : 3u) * HP * 8u;
+  const int xm = (K1M && !first) ? xmode : 0;
+  const uint32_t bytes = (with_p ? (MODE == kK1R ? 9u : 6u) : 3u) * HP * 8u;
   // halo (slot, component) converted by this thread besides its own
   // position: the 84 halo positions x 3 components are spread over threads
   // 0..251, one each, so that no warp carries three times the work
@@ -374,7 +389,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 
   auto issue = [&](int q) {
     if (tid == 0) {
-      const int s = rslot(q), sp = pslot(q);
+      const int s = rsl(q), sp = psl(q);
       fence_proxy_async_smem();
       mbar_expect_tx(&mc.bars[s], bytes);
 #pragma unroll
@@ -384,6 +399,10 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       if (with_p) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) tma_load_4d(mc.sp[sp].v[c], mp, &mc.bars[s], k0, j0, q + 1, c);
+        if (MODE == kK1R) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) tma_load_4d(mc.sa[sp].v[c], mc.ma, &mc.bars[s], k0, j0, q + 1, c);
+        }
       }
     }
   };
@@ -410,8 +429,8 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     }
   };
   // returns the active-dof bits (bit c = component c) of the own position
-  auto convert = [&](int q, bool own_plane, const OwnPre &o, double (&raw)[6]) -> uint32_t {
-    const int s = rslot(q);
+  auto convert = [&](int q, bool own_plane, const OwnPre &o, double (&raw)[9]) -> uint32_t {
+    const int s = rsl(q);
     const int64_t qb = (int64_t)q * L.Si;
 #ifdef MQ_TRACE_MARCH
     if (mc.tr && q - i0 >= 1 && q - i0 < 33) mc.tr[4 * (q - i0 - 1) + 0] = globaltimer_ns();
@@ -435,10 +454,12 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       return act;
     }
     double (&Sr)[3][BOXP] = mc.sr[s].v;
-    const double (&Sp)[3][BOXP] = mc.sp[pslot(q)].v;
+    const double (&Sp)[3][BOXP] = mc.sp[psl(q)].v;
+    const double (&Sa)[3][BOXP] = mc.sa[MODE == kK1R ? psl(q) : 0].v;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const double rq = Sr[c][s_own];
+      double rq = Sr[c][s_own];
+      if (MODE == kK1R && !first) rq = sub(rq, mul(alpha_prev, Sa[c][s_own]));
       const double z = jac ? mul(inv, rq) : rq;
       double pv = z;
       if (!first) {
@@ -450,45 +471,59 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
         }
       }
       raw[c] = pv;
-      raw[3 + c] = (MODE == kK1 && MQ_PRESCALE) ? mul(a.of, pv) : pv;
+      raw[3 + c] = (K1M && MQ_PRESCALE) ? mul(a.of, pv) : pv;
+      raw[6 + c] = rq;
       Sr[c][s_own] = raw[3 + c];
       if ((act >> c) & 1u) {
         pnew[c * L.C + qb + pos_own] = pv;
         push(q, c, pos_own - L.Si, pv);
+        if (MODE == kK1R) {
+          if (!first) mc.rout[c * L.C + qb + pos_own] = rq;
+          mc.crr = add(mc.crr, mul(rq, rq));
+          mc.crz = add(mc.crz, mul(rq, z));
+        }
       }
     }
     if (hs >= 0) {
-      const double rq = Sr[hc][hs];
+      double rq = Sr[hc][hs];
+      if (MODE == kK1R && !first) rq = sub(rq, mul(alpha_prev, Sa[hc][hs]));
       const double z = jac ? mul(inv, rq) : rq;
       const double ph = first ? z : add(z, mul(beta, Sp[hc][hs]));
-      Sr[hc][hs] = (MODE == kK1 && MQ_PRESCALE) ? mul(a.of, ph) : ph;
+      Sr[hc][hs] = (K1M && MQ_PRESCALE) ? mul(a.of, ph) : ph;
     }
     return act;
   };
-  auto stencil_plane = [&](int i, uint32_t act, const double (&prev)[6], const double (&raw)[6],
-                           const double (&next)[6]) {
+  auto stencil_plane = [&](int i, uint32_t act, const double (&prev)[9], const double (&raw)[9],
+                           const double (&next)[9]) {
     if (!act) return;
     const int64_t qb = (int64_t)i * L.Si;
-    const int sm1 = rslot(i - 1), s0 = rslot(i), sp1 = rslot(i + 1);
+    const int sm1 = rsl(i - 1), s0 = rsl(i), sp1 = rsl(i + 1);
     auto ld = [&](int cc, int di, int dj, int dk) {
       const int s = di < 0 ? sm1 : (di == 0 ? s0 : sp1);
       return mc.sr[s].v[cc][s_own + dj * HK + dk];
     };
 #if MQ_PRESCALE && MQ_STENCIL_CSE
-    if constexpr (MODE == kK1) {
+    if constexpr (K1M) {
       // all three rows from the 24 distinct staged values, each loaded once;
-      // the row callback receives the row value
+      // the row callback receives the row value (kK1R: and the own r_{k-1})
       double av[3];
       stencil3s_rows(a.dg, prev, raw, next, ld, av);
 #pragma unroll
       for (int c = 0; c < 3; ++c)
-        if ((act >> c) & 1u) row(c, c * L.C + qb + pos_own, av[c], raw[c]);
+        if ((act >> c) & 1u) {
+          if constexpr (MODE == kK1R) row(c, c * L.C + qb + pos_own, av[c], raw[c], raw[6 + c]);
+          else row(c, c * L.C + qb + pos_own, av[c], raw[c]);
+        }
       return;
     }
+#else
+    static_assert(MODE != kK1R, "kK1R needs the pre-scaled CSE stencil");
 #endif
+    if constexpr (MODE != kK1R) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      if ((act >> c) & 1u) row(c, c * L.C + qb + pos_own, ld, raw[c]);
+      for (int c = 0; c < 3; ++c) {
+        if ((act >> c) & 1u) row(c, c * L.C + qb + pos_own, ld, raw[c]);
+      }
     }
   };
 
@@ -496,16 +531,16 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   // each followed by the issue of the plane that takes over its p slot
   const int last = i1;  // planes i0-1 .. i1 are needed
   OwnPre pa, pb;
-  double rwm[6], rw[6], rw1[6];  // own staged values of planes i-1, i, i+1
+  double rwm[9], rw[9], rw1[9];  // own staged values of planes i-1, i, i+1
 #ifdef MQ_TRACE_MARCH
   if (mc.tr) mc.tr[128] = globaltimer_ns();  // march entry
 #endif
-  for (int q = i0 - 1; q <= i0 + NA - 2 && q <= last; ++q) issue(q);
+  for (int q = i0 - 1; q <= i0 + NAT - 2 && q <= last; ++q) issue(q);
   prefetch_own(pa, i0, true);
   prefetch_own(pb, i0 - 1, false);
   convert(i0 - 1, false, pb, rwm);
   __syncthreads();
-  if (i0 + NA - 1 <= last) issue(i0 + NA - 1);
+  if (i0 + NAT - 1 <= last) issue(i0 + NAT - 1);
   const OwnPre c0 = pa;
   prefetch_own(pa, i0 + 1, i0 + 1 < i1);
 #ifdef MQ_TRACE_MARCH
@@ -516,7 +551,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 #ifdef MQ_TRACE_MARCH
   if (mc.tr) mc.tr[130] = globaltimer_ns();  // plane i0 converted (prologue done)
 #endif
-  if (i0 + NA <= last) issue(i0 + NA);
+  if (i0 + NAT <= last) issue(i0 + NAT);
   for (int i = i0; i < i1; ++i) {
     const OwnPre cur = pa;
     prefetch_own(pa, i + 2, i + 2 < i1);
@@ -530,11 +565,11 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 #endif
     // r slot of plane i-2 (its last stencil was before this barrier), p slot
     // of plane i+1 (converted before this barrier)
-    if (i + NA + 1 <= last) issue(i + NA + 1);
+    if (i + NAT + 1 <= last) issue(i + NAT + 1);
     stencil_plane(i, act, rwm, rw, rw1);
     act = act_next;
 #pragma unroll
-    for (int c = 0; c < 6; ++c) {
+    for (int c = 0; c < 9; ++c) {
       rwm[c] = rw[c];
       rw[c] = rw1[c];
     }
@@ -795,6 +830,284 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __gr
             if (u < n)
               reinterpret_cast<double2 *>(x)[p + u * stride] =
                   make_double2(add(xv[u].x, mul(alpha, pv[u].x)), add(xv[u].y, mul(alpha, pv[u].y)));
+        });
+      }
+      if (!converged) status = MQ_NOT_CONVERGED;
+    }
+  }
+done:
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    PcgOut o;
+    o.iterations = iters;
+    o.converged = converged;
+    o.status = status;
+    o.applies = applies;
+    o.rel = rel;
+    o.bnorm = bnorm;
+    o.alpha = alpha;
+    o.rz = rz;
+    *a.out = o;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One grid barrier per iteration (pcg_tma1_kernel, the default; MQ_PCG_SYNC=2
+// selects pcg_tma_kernel above).  The reference's iteration
+// (krylov.py:231-249) needs p.Ap before alpha and r.z after the r update.
+// With the scalar Jacobi preconditioner (z = inv * r) the next r.z follows
+// from scalars of the current pass,
+//   |r - alpha Ap|^2 = r.r - 2 alpha r.Ap + alpha^2 Ap.Ap,
+// so the K1 pass of iteration k reduces [p.Ap, r.Ap, Ap.Ap, r.r, r.z] once
+// (D'Azevedo, Eijkhout & Romine's reduced-synchronisation CG; the same scheme
+// as pcg_resident1_kernel).  The r update moves into the next pass: K1 of
+// iteration k stages r_{k-2} and Ap_{k-1} with the TMA next to p_{k-1},
+// forms r_{k-1} = r_{k-2} - alpha_{k-1} Ap_{k-1} in shared memory (own and
+// halo positions, bit-identical) and stores it, then p_k = z + beta p_{k-1}
+// and Ap_k as before; the flat K2 pass and its barrier are gone.  Only beta
+// uses the extrapolated r.z; alpha uses r.z and the stopping test |r| <=
+// target uses r.r, both summed from r_{k-1} itself, one barrier later: the
+// test of iteration k-1 is read at the barrier of k, whose pass is then
+// discarded (x, the iteration count, the application count and the reported
+// residual are the reference's).  Exact-arithmetic iterates are unchanged; in
+// fp64 they differ from the two-barrier kernel in the last bits (PCG parity
+// bar: 1e-8 field, +-1 iteration).
+// r and Ap are double-buffered (r_j in r / r2, Ap_j in ap / ap2 by the parity
+// of j): the pass of k writes r_{k-1} and Ap_k while slower CTAs may still
+// stage r_{k-2} and Ap_{k-1} around their bricks; the partial sums alternate
+// between two sets for the same reason.
+// Streams per iteration: r_{k-2}, Ap_{k-1}, p_{k-1} read, r_{k-1}, p_k, Ap_k
+// written, x every second pass (read x, p_{k-2}; write x): 7.5 x 8 B/dof.
+// ---------------------------------------------------------------------------
+// planes in flight ahead of i+1 (two: the three rings of 9 slots fit the
+// smem of the two-ring kernel with three, and leave the same L1 carveout)
+#ifndef MQ_NAHEAD1
+#define MQ_NAHEAD1 2
+#endif
+constexpr int NA1 = MQ_NAHEAD1, NR1 = NA1 + 3, NP1 = NA1;
+constexpr size_t kTmaSmem1 = sizeof(Box3) * (NR1 + 2 * NP1) + 128;
+
+struct TmaPcg1Args {
+  TmaPcgArgs t;
+  CUtensorMap tm_r2, tm_a, tm_a2;  // r of odd j (a.r2); Ap of even (a.ap) / odd (a.ap2) j
+};
+
+__global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __grid_constant__ TmaPcg1Args A1) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t bars[NR1];
+  __shared__ double red[5 * kWarps];
+  __shared__ double tot[5];
+  const TmaPcgArgs &A = A1.t;
+  const StencilPcgArgs &a = A.a;
+  const BrickGeo &g = A.g;
+  const int G = gridDim.x;
+  const Lay &L = a.L;
+  const double dg = a.dg, of = a.of, inv = a.inv;
+  const bool jac = a.use_jac != 0;
+  double *x = a.x, *r = a.r;
+  const double *b = a.b;
+  const int x0_mode = a.x0_mode_dev ? *a.x0_mode_dev : a.x0_mode;
+  if (a.err_word && *((volatile const unsigned int *)a.err_word)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      PcgOut o{};
+      o.status = 99;
+      *a.out = o;
+    }
+    return;
+  }
+  MarchCtx mc;
+  mc.sr = reinterpret_cast<Box3 *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sp = mc.sr + NR1;
+  mc.sa = mc.sp + NP1;
+  mc.bars = bars;
+  mc.ph = 0u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NR1; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned long long *trace = (blockIdx.x == 0 && threadIdx.x == 0) ? a.trace : nullptr;
+  auto stamp = [&](int slot) {
+    if (trace && slot < 4 * 64 + 1) trace[slot] = globaltimer_ns();
+  };
+  stamp(0);
+  // ---- initial residual (krylov.py:209-218), as in pcg_tma_kernel ----
+  double v3[3] = {0.0, 0.0, 0.0};
+  if (x0_mode == 1) {
+    for (int bi = blockIdx.x; bi < g.nbricks; bi += G) {
+      int i0, i1, j0, k0;
+      brick_of(g, bi, i0, i1, j0, k0);
+      march_tma<kInit, NA1>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
+                       [&](int c, int64_t e, auto V, double) {
+                         const double bv = __ldcg(b + e);
+                         const double rv = sub(bv, stencil3(c, dg, of, V));
+                         r[e] = rv;
+                         const double z = jac ? mul(inv, rv) : rv;
+                         v3[0] = add(v3[0], mul(bv, bv));
+                         v3[1] = add(v3[1], mul(rv, rv));
+                         v3[2] = add(v3[2], mul(rv, z));
+                       });
+    }
+  } else {
+    flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
+      double2 bv[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (u < n) bv[u] = __ldcg(reinterpret_cast<const double2 *>(b) + p + u * stride);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (u < n) {
+          reinterpret_cast<double2 *>(x)[p + u * stride] = make_double2(0.0, 0.0);
+          reinterpret_cast<double2 *>(r)[p + u * stride] = bv[u];
+          const double z0 = jac ? mul(inv, bv[u].x) : bv[u].x, z1 = jac ? mul(inv, bv[u].y) : bv[u].y;
+          v3[0] = add(v3[0], mul(bv[u].x, bv[u].x));
+          v3[0] = add(v3[0], mul(bv[u].y, bv[u].y));
+          v3[2] = add(v3[2], mul(bv[u].x, z0));
+          v3[2] = add(v3[2], mul(bv[u].y, z1));
+        }
+    });
+    v3[1] = v3[0];
+  }
+  block_sum<3>(v3, red);
+  if (threadIdx.x == 0) {
+    a.partials[0 * G + blockIdx.x] = v3[0];
+    a.partials[1 * G + blockIdx.x] = v3[1];
+    a.partials[2 * G + blockIdx.x] = v3[2];
+  }
+  int status = MQ_OK, iters = 0, converged = 0;
+  double rel = 0.0, bnorm = 0.0, alpha = 0.0, rz = 0.0;
+  bool pold_is_a = true;  // pold = pa, pnew = pb
+  int applies = (x0_mode == 2) ? 0 : 1;
+  if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
+  if (threadIdx.x == 0) fence_proxy_async_global();
+  {
+    double s3[3];
+    grid_partials_sum<3>(a.partials, G, s3, tot);
+    bnorm = sqrt(s3[0]);
+    const double target = fmax(a.rel_tol * bnorm, a.abs_tol);
+    double rnorm = sqrt(s3[1]);
+    rz = jac ? s3[2] : s3[1];
+    auto relf = [&](double res) { return bnorm > 0.0 ? res / bnorm : (res == 0.0 ? 0.0 : INFINITY); };
+    rel = relf(rnorm);
+    if (rnorm <= target) { converged = 1; goto done; }
+    if (a.max_iter < 1) { status = MQ_NOT_CONVERGED; goto done; }
+    double beta = 0.0, alpha_prev = 0.0, alpha_prev2 = 0.0;
+    bool pend = false;  // deferred x update, as in pcg_tma_kernel
+    int xmode = 0;
+    const int tid = threadIdx.x, ty = tid >> 5, tx = tid & 31;
+    for (int it = 1;; ++it) {
+      const bool first = it == 1;
+      double *pnew = pold_is_a ? a.pb : a.pa;
+      const CUtensorMap *mp = pold_is_a ? &A.tm_pa : &A.tm_pb;
+      // r_j in (r, r2), Ap_j in (ap, ap2) by the parity of j
+      const CUtensorMap *mr = (!first && (it & 1)) ? &A1.tm_r2 : &A.tm_r;  // r_{it-2} (r_0 when first)
+      mc.ma = ((it - 1) & 1) ? &A1.tm_a2 : &A1.tm_a;                          // Ap_{it-1}
+      mc.rout = ((it - 1) & 1) ? a.r2 : a.r;                                   // r_{it-1}
+      double *apw = (it & 1) ? a.ap2 : a.ap;                                   // Ap_it
+      mc.crr = 0.0;
+      mc.crz = 0.0;
+      xmode = 0;
+      if (!first) {
+#if MQ_XDEFER
+        xmode = pend ? 2 : 0;
+        pend = !pend;
+#else
+        xmode = 1;
+#endif
+      }
+      double v[3] = {0.0, 0.0, 0.0};
+      for (int bi = blockIdx.x; bi < g.nbricks; bi += G) {
+        int i0, i1, j0, k0;
+        brick_of(g, bi, i0, i1, j0, k0);
+        march_tma<kK1R, NA1>(mc, A, mr, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0,
+                        [&](int, int64_t e, double av, double own, double rown) {
+                          apw[e] = av;
+                          v[0] = add(v[0], mul(own, av));
+                          v[1] = add(v[1], mul(rown, av));
+                          v[2] = add(v[2], mul(av, av));
+                        });
+      }
+      double v5[5] = {v[0], v[1], v[2], mc.crr, mc.crz};
+      block_sum<5>(v5, red);
+      double *pt = a.partials + 3 * G + (it & 1) * 5 * G;
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) pt[q * G + blockIdx.x] = v5[q];
+      }
+      ++applies;
+      stamp(4 * (it - 1) + 1);
+      if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
+      stamp(4 * (it - 1) + 2);
+      stress_after_barrier(a.stress_ns, it);
+      if (threadIdx.x == 0) fence_proxy_async_global();
+      double s5[5];
+      {
+        // warp q < 5 sums partial row q in a fixed order (identical in every CTA)
+        if (ty < 5) {
+          double pv[kPB];
+#pragma unroll
+          for (int u = 0; u < kPB; ++u) {
+            const int bb = tx + 32 * u;
+            pv[u] = bb < G ? __ldcg(pt + (int64_t)ty * G + bb) : 0.0;
+          }
+          double sacc = 0.0;
+#pragma unroll
+          for (int u = 0; u < kPB; ++u)
+            if (tx + 32 * u < G) sacc = add(sacc, pv[u]);
+          for (int bb = tx + 32 * kPB; bb < G; bb += 32) sacc = add(sacc, __ldcg(pt + (int64_t)ty * G + bb));
+          sacc = warp_sum(sacc);
+          if (tx == 0) tot[ty] = sacc;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 5; ++q) s5[q] = tot[q];
+        __syncthreads();
+      }
+      stamp(4 * (it - 1) + 3);
+      stamp(4 * (it - 1) + 4);
+      if (!first) {
+        // the test of iteration it-1 (krylov.py:239-246) on r_{it-1}; this
+        // pass is then discarded
+        rnorm = sqrt(s5[3]);
+        iters = it - 1;
+        rel = relf(rnorm);
+        if (rnorm <= target) { converged = 1; --applies; break; }
+        const double rz_d = jac ? s5[4] : s5[3];
+        if (!isfinite(rz_d)) { status = MQ_INDEFINITE; break; }
+        rz = rz_d;
+        if (it - 1 >= a.max_iter) { --applies; break; }  // budget spent: iters == max_iter
+      }
+      const double pap = s5[0];
+      if (!isfinite(pap) || pap <= 0.0) { status = MQ_INDEFINITE; iters = it; break; }
+      alpha = rz / pap;
+      {
+        // beta from the extrapolated r.z of r_it
+        const double rr_new = add(sub(s5[3], mul(mul(2.0, alpha), s5[1])), mul(mul(alpha, alpha), s5[2]));
+        const double rz_new = jac ? mul(inv, rr_new) : rr_new;
+        beta = rz_new > 0.0 ? rz_new / rz : 0.0;
+      }
+      alpha_prev2 = alpha_prev;
+      alpha_prev = alpha;
+      pold_is_a = !pold_is_a;
+    }
+    if (status == MQ_OK) {
+      // the pass that read the final test ran with xmode 2 (x complete) or 0:
+      // x += alpha_K p_K pending, p_K = that pass's p_old
+      if (xmode == 0) {
+        const double *pdir = pold_is_a ? a.pa : a.pb;
+        const double aK = alpha;
+        flat_pairs(L.total, [&](int64_t p, int64_t stride, int n) {
+          double2 xv[kUnroll], pv[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u)
+            if (u < n) {
+              xv[u] = __ldcg(reinterpret_cast<const double2 *>(x) + p + u * stride);
+              pv[u] = __ldcg(reinterpret_cast<const double2 *>(pdir) + p + u * stride);
+            }
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u)
+            if (u < n)
+              reinterpret_cast<double2 *>(x)[p + u * stride] =
+                  make_double2(add(xv[u].x, mul(aK, pv[u].x)), add(xv[u].y, mul(aK, pv[u].y)));
         });
       }
       if (!converged) status = MQ_NOT_CONVERGED;
@@ -1207,12 +1520,28 @@ static BrickGeo make_geo(int nx, int ny, int nz, int resident) {
 // stores of K1 throttle (ncu stall_lg 0.61 -> 1.53 per issue) and an iteration
 // at 128^3 takes 104 instead of 94 us; left to the driver the carveout
 // sometimes fits only one CTA per SM (118 us).  MQ_PCG_CARVEOUT overrides.
-static cudaError_t two_cta_carveout(const void *fn, int want = 2) {
+// One grid barrier per iteration (pcg_tma1_kernel) for bricks of <= 64
+// planes, two (pcg_tma_kernel) for longer ones: measured at 128^3 (32-plane
+// bricks) 84.0 vs 86.6 us per iteration, at 256^3 (256-plane bricks) 657 vs
+// 642 -- the one-barrier pass is the whole iteration, and the imbalance
+// between CTAs alone on an SM and CTAs sharing one grows with the brick,
+// where the two-barrier kernel's flat K2 pass is balanced.  MQ_PCG_SYNC=1|2
+// forces either; read per launch.
+static bool tma_one_barrier(const BrickGeo &g) {
+  if (const char *v = getenv("MQ_PCG_SYNC")) {
+    const int k = atoi(v);
+    if (k == 1 || k == 2) return k == 1;
+  }
+  return (g.nx + g.chunks - 1) / g.chunks <= 64;
+}
+bool tma_single_reduction(const BrickGeo &g) { return tma_one_barrier(g); }
+
+static cudaError_t two_cta_carveout(const void *fn, int want = 2, size_t smem = kTmaSmem) {
   int pct = 100;
   for (int c = 50; c <= 100; ++c) {
     int per2 = 0;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, c);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, fn, kBlock, kTmaSmem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, fn, kBlock, smem);
     if (e != cudaSuccess) return e;
     if (per2 >= want) { pct = c; break; }
   }
@@ -1228,10 +1557,13 @@ int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int sm_cap, int *grid,
   MQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (sm_cap > 0 && sm_cap < sms) sms = sm_cap;
   MQ_CUDA(cudaFuncSetAttribute(pcg_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+  MQ_CUDA(cudaFuncSetAttribute(pcg_tma1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem1));
   MQ_CUDA(cudaFuncSetAttribute(kn_apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
   MQ_CUDA(two_cta_carveout((const void *)pcg_tma_kernel, MQ_TMA_MINB));
+  MQ_CUDA(two_cta_carveout((const void *)pcg_tma1_kernel, MQ_TMA_MINB, kTmaSmem1));
   MQ_CUDA(two_cta_carveout((const void *)kn_apply_tma_kernel));
   MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pcg_tma_kernel, kBlock, kTmaSmem));
+  static_assert(kTmaSmem1 <= kTmaSmem, "both TMA PCG kernels place as many CTAs per SM");
   if (getenv("MQ_PCG_VERBOSE")) fprintf(stderr, "pcg_tma_kernel: %d CTAs per SM, %zu B smem\n", per, kTmaSmem);
   if (per < 1) { set_error("TMA PCG kernel cannot be resident"); return MQ_CUDA_ERROR; }
   if (const char *v = getenv("MQ_BRICK_CTAS_PER_SM")) {
@@ -1256,6 +1588,18 @@ int launch_pcg_brick(const StencilPcgArgs &args, const BrickGeo &geo, int grid, 
   rc = rc ? rc : make_vec_map(L, geo.nx, geo.ny, geo.nz, args.x, &A.tm_x);
   if (rc) return rc;
   MQ_CUDA(cudaMemsetAsync(&args.bar->count, 0, sizeof(unsigned long long), s));
+  if (tma_one_barrier(geo) && args.r2 && args.ap2) {
+    TmaPcg1Args A1;
+    std::memset(&A1, 0, sizeof(A1));
+    A1.t = A;
+    rc = make_vec_map(L, geo.nx, geo.ny, geo.nz, args.r2, &A1.tm_r2);
+    rc = rc ? rc : make_vec_map(L, geo.nx, geo.ny, geo.nz, args.ap, &A1.tm_a);
+    rc = rc ? rc : make_vec_map(L, geo.nx, geo.ny, geo.nz, args.ap2, &A1.tm_a2);
+    if (rc) return rc;
+    void *params[] = {&A1};
+    MQ_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_tma1_kernel, dim3(grid), dim3(kBlock), params, kTmaSmem1, s));
+    return MQ_OK;
+  }
   void *params[] = {&A};
   MQ_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_tma_kernel, dim3(grid), dim3(kBlock), params, kTmaSmem, s));
   return MQ_OK;

@@ -1653,6 +1653,7 @@ static int solve_enqueue(mq_ctx *ctx, int fam, const double *rhs, double *y, boo
   a.pb = ctx->d_p1;
   a.ap = ctx->d_ap;
   a.ap2 = ctx->d_ap2;
+  a.r2 = ctx->d_r2;
   a.stress_ns = pcg_stress_ns();
   a.rel_tol = s->cfg.rel_tol;
   a.abs_tol = s->cfg.abs_tol;
@@ -2857,7 +2858,7 @@ __global__ void k_guard(Lay L, const uint32_t *__restrict__ mask, const double *
 extern "C" int mq_guard_check(mq_ctx *ctx, int64_t *bad_entries, int32_t *bad_vectors, int32_t *checked) {
   if (!ctx || !bad_entries || !bad_vectors) { set_error("NULL argument"); return MQ_INVALID; }
   MQ_CUDA(cudaSetDevice(ctx->device));
-  std::vector<const double *> vs = {ctx->d_r, ctx->d_p0, ctx->d_p1, ctx->d_ap, ctx->d_ap2};
+  std::vector<const double *> vs = {ctx->d_r, ctx->d_p0, ctx->d_p1, ctx->d_ap, ctx->d_ap2, ctx->d_r2};
   for (double *p : ctx->vecs) vs.push_back(p);
   if (SolverHost *s = ctx->solver) {
     for (int f = 0; f < 3; ++f) {

@@ -797,10 +797,10 @@ def test_ensemble_member_first_steps(gpu_ok):
         assert rel(res.a_c_history[i], tr.a_c[i + 1]) <= REL_FIELD
 
 
-@pytest.mark.parametrize("variant", ["simple", "brick", "resident", "resident2"])
+@pytest.mark.parametrize("variant", ["simple", "brick", "brick2", "resident", "resident2"])
 def test_pcg_kernel_variants_agree(gpu_ok, variant, monkeypatch):
     """All fused-PCG kernels (thread-per-row, TMA brick, shared-memory
-    resident with one or -- MQ_PCG_SYNC=2 -- two grid reductions per
+    resident, each with one or -- MQ_PCG_SYNC=2 -- two grid reductions per
     iteration) solve the same system like the oracle; they differ only in the
     dot-product summation order (and, single-reduction, beta from the
     extrapolated r.z)."""
@@ -824,22 +824,25 @@ def test_pcg_kernel_variants_agree(gpu_ok, variant, monkeypatch):
                 assert rel(x, ref.x) <= 1e-8
 
 
-@pytest.mark.parametrize("sync", ["1", "2"])
-def test_resident_pcg_semantics(gpu_ok, sync, monkeypatch):
-    """64^3 (shared-memory resident kernel, one or two reductions per
-    iteration): krylov.py's budget exhaustion, exact start vector, zero rhs and
-    application counts, against the oracle.  The single-reduction kernel reads
-    the stopping test one barrier late; the counts must not see it."""
+@pytest.mark.parametrize("kernel,sync", [("resident", "1"), ("resident", "2"), ("brick", "1"), ("brick", "2")])
+def test_resident_pcg_semantics(gpu_ok, kernel, sync, monkeypatch):
+    """64^3 (shared-memory resident and TMA brick kernels, one or two
+    reductions per iteration): krylov.py's budget exhaustion, exact start
+    vector, zero rhs and application counts, against the oracle.  The
+    single-reduction kernels read the stopping test one barrier late; the
+    counts must not see it."""
     from paper_1611_06721_b200 import PcgConfig, Preconditioner, pcg_solve
     from paper_1611_06721_b200 import configs as C
     from paper_1611_06721_b200.device import DeviceGrid
-    monkeypatch.setenv("MQ_PCG_KERNEL", "resident")
+    monkeypatch.setenv("MQ_PCG_KERNEL", kernel)
     monkeypatch.setenv("MQ_PCG_SYNC", sync)
     spec, m = oracle_model(1)
     inv = O.jacobi_inverse(m.kn.diagonal())
     with DeviceGrid(C.make_problem(1)) as g:
         name, _ = g.pcg_kernel()
-        assert name.startswith("pcg_resident1_kernel" if sync == "1" else "pcg_resident_kernel"), name
+        want = {("resident", "1"): "pcg_resident1_kernel", ("resident", "2"): "pcg_resident_kernel",
+                ("brick", "1"): "pcg_tma1_kernel", ("brick", "2"): "pcg_tma_kernel"}[(kernel, sync)]
+        assert name.startswith(want), name
         op = g.kn_operator()
         jac = Preconditioner.JACOBI
         for budget in (1, 2, 3):
@@ -861,7 +864,7 @@ def test_resident_pcg_semantics(gpu_ok, sync, monkeypatch):
         assert rep2.iterations == 0 and rep2.applications == 1 and np.array_equal(x2, x)
 
 
-@pytest.mark.parametrize("kernel,sync", [("resident", "1"), ("resident", "2"), ("brick", "2")])
+@pytest.mark.parametrize("kernel,sync", [("resident", "1"), ("resident", "2"), ("brick", "1"), ("brick", "2")])
 def test_pcg_barrier_stress(gpu_ok, kernel, sync, monkeypatch):
     """Race check of the persistent kernels' halo exchange: with MQ_PCG_STRESS a
     pseudo-random subset of CTAs sleeps 20 us after every grid barrier, so
