@@ -140,15 +140,18 @@ def dist_init():
     if world > 1:
         import torch
         import torch.distributed as dist
+        import datetime
+        # ranks wait in collectives while rank 0 runs its single-GPU legs
+        timeout = datetime.timedelta(minutes=60)
         if os.environ.get("MQ_BENCH_PLUMBING_TEST"):
             # functional check of the multi-rank path on a one-GPU box (every
             # rank on cuda:0, gloo): never a measurement
             local = 0
             torch.cuda.set_device(0)
-            dist.init_process_group("gloo")
+            dist.init_process_group("gloo", timeout=timeout)
             return world, rank, local, dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), timeout=timeout)
         return world, rank, local, dist
     return 1, 0, 0, None
 
@@ -539,6 +542,9 @@ def cfg_pcg_roofline(index, hbm_peak, reps=2):
             "bytes_per_launch": byts, "bytes_per_iteration": 72.0 * n_n}
 
 
+SHARDED_DEADLINE_S = 600
+
+
 def cfg4_sharded(dist, world, local, hbm_peak, warmup=1, steps=2):
     """configs[4] (256^3, Brauer, CSPE k = 5) with the sharded step over the
     ranks of this job (slabstep.py: one i-slab per rank and GPU, fused slab
@@ -669,13 +675,6 @@ def run_device_arm(args):
                 "algorithmic_bytes": "72 B per dof per iteration (9 fp64 streams) + 32 B/dof initial residual "
                                      "+ 24 B/dof final x update per launch (pcg_launch_bytes)"}
     op.grid.close()
-    sharded = None
-    if not args.skip_cfg4:
-        try:
-            sharded = cfg4_sharded(dist, world, local, hbm_peak)
-        except Exception as exc:  # noqa: BLE001  (reported, never silently dropped)
-            sharded = {"workload": "cfg4_256cube_two_blocks_cspe5_sharded", "ranks": world,
-                       "error": f"{type(exc).__name__}: {exc}"}
     ens = None
     if not args.skip_secondary:
         ens = ensemble_members(dist, world, rank, local)
@@ -719,7 +718,7 @@ def run_device_arm(args):
             "cfg1_pod_steps": cfg1_pod,
             "roofline_cfg4_1gpu": roof4,
             "cfg4_steps_1gpu": steps4,
-            "cfg4_sharded": sharded,
+            "cfg4_sharded": None,
             "cfg3_ensemble": ens,
             "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "explicit_euler_step + recover_an + probe_b (host arrays)",
@@ -727,6 +726,32 @@ def run_device_arm(args):
             "gpu_launches": launches,
             "cpu_baseline": cpu,
         }
+    # configs[4] sharded over the job's ranks, last and under a watchdog: with
+    # N > 1 its slab PCG waits on the peer GPUs (CUDA IPC, device mailboxes
+    # with a 5 s watchdog of their own), and a rank that fails while the
+    # others sit in a collective would otherwise hold the job -- on expiry
+    # rank 0 prints the line with the leg marked and every rank exits
+    if not args.skip_cfg4:
+        leg = {"workload": "cfg4_256cube_two_blocks_cspe5_sharded", "ranks": world}
+
+        def expire():
+            if line is not None:
+                line["cfg4_sharded"] = dict(leg, error=f"watchdog: not done after {SHARDED_DEADLINE_S} s")
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+
+        dog = threading.Timer(SHARDED_DEADLINE_S, expire)
+        dog.daemon = True
+        dog.start()
+        barrier(dist)
+        try:
+            sharded = cfg4_sharded(dist, world, local, hbm_peak)
+        except Exception as exc:  # noqa: BLE001  (reported, never silently dropped)
+            sharded = dict(leg, error=f"{type(exc).__name__}: {exc}")
+        dog.cancel()
+        if line is not None:
+            line["cfg4_sharded"] = sharded
+    if line is not None:
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

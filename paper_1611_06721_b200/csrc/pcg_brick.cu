@@ -1035,6 +1035,14 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
       }
       ++applies;
       stamp(4 * (it - 1) + 1);
+#ifdef MQ_TRACE_SPREAD
+      if (a.trace && threadIdx.x == 0 && it == 10 && blockIdx.x < 512) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.trace[1024 + blockIdx.x] = globaltimer_ns();
+        a.trace[1536 + blockIdx.x] = smid;
+      }
+#endif
       if (!grid_sync(a.bar)) { status = MQ_CUDA_ERROR; goto done; }
       stamp(4 * (it - 1) + 2);
       stress_after_barrier(a.stress_ns, it);

@@ -188,9 +188,11 @@ class TorchComm:
 
     def __init__(self, dist, device=None):
         self.dist = dist
-        self.device = device
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
+        # gloo moves host memory only: device planes are staged through the host
+        self.host_staged = dist.get_backend() == "gloo"
+        self.device = "cpu" if self.host_staged else device
 
     def allreduce(self, parts):
         import torch
@@ -201,23 +203,36 @@ class TorchComm:
 
     def exchange(self, slabs, names):
         (s,) = slabs
-        ops = []
+        ops, land = [], []
         P2P = self.dist.P2POp
+
+        def out(t):
+            return t.cpu() if self.host_staged and t.is_cuda else t
+
+        def into(t):
+            if self.host_staged and t.is_cuda:
+                h = t.new_empty(t.shape, device="cpu")
+                land.append((t, h))
+                return h
+            return t
+
         for name in names:
             send, ghost = s.send_planes(name), s.ghost_planes(name)
             if self.rank > 0:
                 for t in send["lo"]:
-                    ops.append(P2P(self.dist.isend, t, self.rank - 1))
+                    ops.append(P2P(self.dist.isend, out(t), self.rank - 1))
                 for t in ghost["lo"]:
-                    ops.append(P2P(self.dist.irecv, t, self.rank - 1))
+                    ops.append(P2P(self.dist.irecv, into(t), self.rank - 1))
             if self.rank + 1 < self.world:
                 for t in send["hi"]:
-                    ops.append(P2P(self.dist.isend, t, self.rank + 1))
+                    ops.append(P2P(self.dist.isend, out(t), self.rank + 1))
                 for t in ghost["hi"]:
-                    ops.append(P2P(self.dist.irecv, t, self.rank + 1))
+                    ops.append(P2P(self.dist.irecv, into(t), self.rank + 1))
         if ops:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
+        for t, h in land:
+            t.copy_(h)
         if hasattr(s, "sync_torch"):
             s.sync_torch()
 

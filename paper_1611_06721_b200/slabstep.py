@@ -185,7 +185,8 @@ class _Torch:
     def __init__(self, dist, device=None):
         self.dist = dist
         self.halo = TorchComm(dist, device)
-        self.device = device if device is not None else "cpu"
+        # gloo moves host memory only
+        self.device = "cpu" if (device is None or dist.get_backend() == "gloo") else device
         self.world = dist.get_world_size()
 
     def _gather(self, arr: np.ndarray) -> list[np.ndarray]:

@@ -1,7 +1,7 @@
 """K1 finish-time spread of the TMA PCG kernel across CTAs (load imbalance).
 
 Needs a -DMQ_TRACE_SPREAD build (tools/build_variant.py sp -DMQ_TRACE_SPREAD):
-    MQ_LIB_PATH=variants/sp.so MQ_PCG_TRACE=1 MQ_PCG_KERNEL=brick python tools/k1_spread.py
+    MQ_LIB_PATH=variants/sp.so MQ_PCG_TRACE=1 MQ_PCG_KERNEL=brick [MQ_PCG_SYNC=1] python tools/k1_spread.py
 Prints, for configs[2] and configs[4], the per-CTA %globaltimer at the end of
 K1 of iteration 10 relative to the earliest CTA.
 """
@@ -24,6 +24,13 @@ for cfg in (2, 4):
     t = st[1024:1024 + grid].astype(np.float64)
     t = (t - t.min()) / 1e3
     print(cfg, name, grid, "K1-end spread us: min 0 median %.2f p90 %.2f max %.2f" % (np.median(t), np.percentile(t, 90), t.max()))
-    # by SM sharing: first 148 CTAs vs rest
-    print("   first 148 CTAs median %.2f, last %d median %.2f" % (np.median(t[:148]), grid - 148, np.median(t[148:])))
+    sm = st[1536:1536 + grid].astype(np.int64)
+    if sm.any():  # pcg_tma1_kernel also records %smid: CTAs alone on their SM vs sharing one
+        cnt = np.bincount(sm)[sm]
+        lone, shared = t[cnt == 1], t[cnt >= 2]
+        print("   alone on an SM: %d CTAs, median %.2f max %.2f; sharing: %d CTAs, median %.2f max %.2f"
+              % (lone.size, np.median(lone) if lone.size else -1, lone.max() if lone.size else -1,
+                 shared.size, np.median(shared), shared.max()))
+    else:  # by launch order: first 148 CTAs vs rest
+        print("   first 148 CTAs median %.2f, last %d median %.2f" % (np.median(t[:148]), grid - 148, np.median(t[148:])))
     g.close()
