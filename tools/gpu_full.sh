@@ -9,3 +9,8 @@ python bench.py > gpurun_out/full/bench.log 2>&1
 echo "bench rc=$?" >> gpurun_out/full/bench.log
 tail -n 3 gpurun_out/full/tests.log gpurun_out/full/smoke.log
 tail -c 1500 gpurun_out/full/bench.log
+# launch list of the headline leg (per-launch times are cold-cache and serialised: shares only)
+timeout 1200 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/full/launches.csv python bench.py --steps 3 --warmup 3 --skip-secondary --skip-cpu --skip-cfg4 \
+  > gpurun_out/full/ncu.log 2>&1
+echo "ncu rc=$?"
