@@ -318,8 +318,9 @@ int mq_slab_final(mq_ctx *ctx, double *x_dev, double alpha, int32_t p_is_a);
 int mq_slab_fused_solve_local(mq_ctx **ctxs, int32_t nranks, const double *const *b, double *const *x,
                               int32_t x0_given, double rel_tol, double abs_tol, int32_t max_iter,
                               int32_t use_jacobi, mq_solve_report *report);
-/* One rank per process (one GPU each): exchange kIpcBufs (6) CUDA IPC
- * handles per rank (r, p_a, p_b, x, mailbox, counter; 64 bytes each) with
+/* One rank per process (one GPU each): exchange kIpcBufs (9) CUDA IPC
+ * handles per rank (r, p_a, p_b, x, mailbox, counter, r2, ap, ap2; 64 bytes
+ * each) with
  * mq_slab_ipc_export / an all-gather / mq_slab_ipc_import, then every rank
  * calls mq_slab_fused_solve_peer; the neighbours' ghost planes, mailboxes
  * and counters are written over NVLink by the kernel itself. */

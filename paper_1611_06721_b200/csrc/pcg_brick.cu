@@ -340,10 +340,12 @@ struct MarchCtx {
 
 struct NoPush {
   __device__ __forceinline__ void operator()(int, int, int64_t, double) const {}
+  __device__ __forceinline__ void operator()(int, int, int64_t, double, double) const {}
 };
 
 // push(q, c, jk, v): p_new of an own active position of plane q (jk = its
-// offset inside the padded plane), for the slab kernel's ghost stores
+// offset inside the padded plane), for the slab kernel's ghost stores;
+// kK1R: push(q, c, jk, v, r) with the position's r_{k-1} as well
 template <int MODE, int NAT = NA, class ROW, class PUSH = NoPush>
 __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, const CUtensorMap *mr,
                                           const CUtensorMap *mp, bool first, double beta, double alpha_prev,
@@ -476,7 +478,8 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       Sr[c][s_own] = raw[3 + c];
       if ((act >> c) & 1u) {
         pnew[c * L.C + qb + pos_own] = pv;
-        push(q, c, pos_own - L.Si, pv);
+        if constexpr (MODE == kK1R) push(q, c, pos_own - L.Si, pv, rq);
+        else push(q, c, pos_own - L.Si, pv);
         if (MODE == kK1R) {
           if (!first) mc.rout[c * L.C + qb + pos_own] = rq;
           mc.crr = add(mc.crr, mul(rq, rq));
@@ -511,7 +514,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 #pragma unroll
       for (int c = 0; c < 3; ++c)
         if ((act >> c) & 1u) {
-          if constexpr (MODE == kK1R) row(c, c * L.C + qb + pos_own, av[c], raw[c], raw[6 + c]);
+          if constexpr (MODE == kK1R) row(c, c * L.C + qb + pos_own, av[c], raw[c], raw[6 + c], i);
           else row(c, c * L.C + qb + pos_own, av[c], raw[c]);
         }
       return;
@@ -1019,7 +1022,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
         int i0, i1, j0, k0;
         brick_of(g, bi, i0, i1, j0, k0);
         march_tma<kK1R, NA1>(mc, A, mr, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0,
-                        [&](int, int64_t e, double av, double own, double rown) {
+                        [&](int, int64_t e, double av, double own, double rown, int) {
                           apw[e] = av;
                           v[0] = add(v[0], mul(own, av));
                           v[1] = add(v[1], mul(rown, av));
@@ -1400,6 +1403,213 @@ done:
   }
 }
 
+// One-barrier slab variant (pcg_tma1_kernel's recurrence on one i-slab per
+// rank): one rank all-reduce of [p.Ap, r.Ap, Ap.Ap, r.r, r.z] per iteration
+// instead of two.  The march stores r_{k-1} (convert), p_k (convert) and Ap_k
+// (row) of the planes 0 / n-1 into the neighbours' ghost planes of the
+// buffers of that parity; the next pass stages them through the halo.  x is
+// updated in every pass (x += alpha_{k-1} p_{k-1}), so the discarded pass that
+// reads the last test leaves x complete.  The default for every slab depth
+// (MQ_PCG_SYNC=2 selects pcg_tma_slab_kernel).
+struct TmaSlab1Group {
+  TmaPcg1Args t1;
+  SlabRank rk;
+};
+
+struct TmaSlab1Args {
+  TmaSlab1Group grp[kMaxRanks];
+  int ngroups, nranks, rank0;
+};
+
+__global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_slab_kernel(const __grid_constant__ TmaSlab1Args S) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t bars[NR1];
+  __shared__ double red[5 * kWarps];
+  __shared__ double tot[5];
+  const int Gr = gridDim.x / S.ngroups;
+  const int gi = blockIdx.x / Gr, lb = blockIdx.x % Gr;
+  const TmaPcg1Args &A1 = S.grp[gi].t1;
+  const TmaPcgArgs &A = A1.t;
+  const SlabRank &me = S.grp[gi].rk;
+  const int rank = S.rank0 + gi, R = S.nranks;
+  const StencilPcgArgs &a = A.a;
+  const BrickGeo &g = A.g;
+  const Lay &L = a.L;
+  const double dg = a.dg, of = a.of, inv = a.inv;
+  const bool jac = a.use_jac != 0;
+  double *x = a.x, *r = a.r;
+  const double *b = a.b;
+  const int x0_mode = a.x0_mode;
+  MarchCtx mc;
+  mc.sr = reinterpret_cast<Box3 *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sp = mc.sr + NR1;
+  mc.sa = mc.sp + NP1;
+  mc.bars = bars;
+  mc.ph = 0u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NR1; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned long long inst = *me.epoch;
+  int status = MQ_OK, iters = 0, converged = 0;
+  double rel = 0.0, bnorm = 0.0, alpha = 0.0, rz = 0.0;
+  bool pold_is_a = true;
+  int applies = (x0_mode == 2) ? 0 : 1;
+  double v3[3] = {0.0, 0.0, 0.0};
+  const int nmax = me.n - 1;
+  auto push_r = [&](int64_t e, double v) {  // own row e of r (init pass)
+    const int c = e < L.C ? 0 : (e < 2 * L.C ? 1 : 2);
+    const int64_t rel_e = e - c * L.C, plane = rel_e / L.Si, jk = rel_e - plane * L.Si;
+    if (plane == 1 && me.lo_r) me.lo_r[c * me.lo_C + me.lo_top + jk] = v;
+    if (plane == me.n && me.hi_r) me.hi_r[c * me.hi_C + jk] = v;
+  };
+  // ---- initial residual (krylov.py:209-218), as in pcg_tma_slab_kernel ----
+  if (x0_mode == 1) {
+    push_planes_group(me, x, me.lo_x, me.hi_x, lb, Gr);
+    double v0[1] = {0.0};
+    if (!rank_allreduce<1>(me, R, rank, lb, Gr, inst++, v0, red, tot)) { status = MQ_CUDA_ERROR; goto done; }
+    if (threadIdx.x == 0) fence_proxy_async_global();
+    for (int bi = lb; bi < g.nbricks; bi += Gr) {
+      int i0, i1, j0, k0;
+      brick_of(g, bi, i0, i1, j0, k0);
+      march_tma<kInit, NA1>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
+                            [&](int c, int64_t e, auto V, double) {
+                              const double bv = __ldcg(b + e);
+                              const double rv = sub(bv, stencil3(c, dg, of, V));
+                              r[e] = rv;
+                              push_r(e, rv);
+                              const double z = jac ? mul(inv, rv) : rv;
+                              v3[0] = add(v3[0], mul(bv, bv));
+                              v3[1] = add(v3[1], mul(rv, rv));
+                              v3[2] = add(v3[2], mul(rv, z));
+                            });
+    }
+  } else {
+    flat_pairs_owned(L, me.n, lb, Gr, [&](int64_t p, int64_t stride, int n) {
+      double2 bv[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (u < n) bv[u] = __ldcg(reinterpret_cast<const double2 *>(b) + p + u * stride);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (u < n) {
+          reinterpret_cast<double2 *>(x)[p + u * stride] = make_double2(0.0, 0.0);
+          reinterpret_cast<double2 *>(r)[p + u * stride] = bv[u];
+          const double z0 = jac ? mul(inv, bv[u].x) : bv[u].x, z1 = jac ? mul(inv, bv[u].y) : bv[u].y;
+          v3[0] = add(v3[0], mul(bv[u].x, bv[u].x));
+          v3[0] = add(v3[0], mul(bv[u].y, bv[u].y));
+          v3[2] = add(v3[2], mul(bv[u].x, z0));
+          v3[2] = add(v3[2], mul(bv[u].y, z1));
+        }
+    });
+    v3[1] = v3[0];
+    push_planes_group(me, r, me.lo_r, me.hi_r, lb, Gr);
+  }
+  if (!rank_allreduce<3>(me, R, rank, lb, Gr, inst++, v3, red, tot)) { status = MQ_CUDA_ERROR; goto done; }
+  if (threadIdx.x == 0) fence_proxy_async_global();
+  {
+    bnorm = sqrt(v3[0]);
+    const double target = fmax(a.rel_tol * bnorm, a.abs_tol);
+    double rnorm = sqrt(v3[1]);
+    rz = jac ? v3[2] : v3[1];
+    auto relf = [&](double res) { return bnorm > 0.0 ? res / bnorm : (res == 0.0 ? 0.0 : INFINITY); };
+    rel = relf(rnorm);
+    if (rnorm <= target) { converged = 1; goto done; }
+    if (a.max_iter < 1) { status = MQ_NOT_CONVERGED; goto done; }
+    double beta = 0.0, alpha_prev = 0.0;
+    for (int it = 1;; ++it) {
+      const bool first = it == 1;
+      double *pnew = pold_is_a ? a.pb : a.pa;
+      const CUtensorMap *mp = pold_is_a ? &A.tm_pa : &A.tm_pb;
+      const bool odd_r = (it - 1) & 1;  // r_{it-1} goes to r2 when odd
+      const bool odd_a = it & 1;        // Ap_it goes to ap2 when odd
+      const CUtensorMap *mr = (!first && (it & 1)) ? &A1.tm_r2 : &A.tm_r;
+      mc.ma = odd_r ? &A1.tm_a2 : &A1.tm_a;
+      mc.rout = odd_r ? a.r2 : a.r;
+      double *apw = odd_a ? a.ap2 : a.ap;
+      mc.crr = 0.0;
+      mc.crz = 0.0;
+      // neighbour pointers are read from the kernel parameters where they are
+      // used (no registers held across the march)
+      auto push = [&](int q, int c, int64_t jk, double v, double rv) {
+        if (q == 0 && me.lo_pa) {
+          const int64_t d = c * me.lo_C + me.lo_top + jk;
+          (pold_is_a ? me.lo_pb : me.lo_pa)[d] = v;
+          if (!first) (odd_r ? me.lo_r2 : me.lo_r)[d] = rv;
+        }
+        if (q == nmax && me.hi_pa) {
+          const int64_t d = c * me.hi_C + jk;
+          (pold_is_a ? me.hi_pb : me.hi_pa)[d] = v;
+          if (!first) (odd_r ? me.hi_r2 : me.hi_r)[d] = rv;
+        }
+      };
+      double v[3] = {0.0, 0.0, 0.0};
+      for (int bi = lb; bi < g.nbricks; bi += Gr) {
+        int i0, i1, j0, k0;
+        brick_of(g, bi, i0, i1, j0, k0);
+        march_tma<kK1R, NA1>(mc, A, mr, mp, first, beta, alpha_prev, first ? 0 : 1, 0.0, pnew, i0, i1, j0, k0,
+                             [&](int c, int64_t e, double av, double own, double rown, int i) {
+                               apw[e] = av;
+                               v[0] = add(v[0], mul(own, av));
+                               v[1] = add(v[1], mul(rown, av));
+                               v[2] = add(v[2], mul(av, av));
+                               if (i == 0 && me.lo_a) {
+                                 const int64_t jk = e - c * L.C - L.Si;
+                                 (odd_a ? me.lo_a2 : me.lo_a)[c * me.lo_C + me.lo_top + jk] = av;
+                               }
+                               if (i == nmax && me.hi_a) {
+                                 const int64_t jk = e - c * L.C - (int64_t)me.n * L.Si;
+                                 (odd_a ? me.hi_a2 : me.hi_a)[c * me.hi_C + jk] = av;
+                               }
+                             },
+                             push);
+      }
+      ++applies;
+      double v5[5] = {v[0], v[1], v[2], mc.crr, mc.crz};
+      if (!rank_allreduce<5>(me, R, rank, lb, Gr, inst++, v5, red, tot)) { status = MQ_CUDA_ERROR; goto done; }
+      stress_after_barrier(a.stress_ns, it);
+      if (threadIdx.x == 0) fence_proxy_async_global();
+      if (!first) {
+        // the test of iteration it-1 on r_{it-1}; this pass is then discarded
+        rnorm = sqrt(v5[3]);
+        iters = it - 1;
+        rel = relf(rnorm);
+        if (rnorm <= target) { converged = 1; --applies; break; }
+        const double rz_d = jac ? v5[4] : v5[3];
+        if (!isfinite(rz_d)) { status = MQ_INDEFINITE; break; }
+        rz = rz_d;
+        if (it - 1 >= a.max_iter) { --applies; break; }
+      }
+      const double pap = v5[0];
+      if (!isfinite(pap) || pap <= 0.0) { status = MQ_INDEFINITE; iters = it; break; }
+      alpha = rz / pap;
+      {
+        const double rr_new = add(sub(v5[3], mul(mul(2.0, alpha), v5[1])), mul(mul(alpha, alpha), v5[2]));
+        const double rz_new = jac ? mul(inv, rr_new) : rr_new;
+        beta = rz_new > 0.0 ? rz_new / rz : 0.0;
+      }
+      alpha_prev = alpha;
+      pold_is_a = !pold_is_a;
+    }
+    if (status == MQ_OK && !converged) status = MQ_NOT_CONVERGED;
+  }
+done:
+  if (lb == 0 && threadIdx.x == 0) {
+    *me.epoch = inst;
+    PcgOut o;
+    o.iterations = iters;
+    o.converged = converged;
+    o.status = status;
+    o.applies = applies;
+    o.rel = rel;
+    o.bnorm = bnorm;
+    o.alpha = alpha;
+    o.rz = rz;
+    *a.out = o;
+  }
+}
+
 // K_n SpMV through the same TMA march (y on active rows only).
 __global__ void __launch_bounds__(kBlock, 2) kn_apply_tma_kernel(const __grid_constant__ TmaPcgArgs A,
                                                                  double *__restrict__ y) {
@@ -1650,6 +1860,40 @@ int launch_pcg_tma_slab(const StencilPcgArgs *args, const SlabRank *ranks, const
       cudaError_t e = cudaMemsetAsync(&args[q].bar->count, 0, sizeof(unsigned long long), s);
       if (e != cudaSuccess) { rc = cuda_fail(e, "slab barrier reset"); break; }
     }
+  }
+  // one rank all-reduce per iteration unless MQ_PCG_SYNC=2 (measured faster
+  // at every slab depth: one GPU's slab of configs[4] split 1/2/4/8 ways,
+  // 687/343/181/100 -> 660/327/169/92 us per iteration), when the contexts
+  // carry the double buffers
+  const char *sv = getenv("MQ_PCG_SYNC");
+  bool one = !(sv && atoi(sv) == 2);
+  for (int q = 0; q < ngroups; ++q) one = one && args[q].r2 && args[q].ap2;
+  if (rc == MQ_OK && one) {
+    TmaSlab1Args *S1 = new TmaSlab1Args;
+    std::memset(S1, 0, sizeof(TmaSlab1Args));
+    S1->ngroups = ngroups;
+    S1->nranks = nranks;
+    S1->rank0 = rank0;
+    for (int q = 0; q < ngroups && rc == MQ_OK; ++q) {
+      TmaPcg1Args &t1 = S1->grp[q].t1;
+      t1.t = S->grp[q].t;
+      const Lay &L = args[q].L;
+      rc = make_vec_map(L, nplanes[q], ny, nz, args[q].r2, &t1.tm_r2);
+      rc = rc ? rc : make_vec_map(L, nplanes[q], ny, nz, args[q].ap, &t1.tm_a);
+      rc = rc ? rc : make_vec_map(L, nplanes[q], ny, nz, args[q].ap2, &t1.tm_a2);
+      S1->grp[q].rk = S->grp[q].rk;
+    }
+    if (rc == MQ_OK) {
+      MQ_CUDA(cudaFuncSetAttribute(pcg_tma1_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem1));
+      MQ_CUDA(two_cta_carveout((const void *)pcg_tma1_slab_kernel, 2, kTmaSmem1));
+      void *params[] = {S1};
+      cudaError_t e = cudaLaunchCooperativeKernel((const void *)pcg_tma1_slab_kernel, dim3(Gr * ngroups),
+                                                  dim3(kBlock), params, kTmaSmem1, s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "TMA slab PCG launch");
+    }
+    delete S1;
+    delete S;
+    return rc;
   }
   if (rc == MQ_OK) {
     void *params[] = {S};

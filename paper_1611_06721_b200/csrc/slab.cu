@@ -184,6 +184,9 @@ int mq_ctx_create_slab(const mq_grid_desc *desc, int32_t i_lo, int32_t i_hi, int
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_p0, sizeof(double) * t.L.total);
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_p1, sizeof(double) * t.L.total);
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_ap, sizeof(double) * t.L.total);
+  // double buffers of the one-barrier fused slab kernel (pcg_tma1_slab_kernel)
+  rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_ap2, sizeof(double) * t.L.total);
+  rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_r2, sizeof(double) * t.L.total);
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_tmp0, sizeof(double) * t.L.total);
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_tmp1, sizeof(double) * t.L.total);
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_partials, sizeof(double) * 8 * 1024);

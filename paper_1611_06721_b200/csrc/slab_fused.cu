@@ -205,7 +205,7 @@ static bool slab_use_tma() {
 
 static int fused_ready(mq_ctx *ctx) {
   if (ctx->d_mbox) return MQ_OK;
-  int rc = ctx_alloc(ctx, (void **)&ctx->d_mbox, sizeof(double) * kRing * kMaxRanks * 4);
+  int rc = ctx_alloc(ctx, (void **)&ctx->d_mbox, sizeof(double) * kRing * kMaxRanks * kMbW);
   rc = rc ? rc : ctx_alloc(ctx, (void **)&ctx->d_mcount, sizeof(unsigned long long) * 2);
   if (rc) return rc;
   MQ_CUDA(cudaMemsetAsync(ctx->d_mcount, 0, sizeof(unsigned long long) * 2, ctx->stream));
@@ -242,8 +242,12 @@ static void fill_rank(SlabRank &s, mq_ctx *ctx, const double *b, double *x) {
   s.epoch = ctx->d_mcount + 1;
 }
 
+// the one-barrier TMA slab kernel's double buffers (r of odd, Ap of both
+// iteration parities), allocated with the slab context
+static bool has_one_barrier_buffers(const mq_ctx *ctx) { return ctx->d_r2 && ctx->d_ap && ctx->d_ap2; }
+
 // ---- one rank per process: IPC-mapped neighbour buffers ------------------
-constexpr int kIpcBufs = 6;  // r, pa, pb, x, mailbox, counter
+constexpr int kIpcBufs = 9;  // r, pa, pb, x, mailbox, counter, r2, ap, ap2
 
 struct SlabPeer {
   SlabRank rk{};
@@ -303,6 +307,9 @@ int mq_slab_fused_solve_local(mq_ctx **ctxs, int32_t nranks, const double *const
       s.lo_r = lo->d_r;
       s.lo_pa = lo->d_p0;
       s.lo_pb = lo->d_p1;
+      s.lo_r2 = lo->d_r2;
+      s.lo_a = lo->d_ap;
+      s.lo_a2 = lo->d_ap2;
       s.lo_C = lo->topo.L.C;
       s.lo_top = (int64_t)(lo->topo.nx + 1) * lo->topo.L.Si;
     }
@@ -312,6 +319,9 @@ int mq_slab_fused_solve_local(mq_ctx **ctxs, int32_t nranks, const double *const
       s.hi_r = hi->d_r;
       s.hi_pa = hi->d_p0;
       s.hi_pb = hi->d_p1;
+      s.hi_r2 = hi->d_r2;
+      s.hi_a = hi->d_ap;
+      s.hi_a2 = hi->d_ap2;
       s.hi_C = hi->topo.L.C;
     }
   }
@@ -341,6 +351,8 @@ int mq_slab_fused_solve_local(mq_ctx **ctxs, int32_t nranks, const double *const
       t.pa = c->d_p0;
       t.pb = c->d_p1;
       t.ap = c->d_ap;
+      t.ap2 = c->d_ap2;
+      t.r2 = c->d_r2;
       t.rel_tol = rel_tol;
       t.stress_ns = pcg_stress_ns();
       t.abs_tol = abs_tol;
@@ -389,7 +401,9 @@ int mq_slab_fused_solve_local(mq_ctx **ctxs, int32_t nranks, const double *const
 int mq_slab_ipc_export(mq_ctx *ctx, const double *x_dev, void *handles_out) {
   int rc = fused_ready(ctx);
   if (rc) return rc;
-  const void *bufs[kIpcBufs] = {ctx->d_r, ctx->d_p0, ctx->d_p1, x_dev, ctx->d_mbox, ctx->d_mcount};
+  if (!has_one_barrier_buffers(ctx)) { set_error("slab context without the one-barrier buffers"); return MQ_INVALID; }
+  const void *bufs[kIpcBufs] = {ctx->d_r, ctx->d_p0, ctx->d_p1, x_dev, ctx->d_mbox, ctx->d_mcount,
+                                ctx->d_r2, ctx->d_ap, ctx->d_ap2};
   cudaIpcMemHandle_t *h = reinterpret_cast<cudaIpcMemHandle_t *>(handles_out);
   for (int q = 0; q < kIpcBufs; ++q) MQ_CUDA(cudaIpcGetMemHandle(&h[q], const_cast<void *>(bufs[q])));
   return MQ_OK;
@@ -412,7 +426,8 @@ int mq_slab_ipc_import(mq_ctx *ctx, int32_t rank, int32_t nranks, const void *al
   const cudaIpcMemHandle_t *h = reinterpret_cast<const cudaIpcMemHandle_t *>(all_handles);
   auto open = [&](int q, int k, void **out) -> int {
     if (q == rank) {
-      void *own[kIpcBufs] = {ctx->d_r, ctx->d_p0, ctx->d_p1, x_dev, ctx->d_mbox, ctx->d_mcount};
+      void *own[kIpcBufs] = {ctx->d_r, ctx->d_p0, ctx->d_p1, x_dev, ctx->d_mbox, ctx->d_mcount,
+                             ctx->d_r2, ctx->d_ap, ctx->d_ap2};
       *out = own[k];
       return MQ_OK;
     }
@@ -431,23 +446,31 @@ int mq_slab_ipc_import(mq_ctx *ctx, int32_t rank, int32_t nranks, const void *al
     s.mbox[q] = (double *)mb;
     s.mcount[q] = (unsigned long long *)mc;
   }
+  // neighbour buffers: r, pa, pb, x and the one-barrier r2, ap, ap2
+  const int nb[7] = {0, 1, 2, 3, 6, 7, 8};
   if (rc == MQ_OK && rank > 0) {
-    void *v[4];
-    for (int k = 0; k < 4 && rc == MQ_OK; ++k) rc = open(rank - 1, k, &v[k]);
+    void *v[7];
+    for (int k = 0; k < 7 && rc == MQ_OK; ++k) rc = open(rank - 1, nb[k], &v[k]);
     s.lo_r = (double *)v[0];
     s.lo_pa = (double *)v[1];
     s.lo_pb = (double *)v[2];
     s.lo_x = (double *)v[3];
+    s.lo_r2 = (double *)v[4];
+    s.lo_a = (double *)v[5];
+    s.lo_a2 = (double *)v[6];
     s.lo_C = comp_stride(nplanes[rank - 1]);
     s.lo_top = (int64_t)(nplanes[rank - 1] + 1) * L.Si;
   }
   if (rc == MQ_OK && rank + 1 < nranks) {
-    void *v[4];
-    for (int k = 0; k < 4 && rc == MQ_OK; ++k) rc = open(rank + 1, k, &v[k]);
+    void *v[7];
+    for (int k = 0; k < 7 && rc == MQ_OK; ++k) rc = open(rank + 1, nb[k], &v[k]);
     s.hi_r = (double *)v[0];
     s.hi_pa = (double *)v[1];
     s.hi_pb = (double *)v[2];
     s.hi_x = (double *)v[3];
+    s.hi_r2 = (double *)v[4];
+    s.hi_a = (double *)v[5];
+    s.hi_a2 = (double *)v[6];
     s.hi_C = comp_stride(nplanes[rank + 1]);
   }
   ctx->peer = P;
@@ -478,6 +501,8 @@ int mq_slab_fused_solve_peer(mq_ctx *ctx, const double *b, int32_t x0_given, dou
   t.pa = ctx->d_p0;
   t.pb = ctx->d_p1;
   t.ap = ctx->d_ap;
+  t.ap2 = ctx->d_ap2;
+  t.r2 = ctx->d_r2;
   t.rel_tol = rel_tol;
   t.stress_ns = pcg_stress_ns();
   t.abs_tol = abs_tol;

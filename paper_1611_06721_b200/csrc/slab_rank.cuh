@@ -10,6 +10,7 @@ namespace mq {
 
 constexpr int kMaxRanks = 8;
 constexpr int kRing = 8;
+constexpr int kMbW = 8;  // mailbox values per rank and slot (all-reduces of up to 8 sums)
 
 struct SlabRank {
   Lay L;
@@ -19,15 +20,17 @@ struct SlabRank {
   int n;  // owned planes
   // neighbour below (rank - 1): our plane 0 -> its top ghost plane (n_lo)
   double *lo_x, *lo_r, *lo_pa, *lo_pb;
+  double *lo_r2, *lo_a, *lo_a2;  // one-barrier kernel: r of odd, Ap of even / odd iterations
   int64_t lo_C, lo_top;
   // neighbour above (rank + 1): our plane n - 1 -> its bottom ghost plane (-1)
   double *hi_x, *hi_r, *hi_pa, *hi_pb;
+  double *hi_r2, *hi_a, *hi_a2;
   int64_t hi_C;
-  // all-reduce: every rank's mailbox [kRing][kMaxRanks][4] and counter
+  // all-reduce: every rank's mailbox [kRing][kMaxRanks][kMbW] and counter
   double *mbox[kMaxRanks];
   unsigned long long *mcount[kMaxRanks];
   unsigned long long *epoch;  // this rank's instances of earlier solves
-  double *partials;           // group partials, 6 * group size
+  double *partials;           // group partials, 2 sets x NV x group size
   GridBar *bar;               // group barrier
   PcgOut *out;
 };
@@ -85,20 +88,24 @@ __device__ __forceinline__ bool group_sync(GridBar *bar, int Gr) {
 template <int NV>
 __device__ bool rank_allreduce(const SlabRank &me, int nranks, int rank, int lb, int Gr, unsigned long long inst,
                                double (&v)[NV], double *red, double *tot) {
+  static_assert(NV <= kMbW, "mailbox width");
   block_sum<NV>(v, red);
+  // two alternating partial sets: a CTA that is already in the next
+  // all-reduce never overwrites values a slower CTA of the group still reads
+  double *pt = me.partials + (int64_t)(inst & 1ull) * NV * Gr;
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int q = 0; q < NV; ++q) me.partials[(int64_t)q * Gr + lb] = v[q];
+    for (int q = 0; q < NV; ++q) pt[(int64_t)q * Gr + lb] = v[q];
   }
   if (!group_sync(me.bar, Gr)) return false;
-  grid_partials_sum<NV>(me.partials, Gr, v, tot);  // rank total, identical in the group
+  grid_partials_sum<NV>(pt, Gr, v, tot);  // rank total, identical in the group
   const int R = nranks;
   if (R == 1) return true;  // a single rank: the group total is the total
   const int slot = (int)(inst % kRing);
   if (lb == 0 && threadIdx.x == 0) {
     for (int q = 0; q < R; ++q)
 #pragma unroll
-      for (int k = 0; k < NV; ++k) st_relaxed_sys_f64(me.mbox[q] + ((int64_t)slot * kMaxRanks + rank) * 4 + k, v[k]);
+      for (int k = 0; k < NV; ++k) st_relaxed_sys_f64(me.mbox[q] + ((int64_t)slot * kMaxRanks + rank) * kMbW + k, v[k]);
     for (int q = 0; q < R; ++q) red_add_release_sys(me.mcount[q], 1ull);
   }
   __shared__ int s_fail;
@@ -119,12 +126,12 @@ __device__ bool rank_allreduce(const SlabRank &me, int nranks, int rank, int lb,
   if (s_fail) return false;
   if (threadIdx.x == 0) {
     fence_acq_rel_sys();
-    const double *box = me.mbox[rank] + (int64_t)slot * kMaxRanks * 4;
+    const double *box = me.mbox[rank] + (int64_t)slot * kMaxRanks * kMbW;
     double val[kMaxRanks][NV];  // all loads in flight, then the rank-order sums
 #pragma unroll
     for (int q = 0; q < kMaxRanks; ++q)
 #pragma unroll
-      for (int k = 0; k < NV; ++k) val[q][k] = q < R ? ld_relaxed_sys_f64(box + q * 4 + k) : 0.0;
+      for (int k = 0; k < NV; ++k) val[q][k] = q < R ? ld_relaxed_sys_f64(box + q * kMbW + k) : 0.0;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       double s = 0.0;

@@ -30,7 +30,7 @@ from ._lib import check, dptr, f64
 __all__ = ["slab_range", "SlabGrid", "TorchComm", "LoopbackComm", "slab_pcg_solve", "fused_slab_pcg_solve_local",
            "gather_ipc_tables", "fused_peer_setup", "fused_peer_solve"]
 
-IPC_HANDLE_BYTES = 6 * 64  # r, p_a, p_b, x, mailbox, counter (cudaIpcMemHandle_t = 64 B)
+IPC_HANDLE_BYTES = 9 * 64  # r, p_a, p_b, x, mailbox, counter, r2, ap, ap2 (cudaIpcMemHandle_t = 64 B)
 
 
 def slab_range(nx: int, world: int, rank: int) -> tuple[int, int]:

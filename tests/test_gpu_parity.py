@@ -964,13 +964,17 @@ def test_slab_pcg_loopback_on_one_gpu(gpu_ok, world, x0_given):
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4])
 @pytest.mark.parametrize("x0_given", [False, True])
-def test_fused_slab_pcg_on_one_gpu(gpu_ok, world, x0_given):
-    """The fused per-rank slab kernel (ghost stores into the neighbour slab,
-    rank all-reduce through device mailboxes), its ranks emulated as the CTA
-    groups of one cooperative launch: solution vs the single-domain oracle,
-    iterations within +-1; repeated solves reuse the mailboxes (epochs)."""
+@pytest.mark.parametrize("sync", ["1", "2"])
+def test_fused_slab_pcg_on_one_gpu(gpu_ok, world, x0_given, sync, monkeypatch):
+    """The fused per-rank slab kernels (ghost stores into the neighbour slab,
+    rank all-reduce through device mailboxes; one all-reduce per iteration --
+    pcg_tma1_slab_kernel -- or, MQ_PCG_SYNC=2, two), their ranks emulated as
+    the CTA groups of one cooperative launch: solution vs the single-domain
+    oracle, iterations within +-1, application counts; repeated solves reuse
+    the mailboxes (epochs)."""
     from paper_1611_06721_b200 import configs as C
     from paper_1611_06721_b200.slab import SlabGrid, fused_slab_pcg_solve_local
+    monkeypatch.setenv("MQ_PCG_SYNC", sync)
     spec, m = oracle_model(0)
     prob = C.make_problem(0)
     slabs = [SlabGrid(prob, r, world) for r in range(world)]
@@ -996,13 +1000,15 @@ def test_fused_slab_pcg_on_one_gpu(gpu_ok, world, x0_given):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_fused_slab_barrier_stress(gpu_ok, world, monkeypatch):
+@pytest.mark.parametrize("sync", ["1", "2"])
+def test_fused_slab_barrier_stress(gpu_ok, world, sync, monkeypatch):
     """The fused slab kernel with some CTAs of every rank group delayed after
     each rank all-reduce (MQ_PCG_STRESS): ghost stores into the neighbours'
     slabs and the mailbox protocol depend on no timing, so x and the
     iteration count are bit-identical to the unstressed solve."""
     from paper_1611_06721_b200 import configs as C
     from paper_1611_06721_b200.slab import SlabGrid, fused_slab_pcg_solve_local
+    monkeypatch.setenv("MQ_PCG_SYNC", sync)
     spec, m = oracle_model(0)
     prob = C.make_problem(0)
     slabs = [SlabGrid(prob, r, world) for r in range(world)]
@@ -1029,13 +1035,15 @@ def test_fused_slab_barrier_stress(gpu_ok, world, monkeypatch):
         s.close()
 
 
-def test_fused_slab_peer_path_single_rank(gpu_ok):
+@pytest.mark.parametrize("sync", ["1", "2"])
+def test_fused_slab_peer_path_single_rank(gpu_ok, sync, monkeypatch):
     """The one-rank-per-process entry points (IPC export/import, the kernel
     launched as a single CTA group) at one rank: same answer as the oracle.
     (More ranks need more GPUs; the protocol is the one the emulated
     multi-group launches above exercise.)"""
     from paper_1611_06721_b200 import configs as C
     from paper_1611_06721_b200.slab import SlabGrid, fused_peer_setup, fused_peer_solve
+    monkeypatch.setenv("MQ_PCG_SYNC", sync)
     spec, m = oracle_model(0)
     s = SlabGrid(C.make_problem(0), 0, 1)
     fused_peer_setup(s)
