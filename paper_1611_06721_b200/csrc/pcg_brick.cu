@@ -333,6 +333,9 @@ struct MarchCtx {
   const CUtensorMap *ma = nullptr;
   double *rout = nullptr;
   double crr = 0.0, crz = 0.0;
+  // planes i0-1 .. of the next march's first brick already in flight
+  // (tma_preissue), skipped by its prologue
+  int pre = 0;
 #ifdef MQ_TRACE_MARCH
   unsigned long long *tr = nullptr;  // CTA 0 thread 0, one iteration: 4 stamps per plane step
 #endif
@@ -342,6 +345,61 @@ struct NoPush {
   __device__ __forceinline__ void operator()(int, int, int64_t, double) const {}
   __device__ __forceinline__ void operator()(int, int, int64_t, double, double) const {}
 };
+
+// The TMA loads of one staged plane q of a brick (tile origin j0, k0): the
+// r (or x) box, with_p: the p_old box and, kK1R, the Ap box, all on the
+// plane's r-slot mbarrier.  One thread.
+template <int MODE, int NAT>
+__device__ __forceinline__ void tma_issue_plane(MarchCtx &mc, const CUtensorMap *mr, const CUtensorMap *mp,
+                                                bool with_p, int q, int j0, int k0) {
+  constexpr int NRT = NAT + 3, NPT = NAT;
+  const int s = (q + NRT) % NRT, sp = (q + NPT) % NPT;
+  const uint32_t bytes = (with_p ? (MODE == kK1R ? 9u : 6u) : 3u) * HP * 8u;
+  fence_proxy_async_smem();
+  mbar_expect_tx(&mc.bars[s], bytes);
+  // box origin (k0-1, j0-1, q) in node coordinates = (k0, j0, q+1) in the
+  // guard-shifted map: never negative
+#pragma unroll
+  for (int c = 0; c < 3; ++c) tma_load_4d(mc.sr[s].v[c], mr, &mc.bars[s], k0, j0, q + 1, c);
+  if (with_p) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) tma_load_4d(mc.sp[sp].v[c], mp, &mc.bars[s], k0, j0, q + 1, c);
+    if (MODE == kK1R) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) tma_load_4d(mc.sa[sp].v[c], mc.ma, &mc.bars[s], k0, j0, q + 1, c);
+    }
+  }
+}
+
+// The prologue loads of the next march (planes i0-1 .. i0+NAT-2 of brick
+// (i0, i1, j0, k0)) issued ahead, by thread `who`, right after the grid
+// barrier that makes their data visible -- their latency then overlaps the
+// partial-sum read.  Every thread records the count in mc.pre.
+template <int MODE, int NAT>
+__device__ __forceinline__ void tma_preissue(MarchCtx &mc, const CUtensorMap *mr, const CUtensorMap *mp,
+                                             bool with_p, int i0, int i1, int j0, int k0, int who) {
+  int n = 0;
+  for (int q = i0 - 1; q <= i0 + NAT - 2 && q <= i1; ++q) ++n;
+  if ((int)threadIdx.x == who) {
+    fence_proxy_async_global();
+    for (int q = i0 - 1; q < i0 - 1 + n; ++q) tma_issue_plane<MODE, NAT>(mc, mr, mp, with_p, q, j0, k0);
+  }
+  mc.pre = n;
+}
+
+// Wait out pre-issued loads that no march will consume (the solve ended at
+// this barrier): no bulk copy may still target the CTA's shared memory when
+// it exits.
+template <int NAT>
+__device__ __forceinline__ void tma_drain(MarchCtx &mc, int i0) {
+  constexpr int NRT = NAT + 3;
+  for (int q = i0 - 1; q < i0 - 1 + mc.pre; ++q) {
+    const int s = (q + NRT) % NRT;
+    mbar_wait(&mc.bars[s], (mc.ph >> s) & 1u);
+    mc.ph ^= (1u << s);
+  }
+  mc.pre = 0;
+}
 
 // push(q, c, jk, v): p_new of an own active position of plane q (jk = its
 // offset inside the padded plane), for the slab kernel's ghost stores;
@@ -369,7 +427,6 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   // 2 x = (x + a2 p_prev2) + a1 p_old with p_prev2 read from the p_new buffer
   // at the own position just before it is overwritten
   const int xm = (K1M && !first) ? xmode : 0;
-  const uint32_t bytes = (with_p ? (MODE == kK1R ? 9u : 6u) : 3u) * HP * 8u;
   // halo (slot, component) converted by this thread besides its own
   // position: the 84 halo positions x 3 components are spread over threads
   // 0..251, one each, so that no warp carries three times the work
@@ -390,23 +447,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   double *x = a.x;
 
   auto issue = [&](int q) {
-    if (tid == 0) {
-      const int s = rsl(q), sp = psl(q);
-      fence_proxy_async_smem();
-      mbar_expect_tx(&mc.bars[s], bytes);
-#pragma unroll
-      // box origin (k0-1, j0-1, q) in node coordinates = (k0, j0, q+1) in the
-      // guard-shifted map: never negative
-      for (int c = 0; c < 3; ++c) tma_load_4d(mc.sr[s].v[c], mr, &mc.bars[s], k0, j0, q + 1, c);
-      if (with_p) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) tma_load_4d(mc.sp[sp].v[c], mp, &mc.bars[s], k0, j0, q + 1, c);
-        if (MODE == kK1R) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) tma_load_4d(mc.sa[sp].v[c], mc.ma, &mc.bars[s], k0, j0, q + 1, c);
-        }
-      }
-    }
+    if (tid == 0) tma_issue_plane<MODE, NAT>(mc, mr, mp, with_p, q, j0, k0);
   };
   // Own-position mask words and x values are software-pipelined ahead in
   // registers: they are loaded while earlier planes are processed, so neither
@@ -538,7 +579,8 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 #ifdef MQ_TRACE_MARCH
   if (mc.tr) mc.tr[128] = globaltimer_ns();  // march entry
 #endif
-  for (int q = i0 - 1; q <= i0 + NAT - 2 && q <= last; ++q) issue(q);
+  for (int q = i0 - 1 + mc.pre; q <= i0 + NAT - 2 && q <= last; ++q) issue(q);
+  mc.pre = 0;
   prefetch_own(pa, i0, true);
   prefetch_own(pb, i0 - 1, false);
   convert(i0 - 1, false, pb, rwm);
@@ -887,6 +929,9 @@ done:
 #define MQ_NAHEAD1 2
 #endif
 constexpr int NA1 = MQ_NAHEAD1, NR1 = NA1 + 3, NP1 = NA1;
+#ifndef MQ_TMA_PREISSUE
+#define MQ_TMA_PREISSUE 1
+#endif
 constexpr size_t kTmaSmem1 = sizeof(Box3) * (NR1 + 2 * NP1) + 128;
 
 struct TmaPcg1Args {
@@ -997,6 +1042,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
     bool pend = false;  // deferred x update, as in pcg_tma_kernel
     int xmode = 0;
     const int tid = threadIdx.x, ty = tid >> 5, tx = tid & 31;
+    int pre_i0 = 0;  // first plane of the brick whose prologue is pre-issued
     for (int it = 1;; ++it) {
       const bool first = it == 1;
       double *pnew = pold_is_a ? a.pb : a.pa;
@@ -1050,6 +1096,18 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
       stamp(4 * (it - 1) + 2);
       stress_after_barrier(a.stress_ns, it);
       if (threadIdx.x == 0) fence_proxy_async_global();
+#if MQ_TMA_PREISSUE
+      // the next pass's first planes, in flight while the sums are read
+      // (its maps depend only on the iteration parity)
+      if ((int)blockIdx.x < g.nbricks) {
+        int i0, i1, j0, k0;
+        brick_of(g, blockIdx.x, i0, i1, j0, k0);
+        mc.ma = (it & 1) ? &A1.tm_a2 : &A1.tm_a;
+        tma_preissue<kK1R, NA1>(mc, ((it + 1) & 1) ? &A1.tm_r2 : &A.tm_r, pold_is_a ? &A.tm_pb : &A.tm_pa, true,
+                                i0, i1, j0, k0, 5 * 32);
+        pre_i0 = i0;
+      }
+#endif
       double s5[5];
       {
         // warp q < 5 sums partial row q in a fixed order (identical in every CTA)
@@ -1100,6 +1158,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
       alpha_prev = alpha;
       pold_is_a = !pold_is_a;
     }
+    if (mc.pre) tma_drain<NA1>(mc, pre_i0);
     if (status == MQ_OK) {
       // the pass that read the final test ran with xmode 2 (x complete) or 0:
       // x += alpha_K p_K pending, p_K = that pass's p_old
