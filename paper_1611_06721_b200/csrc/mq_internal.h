@@ -74,6 +74,10 @@ struct BrickGeo {
   int nx, ny, nz;
   int tiles_k, tiles_j, chunks;
   int nbricks;
+  // mixed chunking (make_geo, one-barrier kernel): tiles [0, xtiles) are cut
+  // into chunks + 1 i-chunks, the others into chunks; bricks [0, nbig) are
+  // the longer ones (0 / nbricks: every tile in `chunks`)
+  int xtiles, nbig;
 };
 
 struct CsrPcgArgs {

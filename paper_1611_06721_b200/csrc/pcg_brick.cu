@@ -34,7 +34,7 @@ namespace mq {
 
 constexpr int TJ = 8, TK = 32;                 // kBlock = TJ * TK threads
 constexpr int HJ = TJ + 2, HK = TK + 2, HP = HJ * HK;  // 10 x 34 box
-constexpr int BOXP = 352;                      // box slot padded to a 128-byte multiple
+constexpr int BOXP = HP;                       // one TMA box (34 x 10 x 1 x 3) fills a slot
 #ifndef MQ_XDEFER
 #define MQ_XDEFER 1
 #endif
@@ -57,17 +57,21 @@ constexpr int NA = MQ_NAHEAD;                  // planes in flight ahead of i+1
 constexpr int NR = NA + 3, NP = NA;            // r-ring and p-ring slots
 constexpr int NHALO = 2 * HK + 2 * TJ;         // 84 halo positions per plane
 static_assert(TJ * TK == kBlock, "one thread per tile position");
-static_assert(HP <= BOXP && (BOXP * 8) % 128 == 0, "TMA destination alignment");
+static_assert(HP <= BOXP, "box slot");
 static_assert(NA >= 1 && NR <= 32, "ring sizes");
 
+// One staged plane of one field, three components packed as the 4-D TMA box
+// (k, j, i, c) = (34, 10, 1, 3) lands: one bulk tensor load per field and
+// plane (three per plane for r, p_old, Ap instead of nine).
 struct __align__(128) Box3 {
-  double v[3][BOXP];  // one staged plane of one field, three components
+  double v[3][BOXP];
 };
+static_assert(sizeof(Box3) % 128 == 0, "TMA destination alignment");
 
 struct TmaPcgArgs {
   StencilPcgArgs a;
   BrickGeo g;
-  CUtensorMap tm_r, tm_pa, tm_pb, tm_x;  // 4-D maps (k, j, i, c), box 34 x 10 x 1 x 1
+  CUtensorMap tm_r, tm_pa, tm_pb, tm_x;  // 4-D maps (k, j, i, c), box 34 x 10 x 1 x 3
 };
 
 constexpr size_t kTmaSmem = sizeof(Box3) * (NR + NP) + 128;
@@ -107,14 +111,22 @@ __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void brick_of(const BrickGeo &g, int b, int &i0, int &i1, int &j0, int &k0) {
-  const int tk = b % g.tiles_k;
-  const int r = b / g.tiles_k;
-  const int tj = r % g.tiles_j;
-  const int ic = r / g.tiles_j;
-  k0 = tk * TK;
-  j0 = tj * TJ;
-  i0 = (int)(((int64_t)ic * g.nx) / g.chunks);
-  i1 = (int)(((int64_t)(ic + 1) * g.nx) / g.chunks);
+  const int tiles = g.tiles_k * g.tiles_j;
+  int tile, ic, nch;
+  if (b < g.nbig) {  // tiles [xtiles, tiles) in `chunks` i-chunks
+    tile = g.xtiles + b % (tiles - g.xtiles);
+    ic = b / (tiles - g.xtiles);
+    nch = g.chunks;
+  } else {  // tiles [0, xtiles) in chunks + 1
+    const int b2 = b - g.nbig;
+    tile = b2 % g.xtiles;
+    ic = b2 / g.xtiles;
+    nch = g.chunks + 1;
+  }
+  k0 = (tile % g.tiles_k) * TK;
+  j0 = (tile / g.tiles_k) * TJ;
+  i0 = (int)(((int64_t)ic * g.nx) / nch);
+  i1 = (int)(((int64_t)(ic + 1) * g.nx) / nch);
 }
 
 // K_n row in CSR column order on a 3-plane neighbourhood:
@@ -359,15 +371,10 @@ __device__ __forceinline__ void tma_issue_plane(MarchCtx &mc, const CUtensorMap 
   mbar_expect_tx(&mc.bars[s], bytes);
   // box origin (k0-1, j0-1, q) in node coordinates = (k0, j0, q+1) in the
   // guard-shifted map: never negative
-#pragma unroll
-  for (int c = 0; c < 3; ++c) tma_load_4d(mc.sr[s].v[c], mr, &mc.bars[s], k0, j0, q + 1, c);
+  tma_load_4d(mc.sr[s].v[0], mr, &mc.bars[s], k0, j0, q + 1, 0);
   if (with_p) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) tma_load_4d(mc.sp[sp].v[c], mp, &mc.bars[s], k0, j0, q + 1, c);
-    if (MODE == kK1R) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) tma_load_4d(mc.sa[sp].v[c], mc.ma, &mc.bars[s], k0, j0, q + 1, c);
-    }
+    tma_load_4d(mc.sp[sp].v[0], mp, &mc.bars[s], k0, j0, q + 1, 0);
+    if (MODE == kK1R) tma_load_4d(mc.sa[sp].v[0], mc.ma, &mc.bars[s], k0, j0, q + 1, 0);
   }
 }
 
@@ -1745,13 +1752,13 @@ static int get_encoder() {
 }
 
 // 4-D view (k, j, i, c) of a padded device vector including the guard layer
-// (coordinate 0 = node -1); box = tile + 1-node halo.
+// (coordinate 0 = node -1); box = tile + 1-node halo, all three components.
 int make_vec_map(const Lay &L, int nx, int ny, int nz, const double *base, CUtensorMap *map, int bk = HK, int bj = HJ) {
   int rc = get_encoder();
   if (rc) return rc;
   cuuint64_t dims[4] = {(cuuint64_t)nz + 2, (cuuint64_t)ny + 2, (cuuint64_t)nx + 2, 3};
   cuuint64_t strides[3] = {(cuuint64_t)L.Sj * 8, (cuuint64_t)L.Si * 8, (cuuint64_t)L.C * 8};
-  cuuint32_t box[4] = {(cuuint32_t)bk, (cuuint32_t)bj, 1, 1};
+  cuuint32_t box[4] = {(cuuint32_t)bk, (cuuint32_t)bj, 1, 3};  // all three components
   cuuint32_t estr[4] = {1, 1, 1, 1};
   // the map starts at node (-1,-1,-1) of component 0: index off - Si - Sj - 1 = 0
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)base, dims, strides, box, estr,
@@ -1788,6 +1795,42 @@ static BrickGeo make_geo(int nx, int ny, int nz, int resident) {
   }
   g.chunks = chunks;
   g.nbricks = tiles * chunks;
+  g.xtiles = 0;
+  g.nbig = g.nbricks;
+  return g;
+}
+
+// Mixed chunking for the one-barrier kernel (opt-in, MQ_BRICK_MIX=1; measured
+// slower at 128^3: 81.2 -> 84.4 us per iteration, the pass of CTA 0 69.6 ->
+// 74.7 us with every SM carrying two CTAs -- the SMs are not the bound, see
+// DESIGN.md §3).  When
+// the co-resident CTA count R is not a multiple of the tile count, the first
+// x = R mod tiles tiles (whole rows of tiles along j, so that the i-chunk
+// boundaries of neighbouring tiles coincide everywhere but at one row
+// boundary: the halo rows a brick stages are then rows its neighbour streamed
+// a moment earlier, read from L2) are cut into chunks + 1 i-chunks, the rest
+// into chunks, so that all R slots hold a brick.  The longer bricks take CTA
+// indices [0, nbig), the shorter ones the rest: with two CTAs per SM, CTA b
+// and CTA b + R/2 share an SM (%smid census), so every long brick shares its
+// SM with a short one.  At 128^3: 96 bricks of 32 planes + 200 of 25-26 on
+// 296 slots (the equal split: 256 bricks of 32 planes, 40 SMs with one CTA).
+// The split depends only on the grid, never on the CTA placement: the
+// partial sums, hence the iterates, stay run-to-run deterministic.
+static BrickGeo make_geo_mixed(int nx, int ny, int nz, int resident) {
+  BrickGeo g = make_geo(nx, ny, nz, resident);
+  const char *v = getenv("MQ_BRICK_MIX");
+  if (!v || atoi(v) != 1) return g;
+  const int tiles = g.tiles_k * g.tiles_j;
+  const int c = resident / tiles, x = resident - c * tiles;
+  if (c < 1 || x == 0 || c + 1 > nx) return g;
+  if ((nx + c - 1) / c > 64) return g;  // two-barrier bricks: keep equal
+  if (x % g.tiles_k != 0) return g;     // whole tile rows only
+  const int nbig = (tiles - x) * c;
+  if (nbig > resident / 2) return g;    // every long brick paired with a short one
+  g.chunks = c;
+  g.xtiles = x;
+  g.nbig = nbig;
+  g.nbricks = resident;
   return g;
 }
 
@@ -1848,7 +1891,7 @@ int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int sm_cap, int *grid,
     if (want >= 1 && want < per) per = want;
   }
   const int resident = sms * per;
-  *geo = make_geo(nx, ny, nz, resident);
+  *geo = make_geo_mixed(nx, ny, nz, resident);
   *grid = geo->nbricks < resident ? geo->nbricks : resident;
   return MQ_OK;
 }

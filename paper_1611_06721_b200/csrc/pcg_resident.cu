@@ -1012,6 +1012,8 @@ int resident_pcg_setup(int nx, int ny, int nz, int *grid, BrickGeo *geo_out) {
   geo_out->tiles_j = tiles_j;
   geo_out->chunks = best;
   geo_out->nbricks = tiles * best;
+  geo_out->xtiles = 0;
+  geo_out->nbig = tiles * best;
   *grid = tiles * best;
   return MQ_OK;
 }

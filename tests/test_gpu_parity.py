@@ -797,18 +797,21 @@ def test_ensemble_member_first_steps(gpu_ok):
         assert rel(res.a_c_history[i], tr.a_c[i + 1]) <= REL_FIELD
 
 
-@pytest.mark.parametrize("variant", ["simple", "brick", "brick2", "resident", "resident2"])
+@pytest.mark.parametrize("variant", ["simple", "brick", "brick2", "brick-mixed", "resident", "resident2"])
 def test_pcg_kernel_variants_agree(gpu_ok, variant, monkeypatch):
     """All fused-PCG kernels (thread-per-row, TMA brick, shared-memory
     resident, each with one or -- MQ_PCG_SYNC=2 -- two grid reductions per
-    iteration) solve the same system like the oracle; they differ only in the
+    iteration; brick-mixed: the opt-in mixed i-chunking, MQ_BRICK_MIX=1)
+    solve the same system like the oracle; they differ only in the
     dot-product summation order (and, single-reduction, beta from the
     extrapolated r.z)."""
     from paper_1611_06721_b200 import PcgConfig, Preconditioner, pcg_solve
     from paper_1611_06721_b200 import configs as C
     from paper_1611_06721_b200.device import DeviceGrid
-    monkeypatch.setenv("MQ_PCG_KERNEL", variant.rstrip("2"))
-    monkeypatch.setenv("MQ_PCG_SYNC", "2" if variant.endswith("2") else "1")
+    kernel, _, mode = variant.partition("-")
+    monkeypatch.setenv("MQ_PCG_KERNEL", kernel.rstrip("2"))
+    monkeypatch.setenv("MQ_PCG_SYNC", "2" if kernel.endswith("2") else "1")
+    monkeypatch.setenv("MQ_BRICK_MIX", "1" if mode == "mixed" else "0")
     for index in (0, 1):
         spec, m = oracle_model(index)
         with DeviceGrid(C.make_problem(index)) as g:
