@@ -75,6 +75,7 @@ struct TmaPcgArgs {
 };
 
 constexpr size_t kTmaSmem = sizeof(Box3) * (NR + NP) + 128;
+constexpr int kMaskPlanes = 64;  // MarchCtx::mrow capacity in planes
 constexpr int kMaxMultiVec = 32;  // POD basis slots (MAXS)
 
 // ---- PTX helpers ----------------------------------------------------------
@@ -348,6 +349,12 @@ struct MarchCtx {
   // planes i0-1 .. of the next march's first brick already in flight
   // (tma_preissue), skipped by its prologue
   int pre = 0;
+  // one-barrier kernels: the active-dof bits of the brick's own positions,
+  // one 32-bit word per (plane, component, tile row) aligned to the tile's
+  // k0, kept in shared memory while the CTA stays on the brick (bricks of
+  // <= kMaskPlanes planes); nullptr: the mask words are loaded per plane
+  uint32_t *mrow = nullptr;
+  int mi0 = -1, mj0 = -1, mk0 = -1;  // brick whose bits mrow holds
 #ifdef MQ_TRACE_MARCH
   unsigned long long *tr = nullptr;  // CTA 0 thread 0, one iteration: 4 stamps per plane step
 #endif
@@ -452,6 +459,25 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   const bool jac = a.use_jac != 0;
   const uint32_t *mask = a.mask;
   double *x = a.x;
+  // own-position mask bits from shared memory (filled once per brick; the
+  // prologue's first __syncthreads orders the fill before any read)
+  const bool mcache = mc.mrow != nullptr && i1 - i0 <= kMaskPlanes;
+  if (mcache && (mc.mi0 != i0 || mc.mj0 != j0 || mc.mk0 != k0)) {
+    for (int w = tid; w < (i1 - i0) * 3 * TJ; w += kBlock) {
+      const int q = i0 + w / (3 * TJ), c = (w / TJ) % 3, jj = j0 + w % TJ;
+      uint32_t bits = 0u;
+      if (jj < g.ny) {
+        const int64_t e0 = c * L.C + (int64_t)q * L.Si + L.off + (int64_t)jj * L.Sj + k0;
+        const uint32_t w0 = __ldg(mask + (e0 >> 5));
+        const uint32_t w1 = (e0 & 31) ? __ldg(mask + (e0 >> 5) + 1) : 0u;
+        bits = __funnelshift_r(w0, w1, (uint32_t)(e0 & 31));
+      }
+      mc.mrow[w] = bits;
+    }
+    mc.mi0 = i0;
+    mc.mj0 = j0;
+    mc.mk0 = k0;
+  }
 
   auto issue = [&](int q) {
     if (tid == 0) tma_issue_plane<MODE, NAT>(mc, mr, mp, with_p, q, j0, k0);
@@ -469,7 +495,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const int64_t e = c * L.C + qb + pos_own;
-        o.mw[c] = __ldg(mask + (e >> 5));
+        o.mw[c] = mcache ? 0u : __ldg(mask + (e >> 5));
         if (xm >= 1) o.xo[c] = __ldcg(x + e);
         if (xm == 2) o.p2[c] = __ldcg(pnew + e);
       }
@@ -495,7 +521,8 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const int64_t e = c * L.C + qb + pos_own;
-        act |= ((o.mw[c] >> (e & 31)) & 1u) << c;
+        const uint32_t bit = mcache ? (mc.mrow[((q - i0) * 3 + c) * TJ + ty] >> tx) & 1u : (o.mw[c] >> (e & 31)) & 1u;
+        act |= bit << c;
       }
     }
     if (MODE == kInit) {  // the staged x0 is used as is
@@ -974,6 +1001,8 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
   mc.sp = mc.sr + NR1;
   mc.sa = mc.sp + NP1;
   mc.bars = bars;
+  __shared__ uint32_t mrow_s[kMaskPlanes * 3 * TJ];
+  mc.mrow = mrow_s;
   mc.ph = 0u;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NR1; ++s) mbar_init(&bars[s], 1);
@@ -1511,6 +1540,8 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_slab_kernel(cons
   mc.sp = mc.sr + NR1;
   mc.sa = mc.sp + NP1;
   mc.bars = bars;
+  __shared__ uint32_t mrow_s[kMaskPlanes * 3 * TJ];
+  mc.mrow = mrow_s;
   mc.ph = 0u;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NR1; ++s) mbar_init(&bars[s], 1);
