@@ -242,8 +242,8 @@ __device__ __forceinline__ double stencil3s(int c, double dg, double own, V v) {
 // in registers;
 // identical arithmetic and order per row); own[c] / own[3+c] the raw /
 // pre-scaled own p of the row's node.
-template <class V, int N>
-__device__ __forceinline__ void stencil3s_rows(double dg, const double (&prev)[N], const double (&own)[N],
+template <class V, int NPV, int N>
+__device__ __forceinline__ void stencil3s_rows(double dg, const double (&prev)[NPV], const double (&own)[N],
                                                const double (&next)[N], V v, double (&av)[3]) {
   const double v0_0m10 = v(0, 0, -1, 0);
   const double v0_00m1 = v(0, 0, 0, -1);
@@ -418,7 +418,7 @@ __device__ __forceinline__ void tma_drain(MarchCtx &mc, int i0) {
 // push(q, c, jk, v): p_new of an own active position of plane q (jk = its
 // offset inside the padded plane), for the slab kernel's ghost stores;
 // kK1R: push(q, c, jk, v, r) with the position's r_{k-1} as well
-template <int MODE, int NAT = NA, class ROW, class PUSH = NoPush>
+template <int MODE, int NAT = NA, int MC = 0, class ROW, class PUSH = NoPush>
 __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, const CUtensorMap *mr,
                                           const CUtensorMap *mp, bool first, double beta, double alpha_prev,
                                           int xmode, double alpha_prev2, double *pnew, int i0, int i1, int j0,
@@ -426,7 +426,10 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
                                           PUSH push = PUSH()) {
   const StencilPcgArgs &a = A.a;
   const BrickGeo &g = A.g;
-  const Lay &L = a.L;
+  // 32-bit element indices inside the march (brick_pcg_setup refuses layouts
+  // of 2^31 entries or more): one IMAD / IMAD.WIDE per address instead of
+  // 64-bit multiply chains, and half the registers per index
+  const int LC = (int)a.L.C, LSi = (int)a.L.Si, LSj = (int)a.L.Sj, Loff = (int)a.L.off;
   constexpr int NRT = NAT + 3, NPT = NAT;  // ring slots (the kernel's allocation)
   auto rsl = [](int q) { return (q + NRT) % NRT; };  // q >= -1
   auto psl = [](int q) { return (q + NPT) % NPT; };
@@ -434,7 +437,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   const int j = j0 + ty, k = k0 + tx;
   const bool own_ok = j < g.ny && k < g.nz;
   const int s_own = (ty + 1) * HK + (tx + 1);
-  const int64_t pos_own = L.off + (int64_t)j * L.Sj + k;
+  const int pos_own = Loff + j * LSj + k;
   constexpr bool K1M = MODE == kK1 || MODE == kK1R;
   const bool with_p = K1M && !first;
   // x update of this pass (kK1, !first): 0 none (deferred), 1 x += a1 p_old,
@@ -444,30 +447,31 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   // halo (slot, component) converted by this thread besides its own
   // position: the 84 halo positions x 3 components are spread over threads
   // 0..251, one each, so that no warp carries three times the work
-  int hs = -1, hc = 0;
+  int hs = -1;
   if (tid < 3 * NHALO) {
     const int h = tid % NHALO;
-    hc = tid / NHALO;
+    const int hc = tid / NHALO;
     int hj, hk;
     if (h < HK) { hj = 0; hk = h; }
     else if (h < 2 * HK) { hj = TJ + 1; hk = h - HK; }
     else if (h < 2 * HK + TJ) { hj = 1 + (h - 2 * HK); hk = 0; }
     else { hj = 1 + (h - 2 * HK - TJ); hk = TK + 1; }
-    hs = hj * HK + hk;
+    hs = hc * BOXP + hj * HK + hk;  // offset inside a Box3
   }
   const double inv = a.inv;
   const bool jac = a.use_jac != 0;
   const uint32_t *mask = a.mask;
   double *x = a.x;
-  // own-position mask bits from shared memory (filled once per brick; the
-  // prologue's first __syncthreads orders the fill before any read)
-  const bool mcache = mc.mrow != nullptr && i1 - i0 <= kMaskPlanes;
+  // MC: own-position mask bits from shared memory (filled once per brick; the
+  // prologue's first __syncthreads orders the fill before any read; the
+  // caller guarantees bricks of <= kMaskPlanes planes)
+  constexpr bool mcache = MC != 0;
   if (mcache && (mc.mi0 != i0 || mc.mj0 != j0 || mc.mk0 != k0)) {
     for (int w = tid; w < (i1 - i0) * 3 * TJ; w += kBlock) {
       const int q = i0 + w / (3 * TJ), c = (w / TJ) % 3, jj = j0 + w % TJ;
       uint32_t bits = 0u;
       if (jj < g.ny) {
-        const int64_t e0 = c * L.C + (int64_t)q * L.Si + L.off + (int64_t)jj * L.Sj + k0;
+        const int e0 = c * LC + q * LSi + Loff + jj * LSj + k0;
         const uint32_t w0 = __ldg(mask + (e0 >> 5));
         const uint32_t w1 = (e0 & 31) ? __ldg(mask + (e0 >> 5) + 1) : 0u;
         bits = __funnelshift_r(w0, w1, (uint32_t)(e0 & 31));
@@ -484,17 +488,17 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   };
   // Own-position mask words and x values are software-pipelined ahead in
   // registers: they are loaded while earlier planes are processed, so neither
-  // their latency nor the TMA's is exposed.
+  // their latency nor the TMA's is exposed.  eq = q * LSi + pos_own is the
+  // own-position entry of plane q, component 0, carried along the march.
   struct OwnPre {
     uint32_t mw[3];
     double xo[3], p2[3];
   };
-  auto prefetch_own = [&](OwnPre &o, int q, bool own_plane) {
+  auto prefetch_own = [&](OwnPre &o, int eq, bool own_plane) {
     if (own_plane && own_ok) {
-      const int64_t qb = (int64_t)q * L.Si;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const int64_t e = c * L.C + qb + pos_own;
+        const int e = c * LC + eq;
         o.mw[c] = mcache ? 0u : __ldg(mask + (e >> 5));
         if (xm >= 1) o.xo[c] = __ldcg(x + e);
         if (xm == 2) o.p2[c] = __ldcg(pnew + e);
@@ -504,10 +508,12 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       for (int c = 0; c < 3; ++c) o.mw[c] = 0u;
     }
   };
-  // returns the active-dof bits (bit c = component c) of the own position
-  auto convert = [&](int q, bool own_plane, const OwnPre &o, double (&raw)[9]) -> uint32_t {
-    const int s = rsl(q);
-    const int64_t qb = (int64_t)q * L.Si;
+  // Ring slots are carried along the march (wrapping increments) instead of
+  // q mod ring size at every use.
+  auto winc = [](int s, int n) { return s + 1 == n ? 0 : s + 1; };
+  // returns the active-dof bits (bit c = component c) of the own position;
+  // s / sp: the r-ring and p-ring slots of plane q
+  auto convert = [&](int q, int s, int sp, int eq, bool own_plane, const OwnPre &o, double (&raw)[9]) -> uint32_t {
 #ifdef MQ_TRACE_MARCH
     if (mc.tr && q - i0 >= 1 && q - i0 < 33) mc.tr[4 * (q - i0 - 1) + 0] = globaltimer_ns();
 #endif
@@ -518,79 +524,92 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
 #endif
     uint32_t act = 0u;
     if (own_plane && own_ok) {
+      if (mcache) {
+        const uint32_t *mq = mc.mrow + (q - i0) * (3 * TJ) + ty;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int64_t e = c * L.C + qb + pos_own;
-        const uint32_t bit = mcache ? (mc.mrow[((q - i0) * 3 + c) * TJ + ty] >> tx) & 1u : (o.mw[c] >> (e & 31)) & 1u;
-        act |= bit << c;
+        for (int c = 0; c < 3; ++c) act |= ((mq[c * TJ] >> tx) & 1u) << c;
+      } else {
+        const int sh = eq & 31;  // LC is a multiple of 32: the same bit position in the three words
+#pragma unroll
+        for (int c = 0; c < 3; ++c) act |= ((o.mw[c] >> sh) & 1u) << c;
       }
     }
+    double *Sr = &mc.sr[s].v[0][0];
     if (MODE == kInit) {  // the staged x0 is used as is
 #pragma unroll
-      for (int c = 0; c < 3; ++c) raw[c] = raw[3 + c] = mc.sr[s].v[c][s_own];
+      for (int c = 0; c < 3; ++c) raw[c] = raw[3 + c] = Sr[c * BOXP + s_own];
       return act;
     }
-    double (&Sr)[3][BOXP] = mc.sr[s].v;
-    const double (&Sp)[3][BOXP] = mc.sp[psl(q)].v;
-    const double (&Sa)[3][BOXP] = mc.sa[MODE == kK1R ? psl(q) : 0].v;
+    const double *Sp = &mc.sp[sp].v[0][0];
+    const double *Sa = &mc.sa[MODE == kK1R ? sp : 0].v[0][0];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      double rq = Sr[c][s_own];
-      if (MODE == kK1R && !first) rq = sub(rq, mul(alpha_prev, Sa[c][s_own]));
+      const int e = c * LC + eq;
+      const bool on = (act >> c) & 1u;
+      double rq = Sr[c * BOXP + s_own];
+      if (MODE == kK1R && !first) rq = sub(rq, mul(alpha_prev, Sa[c * BOXP + s_own]));
       const double z = jac ? mul(inv, rq) : rq;
       double pv = z;
       if (!first) {
-        const double po = Sp[c][s_own];
+        const double po = Sp[c * BOXP + s_own];
         pv = add(z, mul(beta, po));
-        if (xm >= 1 && ((act >> c) & 1u)) {
+        if (xm >= 1 && on) {
           const double xv = xm == 2 ? add(o.xo[c], mul(alpha_prev2, o.p2[c])) : o.xo[c];
-          x[c * L.C + qb + pos_own] = add(xv, mul(alpha_prev, po));
+          x[e] = add(xv, mul(alpha_prev, po));
         }
       }
       raw[c] = pv;
       raw[3 + c] = (K1M && MQ_PRESCALE) ? mul(a.of, pv) : pv;
       raw[6 + c] = rq;
-      Sr[c][s_own] = raw[3 + c];
-      if ((act >> c) & 1u) {
-        pnew[c * L.C + qb + pos_own] = pv;
-        if constexpr (MODE == kK1R) push(q, c, pos_own - L.Si, pv, rq);
-        else push(q, c, pos_own - L.Si, pv);
+      Sr[c * BOXP + s_own] = raw[3 + c];
+      if (on) {
+        pnew[e] = pv;
+        if constexpr (MODE == kK1R) push(q, c, pos_own - LSi, pv, rq);
+        else push(q, c, pos_own - LSi, pv);
         if (MODE == kK1R) {
-          if (!first) mc.rout[c * L.C + qb + pos_own] = rq;
+          if (!first) mc.rout[e] = rq;
           mc.crr = add(mc.crr, mul(rq, rq));
           mc.crz = add(mc.crz, mul(rq, z));
         }
       }
     }
     if (hs >= 0) {
-      double rq = Sr[hc][hs];
-      if (MODE == kK1R && !first) rq = sub(rq, mul(alpha_prev, Sa[hc][hs]));
+      double rq = Sr[hs];
+      if (MODE == kK1R && !first) rq = sub(rq, mul(alpha_prev, Sa[hs]));
       const double z = jac ? mul(inv, rq) : rq;
-      const double ph = first ? z : add(z, mul(beta, Sp[hc][hs]));
-      Sr[hc][hs] = (K1M && MQ_PRESCALE) ? mul(a.of, ph) : ph;
+      const double ph = first ? z : add(z, mul(beta, Sp[hs]));
+      Sr[hs] = (K1M && MQ_PRESCALE) ? mul(a.of, ph) : ph;
     }
     return act;
   };
-  auto stencil_plane = [&](int i, uint32_t act, const double (&prev)[9], const double (&raw)[9],
-                           const double (&next)[9]) {
+  // sm1, s0, sp1: the r-ring slots of planes i-1, i, i+1; pm: the own
+  // pre-scaled values of plane i-1
+  auto stencil_plane = [&](int i, int sm1, int s0, int sp1, int ei, uint32_t act, const double (&pm)[3],
+                           const double (&raw)[9], const double (&next)[9]) {
     if (!act) return;
-    const int64_t qb = (int64_t)i * L.Si;
-    const int sm1 = rsl(i - 1), s0 = rsl(i), sp1 = rsl(i + 1);
+    const double *bm1 = &mc.sr[sm1].v[0][0] + s_own, *b0 = &mc.sr[s0].v[0][0] + s_own,
+                 *bp1 = &mc.sr[sp1].v[0][0] + s_own;
     auto ld = [&](int cc, int di, int dj, int dk) {
-      const int s = di < 0 ? sm1 : (di == 0 ? s0 : sp1);
-      return mc.sr[s].v[cc][s_own + dj * HK + dk];
+      const double *bq = di < 0 ? bm1 : (di == 0 ? b0 : bp1);
+      return bq[cc * BOXP + dj * HK + dk];
     };
 #if MQ_PRESCALE && MQ_STENCIL_CSE
     if constexpr (K1M) {
       // all three rows from the 24 distinct staged values, each loaded once;
       // the row callback receives the row value (kK1R: and the own r_{k-1})
       double av[3];
-      stencil3s_rows(a.dg, prev, raw, next, ld, av);
+      const double prev[6] = {0.0, 0.0, 0.0, pm[0], pm[1], pm[2]};
+      // the pre-scaled own values of plane i are re-formed from the raw ones
+      // (the same product as at the convert step) instead of being carried
+      // in registers across the plane step
+      const double own2[9] = {raw[0], raw[1], raw[2], mul(a.of, raw[0]), mul(a.of, raw[1]), mul(a.of, raw[2]),
+                              raw[6], raw[7], raw[8]};
+      stencil3s_rows(a.dg, prev, own2, next, ld, av);
 #pragma unroll
       for (int c = 0; c < 3; ++c)
         if ((act >> c) & 1u) {
-          if constexpr (MODE == kK1R) row(c, c * L.C + qb + pos_own, av[c], raw[c], raw[6 + c], i);
-          else row(c, c * L.C + qb + pos_own, av[c], raw[c]);
+          if constexpr (MODE == kK1R) row(c, c * LC + ei, av[c], raw[c], raw[6 + c], i);
+          else row(c, c * LC + ei, av[c], raw[c]);
         }
       return;
     }
@@ -600,7 +619,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     if constexpr (MODE != kK1R) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        if ((act >> c) & 1u) row(c, c * L.C + qb + pos_own, ld, raw[c]);
+        if ((act >> c) & 1u) row(c, c * LC + ei, ld, raw[c]);
       }
     }
   };
@@ -608,33 +627,41 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   // prologue: planes i0-1 .. i0+NA-2 in flight, then convert i0-1 and i0,
   // each followed by the issue of the plane that takes over its p slot
   const int last = i1;  // planes i0-1 .. i1 are needed
-  OwnPre pa, pb;
-  double rwm[9], rw[9], rw1[9];  // own staged values of planes i-1, i, i+1
+  OwnPre o;
+  double pm[3], ra[9], rb[9];  // own staged values: pre-scaled of plane i-1, all of planes i / i+1 (ping-pong)
 #ifdef MQ_TRACE_MARCH
   if (mc.tr) mc.tr[128] = globaltimer_ns();  // march entry
 #endif
   for (int q = i0 - 1 + mc.pre; q <= i0 + NAT - 2 && q <= last; ++q) issue(q);
   mc.pre = 0;
-  prefetch_own(pa, i0, true);
-  prefetch_own(pb, i0 - 1, false);
-  convert(i0 - 1, false, pb, rwm);
+  int ei = i0 * LSi + pos_own;  // own entry of plane i, component 0
+  prefetch_own(o, ei, true);
+  // slots of planes i-1, i, i+1 (r ring) and i+1 (p ring), carried
+  int sm1 = rsl(i0 - 1), s0 = winc(sm1, NRT), sp1 = winc(s0, NRT), pp1 = psl(i0 + 1);
+  convert(i0 - 1, sm1, psl(i0 - 1), ei - LSi, false, o, rb);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) pm[c] = rb[3 + c];
   __syncthreads();
   if (i0 + NAT - 1 <= last) issue(i0 + NAT - 1);
-  const OwnPre c0 = pa;
-  prefetch_own(pa, i0 + 1, i0 + 1 < i1);
 #ifdef MQ_TRACE_MARCH
   if (mc.tr) mc.tr[129] = globaltimer_ns();  // planes i0-1 converted
 #endif
-  uint32_t act = convert(i0, true, c0, rw);
+  uint32_t act = convert(i0, s0, psl(i0), ei, true, o, ra);
+  prefetch_own(o, ei + LSi, i0 + 1 < i1);
   __syncthreads();
 #ifdef MQ_TRACE_MARCH
   if (mc.tr) mc.tr[130] = globaltimer_ns();  // plane i0 converted (prologue done)
 #endif
   if (i0 + NAT <= last) issue(i0 + NAT);
-  for (int i = i0; i < i1; ++i) {
-    const OwnPre cur = pa;
-    prefetch_own(pa, i + 2, i + 2 < i1);
-    const uint32_t act_next = convert(i + 1, i + 1 < i1, cur, rw1);
+  // one plane step: own = the staged own values of plane i (from the previous
+  // step), nxt receives those of plane i+1; o holds the prefetched own words
+  // of plane i+1 and is refilled for plane i+2 as soon as the convert step
+  // has consumed it (one register set; the loads have the barrier and the
+  // stencil of plane i to land).  The march calls it with the two staged
+  // register sets swapped every plane (no rotation copies).
+  auto step = [&](int i, double (&own)[9], double (&nxt)[9]) {
+    const uint32_t act_next = convert(i + 1, sp1, pp1, ei + LSi, i + 1 < i1, o, nxt);
+    prefetch_own(o, ei + 2 * LSi, i + 2 < i1);
 #ifdef MQ_TRACE_MARCH
     if (mc.tr) mc.tr[4 * (i - i0) + 2] = globaltimer_ns();
 #endif
@@ -645,13 +672,23 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     // r slot of plane i-2 (its last stencil was before this barrier), p slot
     // of plane i+1 (converted before this barrier)
     if (i + NAT + 1 <= last) issue(i + NAT + 1);
-    stencil_plane(i, act, rwm, rw, rw1);
+    stencil_plane(i, sm1, s0, sp1, ei, act, pm, own, nxt);
     act = act_next;
 #pragma unroll
-    for (int c = 0; c < 9; ++c) {
-      rwm[c] = rw[c];
-      rw[c] = rw1[c];
+    for (int c = 0; c < 3; ++c) pm[c] = (K1M && MQ_PRESCALE) ? mul(a.of, own[c]) : own[3 + c];
+    sm1 = s0;
+    s0 = sp1;
+    sp1 = winc(sp1, NRT);
+    pp1 = winc(pp1, NPT);
+    ei += LSi;
+  };
+  {
+    int i = i0;
+    for (; i + 1 < i1; i += 2) {
+      step(i, ra, rb);
+      step(i + 1, rb, ra);
     }
+    if (i < i1) step(i, ra, rb);
   }
   __syncthreads();
 #ifdef MQ_TRACE_MARCH
@@ -697,7 +734,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __gr
     return;
   }
   MarchCtx mc;
-  mc.sr = reinterpret_cast<Box3 *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sr = reinterpret_cast<Box3 *>(dsm + ((128u - (su32(dsm) & 127u)) & 127u));  // pointer arithmetic on dsm keeps the shared address space (LDS/STS, not generic LD/ST)
   mc.sp = mc.sr + NR;
   mc.bars = bars;
   mc.ph = 0u;
@@ -718,7 +755,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __gr
       int i0, i1, j0, k0;
       brick_of(g, bi, i0, i1, j0, k0);
       march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
-                       [&](int c, int64_t e, auto V, double) {
+                       [&](int c, int e, auto V, double) {
                          const double bv = __ldcg(b + e);
                          const double rv = sub(bv, stencil3(c, dg, of, V));
                          r[e] = rv;
@@ -796,7 +833,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma_kernel(const __gr
         int i0, i1, j0, k0;
         brick_of(g, bi, i0, i1, j0, k0);
         march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0,
-                       [&](int c, int64_t e, auto V, double own) {
+                       [&](int c, int e, auto V, double own) {
                          double av;
                          if constexpr (std::is_same_v<decltype(V), double>) av = V;  // stencil3s_rows
 #if MQ_PRESCALE
@@ -997,7 +1034,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
     return;
   }
   MarchCtx mc;
-  mc.sr = reinterpret_cast<Box3 *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sr = reinterpret_cast<Box3 *>(dsm + ((128u - (su32(dsm) & 127u)) & 127u));  // pointer arithmetic on dsm keeps the shared address space (LDS/STS, not generic LD/ST)
   mc.sp = mc.sr + NR1;
   mc.sa = mc.sp + NP1;
   mc.bars = bars;
@@ -1021,7 +1058,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
       int i0, i1, j0, k0;
       brick_of(g, bi, i0, i1, j0, k0);
       march_tma<kInit, NA1>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
-                       [&](int c, int64_t e, auto V, double) {
+                       [&](int c, int e, auto V, double) {
                          const double bv = __ldcg(b + e);
                          const double rv = sub(bv, stencil3(c, dg, of, V));
                          r[e] = rv;
@@ -1103,13 +1140,18 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
       for (int bi = blockIdx.x; bi < g.nbricks; bi += G) {
         int i0, i1, j0, k0;
         brick_of(g, bi, i0, i1, j0, k0);
-        march_tma<kK1R, NA1>(mc, A, mr, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0,
-                        [&](int, int64_t e, double av, double own, double rown, int) {
-                          apw[e] = av;
-                          v[0] = add(v[0], mul(own, av));
-                          v[1] = add(v[1], mul(rown, av));
-                          v[2] = add(v[2], mul(av, av));
-                        });
+        auto rowf = [&](int, int e, double av, double own, double rown, int) {
+          apw[e] = av;
+          v[0] = add(v[0], mul(own, av));
+          v[1] = add(v[1], mul(rown, av));
+          v[2] = add(v[2], mul(av, av));
+        };
+        // bricks of <= kMaskPlanes planes (the default geometry of this kernel):
+        // own-position mask bits from shared memory
+        if (i1 - i0 <= kMaskPlanes)
+          march_tma<kK1R, NA1, 1>(mc, A, mr, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0, rowf);
+        else
+          march_tma<kK1R, NA1, 0>(mc, A, mr, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0, rowf);
       }
       double v5[5] = {v[0], v[1], v[2], mc.crr, mc.crz};
       block_sum<5>(v5, red);
@@ -1315,7 +1357,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_slab_kernel(const __grid_co
   const double *b = a.b;
   const int x0_mode = a.x0_mode;
   MarchCtx mc;
-  mc.sr = reinterpret_cast<Box3 *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sr = reinterpret_cast<Box3 *>(dsm + ((128u - (su32(dsm) & 127u)) & 127u));  // pointer arithmetic on dsm keeps the shared address space (LDS/STS, not generic LD/ST)
   mc.sp = mc.sr + NR;
   mc.bars = bars;
   mc.ph = 0u;
@@ -1347,7 +1389,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_slab_kernel(const __grid_co
       int i0, i1, j0, k0;
       brick_of(g, bi, i0, i1, j0, k0);
       march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
-                       [&](int c, int64_t e, auto V, double) {
+                       [&](int c, int e, auto V, double) {
                          const double bv = __ldcg(b + e);
                          const double rv = sub(bv, stencil3(c, dg, of, V));
                          r[e] = rv;
@@ -1405,7 +1447,7 @@ __global__ void __launch_bounds__(kBlock, 2) pcg_tma_slab_kernel(const __grid_co
         int i0, i1, j0, k0;
         brick_of(g, bi, i0, i1, j0, k0);
         march_tma<kK1>(mc, A, &A.tm_r, mp, first, beta, alpha_prev, 1, 0.0, pnew, i0, i1, j0, k0,
-                       [&](int c, int64_t e, auto V, double own) {
+                       [&](int c, int e, auto V, double own) {
                          double av;
                          if constexpr (std::is_same_v<decltype(V), double>) av = V;  // stencil3s_rows
 #if MQ_PRESCALE
@@ -1536,7 +1578,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_slab_kernel(cons
   const double *b = a.b;
   const int x0_mode = a.x0_mode;
   MarchCtx mc;
-  mc.sr = reinterpret_cast<Box3 *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sr = reinterpret_cast<Box3 *>(dsm + ((128u - (su32(dsm) & 127u)) & 127u));  // pointer arithmetic on dsm keeps the shared address space (LDS/STS, not generic LD/ST)
   mc.sp = mc.sr + NR1;
   mc.sa = mc.sp + NP1;
   mc.bars = bars;
@@ -1571,7 +1613,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_slab_kernel(cons
       int i0, i1, j0, k0;
       brick_of(g, bi, i0, i1, j0, k0);
       march_tma<kInit, NA1>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
-                            [&](int c, int64_t e, auto V, double) {
+                            [&](int c, int e, auto V, double) {
                               const double bv = __ldcg(b + e);
                               const double rv = sub(bv, stencil3(c, dg, of, V));
                               r[e] = rv;
@@ -1645,22 +1687,26 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_slab_kernel(cons
       for (int bi = lb; bi < g.nbricks; bi += Gr) {
         int i0, i1, j0, k0;
         brick_of(g, bi, i0, i1, j0, k0);
-        march_tma<kK1R, NA1>(mc, A, mr, mp, first, beta, alpha_prev, first ? 0 : 1, 0.0, pnew, i0, i1, j0, k0,
-                             [&](int c, int64_t e, double av, double own, double rown, int i) {
-                               apw[e] = av;
-                               v[0] = add(v[0], mul(own, av));
-                               v[1] = add(v[1], mul(rown, av));
-                               v[2] = add(v[2], mul(av, av));
-                               if (i == 0 && me.lo_a) {
-                                 const int64_t jk = e - c * L.C - L.Si;
-                                 (odd_a ? me.lo_a2 : me.lo_a)[c * me.lo_C + me.lo_top + jk] = av;
-                               }
-                               if (i == nmax && me.hi_a) {
-                                 const int64_t jk = e - c * L.C - (int64_t)me.n * L.Si;
-                                 (odd_a ? me.hi_a2 : me.hi_a)[c * me.hi_C + jk] = av;
-                               }
-                             },
-                             push);
+        auto rowf = [&](int c, int e, double av, double own, double rown, int i) {
+          apw[e] = av;
+          v[0] = add(v[0], mul(own, av));
+          v[1] = add(v[1], mul(rown, av));
+          v[2] = add(v[2], mul(av, av));
+          if (i == 0 && me.lo_a) {
+            const int64_t jk = e - c * L.C - L.Si;
+            (odd_a ? me.lo_a2 : me.lo_a)[c * me.lo_C + me.lo_top + jk] = av;
+          }
+          if (i == nmax && me.hi_a) {
+            const int64_t jk = e - c * L.C - (int64_t)me.n * L.Si;
+            (odd_a ? me.hi_a2 : me.hi_a)[c * me.hi_C + jk] = av;
+          }
+        };
+        if (i1 - i0 <= kMaskPlanes)
+          march_tma<kK1R, NA1, 1>(mc, A, mr, mp, first, beta, alpha_prev, first ? 0 : 1, 0.0, pnew, i0, i1, j0, k0, rowf,
+                                  push);
+        else
+          march_tma<kK1R, NA1, 0>(mc, A, mr, mp, first, beta, alpha_prev, first ? 0 : 1, 0.0, pnew, i0, i1, j0, k0, rowf,
+                                  push);
       }
       ++applies;
       double v5[5] = {v[0], v[1], v[2], mc.crr, mc.crz};
@@ -1713,7 +1759,7 @@ __global__ void __launch_bounds__(kBlock, 2) kn_apply_tma_kernel(const __grid_co
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t bars[NR];
   MarchCtx mc;
-  mc.sr = reinterpret_cast<Box3 *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sr = reinterpret_cast<Box3 *>(dsm + ((128u - (su32(dsm) & 127u)) & 127u));  // pointer arithmetic on dsm keeps the shared address space (LDS/STS, not generic LD/ST)
   mc.sp = mc.sr + NR;
   mc.bars = bars;
   mc.ph = 0u;
@@ -1726,7 +1772,7 @@ __global__ void __launch_bounds__(kBlock, 2) kn_apply_tma_kernel(const __grid_co
     int i0, i1, j0, k0;
     brick_of(A.g, bi, i0, i1, j0, k0);
     march_tma<kInit>(mc, A, &A.tm_x, nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
-                     [&](int c, int64_t e, auto V, double own) { y[e] = stencil3(c, A.a.dg, A.a.of, V); });
+                     [&](int c, int e, auto V, double own) { y[e] = stencil3(c, A.a.dg, A.a.of, V); });
   }
 }
 
@@ -1746,7 +1792,7 @@ __global__ void __launch_bounds__(kBlock, 2) kn_apply_tma_multi_kernel(const __g
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t bars[NR];
   MarchCtx mc;
-  mc.sr = reinterpret_cast<Box3 *>(((uintptr_t)dsm + 127) & ~(uintptr_t)127);
+  mc.sr = reinterpret_cast<Box3 *>(dsm + ((128u - (su32(dsm) & 127u)) & 127u));  // pointer arithmetic on dsm keeps the shared address space (LDS/STS, not generic LD/ST)
   mc.sp = mc.sr + NR;
   mc.bars = bars;
   mc.ph = 0u;
@@ -1760,7 +1806,7 @@ __global__ void __launch_bounds__(kBlock, 2) kn_apply_tma_multi_kernel(const __g
     int i0, i1, j0, k0;
     brick_of(M.A.g, bi, i0, i1, j0, k0);
     march_tma<kInit>(mc, M.A, &M.tm[j], nullptr, true, 0.0, 0.0, 0, 0.0, nullptr, i0, i1, j0, k0,
-                     [&](int c, int64_t e, auto V, double) { y[e] = stencil3(c, M.A.a.dg, M.A.a.of, V); });
+                     [&](int c, int e, auto V, double) { y[e] = stencil3(c, M.A.a.dg, M.A.a.of, V); });
   }
 }
 
@@ -1902,7 +1948,8 @@ static cudaError_t two_cta_carveout(const void *fn, int want = 2, size_t smem = 
 }
 
 int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int sm_cap, int *grid, BrickGeo *geo) {
-  (void)L;
+  // the march indexes entries with 32-bit integers
+  if (L.total >= (int64_t)1 << 31) { set_error("TMA PCG kernels: padded vector of 2^31 entries or more"); return MQ_INVALID; }
   int dev = 0, sms = 0, per = 0;
   MQ_CUDA(cudaGetDevice(&dev));
   MQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1962,6 +2009,8 @@ int launch_pcg_brick(const StencilPcgArgs &args, const BrickGeo &geo, int grid, 
 int launch_pcg_tma_slab(const StencilPcgArgs *args, const SlabRank *ranks, const int *nplanes, int ngroups,
                         int nranks, int rank0, int ny, int nz, cudaStream_t s) {
   if (ngroups < 1 || ngroups > kMaxRanks) { set_error("1..8 rank groups per launch"); return MQ_INVALID; }
+  for (int q = 0; q < ngroups; ++q)
+    if (args[q].L.total >= (int64_t)1 << 31) { set_error("TMA PCG kernels: padded vector of 2^31 entries or more"); return MQ_INVALID; }
   int dev = 0, sms = 0, per = 0;
   MQ_CUDA(cudaGetDevice(&dev));
   MQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
