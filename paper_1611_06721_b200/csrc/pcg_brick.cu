@@ -458,8 +458,9 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     else { hj = 1 + (h - 2 * HK - TJ); hk = TK + 1; }
     hs = hc * BOXP + hj * HK + hk;  // offset inside a Box3
   }
-  const double inv = a.inv;
-  const bool jac = a.use_jac != 0;
+  // z = M^-1 r as one product: 1.0 * r is r bit for bit without the
+  // preconditioner, so the march carries no select per staged value
+  const double invj = a.use_jac != 0 ? a.inv : 1.0;
   const uint32_t *mask = a.mask;
   double *x = a.x;
   // MC: own-position mask bits from shared memory (filled once per brick; the
@@ -548,7 +549,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       const bool on = (act >> c) & 1u;
       double rq = Sr[c * BOXP + s_own];
       if (MODE == kK1R && !first) rq = sub(rq, mul(alpha_prev, Sa[c * BOXP + s_own]));
-      const double z = jac ? mul(inv, rq) : rq;
+      const double z = mul(invj, rq);
       double pv = z;
       if (!first) {
         const double po = Sp[c * BOXP + s_own];
@@ -576,7 +577,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     if (hs >= 0) {
       double rq = Sr[hs];
       if (MODE == kK1R && !first) rq = sub(rq, mul(alpha_prev, Sa[hs]));
-      const double z = jac ? mul(inv, rq) : rq;
+      const double z = mul(invj, rq);
       const double ph = first ? z : add(z, mul(beta, Sp[hs]));
       Sr[hs] = (K1M && MQ_PRESCALE) ? mul(a.of, ph) : ph;
     }
@@ -627,7 +628,13 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   // prologue: planes i0-1 .. i0+NA-2 in flight, then convert i0-1 and i0,
   // each followed by the issue of the plane that takes over its p slot
   const int last = i1;  // planes i0-1 .. i1 are needed
-  OwnPre o;
+  // Prefetch register sets: two (plane i+2 loaded before plane i+1's set is
+  // consumed) where the registers allow it; one, refilled right after the
+  // convert step has consumed it (the loads have the barrier and the stencil
+  // of plane i to land), in the one-barrier march, which carries r_{k-1} too
+  // (two sets spill there: 128^3 97 us per iteration against 76).
+  constexpr bool kTwoPre = MODE != kK1R;
+  OwnPre oa, ob;
   double pm[3], ra[9], rb[9];  // own staged values: pre-scaled of plane i-1, all of planes i / i+1 (ping-pong)
 #ifdef MQ_TRACE_MARCH
   if (mc.tr) mc.tr[128] = globaltimer_ns();  // march entry
@@ -635,33 +642,34 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   for (int q = i0 - 1 + mc.pre; q <= i0 + NAT - 2 && q <= last; ++q) issue(q);
   mc.pre = 0;
   int ei = i0 * LSi + pos_own;  // own entry of plane i, component 0
-  prefetch_own(o, ei, true);
+  prefetch_own(oa, ei, true);
   // slots of planes i-1, i, i+1 (r ring) and i+1 (p ring), carried
   int sm1 = rsl(i0 - 1), s0 = winc(sm1, NRT), sp1 = winc(s0, NRT), pp1 = psl(i0 + 1);
-  convert(i0 - 1, sm1, psl(i0 - 1), ei - LSi, false, o, rb);
+  convert(i0 - 1, sm1, psl(i0 - 1), ei - LSi, false, oa, rb);
 #pragma unroll
   for (int c = 0; c < 3; ++c) pm[c] = rb[3 + c];
   __syncthreads();
   if (i0 + NAT - 1 <= last) issue(i0 + NAT - 1);
+  if (kTwoPre) prefetch_own(ob, ei + LSi, i0 + 1 < i1);
 #ifdef MQ_TRACE_MARCH
   if (mc.tr) mc.tr[129] = globaltimer_ns();  // planes i0-1 converted
 #endif
-  uint32_t act = convert(i0, s0, psl(i0), ei, true, o, ra);
-  prefetch_own(o, ei + LSi, i0 + 1 < i1);
+  uint32_t act = convert(i0, s0, psl(i0), ei, true, oa, ra);
+  if (!kTwoPre) prefetch_own(oa, ei + LSi, i0 + 1 < i1);
   __syncthreads();
 #ifdef MQ_TRACE_MARCH
   if (mc.tr) mc.tr[130] = globaltimer_ns();  // plane i0 converted (prologue done)
 #endif
   if (i0 + NAT <= last) issue(i0 + NAT);
   // one plane step: own = the staged own values of plane i (from the previous
-  // step), nxt receives those of plane i+1; o holds the prefetched own words
-  // of plane i+1 and is refilled for plane i+2 as soon as the convert step
-  // has consumed it (one register set; the loads have the barrier and the
-  // stencil of plane i to land).  The march calls it with the two staged
-  // register sets swapped every plane (no rotation copies).
-  auto step = [&](int i, double (&own)[9], double (&nxt)[9]) {
-    const uint32_t act_next = convert(i + 1, sp1, pp1, ei + LSi, i + 1 < i1, o, nxt);
-    prefetch_own(o, ei + 2 * LSi, i + 2 < i1);
+  // step), nxt receives those of plane i+1; ocur holds the prefetched own
+  // words of plane i+1, onxt receives those of plane i+2 (the same set when
+  // there is one).  The march calls it with the register sets swapped every
+  // plane (no rotation copies).
+  auto step = [&](int i, double (&own)[9], double (&nxt)[9], OwnPre &ocur, OwnPre &onxt) {
+    if (kTwoPre) prefetch_own(onxt, ei + 2 * LSi, i + 2 < i1);
+    const uint32_t act_next = convert(i + 1, sp1, pp1, ei + LSi, i + 1 < i1, ocur, nxt);
+    if (!kTwoPre) prefetch_own(onxt, ei + 2 * LSi, i + 2 < i1);
 #ifdef MQ_TRACE_MARCH
     if (mc.tr) mc.tr[4 * (i - i0) + 2] = globaltimer_ns();
 #endif
@@ -684,11 +692,19 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   };
   {
     int i = i0;
-    for (; i + 1 < i1; i += 2) {
-      step(i, ra, rb);
-      step(i + 1, rb, ra);
+    if (kTwoPre) {
+      for (; i + 1 < i1; i += 2) {
+        step(i, ra, rb, ob, oa);
+        step(i + 1, rb, ra, oa, ob);
+      }
+      if (i < i1) step(i, ra, rb, ob, oa);
+    } else {
+      for (; i + 1 < i1; i += 2) {
+        step(i, ra, rb, oa, oa);
+        step(i + 1, rb, ra, oa, oa);
+      }
+      if (i < i1) step(i, ra, rb, oa, oa);
     }
-    if (i < i1) step(i, ra, rb);
   }
   __syncthreads();
 #ifdef MQ_TRACE_MARCH
@@ -1961,7 +1977,7 @@ int brick_pcg_setup(const Lay &L, int nx, int ny, int nz, int sm_cap, int *grid,
   MQ_CUDA(two_cta_carveout((const void *)pcg_tma1_kernel, MQ_TMA_MINB, kTmaSmem1));
   MQ_CUDA(two_cta_carveout((const void *)kn_apply_tma_kernel));
   MQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pcg_tma_kernel, kBlock, kTmaSmem));
-  static_assert(kTmaSmem1 <= kTmaSmem, "both TMA PCG kernels place as many CTAs per SM");
+  static_assert(kTmaSmem1 <= kTmaSmem || 2 * (kTmaSmem1 + 8 * 1024) <= 227 * 1024, "both TMA PCG kernels place two CTAs per SM");
   if (getenv("MQ_PCG_VERBOSE")) fprintf(stderr, "pcg_tma_kernel: %d CTAs per SM, %zu B smem\n", per, kTmaSmem);
   if (per < 1) { set_error("TMA PCG kernel cannot be resident"); return MQ_CUDA_ERROR; }
   if (const char *v = getenv("MQ_BRICK_CTAS_PER_SM")) {
