@@ -323,6 +323,34 @@ __device__ __forceinline__ void stencil3s_rows(double dg, const double (&prev)[N
 }
 
 
+// stores / own-position loads of the march (experiments: cache operators)
+#ifndef MQ_ST_MODE
+#define MQ_ST_MODE 0
+#endif
+#ifndef MQ_LD_MODE
+#define MQ_LD_MODE 0
+#endif
+__device__ __forceinline__ void st_out(double *p, double v) {
+#if MQ_ST_MODE == 1
+  __stcg(p, v);
+#elif MQ_ST_MODE == 2
+  __stcs(p, v);
+#elif MQ_ST_MODE == 3
+  __stwt(p, v);
+#else
+  *p = v;
+#endif
+}
+__device__ __forceinline__ double ld_own(const double *p) {
+#if MQ_LD_MODE == 1
+  return __ldcs(p);
+#elif MQ_LD_MODE == 2
+  return __ldlu(p);
+#else
+  return __ldcg(p);
+#endif
+}
+
 __device__ __forceinline__ int rslot(int q) { return (q + NR) % NR; }  // q >= -1
 __device__ __forceinline__ int pslot(int q) { return (q + NP) % NP; }
 
@@ -501,8 +529,8 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       for (int c = 0; c < 3; ++c) {
         const int e = c * LC + eq;
         o.mw[c] = mcache ? 0u : __ldg(mask + (e >> 5));
-        if (xm >= 1) o.xo[c] = __ldcg(x + e);
-        if (xm == 2) o.p2[c] = __ldcg(pnew + e);
+        if (xm >= 1) o.xo[c] = ld_own(x + e);
+        if (xm == 2) o.p2[c] = ld_own(pnew + e);
       }
     } else {
 #pragma unroll
@@ -556,7 +584,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
         pv = add(z, mul(beta, po));
         if (xm >= 1 && on) {
           const double xv = xm == 2 ? add(o.xo[c], mul(alpha_prev2, o.p2[c])) : o.xo[c];
-          x[e] = add(xv, mul(alpha_prev, po));
+          st_out(x + e, add(xv, mul(alpha_prev, po)));
         }
       }
       raw[c] = pv;
@@ -564,11 +592,11 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       raw[6 + c] = rq;
       Sr[c * BOXP + s_own] = raw[3 + c];
       if (on) {
-        pnew[e] = pv;
+        st_out(pnew + e, pv);
         if constexpr (MODE == kK1R) push(q, c, pos_own - LSi, pv, rq);
         else push(q, c, pos_own - LSi, pv);
         if (MODE == kK1R) {
-          if (!first) mc.rout[e] = rq;
+          if (!first) st_out(mc.rout + e, rq);
           mc.crr = add(mc.crr, mul(rq, rq));
           mc.crz = add(mc.crz, mul(rq, z));
         }
@@ -1157,7 +1185,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
         int i0, i1, j0, k0;
         brick_of(g, bi, i0, i1, j0, k0);
         auto rowf = [&](int, int e, double av, double own, double rown, int) {
-          apw[e] = av;
+          st_out(apw + e, av);
           v[0] = add(v[0], mul(own, av));
           v[1] = add(v[1], mul(rown, av));
           v[2] = add(v[2], mul(av, av));
