@@ -1961,19 +1961,22 @@ static BrickGeo make_geo_mixed(int nx, int ny, int nz, int resident) {
 // stores of K1 throttle (ncu stall_lg 0.61 -> 1.53 per issue) and an iteration
 // at 128^3 takes 104 instead of 94 us; left to the driver the carveout
 // sometimes fits only one CTA per SM (118 us).  MQ_PCG_CARVEOUT overrides.
-// One grid barrier per iteration (pcg_tma1_kernel) for bricks of <= 64
-// planes, two (pcg_tma_kernel) for longer ones: measured at 128^3 (32-plane
-// bricks) 84.0 vs 86.6 us per iteration, at 256^3 (256-plane bricks) 657 vs
-// 642 -- the one-barrier pass is the whole iteration, and the imbalance
-// between CTAs alone on an SM and CTAs sharing one grows with the brick,
-// where the two-barrier kernel's flat K2 pass is balanced.  MQ_PCG_SYNC=1|2
-// forces either; read per launch.
+//
+// One grid barrier per iteration (pcg_tma1_kernel) at every brick length.
+// Before the march's instruction diet the one-barrier pass lost at 256^3
+// (256-plane bricks: 657 vs 642 us per iteration -- the single pass carried
+// the whole iteration's CTA imbalance) and the two-barrier kernel was kept
+// for bricks of more than 64 planes; with the leaner march the pass is
+// DRAM-bound and the imbalance small: 128^3 75.8 vs 85.5, 256^3 551.5 vs
+// 612.8 us per iteration.  MQ_PCG_SYNC=1|2 forces either (pcg_tma_kernel stays
+// as the two-barrier reference variant); read per launch.
 static bool tma_one_barrier(const BrickGeo &g) {
+  (void)g;
   if (const char *v = getenv("MQ_PCG_SYNC")) {
     const int k = atoi(v);
     if (k == 1 || k == 2) return k == 1;
   }
-  return (g.nx + g.chunks - 1) / g.chunks <= 64;
+  return true;
 }
 bool tma_single_reduction(const BrickGeo &g) { return tma_one_barrier(g); }
 
