@@ -446,7 +446,9 @@ __device__ __forceinline__ void tma_drain(MarchCtx &mc, int i0) {
 // push(q, c, jk, v): p_new of an own active position of plane q (jk = its
 // offset inside the padded plane), for the slab kernel's ghost stores;
 // kK1R: push(q, c, jk, v, r) with the position's r_{k-1} as well
-template <int MODE, int NAT = NA, int MC = 0, class ROW, class PUSH = NoPush>
+// XM2 = 0: the instance carries no deferred (two-term) x update: xmode != 0
+// means x += a1 p_old (fewer live registers; the slab kernel's short bricks)
+template <int MODE, int NAT = NA, int MC = 0, int XM2 = 1, class ROW, class PUSH = NoPush>
 __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, const CUtensorMap *mr,
                                           const CUtensorMap *mp, bool first, double beta, double alpha_prev,
                                           int xmode, double alpha_prev2, double *pnew, int i0, int i1, int j0,
@@ -471,7 +473,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   // x update of this pass (kK1, !first): 0 none (deferred), 1 x += a1 p_old,
   // 2 x = (x + a2 p_prev2) + a1 p_old with p_prev2 read from the p_new buffer
   // at the own position just before it is overwritten
-  const int xm = (K1M && !first) ? xmode : 0;
+  const int xm = (K1M && !first) ? (XM2 ? xmode : (xmode ? 1 : 0)) : 0;
   // halo (slot, component) converted by this thread besides its own
   // position: the 84 halo positions x 3 components are spread over threads
   // 0..251, one each, so that no warp carries three times the work
@@ -530,7 +532,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
         const int e = c * LC + eq;
         o.mw[c] = mcache ? 0u : __ldg(mask + (e >> 5));
         if (xm >= 1) o.xo[c] = ld_own(x + e);
-        if (xm == 2) o.p2[c] = ld_own(pnew + e);
+        if (XM2 && xm == 2) o.p2[c] = ld_own(pnew + e);
       }
     } else {
 #pragma unroll
@@ -583,7 +585,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
         const double po = Sp[c * BOXP + s_own];
         pv = add(z, mul(beta, po));
         if (xm >= 1 && on) {
-          const double xv = xm == 2 ? add(o.xo[c], mul(alpha_prev2, o.p2[c])) : o.xo[c];
+          const double xv = (XM2 && xm == 2) ? add(o.xo[c], mul(alpha_prev2, o.p2[c])) : o.xo[c];
           st_out(x + e, add(xv, mul(alpha_prev, po)));
         }
       }
@@ -1046,6 +1048,9 @@ done:
 constexpr int NA1 = MQ_NAHEAD1, NR1 = NA1 + 3, NP1 = NA1;
 #ifndef MQ_TMA_PREISSUE
 #define MQ_TMA_PREISSUE 1
+#endif
+#ifndef MQ_SLAB_XDEFER
+#define MQ_SLAB_XDEFER 1
 #endif
 constexpr size_t kTmaSmem1 = sizeof(Box3) * (NR1 + 2 * NP1) + 128;
 
@@ -1700,9 +1705,26 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_slab_kernel(cons
     rel = relf(rnorm);
     if (rnorm <= target) { converged = 1; goto done; }
     if (a.max_iter < 1) { status = MQ_NOT_CONVERGED; goto done; }
-    double beta = 0.0, alpha_prev = 0.0;
+    double beta = 0.0, alpha_prev = 0.0, alpha_prev2 = 0.0;
+    // deferred x update as in pcg_tma1_kernel (MQ_SLAB_XDEFER) for long
+    // bricks (> kMaskPlanes planes: slabs of 128 / 256 planes, 671 -> 625 us
+    // per iteration at one rank); short bricks (slabs of <= 64 planes) update
+    // x every pass: the two-term update's extra registers spill in this
+    // kernel (32-plane slab 89.8 -> 91.4 us).  Uniform per launch.
+    const bool defer = MQ_SLAB_XDEFER && (g.nx + g.chunks - 1) / g.chunks > kMaskPlanes;
+    bool pend = false;
+    int xmode = 0;
     for (int it = 1;; ++it) {
       const bool first = it == 1;
+      xmode = 0;
+      if (!first) {
+        if (defer) {
+          xmode = pend ? 2 : 0;
+          pend = !pend;
+        } else {
+          xmode = 1;
+        }
+      }
       double *pnew = pold_is_a ? a.pb : a.pa;
       const CUtensorMap *mp = pold_is_a ? &A.tm_pa : &A.tm_pb;
       const bool odd_r = (it - 1) & 1;  // r_{it-1} goes to r2 when odd
@@ -1745,12 +1767,11 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_slab_kernel(cons
             (odd_a ? me.hi_a2 : me.hi_a)[c * me.hi_C + jk] = av;
           }
         };
-        if (i1 - i0 <= kMaskPlanes)
-          march_tma<kK1R, NA1, 1>(mc, A, mr, mp, first, beta, alpha_prev, first ? 0 : 1, 0.0, pnew, i0, i1, j0, k0, rowf,
-                                  push);
+        if (!defer && i1 - i0 <= kMaskPlanes)
+          march_tma<kK1R, NA1, 1, 0>(mc, A, mr, mp, first, beta, alpha_prev, xmode, 0.0, pnew, i0, i1, j0, k0, rowf, push);
         else
-          march_tma<kK1R, NA1, 0>(mc, A, mr, mp, first, beta, alpha_prev, first ? 0 : 1, 0.0, pnew, i0, i1, j0, k0, rowf,
-                                  push);
+          march_tma<kK1R, NA1, 0, 1>(mc, A, mr, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0,
+                                     rowf, push);
       }
       ++applies;
       double v5[5] = {v[0], v[1], v[2], mc.crr, mc.crz};
@@ -1776,8 +1797,29 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_slab_kernel(cons
         const double rz_new = jac ? mul(inv, rr_new) : rr_new;
         beta = rz_new > 0.0 ? rz_new / rz : 0.0;
       }
+      alpha_prev2 = alpha_prev;
       alpha_prev = alpha;
       pold_is_a = !pold_is_a;
+    }
+    if (status == MQ_OK && defer && xmode == 0) {
+      // the pass that read the final test left x += alpha_K p_K pending
+      // (p_K = that pass's p_old); with xmode 2 x is complete
+      const double *pdir = pold_is_a ? a.pa : a.pb;
+      const double aK = alpha;
+      flat_pairs_owned(L, me.n, lb, Gr, [&](int64_t p, int64_t stride, int n) {
+        double2 xv[kUnroll], pv[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+          if (u < n) {
+            xv[u] = __ldcg(reinterpret_cast<const double2 *>(x) + p + u * stride);
+            pv[u] = __ldcg(reinterpret_cast<const double2 *>(pdir) + p + u * stride);
+          }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+          if (u < n)
+            reinterpret_cast<double2 *>(x)[p + u * stride] =
+                make_double2(add(xv[u].x, mul(aK, pv[u].x)), add(xv[u].y, mul(aK, pv[u].y)));
+      });
     }
     if (status == MQ_OK && !converged) status = MQ_NOT_CONVERGED;
   }
