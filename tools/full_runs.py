@@ -1,7 +1,7 @@
 """Every BASELINE config at its full length on one GPU (device-resident loop,
 recovery and the B probe every step): completes without a step failure, and
 a summary per run — steps/s, iterations per family, final field norms, start
-vector diagnostics — as JSON lines (profiles/r01_full_runs.jsonl).
+vector diagnostics — as JSON lines (profiles/r0N_full_runs.jsonl).
 
     python tools/full_runs.py [--only 0,1,2,3,4]
 
