@@ -242,9 +242,9 @@ __device__ __forceinline__ double stencil3s(int c, double dg, double own, V v) {
 // in registers;
 // identical arithmetic and order per row); own[c] / own[3+c] the raw /
 // pre-scaled own p of the row's node.
-template <class V, int NPV, int N>
+template <class V, int NPV, int N, int NNV>
 __device__ __forceinline__ void stencil3s_rows(double dg, const double (&prev)[NPV], const double (&own)[N],
-                                               const double (&next)[N], V v, double (&av)[3]) {
+                                               const double (&next)[NNV], V v, double (&av)[3]) {
   const double v0_0m10 = v(0, 0, -1, 0);
   const double v0_00m1 = v(0, 0, 0, -1);
   const double v0_001 = v(0, 0, 0, 1);
@@ -417,14 +417,14 @@ __device__ __forceinline__ void tma_issue_plane(MarchCtx &mc, const CUtensorMap 
 // (i0, i1, j0, k0)) issued ahead, by thread `who`, right after the grid
 // barrier that makes their data visible -- their latency then overlaps the
 // partial-sum read.  Every thread records the count in mc.pre.
-template <int MODE, int NAT>
+template <int MODE, int NAT, int DIR = 1>
 __device__ __forceinline__ void tma_preissue(MarchCtx &mc, const CUtensorMap *mr, const CUtensorMap *mp,
                                              bool with_p, int i0, int i1, int j0, int k0, int who) {
-  int n = 0;
-  for (int q = i0 - 1; q <= i0 + NAT - 2 && q <= i1; ++q) ++n;
+  // the first staged planes of a march in direction DIR: i0-1, i0, .. (DIR > 0) or i1, i1-1, .. (DIR < 0)
+  const int n = (NAT < i1 - i0 + 2) ? NAT : i1 - i0 + 2;
   if ((int)threadIdx.x == who) {
     fence_proxy_async_global();
-    for (int q = i0 - 1; q < i0 - 1 + n; ++q) tma_issue_plane<MODE, NAT>(mc, mr, mp, with_p, q, j0, k0);
+    for (int t = 0; t < n; ++t) tma_issue_plane<MODE, NAT>(mc, mr, mp, with_p, DIR > 0 ? i0 - 1 + t : i1 - t, j0, k0);
   }
   mc.pre = n;
 }
@@ -432,10 +432,11 @@ __device__ __forceinline__ void tma_preissue(MarchCtx &mc, const CUtensorMap *mr
 // Wait out pre-issued loads that no march will consume (the solve ended at
 // this barrier): no bulk copy may still target the CTA's shared memory when
 // it exits.
-template <int NAT>
-__device__ __forceinline__ void tma_drain(MarchCtx &mc, int i0) {
+template <int NAT, int DIR = 1>
+__device__ __forceinline__ void tma_drain(MarchCtx &mc, int i0, int i1) {
   constexpr int NRT = NAT + 3;
-  for (int q = i0 - 1; q < i0 - 1 + mc.pre; ++q) {
+  for (int t = 0; t < mc.pre; ++t) {
+    const int q = DIR > 0 ? i0 - 1 + t : i1 - t;
     const int s = (q + NRT) % NRT;
     mbar_wait(&mc.bars[s], (mc.ph >> s) & 1u);
     mc.ph ^= (1u << s);
@@ -448,7 +449,12 @@ __device__ __forceinline__ void tma_drain(MarchCtx &mc, int i0) {
 // kK1R: push(q, c, jk, v, r) with the position's r_{k-1} as well
 // XM2 = 0: the instance carries no deferred (two-term) x update: xmode != 0
 // means x += a1 p_old (fewer live registers; the slab kernel's short bricks)
-template <int MODE, int NAT = NA, int MC = 0, int XM2 = 1, class ROW, class PUSH = NoPush>
+// DIR = -1: the brick is marched from plane i1-1 down to i0 (staged planes
+// i1 .. i0-1): same rows, same arithmetic per row; the one-barrier kernel
+// alternates the direction from pass to pass so that the planes a pass wrote
+// last (r, p, Ap around the end of every brick, still in L2) are the first
+// the next pass reads.
+template <int MODE, int NAT = NA, int MC = 0, int XM2 = 1, int DIR = 1, class ROW, class PUSH = NoPush>
 __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, const CUtensorMap *mr,
                                           const CUtensorMap *mp, bool first, double beta, double alpha_prev,
                                           int xmode, double alpha_prev2, double *pnew, int i0, int i1, int j0,
@@ -541,7 +547,7 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
   };
   // Ring slots are carried along the march (wrapping increments) instead of
   // q mod ring size at every use.
-  auto winc = [](int s, int n) { return s + 1 == n ? 0 : s + 1; };
+  auto winc = [](int s, int n) { return DIR > 0 ? (s + 1 == n ? 0 : s + 1) : (s == 0 ? n - 1 : s - 1); };  // next staged plane's slot
   // returns the active-dof bits (bit c = component c) of the own position;
   // s / sp: the r-ring and p-ring slots of plane q
   auto convert = [&](int q, int s, int sp, int eq, bool own_plane, const OwnPre &o, double (&raw)[9]) -> uint32_t {
@@ -629,13 +635,18 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
       // all three rows from the 24 distinct staged values, each loaded once;
       // the row callback receives the row value (kK1R: and the own r_{k-1})
       double av[3];
-      const double prev[6] = {0.0, 0.0, 0.0, pm[0], pm[1], pm[2]};
+      // own pre-scaled values of the actual planes i-1 (prev[3..5]) and i+1
+      // (next[4], next[5]): pm holds those of the plane staged before plane
+      // i, next those of the plane staged after it
+      const double prev[6] = {0.0, 0.0, 0.0, DIR > 0 ? pm[0] : next[3], DIR > 0 ? pm[1] : next[4],
+                              DIR > 0 ? pm[2] : next[5]};
+      const double nextd[6] = {0.0, 0.0, 0.0, 0.0, DIR > 0 ? next[4] : pm[1], DIR > 0 ? next[5] : pm[2]};
       // the pre-scaled own values of plane i are re-formed from the raw ones
       // (the same product as at the convert step) instead of being carried
       // in registers across the plane step
       const double own2[9] = {raw[0], raw[1], raw[2], mul(a.of, raw[0]), mul(a.of, raw[1]), mul(a.of, raw[2]),
                               raw[6], raw[7], raw[8]};
-      stencil3s_rows(a.dg, prev, own2, next, ld, av);
+      stencil3s_rows(a.dg, prev, own2, nextd, ld, av);
 #pragma unroll
       for (int c = 0; c < 3; ++c)
         if ((act >> c) & 1u) {
@@ -655,85 +666,91 @@ __device__ __forceinline__ void march_tma(MarchCtx &mc, const TmaPcgArgs &A, con
     }
   };
 
-  // prologue: planes i0-1 .. i0+NA-2 in flight, then convert i0-1 and i0,
-  // each followed by the issue of the plane that takes over its p slot
-  const int last = i1;  // planes i0-1 .. i1 are needed
-  // Prefetch register sets: two (plane i+2 loaded before plane i+1's set is
+  // The march in staging order: t = 0 .. n+1 are the planes i0-1 .. i1
+  // (DIR > 0) or i1 .. i0-1 (DIR < 0), qa(t) the plane of step t; the own
+  // planes are t = 1 .. n.
+  // prologue: staged planes 0 .. NA-1 in flight, then convert 0 and 1, each
+  // followed by the issue of the plane that takes over its p slot
+  const int n = i1 - i0;
+  auto qa = [&](int t) { return DIR > 0 ? i0 - 1 + t : i1 - t; };
+  const int dE = DIR > 0 ? LSi : -LSi;
+  // Prefetch register sets: two (plane t+2 loaded before plane t+1's set is
   // consumed) where the registers allow it; one, refilled right after the
   // convert step has consumed it (the loads have the barrier and the stencil
-  // of plane i to land), in the one-barrier march, which carries r_{k-1} too
+  // of plane t to land), in the one-barrier march, which carries r_{k-1} too
   // (two sets spill there: 128^3 97 us per iteration against 76).
   constexpr bool kTwoPre = MODE != kK1R;
   OwnPre oa, ob;
-  double pm[3], ra[9], rb[9];  // own staged values: pre-scaled of plane i-1, all of planes i / i+1 (ping-pong)
+  double pm[3], ra[9], rb[9];  // own staged values: pre-scaled of plane t-1, all of planes t / t+1 (ping-pong)
 #ifdef MQ_TRACE_MARCH
   if (mc.tr) mc.tr[128] = globaltimer_ns();  // march entry
 #endif
-  for (int q = i0 - 1 + mc.pre; q <= i0 + NAT - 2 && q <= last; ++q) issue(q);
+  for (int t = mc.pre; t <= NAT - 1 && t <= n + 1; ++t) issue(qa(t));
   mc.pre = 0;
-  int ei = i0 * LSi + pos_own;  // own entry of plane i, component 0
+  int ei = qa(1) * LSi + pos_own;  // own entry of plane t, component 0
   prefetch_own(oa, ei, true);
-  // slots of planes i-1, i, i+1 (r ring) and i+1 (p ring), carried
-  int sm1 = rsl(i0 - 1), s0 = winc(sm1, NRT), sp1 = winc(s0, NRT), pp1 = psl(i0 + 1);
-  convert(i0 - 1, sm1, psl(i0 - 1), ei - LSi, false, oa, rb);
+  // ring slots of planes t-1, t, t+1 (r ring) and t+1 (p ring), carried
+  int sl_m = rsl(qa(0)), sl_0 = winc(sl_m, NRT), sl_p = winc(sl_0, NRT), pp1 = psl(qa(2));
+  convert(qa(0), sl_m, psl(qa(0)), ei - dE, false, oa, rb);
 #pragma unroll
   for (int c = 0; c < 3; ++c) pm[c] = rb[3 + c];
   __syncthreads();
-  if (i0 + NAT - 1 <= last) issue(i0 + NAT - 1);
-  if (kTwoPre) prefetch_own(ob, ei + LSi, i0 + 1 < i1);
+  if (NAT <= n + 1) issue(qa(NAT));
+  if (kTwoPre) prefetch_own(ob, ei + dE, 2 <= n);
 #ifdef MQ_TRACE_MARCH
-  if (mc.tr) mc.tr[129] = globaltimer_ns();  // planes i0-1 converted
+  if (mc.tr) mc.tr[129] = globaltimer_ns();  // plane 0 converted
 #endif
-  uint32_t act = convert(i0, s0, psl(i0), ei, true, oa, ra);
-  if (!kTwoPre) prefetch_own(oa, ei + LSi, i0 + 1 < i1);
+  uint32_t act = convert(qa(1), sl_0, psl(qa(1)), ei, true, oa, ra);
+  if (!kTwoPre) prefetch_own(oa, ei + dE, 2 <= n);
   __syncthreads();
 #ifdef MQ_TRACE_MARCH
-  if (mc.tr) mc.tr[130] = globaltimer_ns();  // plane i0 converted (prologue done)
+  if (mc.tr) mc.tr[130] = globaltimer_ns();  // plane 1 converted (prologue done)
 #endif
-  if (i0 + NAT <= last) issue(i0 + NAT);
-  // one plane step: own = the staged own values of plane i (from the previous
-  // step), nxt receives those of plane i+1; ocur holds the prefetched own
-  // words of plane i+1, onxt receives those of plane i+2 (the same set when
+  if (NAT + 1 <= n + 1) issue(qa(NAT + 1));
+  // one plane step: own = the staged own values of plane t (from the previous
+  // step), nxt receives those of plane t+1; ocur holds the prefetched own
+  // words of plane t+1, onxt receives those of plane t+2 (the same set when
   // there is one).  The march calls it with the register sets swapped every
   // plane (no rotation copies).
-  auto step = [&](int i, double (&own)[9], double (&nxt)[9], OwnPre &ocur, OwnPre &onxt) {
-    if (kTwoPre) prefetch_own(onxt, ei + 2 * LSi, i + 2 < i1);
-    const uint32_t act_next = convert(i + 1, sp1, pp1, ei + LSi, i + 1 < i1, ocur, nxt);
-    if (!kTwoPre) prefetch_own(onxt, ei + 2 * LSi, i + 2 < i1);
+  auto step = [&](int t, double (&own)[9], double (&nxt)[9], OwnPre &ocur, OwnPre &onxt) {
+    if (kTwoPre) prefetch_own(onxt, ei + 2 * dE, t + 2 <= n);
+    const uint32_t act_next = convert(qa(t + 1), sl_p, pp1, ei + dE, t + 1 <= n, ocur, nxt);
+    if (!kTwoPre) prefetch_own(onxt, ei + 2 * dE, t + 2 <= n);
 #ifdef MQ_TRACE_MARCH
-    if (mc.tr) mc.tr[4 * (i - i0) + 2] = globaltimer_ns();
+    if (mc.tr) mc.tr[4 * (t - 1) + 2] = globaltimer_ns();
 #endif
     __syncthreads();
 #ifdef MQ_TRACE_MARCH
-    if (mc.tr) mc.tr[4 * (i - i0) + 3] = globaltimer_ns();
+    if (mc.tr) mc.tr[4 * (t - 1) + 3] = globaltimer_ns();
 #endif
-    // r slot of plane i-2 (its last stencil was before this barrier), p slot
-    // of plane i+1 (converted before this barrier)
-    if (i + NAT + 1 <= last) issue(i + NAT + 1);
-    stencil_plane(i, sm1, s0, sp1, ei, act, pm, own, nxt);
+    // r slot of plane t-2 (its last stencil was before this barrier), p slot
+    // of plane t+1 (converted before this barrier)
+    if (t + NAT + 1 <= n + 1) issue(qa(t + NAT + 1));
+    // slots of the actual planes i-1, i, i+1
+    stencil_plane(qa(t), DIR > 0 ? sl_m : sl_p, sl_0, DIR > 0 ? sl_p : sl_m, ei, act, pm, own, nxt);
     act = act_next;
 #pragma unroll
     for (int c = 0; c < 3; ++c) pm[c] = (K1M && MQ_PRESCALE) ? mul(a.of, own[c]) : own[3 + c];
-    sm1 = s0;
-    s0 = sp1;
-    sp1 = winc(sp1, NRT);
+    sl_m = sl_0;
+    sl_0 = sl_p;
+    sl_p = winc(sl_p, NRT);
     pp1 = winc(pp1, NPT);
-    ei += LSi;
+    ei += dE;
   };
   {
-    int i = i0;
+    int t = 1;
     if (kTwoPre) {
-      for (; i + 1 < i1; i += 2) {
-        step(i, ra, rb, ob, oa);
-        step(i + 1, rb, ra, oa, ob);
+      for (; t + 1 <= n; t += 2) {
+        step(t, ra, rb, ob, oa);
+        step(t + 1, rb, ra, oa, ob);
       }
-      if (i < i1) step(i, ra, rb, ob, oa);
+      if (t <= n) step(t, ra, rb, ob, oa);
     } else {
-      for (; i + 1 < i1; i += 2) {
-        step(i, ra, rb, oa, oa);
-        step(i + 1, rb, ra, oa, oa);
+      for (; t + 1 <= n; t += 2) {
+        step(t, ra, rb, oa, oa);
+        step(t + 1, rb, ra, oa, oa);
       }
-      if (i < i1) step(i, ra, rb, oa, oa);
+      if (t <= n) step(t, ra, rb, oa, oa);
     }
   }
   __syncthreads();
@@ -1052,6 +1069,15 @@ constexpr int NA1 = MQ_NAHEAD1, NR1 = NA1 + 3, NP1 = NA1;
 #ifndef MQ_SLAB_XDEFER
 #define MQ_SLAB_XDEFER 1
 #endif
+// Alternating march direction (odd passes from the top plane of every brick
+// down): opt-in.  Measured at 128^3: the L2 reuse is real (DRAM reads 13.22 ->
+// 11.12 GB per 60 iterations, 398 -> 364 MB per iteration, L2 hit rate 35.8 ->
+// 42.2 %) but an iteration takes 78.4 instead of 76.3 us -- the pass is bound
+// by the latency of its staged planes (two in flight per CTA), not by DRAM
+// bytes.
+#ifndef MQ_TMA_ALTDIR
+#define MQ_TMA_ALTDIR 0
+#endif
 constexpr size_t kTmaSmem1 = sizeof(Box3) * (NR1 + 2 * NP1) + 128;
 
 struct TmaPcg1Args {
@@ -1164,7 +1190,12 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
     bool pend = false;  // deferred x update, as in pcg_tma_kernel
     int xmode = 0;
     const int tid = threadIdx.x, ty = tid >> 5, tx = tid & 31;
-    int pre_i0 = 0;  // first plane of the brick whose prologue is pre-issued
+    int pre_i0 = 0, pre_i1 = 0;  // brick whose prologue is pre-issued
+    bool pre_back = false;
+    // alternate march direction (odd passes backwards: pass 1 starts where
+    // the initial-residual march ended) when every brick is short; long
+    // bricks (256^3: vectors far larger than L2) march forwards
+    const bool alt = MQ_TMA_ALTDIR && (g.nx + g.chunks - 1) / g.chunks <= kMaskPlanes;
     for (int it = 1;; ++it) {
       const bool first = it == 1;
       double *pnew = pold_is_a ? a.pb : a.pa;
@@ -1197,7 +1228,10 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
         };
         // bricks of <= kMaskPlanes planes (the default geometry of this kernel):
         // own-position mask bits from shared memory
-        if (i1 - i0 <= kMaskPlanes)
+        if (alt && (it & 1))
+          march_tma<kK1R, NA1, 1, 1, -1>(mc, A, mr, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0,
+                                         rowf);
+        else if (i1 - i0 <= kMaskPlanes)
           march_tma<kK1R, NA1, 1>(mc, A, mr, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0, rowf);
         else
           march_tma<kK1R, NA1, 0>(mc, A, mr, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0, rowf);
@@ -1230,9 +1264,15 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
         int i0, i1, j0, k0;
         brick_of(g, blockIdx.x, i0, i1, j0, k0);
         mc.ma = (it & 1) ? &A1.tm_a2 : &A1.tm_a;
-        tma_preissue<kK1R, NA1>(mc, ((it + 1) & 1) ? &A1.tm_r2 : &A.tm_r, pold_is_a ? &A.tm_pb : &A.tm_pa, true,
-                                i0, i1, j0, k0, 5 * 32);
+        pre_back = alt && ((it + 1) & 1);
+        if (pre_back)
+          tma_preissue<kK1R, NA1, -1>(mc, ((it + 1) & 1) ? &A1.tm_r2 : &A.tm_r, pold_is_a ? &A.tm_pb : &A.tm_pa, true,
+                                      i0, i1, j0, k0, 5 * 32);
+        else
+          tma_preissue<kK1R, NA1, 1>(mc, ((it + 1) & 1) ? &A1.tm_r2 : &A.tm_r, pold_is_a ? &A.tm_pb : &A.tm_pa, true,
+                                     i0, i1, j0, k0, 5 * 32);
         pre_i0 = i0;
+        pre_i1 = i1;
       }
 #endif
       double s5[5];
@@ -1285,7 +1325,10 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_kernel(const __g
       alpha_prev = alpha;
       pold_is_a = !pold_is_a;
     }
-    if (mc.pre) tma_drain<NA1>(mc, pre_i0);
+    if (mc.pre) {
+      if (pre_back) tma_drain<NA1, -1>(mc, pre_i0, pre_i1);
+      else tma_drain<NA1, 1>(mc, pre_i0, pre_i1);
+    }
     if (status == MQ_OK) {
       // the pass that read the final test ran with xmode 2 (x complete) or 0:
       // x += alpha_K p_K pending, p_K = that pass's p_old
