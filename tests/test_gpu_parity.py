@@ -931,6 +931,47 @@ def test_resident_pcg_other_brick_depths(gpu_ok, shape, li, sync, monkeypatch):
             assert rel(x, ref.x) <= 1e-8
 
 
+@pytest.mark.parametrize("sync", ["1", "2"])
+@pytest.mark.parametrize("shape", [(150, 40, 40), (97, 24, 70)])
+def test_tma_pcg_long_bricks(gpu_ok, shape, sync, monkeypatch):
+    """TMA brick kernels on bricks longer than the shared-memory mask cache
+    (MQ_BRICK_CHUNKS=1: one brick per tile column, 150 / 97 planes; the
+    configs[4] case): the one-barrier kernel -- the default at every brick
+    length -- takes the mask words from global memory there, odd plane counts
+    end the two-plane unrolled march on a single step.  PCG against the oracle,
+    cold and warm start, budget exhaustion."""
+    from paper_1611_06721_b200 import PcgConfig, Preconditioner, pcg_solve
+    from paper_1611_06721_b200.device import DeviceGrid, Problem
+    monkeypatch.setenv("MQ_PCG_KERNEL", "brick")
+    monkeypatch.setenv("MQ_PCG_SYNC", sync)
+    monkeypatch.setenv("MQ_BRICK_CHUNKS", "1")
+    mat = np.zeros(shape, np.int8)
+    nx, ny, nz = shape
+    mat[nx // 3:nx // 3 + 11, ny // 3:ny // 3 + 9, nz // 4:nz // 4 + 7] = 1
+    h = 1.0 / max(shape)
+    m = O.assemble(mat, h, O.Conductor(5e6, 3.8, 2.17, 396.2), [])
+    inv = O.jacobi_inverse(m.kn.diagonal())
+    rng = np.random.default_rng(sum(shape))
+    b = m.kn @ rng.standard_normal(m.n_n)
+    x0 = rng.standard_normal(m.n_n) * 1e-3
+    jac = Preconditioner.JACOBI
+    with DeviceGrid(Problem(material=mat, h=h, kappa=5e6, brauer=(3.8, 2.17, 396.2),
+                            pattern=np.zeros(m.n_n))) as g:
+        name, _ = g.pcg_kernel()
+        assert name == ("pcg_tma1_kernel" if sync == "1" else "pcg_tma_kernel"), name
+        for start in (None, x0):
+            x, rep = pcg_solve(g.kn_operator(), b, x0=start, config=PcgConfig(rel_tol=1e-8, preconditioner=jac))
+            ref = O.pcg(m.kn_apply, b, x0=start, rel_tol=1e-8, inv_diag=inv)
+            assert rep.converged and abs(rep.iterations - ref.iterations) <= 1
+            assert rep.applications == ref.applies + (rep.iterations - ref.iterations)
+            assert rel(x, ref.x) <= 1e-8
+        for budget in (1, 2, 3, 4):
+            x, rep = pcg_solve(g.kn_operator(), b, config=PcgConfig(rel_tol=1e-14, max_iter=budget, preconditioner=jac))
+            ref = O.pcg(m.kn_apply, b, rel_tol=1e-14, max_iter=budget, inv_diag=inv)
+            assert not rep.converged and rep.iterations == budget and rep.applications == ref.applies
+            assert rel(x, ref.x) <= 1e-12
+
+
 @pytest.mark.parametrize("world", [1, 2, 3])
 @pytest.mark.parametrize("x0_given", [False, True])
 def test_slab_pcg_loopback_on_one_gpu(gpu_ok, world, x0_given):
