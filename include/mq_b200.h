@@ -114,6 +114,9 @@ int mq_device_sm_count(int32_t device, int32_t *sms);
 /* page-locked host memory (result arrays of the Python mirror) */
 int mq_host_alloc(int64_t bytes, void **out);
 int mq_host_free(void *p);
+/* MQ_INVALID when a padded device vector would hold 2^31 entries or more
+ * (about 890^3 cells: 16 GB per vector; the fused PCG kernels index entries
+ * with 32-bit integers) */
 int mq_ctx_create(const mq_grid_desc *desc, int32_t device, mq_ctx **out);
 void mq_ctx_destroy(mq_ctx *ctx);
 int64_t mq_n_n(const mq_ctx *ctx);     /* nonconducting interior dofs */
