@@ -1075,6 +1075,9 @@ constexpr int NA1 = MQ_NAHEAD1, NR1 = NA1 + 3, NP1 = NA1;
 // 42.2 %) but an iteration takes 78.4 instead of 76.3 us -- the pass is bound
 // by the latency of its staged planes (two in flight per CTA), not by DRAM
 // bytes.
+#ifndef MQ_SLAB_DEFER_SHORT
+#define MQ_SLAB_DEFER_SHORT 0
+#endif
 #ifndef MQ_TMA_ALTDIR
 #define MQ_TMA_ALTDIR 0
 #endif
@@ -1754,7 +1757,7 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_slab_kernel(cons
     // per iteration at one rank); short bricks (slabs of <= 64 planes) update
     // x every pass: the two-term update's extra registers spill in this
     // kernel (32-plane slab 89.8 -> 91.4 us).  Uniform per launch.
-    const bool defer = MQ_SLAB_XDEFER && (g.nx + g.chunks - 1) / g.chunks > kMaskPlanes;
+    const bool defer = MQ_SLAB_XDEFER && (MQ_SLAB_DEFER_SHORT || (g.nx + g.chunks - 1) / g.chunks > kMaskPlanes);
     bool pend = false;
     int xmode = 0;
     for (int it = 1;; ++it) {
@@ -1778,43 +1781,59 @@ __global__ void __launch_bounds__(kBlock, MQ_TMA_MINB) pcg_tma1_slab_kernel(cons
       double *apw = odd_a ? a.ap2 : a.ap;
       mc.crr = 0.0;
       mc.crz = 0.0;
-      // neighbour pointers are read from the kernel parameters where they are
-      // used (no registers held across the march)
-      auto push = [&](int q, int c, int64_t jk, double v, double rv) {
-        if (q == 0 && me.lo_pa) {
-          const int64_t d = c * me.lo_C + me.lo_top + jk;
-          (pold_is_a ? me.lo_pb : me.lo_pa)[d] = v;
-          if (!first) (odd_r ? me.lo_r2 : me.lo_r)[d] = rv;
-        }
-        if (q == nmax && me.hi_pa) {
-          const int64_t d = c * me.hi_C + jk;
-          (pold_is_a ? me.hi_pb : me.hi_pa)[d] = v;
-          if (!first) (odd_r ? me.hi_r2 : me.hi_r)[d] = rv;
+      // Ghost stores: after the march of a brick that holds the slab's first
+      // or last plane, every thread re-reads the p_new, r_{k-1} and Ap_k it
+      // stored itself at its own position of that plane (L1/L2 hits) and
+      // stores them into the neighbour ranks' ghost planes -- the plane loop
+      // itself carries no ghost logic (it is the march of pcg_tma1_kernel: 395
+      // instead of ~ 880 instructions per plane step).  Neighbour pointers are
+      // read from the kernel parameters where they are used.
+      auto push_edges = [&](int i0, int i1, int j0, int k0) {
+        const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
+        const int j = j0 + ty, kk = k0 + tx;
+        if (j >= g.ny || kk >= g.nz) return;
+        const int64_t pos = L.off + (int64_t)j * L.Sj + kk, jk = pos - L.Si;
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+          const int q = side == 0 ? 0 : nmax;
+          if (q < i0 || q >= i1) continue;
+          double *dp = side == 0 ? (pold_is_a ? me.lo_pb : me.lo_pa) : (pold_is_a ? me.hi_pb : me.hi_pa);
+          if (!dp) continue;
+          double *dr = side == 0 ? (odd_r ? me.lo_r2 : me.lo_r) : (odd_r ? me.hi_r2 : me.hi_r);
+          double *da = side == 0 ? (odd_a ? me.lo_a2 : me.lo_a) : (odd_a ? me.hi_a2 : me.hi_a);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const int64_t e = c * L.C + (int64_t)q * L.Si + pos;
+            if (!((__ldg(a.mask + (e >> 5)) >> (e & 31)) & 1u)) continue;
+            const int64_t d = side == 0 ? c * me.lo_C + me.lo_top + jk : c * me.hi_C + jk;
+            dp[d] = pnew[e];
+            if (!first) dr[d] = mc.rout[e];
+            da[d] = apw[e];
+          }
         }
       };
       double v[3] = {0.0, 0.0, 0.0};
       for (int bi = lb; bi < g.nbricks; bi += Gr) {
         int i0, i1, j0, k0;
         brick_of(g, bi, i0, i1, j0, k0);
-        auto rowf = [&](int c, int e, double av, double own, double rown, int i) {
+        auto rowf = [&](int, int e, double av, double own, double rown, int) {
           apw[e] = av;
           v[0] = add(v[0], mul(own, av));
           v[1] = add(v[1], mul(rown, av));
           v[2] = add(v[2], mul(av, av));
-          if (i == 0 && me.lo_a) {
-            const int64_t jk = e - c * L.C - L.Si;
-            (odd_a ? me.lo_a2 : me.lo_a)[c * me.lo_C + me.lo_top + jk] = av;
-          }
-          if (i == nmax && me.hi_a) {
-            const int64_t jk = e - c * L.C - (int64_t)me.n * L.Si;
-            (odd_a ? me.hi_a2 : me.hi_a)[c * me.hi_C + jk] = av;
-          }
         };
+#if MQ_SLAB_DEFER_SHORT
+        if (i1 - i0 <= kMaskPlanes)
+          march_tma<kK1R, NA1, 1, 1>(mc, A, mr, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0,
+                                     rowf);
+#else
         if (!defer && i1 - i0 <= kMaskPlanes)
-          march_tma<kK1R, NA1, 1, 0>(mc, A, mr, mp, first, beta, alpha_prev, xmode, 0.0, pnew, i0, i1, j0, k0, rowf, push);
+          march_tma<kK1R, NA1, 1, 0>(mc, A, mr, mp, first, beta, alpha_prev, xmode, 0.0, pnew, i0, i1, j0, k0, rowf);
+#endif
         else
           march_tma<kK1R, NA1, 0, 1>(mc, A, mr, mp, first, beta, alpha_prev, xmode, alpha_prev2, pnew, i0, i1, j0, k0,
-                                     rowf, push);
+                                     rowf);
+        push_edges(i0, i1, j0, k0);
       }
       ++applies;
       double v5[5] = {v[0], v[1], v[2], mc.crr, mc.crz};
